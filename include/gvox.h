@@ -1,0 +1,238 @@
+/*
+ * gvox.h -- C ABI of the B200-native batched VGICP linearization library
+ * (libgvox.so), the data-parallel hot path of GLIM (arXiv 2407.10344).
+ *
+ * Citations: "P:n" = PAPER.md line n of the paper's source (Sec. III-C
+ * "Matching Cost Factor": Preprocessing P:186, Correspondence search P:197,
+ * Linearization P:199-218 = Eqs. 2-8, Implementation P:221-224 / Fig. 4
+ * P:190-195; overlap rate P:280; global factor selection P:391).  Readings of
+ * ambiguous passages (Q1..Q19) are listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Poses are fp64, row-major 3x4 [R | t], world <- sensor.  The relative
+ *    pose of a factor is T_ij = T_j^-1 T_i (source cloud i, target map j;
+ *    reading Q1).  Tangent vectors are rotation-first [w; rho]; perturbations
+ *    are right-multiplied, T <- T Exp(xi).
+ *  - Covariances are 6 floats per point: xx, xy, xz, yy, yz, zz.
+ *  - Voxel level l (0-based) has resolution r_l = r0 * 2^l (P:186, 1-based
+ *    there).  A voxel key is floor(p / r_l) per axis, evaluated in fp64 from
+ *    the fp32 input promoted exactly (reading Q10); it is identified by the
+ *    packed key ((kx+2^20)<<42) | ((ky+2^20)<<21) | (kz+2^20), valid for
+ *    -2^20 <= k < 2^20 (reading Q11).
+ *  - Every call enqueues its work on the context's CUDA stream.  Calls whose
+ *    outputs are host memory (mem == GVOX_HOST) synchronize that stream before
+ *    returning; calls with device outputs do not.
+ *  - Status codes only; no exception crosses the ABI.  On failure
+ *    gvox_last_error() returns a thread-local message naming the offending
+ *    argument (for factors: the factor index).
+ *  - Not thread-safe per context: one host thread drives one gvox_ctx.
+ */
+#ifndef GVOX_H_
+#define GVOX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GVOX_VERSION_MAJOR 0
+#define GVOX_VERSION_MINOR 1
+#define GVOX_MAX_LEVELS 8
+
+typedef enum gvox_status {
+  GVOX_OK = 0,
+  GVOX_ERR_INVALID = 1, /* null pointer, bad size, r0 <= 0 or non-finite, levels
+                           outside [1, 8], index out of range, non-finite input */
+  GVOX_ERR_RANGE = 2,   /* a voxel key outside [-2^20, 2^20) during a map build */
+  GVOX_ERR_CUDA = 3,    /* CUDA runtime error (message has cudaGetErrorString) */
+  GVOX_ERR_NOMEM = 4    /* device or pinned host allocation failed */
+} gvox_status;
+
+/* Where a caller-provided buffer lives. */
+enum { GVOX_HOST = 0, GVOX_DEVICE = 1 };
+
+/* Per-factor flags. */
+enum {
+  /* P:197 surface-orientation validation: discard point k at every level when
+     (mu_k - T_i^-1 t_j) . n_k > 0 (strict; a zero normal disables it, Q7).
+     Needs normals oriented toward the source sensor origin. */
+  GVOX_F_VALIDATE_SURFACE = 1u,
+  /* Error and counts only; H and b are left zero (LM trial steps). */
+  GVOX_F_ERROR_ONLY = 2u
+};
+
+typedef struct gvox_ctx gvox_ctx;
+typedef struct gvox_cloud gvox_cloud;
+typedef struct gvox_map gvox_map;
+
+/* One matching cost factor: indices into the clouds[], maps[] and poses[]
+   arrays of the call. */
+typedef struct gvox_factor {
+  int32_t source_cloud; /* P_i, points in frame i */
+  int32_t target_map;   /* voxelmap of P_j, in frame j */
+  int32_t pose_i;       /* linearization point T_i */
+  int32_t pose_j;       /* linearization point T_j */
+  uint32_t flags;       /* GVOX_F_* */
+} gvox_factor;
+
+/* One overlap query: source cloud P_i against the voxels of P_j. */
+typedef struct gvox_pair {
+  int32_t source_cloud;
+  int32_t target_map;
+  int32_t pose_i;
+  int32_t pose_j;
+} gvox_pair;
+
+/* Linearized factor (Eqs. 4-8), blocks over (x_i, x_j):
+     H_ii = sum A^T Omega A, H_ij = sum A^T Omega B, H_jj = sum B^T Omega B,
+     b_i  = sum A^T Omega d,  b_j  = sum B^T Omega d,  error = sum d^T Omega d
+   with d = mu~ - T_ij mu, A = [R_ij (mu)x, -R_ij], B = [-(T_ij mu)x, I]
+   (readings Q2-Q5: sums over points and levels, no 1/2, b as printed).
+   Matrices are row-major 6x6.  e(delta) ~ error + 2 b^T delta + delta^T H delta;
+   the Gauss-Newton step is -H^-1 b. */
+typedef struct gvox_linear_factor {
+  double H_ii[36];
+  double H_ij[36];
+  double H_jj[36];
+  double b_i[6];
+  double b_j[6];
+  double error;
+  int32_t inliers[GVOX_MAX_LEVELS]; /* correspondences found per level */
+  int32_t num_invisible;            /* points discarded by validation */
+  int32_t num_degenerate;           /* terms skipped: fused covariance not PD (Q16) */
+} gvox_linear_factor;
+
+/* Compact per-factor result in target-block form, 288 bytes: what one rank
+   contributes to the multi-GPU gather.  terms[0..20] = upper triangle of H_jj
+   (row-major), terms[21..26] = b_j, terms[27] = error.  gvox_expand() turns it
+   into a gvox_linear_factor via H_ii = Ad^T H_jj Ad, H_ij = -Ad^T H_jj,
+   b_i = -Ad^T b_j with Ad = Ad(T_ij) (exact: A = -B Ad(T_ij)). */
+typedef struct gvox_factor_accum {
+  double terms[28];
+  int32_t inliers[GVOX_MAX_LEVELS];
+  int32_t num_invisible;
+  int32_t num_degenerate;
+  int32_t reserved[6];
+} gvox_factor_accum;
+
+/* ---------------------------------------------------------------- context */
+
+/* Create a context on CUDA device `device`, enqueuing on `cuda_stream`
+   (a cudaStream_t; NULL = the legacy default stream).  The stream is not owned. */
+gvox_status gvox_ctx_create(int device, void* cuda_stream, gvox_ctx** out);
+gvox_status gvox_ctx_set_stream(gvox_ctx* ctx, void* cuda_stream);
+void gvox_ctx_destroy(gvox_ctx* ctx);
+
+/* ----------------------------------------------------------------- clouds */
+
+/* Gaussian point cloud (p_k = (mu_k, C_k)), optionally with normals for
+   the P:197 validation.  mu: n x 3 floats, cov: n x 6 floats, normals: n x 3
+   floats or NULL.  mem selects where the three arrays live (all the same).
+   The data are copied into a device-resident, library-owned handle (planar
+   float4 layout), so the caller may free its arrays after return.
+   Errors: GVOX_ERR_INVALID for null pointers (with n > 0), n < 0, or a
+   non-finite coordinate / covariance / normal (this call synchronizes). */
+gvox_status gvox_cloud_create(gvox_ctx* ctx, const float* mu, const float* cov,
+                              const float* normals, int64_t n, int mem, gvox_cloud** out);
+int64_t gvox_cloud_size(const gvox_cloud* cloud);
+void gvox_cloud_destroy(gvox_cloud* cloud);
+
+/* -------------------------------------------------------------- voxelmaps */
+
+/* Multi-resolution Gaussian voxelmap of a cloud: for each level
+   l < levels, voxels keyed by floor(mu / r_l); each voxel holds the mean of
+   its points' means, the mean of their covariances and the point count
+   (reading Q9).  Built on the device by spatial hashing.
+   Errors: GVOX_ERR_INVALID (r0 <= 0 or non-finite, levels outside [1, 8]),
+   GVOX_ERR_RANGE (some key outside [-2^20, 2^20) at some level).
+   Synchronizes once (to size the voxel arrays). */
+gvox_status gvox_create_voxelmap(gvox_ctx* ctx, const gvox_cloud* cloud, double r0, int levels,
+                                 gvox_map** out);
+
+/* Batched build of `count` maps with one launch sequence (same r0, levels).
+   maps_out[k] receives the map of clouds[k].  All-or-nothing on error. */
+gvox_status gvox_create_voxelmaps(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t count,
+                                  double r0, int levels, gvox_map** maps_out);
+
+gvox_status gvox_voxelmap_info(const gvox_map* map, int level, int64_t* num_voxels,
+                               double* resolution);
+int gvox_voxelmap_levels(const gvox_map* map);
+
+/* Canonical export of one level to HOST arrays, voxels in ascending packed-key
+   order: keys [V], means [V x 3] (fp64 = centre + stored fp32 offset),
+   covs [V x 6], counts [V].  Any output pointer may be NULL.  Synchronizes. */
+gvox_status gvox_voxelmap_export(gvox_ctx* ctx, const gvox_map* map, int level, int64_t* keys,
+                                 double* means, double* covs, int32_t* counts);
+
+/* Lookup: for n query points q (fp64, n x 3, in the map frame),
+   the packed key of the containing voxel at `level`, or -1 if that voxel is
+   empty or out of key range (no neighbour search, reading Q8).
+   q and keys_out live in `mem`. */
+gvox_status gvox_voxelmap_lookup(gvox_ctx* ctx, const gvox_map* map, int level, const double* q,
+                                 int64_t n, int64_t* keys_out, int mem);
+
+void gvox_map_destroy(gvox_map* map);
+
+/* ---------------------------------------------------------------- overlap */
+
+/* Overlap counts ("the fraction of points in P_i that fall within a
+   voxel of P_j"): counts[p] = number of points of clouds[pairs[p].source_cloud]
+   whose key under T_ij = T_j^-1 T_i (fp64, pinned fma order) is occupied at
+   `level` of maps[pairs[p].target_map].  No validation (reading Q15).  The
+   rate is counts[p] / n (0 for an empty source); the global-mapping factor
+   test "exceeds 5 %" is 20 * count > n.
+   pairs, poses: host arrays.  counts: int32 [num_pairs] in `mem`.
+   Exactly one H2D (pairs + poses) per call; one D2H when mem == GVOX_HOST. */
+gvox_status gvox_overlap(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t num_clouds,
+                         const gvox_map* const* maps, int64_t num_maps, const gvox_pair* pairs,
+                         int64_t num_pairs, const double* poses, int64_t num_poses, int level,
+                         int32_t* counts, int mem);
+
+/* ------------------------------------------------------------- linearize */
+
+/* Batched linearization of matching cost factors (Eqs. 2-8; Fig. 4 / P:224:
+   inputs serialized into one block, one H2D, all factors processed in one
+   fused launch, results serialized, one D2H).  Stateless: correspondences and
+   Omega are recomputed at the given linearization points every call (P:208,
+   P:313).
+   factors, poses: host arrays (poses: num_poses x 12).  out: num_factors
+   records in `mem`.  corr_dump (optional, DEVICE, int64 [sum_f N_f][L_f] packed
+   per factor in factor order, L_f = levels of the factor's map): the packed key
+   of each correspondence, -1 none, -2 discarded by validation.
+   Errors: GVOX_ERR_INVALID with the factor index for an out-of-range cloud /
+   map / pose index; non-finite poses. */
+gvox_status gvox_linearize_batch(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                 int64_t num_clouds, const gvox_map* const* maps, int64_t num_maps,
+                                 const gvox_factor* factors, int64_t num_factors,
+                                 const double* poses, int64_t num_poses, gvox_linear_factor* out,
+                                 int mem, int64_t* corr_dump);
+
+/* Same, compact target-block records (for sharded runs and the NCCL gather). */
+gvox_status gvox_linearize_batch_accum(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                       int64_t num_clouds, const gvox_map* const* maps,
+                                       int64_t num_maps, const gvox_factor* factors,
+                                       int64_t num_factors, const double* poses, int64_t num_poses,
+                                       gvox_factor_accum* out, int mem);
+
+/* Expand compact records (DEVICE, e.g. after an all-gather) into full records:
+   accum[k] belongs to factors[k]; poses as in gvox_linearize_batch (host).
+   out in `mem`. */
+gvox_status gvox_expand(gvox_ctx* ctx, const gvox_factor* factors, int64_t num_factors,
+                        const double* poses, int64_t num_poses, const gvox_factor_accum* accum,
+                        gvox_linear_factor* out, int mem);
+
+/* ------------------------------------------------------------- utilities */
+
+const char* gvox_status_string(gvox_status s);
+const char* gvox_last_error(void);
+/* Kernel launches issued by this thread since the last reset (evidence for
+   bench.py's gpu_launches). */
+int64_t gvox_launch_count(int reset);
+const char* gvox_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GVOX_H_ */

@@ -1,0 +1,24 @@
+"""paper_2407_10344_b200 -- B200-native batched VGICP linearization (GLIM,
+arXiv 2407.10344): libgvox.so (hand-written sm_100a CUDA behind the C ABI of
+include/gvox.h) and its thin Python binding.
+
+Importing this package loads libgvox.so and raises if it is missing; there is
+no CPU fallback.
+"""
+from ._lib import (FACTOR_ACCUM_DTYPE, FACTOR_DTYPE, F_ERROR_ONLY, F_VALIDATE_SURFACE,
+                   GVOX_DEVICE, GVOX_HOST, LINEAR_FACTOR_DTYPE, MAX_LEVELS, PAIR_DTYPE, GvoxError,
+                   launch_count, lib, version)
+from .api import (Cloud, Context, HandleArray, VoxelMap, as_factors, as_pairs, as_poses,
+                  corr_dump_size, create_voxelmap, create_voxelmaps, device_records, expand,
+                  full_blocks, linearize_batch, linearize_batch_accum, overlap, records_to_numpy)
+
+lib()  # fail loudly at import if the CUDA library is absent
+
+__all__ = [
+    "Cloud", "Context", "VoxelMap", "HandleArray", "create_voxelmap", "create_voxelmaps",
+    "overlap", "linearize_batch", "linearize_batch_accum", "expand", "device_records",
+    "records_to_numpy", "full_blocks", "corr_dump_size", "as_factors", "as_pairs", "as_poses",
+    "FACTOR_DTYPE", "PAIR_DTYPE", "LINEAR_FACTOR_DTYPE", "FACTOR_ACCUM_DTYPE", "MAX_LEVELS",
+    "F_VALIDATE_SURFACE", "F_ERROR_ONLY", "GVOX_HOST", "GVOX_DEVICE", "GvoxError",
+    "launch_count", "version", "lib",
+]

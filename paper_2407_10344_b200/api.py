@@ -1,0 +1,303 @@
+"""Thin Python front end of libgvox (include/gvox.h).
+
+Argument marshalling only: numpy arrays are host buffers, torch CUDA tensors are
+device buffers (torch provides device memory and the CUDA stream), and every
+computation runs in the library's sm_100a kernels.  Names follow the C ABI
+(gvox_create_voxelmap -> create_voxelmap, gvox_overlap -> overlap,
+gvox_linearize_batch -> linearize_batch, ...).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import numpy as np
+
+from ._lib import (FACTOR_ACCUM_DTYPE, FACTOR_DTYPE, GVOX_DEVICE, GVOX_HOST, LINEAR_FACTOR_DTYPE,
+                   PAIR_DTYPE, check, lib)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _is_cuda_tensor(x) -> bool:
+    try:
+        torch = _torch()
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _ptr(x):
+    """(pointer, mem) of a numpy array or torch CUDA tensor (contiguous)."""
+    if x is None:
+        return None, None
+    if _is_cuda_tensor(x):
+        assert x.is_contiguous(), "device tensors must be contiguous"
+        return ctypes.c_void_p(x.data_ptr()), GVOX_DEVICE
+    assert isinstance(x, np.ndarray) and x.flags["C_CONTIGUOUS"], type(x)
+    return ctypes.c_void_p(x.ctypes.data), GVOX_HOST
+
+
+class Context:
+    """gvox_ctx on one CUDA device, enqueuing on a torch stream (default: the
+    device's current stream)."""
+
+    def __init__(self, device: int = 0, stream=None):
+        torch = _torch()
+        self.device_index = int(device)
+        self.device = torch.device("cuda", self.device_index)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        h = ctypes.c_void_p()
+        check(lib().gvox_ctx_create(self.device_index, ctypes.c_void_p(stream.cuda_stream),
+                                    ctypes.byref(h)))
+        self.handle = h
+
+    def set_stream(self, stream):
+        self.stream = stream
+        check(lib().gvox_ctx_set_stream(self.handle, ctypes.c_void_p(stream.cuda_stream)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().gvox_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover
+            pass
+
+
+class Cloud:
+    """gvox_cloud: Gaussian points copied into device-resident planar float4
+    arrays.  mu [n,3], cov [n,6] (xx xy xz yy yz zz), normals [n,3] or None;
+    numpy (host) or torch CUDA tensors (device), float32."""
+
+    def __init__(self, ctx: Context, mu, cov, normals=None):
+        if not _is_cuda_tensor(mu):
+            mu = np.ascontiguousarray(np.asarray(mu, np.float32).reshape(-1, 3))
+            cov = np.ascontiguousarray(np.asarray(cov, np.float32).reshape(-1, 6))
+            if normals is not None:
+                normals = np.ascontiguousarray(np.asarray(normals, np.float32).reshape(-1, 3))
+        n = int(mu.shape[0])
+        pm, mem = _ptr(mu)
+        pc, _ = _ptr(cov)
+        pn, _ = _ptr(normals)
+        h = ctypes.c_void_p()
+        check(lib().gvox_cloud_create(ctx.handle, pm, pc, pn, n, mem, ctypes.byref(h)))
+        self.handle = h
+        self.n = n
+
+    def __len__(self):
+        return self.n
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().gvox_cloud_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover
+            pass
+
+
+class VoxelMap:
+    """gvox_map: multi-resolution Gaussian voxelmap."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self.handle = handle
+        self.levels = int(lib().gvox_voxelmap_levels(handle))
+
+    def info(self, level: int):
+        n = ctypes.c_int64()
+        r = ctypes.c_double()
+        check(lib().gvox_voxelmap_info(self.handle, level, ctypes.byref(n), ctypes.byref(r)))
+        return int(n.value), float(r.value)
+
+    def num_voxels(self, level: int) -> int:
+        return self.info(level)[0]
+
+    def export(self, ctx: Context, level: int):
+        """(keys int64 [V], means f64 [V,3], covs f64 [V,6], counts int32 [V]) in
+        ascending packed-key order."""
+        V = self.num_voxels(level)
+        keys = np.empty(V, np.int64)
+        means = np.empty((V, 3), np.float64)
+        covs = np.empty((V, 6), np.float64)
+        counts = np.empty(V, np.int32)
+        check(lib().gvox_voxelmap_export(ctx.handle, self.handle, level, _ptr(keys)[0],
+                                         _ptr(means)[0], _ptr(covs)[0], _ptr(counts)[0]))
+        return keys, means, covs, counts
+
+    def lookup(self, ctx: Context, level: int, q):
+        """Packed key of the voxel containing each q (fp64 [n,3]) or -1."""
+        if _is_cuda_tensor(q):
+            torch = _torch()
+            out = torch.empty(q.shape[0], dtype=torch.int64, device=q.device)
+        else:
+            q = np.ascontiguousarray(np.asarray(q, np.float64).reshape(-1, 3))
+            out = np.empty(q.shape[0], np.int64)
+        pq, mem = _ptr(q)
+        check(lib().gvox_voxelmap_lookup(ctx.handle, self.handle, level, pq, int(q.shape[0]),
+                                         _ptr(out)[0], mem))
+        return out
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().gvox_map_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover
+            pass
+
+
+def create_voxelmap(ctx: Context, cloud: Cloud, r0: float, levels: int) -> VoxelMap:
+    h = ctypes.c_void_p()
+    check(lib().gvox_create_voxelmap(ctx.handle, cloud.handle, float(r0), int(levels),
+                                     ctypes.byref(h)))
+    return VoxelMap(h)
+
+
+def create_voxelmaps(ctx: Context, clouds: Sequence[Cloud], r0: float, levels: int):
+    n = len(clouds)
+    arr = (ctypes.c_void_p * max(n, 1))(*[c.handle.value for c in clouds])
+    out = (ctypes.c_void_p * max(n, 1))()
+    check(lib().gvox_create_voxelmaps(ctx.handle, arr, n, float(r0), int(levels), out))
+    return [VoxelMap(ctypes.c_void_p(out[i])) for i in range(n)]
+
+
+class HandleArray:
+    """Pre-built array of handles (avoids rebuilding it on every call)."""
+
+    def __init__(self, objs):
+        self.objs = list(objs)
+        self.n = len(self.objs)
+        self.arr = (ctypes.c_void_p * max(self.n, 1))(*[o.handle.value for o in self.objs])
+
+
+def _handles(objs):
+    return objs if isinstance(objs, HandleArray) else HandleArray(objs)
+
+
+def as_factors(factors) -> np.ndarray:
+    f = np.asarray(factors)
+    if f.dtype == FACTOR_DTYPE:
+        return np.ascontiguousarray(f)
+    f = f.reshape(-1, 5).astype(np.int64)
+    out = np.empty(f.shape[0], FACTOR_DTYPE)
+    for i, name in enumerate(FACTOR_DTYPE.names):
+        out[name] = f[:, i]
+    return out
+
+
+def as_pairs(pairs) -> np.ndarray:
+    p = np.asarray(pairs)
+    if p.dtype == PAIR_DTYPE:
+        return np.ascontiguousarray(p)
+    p = p.reshape(-1, 4).astype(np.int64)
+    out = np.empty(p.shape[0], PAIR_DTYPE)
+    for i, name in enumerate(PAIR_DTYPE.names):
+        out[name] = p[:, i]
+    return out
+
+
+def as_poses(poses) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(poses, np.float64).reshape(-1, 12))
+
+
+def overlap(ctx: Context, clouds, maps, pairs, poses, level: int, out=None):
+    """gvox_overlap: int32 counts per pair (numpy, or into the int32 CUDA tensor `out`)."""
+    C, M = _handles(clouds), _handles(maps)
+    pairs = as_pairs(pairs)
+    poses = as_poses(poses)
+    if out is None:
+        out = np.empty(pairs.shape[0], np.int32)
+    po, mem = _ptr(out)
+    check(lib().gvox_overlap(ctx.handle, C.arr, C.n, M.arr, M.n, _ptr(pairs)[0], pairs.shape[0],
+                             _ptr(poses)[0], poses.shape[0], int(level), po, mem))
+    return out
+
+
+def device_records(ctx: Context, n: int, dtype: np.dtype):
+    torch = _torch()
+    return torch.empty((n, dtype.itemsize), dtype=torch.uint8, device=ctx.device)
+
+
+def records_to_numpy(t, dtype: np.dtype = LINEAR_FACTOR_DTYPE) -> np.ndarray:
+    if _is_cuda_tensor(t):
+        t = t.cpu().numpy()
+    return np.ascontiguousarray(t).view(dtype).reshape(-1)
+
+
+def linearize_batch(ctx: Context, clouds, maps, factors, poses, out=None, corr_dump=None):
+    """gvox_linearize_batch.  Returns a numpy structured array of
+    LINEAR_FACTOR_DTYPE (host) or fills the uint8 CUDA tensor `out`
+    ([F, 1008], see device_records).  corr_dump: optional int64 CUDA tensor
+    [sum_f N_f * L_f]."""
+    C, M = _handles(clouds), _handles(maps)
+    factors = as_factors(factors)
+    poses = as_poses(poses)
+    F = factors.shape[0]
+    if out is None:
+        out = np.zeros(F, LINEAR_FACTOR_DTYPE)
+    po, mem = _ptr(out)
+    pc = None
+    if corr_dump is not None:
+        assert _is_cuda_tensor(corr_dump)
+        pc = ctypes.c_void_p(corr_dump.data_ptr())
+    check(lib().gvox_linearize_batch(ctx.handle, C.arr, C.n, M.arr, M.n, _ptr(factors)[0], F,
+                                     _ptr(poses)[0], poses.shape[0], po, mem, pc))
+    return out
+
+
+def linearize_batch_accum(ctx: Context, clouds, maps, factors, poses, out=None):
+    """gvox_linearize_batch_accum: compact target-block records (FACTOR_ACCUM_DTYPE)."""
+    C, M = _handles(clouds), _handles(maps)
+    factors = as_factors(factors)
+    poses = as_poses(poses)
+    F = factors.shape[0]
+    if out is None:
+        out = np.zeros(F, FACTOR_ACCUM_DTYPE)
+    po, mem = _ptr(out)
+    check(lib().gvox_linearize_batch_accum(ctx.handle, C.arr, C.n, M.arr, M.n, _ptr(factors)[0], F,
+                                           _ptr(poses)[0], poses.shape[0], po, mem))
+    return out
+
+
+def expand(ctx: Context, factors, poses, accum, out=None):
+    """gvox_expand: compact records (uint8 CUDA tensor [F, 288]) -> full records."""
+    factors = as_factors(factors)
+    poses = as_poses(poses)
+    F = factors.shape[0]
+    assert _is_cuda_tensor(accum)
+    if out is None:
+        out = np.zeros(F, LINEAR_FACTOR_DTYPE)
+    po, mem = _ptr(out)
+    check(lib().gvox_expand(ctx.handle, _ptr(factors)[0], F, _ptr(poses)[0], poses.shape[0],
+                            ctypes.c_void_p(accum.data_ptr()), po, mem))
+    return out
+
+
+def corr_dump_size(clouds: Sequence[Cloud], maps: Sequence[VoxelMap], factors) -> int:
+    f = as_factors(factors)
+    return int(sum(clouds[int(a)].n * maps[int(b)].levels
+                   for a, b in zip(f["source_cloud"], f["target_map"])))
+
+
+def full_blocks(rec) -> dict:
+    """One LINEAR_FACTOR_DTYPE record -> dict of 6x6 / 6 numpy blocks."""
+    return {"H_ii": rec["H_ii"].reshape(6, 6), "H_ij": rec["H_ij"].reshape(6, 6),
+            "H_jj": rec["H_jj"].reshape(6, 6), "b_i": rec["b_i"], "b_j": rec["b_j"],
+            "e": float(rec["error"]), "inliers": rec["inliers"].copy(),
+            "num_invisible": int(rec["num_invisible"]),
+            "num_degenerate": int(rec["num_degenerate"])}

@@ -1,0 +1,165 @@
+// gvox_internal.h -- device-side data layout shared by the runtime
+// (gvox_runtime.cu) and the kernels (k_*.cu).  Not part of the ABI.
+//
+// HBM layout:
+//  * cloud: three planar float4 arrays of n points (48 B/point):
+//      A[k] = {mu.x, mu.y, mu.z, C.xx}
+//      B[k] = {C.xy, C.xz, C.yy, C.yz}
+//      N[k] = {C.zz, n.x, n.y, n.z}
+//    the overlap kernel streams only A (16 B/point); linearize streams all 3.
+//  * map level: open-addressing hash of 16 B slots {u64 packed key, i32 voxel
+//    index, pad} (capacity 2^k >= 2V, EMPTY key = ~0) + compact voxel records
+//    of 48 B: {off.x, off.y, off.z, C.xx}, {C.xy, C.xz, C.yy, C.yz},
+//    {C.zz, count (int bits), 0, 0}; `off` = voxel mean minus voxel centre in
+//    fp32 (the residual is formed as fp32(centre - q64) + off, reading Q12);
+//    + the packed key per voxel (u64) for export.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/gvox.h"
+
+namespace gvox {
+
+constexpr uint64_t kEmptyKey = ~0ull;
+constexpr int kKeyBits = 21;
+constexpr int32_t kKeyHalf = 1 << 20;
+
+struct CloudDev {
+  const float4* A;
+  const float4* B;
+  const float4* N;
+  int64_t n;
+  int32_t has_normals;
+  int32_t pad;
+};
+
+struct MapLevelDev {
+  const ulonglong2* slots;  // [mask + 1] {key, idx}
+  const float4* vox;        // [3 * nvox]
+  uint64_t mask;
+  double r;      // r0 * 2^l
+  double inv_r;  // 1 / r (used only when dyadic)
+  int64_t nvox;
+};
+
+struct MapDev {
+  int32_t levels;
+  int32_t dyadic;  // r0 is a power of two: floor(q * inv_r0) == floor(q / r0)
+  double r0;
+  double inv_r0;
+  MapLevelDev lv[GVOX_MAX_LEVELS];
+};
+
+// Per-tile partial of the linearize kernel (doubles; counts stored exactly).
+constexpr int kNumTerms = 28;
+constexpr int kPartialStride = 40;  // 28 terms, 8 inliers, invisible, degenerate, 2 pad
+
+__host__ __device__ inline uint64_t hash_slot(uint64_t key, uint64_t mask) {
+  // Fibonacci hashing of the packed key; the probe sequence is linear.
+  return (key * 0x9E3779B97F4A7C15ull) >> 20 & mask;
+}
+
+__host__ __device__ inline uint64_t pack_key(int32_t kx, int32_t ky, int32_t kz) {
+  return ((uint64_t)(uint32_t)(kx + kKeyHalf) << 42) | ((uint64_t)(uint32_t)(ky + kKeyHalf) << 21) |
+         (uint64_t)(uint32_t)(kz + kKeyHalf);
+}
+
+__host__ __device__ inline bool key_in_range(int32_t k) { return k >= -kKeyHalf && k < kKeyHalf; }
+
+// ---------------------------------------------------------------- launchers
+// (defined in k_*.cu; all asynchronous on `stream`)
+
+// cloud: pack user arrays into the planar layout; flags[0] |= 1 on non-finite
+// input; cmax_bits = max |C_ij| as float bits (atomicMax on non-negative floats).
+void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* A,
+                       float4* B, float4* N, int32_t* flags, uint32_t* cmax_bits,
+                       cudaStream_t stream);
+
+// voxelmap build, phase 1: insert keys of every (cloud point, level) into the
+// per-(map, level) temporary tables; assign compact voxel indices.
+struct BuildSeg {
+  const float4* A;          // cloud means (+C.xx)
+  int64_t n;                // points
+  int64_t pl_offset;        // offset of this cloud's (point, level) records
+  ulonglong2* tmp_slots[GVOX_MAX_LEVELS];  // temp tables (capacity tmp_mask+1)
+  uint64_t tmp_mask;
+  uint64_t* keys_by_idx[GVOX_MAX_LEVELS];  // [n] workspace: key of voxel idx
+  int32_t* counter;         // [levels] voxel counts (atomic)
+  // phase 1 records, per (point, level), the temp-table SLOT of its key;
+  // phase 2 reads the voxel index from that slot (all indices assigned by then).
+};
+void launch_build_insert(const BuildSeg* segs_dev, int64_t num_segs, const int64_t* seg_point_start,
+                         int64_t total_points, int levels, double r0, int dyadic, int32_t* pslot,
+                         int32_t* err, cudaStream_t stream);
+
+// phase 2: fixed-point accumulation of (sum offsets, sum cov, count) per voxel.
+struct AccumSeg {
+  const float4* A;
+  const float4* B;
+  const float4* N;
+  int64_t n;
+  int64_t pl_offset;
+  int64_t acc_offset[GVOX_MAX_LEVELS];  // first voxel of (seg, level) in acc[]
+  double mu_scale[GVOX_MAX_LEVELS];     // S_l = 2^F / r_l
+  double cov_scale;                     // 2^(F - e_c), 2^e_c >= max |C_ij| of the cloud
+};
+void launch_build_accum(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int64_t num_segs,
+                        const int64_t* seg_point_start, int64_t total_points, int levels,
+                        double r0, int dyadic, const int32_t* pslot, unsigned long long* acc,
+                        cudaStream_t stream);
+
+// phase 3: per voxel, finalize the record and insert into the final table.
+struct FinalSeg {
+  int64_t acc_offset;       // first voxel in acc[] / keys
+  int64_t nvox;
+  const uint64_t* keys_by_idx;
+  double r;
+  double mu_scale;
+  double cov_scale;
+  ulonglong2* slots;        // final table
+  uint64_t mask;
+  float4* vox;              // [3 * nvox]
+  uint64_t* keys_out;       // [nvox]
+};
+void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs,
+                           const int64_t* seg_vox_start, int64_t total_voxels,
+                           const unsigned long long* acc, cudaStream_t stream);
+
+void launch_fill_u64(uint64_t* p, uint64_t value, int64_t count, cudaStream_t stream);
+
+// lookup
+void launch_lookup(const MapDev* map, int level, const double* q, int64_t n, int64_t* out,
+                   cudaStream_t stream);
+
+// overlap
+struct PairDev {
+  int32_t src, tgt, pi, pj;
+};
+void launch_overlap(const CloudDev* const* clouds, const MapDev* const* maps, const PairDev* pairs,
+                    const int32_t* tile_start, int64_t num_pairs, int64_t num_tiles, int tile_pts,
+                    const double* poses, int level, int32_t* tile_pair, int32_t* counts,
+                    cudaStream_t stream);
+
+// linearize
+struct FactorDev {
+  int32_t src, tgt, pi, pj;
+  uint32_t flags;
+  int32_t pad;
+  int64_t corr_offset;  // first (point, level) record in corr_dump
+};
+void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
+                      const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
+                      int64_t num_tiles, int tile_pts, int max_levels, const double* poses,
+                      double* partials, int32_t* tile_factor, int64_t* corr_dump,
+                      cudaStream_t stream);
+// reduce tile partials per factor in fixed order; write full or compact records.
+void launch_reduce(const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
+                   const double* poses, const double* partials, gvox_linear_factor* out_full,
+                   gvox_factor_accum* out_accum, cudaStream_t stream);
+void launch_expand(const FactorDev* factors, int64_t num_factors, const double* poses,
+                   const gvox_factor_accum* accum, gvox_linear_factor* out, cudaStream_t stream);
+
+void note_launch();
+
+}  // namespace gvox

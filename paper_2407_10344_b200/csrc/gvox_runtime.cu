@@ -1,0 +1,950 @@
+// gvox_runtime.cu -- host runtime behind the C ABI of include/gvox.h:
+// contexts, device-resident cloud and map handles, the batch serializer
+// (P:224 / Fig.4: inputs serialized into ONE host block, ONE H2D, fused
+// launches, ONE D2H), workspace management and error reporting.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "gvox_internal.h"
+
+using namespace gvox;
+
+// ------------------------------------------------------------------ errors
+namespace {
+thread_local std::string g_last_error;
+thread_local int64_t g_launches = 0;
+
+gvox_status fail(gvox_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+gvox_status cuda_fail(cudaError_t e, const char* where) {
+  cudaGetLastError();  // clear sticky-free errors
+  if (e == cudaErrorMemoryAllocation)
+    return fail(GVOX_ERR_NOMEM, "%s: %s", where, cudaGetErrorString(e));
+  return fail(GVOX_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(call)                                        \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+#define CK_LAUNCH(where)                                 \
+  do {                                                   \
+    cudaError_t e_ = cudaGetLastError();                 \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where);  \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  bool changed = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) {
+      changed = cudaSetDevice(dev) == cudaSuccess;
+    }
+  }
+  ~DeviceGuard() {
+    if (changed) cudaSetDevice(prev);
+  }
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+uint64_t pow2_at_least(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+bool finite_pose(const double* T) {
+  for (int i = 0; i < 12; ++i)
+    if (!std::isfinite(T[i])) return false;
+  return true;
+}
+
+bool is_dyadic(double r) {
+  int e;
+  return std::frexp(r, &e) == 0.5;
+}
+
+// A device allocation shared by the handles carved out of it.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int device = 0;
+  ~DevBuf() {
+    if (ptr) {
+      DeviceGuard g(device);
+      cudaFree(ptr);
+    }
+  }
+};
+
+gvox_status devbuf_alloc(size_t bytes, int device, std::shared_ptr<DevBuf>* out) {
+  auto b = std::make_shared<DevBuf>();
+  b->device = device;
+  b->bytes = bytes;
+  if (bytes) {
+    cudaError_t e = cudaMalloc(&b->ptr, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  }
+  *out = b;
+  return GVOX_OK;
+}
+
+}  // namespace
+
+namespace gvox {
+void note_launch() { ++g_launches; }
+}  // namespace gvox
+
+// ------------------------------------------------------------------ handles
+struct gvox_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  // grow-only device workspaces
+  void* ws[3] = {nullptr, nullptr, nullptr};
+  size_t ws_bytes[3] = {0, 0, 0};
+  // pinned host staging for the single H2D input block
+  void* pin = nullptr;
+  size_t pin_bytes = 0;
+  cudaEvent_t pin_done = nullptr;  // last H2D out of `pin` has completed
+  bool pin_pending = false;
+};
+
+struct gvox_cloud {
+  std::shared_ptr<DevBuf> buf;
+  CloudDev desc{};       // host copy
+  CloudDev* dev = nullptr;  // device copy of desc
+  int64_t n = 0;
+  float cmax = 0.f;      // max |C_ij| (fixed-point scale of the voxel build)
+  int device = 0;
+};
+
+struct gvox_map {
+  std::shared_ptr<DevBuf> arena;
+  MapDev desc{};         // host copy
+  MapDev* dev = nullptr;
+  int levels = 0;
+  double r0 = 0;
+  int64_t nvox[GVOX_MAX_LEVELS] = {};
+  const uint64_t* keys[GVOX_MAX_LEVELS] = {};
+  int device = 0;
+};
+
+namespace {
+
+gvox_status ws_reserve(gvox_ctx* ctx, int which, size_t bytes, void** out) {
+  if (ctx->ws_bytes[which] < bytes) {
+    if (ctx->ws[which]) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      CK(cudaFree(ctx->ws[which]));
+      ctx->ws[which] = nullptr;
+      ctx->ws_bytes[which] = 0;
+    }
+    size_t nb = std::max(bytes, ctx->ws_bytes[which] * 3 / 2);
+    nb = align_up(nb, 1 << 20);
+    cudaError_t e = cudaMalloc(&ctx->ws[which], nb);
+    if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMalloc");
+    ctx->ws_bytes[which] = nb;
+  }
+  *out = ctx->ws[which];
+  return GVOX_OK;
+}
+
+// Pinned staging for the single H2D block; waits for the previous H2D out of
+// it to finish before handing it out again.
+gvox_status pin_reserve(gvox_ctx* ctx, size_t bytes, void** out) {
+  if (ctx->pin_pending) {
+    CK(cudaEventSynchronize(ctx->pin_done));
+    ctx->pin_pending = false;
+  }
+  if (ctx->pin_bytes < bytes) {
+    if (ctx->pin) CK(cudaFreeHost(ctx->pin));
+    ctx->pin = nullptr;
+    size_t nb = align_up(std::max(bytes, ctx->pin_bytes * 3 / 2), 1 << 16);
+    cudaError_t e = cudaHostAlloc(&ctx->pin, nb, cudaHostAllocDefault);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
+    ctx->pin_bytes = nb;
+  }
+  *out = ctx->pin;
+  return GVOX_OK;
+}
+
+gvox_status h2d_block(gvox_ctx* ctx, void* dst, const void* pinned_src, size_t bytes) {
+  if (bytes == 0) return GVOX_OK;
+  CK(cudaMemcpyAsync(dst, pinned_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaEventRecord(ctx->pin_done, ctx->stream));
+  ctx->pin_pending = true;
+  return GVOX_OK;
+}
+
+// Layout helper: a sequence of 256 B-aligned regions within one block.
+struct Layout {
+  size_t size = 0;
+  size_t add(size_t bytes) {
+    size_t off = size;
+    size = align_up(size + bytes, 256);
+    return off;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+// ------------------------------------------------------------------ context
+gvox_status gvox_ctx_create(int device, void* cuda_stream, gvox_ctx** out) {
+  if (!out) return fail(GVOX_ERR_INVALID, "gvox_ctx_create: out is NULL");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev)
+    return fail(GVOX_ERR_INVALID, "gvox_ctx_create: device %d out of range [0, %d)", device, ndev);
+  DeviceGuard g(device);
+  auto* c = new gvox_ctx;
+  c->device = device;
+  c->stream = (cudaStream_t)cuda_stream;
+  e = cudaEventCreateWithFlags(&c->pin_done, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaEventCreate");
+  }
+  *out = c;
+  return GVOX_OK;
+}
+
+gvox_status gvox_ctx_set_stream(gvox_ctx* ctx, void* cuda_stream) {
+  if (!ctx) return fail(GVOX_ERR_INVALID, "gvox_ctx_set_stream: ctx is NULL");
+  ctx->stream = (cudaStream_t)cuda_stream;
+  return GVOX_OK;
+}
+
+void gvox_ctx_destroy(gvox_ctx* ctx) {
+  if (!ctx) return;
+  DeviceGuard g(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (int i = 0; i < 3; ++i)
+    if (ctx->ws[i]) cudaFree(ctx->ws[i]);
+  if (ctx->pin) cudaFreeHost(ctx->pin);
+  if (ctx->pin_done) cudaEventDestroy(ctx->pin_done);
+  delete ctx;
+}
+
+// ------------------------------------------------------------------ clouds
+gvox_status gvox_cloud_create(gvox_ctx* ctx, const float* mu, const float* cov,
+                              const float* normals, int64_t n, int mem, gvox_cloud** out) {
+  if (!ctx || !out) return fail(GVOX_ERR_INVALID, "gvox_cloud_create: ctx/out is NULL");
+  *out = nullptr;
+  if (n < 0) return fail(GVOX_ERR_INVALID, "gvox_cloud_create: n = %lld < 0", (long long)n);
+  if (n > 0 && (!mu || !cov))
+    return fail(GVOX_ERR_INVALID, "gvox_cloud_create: mu/cov is NULL with n = %lld", (long long)n);
+  if (mem != GVOX_HOST && mem != GVOX_DEVICE)
+    return fail(GVOX_ERR_INVALID, "gvox_cloud_create: mem must be GVOX_HOST or GVOX_DEVICE");
+  DeviceGuard g(ctx->device);
+  Layout lay;
+  size_t o_desc = lay.add(sizeof(CloudDev));
+  size_t o_a = lay.add(16 * (size_t)n), o_b = lay.add(16 * (size_t)n), o_n = lay.add(16 * (size_t)n);
+  std::shared_ptr<DevBuf> buf;
+  gvox_status st = devbuf_alloc(lay.size, ctx->device, &buf);
+  if (st) return st;
+  char* base = (char*)buf->ptr;
+  auto* c = new gvox_cloud;
+  c->buf = buf;
+  c->n = n;
+  c->device = ctx->device;
+  c->dev = (CloudDev*)(base + o_desc);
+  c->desc.n = n;
+  c->desc.has_normals = normals != nullptr;
+  c->desc.A = n ? (const float4*)(base + o_a) : nullptr;
+  c->desc.B = n ? (const float4*)(base + o_b) : nullptr;
+  c->desc.N = n ? (const float4*)(base + o_n) : nullptr;
+  if (n > 0) {
+    // source arrays on the device (copy host arrays into a workspace first)
+    const float *dmu = mu, *dcov = cov, *dnrm = normals;
+    void* ws = nullptr;
+    size_t bytes_in = (size_t)n * (3 + 6 + (normals ? 3 : 0)) * 4;
+    st = ws_reserve(ctx, 2, bytes_in + 256, &ws);
+    if (st) {
+      delete c;
+      return st;
+    }
+    int32_t* flags = (int32_t*)ws;
+    uint32_t* cmax = (uint32_t*)((char*)ws + 4);
+    if (mem == GVOX_HOST) {
+      char* p = (char*)ws + 256;
+      cudaMemcpyAsync(p, mu, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream);
+      cudaMemcpyAsync(p + n * 12, cov, (size_t)n * 24, cudaMemcpyHostToDevice, ctx->stream);
+      if (normals)
+        cudaMemcpyAsync(p + n * 36, normals, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream);
+      dmu = (const float*)p;
+      dcov = (const float*)(p + n * 12);
+      dnrm = normals ? (const float*)(p + n * 36) : nullptr;
+    }
+    cudaMemsetAsync(ws, 0, 8, ctx->stream);
+    launch_cloud_pack(dmu, dcov, dnrm, n, (float4*)c->desc.A, (float4*)c->desc.B,
+                      (float4*)c->desc.N, flags, cmax, ctx->stream);
+    cudaError_t e = cudaGetLastError();
+    int32_t hflags[2] = {0, 0};
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(hflags, ws, 8, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+      delete c;
+      return cuda_fail(e, "gvox_cloud_create");
+    }
+    if (hflags[0] & 1) {
+      delete c;
+      return fail(GVOX_ERR_INVALID, "gvox_cloud_create: non-finite coordinate, covariance or normal");
+    }
+    uint32_t bits = (uint32_t)hflags[1];
+    std::memcpy(&c->cmax, &bits, 4);
+  }
+  cudaError_t e = cudaMemcpyAsync(c->dev, &c->desc, sizeof(CloudDev), cudaMemcpyHostToDevice,
+                                  ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "gvox_cloud_create: descriptor upload");
+  }
+  *out = c;
+  return GVOX_OK;
+}
+
+int64_t gvox_cloud_size(const gvox_cloud* cloud) { return cloud ? cloud->n : -1; }
+
+void gvox_cloud_destroy(gvox_cloud* cloud) { delete cloud; }
+
+// ------------------------------------------------------------------ voxelmaps
+namespace {
+
+constexpr int64_t kBuildChunkPoints = 8 << 20;
+
+gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t count, double r0,
+                        int levels, gvox_map** maps_out) {
+  const int dyadic = is_dyadic(r0);
+  const int L = levels;
+  // ---- phase 1 layout (workspace 0)
+  std::vector<int64_t> seg_start(count + 1, 0);
+  for (int64_t s = 0; s < count; ++s) seg_start[s + 1] = seg_start[s] + clouds[s]->n;
+  const int64_t total = seg_start[count];
+  std::vector<uint64_t> tcap(count);
+  Layout lay;
+  std::vector<size_t> o_tmp(count), o_keys(count);
+  for (int64_t s = 0; s < count; ++s) {
+    tcap[s] = pow2_at_least(std::max<uint64_t>(16, 2 * (uint64_t)clouds[s]->n));
+    o_tmp[s] = lay.add(tcap[s] * 16 * L);
+    o_keys[s] = lay.add((size_t)clouds[s]->n * 8 * L);
+  }
+  size_t o_pslot = lay.add((size_t)total * L * 4);
+  size_t o_cnt = lay.add((size_t)count * L * 4 + 4);
+  size_t o_bseg = lay.add(sizeof(BuildSeg) * count);
+  size_t o_aseg = lay.add(sizeof(AccumSeg) * count);
+  size_t o_start = lay.add(8 * (count + 1));
+  void* ws0 = nullptr;
+  gvox_status st = ws_reserve(ctx, 0, lay.size, &ws0);
+  if (st) return st;
+  char* b0 = (char*)ws0;
+  int32_t* d_cnt = (int32_t*)(b0 + o_cnt);
+  int32_t* d_err = d_cnt + count * L;
+
+  std::vector<BuildSeg> bseg(count);
+  for (int64_t s = 0; s < count; ++s) {
+    BuildSeg& g = bseg[s];
+    std::memset(&g, 0, sizeof(g));
+    g.A = clouds[s]->desc.A;
+    g.n = clouds[s]->n;
+    g.pl_offset = seg_start[s] * L;
+    g.tmp_mask = tcap[s] - 1;
+    for (int l = 0; l < L; ++l) {
+      g.tmp_slots[l] = (ulonglong2*)(b0 + o_tmp[s]) + tcap[s] * l;
+      g.keys_by_idx[l] = (uint64_t*)(b0 + o_keys[s]) + (size_t)clouds[s]->n * l;
+    }
+    g.counter = d_cnt + s * L;
+  }
+  // tables -> EMPTY (all 0xFF: key ~0, idx -1), counters + err -> 0
+  for (int64_t s = 0; s < count; ++s)
+    CK(cudaMemsetAsync(b0 + o_tmp[s], 0xFF, tcap[s] * 16 * L, ctx->stream));
+  CK(cudaMemsetAsync(d_cnt, 0, (size_t)count * L * 4 + 4, ctx->stream));
+  CK(cudaMemcpyAsync(b0 + o_bseg, bseg.data(), sizeof(BuildSeg) * count, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(b0 + o_start, seg_start.data(), 8 * (count + 1), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  launch_build_insert((const BuildSeg*)(b0 + o_bseg), count, (const int64_t*)(b0 + o_start), total,
+                      L, r0, dyadic, (int32_t*)(b0 + o_pslot), d_err, ctx->stream);
+  CK_LAUNCH("voxelmap insert");
+  std::vector<int32_t> hcnt((size_t)count * L + 1);
+  CK(cudaMemcpyAsync(hcnt.data(), d_cnt, ((size_t)count * L + 1) * 4, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hcnt[(size_t)count * L])
+    return fail(GVOX_ERR_RANGE,
+                "gvox_create_voxelmap: a voxel key is outside [-2^20, 2^20) (r0 = %g)", r0);
+
+  // ---- final arena (exact sizes)
+  Layout al;
+  std::vector<size_t> o_desc(count);
+  std::vector<std::array<size_t, 3>> o_lv((size_t)count * L);
+  std::vector<uint64_t> fcap((size_t)count * L);
+  int64_t total_vox = 0;
+  for (int64_t s = 0; s < count; ++s) {
+    o_desc[s] = al.add(sizeof(MapDev));
+    for (int l = 0; l < L; ++l) {
+      int64_t V = hcnt[s * L + l];
+      uint64_t cap = pow2_at_least(std::max<uint64_t>(2, 2 * (uint64_t)V));
+      fcap[s * L + l] = cap;
+      o_lv[s * L + l] = {al.add(cap * 16), al.add((size_t)V * 48), al.add((size_t)V * 8)};
+      total_vox += V;
+    }
+  }
+  std::shared_ptr<DevBuf> arena;
+  st = devbuf_alloc(al.size, ctx->device, &arena);
+  if (st) return st;
+  char* ab = (char*)arena->ptr;
+  // ---- phase 2/3 workspace (workspace 1): acc [total_vox][10] + seg tables
+  Layout l1;
+  size_t o_acc = l1.add((size_t)total_vox * 80);
+  size_t o_fseg = l1.add(sizeof(FinalSeg) * count * L);
+  size_t o_vstart = l1.add(8 * ((size_t)count * L + 1));
+  void* ws1 = nullptr;
+  st = ws_reserve(ctx, 1, l1.size, &ws1);
+  if (st) return st;
+  char* b1 = (char*)ws1;
+  CK(cudaMemsetAsync(b1 + o_acc, 0, (size_t)total_vox * 80, ctx->stream));
+
+  std::vector<AccumSeg> aseg(count);
+  std::vector<FinalSeg> fseg((size_t)count * L);
+  std::vector<int64_t> vstart((size_t)count * L + 1, 0);
+  std::vector<MapDev> mdesc(count);
+  int64_t vacc = 0;
+  for (int64_t s = 0; s < count; ++s) {
+    const gvox_cloud* c = clouds[s];
+    // fixed-point: F fraction bits so that n * 2^F <= 2^61
+    int nb = 0;
+    while ((1ll << nb) <= c->n) ++nb;  // 2^nb > n
+    int F = 61 - nb;
+    int ec = 0;
+    if (c->cmax > 0.f) {
+      std::frexp((double)c->cmax, &ec);  // cmax < 2^ec
+    }
+    AccumSeg& a = aseg[s];
+    std::memset(&a, 0, sizeof(a));
+    a.A = c->desc.A;
+    a.B = c->desc.B;
+    a.N = c->desc.N;
+    a.n = c->n;
+    a.pl_offset = seg_start[s] * L;
+    a.cov_scale = std::ldexp(1.0, F - ec);
+    MapDev& md = mdesc[s];
+    std::memset(&md, 0, sizeof(md));
+    md.levels = L;
+    md.dyadic = dyadic;
+    md.r0 = r0;
+    md.inv_r0 = 1.0 / r0;
+    for (int l = 0; l < L; ++l) {
+      int64_t V = hcnt[s * L + l];
+      double r = std::ldexp(r0, l);
+      a.acc_offset[l] = vacc;
+      a.mu_scale[l] = std::ldexp(1.0, F) / r;
+      FinalSeg& f = fseg[s * L + l];
+      f.acc_offset = vacc;
+      f.nvox = V;
+      f.keys_by_idx = bseg[s].keys_by_idx[l];
+      f.r = r;
+      f.mu_scale = a.mu_scale[l];
+      f.cov_scale = a.cov_scale;
+      f.slots = (ulonglong2*)(ab + o_lv[s * L + l][0]);
+      f.mask = fcap[s * L + l] - 1;
+      f.vox = (float4*)(ab + o_lv[s * L + l][1]);
+      f.keys_out = (uint64_t*)(ab + o_lv[s * L + l][2]);
+      vstart[s * L + l + 1] = vstart[s * L + l] + V;
+      MapLevelDev& lv = md.lv[l];
+      lv.slots = f.slots;
+      lv.vox = f.vox;
+      lv.mask = f.mask;
+      lv.r = r;
+      lv.inv_r = 1.0 / r;
+      lv.nvox = V;
+      CK(cudaMemsetAsync(f.slots, 0xFF, fcap[s * L + l] * 16, ctx->stream));
+      vacc += V;
+    }
+  }
+  CK(cudaMemcpyAsync(b0 + o_aseg, aseg.data(), sizeof(AccumSeg) * count, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(b1 + o_fseg, fseg.data(), sizeof(FinalSeg) * count * L,
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(b1 + o_vstart, vstart.data(), 8 * ((size_t)count * L + 1),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  launch_build_accum((const BuildSeg*)(b0 + o_bseg), (const AccumSeg*)(b0 + o_aseg), count,
+                     (const int64_t*)(b0 + o_start), total, L, r0, dyadic,
+                     (const int32_t*)(b0 + o_pslot), (unsigned long long*)(b1 + o_acc), ctx->stream);
+  CK_LAUNCH("voxelmap accumulate");
+  launch_build_finalize((const FinalSeg*)(b1 + o_fseg), count * L, (const int64_t*)(b1 + o_vstart),
+                        total_vox, (const unsigned long long*)(b1 + o_acc), ctx->stream);
+  CK_LAUNCH("voxelmap finalize");
+  for (int64_t s = 0; s < count; ++s)
+    CK(cudaMemcpyAsync(ab + o_desc[s], &mdesc[s], sizeof(MapDev), cudaMemcpyHostToDevice,
+                       ctx->stream));
+  // the host vectors above are pageable: cudaMemcpyAsync has staged them on return,
+  // but keep the stream ordered before the next chunk reuses the workspaces.
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int64_t s = 0; s < count; ++s) {
+    auto* m = new gvox_map;
+    m->arena = arena;
+    m->desc = mdesc[s];
+    m->dev = (MapDev*)(ab + o_desc[s]);
+    m->levels = L;
+    m->r0 = r0;
+    m->device = ctx->device;
+    for (int l = 0; l < L; ++l) {
+      m->nvox[l] = hcnt[s * L + l];
+      m->keys[l] = fseg[s * L + l].keys_out;
+    }
+    maps_out[s] = m;
+  }
+  return GVOX_OK;
+}
+
+}  // namespace
+
+gvox_status gvox_create_voxelmaps(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t count,
+                                  double r0, int levels, gvox_map** maps_out) {
+  if (!ctx || (!clouds && count > 0) || (!maps_out && count > 0))
+    return fail(GVOX_ERR_INVALID, "gvox_create_voxelmaps: NULL argument");
+  if (count < 0) return fail(GVOX_ERR_INVALID, "gvox_create_voxelmaps: count < 0");
+  if (!(r0 > 0.0) || !std::isfinite(r0))
+    return fail(GVOX_ERR_INVALID, "gvox_create_voxelmap: r0 = %g must be finite and > 0", r0);
+  if (levels < 1 || levels > GVOX_MAX_LEVELS)
+    return fail(GVOX_ERR_INVALID, "gvox_create_voxelmap: levels = %d outside [1, %d]", levels,
+                GVOX_MAX_LEVELS);
+  for (int64_t s = 0; s < count; ++s) {
+    if (!clouds[s]) return fail(GVOX_ERR_INVALID, "gvox_create_voxelmaps: clouds[%lld] is NULL", (long long)s);
+    maps_out[s] = nullptr;
+  }
+  DeviceGuard g(ctx->device);
+  int64_t s0 = 0;
+  while (s0 < count) {
+    int64_t s1 = s0, pts = 0;
+    while (s1 < count && (s1 == s0 || pts + clouds[s1]->n <= kBuildChunkPoints)) pts += clouds[s1++]->n;
+    gvox_status st = build_chunk(ctx, clouds + s0, s1 - s0, r0, levels, maps_out + s0);
+    if (st) {
+      for (int64_t s = 0; s < s0; ++s) {
+        delete maps_out[s];
+        maps_out[s] = nullptr;
+      }
+      return st;
+    }
+    s0 = s1;
+  }
+  return GVOX_OK;
+}
+
+gvox_status gvox_create_voxelmap(gvox_ctx* ctx, const gvox_cloud* cloud, double r0, int levels,
+                                 gvox_map** out) {
+  if (!cloud || !out) return fail(GVOX_ERR_INVALID, "gvox_create_voxelmap: NULL argument");
+  return gvox_create_voxelmaps(ctx, &cloud, 1, r0, levels, out);
+}
+
+gvox_status gvox_voxelmap_info(const gvox_map* map, int level, int64_t* num_voxels,
+                               double* resolution) {
+  if (!map) return fail(GVOX_ERR_INVALID, "gvox_voxelmap_info: map is NULL");
+  if (level < 0 || level >= map->levels)
+    return fail(GVOX_ERR_INVALID, "gvox_voxelmap_info: level %d outside [0, %d)", level, map->levels);
+  if (num_voxels) *num_voxels = map->nvox[level];
+  if (resolution) *resolution = std::ldexp(map->r0, level);
+  return GVOX_OK;
+}
+
+int gvox_voxelmap_levels(const gvox_map* map) { return map ? map->levels : -1; }
+
+gvox_status gvox_voxelmap_export(gvox_ctx* ctx, const gvox_map* map, int level, int64_t* keys,
+                                 double* means, double* covs, int32_t* counts) {
+  if (!ctx || !map) return fail(GVOX_ERR_INVALID, "gvox_voxelmap_export: NULL argument");
+  if (level < 0 || level >= map->levels)
+    return fail(GVOX_ERR_INVALID, "gvox_voxelmap_export: level %d outside [0, %d)", level, map->levels);
+  DeviceGuard g(ctx->device);
+  const int64_t V = map->nvox[level];
+  std::vector<uint64_t> k(V);
+  std::vector<float4> v(3 * V);
+  if (V) {
+    CK(cudaMemcpyAsync(k.data(), map->keys[level], 8 * V, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(v.data(), map->desc.lv[level].vox, 48 * V, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::vector<int64_t> ord(V);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return k[a] < k[b]; });
+  const double r = std::ldexp(map->r0, level);
+  for (int64_t i = 0; i < V; ++i) {
+    int64_t j = ord[i];
+    uint64_t key = k[j];
+    int64_t kk[3] = {(int64_t)((key >> 42) & 0x1FFFFF) - kKeyHalf,
+                     (int64_t)((key >> 21) & 0x1FFFFF) - kKeyHalf, (int64_t)(key & 0x1FFFFF) - kKeyHalf};
+    const float4 a = v[3 * j], b = v[3 * j + 1], c = v[3 * j + 2];
+    if (keys) keys[i] = (int64_t)key;
+    if (means) {
+      const float off[3] = {a.x, a.y, a.z};
+      for (int d = 0; d < 3; ++d) means[3 * i + d] = ((double)kk[d] + 0.5) * r + (double)off[d];
+    }
+    if (covs) {
+      const float cv[6] = {a.w, b.x, b.y, b.z, b.w, c.x};
+      for (int d = 0; d < 6; ++d) covs[6 * i + d] = cv[d];
+    }
+    if (counts) {
+      int32_t cnt;
+      std::memcpy(&cnt, &c.y, 4);
+      counts[i] = cnt;
+    }
+  }
+  return GVOX_OK;
+}
+
+gvox_status gvox_voxelmap_lookup(gvox_ctx* ctx, const gvox_map* map, int level, const double* q,
+                                 int64_t n, int64_t* keys_out, int mem) {
+  if (!ctx || !map || (n > 0 && (!q || !keys_out)))
+    return fail(GVOX_ERR_INVALID, "gvox_voxelmap_lookup: NULL argument");
+  if (n < 0) return fail(GVOX_ERR_INVALID, "gvox_voxelmap_lookup: n < 0");
+  if (level < 0 || level >= map->levels)
+    return fail(GVOX_ERR_INVALID, "gvox_voxelmap_lookup: level %d outside [0, %d)", level, map->levels);
+  if (n == 0) return GVOX_OK;
+  DeviceGuard g(ctx->device);
+  const double* dq = q;
+  int64_t* dout = keys_out;
+  if (mem == GVOX_HOST) {
+    void* ws = nullptr;
+    gvox_status st = ws_reserve(ctx, 2, (size_t)n * 32 + 256, &ws);
+    if (st) return st;
+    dq = (const double*)ws;
+    dout = (int64_t*)((char*)ws + align_up((size_t)n * 24, 256));
+    CK(cudaMemcpyAsync((void*)dq, q, (size_t)n * 24, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  launch_lookup(map->dev, level, dq, n, dout, ctx->stream);
+  CK_LAUNCH("gvox_voxelmap_lookup");
+  if (mem == GVOX_HOST) {
+    CK(cudaMemcpyAsync(keys_out, dout, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return GVOX_OK;
+}
+
+void gvox_map_destroy(gvox_map* map) { delete map; }
+
+// ------------------------------------------------------------------ overlap
+gvox_status gvox_overlap(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t num_clouds,
+                         const gvox_map* const* maps, int64_t num_maps, const gvox_pair* pairs,
+                         int64_t num_pairs, const double* poses, int64_t num_poses, int level,
+                         int32_t* counts, int mem) {
+  if (!ctx) return fail(GVOX_ERR_INVALID, "gvox_overlap: ctx is NULL");
+  if (num_pairs < 0) return fail(GVOX_ERR_INVALID, "gvox_overlap: num_pairs < 0");
+  if (num_pairs == 0) return GVOX_OK;
+  if (!clouds || !maps || !pairs || !poses || !counts)
+    return fail(GVOX_ERR_INVALID, "gvox_overlap: NULL argument");
+  for (int64_t p = 0; p < num_pairs; ++p) {
+    const gvox_pair& q = pairs[p];
+    if (q.source_cloud < 0 || q.source_cloud >= num_clouds || !clouds[q.source_cloud])
+      return fail(GVOX_ERR_INVALID, "gvox_overlap: pair %lld: source_cloud %d out of range [0, %lld)",
+                  (long long)p, q.source_cloud, (long long)num_clouds);
+    if (q.target_map < 0 || q.target_map >= num_maps || !maps[q.target_map])
+      return fail(GVOX_ERR_INVALID, "gvox_overlap: pair %lld: target_map %d out of range [0, %lld)",
+                  (long long)p, q.target_map, (long long)num_maps);
+    if (q.pose_i < 0 || q.pose_i >= num_poses || q.pose_j < 0 || q.pose_j >= num_poses)
+      return fail(GVOX_ERR_INVALID, "gvox_overlap: pair %lld: pose index out of range [0, %lld)",
+                  (long long)p, (long long)num_poses);
+    if (level < 0 || level >= maps[q.target_map]->levels)
+      return fail(GVOX_ERR_INVALID, "gvox_overlap: pair %lld: level %d outside the target map's [0, %d)",
+                  (long long)p, level, maps[q.target_map]->levels);
+  }
+  for (int64_t i = 0; i < num_poses; ++i)
+    if (!finite_pose(poses + 12 * i))
+      return fail(GVOX_ERR_INVALID, "gvox_overlap: pose %lld is not finite", (long long)i);
+  DeviceGuard g(ctx->device);
+  // tiles of 2048 source points
+  const int tile_pts = 2048;
+  std::vector<int32_t> tstart(num_pairs + 1, 0);
+  for (int64_t p = 0; p < num_pairs; ++p) {
+    int64_t n = clouds[pairs[p].source_cloud]->n;
+    tstart[p + 1] = tstart[p] + (int32_t)((n + tile_pts - 1) / tile_pts);
+  }
+  const int64_t T = tstart[num_pairs];
+  // ---- one serialized input block
+  Layout lay;
+  size_t o_pose = lay.add(96 * num_poses);
+  size_t o_pair = lay.add(sizeof(PairDev) * num_pairs);
+  size_t o_ts = lay.add(4 * (num_pairs + 1));
+  size_t o_cl = lay.add(8 * num_clouds);
+  size_t o_mp = lay.add(8 * num_maps);
+  size_t in_bytes = lay.size;
+  void* pin = nullptr;
+  gvox_status st = pin_reserve(ctx, in_bytes, &pin);
+  if (st) return st;
+  char* hp = (char*)pin;
+  std::memcpy(hp + o_pose, poses, 96 * num_poses);
+  std::memcpy(hp + o_pair, pairs, sizeof(PairDev) * num_pairs);
+  std::memcpy(hp + o_ts, tstart.data(), 4 * (num_pairs + 1));
+  for (int64_t i = 0; i < num_clouds; ++i) ((const CloudDev**)(hp + o_cl))[i] = clouds[i] ? clouds[i]->dev : nullptr;
+  for (int64_t i = 0; i < num_maps; ++i) ((const MapDev**)(hp + o_mp))[i] = maps[i] ? maps[i]->dev : nullptr;
+  Layout wl;
+  size_t o_in = wl.add(in_bytes);
+  size_t o_tp = wl.add(4 * (size_t)std::max<int64_t>(T, 1));
+  size_t o_cnt = wl.add(4 * num_pairs);
+  void* ws = nullptr;
+  st = ws_reserve(ctx, 0, wl.size, &ws);
+  if (st) return st;
+  char* wb = (char*)ws;
+  st = h2d_block(ctx, wb + o_in, hp, in_bytes);
+  if (st) return st;
+  char* din = wb + o_in;
+  int32_t* dcounts = mem == GVOX_DEVICE ? counts : (int32_t*)(wb + o_cnt);
+  CK(cudaMemsetAsync(dcounts, 0, 4 * num_pairs, ctx->stream));
+  launch_overlap((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
+                 (const PairDev*)(din + o_pair), (const int32_t*)(din + o_ts), num_pairs, T, tile_pts,
+                 (const double*)(din + o_pose), level, (int32_t*)(wb + o_tp), dcounts, ctx->stream);
+  CK_LAUNCH("gvox_overlap");
+  if (mem == GVOX_HOST) {
+    CK(cudaMemcpyAsync(counts, dcounts, 4 * num_pairs, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return GVOX_OK;
+}
+
+// ------------------------------------------------------------------ linearize
+namespace {
+
+gvox_status validate_factors(const char* fn, const gvox_cloud* const* clouds, int64_t num_clouds,
+                             const gvox_map* const* maps, int64_t num_maps,
+                             const gvox_factor* factors, int64_t num_factors, const double* poses,
+                             int64_t num_poses) {
+  for (int64_t f = 0; f < num_factors; ++f) {
+    const gvox_factor& q = factors[f];
+    if (clouds) {
+      if (q.source_cloud < 0 || q.source_cloud >= num_clouds || !clouds[q.source_cloud])
+        return fail(GVOX_ERR_INVALID, "%s: factor %lld: source_cloud %d out of range [0, %lld)", fn,
+                    (long long)f, q.source_cloud, (long long)num_clouds);
+    }
+    if (maps) {
+      if (q.target_map < 0 || q.target_map >= num_maps || !maps[q.target_map])
+        return fail(GVOX_ERR_INVALID, "%s: factor %lld: target_map %d out of range [0, %lld)", fn,
+                    (long long)f, q.target_map, (long long)num_maps);
+    }
+    if (q.pose_i < 0 || q.pose_i >= num_poses)
+      return fail(GVOX_ERR_INVALID, "%s: factor %lld: pose_i %d missing (pose table has %lld)", fn,
+                  (long long)f, q.pose_i, (long long)num_poses);
+    if (q.pose_j < 0 || q.pose_j >= num_poses)
+      return fail(GVOX_ERR_INVALID, "%s: factor %lld: pose_j %d missing (pose table has %lld)", fn,
+                  (long long)f, q.pose_j, (long long)num_poses);
+    if (q.flags & ~(uint32_t)(GVOX_F_VALIDATE_SURFACE | GVOX_F_ERROR_ONLY))
+      return fail(GVOX_ERR_INVALID, "%s: factor %lld: unknown flags 0x%x", fn, (long long)f, q.flags);
+  }
+  for (int64_t i = 0; i < num_poses; ++i)
+    if (!finite_pose(poses + 12 * i))
+      return fail(GVOX_ERR_INVALID, "%s: pose %lld is not finite", fn, (long long)i);
+  return GVOX_OK;
+}
+
+gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t num_clouds,
+                           const gvox_map* const* maps, int64_t num_maps,
+                           const gvox_factor* factors, int64_t num_factors, const double* poses,
+                           int64_t num_poses, gvox_linear_factor* out_full,
+                           gvox_factor_accum* out_accum, int mem, int64_t* corr_dump) {
+  const char* fn = out_full ? "gvox_linearize_batch" : "gvox_linearize_batch_accum";
+  if (!ctx) return fail(GVOX_ERR_INVALID, "%s: ctx is NULL", fn);
+  if (num_factors < 0) return fail(GVOX_ERR_INVALID, "%s: num_factors < 0", fn);
+  if (num_factors == 0) return GVOX_OK;
+  if (!clouds || !maps || !factors || !poses || !(out_full || out_accum))
+    return fail(GVOX_ERR_INVALID, "%s: NULL argument", fn);
+  if (mem != GVOX_HOST && mem != GVOX_DEVICE)
+    return fail(GVOX_ERR_INVALID, "%s: mem must be GVOX_HOST or GVOX_DEVICE", fn);
+  gvox_status st = validate_factors(fn, clouds, num_clouds, maps, num_maps, factors, num_factors,
+                                    poses, num_poses);
+  if (st) return st;
+  DeviceGuard g(ctx->device);
+  // ---- tile plan: tiles of tile_pts consecutive points of one factor
+  int64_t total_pf = 0;
+  int max_levels = 1;
+  for (int64_t f = 0; f < num_factors; ++f) {
+    total_pf += clouds[factors[f].source_cloud]->n;
+    max_levels = std::max(max_levels, maps[factors[f].target_map]->levels);
+  }
+  int ppt = 1;  // points per thread per tile: enough tiles for ~4 waves of 296 CTAs
+  while (ppt < 16 && total_pf / ((int64_t)256 * ppt * 2) >= 148 * 2 * 4) ppt *= 2;
+  const int tile_pts = 256 * ppt;
+  std::vector<int32_t> tstart(num_factors + 1, 0);
+  std::vector<FactorDev> fdev(num_factors);
+  int64_t corr_off = 0;
+  for (int64_t f = 0; f < num_factors; ++f) {
+    const gvox_factor& q = factors[f];
+    int64_t n = clouds[q.source_cloud]->n;
+    int64_t nt = (n + tile_pts - 1) / tile_pts;
+    if ((int64_t)tstart[f] + nt > INT32_MAX)
+      return fail(GVOX_ERR_INVALID, "%s: batch too large (more than 2^31 tiles)", fn);
+    tstart[f + 1] = tstart[f] + (int32_t)nt;
+    FactorDev& d = fdev[f];
+    d.src = q.source_cloud;
+    d.tgt = q.target_map;
+    d.pi = q.pose_i;
+    d.pj = q.pose_j;
+    d.flags = q.flags;
+    d.pad = 0;
+    d.corr_offset = corr_off;
+    corr_off += n * maps[q.target_map]->levels;
+  }
+  const int64_t T = tstart[num_factors];
+  // ---- the single serialized input block
+  Layout lay;
+  size_t o_pose = lay.add(96 * num_poses);
+  size_t o_fac = lay.add(sizeof(FactorDev) * num_factors);
+  size_t o_ts = lay.add(4 * (num_factors + 1));
+  size_t o_cl = lay.add(8 * num_clouds);
+  size_t o_mp = lay.add(8 * num_maps);
+  const size_t in_bytes = lay.size;
+  void* pin = nullptr;
+  st = pin_reserve(ctx, in_bytes, &pin);
+  if (st) return st;
+  char* hp = (char*)pin;
+  std::memcpy(hp + o_pose, poses, 96 * num_poses);
+  std::memcpy(hp + o_fac, fdev.data(), sizeof(FactorDev) * num_factors);
+  std::memcpy(hp + o_ts, tstart.data(), 4 * (num_factors + 1));
+  for (int64_t i = 0; i < num_clouds; ++i) ((const CloudDev**)(hp + o_cl))[i] = clouds[i] ? clouds[i]->dev : nullptr;
+  for (int64_t i = 0; i < num_maps; ++i) ((const MapDev**)(hp + o_mp))[i] = maps[i] ? maps[i]->dev : nullptr;
+  // ---- device workspace
+  Layout wl;
+  size_t o_in = wl.add(in_bytes);
+  size_t o_part = wl.add(8 * kPartialStride * (size_t)std::max<int64_t>(T, 1));
+  size_t o_tf = wl.add(4 * (size_t)std::max<int64_t>(T, 1));
+  size_t out_rec = out_full ? sizeof(gvox_linear_factor) : sizeof(gvox_factor_accum);
+  size_t o_out = wl.add(mem == GVOX_HOST ? out_rec * num_factors : 0);
+  void* ws = nullptr;
+  st = ws_reserve(ctx, 0, wl.size, &ws);
+  if (st) return st;
+  char* wb = (char*)ws;
+  st = h2d_block(ctx, wb + o_in, hp, in_bytes);
+  if (st) return st;
+  char* din = wb + o_in;
+  void* dout = mem == GVOX_DEVICE ? (out_full ? (void*)out_full : (void*)out_accum) : (void*)(wb + o_out);
+  launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
+                   (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
+                   tile_pts, max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
+                   (int32_t*)(wb + o_tf), corr_dump, ctx->stream);
+  CK_LAUNCH("linearize");
+  launch_reduce((const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors,
+                (const double*)(din + o_pose), (const double*)(wb + o_part),
+                out_full ? (gvox_linear_factor*)dout : nullptr,
+                out_full ? nullptr : (gvox_factor_accum*)dout, ctx->stream);
+  CK_LAUNCH("linearize reduce");
+  if (mem == GVOX_HOST) {
+    void* host_out = out_full ? (void*)out_full : (void*)out_accum;
+    CK(cudaMemcpyAsync(host_out, dout, out_rec * num_factors, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return GVOX_OK;
+}
+
+}  // namespace
+
+gvox_status gvox_linearize_batch(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                 int64_t num_clouds, const gvox_map* const* maps, int64_t num_maps,
+                                 const gvox_factor* factors, int64_t num_factors,
+                                 const double* poses, int64_t num_poses, gvox_linear_factor* out,
+                                 int mem, int64_t* corr_dump) {
+  if (!out && num_factors > 0) return fail(GVOX_ERR_INVALID, "gvox_linearize_batch: out is NULL");
+  return linearize_impl(ctx, clouds, num_clouds, maps, num_maps, factors, num_factors, poses,
+                        num_poses, out, nullptr, mem, corr_dump);
+}
+
+gvox_status gvox_linearize_batch_accum(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                       int64_t num_clouds, const gvox_map* const* maps,
+                                       int64_t num_maps, const gvox_factor* factors,
+                                       int64_t num_factors, const double* poses, int64_t num_poses,
+                                       gvox_factor_accum* out, int mem) {
+  if (!out && num_factors > 0) return fail(GVOX_ERR_INVALID, "gvox_linearize_batch_accum: out is NULL");
+  return linearize_impl(ctx, clouds, num_clouds, maps, num_maps, factors, num_factors, poses,
+                        num_poses, nullptr, out, mem, nullptr);
+}
+
+gvox_status gvox_expand(gvox_ctx* ctx, const gvox_factor* factors, int64_t num_factors,
+                        const double* poses, int64_t num_poses, const gvox_factor_accum* accum,
+                        gvox_linear_factor* out, int mem) {
+  if (!ctx) return fail(GVOX_ERR_INVALID, "gvox_expand: ctx is NULL");
+  if (num_factors < 0) return fail(GVOX_ERR_INVALID, "gvox_expand: num_factors < 0");
+  if (num_factors == 0) return GVOX_OK;
+  if (!factors || !poses || !accum || !out) return fail(GVOX_ERR_INVALID, "gvox_expand: NULL argument");
+  gvox_status st = validate_factors("gvox_expand", nullptr, 0, nullptr, 0, factors, num_factors,
+                                    poses, num_poses);
+  if (st) return st;
+  DeviceGuard g(ctx->device);
+  std::vector<FactorDev> fdev(num_factors);
+  for (int64_t f = 0; f < num_factors; ++f) {
+    fdev[f] = FactorDev{factors[f].source_cloud, factors[f].target_map, factors[f].pose_i,
+                        factors[f].pose_j, factors[f].flags, 0, 0};
+  }
+  Layout lay;
+  size_t o_pose = lay.add(96 * num_poses);
+  size_t o_fac = lay.add(sizeof(FactorDev) * num_factors);
+  void* pin = nullptr;
+  st = pin_reserve(ctx, lay.size, &pin);
+  if (st) return st;
+  std::memcpy((char*)pin + o_pose, poses, 96 * num_poses);
+  std::memcpy((char*)pin + o_fac, fdev.data(), sizeof(FactorDev) * num_factors);
+  Layout wl;
+  size_t o_in = wl.add(lay.size);
+  size_t o_out = wl.add(mem == GVOX_HOST ? sizeof(gvox_linear_factor) * num_factors : 0);
+  void* ws = nullptr;
+  st = ws_reserve(ctx, 0, wl.size, &ws);
+  if (st) return st;
+  char* wb = (char*)ws;
+  st = h2d_block(ctx, wb + o_in, pin, lay.size);
+  if (st) return st;
+  gvox_linear_factor* dout = mem == GVOX_DEVICE ? out : (gvox_linear_factor*)(wb + o_out);
+  launch_expand((const FactorDev*)(wb + o_in + o_fac), num_factors,
+                (const double*)(wb + o_in + o_pose), accum, dout, ctx->stream);
+  CK_LAUNCH("gvox_expand");
+  if (mem == GVOX_HOST) {
+    CK(cudaMemcpyAsync(out, dout, sizeof(gvox_linear_factor) * num_factors,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return GVOX_OK;
+}
+
+// ------------------------------------------------------------------ utilities
+const char* gvox_status_string(gvox_status s) {
+  switch (s) {
+    case GVOX_OK: return "GVOX_OK";
+    case GVOX_ERR_INVALID: return "GVOX_ERR_INVALID";
+    case GVOX_ERR_RANGE: return "GVOX_ERR_RANGE";
+    case GVOX_ERR_CUDA: return "GVOX_ERR_CUDA";
+    case GVOX_ERR_NOMEM: return "GVOX_ERR_NOMEM";
+  }
+  return "GVOX_ERR_UNKNOWN";
+}
+
+const char* gvox_last_error(void) { return g_last_error.c_str(); }
+
+int64_t gvox_launch_count(int reset) {
+  int64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+const char* gvox_version(void) { return "gvox 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,271 @@
+// k_build.cu -- cloud packing, voxelmap build (K1) and lookup kernels.
+//
+// Voxelmap ("we create a sparse voxelmap with spatial voxel hashing and
+// take the average of the points and their covariances in each voxel";
+// multi-resolution r_l = r0 2^l).  B200 design:
+//  phase 1  one thread per (point, level): fp64 key, open-addressing insert
+//           with a 64-bit atomicCAS into a temporary per-(map, level) table;
+//           the inserting thread takes a compact voxel index (atomicAdd).
+//  -- host reads the voxel counts (one sync per chunk) and sizes the final
+//     arrays exactly --
+//  phase 2  one thread per (point, level): FIXED-POINT integer accumulation
+//           (64-bit atomicAdd) of the mean offset within the voxel, the
+//           covariance and the count.  Integer addition is associative, so
+//           the result is bitwise independent of scheduling.
+//  phase 3  one thread per voxel: mean/cov = sums / count, stored as fp32
+//           offset-from-centre and fp32 covariance; insert into the final
+//           table (capacity 2^k >= 2V).
+#include <cstdint>
+
+#include "k_common.cuh"
+
+namespace gvox {
+
+namespace {
+
+__device__ inline bool finite3(float a, float b, float c) {
+  return isfinite(a) && isfinite(b) && isfinite(c);
+}
+
+__global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restrict__ cov,
+                             const float* __restrict__ nrm, int64_t n, float4* __restrict__ A,
+                             float4* __restrict__ B, float4* __restrict__ N,
+                             int32_t* __restrict__ flags, uint32_t* __restrict__ cmax_bits) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float cm = 0.f;
+  bool bad = false;
+  if (i < n) {
+    float x = mu[3 * i], y = mu[3 * i + 1], z = mu[3 * i + 2];
+    float c0 = cov[6 * i], c1 = cov[6 * i + 1], c2 = cov[6 * i + 2];
+    float c3 = cov[6 * i + 3], c4 = cov[6 * i + 4], c5 = cov[6 * i + 5];
+    float nx = 0.f, ny = 0.f, nz = 0.f;
+    if (nrm) {
+      nx = nrm[3 * i];
+      ny = nrm[3 * i + 1];
+      nz = nrm[3 * i + 2];
+    }
+    bad = !(finite3(x, y, z) && finite3(c0, c1, c2) && finite3(c3, c4, c5) && finite3(nx, ny, nz));
+    A[i] = make_float4(x, y, z, c0);
+    B[i] = make_float4(c1, c2, c3, c4);
+    N[i] = make_float4(c5, nx, ny, nz);
+    cm = fmaxf(fmaxf(fmaxf(fabsf(c0), fabsf(c1)), fmaxf(fabsf(c2), fabsf(c3))),
+               fmaxf(fabsf(c4), fabsf(c5)));
+    if (bad) cm = 0.f;
+  }
+  // warp max then one atomic per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+  unsigned anybad = __ballot_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    if (cm > 0.f) atomicMax(cmax_bits, __float_as_uint(cm));
+    if (anybad) atomicOr(flags, 1);
+  }
+}
+
+// segment (cloud) of a global point index: largest s with start[s] <= i
+__device__ inline int64_t seg_of(const int64_t* start, int64_t nseg, int64_t i) {
+  int64_t lo = 0, hi = nseg;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (__ldg(start + mid) <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_build_insert(const BuildSeg* __restrict__ segs, int64_t nseg,
+                               const int64_t* __restrict__ seg_start, int64_t total, int levels,
+                               double r0, double inv_r0, int dyadic, int32_t* __restrict__ pslot,
+                               int32_t* __restrict__ err) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  int64_t s = seg_of(seg_start, nseg, i);
+  const BuildSeg& sg = segs[s];
+  int64_t k = i - seg_start[s];
+  float4 a = __ldg(sg.A + k);
+  int32_t k0x = voxel_coord0((double)a.x, r0, inv_r0, dyadic);
+  int32_t k0y = voxel_coord0((double)a.y, r0, inv_r0, dyadic);
+  int32_t k0z = voxel_coord0((double)a.z, r0, inv_r0, dyadic);
+  for (int l = 0; l < levels; ++l) {
+    // floor(x / r_l) = floor(x / r0) >> l exactly (r_l = r0 2^l)
+    int32_t kx = k0x >> l, ky = k0y >> l, kz = k0z >> l;
+    int64_t rec = sg.pl_offset + k * levels + l;
+    if (!key_in_range(kx) || !key_in_range(ky) || !key_in_range(kz)) {
+      atomicOr(err, 1);
+      pslot[rec] = -1;
+      continue;
+    }
+    uint64_t key = pack_key(kx, ky, kz);
+    ulonglong2* slots = sg.tmp_slots[l];
+    uint64_t h = hash_slot(key, sg.tmp_mask);
+    for (;;) {
+      unsigned long long* kp = reinterpret_cast<unsigned long long*>(&slots[h].x);
+      unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(kp);
+      if (cur == key) break;
+      if (cur == kEmptyKey) {
+        unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
+        if (prev == kEmptyKey) {
+          int32_t idx = atomicAdd(sg.counter + l, 1);
+          slots[h].y = (unsigned long long)(uint32_t)idx | 0xFFFFFFFF00000000ull;
+          sg.keys_by_idx[l][idx] = key;
+          break;
+        }
+        if (prev == key) break;
+      }
+      h = (h + 1) & sg.tmp_mask;
+    }
+    pslot[rec] = (int32_t)h;
+  }
+}
+
+__device__ inline unsigned long long to_fixed(double x) {
+  return (unsigned long long)__double2ll_rn(x);
+}
+
+__global__ void k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg* __restrict__ segs,
+                              int64_t nseg, const int64_t* __restrict__ seg_start, int64_t total,
+                              int levels, double r0, double inv_r0, int dyadic,
+                              const int32_t* __restrict__ pslot,
+                              unsigned long long* __restrict__ acc) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  int64_t s = seg_of(seg_start, nseg, i);
+  const AccumSeg& sg = segs[s];
+  const BuildSeg& bs = bsegs[s];
+  int64_t k = i - seg_start[s];
+  float4 a = __ldg(sg.A + k), b = __ldg(sg.B + k), c = __ldg(sg.N + k);
+  double x = a.x, y = a.y, z = a.z;
+  int32_t k0x = voxel_coord0(x, r0, inv_r0, dyadic);
+  int32_t k0y = voxel_coord0(y, r0, inv_r0, dyadic);
+  int32_t k0z = voxel_coord0(z, r0, inv_r0, dyadic);
+  const float cv[6] = {a.w, b.x, b.y, b.z, b.w, c.x};
+  for (int l = 0; l < levels; ++l) {
+    int32_t sl = pslot[sg.pl_offset + k * levels + l];
+    if (sl < 0) continue;
+    int32_t idx = (int32_t)(uint32_t)bs.tmp_slots[l][sl].y;
+    double r = ldexp(r0, l);
+    // offset of the point within its voxel (voxel corner = k_l * r_l)
+    double ox = x - (double)(k0x >> l) * r, oy = y - (double)(k0y >> l) * r,
+           oz = z - (double)(k0z >> l) * r;
+    unsigned long long* dst = acc + (sg.acc_offset[l] + idx) * 10;
+    double S = sg.mu_scale[l];
+    atomicAdd(dst + 0, to_fixed(ox * S));
+    atomicAdd(dst + 1, to_fixed(oy * S));
+    atomicAdd(dst + 2, to_fixed(oz * S));
+#pragma unroll
+    for (int j = 0; j < 6; ++j) atomicAdd(dst + 3 + j, to_fixed((double)cv[j] * sg.cov_scale));
+    atomicAdd(dst + 9, 1ull);
+  }
+}
+
+__global__ void k_build_finalize(const FinalSeg* __restrict__ segs, int64_t nseg,
+                                 const int64_t* __restrict__ seg_vox_start, int64_t total,
+                                 const unsigned long long* __restrict__ acc) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  int64_t s = seg_of(seg_vox_start, nseg, i);
+  const FinalSeg& sg = segs[s];
+  int64_t v = i - seg_vox_start[s];
+  const unsigned long long* src = acc + (sg.acc_offset + v) * 10;
+  double cnt = (double)(long long)src[9];
+  double inv = 1.0 / cnt;
+  double m[3], cv[6];
+  for (int j = 0; j < 3; ++j) m[j] = (double)(long long)src[j] * inv / sg.mu_scale - 0.5 * sg.r;
+  for (int j = 0; j < 6; ++j) cv[j] = (double)(long long)src[3 + j] * inv / sg.cov_scale;
+  float4* o = sg.vox + 3 * v;
+  o[0] = make_float4((float)m[0], (float)m[1], (float)m[2], (float)cv[0]);
+  o[1] = make_float4((float)cv[1], (float)cv[2], (float)cv[3], (float)cv[4]);
+  o[2] = make_float4((float)cv[5], __int_as_float((int)src[9]), 0.f, 0.f);
+  uint64_t key = sg.keys_by_idx[v];
+  sg.keys_out[v] = key;
+  uint64_t h = hash_slot(key, sg.mask);
+  for (;;) {
+    unsigned long long* kp = reinterpret_cast<unsigned long long*>(&sg.slots[h].x);
+    unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
+    if (prev == kEmptyKey) {
+      sg.slots[h].y = (unsigned long long)(uint32_t)v | 0xFFFFFFFF00000000ull;
+      break;
+    }
+    h = (h + 1) & sg.mask;
+  }
+}
+
+__global__ void k_fill_u64(uint64_t* p, uint64_t value, int64_t count) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < count; i += stride) p[i] = value;
+}
+
+__global__ void k_lookup(const MapDev* __restrict__ map, int level, const double* __restrict__ q,
+                         int64_t n, int64_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const MapLevelDev& lv = map->lv[level];
+  int dy = map->dyadic;
+  int32_t kx = voxel_coord0(q[3 * i], lv.r, lv.inv_r, dy);
+  int32_t ky = voxel_coord0(q[3 * i + 1], lv.r, lv.inv_r, dy);
+  int32_t kz = voxel_coord0(q[3 * i + 2], lv.r, lv.inv_r, dy);
+  int64_t res = -1;
+  if (key_in_range(kx) && key_in_range(ky) && key_in_range(kz)) {
+    uint64_t key = pack_key(kx, ky, kz);
+    if (probe(lv, key) >= 0) res = (int64_t)key;
+  }
+  out[i] = res;
+}
+
+inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
+
+}  // namespace
+
+void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* A,
+                       float4* B, float4* N, int32_t* flags, uint32_t* cmax_bits,
+                       cudaStream_t stream) {
+  if (n <= 0) return;
+  k_cloud_pack<<<grid_for(n, 256), 256, 0, stream>>>(mu, cov, nrm, n, A, B, N, flags, cmax_bits);
+  note_launch();
+}
+
+void launch_build_insert(const BuildSeg* segs_dev, int64_t num_segs, const int64_t* seg_point_start,
+                         int64_t total_points, int levels, double r0, int dyadic, int32_t* pslot,
+                         int32_t* err, cudaStream_t stream) {
+  if (total_points <= 0) return;
+  k_build_insert<<<grid_for(total_points, 256), 256, 0, stream>>>(
+      segs_dev, num_segs, seg_point_start, total_points, levels, r0, 1.0 / r0, dyadic, pslot, err);
+  note_launch();
+}
+
+void launch_build_accum(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int64_t num_segs,
+                        const int64_t* seg_point_start, int64_t total_points, int levels,
+                        double r0, int dyadic, const int32_t* pslot, unsigned long long* acc,
+                        cudaStream_t stream) {
+  if (total_points <= 0) return;
+  k_build_accum<<<grid_for(total_points, 256), 256, 0, stream>>>(
+      bsegs_dev, segs_dev, num_segs, seg_point_start, total_points, levels, r0, 1.0 / r0, dyadic,
+      pslot, acc);
+  note_launch();
+}
+
+void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs,
+                           const int64_t* seg_vox_start, int64_t total_voxels,
+                           const unsigned long long* acc, cudaStream_t stream) {
+  if (total_voxels <= 0) return;
+  k_build_finalize<<<grid_for(total_voxels, 256), 256, 0, stream>>>(segs_dev, num_segs,
+                                                                     seg_vox_start, total_voxels, acc);
+  note_launch();
+}
+
+void launch_fill_u64(uint64_t* p, uint64_t value, int64_t count, cudaStream_t stream) {
+  if (count <= 0) return;
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_fill_u64<<<(unsigned)blocks, 256, 0, stream>>>(p, value, count);
+  note_launch();
+}
+
+void launch_lookup(const MapDev* map, int level, const double* q, int64_t n, int64_t* out,
+                   cudaStream_t stream) {
+  if (n <= 0) return;
+  k_lookup<<<grid_for(n, 256), 256, 0, stream>>>(map, level, q, n, out);
+  note_launch();
+}
+
+}  // namespace gvox

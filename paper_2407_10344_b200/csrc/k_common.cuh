@@ -1,0 +1,75 @@
+// k_common.cuh -- device helpers shared by the gvox kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "gvox_internal.h"
+
+namespace gvox {
+
+// T_ij = T_j^-1 T_i and v = T_i^-1 t_j (reading Q1), with the pinned fma order
+// of reading Q10: R_ij[a][b] = fma(Rj[0][a], Ri[0][b], fma(Rj[1][a], Ri[1][b],
+// Rj[2][a] * Ri[2][b])); t_ij = R_j^T (t_i - t_j); v = R_i^T (t_j - t_i).
+// Poses are row-major 3x4.
+__device__ inline void relative_pose_dev(const double* Ti, const double* Tj, double* R, double* t,
+                                         double* v) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      R[a * 3 + b] = __fma_rn(Tj[0 * 4 + a], Ti[0 * 4 + b],
+                              __fma_rn(Tj[1 * 4 + a], Ti[1 * 4 + b],
+                                       __dmul_rn(Tj[2 * 4 + a], Ti[2 * 4 + b])));
+  double dt0 = __dsub_rn(Ti[3], Tj[3]), dt1 = __dsub_rn(Ti[7], Tj[7]), dt2 = __dsub_rn(Ti[11], Tj[11]);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    t[a] = __fma_rn(Tj[0 * 4 + a], dt0, __fma_rn(Tj[1 * 4 + a], dt1, __dmul_rn(Tj[2 * 4 + a], dt2)));
+  double dv0 = __dsub_rn(Tj[3], Ti[3]), dv1 = __dsub_rn(Tj[7], Ti[7]), dv2 = __dsub_rn(Tj[11], Ti[11]);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    v[a] = __fma_rn(Ti[0 * 4 + a], dv0, __fma_rn(Ti[1 * 4 + a], dv1, __dmul_rn(Ti[2 * 4 + a], dv2)));
+}
+
+// floor(x / r) as int32, saturating (|result| >= 2^30 is out of key range at
+// every level l <= 7).  For a power-of-two r the product by 1/r is exact and
+// equals the correctly rounded quotient; otherwise an IEEE division is used.
+__device__ inline int32_t voxel_coord0(double x, double r, double inv_r, int dyadic) {
+  double s = dyadic ? __dmul_rn(x, inv_r) : __ddiv_rn(x, r);
+  return __double2int_rd(s);
+}
+
+// Probe a level's hash table: voxel index or -1.
+__device__ inline int32_t probe(const MapLevelDev& lv, uint64_t key) {
+  uint64_t h = hash_slot(key, lv.mask);
+  for (;;) {
+    ulonglong2 s = __ldg(lv.slots + h);
+    if (s.x == key) return (int32_t)(uint32_t)s.y;
+    if (s.x == kEmptyKey) return -1;
+    h = (h + 1) & lv.mask;
+  }
+}
+
+__device__ inline double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ inline int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// upper_bound(tile_start[0..num_factors], tile) - 1: the factor owning `tile`
+// (factors with zero tiles are skipped).
+__device__ inline int64_t owner_of_tile(const int32_t* tile_start, int64_t num_factors,
+                                        int64_t tile) {
+  int64_t lo = 0, hi = num_factors;  // tile_start[lo] <= tile < tile_start[hi]
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (__ldg(tile_start + mid) <= tile) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace gvox

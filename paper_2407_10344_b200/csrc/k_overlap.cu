@@ -1,0 +1,110 @@
+// k_overlap.cu -- voxel overlap counts (K2).
+//
+// "we define an overlap rate between two point clouds P_i and P_j as the
+// fraction of points in P_i that fall within a voxel of P_j"; global
+// factors for submap pairs whose overlap "exceeds a small threshold (e.g. 5%)".
+//
+// B200 design: one CTA per tile of consecutive source points
+// of one pair; each thread streams only the 16 B {mu, C.xx} plane of the cloud,
+// transforms in fp64 with the pinned fma order (bit-exact keys, Q10), probes
+// one 16 B hash slot; hits are counted with __ballot_sync/__popc per warp and
+// one integer atomicAdd per CTA (integer: exact and order-independent).
+#include <cstdint>
+
+#include "k_common.cuh"
+
+namespace gvox {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__global__ void k_tile_map_pairs(const int32_t* __restrict__ tile_start, int64_t n,
+                                 int32_t* __restrict__ tile_pair) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  for (int32_t t = tile_start[p]; t < tile_start[p + 1]; ++t) tile_pair[t] = (int32_t)p;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_overlap(const CloudDev* const* __restrict__ clouds, const MapDev* const* __restrict__ maps,
+              const PairDev* __restrict__ pairs, const int32_t* __restrict__ tile_start,
+              const int32_t* __restrict__ tile_pair, int tile_pts, const double* __restrict__ poses,
+              int level, int32_t* __restrict__ counts) {
+  __shared__ double pose_s[24];
+  __shared__ double R[9], t[3];
+  __shared__ const float4* A_s;
+  __shared__ int64_t range_s[2];
+  __shared__ MapLevelDev lv_s;
+  __shared__ int dyadic_s;
+  __shared__ int warp_cnt[kThreads / 32];
+  const int tid = threadIdx.x;
+  const int64_t tile = blockIdx.x;
+  const int32_t p = __ldg(tile_pair + tile);
+  const PairDev pd = pairs[p];
+  if (tid < 24) {
+    pose_s[tid] = __ldg(poses + 12 * (int64_t)(tid < 12 ? pd.pi : pd.pj) + (tid % 12));
+  } else if (tid == 32) {
+    const CloudDev* cd = clouds[pd.src];
+    int64_t b = (int64_t)(tile - __ldg(tile_start + p)) * tile_pts;
+    int64_t e = b + tile_pts;
+    A_s = cd->A;
+    range_s[0] = b;
+    range_s[1] = e < cd->n ? e : cd->n;
+  } else if (tid == 64) {
+    const MapDev* md = maps[pd.tgt];
+    lv_s = md->lv[level];
+    dyadic_s = md->dyadic;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double v[3];
+    relative_pose_dev(pose_s, pose_s + 12, R, t, v);
+  }
+  __syncthreads();
+  const MapLevelDev lv = lv_s;
+  const int dyadic = dyadic_s;
+  const float4* __restrict__ A = A_s;
+  int cnt = 0;
+  for (int64_t k = range_s[0] + tid; k < range_s[1]; k += kThreads) {
+    const float4 a = __ldg(A + k);
+    const double mx = a.x, my = a.y, mz = a.z;
+    const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
+    const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
+    const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
+    const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
+    const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
+    const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
+    bool hit = false;
+    if (key_in_range(kx) && key_in_range(ky) && key_in_range(kz))
+      hit = probe(lv, pack_key(kx, ky, kz)) >= 0;
+    cnt += hit;
+  }
+  // warp counts, then one atomic per CTA
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((tid & 31) == 0) warp_cnt[tid >> 5] = cnt;
+  __syncthreads();
+  if (tid == 0) {
+    int s = 0;
+    for (int w = 0; w < kThreads / 32; ++w) s += warp_cnt[w];
+    if (s) atomicAdd(counts + p, s);
+  }
+}
+
+}  // namespace
+
+void launch_overlap(const CloudDev* const* clouds, const MapDev* const* maps, const PairDev* pairs,
+                    const int32_t* tile_start, int64_t num_pairs, int64_t num_tiles, int tile_pts,
+                    const double* poses, int level, int32_t* tile_pair, int32_t* counts,
+                    cudaStream_t stream) {
+  if (num_tiles <= 0) return;
+  k_tile_map_pairs<<<(unsigned)((num_pairs + 255) / 256), 256, 0, stream>>>(tile_start, num_pairs,
+                                                                             tile_pair);
+  note_launch();
+  k_overlap<<<(unsigned)num_tiles, kThreads, 0, stream>>>(clouds, maps, pairs, tile_start,
+                                                          tile_pair, tile_pts, poses, level, counts);
+  note_launch();
+}
+
+}  // namespace gvox

@@ -1,0 +1,385 @@
+"""CUDA path (libgvox.so through the C ABI) vs the fp64 oracle, element by element.
+
+Bars (BASELINE.json north_star): voxel keys, voxel counts, correspondences
+(packed keys) and overlap counts bit-exact; H and b within 1e-4 relative
+Frobenius error, e within 1e-5 (tests/parity.py).  Sizes span several tiles and
+a ragged tail; edge cases: empty clouds, zero-hit factors, degenerate
+covariances, validation, non-dyadic resolutions, out-of-range keys.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from tests.parity import compare_factor
+from tests.se3 import plane_cov, random_pose, rel_pose, right_perturb, to12, to44
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+
+
+@pytest.fixture(scope="module")
+def ctx(gv):
+    return gv.Context(0)
+
+
+def rand_scene(rs, n, extent=20.0):
+    """Plane-like Gaussian points on a few surfaces (like tests/test_oracle_linearize)."""
+    normals = rs.normal(0, 1, (6, 3))
+    normals /= np.linalg.norm(normals, axis=1, keepdims=True)
+    pts, covs, nrms = [], [], []
+    which = rs.integers(0, 6, n)
+    for k in range(n):
+        nv = normals[which[k]]
+        t1 = np.cross(nv, [0.3, 0.5, 0.7]); t1 /= np.linalg.norm(t1)
+        t2 = np.cross(nv, t1)
+        p = nv * which[k] * 1.3 + t1 * rs.uniform(-extent, extent) + t2 * rs.uniform(-extent, extent)
+        pts.append(p)
+        covs.append(plane_cov(nv + rs.normal(0, 0.05, 3)))
+        nrms.append(nv)
+    return np.array(pts, np.float32), np.array(covs, np.float32), np.array(nrms, np.float32)
+
+
+def transform_cloud(mu, cov, nrm, T12):
+    """Express world-frame points in the frame of pose T (world <- frame)."""
+    T = to44(T12)
+    R, t = T[:3, :3], T[:3, 3]
+    m = (mu.astype(float) - t) @ R
+    C = np.zeros((len(cov), 3, 3))
+    idx = [(0, 0, 0), (0, 1, 1), (0, 2, 2), (1, 1, 3), (1, 2, 4), (2, 2, 5)]
+    for a, b, c in idx:
+        C[:, a, b] = cov[:, c]
+        C[:, b, a] = cov[:, c]
+    C = np.einsum("ji,njk,kl->nil", R, C, R)
+    c6 = np.stack([C[:, a, b] for a, b, _ in idx], 1)
+    return m.astype(np.float32), c6.astype(np.float32), (nrm.astype(float) @ R).astype(np.float32)
+
+
+# ---------------------------------------------------------------------- voxelmap
+@pytest.mark.parametrize("r0,L,n,seed", [(0.25, 3, 20000, 0), (0.5, 3, 5000, 1), (0.3, 2, 7000, 2),
+                                         (1.0, 1, 1000, 3), (0.125, 4, 3001, 4)])
+def test_voxelmap_parity(gv, ctx, oracle, r0, L, n, seed):
+    rs = np.random.default_rng(seed)
+    mu, cov, nrm = rand_scene(rs, n)
+    cl = gv.Cloud(ctx, mu, cov, nrm)
+    m = gv.create_voxelmap(ctx, cl, r0, L)
+    om = oracle.VoxelMap(mu, cov, r0, L)
+    for l in range(L):
+        keys, means, covs, counts = m.export(ctx, l)
+        okeys, omeans, ocovs, ocounts = om.export(l)
+        assert np.array_equal(keys, okeys), f"level {l}: keys differ"
+        assert np.array_equal(counts.astype(np.int64), ocounts)
+        r = r0 * 2 ** l
+        np.testing.assert_allclose(means, omeans, rtol=0, atol=2e-7 * r + 1e-6 * 0)
+        cmax = np.abs(cov).max()
+        np.testing.assert_allclose(covs, ocovs, rtol=0, atol=2e-7 * cmax)
+
+
+def test_voxelmap_batched_equals_single(gv, ctx):
+    rs = np.random.default_rng(5)
+    clouds = [gv.Cloud(ctx, *rand_scene(rs, n)) for n in (3000, 1, 0, 4500)]
+    ms = gv.create_voxelmaps(ctx, clouds, 0.5, 3)
+    for c, m in zip(clouds, ms):
+        s = gv.create_voxelmap(ctx, c, 0.5, 3)
+        for l in range(3):
+            a, b = m.export(ctx, l), s.export(ctx, l)
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y)
+
+
+def test_voxelmap_golden_and_errors(gv, ctx, oracle):
+    g = GOLDEN["two_points_voxel"]
+    cl = gv.Cloud(ctx, np.array(g["mu"], np.float32), np.array(g["cov"], np.float32))
+    m = gv.create_voxelmap(ctx, cl, g["r0"], 1)
+    keys, means, covs, counts = m.export(ctx, 0)
+    assert keys.tolist() == [oracle.pack_key(*g["voxel_key_xyz"])]
+    np.testing.assert_allclose(means[0], g["mean"], atol=1e-7)
+    np.testing.assert_allclose(covs[0], g["cov_mean"], atol=1e-6)
+    assert counts.tolist() == [g["count"]]
+    far = gv.Cloud(ctx, np.array([[3e6, 0, 0]], np.float32), np.ones((1, 6), np.float32))
+    with pytest.raises(gv.GvoxError, match="GVOX_ERR_RANGE"):
+        gv.create_voxelmap(ctx, far, 1.0, 1)
+    with pytest.raises(gv.GvoxError, match="GVOX_ERR_INVALID"):
+        gv.create_voxelmap(ctx, cl, 0.0, 1)
+    with pytest.raises(gv.GvoxError, match="GVOX_ERR_INVALID"):
+        gv.create_voxelmap(ctx, cl, 1.0, 9)
+    with pytest.raises(gv.GvoxError, match="non-finite"):
+        gv.Cloud(ctx, np.array([[np.nan, 0, 0]], np.float32), np.ones((1, 6), np.float32))
+
+
+def test_lookup_parity(gv, ctx, oracle):
+    rs = np.random.default_rng(6)
+    mu, cov, nrm = rand_scene(rs, 4000, 10.0)
+    for r0 in (0.5, 0.3):
+        m = gv.create_voxelmap(ctx, gv.Cloud(ctx, mu, cov), r0, 3)
+        om = oracle.VoxelMap(mu, cov, r0, 3)
+        q = np.concatenate([mu[:500].astype(float) + rs.normal(0, 0.3, (500, 3)),
+                            rs.uniform(-15, 15, (500, 3)),
+                            np.round(mu[:200].astype(float) / r0) * r0])  # exact boundaries
+        for l in range(3):
+            got = m.lookup(ctx, l, q)
+            want = np.array([om.lookup(l, p) for p in q])
+            assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------------- overlap
+def test_overlap_parity_random_poses(gv, ctx, oracle):
+    rs = np.random.default_rng(7)
+    mu, cov, nrm = rand_scene(rs, 6000, 15.0)
+    srcs = [rand_scene(rs, n, 15.0)[0] for n in (5000, 2049, 1, 0, 4096)]
+    clouds = [gv.Cloud(ctx, s, np.tile(cov[:1], (len(s), 1))) for s in srcs]
+    maps = gv.create_voxelmaps(ctx, [gv.Cloud(ctx, mu, cov)], 0.5, 3)
+    om = oracle.VoxelMap(mu, cov, 0.5, 3)
+    poses = [to12(np.eye(4))] + [random_pose(rs, 0.05, 1.0) for _ in range(8)]
+    pairs = [[s, 0, 1 + (s + k) % 8, 0] for s in range(len(srcs)) for k in range(3)]
+    for level in range(3):
+        got = gv.overlap(ctx, clouds, maps, pairs, poses, level)
+        for p, g in zip(pairs, got):
+            want = oracle.overlap(srcs[p[0]], om, poses[p[2]], poses[p[3]], level)
+            assert int(g) == want
+
+
+def test_overlap_c2(gv, ctx, oracle):
+    sc = synth.make("C2")
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    for level in range(sc.levels):
+        got = gv.overlap(ctx, clouds, maps, sc.pairs, sc.poses, level)
+        for p, g in zip(sc.pairs, got):
+            om = oracle.VoxelMap(*sc.cloud(int(sc.map_clouds[p[1]]))[:2], sc.r0, sc.levels)
+            want = oracle.overlap(sc.cloud(int(p[0]))[0], om, sc.poses[p[2]], sc.poses[p[3]], level)
+            assert int(g) == want
+        # cross-kernel identity: overlap count at level l = linearize inliers[l] (no validation)
+    f = sc.factors.copy()
+    f[:, 4] = 0
+    out = gv.linearize_batch(ctx, clouds, maps, f, sc.poses)
+    for level in range(sc.levels):
+        got = gv.overlap(ctx, clouds, maps, sc.pairs, sc.poses, level)
+        assert np.array_equal(got, out["inliers"][:, level])
+
+
+# ---------------------------------------------------------------------- linearize
+def _scene_parity(gv, ctx, oracle, sc, check_corr=True):
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    import torch
+    corr = None
+    if check_corr:
+        corr = torch.empty(gv.corr_dump_size(clouds, maps, sc.factors), dtype=torch.int64,
+                           device=ctx.device)
+    out = gv.linearize_batch(ctx, clouds, maps, sc.factors, sc.poses, corr_dump=corr)
+    corr_h = corr.cpu().numpy() if check_corr else None
+    omaps = {}
+    off = 0
+    worst = {}
+    for k, f in enumerate(sc.factors):
+        t = int(f[1])
+        if t not in omaps:
+            omaps[t] = oracle.VoxelMap(*sc.cloud(int(sc.map_clouds[t]))[:2], sc.r0, sc.levels)
+        mu, cov, nrm = sc.cloud(int(f[0]))
+        ref = oracle.linearize(mu, cov, nrm, omaps[t], sc.poses[f[2]], sc.poses[f[3]],
+                               validate=bool(f[4] & 1), return_corr=check_corr)
+        errs = compare_factor(out[k], ref, sc.levels, what=f"{sc.name} factor {k}")
+        for a, b in errs.items():
+            worst[a] = max(worst.get(a, 0.0), b)
+        if check_corr:
+            n = len(mu) * sc.levels
+            assert np.array_equal(corr_h[off:off + n], ref["corr"].reshape(-1)), f"factor {k} corr"
+            off += n
+    return out, worst
+
+
+def test_linearize_c1(gv, ctx, oracle):
+    _scene_parity(gv, ctx, oracle, synth.make("C1"))
+
+
+def test_linearize_c2_validation(gv, ctx, oracle):
+    out, worst = _scene_parity(gv, ctx, oracle, synth.make("C2"))
+    assert out["inliers"][:, :3].min() > 0
+    print("C2 worst relative errors:", worst)
+
+
+def test_linearize_c3_subset(gv, ctx, oracle):
+    sc = synth.make("C3")
+    sc.factors = sc.factors[::7].copy()  # 43 of 300 factors, all 50 clouds uploaded
+    _scene_parity(gv, ctx, oracle, sc)
+
+
+def test_linearize_random_factors_nondyadic(gv, ctx, oracle):
+    rs = np.random.default_rng(11)
+    mu_w, cov_w, n_w = rand_scene(rs, 9000, 12.0)
+    Ts = [random_pose(rs, 0.4, 4.0) for _ in range(5)]
+    clouds = [transform_cloud(mu_w[k * 1500:(k + 1) * 1500 + 777], cov_w[k * 1500:(k + 1) * 1500 + 777],
+                              n_w[k * 1500:(k + 1) * 1500 + 777], Ts[k]) for k in range(5)]
+    poses = np.stack([right_perturb(T, rs.normal(0, 0.01, 6)) for T in Ts])
+    for r0, L in ((0.3, 3), (0.7, 1), (0.25, 5)):
+        sc = synth.Scene("rand", np.concatenate([c[0] for c in clouds]),
+                         np.concatenate([c[1] for c in clouds]), np.concatenate([c[2] for c in clouds]),
+                         np.concatenate([[0], np.cumsum([len(c[0]) for c in clouds])]).astype(np.int64),
+                         np.arange(5, dtype=np.int64), r0, L,
+                         np.array([[i, j, i, j, (i + j) % 2] for i in range(5) for j in range(5) if i != j],
+                                  np.int64), poses, poses, np.zeros((0, 4), np.int64), 0)
+        _scene_parity(gv, ctx, oracle, sc)
+
+
+def test_linearize_zero_at_ground_truth_lattice(gv, ctx):
+    # dyadic lattice, 90-degree rotations: every fp op exact on both paths -> e = b = 0 exactly
+    g = np.stack(np.meshgrid(np.arange(-2, 3), np.arange(-2, 3), np.arange(0, 2), indexing="ij"), -1).reshape(-1, 3)
+    src = (g * 8.0 + np.array([1.5, 2.25, 3.125])).astype(np.float32)
+    Rz = np.array([[0, -1, 0], [1, 0, 0], [0, 0, 1.0]])
+    Rx = np.array([[1, 0, 0], [0, 0, -1], [0, 1, 0.0]])
+    Ti = np.eye(4); Ti[:3, :3] = Rz; Ti[:3, 3] = [16.0, -8.0, 0.0]
+    Tj = np.eye(4); Tj[:3, :3] = Rx; Tj[:3, 3] = [-24.0, 8.0, 32.0]
+    Tij = np.linalg.inv(Tj) @ Ti
+    tgt = (src.astype(float) @ Tij[:3, :3].T + Tij[:3, 3]).astype(np.float32)
+    cov = np.tile(np.array(plane_cov([0.3, 0.4, 0.866]), np.float32), (len(src), 1))
+    cs, ct = gv.Cloud(ctx, src, cov), gv.Cloud(ctx, tgt, cov)
+    m = gv.create_voxelmap(ctx, ct, 1.0, 3)
+    out = gv.linearize_batch(ctx, [cs], [m], [[0, 0, 0, 1, 0]], np.stack([to12(Ti), to12(Tj)]))
+    assert out["inliers"][0][:3].tolist() == [len(src)] * 3
+    assert out["error"][0] == 0.0
+    assert np.all(out["b_i"][0] == 0.0) and np.all(out["b_j"][0] == 0.0)
+
+
+@pytest.mark.parametrize("name", ["d2d_unit", "d2d_rotated"])
+def test_linearize_golden(gv, ctx, name):
+    g = GOLDEN[name]
+    ct = gv.Cloud(ctx, np.array(g["target_mu"], np.float32), np.array(g["target_cov"], np.float32))
+    cs = gv.Cloud(ctx, np.array(g["source_mu"], np.float32), np.array(g["source_cov"], np.float32))
+    m = gv.create_voxelmap(ctx, ct, g["r0"], g["levels"])
+    out = gv.linearize_batch(ctx, [cs], [m], [[0, 0, 0, 1, 0]], np.stack([g["T_i"], g["T_j"]]))
+    assert out["error"][0] == pytest.approx(g["e"], rel=1e-6)
+
+
+def test_visibility_golden(gv, ctx):
+    g = GOLDEN["visibility_wall"]
+    mu = np.array([g["point"]], np.float32)
+    unit = np.array([[1, 0, 0, 1, 0, 1]], np.float32)
+    cs = gv.Cloud(ctx, mu, unit, np.array([g["normal"]], np.float32))
+    for x, inv in zip(g["viewer_x"], g["invisible"]):
+        m = gv.create_voxelmap(ctx, gv.Cloud(ctx, mu - np.array([[x, 0, 0]], np.float32), unit), 1.0, 1)
+        poses = np.stack([np.eye(4)[:3].reshape(-1), np.array([1, 0, 0, x, 0, 1, 0, 0, 0, 0, 1, 0.0])])
+        out = gv.linearize_batch(ctx, [cs], [m], [[0, 0, 0, 1, gv.F_VALIDATE_SURFACE]], poses)
+        assert int(out["num_invisible"][0]) == inv
+        assert int(out["inliers"][0][0]) == 1 - inv
+
+
+def test_edge_cases(gv, ctx, oracle):
+    rs = np.random.default_rng(12)
+    mu, cov, nrm = rand_scene(rs, 3000, 8.0)
+    full = gv.Cloud(ctx, mu, cov, nrm)
+    empty = gv.Cloud(ctx, np.zeros((0, 3), np.float32), np.zeros((0, 6), np.float32))
+    m = gv.create_voxelmap(ctx, full, 0.5, 3)
+    m_empty = gv.create_voxelmap(ctx, empty, 0.5, 3)
+    I = to12(np.eye(4))
+    far = to44(I); far[0, 3] = 1e4
+    poses = np.stack([I, to12(far)])
+    f = [[1, 0, 0, 0, 0],   # empty source
+         [0, 1, 0, 0, 0],   # empty target map
+         [0, 0, 1, 0, 0],   # no overlap (far away)
+         [0, 0, 0, 0, 0]]   # self
+    out = gv.linearize_batch(ctx, [full, empty], [m, m_empty], f, poses)
+    for k in range(3):
+        assert out["error"][k] == 0 and np.all(out["H_jj"][k] == 0) and out["inliers"][k].sum() == 0
+    ref = oracle.linearize(mu, cov, None, oracle.VoxelMap(mu, cov, 0.5, 3), I, I)
+    compare_factor(out[3], ref, 3)
+    # degenerate (exactly zero) covariances: skipped and counted (Q16)
+    z = np.zeros((1, 6), np.float32)
+    cz = gv.Cloud(ctx, np.array([[0.2, 0.5, 0.5]], np.float32), z)
+    mz = gv.create_voxelmap(ctx, gv.Cloud(ctx, np.array([[0.5, 0.5, 0.5]], np.float32), z), 1.0, 1)
+    out = gv.linearize_batch(ctx, [cz], [mz], [[0, 0, 0, 0, 0]], np.stack([I]))
+    assert int(out["num_degenerate"][0]) == 1 and out["inliers"][0][0] == 0 and out["error"][0] == 0
+    # argument errors name the factor
+    with pytest.raises(gv.GvoxError, match="factor 1: pose_j 7 missing"):
+        gv.linearize_batch(ctx, [full], [m], [[0, 0, 0, 0, 0], [0, 0, 0, 7, 0]], np.stack([I]))
+    with pytest.raises(gv.GvoxError, match="factor 0: target_map 3"):
+        gv.linearize_batch(ctx, [full], [m], [[0, 3, 0, 0, 0]], np.stack([I]))
+    bad = np.stack([I]).copy(); bad[0, 3] = np.inf
+    with pytest.raises(gv.GvoxError, match="not finite"):
+        gv.linearize_batch(ctx, [full], [m], [[0, 0, 0, 0, 0]], bad)
+
+
+def test_batch_equals_serial_and_determinism(gv, ctx):
+    sc = synth.make("C2")
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    a = gv.linearize_batch(ctx, clouds, maps, sc.factors, sc.poses)
+    b = gv.linearize_batch(ctx, clouds, maps, sc.factors, sc.poses)
+    assert a.tobytes() == b.tobytes(), "repeated runs must be bitwise identical"
+    for k in range(len(sc.factors)):
+        s = gv.linearize_batch(ctx, clouds, maps, sc.factors[k:k + 1], sc.poses)
+        for name in ("H_ii", "H_ij", "H_jj", "b_i", "b_j", "error"):
+            np.testing.assert_allclose(s[name][0], a[name][k], rtol=1e-9,
+                                       atol=1e-9 * np.abs(a[name][k]).max())
+        assert np.array_equal(s["inliers"][0], a["inliers"][k])
+    # N identical factors -> N identical outputs
+    rep = np.repeat(sc.factors[:1], 5, axis=0)
+    r = gv.linearize_batch(ctx, clouds, maps, rep, sc.poses)
+    assert all(r[k].tobytes() == r[0].tobytes() for k in range(5))
+
+
+def test_compact_expand_equals_full(gv, ctx):
+    import torch
+    sc = synth.make("C2")
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    full = gv.linearize_batch(ctx, clouds, maps, sc.factors, sc.poses)
+    acc = gv.device_records(ctx, len(sc.factors), gv.FACTOR_ACCUM_DTYPE)
+    gv.linearize_batch_accum(ctx, clouds, maps, sc.factors, sc.poses, out=acc)
+    exp = gv.expand(ctx, sc.factors, sc.poses, acc)
+    assert exp.tobytes() == full.tobytes()
+    dev = gv.device_records(ctx, len(sc.factors), gv.LINEAR_FACTOR_DTYPE)
+    gv.linearize_batch(ctx, clouds, maps, sc.factors, sc.poses, out=dev)
+    torch.cuda.synchronize()
+    assert gv.records_to_numpy(dev).tobytes() == full.tobytes()
+
+
+def test_error_only_flag(gv, ctx):
+    sc = synth.make("C2")
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    full = gv.linearize_batch(ctx, clouds, maps, sc.factors, sc.poses)
+    f = sc.factors.copy()
+    f[:, 4] |= gv.F_ERROR_ONLY
+    eo = gv.linearize_batch(ctx, clouds, maps, f, sc.poses)
+    assert np.array_equal(eo["error"], full["error"]) or np.allclose(eo["error"], full["error"], rtol=1e-12)
+    assert np.all(eo["H_jj"] == 0) and np.array_equal(eo["inliers"], full["inliers"])
+
+
+# ------------------------------------------------------------ full-size samples
+def test_full_size_submaps_sampled(gv, ctx, oracle):
+    """Per-factor sizes of C5 (100k-point submaps, r = 0.5/1/2 m) in the bench's
+    launch configuration (one batch over all factors, validation off); a sample
+    of factors and pairs is recomputed by the oracle."""
+    sc = synth.make("C5", n_submaps=48, half_blocks=4)
+    assert sc.cloud_size(0) == 100000
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    maps = gv.create_voxelmaps(ctx, clouds, sc.r0, sc.levels)
+    out = gv.linearize_batch(ctx, clouds, maps, sc.factors, sc.poses)
+    cnt = gv.overlap(ctx, clouds, maps, sc.pairs, sc.poses, sc.overlap_level)
+    rs = np.random.default_rng(0)
+    omaps = {}
+    for k in rs.choice(len(sc.factors), 6, replace=False):
+        f = sc.factors[k]
+        t = int(f[1])
+        omaps.setdefault(t, oracle.VoxelMap(*sc.cloud(t)[:2], sc.r0, sc.levels))
+        mu, cov, nrm = sc.cloud(int(f[0]))
+        ref = oracle.linearize(mu, cov, nrm, omaps[t], sc.poses[f[2]], sc.poses[f[3]])
+        compare_factor(out[k], ref, sc.levels, what=f"C5-size factor {k}")
+    for k in rs.choice(len(sc.pairs), 6, replace=False):
+        p = sc.pairs[k]
+        t = int(p[1])
+        omaps.setdefault(t, oracle.VoxelMap(*sc.cloud(t)[:2], sc.r0, sc.levels))
+        want = oracle.overlap(sc.cloud(int(p[0]))[0], omaps[t], sc.poses[p[2]], sc.poses[p[3]],
+                              sc.overlap_level)
+        assert int(cnt[k]) == want
+    # one sampled map, exported and compared bit-exactly on keys/counts
+    t = int(sc.factors[0][1])
+    omaps.setdefault(t, oracle.VoxelMap(*sc.cloud(t)[:2], sc.r0, sc.levels))
+    for l in range(sc.levels):
+        keys, means, covs, counts = maps[t].export(ctx, l)
+        okeys, omeans, ocovs, ocounts = omaps[t].export(l)
+        assert np.array_equal(keys, okeys) and np.array_equal(counts.astype(np.int64), ocounts)
