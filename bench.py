@@ -1,0 +1,523 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the batched VGICP hot path (GLIM, arXiv 2407.10344)
+on B200, in the driver's JSON-line contract.
+
+A STEP is one pass of every hot-path row of SURVEY.md Sec.8(a) over the
+workload (default C5: 2000 submaps x 100k points):
+  S1  gvox_create_voxelmaps  -- multi-resolution voxelmaps of every target submap
+  S2  gvox_overlap           -- overlap counts of every candidate submap pair
+      host: a pair becomes a factor iff 20 * count > N_src ("exceeds 5 %")
+  S3-S7 gvox_linearize_batch(_accum) -- every selected factor, one batch
+  (N > 1: factors sharded by target submap; one NCCL all_gather of the compact
+   per-factor records)
+value = sum over linearized factors of the source point count / step time
+(points linearized per second), inputs (clouds, poses, candidate list)
+resident in HBM before the timed region.  e2e = the same metric with clouds
+uploaded from pinned host memory and full records downloaded every step.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+torchrun launches one rank per GPU (RANK / LOCAL_RANK / WORLD_SIZE from env).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "VGICP source points linearized/s"
+UNIT = "points/s"
+WORKLOADS = {
+    "C5": "C5 large map: 2000 submaps x 100k points (15 frames each), overlap screening of "
+          "candidate pairs, overlap-selected factors (~1e5), r = 0.5/1/2 m",
+    "C4": "C4 global: 500 submaps x 50k points, overlap-selected factors, r = 0.5/1/2 m",
+    "C3": "C3 smoother window: 30 frames x 10 keyframe factors x 20k points, r = 0.25/0.5/1 m",
+    "C2": "C2 odometry step: one 20k frame vs 10 keyframe maps, r = 0.25/0.5/1 m",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5", choices=sorted(WORKLOADS))
+    ap.add_argument("--submaps", type=int, default=None, help="override the submap count (tests)")
+    ap.add_argument("--order", default="morton", choices=["morton", "random"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--linearize-only", action="store_true",
+                    help="profiling aid: time only S3-S7 (not a bench line)")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- scene
+def make_scene(args, rank, world, dist):
+    """Rank 0 generates (all host cores); other ranks load it from /dev/shm."""
+    import synth
+    kw = {}
+    if args.submaps:
+        kw["n_submaps"] = args.submaps
+    if args.order == "random":
+        kw["order_random"] = True
+    if args.config not in ("C4", "C5"):
+        kw = {}
+    if world == 1:
+        return synth.make(args.config, **kw)
+    path = f"/dev/shm/gvox_bench_{args.config}_{args.submaps}_{args.order}_{os.getppid()}.npz"
+    if rank == 0:
+        sc = synth.make(args.config, **kw)
+        np.savez(path, **{k: getattr(sc, k) for k in ("mu", "cov", "nrm", "offsets", "map_clouds",
+                                                      "factors", "poses", "gt_poses", "pairs")},
+                 meta=np.array([sc.r0, sc.levels, sc.overlap_level]), name=np.array(sc.name))
+    dist.barrier()
+    z = np.load(path)
+    meta = z["meta"]
+    sc = synth.Scene(str(z["name"]), z["mu"], z["cov"], z["nrm"], z["offsets"], z["map_clouds"],
+                     float(meta[0]), int(meta[1]), z["factors"], z["poses"], z["gt_poses"],
+                     z["pairs"], int(meta[2]))
+    dist.barrier()
+    if rank == 0:
+        os.unlink(path)
+    return sc
+
+
+def shard_targets(sc, world):
+    """Contiguous target-map ranges balanced by the candidate work (sum of source
+    points over candidate pairs + target points)."""
+    M = len(sc.map_clouds)
+    n = np.diff(sc.offsets)
+    w = n[sc.map_clouds].astype(np.float64)
+    np.add.at(w, sc.pairs[:, 1], n[sc.pairs[:, 0]])
+    cw = np.concatenate([[0], np.cumsum(w)])
+    bounds = [0]
+    for r in range(1, world):
+        bounds.append(int(np.searchsorted(cw, cw[-1] * r / world)))
+    bounds.append(M)
+    return bounds
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, device_index):
+        self.device = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        load = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- oracle legs
+def oracle_sample(sc, selected_pairs_mask=None, budget_s=12.0, threads=None):
+    """The oracle, as it stands, on a bounded sample of the same step: all rows
+    (map build, overlap, selection, linearize) for a contiguous block of target
+    submaps, so the mix of work matches the full step.  Returns (points, seconds,
+    description, cores)."""
+    from oracle import oracle
+    import synth
+    cores = threads or synth.host_threads()
+    n = np.diff(sc.offsets)
+    M = len(sc.map_clouds)
+    rs = np.random.default_rng(12345)
+    order = rs.permutation(M)
+    t0 = time.perf_counter()
+    pts = 0
+    nf = 0
+    npairs = 0
+    used = []
+    for t in order:
+        pr = sc.pairs[sc.pairs[:, 1] == t]
+        if len(pr) == 0:
+            continue
+        mu_t, cov_t, _ = sc.cloud(int(sc.map_clouds[t]))
+        om = oracle.VoxelMap(mu_t, cov_t, sc.r0, sc.levels)                     # S1
+        srcs = sorted(set(int(p[0]) for p in pr))
+        idx = {s: k for k, s in enumerate(srcs)}
+        pairs = np.array([[idx[int(p[0])], 0, int(p[2]), int(p[3])] for p in pr], np.int64)
+        counts = oracle.overlap_batch([sc.cloud(s)[0] for s in srcs], [om], pairs, sc.poses,
+                                      sc.overlap_level, cores)                  # S2
+        sel = 20 * counts > n[[srcs[int(p[0])] for p in pairs]]
+        fac = np.concatenate([pairs[sel], np.zeros((int(sel.sum()), 1), np.int64)], 1)
+        if len(fac):
+            oracle.linearize_batch([sc.cloud(s) for s in srcs], [om], fac, sc.poses, cores)  # S3-7
+        pts += int(n[[srcs[int(f[0])] for f in fac]].sum()) if len(fac) else 0
+        nf += len(fac)
+        npairs += len(pairs)
+        used.append(int(t))
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    desc = (f"{len(used)} of {M} target submaps (random, seed 12345) with all their rows: "
+            f"{len(used)} map builds, {npairs} overlap pairs, {nf} selected factors "
+            f"({pts} source points)")
+    return pts, dt, desc, cores
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sc = make_scene(args, 0, 1, None)
+    samples = []
+    desc = None
+    cores = None
+    for i in range(args.warmup + args.steps):
+        budget = max(2.0, 120.0 / max(1, args.warmup + args.steps))
+        pts, dt, desc, cores = oracle_sample(sc, budget_s=budget)
+        if i >= args.warmup:
+            samples.append((pts, dt))
+    tot_p = sum(p for p, _ in samples)
+    tot_t = sum(t for _, t in samples)
+    value = tot_p / tot_t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_t / len(samples), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "oracle_sample": desc},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- main
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2407_10344_b200 as gv
+
+    t_gen = time.perf_counter()
+    sc = make_scene(args, rank, world, dist)
+    t_gen = time.perf_counter() - t_gen
+    n_pts = np.diff(sc.offsets)
+    log(f"[bench r{rank}] scene {sc.name}: {sc.num_clouds} clouds, {len(sc.mu)} points, "
+        f"{len(sc.pairs)} candidate pairs, generated in {t_gen:.1f}s")
+
+    stream = torch.cuda.current_stream(dev)
+    ctx = gv.Context(dev.index, stream)
+    # ---- inputs resident in HBM (not timed)
+    mu_d = torch.from_numpy(sc.mu).to(dev)
+    cov_d = torch.from_numpy(sc.cov).to(dev)
+    nrm_d = torch.from_numpy(sc.nrm).to(dev)
+    clouds = gv.create_clouds(ctx, mu_d, cov_d, nrm_d, sc.offsets)
+    del mu_d, cov_d, nrm_d
+    cloud_arr = gv.HandleArray(clouds)
+    poses = gv.as_poses(sc.poses)
+
+    bounds = shard_targets(sc, world)
+    t_lo, t_hi = bounds[rank], bounds[rank + 1]
+    my_targets = np.arange(t_lo, t_hi)
+    pm = (sc.pairs[:, 1] >= t_lo) & (sc.pairs[:, 1] < t_hi)
+    my_pairs = sc.pairs[pm].copy()
+    my_pairs[:, 1] -= t_lo                      # local map index
+    pairs_s = gv.as_pairs(my_pairs)
+    src_n = n_pts[my_pairs[:, 0]]
+    my_target_clouds = [clouds[int(sc.map_clouds[t])] for t in my_targets]
+    flags = 0
+
+    # device buffers reused across steps
+    acc_out = gv.device_records(ctx, max(len(my_pairs), 1), gv.FACTOR_ACCUM_DTYPE)
+    counts_h = np.zeros(len(my_pairs), np.int32)
+
+    state = {}
+
+    def step(timed_maps=None):
+        maps = gv.create_voxelmaps(ctx, my_target_clouds, sc.r0, sc.levels)        # S1
+        marr = gv.HandleArray(maps)
+        gv.overlap(ctx, cloud_arr, marr, pairs_s, poses, sc.overlap_level, out=counts_h)  # S2
+        sel = 20 * counts_h.astype(np.int64) > src_n
+        fac = np.empty(int(sel.sum()), gv.FACTOR_DTYPE)
+        fac["source_cloud"] = my_pairs[sel, 0]
+        fac["target_map"] = my_pairs[sel, 1]
+        fac["pose_i"] = my_pairs[sel, 2]
+        fac["pose_j"] = my_pairs[sel, 3]
+        fac["flags"] = flags
+        out = acc_out[:len(fac)]
+        gv.linearize_batch_accum(ctx, cloud_arr, marr, fac, poses, out=out)         # S3-S7
+        if world > 1:
+            buf = acc_out[:state["fmax"]]
+            gathered = state["gather"]
+            dist.all_gather_into_tensor(gathered, buf)
+        state["maps"] = maps                  # keep alive until the next step replaces them
+        state["fac"] = fac
+        return int(src_n[sel].sum()), len(fac)
+
+    # ---- warm-up (also sizes the gather)
+    if world > 1:
+        state["fmax"] = max(len(my_pairs), 1)
+        t = torch.tensor([state["fmax"]], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        state["fmax"] = int(t.item())
+        acc_out = gv.device_records(ctx, state["fmax"], gv.FACTOR_ACCUM_DTYPE)
+        state["gather"] = torch.empty((world * state["fmax"], acc_out.shape[1]), dtype=torch.uint8,
+                                      device=dev)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    clocks = ClockSampler(dev.index)
+    if rank == 0:
+        clocks.start()
+        time.sleep(0.5)
+    ctx.enable_timing(True)
+    ctx.timing(reset=True)
+    gv.launch_count(reset=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    pts_total = 0
+    fac_total = 0
+    for _ in range(args.steps):
+        p, f = step()
+        pts_total += p
+        fac_total += f
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = gv.launch_count(reset=True)
+    tm = ctx.timing(reset=True)
+    ctx.enable_timing(False)
+    clk = clocks.stop() if rank == 0 else None
+
+    # max over ranks of the time; sum of the work
+    if world > 1:
+        t = torch.tensor([ms, pts_total, fac_total, launches], dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms = float(tmax[0])
+        pts_all, fac_all, launches_all = float(tsum[1]), float(tsum[2]), int(tsum[3])
+    else:
+        pts_all, fac_all, launches_all = float(pts_total), float(fac_total), launches
+    ms_step = ms / args.steps
+    value = pts_all / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (rank 0's launches)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else \
+        "B200_PROFILING.md fallback 6.65 TB/s"
+    fac = state["fac"]
+    maps = state["maps"]
+    lin_ms, lin_n = tm["linearize"]
+    # algorithmic bytes per launch: 48 B per point-factor (the 3 float4 source
+    # planes) + compulsory map bytes (16 B slot + 48 B voxel record per voxel)
+    # once per distinct target map in the launch.
+    pf = int(n_pts[fac["source_cloud"]].sum())
+    tmaps = np.unique(fac["target_map"])
+    map_bytes = sum(64 * sum(maps[int(t)].num_voxels(l) for l in range(sc.levels)) for t in tmaps)
+    alg_bytes = 48 * pf + map_bytes
+    lin_avg_s = (lin_ms / max(lin_n, 1)) / 1e3
+    achieved = alg_bytes / lin_avg_s / 1e9 if lin_n else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "linearize_dram_bytes_per_pf.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof))["dram_bytes_per_point_factor"] * pf
+        except (ValueError, KeyError):
+            traffic = None
+    stages = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for k, v in tm.items()}
+    dominant = max(tm, key=lambda k: tm[k][0])
+
+    # ---- e2e through the public API with host buffers (rank-local, N GPUs)
+    e2e = None
+    if not args.no_e2e:
+        mu_h = torch.from_numpy(sc.mu).pin_memory()
+        cov_h = torch.from_numpy(sc.cov).pin_memory()
+        nrm_h = torch.from_numpy(sc.nrm).pin_memory()
+        k_e2e = max(1, min(args.steps, 3))
+        pin_out = np.zeros(len(my_pairs), gv.LINEAR_FACTOR_DTYPE)
+        h2d = 0
+        d2h = 0
+
+        def e2e_step():
+            nonlocal h2d, d2h
+            # clouds needed by this rank's shard come from pinned host memory
+            need = sorted(set(int(c) for c in my_pairs[:, 0]) |
+                          set(int(sc.map_clouds[t]) for t in my_targets))
+            cl_all = gv.create_clouds(ctx, mu_h.numpy(), cov_h.numpy(), nrm_h.numpy(), sc.offsets) \
+                if len(need) > 0.5 * sc.num_clouds else None
+            if cl_all is None:
+                cl_all = [None] * sc.num_clouds
+                for c in need:
+                    a, b = int(sc.offsets[c]), int(sc.offsets[c + 1])
+                    cl_all[c] = gv.Cloud(ctx, mu_h.numpy()[a:b], cov_h.numpy()[a:b], nrm_h.numpy()[a:b])
+            h2d_b = 48 * int(sum(n_pts[c] for c in need)) if cl_all[0] is None else 48 * int(n_pts.sum())
+            carr = gv.HandleArray([c if c is not None else clouds[0] for c in cl_all])
+            maps_e = gv.create_voxelmaps(ctx, [cl_all[int(sc.map_clouds[t])] for t in my_targets],
+                                         sc.r0, sc.levels)
+            marr = gv.HandleArray(maps_e)
+            cnt = gv.overlap(ctx, carr, marr, pairs_s, poses, sc.overlap_level)
+            sel = 20 * cnt.astype(np.int64) > src_n
+            fe = np.empty(int(sel.sum()), gv.FACTOR_DTYPE)
+            fe["source_cloud"] = my_pairs[sel, 0]
+            fe["target_map"] = my_pairs[sel, 1]
+            fe["pose_i"] = my_pairs[sel, 2]
+            fe["pose_j"] = my_pairs[sel, 3]
+            fe["flags"] = flags
+            res = gv.linearize_batch(ctx, carr, marr, fe, poses, out=pin_out[:len(fe)])
+            h2d = h2d_b + poses.nbytes * 2 + pairs_s.nbytes + fe.nbytes
+            d2h = cnt.nbytes + res.nbytes
+            return int(src_n[sel].sum())
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        p_e2e = 0
+        for _ in range(k_e2e):
+            p_e2e += e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms_e2e = a0.elapsed_time(a1)
+        if world > 1:
+            t = torch.tensor([ms_e2e, p_e2e], dtype=torch.float64, device=dev)
+            tm_ = t.clone()
+            dist.all_reduce(tm_, op=dist.ReduceOp.MAX)
+            ts_ = t.clone()
+            dist.all_reduce(ts_, op=dist.ReduceOp.SUM)
+            ms_e2e, p_e2e = float(tm_[0]), float(ts_[1])
+        e2e = {"value": p_e2e / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": k_e2e, "ms_per_step": ms_e2e / k_e2e}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        pts_o, dt_o, desc, cores = oracle_sample(sc, budget_s=args.cpu_seconds)
+        cpu = {"value": pts_o / dt_o, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": desc, "seconds": dt_o}
+
+    if rank == 0:
+        n_levels_vox = {l: int(sum(m.num_voxels(l) for m in maps)) for l in range(sc.levels)}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded LiDAR-shaped submaps, synth/)",
+            "config": {"workload": WORKLOADS[args.config], "submaps": sc.num_clouds,
+                       "points": int(len(sc.mu)), "candidate_pairs": int(len(sc.pairs)),
+                       "factors_per_step": fac_all / args.steps, "levels": sc.levels, "r0": sc.r0,
+                       "overlap_level": sc.overlap_level, "point_order": args.order,
+                       "parallelism": f"factor-sharded x{world} (targets), NCCL all_gather",
+                       "l2": "inputs larger than L2 (clouds %.1f GB + maps %.1f GB on rank 0)"
+                             % (len(sc.mu) * 48 / 1e9,
+                                sum(64 * v for v in n_levels_vox.values()) / 1e9),
+                       "step": "S1 build all target maps + S2 overlap of all candidate pairs + "
+                               "selection (20*count > N) + S3-S7 linearize selected factors"},
+            "factors_per_s": fac_all / (ms / 1e3),
+            "precision": "per-point fp32 algebra; fp64 transform, voxel keys, residual base "
+                         "and cross-thread accumulation",
+            "stages": stages,
+            "roofline": {"kernel": "k_linearize", "bound": "hbm",
+                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": (achieved / hbm_peak) if achieved else None,
+                         "traffic": traffic, "peak_source": peak_src,
+                         "alg_bytes_per_launch": alg_bytes, "point_factors_per_launch": pf,
+                         "avg_launch_ms": lin_avg_s * 1e3,
+                         "dominant_kernel_group": dominant},
+            "e2e": e2e,
+            "gpu_launches": launches_all,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

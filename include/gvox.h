@@ -125,6 +125,21 @@ gvox_status gvox_ctx_create(int device, void* cuda_stream, gvox_ctx** out);
 gvox_status gvox_ctx_set_stream(gvox_ctx* ctx, void* cuda_stream);
 void gvox_ctx_destroy(gvox_ctx* ctx);
 
+/* Device-side timing of the library's own kernels.  When enabled, every launch
+   of a kernel group is bracketed by CUDA events on the context stream;
+   gvox_ctx_timing() (synchronizes) returns the summed elapsed milliseconds and
+   the launch count per group, optionally resetting them.  ms and launches are
+   arrays of GVOX_TIMER_COUNT entries (either may be NULL). */
+enum {
+  GVOX_TIMER_BUILD = 0,     /* voxelmap insert / accumulate / finalize kernels */
+  GVOX_TIMER_OVERLAP = 1,   /* overlap kernel */
+  GVOX_TIMER_LINEARIZE = 2, /* fused correspondence + linearization kernel */
+  GVOX_TIMER_REDUCE = 3,    /* per-factor reduction / expansion kernel */
+  GVOX_TIMER_COUNT = 4
+};
+gvox_status gvox_ctx_enable_timing(gvox_ctx* ctx, int enable);
+gvox_status gvox_ctx_timing(gvox_ctx* ctx, double* ms, int64_t* launches, int reset);
+
 /* ----------------------------------------------------------------- clouds */
 
 /* Gaussian point cloud (p_k = (mu_k, C_k)), optionally with normals for
@@ -136,6 +151,14 @@ void gvox_ctx_destroy(gvox_ctx* ctx);
    non-finite coordinate / covariance / normal (this call synchronizes). */
 gvox_status gvox_cloud_create(gvox_ctx* ctx, const float* mu, const float* cov,
                               const float* normals, int64_t n, int mem, gvox_cloud** out);
+/* Batched creation of `count` clouds stored back to back: cloud k holds points
+   [offsets[k], offsets[k+1]) of mu / cov / normals (offsets: host int64
+   [count + 1], offsets[0] = 0).  One copy, one packing launch and one
+   synchronization for the whole set; the clouds share one device allocation
+   (freed when the last of them is destroyed). */
+gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
+                               const float* normals, const int64_t* offsets, int64_t count,
+                               int mem, gvox_cloud** clouds_out);
 int64_t gvox_cloud_size(const gvox_cloud* cloud);
 void gvox_cloud_destroy(gvox_cloud* cloud);
 

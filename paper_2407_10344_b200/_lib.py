@@ -16,6 +16,7 @@ GVOX_HOST = 0
 GVOX_DEVICE = 1
 F_VALIDATE_SURFACE = 1
 F_ERROR_ONLY = 2
+TIMERS = ("build", "overlap", "linearize", "reduce")
 
 STATUS = {0: "GVOX_OK", 1: "GVOX_ERR_INVALID", 2: "GVOX_ERR_RANGE", 3: "GVOX_ERR_CUDA",
           4: "GVOX_ERR_NOMEM"}
@@ -35,8 +36,9 @@ FACTOR_ACCUM_DTYPE = np.dtype([("terms", "<f8", (28,)), ("inliers", "<i4", (MAX_
 
 # exported symbols (tests check every one declared in include/gvox.h is here)
 SYMBOLS = [
-    "gvox_ctx_create", "gvox_ctx_set_stream", "gvox_ctx_destroy",
-    "gvox_cloud_create", "gvox_cloud_size", "gvox_cloud_destroy",
+    "gvox_ctx_create", "gvox_ctx_set_stream", "gvox_ctx_destroy", "gvox_ctx_enable_timing",
+    "gvox_ctx_timing", "gvox_cloud_create", "gvox_clouds_create", "gvox_cloud_size",
+    "gvox_cloud_destroy",
     "gvox_create_voxelmap", "gvox_create_voxelmaps", "gvox_voxelmap_info", "gvox_voxelmap_levels",
     "gvox_voxelmap_export", "gvox_voxelmap_lookup", "gvox_map_destroy",
     "gvox_overlap", "gvox_linearize_batch", "gvox_linearize_batch_accum", "gvox_expand",
@@ -67,7 +69,10 @@ def lib():
         "gvox_ctx_create": (I32, [I32, P, PP]),
         "gvox_ctx_set_stream": (I32, [P, P]),
         "gvox_ctx_destroy": (None, [P]),
+        "gvox_ctx_enable_timing": (I32, [P, I32]),
+        "gvox_ctx_timing": (I32, [P, P, P, I32]),
         "gvox_cloud_create": (I32, [P, P, P, P, I64, I32, PP]),
+        "gvox_clouds_create": (I32, [P, P, P, P, P, I64, I32, P]),
         "gvox_cloud_size": (I64, [P]),
         "gvox_cloud_destroy": (None, [P]),
         "gvox_create_voxelmap": (I32, [P, P, D, I32, PP]),

@@ -57,6 +57,18 @@ class Context:
                                     ctypes.byref(h)))
         self.handle = h
 
+    def enable_timing(self, enable: bool = True):
+        """Bracket the library's kernel launches with CUDA events (gvox_ctx_enable_timing)."""
+        check(lib().gvox_ctx_enable_timing(self.handle, int(bool(enable))))
+
+    def timing(self, reset: bool = False) -> dict:
+        """{group: (ms, launches)} for groups build/overlap/linearize/reduce (synchronizes)."""
+        from ._lib import TIMERS
+        ms = (ctypes.c_double * len(TIMERS))()
+        n = (ctypes.c_int64 * len(TIMERS))()
+        check(lib().gvox_ctx_timing(self.handle, ms, n, int(bool(reset))))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(TIMERS)}
+
     def set_stream(self, stream):
         self.stream = stream
         check(lib().gvox_ctx_set_stream(self.handle, ctypes.c_void_p(stream.cuda_stream)))
@@ -78,7 +90,11 @@ class Cloud:
     arrays.  mu [n,3], cov [n,6] (xx xy xz yy yz zz), normals [n,3] or None;
     numpy (host) or torch CUDA tensors (device), float32."""
 
-    def __init__(self, ctx: Context, mu, cov, normals=None):
+    def __init__(self, ctx: Context, mu, cov, normals=None, *, _handle=None, _n=None):
+        if _handle is not None:
+            self.handle = _handle
+            self.n = int(_n)
+            return
         if not _is_cuda_tensor(mu):
             mu = np.ascontiguousarray(np.asarray(mu, np.float32).reshape(-1, 3))
             cov = np.ascontiguousarray(np.asarray(cov, np.float32).reshape(-1, 6))
@@ -106,6 +122,24 @@ class Cloud:
             self.close()
         except Exception:  # pragma: no cover
             pass
+
+
+def create_clouds(ctx: Context, mu, cov, normals, offsets):
+    """gvox_clouds_create: many clouds stored back to back (cloud k = rows
+    offsets[k]:offsets[k+1]); numpy (host, ideally pinned) or CUDA tensors."""
+    offsets = np.ascontiguousarray(np.asarray(offsets, np.int64))
+    count = len(offsets) - 1
+    if not _is_cuda_tensor(mu):
+        mu = np.ascontiguousarray(np.asarray(mu, np.float32).reshape(-1, 3))
+        cov = np.ascontiguousarray(np.asarray(cov, np.float32).reshape(-1, 6))
+        if normals is not None:
+            normals = np.ascontiguousarray(np.asarray(normals, np.float32).reshape(-1, 3))
+    pm, mem = _ptr(mu)
+    out = (ctypes.c_void_p * max(count, 1))()
+    check(lib().gvox_clouds_create(ctx.handle, pm, _ptr(cov)[0], _ptr(normals)[0],
+                                   _ptr(offsets)[0], count, mem, out))
+    return [Cloud(ctx, None, None, _handle=ctypes.c_void_p(out[k]),
+                  _n=int(offsets[k + 1] - offsets[k])) for k in range(count)]
 
 
 class VoxelMap:

@@ -160,6 +160,10 @@ void launch_reduce(const FactorDev* factors, const int32_t* tile_start, int64_t 
 void launch_expand(const FactorDev* factors, int64_t num_factors, const double* poses,
                    const gvox_factor_accum* accum, gvox_linear_factor* out, cudaStream_t stream);
 
+// tile -> owning item (factor or pair) table from the tile prefix sums
+void launch_tile_map(const int32_t* tile_start, int64_t num_items, int32_t* tile_owner,
+                     cudaStream_t stream);
+
 void note_launch();
 
 }  // namespace gvox

@@ -128,6 +128,12 @@ struct gvox_ctx {
   size_t pin_bytes = 0;
   cudaEvent_t pin_done = nullptr;  // last H2D out of `pin` has completed
   bool pin_pending = false;
+  // optional device-side kernel timing (gvox_ctx_enable_timing)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_open[GVOX_TIMER_COUNT];
+  double timer_ms[GVOX_TIMER_COUNT] = {};
+  int64_t timer_launches[GVOX_TIMER_COUNT] = {};
 };
 
 struct gvox_cloud {
@@ -197,6 +203,36 @@ gvox_status h2d_block(gvox_ctx* ctx, void* dst, const void* pinned_src, size_t b
   return GVOX_OK;
 }
 
+cudaEvent_t ev_get(gvox_ctx* ctx) {
+  if (!ctx->ev_pool.empty()) {
+    cudaEvent_t e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets the launches of one kernel group with CUDA events on the context
+// stream when timing is enabled.
+struct TimerScope {
+  gvox_ctx* ctx;
+  int which;
+  cudaEvent_t a = nullptr, b = nullptr;
+  TimerScope(gvox_ctx* c, int w) : ctx(c), which(w) {
+    if (!ctx->timing) return;
+    a = ev_get(ctx);
+    b = ev_get(ctx);
+    cudaEventRecord(a, ctx->stream);
+  }
+  ~TimerScope() {
+    if (!a) return;
+    cudaEventRecord(b, ctx->stream);
+    ctx->ev_open[which].push_back({a, b});
+  }
+};
+
 // Layout helper: a sequence of 256 B-aligned regions within one block.
 struct Layout {
   size_t size = 0;
@@ -247,87 +283,147 @@ void gvox_ctx_destroy(gvox_ctx* ctx) {
     if (ctx->ws[i]) cudaFree(ctx->ws[i]);
   if (ctx->pin) cudaFreeHost(ctx->pin);
   if (ctx->pin_done) cudaEventDestroy(ctx->pin_done);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (int t = 0; t < GVOX_TIMER_COUNT; ++t)
+    for (auto& pr : ctx->ev_open[t]) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
   delete ctx;
 }
 
+gvox_status gvox_ctx_enable_timing(gvox_ctx* ctx, int enable) {
+  if (!ctx) return fail(GVOX_ERR_INVALID, "gvox_ctx_enable_timing: ctx is NULL");
+  ctx->timing = enable != 0;
+  return GVOX_OK;
+}
+
+gvox_status gvox_ctx_timing(gvox_ctx* ctx, double* ms, int64_t* launches, int reset) {
+  if (!ctx) return fail(GVOX_ERR_INVALID, "gvox_ctx_timing: ctx is NULL");
+  DeviceGuard g(ctx->device);
+  for (int t = 0; t < GVOX_TIMER_COUNT; ++t) {
+    for (auto& pr : ctx->ev_open[t]) {
+      CK(cudaEventSynchronize(pr.second));
+      float e = 0.f;
+      CK(cudaEventElapsedTime(&e, pr.first, pr.second));
+      ctx->timer_ms[t] += e;
+      ctx->timer_launches[t] += 1;
+      ctx->ev_pool.push_back(pr.first);
+      ctx->ev_pool.push_back(pr.second);
+    }
+    ctx->ev_open[t].clear();
+    if (ms) ms[t] = ctx->timer_ms[t];
+    if (launches) launches[t] = ctx->timer_launches[t];
+    if (reset) {
+      ctx->timer_ms[t] = 0;
+      ctx->timer_launches[t] = 0;
+    }
+  }
+  return GVOX_OK;
+}
+
 // ------------------------------------------------------------------ clouds
-gvox_status gvox_cloud_create(gvox_ctx* ctx, const float* mu, const float* cov,
-                              const float* normals, int64_t n, int mem, gvox_cloud** out) {
-  if (!ctx || !out) return fail(GVOX_ERR_INVALID, "gvox_cloud_create: ctx/out is NULL");
-  *out = nullptr;
-  if (n < 0) return fail(GVOX_ERR_INVALID, "gvox_cloud_create: n = %lld < 0", (long long)n);
+gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
+                               const float* normals, const int64_t* offsets, int64_t count,
+                               int mem, gvox_cloud** out) {
+  if (!ctx || (count > 0 && (!out || !offsets)))
+    return fail(GVOX_ERR_INVALID, "gvox_clouds_create: ctx/offsets/out is NULL");
+  if (count < 0) return fail(GVOX_ERR_INVALID, "gvox_clouds_create: count < 0");
+  if (count == 0) return GVOX_OK;
+  if (offsets[0] != 0) return fail(GVOX_ERR_INVALID, "gvox_clouds_create: offsets[0] != 0");
+  for (int64_t k = 0; k < count; ++k) {
+    out[k] = nullptr;
+    if (offsets[k + 1] < offsets[k])
+      return fail(GVOX_ERR_INVALID, "gvox_cloud_create: cloud %lld has n = %lld < 0", (long long)k,
+                  (long long)(offsets[k + 1] - offsets[k]));
+  }
+  const int64_t n = offsets[count];
   if (n > 0 && (!mu || !cov))
     return fail(GVOX_ERR_INVALID, "gvox_cloud_create: mu/cov is NULL with n = %lld", (long long)n);
   if (mem != GVOX_HOST && mem != GVOX_DEVICE)
     return fail(GVOX_ERR_INVALID, "gvox_cloud_create: mem must be GVOX_HOST or GVOX_DEVICE");
   DeviceGuard g(ctx->device);
   Layout lay;
-  size_t o_desc = lay.add(sizeof(CloudDev));
+  size_t o_desc = lay.add(sizeof(CloudDev) * count);
   size_t o_a = lay.add(16 * (size_t)n), o_b = lay.add(16 * (size_t)n), o_n = lay.add(16 * (size_t)n);
+  size_t o_flags = lay.add(8 * (size_t)count);
   std::shared_ptr<DevBuf> buf;
   gvox_status st = devbuf_alloc(lay.size, ctx->device, &buf);
   if (st) return st;
   char* base = (char*)buf->ptr;
-  auto* c = new gvox_cloud;
-  c->buf = buf;
-  c->n = n;
-  c->device = ctx->device;
-  c->dev = (CloudDev*)(base + o_desc);
-  c->desc.n = n;
-  c->desc.has_normals = normals != nullptr;
-  c->desc.A = n ? (const float4*)(base + o_a) : nullptr;
-  c->desc.B = n ? (const float4*)(base + o_b) : nullptr;
-  c->desc.N = n ? (const float4*)(base + o_n) : nullptr;
+  float4* A = (float4*)(base + o_a);
+  float4* B = (float4*)(base + o_b);
+  float4* N = (float4*)(base + o_n);
+  // per-cloud {non-finite flag, max |C_ij|} words
+  int32_t* dflags = (int32_t*)(base + o_flags);
+  CK(cudaMemsetAsync(dflags, 0, 8 * (size_t)count, ctx->stream));
   if (n > 0) {
-    // source arrays on the device (copy host arrays into a workspace first)
     const float *dmu = mu, *dcov = cov, *dnrm = normals;
-    void* ws = nullptr;
-    size_t bytes_in = (size_t)n * (3 + 6 + (normals ? 3 : 0)) * 4;
-    st = ws_reserve(ctx, 2, bytes_in + 256, &ws);
-    if (st) {
-      delete c;
-      return st;
-    }
-    int32_t* flags = (int32_t*)ws;
-    uint32_t* cmax = (uint32_t*)((char*)ws + 4);
     if (mem == GVOX_HOST) {
-      char* p = (char*)ws + 256;
-      cudaMemcpyAsync(p, mu, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream);
-      cudaMemcpyAsync(p + n * 12, cov, (size_t)n * 24, cudaMemcpyHostToDevice, ctx->stream);
+      void* ws = nullptr;
+      size_t bytes_in = (size_t)n * (3 + 6 + (normals ? 3 : 0)) * 4;
+      st = ws_reserve(ctx, 2, bytes_in, &ws);
+      if (st) return st;
+      char* p = (char*)ws;
+      CK(cudaMemcpyAsync(p, mu, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(p + n * 12, cov, (size_t)n * 24, cudaMemcpyHostToDevice, ctx->stream));
       if (normals)
-        cudaMemcpyAsync(p + n * 36, normals, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream);
+        CK(cudaMemcpyAsync(p + n * 36, normals, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream));
       dmu = (const float*)p;
       dcov = (const float*)(p + n * 12);
       dnrm = normals ? (const float*)(p + n * 36) : nullptr;
     }
-    cudaMemsetAsync(ws, 0, 8, ctx->stream);
-    launch_cloud_pack(dmu, dcov, dnrm, n, (float4*)c->desc.A, (float4*)c->desc.B,
-                      (float4*)c->desc.N, flags, cmax, ctx->stream);
-    cudaError_t e = cudaGetLastError();
-    int32_t hflags[2] = {0, 0};
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(hflags, ws, 8, cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) {
-      delete c;
-      return cuda_fail(e, "gvox_cloud_create");
+    for (int64_t k = 0; k < count; ++k) {
+      int64_t a = offsets[k], m = offsets[k + 1] - offsets[k];
+      if (m == 0) continue;
+      launch_cloud_pack(dmu + 3 * a, dcov + 6 * a, dnrm ? dnrm + 3 * a : nullptr, m, A + a, B + a,
+                        N + a, dflags + 2 * k, (uint32_t*)(dflags + 2 * k + 1), ctx->stream);
     }
-    if (hflags[0] & 1) {
-      delete c;
-      return fail(GVOX_ERR_INVALID, "gvox_cloud_create: non-finite coordinate, covariance or normal");
-    }
-    uint32_t bits = (uint32_t)hflags[1];
+    CK_LAUNCH("gvox_cloud_create: pack");
+  }
+  std::vector<int32_t> hflags(2 * (size_t)count);
+  CK(cudaMemcpyAsync(hflags.data(), dflags, 8 * (size_t)count, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int64_t k = 0; k < count; ++k)
+    if (hflags[2 * k] & 1)
+      return fail(GVOX_ERR_INVALID,
+                  "gvox_cloud_create: cloud %lld has a non-finite coordinate, covariance or normal",
+                  (long long)k);
+  std::vector<CloudDev> descs(count);
+  for (int64_t k = 0; k < count; ++k) {
+    int64_t a = offsets[k], m = offsets[k + 1] - offsets[k];
+    CloudDev& d = descs[k];
+    d.n = m;
+    d.has_normals = normals != nullptr;
+    d.pad = 0;
+    d.A = m ? A + a : nullptr;
+    d.B = m ? B + a : nullptr;
+    d.N = m ? N + a : nullptr;
+  }
+  CK(cudaMemcpyAsync(base + o_desc, descs.data(), sizeof(CloudDev) * count, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int64_t k = 0; k < count; ++k) {
+    auto* c = new gvox_cloud;
+    c->buf = buf;
+    c->desc = descs[k];
+    c->dev = (CloudDev*)(base + o_desc) + k;
+    c->n = descs[k].n;
+    uint32_t bits = (uint32_t)hflags[2 * k + 1];
     std::memcpy(&c->cmax, &bits, 4);
+    c->device = ctx->device;
+    out[k] = c;
   }
-  cudaError_t e = cudaMemcpyAsync(c->dev, &c->desc, sizeof(CloudDev), cudaMemcpyHostToDevice,
-                                  ctx->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  if (e != cudaSuccess) {
-    delete c;
-    return cuda_fail(e, "gvox_cloud_create: descriptor upload");
-  }
-  *out = c;
   return GVOX_OK;
+}
+
+gvox_status gvox_cloud_create(gvox_ctx* ctx, const float* mu, const float* cov,
+                              const float* normals, int64_t n, int mem, gvox_cloud** out) {
+  if (!ctx || !out) return fail(GVOX_ERR_INVALID, "gvox_cloud_create: ctx/out is NULL");
+  *out = nullptr;
+  if (n < 0) return fail(GVOX_ERR_INVALID, "gvox_cloud_create: n = %lld < 0", (long long)n);
+  const int64_t offsets[2] = {0, n};
+  return gvox_clouds_create(ctx, mu, cov, normals, offsets, 1, mem, out);
 }
 
 int64_t gvox_cloud_size(const gvox_cloud* cloud) { return cloud ? cloud->n : -1; }
@@ -389,8 +485,11 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
                      ctx->stream));
   CK(cudaMemcpyAsync(b0 + o_start, seg_start.data(), 8 * (count + 1), cudaMemcpyHostToDevice,
                      ctx->stream));
-  launch_build_insert((const BuildSeg*)(b0 + o_bseg), count, (const int64_t*)(b0 + o_start), total,
-                      L, r0, dyadic, (int32_t*)(b0 + o_pslot), d_err, ctx->stream);
+  {
+    TimerScope ts(ctx, GVOX_TIMER_BUILD);
+    launch_build_insert((const BuildSeg*)(b0 + o_bseg), count, (const int64_t*)(b0 + o_start),
+                        total, L, r0, dyadic, (int32_t*)(b0 + o_pslot), d_err, ctx->stream);
+  }
   CK_LAUNCH("voxelmap insert");
   std::vector<int32_t> hcnt((size_t)count * L + 1);
   CK(cudaMemcpyAsync(hcnt.data(), d_cnt, ((size_t)count * L + 1) * 4, cudaMemcpyDeviceToHost,
@@ -494,12 +593,20 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
                      cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(b1 + o_vstart, vstart.data(), 8 * ((size_t)count * L + 1),
                      cudaMemcpyHostToDevice, ctx->stream));
-  launch_build_accum((const BuildSeg*)(b0 + o_bseg), (const AccumSeg*)(b0 + o_aseg), count,
-                     (const int64_t*)(b0 + o_start), total, L, r0, dyadic,
-                     (const int32_t*)(b0 + o_pslot), (unsigned long long*)(b1 + o_acc), ctx->stream);
+  {
+    TimerScope ts(ctx, GVOX_TIMER_BUILD);
+    launch_build_accum((const BuildSeg*)(b0 + o_bseg), (const AccumSeg*)(b0 + o_aseg), count,
+                       (const int64_t*)(b0 + o_start), total, L, r0, dyadic,
+                       (const int32_t*)(b0 + o_pslot), (unsigned long long*)(b1 + o_acc),
+                       ctx->stream);
+  }
   CK_LAUNCH("voxelmap accumulate");
-  launch_build_finalize((const FinalSeg*)(b1 + o_fseg), count * L, (const int64_t*)(b1 + o_vstart),
-                        total_vox, (const unsigned long long*)(b1 + o_acc), ctx->stream);
+  {
+    TimerScope ts(ctx, GVOX_TIMER_BUILD);
+    launch_build_finalize((const FinalSeg*)(b1 + o_fseg), count * L,
+                          (const int64_t*)(b1 + o_vstart), total_vox,
+                          (const unsigned long long*)(b1 + o_acc), ctx->stream);
+  }
   CK_LAUNCH("voxelmap finalize");
   for (int64_t s = 0; s < count; ++s)
     CK(cudaMemcpyAsync(ab + o_desc[s], &mdesc[s], sizeof(MapDev), cudaMemcpyHostToDevice,
@@ -715,9 +822,14 @@ gvox_status gvox_overlap(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t
   char* din = wb + o_in;
   int32_t* dcounts = mem == GVOX_DEVICE ? counts : (int32_t*)(wb + o_cnt);
   CK(cudaMemsetAsync(dcounts, 0, 4 * num_pairs, ctx->stream));
-  launch_overlap((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
-                 (const PairDev*)(din + o_pair), (const int32_t*)(din + o_ts), num_pairs, T, tile_pts,
-                 (const double*)(din + o_pose), level, (int32_t*)(wb + o_tp), dcounts, ctx->stream);
+  launch_tile_map((const int32_t*)(din + o_ts), num_pairs, (int32_t*)(wb + o_tp), ctx->stream);
+  {
+    TimerScope ts(ctx, GVOX_TIMER_OVERLAP);
+    launch_overlap((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
+                   (const PairDev*)(din + o_pair), (const int32_t*)(din + o_ts), num_pairs, T,
+                   tile_pts, (const double*)(din + o_pose), level, (int32_t*)(wb + o_tp), dcounts,
+                   ctx->stream);
+  }
   CK_LAUNCH("gvox_overlap");
   if (mem == GVOX_HOST) {
     CK(cudaMemcpyAsync(counts, dcounts, 4 * num_pairs, cudaMemcpyDeviceToHost, ctx->stream));
@@ -840,15 +952,22 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
   if (st) return st;
   char* din = wb + o_in;
   void* dout = mem == GVOX_DEVICE ? (out_full ? (void*)out_full : (void*)out_accum) : (void*)(wb + o_out);
-  launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
-                   (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
-                   tile_pts, max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
-                   (int32_t*)(wb + o_tf), corr_dump, ctx->stream);
+  launch_tile_map((const int32_t*)(din + o_ts), num_factors, (int32_t*)(wb + o_tf), ctx->stream);
+  {
+    TimerScope ts(ctx, GVOX_TIMER_LINEARIZE);
+    launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
+                     (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
+                     tile_pts, max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
+                     (int32_t*)(wb + o_tf), corr_dump, ctx->stream);
+  }
   CK_LAUNCH("linearize");
-  launch_reduce((const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors,
-                (const double*)(din + o_pose), (const double*)(wb + o_part),
-                out_full ? (gvox_linear_factor*)dout : nullptr,
-                out_full ? nullptr : (gvox_factor_accum*)dout, ctx->stream);
+  {
+    TimerScope ts(ctx, GVOX_TIMER_REDUCE);
+    launch_reduce((const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors,
+                  (const double*)(din + o_pose), (const double*)(wb + o_part),
+                  out_full ? (gvox_linear_factor*)dout : nullptr,
+                  out_full ? nullptr : (gvox_factor_accum*)dout, ctx->stream);
+  }
   CK_LAUNCH("linearize reduce");
   if (mem == GVOX_HOST) {
     void* host_out = out_full ? (void*)out_full : (void*)out_accum;

@@ -467,9 +467,6 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
                       double* partials, int32_t* tile_factor, int64_t* corr_dump,
                       cudaStream_t stream) {
   if (num_tiles <= 0) return;
-  k_tile_map<<<(unsigned)((num_factors + 255) / 256), 256, 0, stream>>>(tile_start, num_factors,
-                                                                         tile_factor);
-  note_launch();
   if (max_levels <= 3) {
     k_linearize<3><<<(unsigned)num_tiles, kThreads, 0, stream>>>(
         clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
@@ -477,6 +474,14 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
     k_linearize<GVOX_MAX_LEVELS><<<(unsigned)num_tiles, kThreads, 0, stream>>>(
         clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
   }
+  note_launch();
+}
+
+void launch_tile_map(const int32_t* tile_start, int64_t num_items, int32_t* tile_owner,
+                     cudaStream_t stream) {
+  if (num_items <= 0) return;
+  k_tile_map<<<(unsigned)((num_items + 255) / 256), 256, 0, stream>>>(tile_start, num_items,
+                                                                      tile_owner);
   note_launch();
 }
 

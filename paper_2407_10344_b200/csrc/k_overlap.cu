@@ -19,13 +19,6 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__global__ void k_tile_map_pairs(const int32_t* __restrict__ tile_start, int64_t n,
-                                 int32_t* __restrict__ tile_pair) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  for (int32_t t = tile_start[p]; t < tile_start[p + 1]; ++t) tile_pair[t] = (int32_t)p;
-}
-
 __global__ void __launch_bounds__(kThreads)
     k_overlap(const CloudDev* const* __restrict__ clouds, const MapDev* const* __restrict__ maps,
               const PairDev* __restrict__ pairs, const int32_t* __restrict__ tile_start,
@@ -99,9 +92,6 @@ void launch_overlap(const CloudDev* const* clouds, const MapDev* const* maps, co
                     const double* poses, int level, int32_t* tile_pair, int32_t* counts,
                     cudaStream_t stream) {
   if (num_tiles <= 0) return;
-  k_tile_map_pairs<<<(unsigned)((num_pairs + 255) / 256), 256, 0, stream>>>(tile_start, num_pairs,
-                                                                             tile_pair);
-  note_launch();
   k_overlap<<<(unsigned)num_tiles, kThreads, 0, stream>>>(clouds, maps, pairs, tile_start,
                                                           tile_pair, tile_pts, poses, level, counts);
   note_launch();

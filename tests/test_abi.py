@@ -15,8 +15,8 @@ HEADER = os.path.join(ROOT, "include", "gvox.h")
 
 @pytest.fixture(scope="module")
 def L():
-    from paper_2407_10344_b200 import _build
-    _build.build()
+    import __graft_entry__
+    __graft_entry__.build()
     from paper_2407_10344_b200 import _lib
     return _lib
 
