@@ -15,6 +15,7 @@
 //    + the packed key per voxel (u64) for export.
 #pragma once
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include "../../include/gvox.h"
@@ -34,14 +35,26 @@ struct CloudDev {
   int32_t pad;
 };
 
+// One level of a map.  Voxel lookup uses either
+//  * a DENSE index grid over the level's key bounding box (int32 voxel index
+//    or -1 per cell; chosen when the box has at most kDenseRatio cells per
+//    voxel): one predicated load, no probing; or
+//  * the open-addressing HASH table (sparse / very large extents).
 struct MapLevelDev {
-  const ulonglong2* slots;  // [mask + 1] {key, idx}
+  const ulonglong2* slots;  // hash: [mask + 1] {key, idx}
+  const int32_t* grid;      // dense: [dx * dy * dz], x-major; nullptr for hash
   const float4* vox;        // [3 * nvox]
-  uint64_t mask;
+  uint64_t mask;            // hash capacity - 1
+  int32_t shift;            // 64 - log2(capacity)
+  int32_t dense;            // 1 = dense grid
+  int32_t x0, y0, z0;       // dense: key of cell (0, 0, 0)
+  uint32_t dx, dy, dz;      // dense: box size in cells
   double r;      // r0 * 2^l
   double inv_r;  // 1 / r (used only when dyadic)
   int64_t nvox;
 };
+
+constexpr int kDenseRatio = 128;  // max cells per voxel for a dense grid level
 
 struct MapDev {
   int32_t levels;
@@ -55,9 +68,18 @@ struct MapDev {
 constexpr int kNumTerms = 28;
 constexpr int kPartialStride = 40;  // 28 terms, 8 inliers, invisible, degenerate, 2 pad
 
-__host__ __device__ inline uint64_t hash_slot(uint64_t key, uint64_t mask) {
-  // Fibonacci hashing of the packed key; the probe sequence is linear.
-  return (key * 0x9E3779B97F4A7C15ull) >> 20 & mask;
+// Fibonacci (multiplicative) hashing: the TOP log2(capacity) bits of
+// key * 2^64/phi, i.e. shift = 64 - log2(capacity).  (The low bits of the
+// product depend only on the low bits of the key, which would ignore kx.)
+// The probe sequence is linear.
+__host__ __device__ inline uint64_t hash_slot(uint64_t key, int shift) {
+  return (key * 0x9E3779B97F4A7C15ull) >> shift;
+}
+
+inline int shift_for_capacity(uint64_t cap) {  // cap = 2^k, k >= 1
+  int k = 0;
+  while ((1ull << k) < cap) ++k;
+  return 64 - k;
 }
 
 __host__ __device__ inline uint64_t pack_key(int32_t kx, int32_t ky, int32_t kz) {
@@ -70,11 +92,32 @@ __host__ __device__ inline bool key_in_range(int32_t k) { return k >= -kKeyHalf 
 // ---------------------------------------------------------------- launchers
 // (defined in k_*.cu; all asynchronous on `stream`)
 
-// cloud: pack user arrays into the planar layout; flags[0] |= 1 on non-finite
-// input; cmax_bits = max |C_ij| as float bits (atomicMax on non-negative floats).
+// cloud: pack user arrays into the planar layout and reduce per-cloud stats
+// (8 int32): [0] |= 1 on non-finite input, [1] = max |C_ij| (float bits),
+// [2..4] = min mu, [5..7] = max mu (order-preserving int encoding of floats;
+// initialise [2..4] to INT_MAX and [5..7] to INT_MIN).
 void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* A,
-                       float4* B, float4* N, int32_t* flags, uint32_t* cmax_bits,
-                       cudaStream_t stream);
+                       float4* B, float4* N, int32_t* stats, cudaStream_t stream);
+
+__host__ __device__ inline int32_t float_to_ordered(float f) {
+#ifdef __CUDA_ARCH__
+  int32_t i = __float_as_int(f);
+#else
+  int32_t i;
+  memcpy(&i, &f, 4);
+#endif
+  return i < 0 ? i ^ 0x7FFFFFFF : i;
+}
+__host__ __device__ inline float ordered_to_float(int32_t i) {
+  int32_t j = i < 0 ? i ^ 0x7FFFFFFF : i;
+#ifdef __CUDA_ARCH__
+  return __int_as_float(j);
+#else
+  float f;
+  memcpy(&f, &j, 4);
+  return f;
+#endif
+}
 
 // voxelmap build, phase 1: insert keys of every (cloud point, level) into the
 // per-(map, level) temporary tables; assign compact voxel indices.
@@ -84,6 +127,8 @@ struct BuildSeg {
   int64_t pl_offset;        // offset of this cloud's (point, level) records
   ulonglong2* tmp_slots[GVOX_MAX_LEVELS];  // temp tables (capacity tmp_mask+1)
   uint64_t tmp_mask;
+  int32_t tmp_shift;
+  int32_t pad;
   uint64_t* keys_by_idx[GVOX_MAX_LEVELS];  // [n] workspace: key of voxel idx
   int32_t* counter;         // [levels] voxel counts (atomic)
   // phase 1 records, per (point, level), the temp-table SLOT of its key;
@@ -119,6 +164,11 @@ struct FinalSeg {
   double cov_scale;
   ulonglong2* slots;        // final table
   uint64_t mask;
+  int32_t shift;
+  int32_t dense;
+  int32_t* grid;            // dense index grid (or nullptr)
+  int32_t x0, y0, z0;
+  uint32_t dx, dy, dz;
   float4* vox;              // [3 * nvox]
   uint64_t* keys_out;       // [nvox]
 };

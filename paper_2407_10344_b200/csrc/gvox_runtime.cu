@@ -85,26 +85,35 @@ bool is_dyadic(double r) {
   return std::frexp(r, &e) == 0.5;
 }
 
-// A device allocation shared by the handles carved out of it.
+// A device allocation shared by the handles carved out of it.  Stream-ordered:
+// allocated from the device's default memory pool on the creating context's
+// stream and returned to the pool on that stream when the last handle goes
+// (handles must therefore be destroyed before that stream is).
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
   int device = 0;
+  cudaStream_t stream = nullptr;
   ~DevBuf() {
     if (ptr) {
       DeviceGuard g(device);
-      cudaFree(ptr);
+      if (cudaFreeAsync(ptr, stream) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(ptr);
+      }
     }
   }
 };
 
-gvox_status devbuf_alloc(size_t bytes, int device, std::shared_ptr<DevBuf>* out) {
+gvox_status devbuf_alloc(size_t bytes, int device, cudaStream_t stream,
+                         std::shared_ptr<DevBuf>* out) {
   auto b = std::make_shared<DevBuf>();
   b->device = device;
   b->bytes = bytes;
+  b->stream = stream;
   if (bytes) {
-    cudaError_t e = cudaMalloc(&b->ptr, bytes);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    cudaError_t e = cudaMallocAsync(&b->ptr, bytes, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
   }
   *out = b;
   return GVOX_OK;
@@ -142,6 +151,7 @@ struct gvox_cloud {
   CloudDev* dev = nullptr;  // device copy of desc
   int64_t n = 0;
   float cmax = 0.f;      // max |C_ij| (fixed-point scale of the voxel build)
+  float lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};  // bounding box of the means (n > 0)
   int device = 0;
 };
 
@@ -160,16 +170,15 @@ namespace {
 
 gvox_status ws_reserve(gvox_ctx* ctx, int which, size_t bytes, void** out) {
   if (ctx->ws_bytes[which] < bytes) {
+    size_t nb = std::max(bytes, ctx->ws_bytes[which] * 3 / 2);
+    nb = align_up(nb, 1 << 20);
     if (ctx->ws[which]) {
-      CK(cudaStreamSynchronize(ctx->stream));
-      CK(cudaFree(ctx->ws[which]));
+      CK(cudaFreeAsync(ctx->ws[which], ctx->stream));
       ctx->ws[which] = nullptr;
       ctx->ws_bytes[which] = 0;
     }
-    size_t nb = std::max(bytes, ctx->ws_bytes[which] * 3 / 2);
-    nb = align_up(nb, 1 << 20);
-    cudaError_t e = cudaMalloc(&ctx->ws[which], nb);
-    if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMalloc");
+    cudaError_t e = cudaMallocAsync(&ctx->ws[which], nb, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMallocAsync");
     ctx->ws_bytes[which] = nb;
   }
   *out = ctx->ws[which];
@@ -260,6 +269,11 @@ gvox_status gvox_ctx_create(int device, void* cuda_stream, gvox_ctx** out) {
   auto* c = new gvox_ctx;
   c->device = device;
   c->stream = (cudaStream_t)cuda_stream;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;  // freed blocks stay in the pool for reuse
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   e = cudaEventCreateWithFlags(&c->pin_done, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete c;
@@ -280,7 +294,8 @@ void gvox_ctx_destroy(gvox_ctx* ctx) {
   DeviceGuard g(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (int i = 0; i < 3; ++i)
-    if (ctx->ws[i]) cudaFree(ctx->ws[i]);
+    if (ctx->ws[i]) cudaFreeAsync(ctx->ws[i], ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
   if (ctx->pin) cudaFreeHost(ctx->pin);
   if (ctx->pin_done) cudaEventDestroy(ctx->pin_done);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
@@ -346,17 +361,26 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
   Layout lay;
   size_t o_desc = lay.add(sizeof(CloudDev) * count);
   size_t o_a = lay.add(16 * (size_t)n), o_b = lay.add(16 * (size_t)n), o_n = lay.add(16 * (size_t)n);
-  size_t o_flags = lay.add(8 * (size_t)count);
+  size_t o_flags = lay.add(32 * (size_t)count);
   std::shared_ptr<DevBuf> buf;
-  gvox_status st = devbuf_alloc(lay.size, ctx->device, &buf);
+  gvox_status st = devbuf_alloc(lay.size, ctx->device, ctx->stream, &buf);
   if (st) return st;
   char* base = (char*)buf->ptr;
   float4* A = (float4*)(base + o_a);
   float4* B = (float4*)(base + o_b);
   float4* N = (float4*)(base + o_n);
-  // per-cloud {non-finite flag, max |C_ij|} words
+  // per-cloud statistics (see launch_cloud_pack): flag, max |C_ij|, min / max mean
   int32_t* dflags = (int32_t*)(base + o_flags);
-  CK(cudaMemsetAsync(dflags, 0, 8 * (size_t)count, ctx->stream));
+  std::vector<int32_t> hflags(8 * (size_t)count);
+  for (int64_t k = 0; k < count; ++k) {
+    int32_t* st8 = hflags.data() + 8 * k;
+    st8[0] = st8[1] = 0;
+    st8[2] = st8[3] = st8[4] = INT32_MAX;
+    st8[5] = st8[6] = st8[7] = INT32_MIN;
+  }
+  CK(cudaMemcpyAsync(dflags, hflags.data(), 32 * (size_t)count, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // hflags is reused below
   if (n > 0) {
     const float *dmu = mu, *dcov = cov, *dnrm = normals;
     if (mem == GVOX_HOST) {
@@ -377,15 +401,14 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
       int64_t a = offsets[k], m = offsets[k + 1] - offsets[k];
       if (m == 0) continue;
       launch_cloud_pack(dmu + 3 * a, dcov + 6 * a, dnrm ? dnrm + 3 * a : nullptr, m, A + a, B + a,
-                        N + a, dflags + 2 * k, (uint32_t*)(dflags + 2 * k + 1), ctx->stream);
+                        N + a, dflags + 8 * k, ctx->stream);
     }
     CK_LAUNCH("gvox_cloud_create: pack");
   }
-  std::vector<int32_t> hflags(2 * (size_t)count);
-  CK(cudaMemcpyAsync(hflags.data(), dflags, 8 * (size_t)count, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(hflags.data(), dflags, 32 * (size_t)count, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   for (int64_t k = 0; k < count; ++k)
-    if (hflags[2 * k] & 1)
+    if (hflags[8 * k] & 1)
       return fail(GVOX_ERR_INVALID,
                   "gvox_cloud_create: cloud %lld has a non-finite coordinate, covariance or normal",
                   (long long)k);
@@ -409,8 +432,13 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
     c->desc = descs[k];
     c->dev = (CloudDev*)(base + o_desc) + k;
     c->n = descs[k].n;
-    uint32_t bits = (uint32_t)hflags[2 * k + 1];
+    uint32_t bits = (uint32_t)hflags[8 * k + 1];
     std::memcpy(&c->cmax, &bits, 4);
+    if (c->n > 0)
+      for (int a = 0; a < 3; ++a) {
+        c->lo[a] = ordered_to_float(hflags[8 * k + 2 + a]);
+        c->hi[a] = ordered_to_float(hflags[8 * k + 5 + a]);
+      }
     c->device = ctx->device;
     out[k] = c;
   }
@@ -433,7 +461,7 @@ void gvox_cloud_destroy(gvox_cloud* cloud) { delete cloud; }
 // ------------------------------------------------------------------ voxelmaps
 namespace {
 
-constexpr int64_t kBuildChunkPoints = 8 << 20;
+constexpr int64_t kBuildChunkPoints = 32 << 20;
 
 gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t count, double r0,
                         int levels, gvox_map** maps_out) {
@@ -446,11 +474,13 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   std::vector<uint64_t> tcap(count);
   Layout lay;
   std::vector<size_t> o_tmp(count), o_keys(count);
+  // all temporary tables first (one contiguous region -> one memset)
   for (int64_t s = 0; s < count; ++s) {
     tcap[s] = pow2_at_least(std::max<uint64_t>(16, 2 * (uint64_t)clouds[s]->n));
     o_tmp[s] = lay.add(tcap[s] * 16 * L);
-    o_keys[s] = lay.add((size_t)clouds[s]->n * 8 * L);
   }
+  const size_t tmp_bytes = lay.size;
+  for (int64_t s = 0; s < count; ++s) o_keys[s] = lay.add((size_t)clouds[s]->n * 8 * L);
   size_t o_pslot = lay.add((size_t)total * L * 4);
   size_t o_cnt = lay.add((size_t)count * L * 4 + 4);
   size_t o_bseg = lay.add(sizeof(BuildSeg) * count);
@@ -471,6 +501,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     g.n = clouds[s]->n;
     g.pl_offset = seg_start[s] * L;
     g.tmp_mask = tcap[s] - 1;
+    g.tmp_shift = shift_for_capacity(tcap[s]);
     for (int l = 0; l < L; ++l) {
       g.tmp_slots[l] = (ulonglong2*)(b0 + o_tmp[s]) + tcap[s] * l;
       g.keys_by_idx[l] = (uint64_t*)(b0 + o_keys[s]) + (size_t)clouds[s]->n * l;
@@ -478,8 +509,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     g.counter = d_cnt + s * L;
   }
   // tables -> EMPTY (all 0xFF: key ~0, idx -1), counters + err -> 0
-  for (int64_t s = 0; s < count; ++s)
-    CK(cudaMemsetAsync(b0 + o_tmp[s], 0xFF, tcap[s] * 16 * L, ctx->stream));
+  CK(cudaMemsetAsync(b0, 0xFF, tmp_bytes, ctx->stream));
   CK(cudaMemsetAsync(d_cnt, 0, (size_t)count * L * 4 + 4, ctx->stream));
   CK(cudaMemcpyAsync(b0 + o_bseg, bseg.data(), sizeof(BuildSeg) * count, cudaMemcpyHostToDevice,
                      ctx->stream));
@@ -499,24 +529,66 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     return fail(GVOX_ERR_RANGE,
                 "gvox_create_voxelmap: a voxel key is outside [-2^20, 2^20) (r0 = %g)", r0);
 
-  // ---- final arena (exact sizes)
+  // ---- final arena (exact sizes).  Per level: a dense index grid over the
+  // key box of the cloud when it has at most kDenseRatio cells per voxel,
+  // else a hash table with capacity 2^k >= 2V.
+  struct LevelPlan {
+    uint64_t cap = 0;  // hash capacity (0 = dense)
+    int32_t x0 = 0, y0 = 0, z0 = 0;
+    uint32_t dx = 0, dy = 0, dz = 0;
+    uint64_t cells = 0;
+    size_t o_slots = 0, o_grid = 0, o_vox = 0, o_keys = 0;
+  };
   Layout al;
   std::vector<size_t> o_desc(count);
-  std::vector<std::array<size_t, 3>> o_lv((size_t)count * L);
-  std::vector<uint64_t> fcap((size_t)count * L);
+  std::vector<LevelPlan> plan((size_t)count * L);
   int64_t total_vox = 0;
+  for (int64_t s = 0; s < count; ++s) o_desc[s] = al.add(sizeof(MapDev));
+  // index structures (grids, hash slots) first: one contiguous 0xFF memset
+  const size_t idx_begin = al.size;
   for (int64_t s = 0; s < count; ++s) {
-    o_desc[s] = al.add(sizeof(MapDev));
+    const gvox_cloud* c = clouds[s];
+    int32_t k0lo[3] = {0, 0, 0}, k0hi[3] = {0, 0, 0};
+    for (int a = 0; a < 3; ++a) {
+      // the device key formula (voxel_coord0 + clamp_coord), evaluated on the host
+      double slo = dyadic ? (double)c->lo[a] * (1.0 / r0) : (double)c->lo[a] / r0;
+      double shi = dyadic ? (double)c->hi[a] * (1.0 / r0) : (double)c->hi[a] / r0;
+      double flo = std::floor(slo), fhi = std::floor(shi);
+      k0lo[a] = (int32_t)std::min(std::max(flo, -1073741824.0), 1073741824.0);
+      k0hi[a] = (int32_t)std::min(std::max(fhi, -1073741824.0), 1073741824.0);
+    }
     for (int l = 0; l < L; ++l) {
       int64_t V = hcnt[s * L + l];
-      uint64_t cap = pow2_at_least(std::max<uint64_t>(2, 2 * (uint64_t)V));
-      fcap[s * L + l] = cap;
-      o_lv[s * L + l] = {al.add(cap * 16), al.add((size_t)V * 48), al.add((size_t)V * 8)};
+      LevelPlan& p = plan[s * L + l];
+      uint64_t cells = 1;
+      int32_t lo3[3], n3[3];
+      for (int a = 0; a < 3; ++a) {
+        lo3[a] = k0lo[a] >> l;
+        n3[a] = (k0hi[a] >> l) - lo3[a] + 1;
+        cells *= (uint64_t)n3[a];
+      }
+      if (V > 0 && cells <= (uint64_t)kDenseRatio * (uint64_t)V && cells < (1ull << 31)) {
+        p.x0 = lo3[0]; p.y0 = lo3[1]; p.z0 = lo3[2];
+        p.dx = n3[0]; p.dy = n3[1]; p.dz = n3[2];
+        p.cells = cells;
+        p.o_grid = al.add(cells * 4);
+      } else {
+        p.cap = pow2_at_least(std::max<uint64_t>(2, 2 * (uint64_t)V));
+        p.o_slots = al.add(p.cap * 16);
+      }
       total_vox += V;
     }
   }
+  const size_t idx_end = al.size;
+  for (int64_t s = 0; s < count; ++s)
+    for (int l = 0; l < L; ++l) {
+      const int64_t V = hcnt[s * L + l];
+      LevelPlan& p = plan[s * L + l];
+      p.o_vox = al.add((size_t)V * 48);
+      p.o_keys = al.add((size_t)V * 8);
+    }
   std::shared_ptr<DevBuf> arena;
-  st = devbuf_alloc(al.size, ctx->device, &arena);
+  st = devbuf_alloc(al.size, ctx->device, ctx->stream, &arena);
   if (st) return st;
   char* ab = (char*)arena->ptr;
   // ---- phase 2/3 workspace (workspace 1): acc [total_vox][10] + seg tables
@@ -529,6 +601,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   if (st) return st;
   char* b1 = (char*)ws1;
   CK(cudaMemsetAsync(b1 + o_acc, 0, (size_t)total_vox * 80, ctx->stream));
+  CK(cudaMemsetAsync(ab + idx_begin, 0xFF, idx_end - idx_begin, ctx->stream));
 
   std::vector<AccumSeg> aseg(count);
   std::vector<FinalSeg> fseg((size_t)count * L);
@@ -571,19 +644,29 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       f.r = r;
       f.mu_scale = a.mu_scale[l];
       f.cov_scale = a.cov_scale;
-      f.slots = (ulonglong2*)(ab + o_lv[s * L + l][0]);
-      f.mask = fcap[s * L + l] - 1;
-      f.vox = (float4*)(ab + o_lv[s * L + l][1]);
-      f.keys_out = (uint64_t*)(ab + o_lv[s * L + l][2]);
+      const LevelPlan& p = plan[s * L + l];
+      f.slots = p.cap ? (ulonglong2*)(ab + p.o_slots) : nullptr;
+      f.mask = p.cap ? p.cap - 1 : 0;
+      f.shift = p.cap ? shift_for_capacity(p.cap) : 64;
+      f.dense = p.cap == 0;
+      f.grid = p.cap ? nullptr : (int32_t*)(ab + p.o_grid);
+      f.x0 = p.x0; f.y0 = p.y0; f.z0 = p.z0;
+      f.dx = p.dx; f.dy = p.dy; f.dz = p.dz;
+      f.vox = (float4*)(ab + p.o_vox);
+      f.keys_out = (uint64_t*)(ab + p.o_keys);
       vstart[s * L + l + 1] = vstart[s * L + l] + V;
       MapLevelDev& lv = md.lv[l];
       lv.slots = f.slots;
       lv.vox = f.vox;
       lv.mask = f.mask;
+      lv.shift = f.shift;
+      lv.grid = f.grid;
+      lv.dense = f.dense;
+      lv.x0 = f.x0; lv.y0 = f.y0; lv.z0 = f.z0;
+      lv.dx = f.dx; lv.dy = f.dy; lv.dz = f.dz;
       lv.r = r;
       lv.inv_r = 1.0 / r;
       lv.nvox = V;
-      CK(cudaMemsetAsync(f.slots, 0xFF, fcap[s * L + l] * 16, ctx->stream));
       vacc += V;
     }
   }
@@ -896,8 +979,8 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
     total_pf += clouds[factors[f].source_cloud]->n;
     max_levels = std::max(max_levels, maps[factors[f].target_map]->levels);
   }
-  int ppt = 1;  // points per thread per tile: enough tiles for ~4 waves of 296 CTAs
-  while (ppt < 16 && total_pf / ((int64_t)256 * ppt * 2) >= 148 * 2 * 4) ppt *= 2;
+  int ppt = 1;  // points per thread per tile: keep >= ~8 waves of 296 CTAs
+  while (ppt < 64 && total_pf / ((int64_t)256 * ppt * 2) >= 148 * 2 * 8) ppt *= 2;
   const int tile_pts = 256 * ppt;
   std::vector<int32_t> tstart(num_factors + 1, 0);
   std::vector<FactorDev> fdev(num_factors);

@@ -15,6 +15,7 @@
 //  phase 3  one thread per voxel: mean/cov = sums / count, stored as fp32
 //           offset-from-centre and fp32 covariance; insert into the final
 //           table (capacity 2^k >= 2V).
+#include <climits>
 #include <cstdint>
 
 #include "k_common.cuh"
@@ -30,10 +31,11 @@ __device__ inline bool finite3(float a, float b, float c) {
 __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restrict__ cov,
                              const float* __restrict__ nrm, int64_t n, float4* __restrict__ A,
                              float4* __restrict__ B, float4* __restrict__ N,
-                             int32_t* __restrict__ flags, uint32_t* __restrict__ cmax_bits) {
+                             int32_t* __restrict__ stats) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float cm = 0.f;
   bool bad = false;
+  int32_t lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
   if (i < n) {
     float x = mu[3 * i], y = mu[3 * i + 1], z = mu[3 * i + 2];
     float c0 = cov[6 * i], c1 = cov[6 * i + 1], c2 = cov[6 * i + 2];
@@ -50,15 +52,31 @@ __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restri
     N[i] = make_float4(c5, nx, ny, nz);
     cm = fmaxf(fmaxf(fmaxf(fabsf(c0), fabsf(c1)), fmaxf(fabsf(c2), fabsf(c3))),
                fmaxf(fabsf(c4), fabsf(c5)));
-    if (bad) cm = 0.f;
+    if (!bad) {
+      const float p[3] = {x, y, z};
+      for (int a = 0; a < 3; ++a) lo[a] = hi[a] = float_to_ordered(p[a]);
+    } else {
+      cm = 0.f;
+    }
   }
-  // warp max then one atomic per warp
+  // warp reductions, then one atomic per warp and statistic
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+  for (int o = 16; o > 0; o >>= 1) {
+    cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+  }
   unsigned anybad = __ballot_sync(0xffffffffu, bad);
   if ((threadIdx.x & 31) == 0) {
-    if (cm > 0.f) atomicMax(cmax_bits, __float_as_uint(cm));
-    if (anybad) atomicOr(flags, 1);
+    if (anybad) atomicOr(stats, 1);
+    if (cm > 0.f) atomicMax(reinterpret_cast<uint32_t*>(stats + 1), __float_as_uint(cm));
+    for (int a = 0; a < 3; ++a) {
+      if (lo[a] != INT_MAX) atomicMin(stats + 2 + a, lo[a]);
+      if (hi[a] != INT_MIN) atomicMax(stats + 5 + a, hi[a]);
+    }
   }
 }
 
@@ -96,7 +114,7 @@ __global__ void k_build_insert(const BuildSeg* __restrict__ segs, int64_t nseg,
     }
     uint64_t key = pack_key(kx, ky, kz);
     ulonglong2* slots = sg.tmp_slots[l];
-    uint64_t h = hash_slot(key, sg.tmp_mask);
+    uint64_t h = hash_slot(key, sg.tmp_shift);
     for (;;) {
       unsigned long long* kp = reinterpret_cast<unsigned long long*>(&slots[h].x);
       unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(kp);
@@ -177,7 +195,14 @@ __global__ void k_build_finalize(const FinalSeg* __restrict__ segs, int64_t nseg
   o[2] = make_float4((float)cv[5], __int_as_float((int)src[9]), 0.f, 0.f);
   uint64_t key = sg.keys_by_idx[v];
   sg.keys_out[v] = key;
-  uint64_t h = hash_slot(key, sg.mask);
+  if (sg.grid) {
+    const int32_t kx = (int32_t)((key >> 42) & 0x1FFFFF) - kKeyHalf;
+    const int32_t ky = (int32_t)((key >> 21) & 0x1FFFFF) - kKeyHalf;
+    const int32_t kz = (int32_t)(key & 0x1FFFFF) - kKeyHalf;
+    sg.grid[((size_t)(kx - sg.x0) * sg.dy + (ky - sg.y0)) * sg.dz + (kz - sg.z0)] = (int32_t)v;
+  }
+  if (!sg.slots) return;
+  uint64_t h = hash_slot(key, sg.shift);
   for (;;) {
     unsigned long long* kp = reinterpret_cast<unsigned long long*>(&sg.slots[h].x);
     unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
@@ -201,14 +226,11 @@ __global__ void k_lookup(const MapDev* __restrict__ map, int level, const double
   if (i >= n) return;
   const MapLevelDev& lv = map->lv[level];
   int dy = map->dyadic;
-  int32_t kx = voxel_coord0(q[3 * i], lv.r, lv.inv_r, dy);
-  int32_t ky = voxel_coord0(q[3 * i + 1], lv.r, lv.inv_r, dy);
-  int32_t kz = voxel_coord0(q[3 * i + 2], lv.r, lv.inv_r, dy);
+  int32_t kx = clamp_coord(voxel_coord0(q[3 * i], lv.r, lv.inv_r, dy));
+  int32_t ky = clamp_coord(voxel_coord0(q[3 * i + 1], lv.r, lv.inv_r, dy));
+  int32_t kz = clamp_coord(voxel_coord0(q[3 * i + 2], lv.r, lv.inv_r, dy));
   int64_t res = -1;
-  if (key_in_range(kx) && key_in_range(ky) && key_in_range(kz)) {
-    uint64_t key = pack_key(kx, ky, kz);
-    if (probe(lv, key) >= 0) res = (int64_t)key;
-  }
+  if (lookup_level(lv, kx, ky, kz) >= 0) res = (int64_t)pack_key(kx, ky, kz);
   out[i] = res;
 }
 
@@ -217,10 +239,9 @@ inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 
 }  // namespace
 
 void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* A,
-                       float4* B, float4* N, int32_t* flags, uint32_t* cmax_bits,
-                       cudaStream_t stream) {
+                       float4* B, float4* N, int32_t* stats, cudaStream_t stream) {
   if (n <= 0) return;
-  k_cloud_pack<<<grid_for(n, 256), 256, 0, stream>>>(mu, cov, nrm, n, A, B, N, flags, cmax_bits);
+  k_cloud_pack<<<grid_for(n, 256), 256, 0, stream>>>(mu, cov, nrm, n, A, B, N, stats);
   note_launch();
 }
 

@@ -39,14 +39,32 @@ __device__ inline int32_t voxel_coord0(double x, double r, double inv_r, int dya
 }
 
 // Probe a level's hash table: voxel index or -1.
-__device__ inline int32_t probe(const MapLevelDev& lv, uint64_t key) {
-  uint64_t h = hash_slot(key, lv.mask);
+__device__ inline int32_t probe_hash(const MapLevelDev& lv, uint64_t key) {
+  uint64_t h = hash_slot(key, lv.shift);
   for (;;) {
     ulonglong2 s = __ldg(lv.slots + h);
     if (s.x == key) return (int32_t)(uint32_t)s.y;
     if (s.x == kEmptyKey) return -1;
     h = (h + 1) & lv.mask;
   }
+}
+
+// Voxel index of level key (kx, ky, kz) or -1.  Keys must come from
+// clamp_coord() so that the subtractions below cannot overflow.
+__device__ inline int32_t lookup_level(const MapLevelDev& lv, int32_t kx, int32_t ky, int32_t kz) {
+  if (lv.dense) {
+    const uint32_t cx = (uint32_t)(kx - lv.x0), cy = (uint32_t)(ky - lv.y0), cz = (uint32_t)(kz - lv.z0);
+    if (cx >= lv.dx || cy >= lv.dy || cz >= lv.dz) return -1;
+    return __ldg(lv.grid + ((size_t)cx * lv.dy + cy) * lv.dz + cz);
+  }
+  if (!key_in_range(kx) || !key_in_range(ky) || !key_in_range(kz)) return -1;
+  return probe_hash(lv, pack_key(kx, ky, kz));
+}
+
+// floor(x / r0) clamped to [-2^30, 2^30]: anything clamped is out of key range
+// at every level l <= 7, and (k >> l) - x0 stays inside int32.
+__device__ inline int32_t clamp_coord(int32_t k) {
+  return min(max(k, -(1 << 30)), 1 << 30);
 }
 
 __device__ inline double warp_sum(double v) {

@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int L = sh.L;
   const int dyadic = sh.dyadic;
   const double r0 = sh.r0, inv_r0 = sh.inv_r0;
+  const float r0f = (float)sh.r0;
   const bool validate = sh.validate;
   const bool error_only = sh.error_only;
   const int64_t begin = sh.begin, end = sh.end;
@@ -154,32 +155,58 @@ __global__ void __launch_bounds__(kThreads, 2)
     const double qx = __fma_rn(sh.R[0], mx, __fma_rn(sh.R[1], my, __fma_rn(sh.R[2], mz, sh.t[0])));
     const double qy = __fma_rn(sh.R[3], mx, __fma_rn(sh.R[4], my, __fma_rn(sh.R[5], mz, sh.t[1])));
     const double qz = __fma_rn(sh.R[6], mx, __fma_rn(sh.R[7], my, __fma_rn(sh.R[8], mz, sh.t[2])));
-    const int32_t k0x = voxel_coord0(qx, r0, inv_r0, dyadic);
-    const int32_t k0y = voxel_coord0(qy, r0, inv_r0, dyadic);
-    const int32_t k0z = voxel_coord0(qz, r0, inv_r0, dyadic);
+    const int32_t k0x = clamp_coord(voxel_coord0(qx, r0, inv_r0, dyadic));
+    const int32_t k0y = clamp_coord(voxel_coord0(qy, r0, inv_r0, dyadic));
+    const int32_t k0z = clamp_coord(voxel_coord0(qz, r0, inv_r0, dyadic));
 
-    // R C R^T in fp32 (symmetric), computed lazily on the first hit
-    bool have_rcr = false;
-    float s00 = 0, s01 = 0, s02 = 0, s11 = 0, s12 = 0, s22 = 0;
     const float fqx = (float)qx, fqy = (float)qy, fqz = (float)qz;
-
+    // position inside the level-0 voxel (exact k0 * r0 for dyadic r0)
+    const float fx = (float)(qx - (double)k0x * r0);
+    const float fy = (float)(qy - (double)k0y * r0);
+    const float fz = (float)(qz - (double)k0z * r0);
+    bool have_rcr = false;
+    float s00 = 0.f, s01 = 0.f, s02 = 0.f, s11 = 0.f, s12 = 0.f, s22 = 0.f;
+    // levels are processed in groups of G (all loads of a group in flight together)
+    constexpr int G = MAXL < 4 ? MAXL : 4;
 #pragma unroll
-    for (int l = 0; l < MAXL; ++l) {
-      if (l >= L) break;
-      const int32_t kx = k0x >> l, ky = k0y >> l, kz = k0z >> l;
-      int32_t idx = -1;
-      uint64_t key = 0;
-      if (key_in_range(kx) && key_in_range(ky) && key_in_range(kz)) {
-        key = pack_key(kx, ky, kz);
-        idx = probe(sh.lv[l], key);
+    for (int lb = 0; lb < MAXL; lb += G) {
+      if (lb >= L) break;
+      // stage 1: the voxel index of every level of the group
+      int32_t vid[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int l = lb + j;
+        vid[j] = l < L ? lookup_level(sh.lv[l], k0x >> l, k0y >> l, k0z >> l) : -1;
       }
-      if (corr) corr[sh.corr_base + k * L + l] = idx >= 0 ? (int64_t)key : -1;
-      if (idx < 0) continue;
+      if (corr) {
+        for (int j = 0; j < G && lb + j < L; ++j) {
+          const int l = lb + j;
+          corr[sh.corr_base + k * L + l] =
+              vid[j] >= 0 ? (int64_t)pack_key(k0x >> l, k0y >> l, k0z >> l) : -1;
+        }
+      }
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < G; ++j) any |= vid[j] >= 0;
+      if (!any) continue;
 
+      // stage 2: gather the hit voxels' records (48 B each)
+      float4 v0[G], v1[G];
+      float v2[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        if (vid[j] >= 0) {
+          const float4* vp = sh.lv[lb + j].vox + 3 * (int64_t)vid[j];
+          v0[j] = __ldg(vp);
+          v1[j] = __ldg(vp + 1);
+          v2[j] = __ldg(&vp[2].x);
+        }
+      }
+
+      // R C R^T in fp32 (symmetric), once per point, overlapping the gathers
       if (!have_rcr) {
         have_rcr = true;
         const float* R = sh.Rf;
-        // M = R C
         const float m00 = R[0] * a.w + R[1] * b.x + R[2] * b.y;
         const float m01 = R[0] * b.x + R[1] * b.z + R[2] * b.w;
         const float m02 = R[0] * b.y + R[1] * b.w + R[2] * c.x;
@@ -189,7 +216,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         const float m20 = R[6] * a.w + R[7] * b.x + R[8] * b.y;
         const float m21 = R[6] * b.x + R[7] * b.z + R[8] * b.w;
         const float m22 = R[6] * b.y + R[7] * b.w + R[8] * c.x;
-        // S = M R^T (upper)
         s00 = m00 * R[0] + m01 * R[1] + m02 * R[2];
         s01 = m00 * R[3] + m01 * R[4] + m02 * R[5];
         s02 = m00 * R[6] + m01 * R[7] + m02 * R[8];
@@ -198,68 +224,70 @@ __global__ void __launch_bounds__(kThreads, 2)
         s22 = m20 * R[6] + m21 * R[7] + m22 * R[8];
       }
 
-      const float4* vp = sh.lv[l].vox + 3 * (int64_t)idx;
-      const float4 v0 = __ldg(vp);
-      const float4 v1 = __ldg(vp + 1);
-      const float v2 = __ldg(&vp[2].x);
+      // stage 3: per-level algebra
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        if (vid[j] < 0) continue;
+        const int l = lb + j;
+        // fused covariance (Eq.3) and its inverse by the symmetric adjugate
+        const float ca = v0[j].w + s00, cb = v1[j].x + s01, cc = v1[j].y + s02;
+        const float cd = v1[j].z + s11, ce = v1[j].w + s12, cf = v2[j] + s22;
+        const float i00 = cd * cf - ce * ce;
+        const float i01 = cc * ce - cb * cf;
+        const float i02 = cb * ce - cc * cd;
+        const float i11 = ca * cf - cc * cc;
+        const float i12 = cb * cc - ca * ce;
+        const float i22 = ca * cd - cb * cb;
+        const float det = ca * i00 + cb * i01 + cc * i02;
+        // Q16: a fused covariance that is not positive definite contributes nothing
+        const bool ok = det > 0.f && det < INFINITY;
+        const float id = ok ? __fdividef(1.0f, det) : 0.f;
+        n_degenerate += !ok;
+        inl[l] += ok;
+        const float o00 = i00 * id, o01 = i01 * id, o02 = i02 * id;
+        const float o11 = i11 * id, o12 = i12 * id, o22 = i22 * id;
 
-      // fused covariance (Eq.3) and its inverse by the symmetric adjugate
-      const float ca = v0.w + s00, cb = v1.x + s01, cc = v1.y + s02;
-      const float cd = v1.z + s11, ce = v1.w + s12, cf = v2 + s22;
-      const float i00 = cd * cf - ce * ce;
-      const float i01 = cc * ce - cb * cf;
-      const float i02 = cb * ce - cc * cd;
-      const float i11 = ca * cf - cc * cc;
-      const float i12 = cb * cc - ca * ce;
-      const float i22 = ca * cd - cb * cb;
-      const float det = ca * i00 + cb * i01 + cc * i02;
-      if (!(det > 0.f) || !(det < INFINITY)) {  // Q16: not positive definite
-        ++n_degenerate;
-        continue;
+        // d = mu~ - q = (centre_l - q) + offset (Q12).  With f = q - k0 r0 (the
+        // point's position inside its level-0 voxel, fp64 -> fp32 once per
+        // point) and k_l = k0 >> l:  centre_l - q = r0 (2^(l-1) - (k0 & (2^l - 1))) - f.
+        const int mlo = (1 << l) - 1;
+        const float hl = 0.5f * (float)(1 << l);
+        const float dx = r0f * (hl - (float)(k0x & mlo)) - fx + v0[j].x;
+        const float dy = r0f * (hl - (float)(k0y & mlo)) - fy + v0[j].y;
+        const float dz = r0f * (hl - (float)(k0z & mlo)) - fz + v0[j].z;
+
+        // g = Omega d, e = d^T g
+        const float gx = o00 * dx + o01 * dy + o02 * dz;
+        const float gy = o01 * dx + o11 * dy + o12 * dz;
+        const float gz = o02 * dx + o12 * dy + o22 * dz;
+        acc[27] += dx * gx + dy * gy + dz * gz;
+        if (error_only) continue;
+
+        acc[24] += gx;
+        acc[25] += gy;
+        acc[26] += gz;
+        // b_rot = q x g
+        acc[21] += fqy * gz - fqz * gy;
+        acc[22] += fqz * gx - fqx * gz;
+        acc[23] += fqx * gy - fqy * gx;
+        // sum Omega
+        acc[0] += o00; acc[1] += o01; acc[2] += o02;
+        acc[3] += o11; acc[4] += o12; acc[5] += o22;
+        // W = Omega [q]x
+        const float w00 = o01 * fqz - o02 * fqy, w01 = o02 * fqx - o00 * fqz, w02 = o00 * fqy - o01 * fqx;
+        const float w10 = o11 * fqz - o12 * fqy, w11 = o12 * fqx - o01 * fqz, w12 = o01 * fqy - o11 * fqx;
+        const float w20 = o12 * fqz - o22 * fqy, w21 = o22 * fqx - o02 * fqz, w22 = o02 * fqy - o12 * fqx;
+        acc[6] += w00; acc[7] += w01; acc[8] += w02;
+        acc[9] += w10; acc[10] += w11; acc[11] += w12;
+        acc[12] += w20; acc[13] += w21; acc[14] += w22;
+        // H_rr = -[q]x W (upper): rows of -[q]x are (0, qz, -qy), (-qz, 0, qx), (qy, -qx, 0)
+        acc[15] += fqz * w10 - fqy * w20;
+        acc[16] += fqz * w11 - fqy * w21;
+        acc[17] += fqz * w12 - fqy * w22;
+        acc[18] += fqx * w21 - fqz * w01;
+        acc[19] += fqx * w22 - fqz * w02;
+        acc[20] += fqy * w02 - fqx * w12;
       }
-      const float id = __frcp_rn(det);
-      const float o00 = i00 * id, o01 = i01 * id, o02 = i02 * id;
-      const float o11 = i11 * id, o12 = i12 * id, o22 = i22 * id;
-
-      // d = mu~ - q = fp32(centre - q64) + offset (Q12)
-      const double r = sh.lv[l].r;
-      const double hr = 0.5 * r;
-      const float dx = (float)(__fma_rn((double)kx, r, hr) - qx) + v0.x;
-      const float dy = (float)(__fma_rn((double)ky, r, hr) - qy) + v0.y;
-      const float dz = (float)(__fma_rn((double)kz, r, hr) - qz) + v0.z;
-
-      // g = Omega d, e = d^T g
-      const float gx = o00 * dx + o01 * dy + o02 * dz;
-      const float gy = o01 * dx + o11 * dy + o12 * dz;
-      const float gz = o02 * dx + o12 * dy + o22 * dz;
-      acc[27] += dx * gx + dy * gy + dz * gz;
-      ++inl[l];
-      if (error_only) continue;
-
-      acc[24] += gx;
-      acc[25] += gy;
-      acc[26] += gz;
-      // b_rot = q x g
-      acc[21] += fqy * gz - fqz * gy;
-      acc[22] += fqz * gx - fqx * gz;
-      acc[23] += fqx * gy - fqy * gx;
-      // sum Omega
-      acc[0] += o00; acc[1] += o01; acc[2] += o02;
-      acc[3] += o11; acc[4] += o12; acc[5] += o22;
-      // W = Omega [q]x
-      const float w00 = o01 * fqz - o02 * fqy, w01 = o02 * fqx - o00 * fqz, w02 = o00 * fqy - o01 * fqx;
-      const float w10 = o11 * fqz - o12 * fqy, w11 = o12 * fqx - o01 * fqz, w12 = o01 * fqy - o11 * fqx;
-      const float w20 = o12 * fqz - o22 * fqy, w21 = o22 * fqx - o02 * fqz, w22 = o02 * fqy - o12 * fqx;
-      acc[6] += w00; acc[7] += w01; acc[8] += w02;
-      acc[9] += w10; acc[10] += w11; acc[11] += w12;
-      acc[12] += w20; acc[13] += w21; acc[14] += w22;
-      // H_rr = -[q]x W (upper): rows of -[q]x are (0, qz, -qy), (-qz, 0, qx), (qy, -qx, 0)
-      acc[15] += fqz * w10 - fqy * w20;
-      acc[16] += fqz * w11 - fqy * w21;
-      acc[17] += fqz * w12 - fqy * w22;
-      acc[18] += fqx * w21 - fqz * w01;
-      acc[19] += fqx * w22 - fqz * w02;
-      acc[20] += fqy * w02 - fqx * w12;
     }
   }
 

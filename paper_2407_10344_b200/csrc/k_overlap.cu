@@ -65,13 +65,10 @@ __global__ void __launch_bounds__(kThreads)
     const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
     const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
     const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
-    const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
-    const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
-    const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
-    bool hit = false;
-    if (key_in_range(kx) && key_in_range(ky) && key_in_range(kz))
-      hit = probe(lv, pack_key(kx, ky, kz)) >= 0;
-    cnt += hit;
+    const int32_t kx = clamp_coord(voxel_coord0(qx, lv.r, lv.inv_r, dyadic));
+    const int32_t ky = clamp_coord(voxel_coord0(qy, lv.r, lv.inv_r, dyadic));
+    const int32_t kz = clamp_coord(voxel_coord0(qz, lv.r, lv.inv_r, dyadic));
+    cnt += lookup_level(lv, kx, ky, kz) >= 0;
   }
   // warp counts, then one atomic per CTA
 #pragma unroll
