@@ -329,6 +329,18 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if args.linearize_only:
+        # profiling aid: S3-S7 alone on the last step's maps and factors
+        lin_maps = gv.HandleArray(state["maps"])
+        lin_fac = state["fac"]
+        lin_pts = int(n_pts[lin_fac["source_cloud"]].sum())
+
+        def step():  # noqa: F811
+            gv.linearize_batch_accum(ctx, cloud_arr, lin_maps, lin_fac, poses,
+                                     out=acc_out[:len(lin_fac)])
+            return lin_pts, len(lin_fac)
+        step()
+        torch.cuda.synchronize()
 
     # ---- timed region
     clocks = ClockSampler(dev.index)
@@ -386,6 +398,9 @@ def main():
     fac = state["fac"]
     maps = state["maps"]
     lin_ms, lin_n = tm["linearize"]
+    if args.linearize_only:
+        log(f"[bench] linearize-only: {lin_ms / max(lin_n, 1):.3f} ms/launch, "
+            f"{pts_all / (ms / 1e3):.4g} point-factors/s")
     # algorithmic bytes per launch: 48 B per point-factor (the 3 float4 source
     # planes) + compulsory map bytes (16 B slot + 48 B voxel record per voxel)
     # once per distinct target map in the launch.

@@ -975,9 +975,12 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
   // ---- tile plan: tiles of tile_pts consecutive points of one factor
   int64_t total_pf = 0;
   int max_levels = 1;
+  bool all_dense = true;
   for (int64_t f = 0; f < num_factors; ++f) {
     total_pf += clouds[factors[f].source_cloud]->n;
-    max_levels = std::max(max_levels, maps[factors[f].target_map]->levels);
+    const gvox_map* m = maps[factors[f].target_map];
+    max_levels = std::max(max_levels, m->levels);
+    for (int l = 0; l < m->levels; ++l) all_dense = all_dense && m->desc.lv[l].dense;
   }
   int ppt = 1;  // points per thread per tile: keep >= ~8 waves of 296 CTAs
   while (ppt < 64 && total_pf / ((int64_t)256 * ppt * 2) >= 148 * 2 * 8) ppt *= 2;
@@ -1041,7 +1044,7 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
     launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
                      (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
                      tile_pts, max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
-                     (int32_t*)(wb + o_tf), corr_dump, ctx->stream);
+                     (int32_t*)(wb + o_tf), corr_dump, all_dense, ctx->stream);
   }
   CK_LAUNCH("linearize");
   {

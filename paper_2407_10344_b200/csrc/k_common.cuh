@@ -51,8 +51,9 @@ __device__ inline int32_t probe_hash(const MapLevelDev& lv, uint64_t key) {
 
 // Voxel index of level key (kx, ky, kz) or -1.  Keys must come from
 // clamp_coord() so that the subtractions below cannot overflow.
+template <bool ALL_DENSE = false>
 __device__ inline int32_t lookup_level(const MapLevelDev& lv, int32_t kx, int32_t ky, int32_t kz) {
-  if (lv.dense) {
+  if (ALL_DENSE || lv.dense) {
     const uint32_t cx = (uint32_t)(kx - lv.x0), cy = (uint32_t)(ky - lv.y0), cz = (uint32_t)(kz - lv.z0);
     if (cx >= lv.dx || cy >= lv.dy || cz >= lv.dz) return -1;
     return __ldg(lv.grid + ((size_t)cx * lv.dy + cy) * lv.dz + cz);

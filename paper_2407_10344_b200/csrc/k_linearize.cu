@@ -62,7 +62,7 @@ __global__ void k_tile_map(const int32_t* __restrict__ tile_start, int64_t num_f
   for (int32_t t = tile_start[f]; t < tile_start[f + 1]; ++t) tile_factor[t] = (int32_t)f;
 }
 
-template <int MAXL>
+template <int MAXL, bool ALL_DENSE>
 __global__ void __launch_bounds__(kThreads, 2)
     k_linearize(const CloudDev* const* __restrict__ clouds, const MapDev* const* __restrict__ maps,
                 const FactorDev* __restrict__ factors, const int32_t* __restrict__ tile_start,
@@ -132,10 +132,21 @@ __global__ void __launch_bounds__(kThreads, 2)
   for (int l = 0; l < MAXL; ++l) inl[l] = 0;
   int n_invisible = 0, n_degenerate = 0;
 
+  // software pipeline: the next point's 48 B source record is in flight while
+  // the current one is processed
+  float4 na, nb, nc;
+  if (begin + tid < end) {
+    na = __ldg(Ap + begin + tid);
+    nb = __ldg(Bp + begin + tid);
+    nc = __ldg(Np + begin + tid);
+  }
   for (int64_t k = begin + tid; k < end; k += kThreads) {
-    const float4 a = __ldg(Ap + k);
-    const float4 b = __ldg(Bp + k);
-    const float4 c = __ldg(Np + k);
+    const float4 a = na, b = nb, c = nc;
+    if (k + kThreads < end) {
+      na = __ldg(Ap + k + kThreads);
+      nb = __ldg(Bp + k + kThreads);
+      nc = __ldg(Np + k + kThreads);
+    }
     const double mx = a.x, my = a.y, mz = a.z;
     if (validate) {
       // discard if (mu - T_i^-1 t_j) . n > 0; zero normal = no test (Q7)
@@ -176,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const int l = lb + j;
-        vid[j] = l < L ? lookup_level(sh.lv[l], k0x >> l, k0y >> l, k0z >> l) : -1;
+        vid[j] = l < L ? lookup_level<ALL_DENSE>(sh.lv[l], k0x >> l, k0y >> l, k0z >> l) : -1;
       }
       if (corr) {
         for (int j = 0; j < G && lb + j < L; ++j) {
@@ -493,13 +504,20 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
                       const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
                       int64_t num_tiles, int tile_pts, int max_levels, const double* poses,
                       double* partials, int32_t* tile_factor, int64_t* corr_dump,
-                      cudaStream_t stream) {
+                      bool all_dense, cudaStream_t stream) {
   if (num_tiles <= 0) return;
+  const unsigned grid = (unsigned)num_tiles;
   if (max_levels <= 3) {
-    k_linearize<3><<<(unsigned)num_tiles, kThreads, 0, stream>>>(
-        clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
+    if (all_dense)
+      k_linearize<3, true><<<grid, kThreads, 0, stream>>>(clouds, maps, factors, tile_start,
+                                                          tile_factor, tile_pts, poses, partials,
+                                                          corr_dump);
+    else
+      k_linearize<3, false><<<grid, kThreads, 0, stream>>>(clouds, maps, factors, tile_start,
+                                                           tile_factor, tile_pts, poses, partials,
+                                                           corr_dump);
   } else {
-    k_linearize<GVOX_MAX_LEVELS><<<(unsigned)num_tiles, kThreads, 0, stream>>>(
+    k_linearize<GVOX_MAX_LEVELS, false><<<grid, kThreads, 0, stream>>>(
         clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
   }
   note_launch();
