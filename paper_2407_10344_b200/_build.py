@@ -27,18 +27,21 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile libgvox.so (or a variant with extra -D defines into `out`)."""
+    target = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     objs = []
     os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
     procs = []
     for src in sources():
-        obj = os.path.join(HERE, "build", os.path.basename(src) + ".o")
+        tag = "" if out is None else "_" + os.path.basename(out).replace(".so", "")
+        obj = os.path.join(HERE, "build", os.path.basename(src) + tag + ".o")
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                "--expt-relaxed-constexpr", "-I", os.path.join(os.path.dirname(HERE), "include"),
-               "-c", src, "-o", obj]
+               *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), src))
@@ -49,10 +52,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         logs.append(out.decode())
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{out.decode()}")
-    tmp = LIB + ".tmp"
+    tmp = target + ".tmp"
     subprocess.check_call([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt",
                            "-lpthread", "-ldl"])
-    os.replace(tmp, LIB)
+    os.replace(tmp, target)
     if verbose:
         print("\n".join(logs))
-    return LIB
+    return target

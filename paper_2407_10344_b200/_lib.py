@@ -9,7 +9,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgvox.so")
+# GVOX_LIB overrides the library path (kernel-variant experiments; see tools/)
+LIB_PATH = os.environ.get("GVOX_LIB") or os.path.join(HERE, "libgvox.so")
 
 MAX_LEVELS = 8
 GVOX_HOST = 0

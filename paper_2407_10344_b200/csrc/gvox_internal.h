@@ -9,7 +9,7 @@
 //    the overlap kernel streams only A (16 B/point); linearize streams all 3.
 //  * map level: open-addressing hash of 16 B slots {u64 packed key, i32 voxel
 //    index, pad} (capacity 2^k >= 2V, EMPTY key = ~0) + compact voxel records
-//    of 48 B: {off.x, off.y, off.z, C.xx}, {C.xy, C.xz, C.yy, C.yz},
+//    of 48 B: {off.x, off.y, off.z, C.xx}, {C.xy, C.yy, C.xz, C.yz},
 //    {C.zz, count (int bits), 0, 0}; `off` = voxel mean minus voxel centre in
 //    fp32 (the residual is formed as fp32(centre - q64) + off, reading Q12);
 //    + the packed key per voxel (u64) for export.
@@ -189,7 +189,7 @@ struct PairDev {
 void launch_overlap(const CloudDev* const* clouds, const MapDev* const* maps, const PairDev* pairs,
                     const int32_t* tile_start, int64_t num_pairs, int64_t num_tiles, int tile_pts,
                     const double* poses, int level, int32_t* tile_pair, int32_t* counts,
-                    cudaStream_t stream);
+                    bool all_dense, cudaStream_t stream);
 
 // linearize
 struct FactorDev {

@@ -550,7 +550,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     const gvox_cloud* c = clouds[s];
     int32_t k0lo[3] = {0, 0, 0}, k0hi[3] = {0, 0, 0};
     for (int a = 0; a < 3; ++a) {
-      // the device key formula (voxel_coord0 + clamp_coord), evaluated on the host
+      // the device key formula (voxel_coord0), evaluated on the host; clamped
       double slo = dyadic ? (double)c->lo[a] * (1.0 / r0) : (double)c->lo[a] / r0;
       double shi = dyadic ? (double)c->hi[a] * (1.0 / r0) : (double)c->hi[a] / r0;
       double flo = std::floor(slo), fhi = std::floor(shi);
@@ -567,7 +567,10 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
         n3[a] = (k0hi[a] >> l) - lo3[a] + 1;
         cells *= (uint64_t)n3[a];
       }
-      if (V > 0 && cells <= (uint64_t)kDenseRatio * (uint64_t)V && cells < (1ull << 31)) {
+      // dense grid: each dimension < 2^30 (the kernels rely on it to skip
+      // clamping saturated coordinates) and at most kDenseRatio cells per voxel
+      const bool dims_ok = n3[0] < (1 << 30) && n3[1] < (1 << 30) && n3[2] < (1 << 30);
+      if (V > 0 && dims_ok && cells <= (uint64_t)kDenseRatio * (uint64_t)V && cells < (1ull << 31)) {
         p.x0 = lo3[0]; p.y0 = lo3[1]; p.z0 = lo3[2];
         p.dx = n3[0]; p.dy = n3[1]; p.dz = n3[2];
         p.cells = cells;
@@ -796,7 +799,7 @@ gvox_status gvox_voxelmap_export(gvox_ctx* ctx, const gvox_map* map, int level, 
       for (int d = 0; d < 3; ++d) means[3 * i + d] = ((double)kk[d] + 0.5) * r + (double)off[d];
     }
     if (covs) {
-      const float cv[6] = {a.w, b.x, b.y, b.z, b.w, c.x};
+      const float cv[6] = {a.w, b.x, b.z, b.y, b.w, c.x};  // record: {xy, yy, xz, yz}
       for (int d = 0; d < 6; ++d) covs[6 * i + d] = cv[d];
     }
     if (counts) {
@@ -867,8 +870,16 @@ gvox_status gvox_overlap(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t
     if (!finite_pose(poses + 12 * i))
       return fail(GVOX_ERR_INVALID, "gvox_overlap: pose %lld is not finite", (long long)i);
   DeviceGuard g(ctx->device);
-  // tiles of 2048 source points
-  const int tile_pts = 2048;
+  // tiles of 256 * ppt source points: >= ~8 waves of 8 CTAs per SM
+  int64_t total_pts = 0;
+  bool all_dense = true;
+  for (int64_t p = 0; p < num_pairs; ++p) {
+    total_pts += clouds[pairs[p].source_cloud]->n;
+    all_dense = all_dense && maps[pairs[p].target_map]->desc.lv[level].dense;
+  }
+  int ppt = 1;
+  while (ppt < 32 && total_pts / ((int64_t)256 * ppt * 2) >= 148 * 8 * 8) ppt *= 2;
+  const int tile_pts = 256 * ppt;
   std::vector<int32_t> tstart(num_pairs + 1, 0);
   for (int64_t p = 0; p < num_pairs; ++p) {
     int64_t n = clouds[pairs[p].source_cloud]->n;
@@ -911,7 +922,7 @@ gvox_status gvox_overlap(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t
     launch_overlap((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
                    (const PairDev*)(din + o_pair), (const int32_t*)(din + o_ts), num_pairs, T,
                    tile_pts, (const double*)(din + o_pose), level, (int32_t*)(wb + o_tp), dcounts,
-                   ctx->stream);
+                   all_dense, ctx->stream);
   }
   CK_LAUNCH("gvox_overlap");
   if (mem == GVOX_HOST) {

@@ -90,48 +90,63 @@ __device__ inline int64_t seg_of(const int64_t* start, int64_t nseg, int64_t i) 
   return lo;
 }
 
+// Both passes aggregate within a warp: lanes holding the same (map, key) --
+// frequent, since consecutive points are spatially coherent -- are grouped with
+// __match_any_sync and only the group leader touches the table / issues the
+// atomics.  Every lane runs every level (inactive lanes carry unique dummy
+// keys) so the warp stays converged for the *_sync collectives.
+
 __global__ void k_build_insert(const BuildSeg* __restrict__ segs, int64_t nseg,
                                const int64_t* __restrict__ seg_start, int64_t total, int levels,
                                double r0, double inv_r0, int dyadic, int32_t* __restrict__ pslot,
                                int32_t* __restrict__ err) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  int64_t s = seg_of(seg_start, nseg, i);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool valid = i < total;
+  const int64_t s = valid ? seg_of(seg_start, nseg, i) : 0;
   const BuildSeg& sg = segs[s];
-  int64_t k = i - seg_start[s];
-  float4 a = __ldg(sg.A + k);
-  int32_t k0x = voxel_coord0((double)a.x, r0, inv_r0, dyadic);
-  int32_t k0y = voxel_coord0((double)a.y, r0, inv_r0, dyadic);
-  int32_t k0z = voxel_coord0((double)a.z, r0, inv_r0, dyadic);
+  const int64_t k = valid ? i - seg_start[s] : 0;
+  int32_t k0x = 0, k0y = 0, k0z = 0;
+  if (valid) {
+    const float4 a = __ldg(sg.A + k);
+    k0x = voxel_coord0((double)a.x, r0, inv_r0, dyadic);
+    k0y = voxel_coord0((double)a.y, r0, inv_r0, dyadic);
+    k0z = voxel_coord0((double)a.z, r0, inv_r0, dyadic);
+  }
   for (int l = 0; l < levels; ++l) {
     // floor(x / r_l) = floor(x / r0) >> l exactly (r_l = r0 2^l)
-    int32_t kx = k0x >> l, ky = k0y >> l, kz = k0z >> l;
-    int64_t rec = sg.pl_offset + k * levels + l;
-    if (!key_in_range(kx) || !key_in_range(ky) || !key_in_range(kz)) {
-      atomicOr(err, 1);
-      pslot[rec] = -1;
-      continue;
-    }
-    uint64_t key = pack_key(kx, ky, kz);
-    ulonglong2* slots = sg.tmp_slots[l];
-    uint64_t h = hash_slot(key, sg.tmp_shift);
-    for (;;) {
-      unsigned long long* kp = reinterpret_cast<unsigned long long*>(&slots[h].x);
-      unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(kp);
-      if (cur == key) break;
-      if (cur == kEmptyKey) {
-        unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
-        if (prev == kEmptyKey) {
-          int32_t idx = atomicAdd(sg.counter + l, 1);
-          slots[h].y = (unsigned long long)(uint32_t)idx | 0xFFFFFFFF00000000ull;
-          sg.keys_by_idx[l][idx] = key;
-          break;
+    const int32_t kx = k0x >> l, ky = k0y >> l, kz = k0z >> l;
+    const bool inr = valid && key_in_range(kx) && key_in_range(ky) && key_in_range(kz);
+    if (valid && !inr) atomicOr(err, 1);
+    // real keys are < 2^63; dummies (~0 - lane) are distinct and never inserted
+    const uint64_t key = inr ? pack_key(kx, ky, kz) : ~0ull - (uint64_t)lane;
+    const unsigned grp = __match_any_sync(0xffffffffu, key) &
+                         __match_any_sync(0xffffffffu, (unsigned long long)s);
+    const int leader = __ffs(grp) - 1;
+    int32_t h_out = -1;
+    if (lane == leader && inr) {
+      ulonglong2* slots = sg.tmp_slots[l];
+      uint64_t h = hash_slot(key, sg.tmp_shift);
+      for (;;) {
+        unsigned long long* kp = reinterpret_cast<unsigned long long*>(&slots[h].x);
+        unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(kp);
+        if (cur == key) break;
+        if (cur == kEmptyKey) {
+          unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
+          if (prev == kEmptyKey) {
+            int32_t idx = atomicAdd(sg.counter + l, 1);
+            slots[h].y = (unsigned long long)(uint32_t)idx | 0xFFFFFFFF00000000ull;
+            sg.keys_by_idx[l][idx] = key;
+            break;
+          }
+          if (prev == key) break;
         }
-        if (prev == key) break;
+        h = (h + 1) & sg.tmp_mask;
       }
-      h = (h + 1) & sg.tmp_mask;
+      h_out = (int32_t)h;
     }
-    pslot[rec] = (int32_t)h;
+    h_out = __shfl_sync(0xffffffffu, h_out, leader);
+    if (valid) pslot[sg.pl_offset + k * levels + l] = inr ? h_out : -1;
   }
 }
 
@@ -139,39 +154,64 @@ __device__ inline unsigned long long to_fixed(double x) {
   return (unsigned long long)__double2ll_rn(x);
 }
 
+// Sum of a 64-bit integer over the lanes of `grp` (two's complement, mod 2^64)
+// with 32-bit REDUX on three 22-bit chunks (<= 32 * 2^22 < 2^32: no overflow).
+__device__ inline unsigned long long group_sum_u64(unsigned grp, unsigned long long v) {
+  const unsigned c0 = __reduce_add_sync(grp, (unsigned)(v & 0x3FFFFFull));
+  const unsigned c1 = __reduce_add_sync(grp, (unsigned)((v >> 22) & 0x3FFFFFull));
+  const unsigned c2 = __reduce_add_sync(grp, (unsigned)(v >> 44));
+  return (unsigned long long)c0 + ((unsigned long long)c1 << 22) + ((unsigned long long)c2 << 44);
+}
+
 __global__ void k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg* __restrict__ segs,
                               int64_t nseg, const int64_t* __restrict__ seg_start, int64_t total,
                               int levels, double r0, double inv_r0, int dyadic,
                               const int32_t* __restrict__ pslot,
                               unsigned long long* __restrict__ acc) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  int64_t s = seg_of(seg_start, nseg, i);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool valid = i < total;
+  const int64_t s = valid ? seg_of(seg_start, nseg, i) : 0;
   const AccumSeg& sg = segs[s];
   const BuildSeg& bs = bsegs[s];
-  int64_t k = i - seg_start[s];
-  float4 a = __ldg(sg.A + k), b = __ldg(sg.B + k), c = __ldg(sg.N + k);
-  double x = a.x, y = a.y, z = a.z;
-  int32_t k0x = voxel_coord0(x, r0, inv_r0, dyadic);
-  int32_t k0y = voxel_coord0(y, r0, inv_r0, dyadic);
-  int32_t k0z = voxel_coord0(z, r0, inv_r0, dyadic);
+  const int64_t k = valid ? i - seg_start[s] : 0;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, c = a;
+  if (valid) {
+    a = __ldg(sg.A + k);
+    b = __ldg(sg.B + k);
+    c = __ldg(sg.N + k);
+  }
+  const double x = a.x, y = a.y, z = a.z;
+  const int32_t k0x = voxel_coord0(x, r0, inv_r0, dyadic);
+  const int32_t k0y = voxel_coord0(y, r0, inv_r0, dyadic);
+  const int32_t k0z = voxel_coord0(z, r0, inv_r0, dyadic);
   const float cv[6] = {a.w, b.x, b.y, b.z, b.w, c.x};
   for (int l = 0; l < levels; ++l) {
-    int32_t sl = pslot[sg.pl_offset + k * levels + l];
-    if (sl < 0) continue;
-    int32_t idx = (int32_t)(uint32_t)bs.tmp_slots[l][sl].y;
-    double r = ldexp(r0, l);
-    // offset of the point within its voxel (voxel corner = k_l * r_l)
-    double ox = x - (double)(k0x >> l) * r, oy = y - (double)(k0y >> l) * r,
-           oz = z - (double)(k0z >> l) * r;
-    unsigned long long* dst = acc + (sg.acc_offset[l] + idx) * 10;
-    double S = sg.mu_scale[l];
-    atomicAdd(dst + 0, to_fixed(ox * S));
-    atomicAdd(dst + 1, to_fixed(oy * S));
-    atomicAdd(dst + 2, to_fixed(oz * S));
+    const int32_t sl = valid ? pslot[sg.pl_offset + k * levels + l] : -1;
+    const int32_t idx = sl >= 0 ? (int32_t)(uint32_t)bs.tmp_slots[l][sl].y : -1 - lane;
+    const unsigned grp = __match_any_sync(0xffffffffu, idx) &
+                         __match_any_sync(0xffffffffu, (unsigned long long)s);
+    const int leader = __ffs(grp) - 1;
+    unsigned long long v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (sl >= 0) {
+      const double r = ldexp(r0, l);
+      // offset of the point within its voxel (voxel corner = k_l * r_l), fixed point
+      const double S = sg.mu_scale[l];
+      v[0] = to_fixed((x - (double)(k0x >> l) * r) * S);
+      v[1] = to_fixed((y - (double)(k0y >> l) * r) * S);
+      v[2] = to_fixed((z - (double)(k0z >> l) * r) * S);
 #pragma unroll
-    for (int j = 0; j < 6; ++j) atomicAdd(dst + 3 + j, to_fixed((double)cv[j] * sg.cov_scale));
-    atomicAdd(dst + 9, 1ull);
+      for (int j = 0; j < 6; ++j) v[3 + j] = to_fixed((double)cv[j] * sg.cov_scale);
+    }
+    unsigned long long sum[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) sum[j] = group_sum_u64(grp, v[j]);
+    if (lane == leader && sl >= 0) {
+      unsigned long long* dst = acc + (sg.acc_offset[l] + idx) * 10;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) atomicAdd(dst + j, sum[j]);
+      atomicAdd(dst + 9, (unsigned long long)__popc(grp));
+    }
   }
 }
 
@@ -191,7 +231,9 @@ __global__ void k_build_finalize(const FinalSeg* __restrict__ segs, int64_t nseg
   for (int j = 0; j < 6; ++j) cv[j] = (double)(long long)src[3 + j] * inv / sg.cov_scale;
   float4* o = sg.vox + 3 * v;
   o[0] = make_float4((float)m[0], (float)m[1], (float)m[2], (float)cv[0]);
-  o[1] = make_float4((float)cv[1], (float)cv[2], (float)cv[3], (float)cv[4]);
+  // record layout {C.xy, C.yy, C.xz, C.yz}: pairs (xy, yy), (xz, yz) match the
+  // packed-fp32 column pairs of R C R^T in the linearize kernel
+  o[1] = make_float4((float)cv[1], (float)cv[3], (float)cv[2], (float)cv[4]);
   o[2] = make_float4((float)cv[5], __int_as_float((int)src[9]), 0.f, 0.f);
   uint64_t key = sg.keys_by_idx[v];
   sg.keys_out[v] = key;

@@ -92,3 +92,46 @@ __device__ inline int64_t owner_of_tile(const int32_t* tile_start, int64_t num_f
 }
 
 }  // namespace gvox
+
+// ---------------------------------------------------------------------------
+// Packed fp32 pairs (sm_100a FFMA2 / FADD2 / FMUL2 via PTX f32x2).  A pair is
+// held in one 64-bit register; ptxas folds scalar broadcasts (.F32), half
+// swaps (.LO_HI) and negations into the packed instruction's operands.
+// Round-to-nearest, no contraction beyond the explicit fma.
+// ---------------------------------------------------------------------------
+namespace gvox {
+typedef unsigned long long f2_t;
+
+__device__ __forceinline__ f2_t pk(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f2_t bc(float a) { return pk(a, a); }
+__device__ __forceinline__ float lo(f2_t v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float hi(f2_t v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ f2_t swp(f2_t v) { return pk(hi(v), lo(v)); }
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+  f2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
+  f2_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
+  f2_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+}  // namespace gvox

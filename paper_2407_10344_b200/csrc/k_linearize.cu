@@ -37,7 +37,20 @@ namespace gvox {
 
 namespace {
 
-constexpr int kThreads = 256;
+// Tuning knobs (compile-time; defaults are the measured best on B200)
+#ifndef GVOX_LIN_THREADS
+#define GVOX_LIN_THREADS 256
+#endif
+#ifndef GVOX_LIN_MINB
+#define GVOX_LIN_MINB 2
+#endif
+#ifndef GVOX_LIN_PREFETCH
+#define GVOX_LIN_PREFETCH 1
+#endif
+#ifndef GVOX_LIN_G
+#define GVOX_LIN_G 4
+#endif
+constexpr int kThreads = GVOX_LIN_THREADS;
 constexpr int kWarps = kThreads / 32;
 
 struct FactorShared {
@@ -63,7 +76,7 @@ __global__ void k_tile_map(const int32_t* __restrict__ tile_start, int64_t num_f
 }
 
 template <int MAXL, bool ALL_DENSE>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     k_linearize(const CloudDev* const* __restrict__ clouds, const MapDev* const* __restrict__ maps,
                 const FactorDev* __restrict__ factors, const int32_t* __restrict__ tile_start,
                 const int32_t* __restrict__ tile_factor, int tile_pts,
@@ -124,9 +137,18 @@ __global__ void __launch_bounds__(kThreads, 2)
   const float4* __restrict__ Bp = sh.B;
   const float4* __restrict__ Np = sh.N;
 
-  float acc[kNumTerms];
-#pragma unroll
-  for (int j = 0; j < kNumTerms; ++j) acc[j] = 0.f;
+  // accumulators (fp32 per thread; see the term map at the tile reduction)
+  f2_t accA = 0, accC = 0;            // sum (o00, o01), sum (o02, o12)
+  float acc_o11 = 0.f, acc_o22 = 0.f;
+  f2_t accW0 = 0, accW1 = 0, accW2 = 0;  // sum (W0j, W1j), j = 0, 1, 2
+  float accW20 = 0.f, accW21 = 0.f, accW22 = 0.f;
+  float h00 = 0.f, h01 = 0.f, h02 = 0.f, h11 = 0.f, h12 = 0.f, h22 = 0.f;  // sum -[q]x W
+  f2_t accX = 0, accY = 0;  // sum qz (gx, gy), sum gz (qy, qx)
+  float acc_rz = 0.f;
+  f2_t accG = 0;  // sum (gx, gy)
+  float acc_gz = 0.f;
+  f2_t accE = 0;  // sum (dx gx, dy gy)
+  float acc_ez = 0.f;
   int inl[MAXL];
 #pragma unroll
   for (int l = 0; l < MAXL; ++l) inl[l] = 0;
@@ -134,19 +156,25 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   // software pipeline: the next point's 48 B source record is in flight while
   // the current one is processed
+#if GVOX_LIN_PREFETCH
   float4 na, nb, nc;
   if (begin + tid < end) {
     na = __ldg(Ap + begin + tid);
     nb = __ldg(Bp + begin + tid);
     nc = __ldg(Np + begin + tid);
   }
+#endif
   for (int64_t k = begin + tid; k < end; k += kThreads) {
+#if GVOX_LIN_PREFETCH
     const float4 a = na, b = nb, c = nc;
     if (k + kThreads < end) {
       na = __ldg(Ap + k + kThreads);
       nb = __ldg(Bp + k + kThreads);
       nc = __ldg(Np + k + kThreads);
     }
+#else
+    const float4 a = __ldg(Ap + k), b = __ldg(Bp + k), c = __ldg(Np + k);
+#endif
     const double mx = a.x, my = a.y, mz = a.z;
     if (validate) {
       // discard if (mu - T_i^-1 t_j) . n > 0; zero normal = no test (Q7)
@@ -162,23 +190,25 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
-    // q = T_ij mu in fp64, pinned order (Q10)
+    // q = T_ij mu in fp64, pinned order (Q10); level-0 key floor(q / r0)
+    // (saturating: a saturated coordinate misses every grid / fails key_in_range)
     const double qx = __fma_rn(sh.R[0], mx, __fma_rn(sh.R[1], my, __fma_rn(sh.R[2], mz, sh.t[0])));
     const double qy = __fma_rn(sh.R[3], mx, __fma_rn(sh.R[4], my, __fma_rn(sh.R[5], mz, sh.t[1])));
     const double qz = __fma_rn(sh.R[6], mx, __fma_rn(sh.R[7], my, __fma_rn(sh.R[8], mz, sh.t[2])));
-    const int32_t k0x = clamp_coord(voxel_coord0(qx, r0, inv_r0, dyadic));
-    const int32_t k0y = clamp_coord(voxel_coord0(qy, r0, inv_r0, dyadic));
-    const int32_t k0z = clamp_coord(voxel_coord0(qz, r0, inv_r0, dyadic));
-
+    const int32_t k0x = voxel_coord0(qx, r0, inv_r0, dyadic);
+    const int32_t k0y = voxel_coord0(qy, r0, inv_r0, dyadic);
+    const int32_t k0z = voxel_coord0(qz, r0, inv_r0, dyadic);
     const float fqx = (float)qx, fqy = (float)qy, fqz = (float)qz;
-    // position inside the level-0 voxel (exact k0 * r0 for dyadic r0)
-    const float fx = (float)(qx - (double)k0x * r0);
-    const float fy = (float)(qy - (double)k0y * r0);
-    const float fz = (float)(qz - (double)k0z * r0);
+    const f2_t Qyx = pk(fqy, fqx);
+    // level-0 residual base: centre_0 - q = r0/2 - (q - k0 r0)
+    const float ex = 0.5f * r0f - (float)(qx - (double)k0x * r0);
+    const float ey = 0.5f * r0f - (float)(qy - (double)k0y * r0);
+    const float ez = 0.5f * r0f - (float)(qz - (double)k0z * r0);
     bool have_rcr = false;
-    float s00 = 0.f, s01 = 0.f, s02 = 0.f, s11 = 0.f, s12 = 0.f, s22 = 0.f;
+    f2_t Sp1 = 0, Sp2 = 0;  // (s01, s11), (s02, s12)
+    float s00 = 0.f, s22 = 0.f;
     // levels are processed in groups of G (all loads of a group in flight together)
-    constexpr int G = MAXL < 4 ? MAXL : 4;
+    constexpr int G = MAXL < GVOX_LIN_G ? MAXL : GVOX_LIN_G;
 #pragma unroll
     for (int lb = 0; lb < MAXL; lb += G) {
       if (lb >= L) break;
@@ -214,100 +244,133 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
 
-      // R C R^T in fp32 (symmetric), once per point, overlapping the gathers
+      // R C R^T (symmetric) once per point, in packed pairs over rows 0/1,
+      // overlapping the gathers.  M = R C column by column, S = M R^T.
       if (!have_rcr) {
         have_rcr = true;
         const float* R = sh.Rf;
-        const float m00 = R[0] * a.w + R[1] * b.x + R[2] * b.y;
-        const float m01 = R[0] * b.x + R[1] * b.z + R[2] * b.w;
-        const float m02 = R[0] * b.y + R[1] * b.w + R[2] * c.x;
-        const float m10 = R[3] * a.w + R[4] * b.x + R[5] * b.y;
-        const float m11 = R[3] * b.x + R[4] * b.z + R[5] * b.w;
-        const float m12 = R[3] * b.y + R[4] * b.w + R[5] * c.x;
-        const float m20 = R[6] * a.w + R[7] * b.x + R[8] * b.y;
-        const float m21 = R[6] * b.x + R[7] * b.z + R[8] * b.w;
-        const float m22 = R[6] * b.y + R[7] * b.w + R[8] * c.x;
-        s00 = m00 * R[0] + m01 * R[1] + m02 * R[2];
-        s01 = m00 * R[3] + m01 * R[4] + m02 * R[5];
-        s02 = m00 * R[6] + m01 * R[7] + m02 * R[8];
-        s11 = m10 * R[3] + m11 * R[4] + m12 * R[5];
-        s12 = m10 * R[6] + m11 * R[7] + m12 * R[8];
-        s22 = m20 * R[6] + m21 * R[7] + m22 * R[8];
+        const float c00 = a.w, c01 = b.x, c02 = b.y, c11 = b.z, c12 = b.w, c22 = c.x;
+        const f2_t Rc0 = pk(R[0], R[3]), Rc1 = pk(R[1], R[4]), Rc2 = pk(R[2], R[5]);
+        const f2_t Mp0 = fma2(Rc2, bc(c02), fma2(Rc1, bc(c01), mul2(Rc0, bc(c00))));
+        const f2_t Mp1 = fma2(Rc2, bc(c12), fma2(Rc1, bc(c11), mul2(Rc0, bc(c01))));
+        const f2_t Mp2 = fma2(Rc2, bc(c22), fma2(Rc1, bc(c12), mul2(Rc0, bc(c02))));
+        const float M20 = fmaf(R[8], c02, fmaf(R[7], c01, R[6] * c00));
+        const float M21 = fmaf(R[8], c12, fmaf(R[7], c11, R[6] * c01));
+        const float M22 = fmaf(R[8], c22, fmaf(R[7], c12, R[6] * c02));
+        const f2_t Sp0 = fma2(Mp2, bc(R[2]), fma2(Mp1, bc(R[1]), mul2(Mp0, bc(R[0]))));  // (s00, s10)
+        Sp1 = fma2(Mp2, bc(R[5]), fma2(Mp1, bc(R[4]), mul2(Mp0, bc(R[3]))));             // (s01, s11)
+        Sp2 = fma2(Mp2, bc(R[8]), fma2(Mp1, bc(R[7]), mul2(Mp0, bc(R[6]))));             // (s02, s12)
+        s00 = lo(Sp0);
+        s22 = fmaf(M22, R[8], fmaf(M21, R[7], M20 * R[6]));
       }
 
-      // stage 3: per-level algebra
+      // stage 3: per-level algebra (packed pairs where the data pair up)
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         if (vid[j] < 0) continue;
         const int l = lb + j;
-        // fused covariance (Eq.3) and its inverse by the symmetric adjugate
-        const float ca = v0[j].w + s00, cb = v1[j].x + s01, cc = v1[j].y + s02;
-        const float cd = v1[j].z + s11, ce = v1[j].w + s12, cf = v2[j] + s22;
-        const float i00 = cd * cf - ce * ce;
-        const float i01 = cc * ce - cb * cf;
-        const float i02 = cb * ce - cc * cd;
-        const float i11 = ca * cf - cc * cc;
-        const float i12 = cb * cc - ca * ce;
-        const float i22 = ca * cd - cb * cb;
-        const float det = ca * i00 + cb * i01 + cc * i02;
+        // fused covariance (Eq.3): record v1 = {C.xy, C.yy, C.xz, C.yz}
+        const f2_t P = add2(pk(v1[j].x, v1[j].y), Sp1);  // (cb, cd) = (xy, yy)
+        const f2_t Q = add2(pk(v1[j].z, v1[j].w), Sp2);  // (cc, ce) = (xz, yz)
+        const float ca = v0[j].w + s00, cf = v2[j] + s22;
+        const float cb = lo(P), cd = hi(P), cc = lo(Q), ce = hi(Q);
+        // inverse by the symmetric adjugate
+        const float i00 = fmaf(cd, cf, -ce * ce);
+        const float i01 = fmaf(cc, ce, -cb * cf);
+        const float i02 = fmaf(cb, ce, -cc * cd);
+        const float i11 = fmaf(ca, cf, -cc * cc);
+        const float i12 = fmaf(cb, cc, -ca * ce);
+        const float i22 = fmaf(ca, cd, -cb * cb);
+        const float det = fmaf(ca, i00, fmaf(cb, i01, cc * i02));
         // Q16: a fused covariance that is not positive definite contributes nothing
         const bool ok = det > 0.f && det < INFINITY;
         const float id = ok ? __fdividef(1.0f, det) : 0.f;
         n_degenerate += !ok;
         inl[l] += ok;
-        const float o00 = i00 * id, o01 = i01 * id, o02 = i02 * id;
-        const float o11 = i11 * id, o12 = i12 * id, o22 = i22 * id;
+        const f2_t Om_a = mul2(pk(i00, i01), bc(id));  // (o00, o01) = column 0, rows 0-1
+        const f2_t Om_b = mul2(pk(i01, i11), bc(id));  // (o01, o11) = column 1, rows 0-1
+        const f2_t Om_c = mul2(pk(i02, i12), bc(id));  // (o02, o12) = column 2, rows 0-1
+        const float o22 = i22 * id;
+        const float o02 = lo(Om_c), o12 = hi(Om_c);
 
-        // d = mu~ - q = (centre_l - q) + offset (Q12).  With f = q - k0 r0 (the
-        // point's position inside its level-0 voxel, fp64 -> fp32 once per
-        // point) and k_l = k0 >> l:  centre_l - q = r0 (2^(l-1) - (k0 & (2^l - 1))) - f.
-        const int mlo = (1 << l) - 1;
-        const float hl = 0.5f * (float)(1 << l);
-        const float dx = r0f * (hl - (float)(k0x & mlo)) - fx + v0[j].x;
-        const float dy = r0f * (hl - (float)(k0y & mlo)) - fy + v0[j].y;
-        const float dz = r0f * (hl - (float)(k0z & mlo)) - fz + v0[j].z;
+        // d = mu~ - q = (centre_l - q) + offset (Q12): with k_l = k0 >> l,
+        // centre_l - q = (centre_0 - q) + r0 (2^(l-1) - 1/2 - (k0 & (2^l - 1))).
+        float bx = ex, by = ey, bz = ez;
+        if (l > 0) {
+          const int mlo = (1 << l) - 1;
+          const float sh_l = 0.5f * (float)(1 << l) - 0.5f;
+          bx = fmaf(r0f, sh_l - (float)(k0x & mlo), ex);
+          by = fmaf(r0f, sh_l - (float)(k0y & mlo), ey);
+          bz = fmaf(r0f, sh_l - (float)(k0z & mlo), ez);
+        }
+        const f2_t D = add2(pk(bx, by), pk(v0[j].x, v0[j].y));  // (dx, dy)
+        const float dz = bz + v0[j].z;
+        const float dx = lo(D), dy = hi(D);
 
         // g = Omega d, e = d^T g
-        const float gx = o00 * dx + o01 * dy + o02 * dz;
-        const float gy = o01 * dx + o11 * dy + o12 * dz;
-        const float gz = o02 * dx + o12 * dy + o22 * dz;
-        acc[27] += dx * gx + dy * gy + dz * gz;
+        const f2_t Gp = fma2(Om_c, bc(dz), fma2(Om_b, bc(dy), mul2(Om_a, bc(dx))));  // (gx, gy)
+        const float gz = fmaf(o02, dx, fmaf(o12, dy, o22 * dz));
+        accE = fma2(D, Gp, accE);
+        acc_ez = fmaf(dz, gz, acc_ez);
         if (error_only) continue;
 
-        acc[24] += gx;
-        acc[25] += gy;
-        acc[26] += gz;
-        // b_rot = q x g
-        acc[21] += fqy * gz - fqz * gy;
-        acc[22] += fqz * gx - fqx * gz;
-        acc[23] += fqx * gy - fqy * gx;
+        accG = add2(accG, Gp);
+        acc_gz += gz;
+        // b_rot = q x g:  (qy gz - qz gy, qz gx - qx gz), qx gy - qy gx
+        const float gx = lo(Gp), gy = hi(Gp);
+        // accumulated as X = sum qz (gx, gy), Y = sum gz (qy, qx):
+        // brx = Y.x - X.y, bry = X.x - Y.y (combined at the tile reduction)
+        accX = fma2(bc(fqz), Gp, accX);
+        accY = fma2(bc(gz), Qyx, accY);
+        acc_rz = fmaf(fqx, gy, fmaf(-fqy, gx, acc_rz));
         // sum Omega
-        acc[0] += o00; acc[1] += o01; acc[2] += o02;
-        acc[3] += o11; acc[4] += o12; acc[5] += o22;
-        // W = Omega [q]x
-        const float w00 = o01 * fqz - o02 * fqy, w01 = o02 * fqx - o00 * fqz, w02 = o00 * fqy - o01 * fqx;
-        const float w10 = o11 * fqz - o12 * fqy, w11 = o12 * fqx - o01 * fqz, w12 = o01 * fqy - o11 * fqx;
-        const float w20 = o12 * fqz - o22 * fqy, w21 = o22 * fqx - o02 * fqz, w22 = o02 * fqy - o12 * fqx;
-        acc[6] += w00; acc[7] += w01; acc[8] += w02;
-        acc[9] += w10; acc[10] += w11; acc[11] += w12;
-        acc[12] += w20; acc[13] += w21; acc[14] += w22;
-        // H_rr = -[q]x W (upper): rows of -[q]x are (0, qz, -qy), (-qz, 0, qx), (qy, -qx, 0)
-        acc[15] += fqz * w10 - fqy * w20;
-        acc[16] += fqz * w11 - fqy * w21;
-        acc[17] += fqz * w12 - fqy * w22;
-        acc[18] += fqx * w21 - fqz * w01;
-        acc[19] += fqx * w22 - fqz * w02;
-        acc[20] += fqy * w02 - fqx * w12;
+        accA = add2(accA, Om_a);
+        accC = add2(accC, Om_c);
+        acc_o11 += hi(Om_b);
+        acc_o22 += o22;
+        // W = Omega [q]x by columns: W[:,0] = qz Om[:,1] - qy Om[:,2],
+        // W[:,1] = qx Om[:,2] - qz Om[:,0], W[:,2] = qy Om[:,0] - qx Om[:,1]
+        const f2_t Wc0 = fma2(bc(-fqy), Om_c, mul2(bc(fqz), Om_b));
+        const f2_t Wc1 = fma2(bc(fqx), Om_c, mul2(bc(-fqz), Om_a));
+        const f2_t Wc2 = fma2(bc(-fqx), Om_b, mul2(bc(fqy), Om_a));
+        const float W20 = fmaf(fqz, o12, -fqy * o22);
+        const float W21 = fmaf(fqx, o22, -fqz * o02);
+        const float W22 = fmaf(fqy, o02, -fqx * o12);
+        accW0 = add2(accW0, Wc0);
+        accW1 = add2(accW1, Wc1);
+        accW2 = add2(accW2, Wc2);
+        accW20 += W20;
+        accW21 += W21;
+        accW22 += W22;
+        // H_rr = -[q]x W (upper)
+        h00 = fmaf(fqz, hi(Wc0), fmaf(-fqy, W20, h00));
+        h01 = fmaf(fqz, hi(Wc1), fmaf(-fqy, W21, h01));
+        h02 = fmaf(fqz, hi(Wc2), fmaf(-fqy, W22, h02));
+        h11 = fmaf(fqx, W21, fmaf(-fqz, lo(Wc1), h11));
+        h12 = fmaf(fqx, W22, fmaf(-fqz, lo(Wc2), h12));
+        h22 = fmaf(fqy, lo(Wc2), fmaf(-fqx, hi(Wc2), h22));
       }
     }
   }
 
-  // ---- tile reduction: fp64 warp shuffles, then fixed-order across warps
+  // ---- tile reduction: fp64 warp shuffles, then fixed-order across warps.
+  // Internal term order t[0..27] (see the file header).
   const int lane = tid & 31, warp = tid >> 5;
+  {
+    const float W[9] = {lo(accW0), lo(accW1), lo(accW2), hi(accW0), hi(accW1), hi(accW2),
+                        accW20, accW21, accW22};
+    const double t[27] = {lo(accA), hi(accA), lo(accC), acc_o11, hi(accC), acc_o22,
+                          W[0], W[1], W[2], W[3], W[4], W[5], W[6], W[7], W[8],
+                          h00, h01, h02, h11, h12, h22,
+                          (double)lo(accY) - (double)hi(accX), (double)lo(accX) - (double)hi(accY),
+                          acc_rz, lo(accG), hi(accG), acc_gz};
 #pragma unroll
-  for (int j = 0; j < kNumTerms; ++j) {
-    double s = warp_sum((double)acc[j]);
-    if (lane == 0) red[warp][j] = s;
+    for (int j = 0; j < 27; ++j) {
+      double s = warp_sum(t[j]);
+      if (lane == 0) red[warp][j] = s;
+    }
+    double e = warp_sum((double)lo(accE) + (double)hi(accE) + (double)acc_ez);
+    if (lane == 0) red[warp][27] = e;
   }
 #pragma unroll
   for (int l = 0; l < GVOX_MAX_LEVELS; ++l) {

@@ -19,6 +19,7 @@ namespace {
 
 constexpr int kThreads = 256;
 
+template <bool ALL_DENSE>
 __global__ void __launch_bounds__(kThreads)
     k_overlap(const CloudDev* const* __restrict__ clouds, const MapDev* const* __restrict__ maps,
               const PairDev* __restrict__ pairs, const int32_t* __restrict__ tile_start,
@@ -65,10 +66,10 @@ __global__ void __launch_bounds__(kThreads)
     const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
     const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
     const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
-    const int32_t kx = clamp_coord(voxel_coord0(qx, lv.r, lv.inv_r, dyadic));
-    const int32_t ky = clamp_coord(voxel_coord0(qy, lv.r, lv.inv_r, dyadic));
-    const int32_t kz = clamp_coord(voxel_coord0(qz, lv.r, lv.inv_r, dyadic));
-    cnt += lookup_level(lv, kx, ky, kz) >= 0;
+    const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
+    const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
+    const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
+    cnt += lookup_level<ALL_DENSE>(lv, kx, ky, kz) >= 0;
   }
   // warp counts, then one atomic per CTA
 #pragma unroll
@@ -87,10 +88,14 @@ __global__ void __launch_bounds__(kThreads)
 void launch_overlap(const CloudDev* const* clouds, const MapDev* const* maps, const PairDev* pairs,
                     const int32_t* tile_start, int64_t num_pairs, int64_t num_tiles, int tile_pts,
                     const double* poses, int level, int32_t* tile_pair, int32_t* counts,
-                    cudaStream_t stream) {
+                    bool all_dense, cudaStream_t stream) {
   if (num_tiles <= 0) return;
-  k_overlap<<<(unsigned)num_tiles, kThreads, 0, stream>>>(clouds, maps, pairs, tile_start,
-                                                          tile_pair, tile_pts, poses, level, counts);
+  if (all_dense)
+    k_overlap<true><<<(unsigned)num_tiles, kThreads, 0, stream>>>(
+        clouds, maps, pairs, tile_start, tile_pair, tile_pts, poses, level, counts);
+  else
+    k_overlap<false><<<(unsigned)num_tiles, kThreads, 0, stream>>>(
+        clouds, maps, pairs, tile_start, tile_pair, tile_pts, poses, level, counts);
   note_launch();
 }
 

@@ -1,0 +1,53 @@
+"""Build libgvox kernel variants (compile-time knobs) and time each with
+bench.py --linearize-only on the GPU box.  Usage (on the box):
+  python tools/variants.py build   # here, CPU: compiles variants into build/variants/
+  python tools/variants.py run     # on the GPU: times each variant
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "paper_2407_10344_b200", "build", "variants")
+VARIANTS = {
+    "base": [],
+    "nopf": ["GVOX_LIN_PREFETCH=0"],
+    "g1": ["GVOX_LIN_G=1"],
+    "g1_nopf_b3": ["GVOX_LIN_G=1", "GVOX_LIN_PREFETCH=0", "GVOX_LIN_MINB=3"],
+    "nopf_b3": ["GVOX_LIN_PREFETCH=0", "GVOX_LIN_MINB=3"],
+    "t128_b5": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=5", "GVOX_LIN_PREFETCH=0"],
+    "t128_b4": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=4"],
+}
+
+
+def build(names):
+    sys.path.insert(0, ROOT)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("b", os.path.join(ROOT, "paper_2407_10344_b200", "_build.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    os.makedirs(OUT, exist_ok=True)
+    for n in names:
+        m.build(out=os.path.join(OUT, f"libgvox_{n}.so"), defines=VARIANTS[n], verbose=False)
+        print("built", n, flush=True)
+
+
+def run(names, extra):
+    res = {}
+    for n in names:
+        env = dict(os.environ, GVOX_LIB=os.path.join(OUT, f"libgvox_{n}.so"))
+        p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--linearize-only", "--no-e2e",
+                            "--no-cpu-baseline", "--steps", "6", *extra], env=env, capture_output=True, text=True)
+        line = [l for l in p.stderr.splitlines() if "linearize-only" in l]
+        res[n] = line[-1] if line else p.stderr[-500:]
+        print(n, res[n], flush=True)
+    return res
+
+
+if __name__ == "__main__":
+    names = sys.argv[2].split(",") if len(sys.argv) > 2 and sys.argv[2] else list(VARIANTS)
+    if sys.argv[1] == "build":
+        build(names)
+    else:
+        run(names, sys.argv[3:])
