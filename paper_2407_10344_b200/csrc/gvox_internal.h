@@ -134,9 +134,9 @@ struct BuildSeg {
   // phase 1 records, per (point, level), the temp-table SLOT of its key;
   // phase 2 reads the voxel index from that slot (all indices assigned by then).
 };
-void launch_build_insert(const BuildSeg* segs_dev, int64_t num_segs, const int64_t* seg_point_start,
-                         int64_t total_points, int levels, double r0, int dyadic, int32_t* pslot,
-                         int32_t* err, cudaStream_t stream);
+void launch_build_insert(const BuildSeg* segs_dev, int64_t num_segs, int64_t max_seg_points,
+                         int levels, double r0, int dyadic, int32_t* pslot, int32_t* err,
+                         cudaStream_t stream);
 
 // phase 2: fixed-point accumulation of (sum offsets, sum cov, count) per voxel.
 struct AccumSeg {
@@ -150,9 +150,8 @@ struct AccumSeg {
   double cov_scale;                     // 2^(F - e_c), 2^e_c >= max |C_ij| of the cloud
 };
 void launch_build_accum(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int64_t num_segs,
-                        const int64_t* seg_point_start, int64_t total_points, int levels,
-                        double r0, int dyadic, const int32_t* pslot, unsigned long long* acc,
-                        cudaStream_t stream);
+                        int64_t max_seg_points, int levels, double r0, int dyadic,
+                        const int32_t* pslot, unsigned long long* acc, cudaStream_t stream);
 
 // phase 3: per voxel, finalize the record and insert into the final table.
 struct FinalSeg {
@@ -172,8 +171,7 @@ struct FinalSeg {
   float4* vox;              // [3 * nvox]
   uint64_t* keys_out;       // [nvox]
 };
-void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs,
-                           const int64_t* seg_vox_start, int64_t total_voxels,
+void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs, int64_t max_seg_voxels,
                            const unsigned long long* acc, cudaStream_t stream);
 
 void launch_fill_u64(uint64_t* p, uint64_t value, int64_t count, cudaStream_t stream);

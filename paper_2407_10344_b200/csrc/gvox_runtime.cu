@@ -471,6 +471,8 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   std::vector<int64_t> seg_start(count + 1, 0);
   for (int64_t s = 0; s < count; ++s) seg_start[s + 1] = seg_start[s] + clouds[s]->n;
   const int64_t total = seg_start[count];
+  int64_t max_pts = 0;
+  for (int64_t s = 0; s < count; ++s) max_pts = std::max<int64_t>(max_pts, clouds[s]->n);
   std::vector<uint64_t> tcap(count);
   Layout lay;
   std::vector<size_t> o_tmp(count), o_keys(count);
@@ -517,8 +519,8 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
                      ctx->stream));
   {
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
-    launch_build_insert((const BuildSeg*)(b0 + o_bseg), count, (const int64_t*)(b0 + o_start),
-                        total, L, r0, dyadic, (int32_t*)(b0 + o_pslot), d_err, ctx->stream);
+    launch_build_insert((const BuildSeg*)(b0 + o_bseg), count, max_pts, L, r0, dyadic,
+                        (int32_t*)(b0 + o_pslot), d_err, ctx->stream);
   }
   CK_LAUNCH("voxelmap insert");
   std::vector<int32_t> hcnt((size_t)count * L + 1);
@@ -682,15 +684,15 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   {
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
     launch_build_accum((const BuildSeg*)(b0 + o_bseg), (const AccumSeg*)(b0 + o_aseg), count,
-                       (const int64_t*)(b0 + o_start), total, L, r0, dyadic,
-                       (const int32_t*)(b0 + o_pslot), (unsigned long long*)(b1 + o_acc),
-                       ctx->stream);
+                       max_pts, L, r0, dyadic, (const int32_t*)(b0 + o_pslot),
+                       (unsigned long long*)(b1 + o_acc), ctx->stream);
   }
   CK_LAUNCH("voxelmap accumulate");
   {
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
-    launch_build_finalize((const FinalSeg*)(b1 + o_fseg), count * L,
-                          (const int64_t*)(b1 + o_vstart), total_vox,
+    int64_t max_vox = 0;
+    for (int64_t q = 0; q < count * L; ++q) max_vox = std::max<int64_t>(max_vox, hcnt[q]);
+    launch_build_finalize((const FinalSeg*)(b1 + o_fseg), count * L, max_vox,
                           (const unsigned long long*)(b1 + o_acc), ctx->stream);
   }
   CK_LAUNCH("voxelmap finalize");
@@ -737,7 +739,10 @@ gvox_status gvox_create_voxelmaps(gvox_ctx* ctx, const gvox_cloud* const* clouds
   int64_t s0 = 0;
   while (s0 < count) {
     int64_t s1 = s0, pts = 0;
-    while (s1 < count && (s1 == s0 || pts + clouds[s1]->n <= kBuildChunkPoints)) pts += clouds[s1++]->n;
+    // a chunk: <= kBuildChunkPoints points and <= 65535 / levels maps (grid rows)
+    while (s1 < count && (s1 == s0 || (pts + clouds[s1]->n <= kBuildChunkPoints &&
+                                       (s1 - s0 + 1) * levels <= 65535)))
+      pts += clouds[s1++]->n;
     gvox_status st = build_chunk(ctx, clouds + s0, s1 - s0, r0, levels, maps_out + s0);
     if (st) {
       for (int64_t s = 0; s < s0; ++s) {
@@ -877,7 +882,7 @@ gvox_status gvox_overlap(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t
     total_pts += clouds[pairs[p].source_cloud]->n;
     all_dense = all_dense && maps[pairs[p].target_map]->desc.lv[level].dense;
   }
-  int ppt = 1;
+  int ppt = 4;  // the kernel handles 4 points per thread per iteration
   while (ppt < 32 && total_pts / ((int64_t)256 * ppt * 2) >= 148 * 8 * 8) ppt *= 2;
   const int tile_pts = 256 * ppt;
   std::vector<int32_t> tstart(num_pairs + 1, 0);

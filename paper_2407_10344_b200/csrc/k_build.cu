@@ -80,32 +80,22 @@ __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restri
   }
 }
 
-// segment (cloud) of a global point index: largest s with start[s] <= i
-__device__ inline int64_t seg_of(const int64_t* start, int64_t nseg, int64_t i) {
-  int64_t lo = 0, hi = nseg;
-  while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (__ldg(start + mid) <= i) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
 // Both passes aggregate within a warp: lanes holding the same (map, key) --
 // frequent, since consecutive points are spatially coherent -- are grouped with
 // __match_any_sync and only the group leader touches the table / issues the
 // atomics.  Every lane runs every level (inactive lanes carry unique dummy
 // keys) so the warp stays converged for the *_sync collectives.
 
-__global__ void k_build_insert(const BuildSeg* __restrict__ segs, int64_t nseg,
-                               const int64_t* __restrict__ seg_start, int64_t total, int levels,
-                               double r0, double inv_r0, int dyadic, int32_t* __restrict__ pslot,
+// Grids are 2D: blockIdx.y = segment (cloud), blockIdx.x * blockDim.x +
+// threadIdx.x = point within it, so a block never straddles two maps.
+__global__ void k_build_insert(const BuildSeg* __restrict__ segs, int levels, double r0,
+                               double inv_r0, int dyadic, int32_t* __restrict__ pslot,
                                int32_t* __restrict__ err) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  const bool valid = i < total;
-  const int64_t s = valid ? seg_of(seg_start, nseg, i) : 0;
-  const BuildSeg& sg = segs[s];
-  const int64_t k = valid ? i - seg_start[s] : 0;
+  const BuildSeg& sg = segs[blockIdx.y];
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = k < sg.n;
+  if (__all_sync(0xffffffffu, !valid)) return;
   int32_t k0x = 0, k0y = 0, k0z = 0;
   if (valid) {
     const float4 a = __ldg(sg.A + k);
@@ -120,30 +110,40 @@ __global__ void k_build_insert(const BuildSeg* __restrict__ segs, int64_t nseg,
     if (valid && !inr) atomicOr(err, 1);
     // real keys are < 2^63; dummies (~0 - lane) are distinct and never inserted
     const uint64_t key = inr ? pack_key(kx, ky, kz) : ~0ull - (uint64_t)lane;
-    const unsigned grp = __match_any_sync(0xffffffffu, key) &
-                         __match_any_sync(0xffffffffu, (unsigned long long)s);
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
     const int leader = __ffs(grp) - 1;
+    // leaders claim their key's slot: CAS first (one L2 round trip when the
+    // slot is empty or already holds the key), linear probing on collision
     int32_t h_out = -1;
+    bool is_new = false;
     if (lane == leader && inr) {
       ulonglong2* slots = sg.tmp_slots[l];
       uint64_t h = hash_slot(key, sg.tmp_shift);
       for (;;) {
         unsigned long long* kp = reinterpret_cast<unsigned long long*>(&slots[h].x);
-        unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(kp);
-        if (cur == key) break;
-        if (cur == kEmptyKey) {
-          unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
-          if (prev == kEmptyKey) {
-            int32_t idx = atomicAdd(sg.counter + l, 1);
-            slots[h].y = (unsigned long long)(uint32_t)idx | 0xFFFFFFFF00000000ull;
-            sg.keys_by_idx[l][idx] = key;
-            break;
-          }
-          if (prev == key) break;
+        const unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
+        if (prev == kEmptyKey) {
+          is_new = true;
+          break;
         }
+        if (prev == key) break;
         h = (h + 1) & sg.tmp_mask;
       }
       h_out = (int32_t)h;
+    }
+    // new voxels take consecutive indices: one atomicAdd per warp (all lanes of
+    // a block belong to the same map and level)
+    const unsigned new_mask = __ballot_sync(0xffffffffu, is_new);
+    if (new_mask) {
+      int32_t base = 0;
+      const int first = __ffs(new_mask) - 1;
+      if (lane == first) base = atomicAdd(sg.counter + l, __popc(new_mask));
+      base = __shfl_sync(0xffffffffu, base, first);
+      if (is_new) {
+        const int32_t idx = base + __popc(new_mask & ((1u << lane) - 1u));
+        sg.tmp_slots[l][h_out].y = (unsigned long long)(uint32_t)idx | 0xFFFFFFFF00000000ull;
+        sg.keys_by_idx[l][idx] = key;
+      }
     }
     h_out = __shfl_sync(0xffffffffu, h_out, leader);
     if (valid) pslot[sg.pl_offset + k * levels + l] = inr ? h_out : -1;
@@ -164,17 +164,15 @@ __device__ inline unsigned long long group_sum_u64(unsigned grp, unsigned long l
 }
 
 __global__ void k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg* __restrict__ segs,
-                              int64_t nseg, const int64_t* __restrict__ seg_start, int64_t total,
                               int levels, double r0, double inv_r0, int dyadic,
                               const int32_t* __restrict__ pslot,
                               unsigned long long* __restrict__ acc) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  const bool valid = i < total;
-  const int64_t s = valid ? seg_of(seg_start, nseg, i) : 0;
-  const AccumSeg& sg = segs[s];
-  const BuildSeg& bs = bsegs[s];
-  const int64_t k = valid ? i - seg_start[s] : 0;
+  const AccumSeg& sg = segs[blockIdx.y];
+  const BuildSeg& bs = bsegs[blockIdx.y];
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = k < sg.n;
+  if (__all_sync(0xffffffffu, !valid)) return;
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, c = a;
   if (valid) {
     a = __ldg(sg.A + k);
@@ -189,8 +187,7 @@ __global__ void k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg
   for (int l = 0; l < levels; ++l) {
     const int32_t sl = valid ? pslot[sg.pl_offset + k * levels + l] : -1;
     const int32_t idx = sl >= 0 ? (int32_t)(uint32_t)bs.tmp_slots[l][sl].y : -1 - lane;
-    const unsigned grp = __match_any_sync(0xffffffffu, idx) &
-                         __match_any_sync(0xffffffffu, (unsigned long long)s);
+    const unsigned grp = __match_any_sync(0xffffffffu, idx);
     const int leader = __ffs(grp) - 1;
     unsigned long long v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (sl >= 0) {
@@ -215,14 +212,11 @@ __global__ void k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg
   }
 }
 
-__global__ void k_build_finalize(const FinalSeg* __restrict__ segs, int64_t nseg,
-                                 const int64_t* __restrict__ seg_vox_start, int64_t total,
+__global__ void k_build_finalize(const FinalSeg* __restrict__ segs,
                                  const unsigned long long* __restrict__ acc) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  int64_t s = seg_of(seg_vox_start, nseg, i);
-  const FinalSeg& sg = segs[s];
-  int64_t v = i - seg_vox_start[s];
+  const FinalSeg& sg = segs[blockIdx.y];  // one (segment, level) per grid row
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= sg.nvox) return;
   const unsigned long long* src = acc + (sg.acc_offset + v) * 10;
   double cnt = (double)(long long)src[9];
   double inv = 1.0 / cnt;
@@ -287,32 +281,30 @@ void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int6
   note_launch();
 }
 
-void launch_build_insert(const BuildSeg* segs_dev, int64_t num_segs, const int64_t* seg_point_start,
-                         int64_t total_points, int levels, double r0, int dyadic, int32_t* pslot,
-                         int32_t* err, cudaStream_t stream) {
-  if (total_points <= 0) return;
-  k_build_insert<<<grid_for(total_points, 256), 256, 0, stream>>>(
-      segs_dev, num_segs, seg_point_start, total_points, levels, r0, 1.0 / r0, dyadic, pslot, err);
+void launch_build_insert(const BuildSeg* segs_dev, int64_t num_segs, int64_t max_seg_points,
+                         int levels, double r0, int dyadic, int32_t* pslot, int32_t* err,
+                         cudaStream_t stream) {
+  if (num_segs <= 0 || max_seg_points <= 0) return;
+  dim3 grid(grid_for(max_seg_points, 256), (unsigned)num_segs);
+  k_build_insert<<<grid, 256, 0, stream>>>(segs_dev, levels, r0, 1.0 / r0, dyadic, pslot, err);
   note_launch();
 }
 
 void launch_build_accum(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int64_t num_segs,
-                        const int64_t* seg_point_start, int64_t total_points, int levels,
-                        double r0, int dyadic, const int32_t* pslot, unsigned long long* acc,
-                        cudaStream_t stream) {
-  if (total_points <= 0) return;
-  k_build_accum<<<grid_for(total_points, 256), 256, 0, stream>>>(
-      bsegs_dev, segs_dev, num_segs, seg_point_start, total_points, levels, r0, 1.0 / r0, dyadic,
-      pslot, acc);
+                        int64_t max_seg_points, int levels, double r0, int dyadic,
+                        const int32_t* pslot, unsigned long long* acc, cudaStream_t stream) {
+  if (num_segs <= 0 || max_seg_points <= 0) return;
+  dim3 grid(grid_for(max_seg_points, 256), (unsigned)num_segs);
+  k_build_accum<<<grid, 256, 0, stream>>>(bsegs_dev, segs_dev, levels, r0, 1.0 / r0, dyadic, pslot,
+                                          acc);
   note_launch();
 }
 
-void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs,
-                           const int64_t* seg_vox_start, int64_t total_voxels,
+void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs, int64_t max_seg_voxels,
                            const unsigned long long* acc, cudaStream_t stream) {
-  if (total_voxels <= 0) return;
-  k_build_finalize<<<grid_for(total_voxels, 256), 256, 0, stream>>>(segs_dev, num_segs,
-                                                                     seg_vox_start, total_voxels, acc);
+  if (num_segs <= 0 || max_seg_voxels <= 0) return;
+  dim3 grid(grid_for(max_seg_voxels, 256), (unsigned)num_segs);
+  k_build_finalize<<<grid, 256, 0, stream>>>(segs_dev, acc);
   note_launch();
 }
 

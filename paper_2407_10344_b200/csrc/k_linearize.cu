@@ -37,12 +37,16 @@ namespace gvox {
 
 namespace {
 
-// Tuning knobs (compile-time; defaults are the measured best on B200)
+// Tuning knobs (compile-time; defaults are the measured best on B200, see
+// tools/variants.py).  Measured on C5 (r01): 128 x 4 CTAs/SM 197 ms, 256 x 2
+// 204 ms; forcing 3 CTAs of 256 (80 registers) spills, 280 ms; one level at a
+// time (G = 1) 264 ms; a cp.async two-stage pipeline through shared memory
+// (records + point data, 224 B per point slot) 328 ms at 12 warps/SM.
 #ifndef GVOX_LIN_THREADS
-#define GVOX_LIN_THREADS 256
+#define GVOX_LIN_THREADS 128
 #endif
 #ifndef GVOX_LIN_MINB
-#define GVOX_LIN_MINB 2
+#define GVOX_LIN_MINB 4
 #endif
 #ifndef GVOX_LIN_PREFETCH
 #define GVOX_LIN_PREFETCH 1
@@ -50,6 +54,7 @@ namespace {
 #ifndef GVOX_LIN_G
 #define GVOX_LIN_G 4
 #endif
+
 constexpr int kThreads = GVOX_LIN_THREADS;
 constexpr int kWarps = kThreads / 32;
 
@@ -75,6 +80,262 @@ __global__ void k_tile_map(const int32_t* __restrict__ tile_start, int64_t num_f
   for (int32_t t = tile_start[f]; t < tile_start[f + 1]; ++t) tile_factor[t] = (int32_t)f;
 }
 
+// ---------------------------------------------------------------- shared parts
+
+// Per-thread fp32 accumulators (packed pairs where the algebra pairs up).
+template <int MAXL>
+struct Acc {
+  f2_t A = 0, C = 0;            // sum (o00, o01), sum (o02, o12)
+  float o11 = 0.f, o22 = 0.f;
+  f2_t W0 = 0, W1 = 0, W2 = 0;  // sum (W0j, W1j), j = 0, 1, 2  (W = Omega [q]x)
+  float W20 = 0.f, W21 = 0.f, W22 = 0.f;
+  float h00 = 0.f, h01 = 0.f, h02 = 0.f, h11 = 0.f, h12 = 0.f, h22 = 0.f;  // sum -[q]x W
+  f2_t X = 0, Y = 0;  // sum qz (gx, gy), sum gz (qy, qx)  -> b_rot xy
+  float rz = 0.f;     // sum (q x g)_z
+  f2_t G = 0;         // sum (gx, gy)
+  float gz = 0.f;
+  f2_t E = 0;         // sum (dx gx, dy gy)
+  float ez = 0.f;
+  int inl[MAXL];
+  int n_invisible = 0, n_degenerate = 0;
+  __device__ Acc() {
+#pragma unroll
+    for (int l = 0; l < MAXL; ++l) inl[l] = 0;
+  }
+};
+
+// Per-point quantities shared by its levels.
+struct PointData {
+  float qx, qy, qz;   // T_ij mu (fp32 lever arm)
+  float ex, ey, ez;   // centre_0 - q (level-0 residual base)
+  f2_t Sp1, Sp2;      // (s01, s11), (s02, s12) of R C R^T
+  float s00, s22;
+  int32_t k0x, k0y, k0z;  // level-0 key (low bits give the level-l residual base)
+};
+
+// Stage the factor of `tile` in shared memory (pose, cloud, map levels).
+template <int MAXL>
+__device__ __forceinline__ void stage_factor(FactorShared& sh, double* pose_s,
+                                             const CloudDev* const* clouds, const MapDev* const* maps,
+                                             const FactorDev* factors, const int32_t* tile_start,
+                                             const int32_t* tile_factor, int tile_pts,
+                                             const double* poses, int64_t tile) {
+  const int tid = threadIdx.x;
+  const int32_t f = __ldg(tile_factor + tile);
+  const FactorDev fd = factors[f];
+  if (tid < 24) {
+    pose_s[tid] = __ldg(poses + 12 * (int64_t)(tid < 12 ? fd.pi : fd.pj) + (tid % 12));
+  } else if (tid == 32) {
+    const CloudDev* cd = clouds[fd.src];
+    int64_t b = (int64_t)(tile - __ldg(tile_start + f)) * tile_pts;
+    int64_t e = b + tile_pts;
+    int64_t n = cd->n;
+    sh.A = cd->A;
+    sh.B = cd->B;
+    sh.N = cd->N;
+    sh.begin = b;
+    sh.end = e < n ? e : n;
+    sh.validate = (fd.flags & GVOX_F_VALIDATE_SURFACE) && cd->has_normals;
+    sh.error_only = (fd.flags & GVOX_F_ERROR_ONLY) ? 1 : 0;
+    sh.corr_base = fd.corr_offset;
+  } else if (tid == 64) {
+    const MapDev* md = maps[fd.tgt];
+    sh.L = md->levels;
+    sh.dyadic = md->dyadic;
+    sh.r0 = md->r0;
+    sh.inv_r0 = md->inv_r0;
+  } else if (tid >= 96 && tid < 96 + MAXL) {
+    const MapDev* md = maps[fd.tgt];
+    sh.lv[tid - 96] = md->lv[tid - 96];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    relative_pose_dev(pose_s, pose_s + 12, sh.R, sh.t, sh.v);
+#pragma unroll
+    for (int j = 0; j < 9; ++j) sh.Rf[j] = (float)sh.R[j];
+  }
+  __syncthreads();
+}
+
+// P:197 visibility test: true if the point is discarded.
+__device__ __forceinline__ bool invisible(const FactorShared& sh, const float4 a, const float4 c) {
+  if (c.y == 0.f && c.z == 0.f && c.w == 0.f) return false;  // zero normal: no test (Q7)
+  const double dx = (double)a.x - sh.v[0], dy = (double)a.y - sh.v[1], dz = (double)a.z - sh.v[2];
+  const double dot = __fma_rn(dx, (double)c.y, __fma_rn(dy, (double)c.z, __dmul_rn(dz, (double)c.w)));
+  return dot > 0.0;
+}
+
+// q = T_ij mu (fp64, pinned order, Q10), level-0 key, fp32 residual base.
+__device__ __forceinline__ void transform_point(const FactorShared& sh, const float4 a, int dyadic,
+                                                double r0, double inv_r0, float r0f, PointData& pd) {
+  const double mx = a.x, my = a.y, mz = a.z;
+  const double qx = __fma_rn(sh.R[0], mx, __fma_rn(sh.R[1], my, __fma_rn(sh.R[2], mz, sh.t[0])));
+  const double qy = __fma_rn(sh.R[3], mx, __fma_rn(sh.R[4], my, __fma_rn(sh.R[5], mz, sh.t[1])));
+  const double qz = __fma_rn(sh.R[6], mx, __fma_rn(sh.R[7], my, __fma_rn(sh.R[8], mz, sh.t[2])));
+  // saturating floor: a saturated coordinate misses every grid / fails key_in_range
+  pd.k0x = voxel_coord0(qx, r0, inv_r0, dyadic);
+  pd.k0y = voxel_coord0(qy, r0, inv_r0, dyadic);
+  pd.k0z = voxel_coord0(qz, r0, inv_r0, dyadic);
+  pd.qx = (float)qx;
+  pd.qy = (float)qy;
+  pd.qz = (float)qz;
+  pd.ex = 0.5f * r0f - (float)(qx - (double)pd.k0x * r0);
+  pd.ey = 0.5f * r0f - (float)(qy - (double)pd.k0y * r0);
+  pd.ez = 0.5f * r0f - (float)(qz - (double)pd.k0z * r0);
+}
+
+// R C R^T (symmetric) in packed pairs over rows 0/1: M = R C by columns, S = M R^T.
+__device__ __forceinline__ void rcr(const float* R, const float4 a, const float4 b, const float4 c,
+                                    PointData& pd) {
+  const float c00 = a.w, c01 = b.x, c02 = b.y, c11 = b.z, c12 = b.w, c22 = c.x;
+  const f2_t Rc0 = pk(R[0], R[3]), Rc1 = pk(R[1], R[4]), Rc2 = pk(R[2], R[5]);
+  const f2_t Mp0 = fma2(Rc2, bc(c02), fma2(Rc1, bc(c01), mul2(Rc0, bc(c00))));
+  const f2_t Mp1 = fma2(Rc2, bc(c12), fma2(Rc1, bc(c11), mul2(Rc0, bc(c01))));
+  const f2_t Mp2 = fma2(Rc2, bc(c22), fma2(Rc1, bc(c12), mul2(Rc0, bc(c02))));
+  const float M20 = fmaf(R[8], c02, fmaf(R[7], c01, R[6] * c00));
+  const float M21 = fmaf(R[8], c12, fmaf(R[7], c11, R[6] * c01));
+  const float M22 = fmaf(R[8], c22, fmaf(R[7], c12, R[6] * c02));
+  const f2_t Sp0 = fma2(Mp2, bc(R[2]), fma2(Mp1, bc(R[1]), mul2(Mp0, bc(R[0]))));  // (s00, s10)
+  pd.Sp1 = fma2(Mp2, bc(R[5]), fma2(Mp1, bc(R[4]), mul2(Mp0, bc(R[3]))));          // (s01, s11)
+  pd.Sp2 = fma2(Mp2, bc(R[8]), fma2(Mp1, bc(R[7]), mul2(Mp0, bc(R[6]))));          // (s02, s12)
+  pd.s00 = lo(Sp0);
+  pd.s22 = fmaf(M22, R[8], fmaf(M21, R[7], M20 * R[6]));
+}
+
+// One (point, level) term of Eqs.3-8 in target-block form, accumulated.
+// v0 = {off.xyz, C.xx}, v1 = {C.xy, C.yy, C.xz, C.yz}, v2 = C.zz of the voxel.
+template <int MAXL>
+__device__ __forceinline__ void level_algebra(Acc<MAXL>& ac, const PointData& pd, const float4 v0,
+                                              const float4 v1, const float v2, const int l,
+                                              const float r0f, const bool error_only) {
+  // fused covariance (Eq.3)
+  const f2_t P = add2(pk(v1.x, v1.y), pd.Sp1);  // (cb, cd) = (xy, yy)
+  const f2_t Q = add2(pk(v1.z, v1.w), pd.Sp2);  // (cc, ce) = (xz, yz)
+  const float ca = v0.w + pd.s00, cf = v2 + pd.s22;
+  const float cb = lo(P), cd = hi(P), cc = lo(Q), ce = hi(Q);
+  // inverse by the symmetric adjugate
+  const float i00 = fmaf(cd, cf, -ce * ce);
+  const float i01 = fmaf(cc, ce, -cb * cf);
+  const float i02 = fmaf(cb, ce, -cc * cd);
+  const float i11 = fmaf(ca, cf, -cc * cc);
+  const float i12 = fmaf(cb, cc, -ca * ce);
+  const float i22 = fmaf(ca, cd, -cb * cb);
+  const float det = fmaf(ca, i00, fmaf(cb, i01, cc * i02));
+  // Q16: a fused covariance that is not positive definite contributes nothing
+  const bool ok = det > 0.f && det < INFINITY;
+  const float id = ok ? __fdividef(1.0f, det) : 0.f;
+  ac.n_degenerate += !ok;
+  ac.inl[l] += ok;
+  const f2_t Om_a = mul2(pk(i00, i01), bc(id));  // (o00, o01) = column 0, rows 0-1
+  const f2_t Om_b = mul2(pk(i01, i11), bc(id));  // (o01, o11) = column 1, rows 0-1
+  const f2_t Om_c = mul2(pk(i02, i12), bc(id));  // (o02, o12) = column 2, rows 0-1
+  const float o22 = i22 * id;
+  const float o02 = lo(Om_c), o12 = hi(Om_c);
+
+  // d = mu~ - q = (centre_l - q) + offset (Q12): with k_l = k0 >> l,
+  // centre_l - q = (centre_0 - q) + r0 (2^(l-1) - 1/2 - (k0 & (2^l - 1))).
+  float bx = pd.ex, by = pd.ey, bz = pd.ez;
+  if (l > 0) {
+    const int mlo = (1 << l) - 1;
+    const float sh_l = 0.5f * (float)(1 << l) - 0.5f;
+    bx = fmaf(r0f, sh_l - (float)(pd.k0x & mlo), pd.ex);
+    by = fmaf(r0f, sh_l - (float)(pd.k0y & mlo), pd.ey);
+    bz = fmaf(r0f, sh_l - (float)(pd.k0z & mlo), pd.ez);
+  }
+  const f2_t D = add2(pk(bx, by), pk(v0.x, v0.y));  // (dx, dy)
+  const float dz = bz + v0.z;
+  const float dx = lo(D), dy = hi(D);
+
+  // g = Omega d, e = d^T g
+  const f2_t Gp = fma2(Om_c, bc(dz), fma2(Om_b, bc(dy), mul2(Om_a, bc(dx))));  // (gx, gy)
+  const float gz = fmaf(o02, dx, fmaf(o12, dy, o22 * dz));
+  ac.E = fma2(D, Gp, ac.E);
+  ac.ez = fmaf(dz, gz, ac.ez);
+  if (error_only) return;
+
+  const float qx = pd.qx, qy = pd.qy, qz = pd.qz;
+  ac.G = add2(ac.G, Gp);
+  ac.gz += gz;
+  // b_rot = q x g, with X = sum qz (gx, gy), Y = sum gz (qy, qx):
+  // brx = Y.x - X.y, bry = X.x - Y.y (combined at the tile reduction)
+  const float gx = lo(Gp), gy = hi(Gp);
+  ac.X = fma2(bc(qz), Gp, ac.X);
+  ac.Y = fma2(bc(gz), pk(qy, qx), ac.Y);
+  ac.rz = fmaf(qx, gy, fmaf(-qy, gx, ac.rz));
+  // sum Omega
+  ac.A = add2(ac.A, Om_a);
+  ac.C = add2(ac.C, Om_c);
+  ac.o11 += hi(Om_b);
+  ac.o22 += o22;
+  // W = Omega [q]x by columns: W[:,0] = qz Om[:,1] - qy Om[:,2],
+  // W[:,1] = qx Om[:,2] - qz Om[:,0], W[:,2] = qy Om[:,0] - qx Om[:,1]
+  const f2_t Wc0 = fma2(bc(-qy), Om_c, mul2(bc(qz), Om_b));
+  const f2_t Wc1 = fma2(bc(qx), Om_c, mul2(bc(-qz), Om_a));
+  const f2_t Wc2 = fma2(bc(-qx), Om_b, mul2(bc(qy), Om_a));
+  const float W20 = fmaf(qz, o12, -qy * o22);
+  const float W21 = fmaf(qx, o22, -qz * o02);
+  const float W22 = fmaf(qy, o02, -qx * o12);
+  ac.W0 = add2(ac.W0, Wc0);
+  ac.W1 = add2(ac.W1, Wc1);
+  ac.W2 = add2(ac.W2, Wc2);
+  ac.W20 += W20;
+  ac.W21 += W21;
+  ac.W22 += W22;
+  // H_rr = -[q]x W (upper)
+  ac.h00 = fmaf(qz, hi(Wc0), fmaf(-qy, W20, ac.h00));
+  ac.h01 = fmaf(qz, hi(Wc1), fmaf(-qy, W21, ac.h01));
+  ac.h02 = fmaf(qz, hi(Wc2), fmaf(-qy, W22, ac.h02));
+  ac.h11 = fmaf(qx, W21, fmaf(-qz, lo(Wc1), ac.h11));
+  ac.h12 = fmaf(qx, W22, fmaf(-qz, lo(Wc2), ac.h12));
+  ac.h22 = fmaf(qy, lo(Wc2), fmaf(-qx, hi(Wc2), ac.h22));
+}
+
+// Tile reduction: fp64 warp shuffles, then a fixed-order sum across warps.
+// Internal term order t[0..27] (see the file header).
+template <int MAXL>
+__device__ __forceinline__ void tile_reduce(const Acc<MAXL>& ac, double (*red)[kPartialStride],
+                                            double* partials, int64_t tile) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  {
+    const double t[27] = {lo(ac.A), hi(ac.A), lo(ac.C), ac.o11, hi(ac.C), ac.o22,
+                          lo(ac.W0), lo(ac.W1), lo(ac.W2), hi(ac.W0), hi(ac.W1), hi(ac.W2),
+                          ac.W20, ac.W21, ac.W22,
+                          ac.h00, ac.h01, ac.h02, ac.h11, ac.h12, ac.h22,
+                          (double)lo(ac.Y) - (double)hi(ac.X), (double)lo(ac.X) - (double)hi(ac.Y),
+                          ac.rz, lo(ac.G), hi(ac.G), ac.gz};
+#pragma unroll
+    for (int j = 0; j < 27; ++j) {
+      double s = warp_sum(t[j]);
+      if (lane == 0) red[warp][j] = s;
+    }
+    double e = warp_sum((double)lo(ac.E) + (double)hi(ac.E) + (double)ac.ez);
+    if (lane == 0) red[warp][27] = e;
+  }
+#pragma unroll
+  for (int l = 0; l < GVOX_MAX_LEVELS; ++l) {
+    int s = l < MAXL ? warp_sum_i(ac.inl[l < MAXL ? l : 0]) : 0;
+    if (lane == 0) red[warp][28 + l] = (double)s;
+  }
+  {
+    int s1 = warp_sum_i(ac.n_invisible), s2 = warp_sum_i(ac.n_degenerate);
+    if (lane == 0) {
+      red[warp][36] = (double)s1;
+      red[warp][37] = (double)s2;
+      red[warp][38] = 0.0;
+      red[warp][39] = 0.0;
+    }
+  }
+  __syncthreads();
+  if (tid < kPartialStride) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += red[w][tid];
+    partials[tile * kPartialStride + tid] = s;
+  }
+}
+
+// ---------------------------------------------------------------- K3: register version
 template <int MAXL, bool ALL_DENSE>
 __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     k_linearize(const CloudDev* const* __restrict__ clouds, const MapDev* const* __restrict__ maps,
@@ -85,47 +346,10 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
   __shared__ FactorShared sh;
   __shared__ double red[kWarps][kPartialStride];
   __shared__ double pose_s[24];
-
   const int tid = threadIdx.x;
   const int64_t tile = blockIdx.x;
-  // ---- prologue: stage the factor's constants in shared memory
-  {
-    const int32_t f = __ldg(tile_factor + tile);
-    const FactorDev fd = factors[f];
-    if (tid < 24) {
-      pose_s[tid] = __ldg(poses + 12 * (int64_t)(tid < 12 ? fd.pi : fd.pj) + (tid % 12));
-    } else if (tid == 32) {
-      const CloudDev* cd = clouds[fd.src];
-      int64_t b = (int64_t)(tile - __ldg(tile_start + f)) * tile_pts;
-      int64_t e = b + tile_pts;
-      int64_t n = cd->n;
-      sh.A = cd->A;
-      sh.B = cd->B;
-      sh.N = cd->N;
-      sh.begin = b;
-      sh.end = e < n ? e : n;
-      sh.validate = (fd.flags & GVOX_F_VALIDATE_SURFACE) && cd->has_normals;
-      sh.error_only = (fd.flags & GVOX_F_ERROR_ONLY) ? 1 : 0;
-      sh.corr_base = fd.corr_offset;
-    } else if (tid == 64) {
-      const MapDev* md = maps[fd.tgt];
-      sh.L = md->levels;
-      sh.dyadic = md->dyadic;
-      sh.r0 = md->r0;
-      sh.inv_r0 = md->inv_r0;
-    } else if (tid >= 96 && tid < 96 + MAXL) {
-      const MapDev* md = maps[fd.tgt];
-      sh.lv[tid - 96] = md->lv[tid - 96];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      relative_pose_dev(pose_s, pose_s + 12, sh.R, sh.t, sh.v);
-#pragma unroll
-      for (int j = 0; j < 9; ++j) sh.Rf[j] = (float)sh.R[j];
-    }
-    __syncthreads();
-  }
-
+  stage_factor<MAXL>(sh, pose_s, clouds, maps, factors, tile_start, tile_factor, tile_pts, poses,
+                     tile);
   const int L = sh.L;
   const int dyadic = sh.dyadic;
   const double r0 = sh.r0, inv_r0 = sh.inv_r0;
@@ -136,23 +360,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
   const float4* __restrict__ Ap = sh.A;
   const float4* __restrict__ Bp = sh.B;
   const float4* __restrict__ Np = sh.N;
-
-  // accumulators (fp32 per thread; see the term map at the tile reduction)
-  f2_t accA = 0, accC = 0;            // sum (o00, o01), sum (o02, o12)
-  float acc_o11 = 0.f, acc_o22 = 0.f;
-  f2_t accW0 = 0, accW1 = 0, accW2 = 0;  // sum (W0j, W1j), j = 0, 1, 2
-  float accW20 = 0.f, accW21 = 0.f, accW22 = 0.f;
-  float h00 = 0.f, h01 = 0.f, h02 = 0.f, h11 = 0.f, h12 = 0.f, h22 = 0.f;  // sum -[q]x W
-  f2_t accX = 0, accY = 0;  // sum qz (gx, gy), sum gz (qy, qx)
-  float acc_rz = 0.f;
-  f2_t accG = 0;  // sum (gx, gy)
-  float acc_gz = 0.f;
-  f2_t accE = 0;  // sum (dx gx, dy gy)
-  float acc_ez = 0.f;
-  int inl[MAXL];
-#pragma unroll
-  for (int l = 0; l < MAXL; ++l) inl[l] = 0;
-  int n_invisible = 0, n_degenerate = 0;
+  Acc<MAXL> ac;
 
   // software pipeline: the next point's 48 B source record is in flight while
   // the current one is processed
@@ -175,63 +383,37 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
 #else
     const float4 a = __ldg(Ap + k), b = __ldg(Bp + k), c = __ldg(Np + k);
 #endif
-    const double mx = a.x, my = a.y, mz = a.z;
-    if (validate) {
-      // discard if (mu - T_i^-1 t_j) . n > 0; zero normal = no test (Q7)
-      if (c.y != 0.f || c.z != 0.f || c.w != 0.f) {
-        double dx = mx - sh.v[0], dy = my - sh.v[1], dz = mz - sh.v[2];
-        double dot = __fma_rn(dx, (double)c.y, __fma_rn(dy, (double)c.z, __dmul_rn(dz, (double)c.w)));
-        if (dot > 0.0) {
-          ++n_invisible;
-          if (corr) {
-            for (int l = 0; l < L; ++l) corr[sh.corr_base + k * L + l] = -2;
-          }
-          continue;
-        }
-      }
+    if (validate && invisible(sh, a, c)) {
+      ++ac.n_invisible;
+      if (corr)
+        for (int l = 0; l < L; ++l) corr[sh.corr_base + k * L + l] = -2;
+      continue;
     }
-    // q = T_ij mu in fp64, pinned order (Q10); level-0 key floor(q / r0)
-    // (saturating: a saturated coordinate misses every grid / fails key_in_range)
-    const double qx = __fma_rn(sh.R[0], mx, __fma_rn(sh.R[1], my, __fma_rn(sh.R[2], mz, sh.t[0])));
-    const double qy = __fma_rn(sh.R[3], mx, __fma_rn(sh.R[4], my, __fma_rn(sh.R[5], mz, sh.t[1])));
-    const double qz = __fma_rn(sh.R[6], mx, __fma_rn(sh.R[7], my, __fma_rn(sh.R[8], mz, sh.t[2])));
-    const int32_t k0x = voxel_coord0(qx, r0, inv_r0, dyadic);
-    const int32_t k0y = voxel_coord0(qy, r0, inv_r0, dyadic);
-    const int32_t k0z = voxel_coord0(qz, r0, inv_r0, dyadic);
-    const float fqx = (float)qx, fqy = (float)qy, fqz = (float)qz;
-    const f2_t Qyx = pk(fqy, fqx);
-    // level-0 residual base: centre_0 - q = r0/2 - (q - k0 r0)
-    const float ex = 0.5f * r0f - (float)(qx - (double)k0x * r0);
-    const float ey = 0.5f * r0f - (float)(qy - (double)k0y * r0);
-    const float ez = 0.5f * r0f - (float)(qz - (double)k0z * r0);
+    PointData pd;
+    transform_point(sh, a, dyadic, r0, inv_r0, r0f, pd);
     bool have_rcr = false;
-    f2_t Sp1 = 0, Sp2 = 0;  // (s01, s11), (s02, s12)
-    float s00 = 0.f, s22 = 0.f;
     // levels are processed in groups of G (all loads of a group in flight together)
     constexpr int G = MAXL < GVOX_LIN_G ? MAXL : GVOX_LIN_G;
 #pragma unroll
     for (int lb = 0; lb < MAXL; lb += G) {
       if (lb >= L) break;
-      // stage 1: the voxel index of every level of the group
       int32_t vid[G];
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const int l = lb + j;
-        vid[j] = l < L ? lookup_level<ALL_DENSE>(sh.lv[l], k0x >> l, k0y >> l, k0z >> l) : -1;
+        vid[j] = l < L ? lookup_level<ALL_DENSE>(sh.lv[l], pd.k0x >> l, pd.k0y >> l, pd.k0z >> l) : -1;
       }
       if (corr) {
         for (int j = 0; j < G && lb + j < L; ++j) {
           const int l = lb + j;
           corr[sh.corr_base + k * L + l] =
-              vid[j] >= 0 ? (int64_t)pack_key(k0x >> l, k0y >> l, k0z >> l) : -1;
+              vid[j] >= 0 ? (int64_t)pack_key(pd.k0x >> l, pd.k0y >> l, pd.k0z >> l) : -1;
         }
       }
       bool any = false;
 #pragma unroll
       for (int j = 0; j < G; ++j) any |= vid[j] >= 0;
       if (!any) continue;
-
-      // stage 2: gather the hit voxels' records (48 B each)
       float4 v0[G], v1[G];
       float v2[G];
 #pragma unroll
@@ -243,156 +425,16 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
           v2[j] = __ldg(&vp[2].x);
         }
       }
-
-      // R C R^T (symmetric) once per point, in packed pairs over rows 0/1,
-      // overlapping the gathers.  M = R C column by column, S = M R^T.
       if (!have_rcr) {
         have_rcr = true;
-        const float* R = sh.Rf;
-        const float c00 = a.w, c01 = b.x, c02 = b.y, c11 = b.z, c12 = b.w, c22 = c.x;
-        const f2_t Rc0 = pk(R[0], R[3]), Rc1 = pk(R[1], R[4]), Rc2 = pk(R[2], R[5]);
-        const f2_t Mp0 = fma2(Rc2, bc(c02), fma2(Rc1, bc(c01), mul2(Rc0, bc(c00))));
-        const f2_t Mp1 = fma2(Rc2, bc(c12), fma2(Rc1, bc(c11), mul2(Rc0, bc(c01))));
-        const f2_t Mp2 = fma2(Rc2, bc(c22), fma2(Rc1, bc(c12), mul2(Rc0, bc(c02))));
-        const float M20 = fmaf(R[8], c02, fmaf(R[7], c01, R[6] * c00));
-        const float M21 = fmaf(R[8], c12, fmaf(R[7], c11, R[6] * c01));
-        const float M22 = fmaf(R[8], c22, fmaf(R[7], c12, R[6] * c02));
-        const f2_t Sp0 = fma2(Mp2, bc(R[2]), fma2(Mp1, bc(R[1]), mul2(Mp0, bc(R[0]))));  // (s00, s10)
-        Sp1 = fma2(Mp2, bc(R[5]), fma2(Mp1, bc(R[4]), mul2(Mp0, bc(R[3]))));             // (s01, s11)
-        Sp2 = fma2(Mp2, bc(R[8]), fma2(Mp1, bc(R[7]), mul2(Mp0, bc(R[6]))));             // (s02, s12)
-        s00 = lo(Sp0);
-        s22 = fmaf(M22, R[8], fmaf(M21, R[7], M20 * R[6]));
+        rcr(sh.Rf, a, b, c, pd);
       }
-
-      // stage 3: per-level algebra (packed pairs where the data pair up)
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        if (vid[j] < 0) continue;
-        const int l = lb + j;
-        // fused covariance (Eq.3): record v1 = {C.xy, C.yy, C.xz, C.yz}
-        const f2_t P = add2(pk(v1[j].x, v1[j].y), Sp1);  // (cb, cd) = (xy, yy)
-        const f2_t Q = add2(pk(v1[j].z, v1[j].w), Sp2);  // (cc, ce) = (xz, yz)
-        const float ca = v0[j].w + s00, cf = v2[j] + s22;
-        const float cb = lo(P), cd = hi(P), cc = lo(Q), ce = hi(Q);
-        // inverse by the symmetric adjugate
-        const float i00 = fmaf(cd, cf, -ce * ce);
-        const float i01 = fmaf(cc, ce, -cb * cf);
-        const float i02 = fmaf(cb, ce, -cc * cd);
-        const float i11 = fmaf(ca, cf, -cc * cc);
-        const float i12 = fmaf(cb, cc, -ca * ce);
-        const float i22 = fmaf(ca, cd, -cb * cb);
-        const float det = fmaf(ca, i00, fmaf(cb, i01, cc * i02));
-        // Q16: a fused covariance that is not positive definite contributes nothing
-        const bool ok = det > 0.f && det < INFINITY;
-        const float id = ok ? __fdividef(1.0f, det) : 0.f;
-        n_degenerate += !ok;
-        inl[l] += ok;
-        const f2_t Om_a = mul2(pk(i00, i01), bc(id));  // (o00, o01) = column 0, rows 0-1
-        const f2_t Om_b = mul2(pk(i01, i11), bc(id));  // (o01, o11) = column 1, rows 0-1
-        const f2_t Om_c = mul2(pk(i02, i12), bc(id));  // (o02, o12) = column 2, rows 0-1
-        const float o22 = i22 * id;
-        const float o02 = lo(Om_c), o12 = hi(Om_c);
-
-        // d = mu~ - q = (centre_l - q) + offset (Q12): with k_l = k0 >> l,
-        // centre_l - q = (centre_0 - q) + r0 (2^(l-1) - 1/2 - (k0 & (2^l - 1))).
-        float bx = ex, by = ey, bz = ez;
-        if (l > 0) {
-          const int mlo = (1 << l) - 1;
-          const float sh_l = 0.5f * (float)(1 << l) - 0.5f;
-          bx = fmaf(r0f, sh_l - (float)(k0x & mlo), ex);
-          by = fmaf(r0f, sh_l - (float)(k0y & mlo), ey);
-          bz = fmaf(r0f, sh_l - (float)(k0z & mlo), ez);
-        }
-        const f2_t D = add2(pk(bx, by), pk(v0[j].x, v0[j].y));  // (dx, dy)
-        const float dz = bz + v0[j].z;
-        const float dx = lo(D), dy = hi(D);
-
-        // g = Omega d, e = d^T g
-        const f2_t Gp = fma2(Om_c, bc(dz), fma2(Om_b, bc(dy), mul2(Om_a, bc(dx))));  // (gx, gy)
-        const float gz = fmaf(o02, dx, fmaf(o12, dy, o22 * dz));
-        accE = fma2(D, Gp, accE);
-        acc_ez = fmaf(dz, gz, acc_ez);
-        if (error_only) continue;
-
-        accG = add2(accG, Gp);
-        acc_gz += gz;
-        // b_rot = q x g:  (qy gz - qz gy, qz gx - qx gz), qx gy - qy gx
-        const float gx = lo(Gp), gy = hi(Gp);
-        // accumulated as X = sum qz (gx, gy), Y = sum gz (qy, qx):
-        // brx = Y.x - X.y, bry = X.x - Y.y (combined at the tile reduction)
-        accX = fma2(bc(fqz), Gp, accX);
-        accY = fma2(bc(gz), Qyx, accY);
-        acc_rz = fmaf(fqx, gy, fmaf(-fqy, gx, acc_rz));
-        // sum Omega
-        accA = add2(accA, Om_a);
-        accC = add2(accC, Om_c);
-        acc_o11 += hi(Om_b);
-        acc_o22 += o22;
-        // W = Omega [q]x by columns: W[:,0] = qz Om[:,1] - qy Om[:,2],
-        // W[:,1] = qx Om[:,2] - qz Om[:,0], W[:,2] = qy Om[:,0] - qx Om[:,1]
-        const f2_t Wc0 = fma2(bc(-fqy), Om_c, mul2(bc(fqz), Om_b));
-        const f2_t Wc1 = fma2(bc(fqx), Om_c, mul2(bc(-fqz), Om_a));
-        const f2_t Wc2 = fma2(bc(-fqx), Om_b, mul2(bc(fqy), Om_a));
-        const float W20 = fmaf(fqz, o12, -fqy * o22);
-        const float W21 = fmaf(fqx, o22, -fqz * o02);
-        const float W22 = fmaf(fqy, o02, -fqx * o12);
-        accW0 = add2(accW0, Wc0);
-        accW1 = add2(accW1, Wc1);
-        accW2 = add2(accW2, Wc2);
-        accW20 += W20;
-        accW21 += W21;
-        accW22 += W22;
-        // H_rr = -[q]x W (upper)
-        h00 = fmaf(fqz, hi(Wc0), fmaf(-fqy, W20, h00));
-        h01 = fmaf(fqz, hi(Wc1), fmaf(-fqy, W21, h01));
-        h02 = fmaf(fqz, hi(Wc2), fmaf(-fqy, W22, h02));
-        h11 = fmaf(fqx, W21, fmaf(-fqz, lo(Wc1), h11));
-        h12 = fmaf(fqx, W22, fmaf(-fqz, lo(Wc2), h12));
-        h22 = fmaf(fqy, lo(Wc2), fmaf(-fqx, hi(Wc2), h22));
-      }
+      for (int j = 0; j < G; ++j)
+        if (vid[j] >= 0) level_algebra<MAXL>(ac, pd, v0[j], v1[j], v2[j], lb + j, r0f, error_only);
     }
   }
-
-  // ---- tile reduction: fp64 warp shuffles, then fixed-order across warps.
-  // Internal term order t[0..27] (see the file header).
-  const int lane = tid & 31, warp = tid >> 5;
-  {
-    const float W[9] = {lo(accW0), lo(accW1), lo(accW2), hi(accW0), hi(accW1), hi(accW2),
-                        accW20, accW21, accW22};
-    const double t[27] = {lo(accA), hi(accA), lo(accC), acc_o11, hi(accC), acc_o22,
-                          W[0], W[1], W[2], W[3], W[4], W[5], W[6], W[7], W[8],
-                          h00, h01, h02, h11, h12, h22,
-                          (double)lo(accY) - (double)hi(accX), (double)lo(accX) - (double)hi(accY),
-                          acc_rz, lo(accG), hi(accG), acc_gz};
-#pragma unroll
-    for (int j = 0; j < 27; ++j) {
-      double s = warp_sum(t[j]);
-      if (lane == 0) red[warp][j] = s;
-    }
-    double e = warp_sum((double)lo(accE) + (double)hi(accE) + (double)acc_ez);
-    if (lane == 0) red[warp][27] = e;
-  }
-#pragma unroll
-  for (int l = 0; l < GVOX_MAX_LEVELS; ++l) {
-    int s = l < MAXL ? warp_sum_i(inl[l < MAXL ? l : 0]) : 0;
-    if (lane == 0) red[warp][28 + l] = (double)s;
-  }
-  {
-    int s1 = warp_sum_i(n_invisible), s2 = warp_sum_i(n_degenerate);
-    if (lane == 0) {
-      red[warp][36] = (double)s1;
-      red[warp][37] = (double)s2;
-      red[warp][38] = 0.0;
-      red[warp][39] = 0.0;
-    }
-  }
-  __syncthreads();
-  if (tid < kPartialStride) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += red[w][tid];
-    partials[tile * kPartialStride + tid] = s;
-  }
+  tile_reduce<MAXL>(ac, red, partials, tile);
 }
 
 // ---------------------------------------------------------------- K4 / expand

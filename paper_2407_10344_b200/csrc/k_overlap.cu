@@ -18,9 +18,15 @@ namespace gvox {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef GVOX_OVL_U
+#define GVOX_OVL_U 2
+#endif
+#ifndef GVOX_OVL_MINB
+#define GVOX_OVL_MINB 4
+#endif
 
 template <bool ALL_DENSE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
     k_overlap(const CloudDev* const* __restrict__ clouds, const MapDev* const* __restrict__ maps,
               const PairDev* __restrict__ pairs, const int32_t* __restrict__ tile_start,
               const int32_t* __restrict__ tile_pair, int tile_pts, const double* __restrict__ poses,
@@ -60,16 +66,33 @@ __global__ void __launch_bounds__(kThreads)
   const int dyadic = dyadic_s;
   const float4* __restrict__ A = A_s;
   int cnt = 0;
-  for (int64_t k = range_s[0] + tid; k < range_s[1]; k += kThreads) {
-    const float4 a = __ldg(A + k);
-    const double mx = a.x, my = a.y, mz = a.z;
-    const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
-    const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
-    const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
-    const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
-    const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
-    const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
-    cnt += lookup_level<ALL_DENSE>(lv, kx, ky, kz) >= 0;
+  const int64_t kb = range_s[0], ke = range_s[1];
+  // U points per thread per iteration: their loads are in flight together
+  constexpr int U = GVOX_OVL_U;
+  for (int64_t k0 = kb + tid; k0 < ke; k0 += U * kThreads) {
+    float4 a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + u * kThreads;
+      if (k < ke) a[u] = __ldg(A + k);
+    }
+    int32_t hit[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      hit[u] = -1;
+      if (k0 + u * kThreads < ke) {
+        const double mx = a[u].x, my = a[u].y, mz = a[u].z;
+        const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
+        const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
+        const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
+        const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
+        const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
+        const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
+        hit[u] = lookup_level<ALL_DENSE>(lv, kx, ky, kz);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) cnt += hit[u] >= 0;
   }
   // warp counts, then one atomic per CTA
 #pragma unroll

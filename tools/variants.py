@@ -18,6 +18,10 @@ VARIANTS = {
     "nopf_b3": ["GVOX_LIN_PREFETCH=0", "GVOX_LIN_MINB=3"],
     "t128_b5": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=5", "GVOX_LIN_PREFETCH=0"],
     "t128_b4": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=4"],
+    "ovl_u1_b8": ["GVOX_OVL_U=1", "GVOX_OVL_MINB=8"],
+    "ovl_u2_b6": ["GVOX_OVL_U=2", "GVOX_OVL_MINB=6"],
+    "ovl_u4_b4": ["GVOX_OVL_U=4", "GVOX_OVL_MINB=4"],
+    "ovl_u2_b4": ["GVOX_OVL_U=2", "GVOX_OVL_MINB=4"],
 }
 
 
@@ -33,14 +37,25 @@ def build(names):
         print("built", n, flush=True)
 
 
-def run(names, extra):
+def run(names, extra, stage="linearize"):
     res = {}
     for n in names:
         env = dict(os.environ, GVOX_LIB=os.path.join(OUT, f"libgvox_{n}.so"))
-        p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--linearize-only", "--no-e2e",
-                            "--no-cpu-baseline", "--steps", "6", *extra], env=env, capture_output=True, text=True)
-        line = [l for l in p.stderr.splitlines() if "linearize-only" in l]
-        res[n] = line[-1] if line else p.stderr[-500:]
+        if n.startswith("ovl"):
+            p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--no-e2e",
+                                "--no-cpu-baseline", "--steps", "3", *extra], env=env,
+                               capture_output=True, text=True)
+            try:
+                d = json.loads(p.stdout.strip().splitlines()[-1])
+                res[n] = {k: round(v["ms_per_step"], 2) for k, v in d["stages"].items()}
+            except Exception:
+                res[n] = p.stderr[-500:]
+        else:
+            p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--linearize-only",
+                                "--no-e2e", "--no-cpu-baseline", "--steps", "6", *extra], env=env,
+                               capture_output=True, text=True)
+            line = [l for l in p.stderr.splitlines() if "linearize-only" in l]
+            res[n] = line[-1] if line else p.stderr[-500:]
         print(n, res[n], flush=True)
     return res
 
