@@ -97,21 +97,6 @@ def make_scene(args, rank, world, dist):
     return sc
 
 
-def shard_targets(sc, world):
-    """Contiguous target-map ranges balanced by the candidate work (sum of source
-    points over candidate pairs + target points)."""
-    M = len(sc.map_clouds)
-    n = np.diff(sc.offsets)
-    w = n[sc.map_clouds].astype(np.float64)
-    np.add.at(w, sc.pairs[:, 1], n[sc.pairs[:, 0]])
-    cw = np.concatenate([[0], np.cumsum(w)])
-    bounds = [0]
-    for r in range(1, world):
-        bounds.append(int(np.searchsorted(cw, cw[-1] * r / world)))
-    bounds.append(M)
-    return bounds
-
-
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
     def __init__(self, device_index):
@@ -251,8 +236,16 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        # GVOX_DIST_BACKEND=gloo (+ GVOX_SAME_DEVICE=1) runs the multi-rank plumbing on a
+        # one-GPU box for testing; the product path is NCCL, one GPU per rank
+        backend = os.environ.get("GVOX_DIST_BACKEND", "nccl")
+        if os.environ.get("GVOX_SAME_DEVICE"):
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -279,12 +272,11 @@ def main():
     cloud_arr = gv.HandleArray(clouds)
     poses = gv.as_poses(sc.poses)
 
-    bounds = shard_targets(sc, world)
+    from paper_2407_10344_b200 import dist as gdist
+    bounds = gdist.shard_targets(n_pts, sc.map_clouds, sc.pairs, world)
     t_lo, t_hi = bounds[rank], bounds[rank + 1]
     my_targets = np.arange(t_lo, t_hi)
-    pm = (sc.pairs[:, 1] >= t_lo) & (sc.pairs[:, 1] < t_hi)
-    my_pairs = sc.pairs[pm].copy()
-    my_pairs[:, 1] -= t_lo                      # local map index
+    _, my_pairs = gdist.local_pairs(sc.pairs, bounds, rank)  # target -> local map index
     pairs_s = gv.as_pairs(my_pairs)
     src_n = n_pts[my_pairs[:, 0]]
     my_target_clouds = [clouds[int(sc.map_clouds[t])] for t in my_targets]
@@ -310,9 +302,8 @@ def main():
         out = acc_out[:len(fac)]
         gv.linearize_batch_accum(ctx, cloud_arr, marr, fac, poses, out=out)         # S3-S7
         if world > 1:
-            buf = acc_out[:state["fmax"]]
-            gathered = state["gather"]
-            dist.all_gather_into_tensor(gathered, buf)
+            # the one exchange: all-gather of the compact per-factor records
+            state["gathered"], _ = gdist.gather_records(acc_out, len(fac), state["fmax"])
         state["maps"] = maps                  # keep alive until the next step replaces them
         state["fac"] = fac
         return int(src_n[sel].sum()), len(fac)
@@ -324,8 +315,6 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         state["fmax"] = int(t.item())
         acc_out = gv.device_records(ctx, state["fmax"], gv.FACTOR_ACCUM_DTYPE)
-        state["gather"] = torch.empty((world * state["fmax"], acc_out.shape[1]), dtype=torch.uint8,
-                                      device=dev)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()

@@ -193,7 +193,8 @@ void launch_overlap(const CloudDev* const* clouds, const MapDev* const* maps, co
 struct FactorDev {
   int32_t src, tgt, pi, pj;
   uint32_t flags;
-  int32_t pad;
+  int32_t tile_pts;     // points per tile of this factor (a function of its own size
+                        // only, so results do not depend on the rest of the batch)
   int64_t corr_offset;  // first (point, level) record in corr_dump
 };
 void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,

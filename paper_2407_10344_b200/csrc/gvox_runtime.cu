@@ -998,16 +998,18 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
     max_levels = std::max(max_levels, m->levels);
     for (int l = 0; l < m->levels; ++l) all_dense = all_dense && m->desc.lv[l].dense;
   }
-  int ppt = 1;  // points per thread per tile: keep >= ~8 waves of 296 CTAs
-  while (ppt < 64 && total_pf / ((int64_t)256 * ppt * 2) >= 148 * 2 * 8) ppt *= 2;
-  const int tile_pts = 256 * ppt;
   std::vector<int32_t> tstart(num_factors + 1, 0);
   std::vector<FactorDev> fdev(num_factors);
   int64_t corr_off = 0;
   for (int64_t f = 0; f < num_factors; ++f) {
     const gvox_factor& q = factors[f];
-    int64_t n = clouds[q.source_cloud]->n;
-    int64_t nt = (n + tile_pts - 1) / tile_pts;
+    const int64_t n = clouds[q.source_cloud]->n;
+    // tile = 256 * ppt points, ppt = pow2 <= n / 2048 in [1, 64]: ~8-16 tiles per
+    // factor; depends on the factor alone (bitwise batch/shard independence)
+    int ppt = 1;
+    while (ppt < 64 && (int64_t)256 * 8 * (ppt * 2) <= n) ppt *= 2;
+    const int tile_pts = 256 * ppt;
+    const int64_t nt = (n + tile_pts - 1) / tile_pts;
     if ((int64_t)tstart[f] + nt > INT32_MAX)
       return fail(GVOX_ERR_INVALID, "%s: batch too large (more than 2^31 tiles)", fn);
     tstart[f + 1] = tstart[f] + (int32_t)nt;
@@ -1017,7 +1019,7 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
     d.pi = q.pose_i;
     d.pj = q.pose_j;
     d.flags = q.flags;
-    d.pad = 0;
+    d.tile_pts = tile_pts;
     d.corr_offset = corr_off;
     corr_off += n * maps[q.target_map]->levels;
   }
@@ -1059,7 +1061,7 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
     TimerScope ts(ctx, GVOX_TIMER_LINEARIZE);
     launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
                      (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
-                     tile_pts, max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
+                     0, max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
                      (int32_t*)(wb + o_tf), corr_dump, all_dense, ctx->stream);
   }
   CK_LAUNCH("linearize");
@@ -1115,7 +1117,7 @@ gvox_status gvox_expand(gvox_ctx* ctx, const gvox_factor* factors, int64_t num_f
   std::vector<FactorDev> fdev(num_factors);
   for (int64_t f = 0; f < num_factors; ++f) {
     fdev[f] = FactorDev{factors[f].source_cloud, factors[f].target_map, factors[f].pose_i,
-                        factors[f].pose_j, factors[f].flags, 0, 0};
+                        factors[f].pose_j, factors[f].flags, 0, 0};  // tiles unused by expand
   }
   Layout lay;
   size_t o_pose = lay.add(96 * num_poses);

@@ -127,8 +127,8 @@ __device__ __forceinline__ void stage_factor(FactorShared& sh, double* pose_s,
     pose_s[tid] = __ldg(poses + 12 * (int64_t)(tid < 12 ? fd.pi : fd.pj) + (tid % 12));
   } else if (tid == 32) {
     const CloudDev* cd = clouds[fd.src];
-    int64_t b = (int64_t)(tile - __ldg(tile_start + f)) * tile_pts;
-    int64_t e = b + tile_pts;
+    int64_t b = (int64_t)(tile - __ldg(tile_start + f)) * fd.tile_pts;
+    int64_t e = b + fd.tile_pts;
     int64_t n = cd->n;
     sh.A = cd->A;
     sh.B = cd->B;

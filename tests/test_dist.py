@@ -1,0 +1,90 @@
+"""Host-side logic of the factor-sharded multi-GPU path, on CPU: target-range
+sharding and the one all-gather of fixed-size per-factor records, with
+world_size 2 over gloo (127.0.0.1).  The CUDA kernels are not involved."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2407_10344_b200 import dist as gdist
+
+
+def _scene(rs, M=40, P=300):
+    n_points = rs.integers(0, 5000, M + 3)
+    map_clouds = np.arange(M)
+    src = rs.integers(0, M + 3, P)
+    tgt = np.sort(rs.integers(0, M, P))
+    pairs = np.stack([src, tgt, src, tgt], 1)
+    return n_points, map_clouds, pairs
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shard_targets_partition(world):
+    rs = np.random.default_rng(world)
+    n_points, map_clouds, pairs = _scene(rs)
+    b = gdist.shard_targets(n_points, map_clouds, pairs, world)
+    assert b[0] == 0 and b[-1] == len(map_clouds) and len(b) == world + 1
+    assert all(b[i] <= b[i + 1] for i in range(world))
+    seen = []
+    for r in range(world):
+        rows, loc = gdist.local_pairs(pairs, b, r)
+        assert np.all((loc[:, 1] >= 0) & (loc[:, 1] < b[r + 1] - b[r]))
+        assert np.array_equal(loc[:, 1] + b[r], pairs[rows, 1])
+        seen.extend(rows.tolist())
+    assert sorted(seen) == list(range(len(pairs)))  # every pair on exactly one rank
+    # balance: no rank gets much more than its share (+ the largest single target)
+    w = n_points[map_clouds].astype(float)
+    np.add.at(w, pairs[:, 1], n_points[pairs[:, 0]])
+    per = [w[b[r]:b[r + 1]].sum() for r in range(world)]
+    assert max(per) <= w.sum() / world + w.max() + 1e-9
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rs = np.random.default_rng(7)
+        n_points, map_clouds, pairs = _scene(rs)
+        b = gdist.shard_targets(n_points, map_clouds, pairs, world)
+        rows, _ = gdist.local_pairs(pairs, b, rank)
+        fmax = max(len(gdist.local_pairs(pairs, b, r)[0]) for r in range(world))
+        # fake 288-byte records: the global row index in the first 8 bytes
+        rec = torch.zeros((fmax, 288), dtype=torch.uint8)
+        rec[:len(rows), :8] = torch.from_numpy(rows.astype(np.int64).view(np.uint8).reshape(-1, 8))
+        out, cnts = gdist.gather_records(rec, len(rows), fmax)
+        ids = out[:, :8].contiguous().numpy().view(np.int64).reshape(-1)
+        q.put((rank, ids.tolist(), cnts))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_records_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rs = np.random.default_rng(7)
+    _, _, pairs = _scene(rs)
+    for rank, ids, cnts in res:
+        # every rank holds all records, in rank order = global target order
+        assert ids == list(range(len(pairs))), (rank, ids[:10])
+        assert sum(cnts) == len(pairs)

@@ -1,0 +1,75 @@
+"""Factor-sharded linearization on one GPU with 2 ranks (gloo plumbing): the
+gathered compact records equal the single-process batch bit for bit, because a
+factor's tiling and reduction order depend on the factor alone."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2407_10344_b200 as gv
+        from paper_2407_10344_b200 import dist as gdist
+        import synth
+        sc = synth.make("C4", n_submaps=24, half_blocks=3, n_points=20000)
+        ctx = gv.Context(0)
+        clouds = gv.create_clouds(ctx, sc.mu, sc.cov, sc.nrm, sc.offsets)
+        n = np.diff(sc.offsets)
+        fac = sc.factors
+        b = gdist.shard_targets(n, sc.map_clouds, fac, world)
+        rows, loc = gdist.local_pairs(fac, b, rank)
+        maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds[b[rank]:b[rank + 1]]],
+                                   sc.r0, sc.levels)
+        fmax = max(len(gdist.local_pairs(fac, b, r)[0]) for r in range(world))
+        acc = gv.device_records(ctx, fmax, gv.FACTOR_ACCUM_DTYPE)
+        gv.linearize_batch_accum(ctx, clouds, maps, loc, sc.poses, out=acc[:len(loc)])
+        torch.cuda.synchronize()
+        out, cnts = gdist.gather_records(acc, len(loc), fmax)
+        q.put((rank, out.cpu().numpy().tobytes(), cnts))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_equals_single(gv):
+    import torch.multiprocessing as mp
+    import synth
+    ctx = gv.Context(0)
+    sc = synth.make("C4", n_submaps=24, half_blocks=3, n_points=20000)
+    clouds = gv.create_clouds(ctx, sc.mu, sc.cov, sc.nrm, sc.offsets)
+    maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    ref = gv.linearize_batch_accum(ctx, clouds, maps, sc.factors, sc.poses)
+    assert len(sc.factors) > 20
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    port = _free_port()
+    procs = [mpc.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    from paper_2407_10344_b200 import dist as gdist
+    b = gdist.shard_targets(np.diff(sc.offsets), sc.map_clouds, sc.factors, 2)
+    order = np.concatenate([gdist.local_pairs(sc.factors, b, r)[0] for r in range(2)])
+    want = ref[order].tobytes()  # gathered rows are in shard (target-range) order
+    for rank, blob, cnts in res:
+        assert sum(cnts) == len(sc.factors)
+        assert blob == want, f"rank {rank}: gathered records differ from the single batch"

@@ -309,12 +309,10 @@ def test_batch_equals_serial_and_determinism(gv, ctx):
     a = gv.linearize_batch(ctx, clouds, maps, sc.factors, sc.poses)
     b = gv.linearize_batch(ctx, clouds, maps, sc.factors, sc.poses)
     assert a.tobytes() == b.tobytes(), "repeated runs must be bitwise identical"
+    # a factor's tiling depends on the factor alone: batch == serial bit for bit
     for k in range(len(sc.factors)):
         s = gv.linearize_batch(ctx, clouds, maps, sc.factors[k:k + 1], sc.poses)
-        for name in ("H_ii", "H_ij", "H_jj", "b_i", "b_j", "error"):
-            np.testing.assert_allclose(s[name][0], a[name][k], rtol=1e-9,
-                                       atol=1e-9 * np.abs(a[name][k]).max())
-        assert np.array_equal(s["inliers"][0], a["inliers"][k])
+        assert s[0].tobytes() == a[k].tobytes(), f"factor {k}"
     # N identical factors -> N identical outputs
     rep = np.repeat(sc.factors[:1], 5, axis=0)
     r = gv.linearize_batch(ctx, clouds, maps, rep, sc.poses)
