@@ -40,18 +40,22 @@ struct CloudDev {
 //    or -1 per cell; chosen when the box has at most kDenseRatio cells per
 //    voxel): one predicated load, no probing; or
 //  * the open-addressing HASH table (sparse / very large extents).
-struct MapLevelDev {
-  const ulonglong2* slots;  // hash: [mask + 1] {key, idx}
+struct __align__(16) MapLevelDev {
+  // dense-grid fields first, 16 B aligned: two vector loads per lookup
+  int32_t x0, y0, z0;       // dense: key of cell (0, 0, 0)
+  uint32_t dx;              // dense: box size in cells (each < 2^30, product < 2^31)
+  uint32_t dy, dz;
+  uint32_t syz;             // dy * dz (x stride)
+  int32_t dense;            // 1 = dense grid
   const int32_t* grid;      // dense: [dx * dy * dz], x-major; nullptr for hash
   const float4* vox;        // [3 * nvox]
+  const ulonglong2* slots;  // hash: [mask + 1] {key, idx}
   uint64_t mask;            // hash capacity - 1
-  int32_t shift;            // 64 - log2(capacity)
-  int32_t dense;            // 1 = dense grid
-  int32_t x0, y0, z0;       // dense: key of cell (0, 0, 0)
-  uint32_t dx, dy, dz;      // dense: box size in cells
   double r;      // r0 * 2^l
   double inv_r;  // 1 / r (used only when dyadic)
   int64_t nvox;
+  int32_t shift;            // 64 - log2(capacity)
+  int32_t pad;
 };
 
 constexpr int kDenseRatio = 256;  // max cells per voxel for a dense grid level

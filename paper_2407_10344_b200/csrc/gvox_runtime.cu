@@ -669,6 +669,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       lv.dense = f.dense;
       lv.x0 = f.x0; lv.y0 = f.y0; lv.z0 = f.z0;
       lv.dx = f.dx; lv.dy = f.dy; lv.dz = f.dz;
+      lv.syz = f.dy * f.dz;
       lv.r = r;
       lv.inv_r = 1.0 / r;
       lv.nvox = V;

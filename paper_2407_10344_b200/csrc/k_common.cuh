@@ -54,9 +54,11 @@ __device__ inline int32_t probe_hash(const MapLevelDev& lv, uint64_t key) {
 template <bool ALL_DENSE = false>
 __device__ inline int32_t lookup_level(const MapLevelDev& lv, int32_t kx, int32_t ky, int32_t kz) {
   if (ALL_DENSE || lv.dense) {
-    const uint32_t cx = (uint32_t)(kx - lv.x0), cy = (uint32_t)(ky - lv.y0), cz = (uint32_t)(kz - lv.z0);
-    if (cx >= lv.dx || cy >= lv.dy || cz >= lv.dz) return -1;
-    return __ldg(lv.grid + ((size_t)cx * lv.dy + cy) * lv.dz + cz);
+    const int4 b0 = *reinterpret_cast<const int4*>(&lv.x0);    // x0 y0 z0 dx
+    const uint4 b1 = *reinterpret_cast<const uint4*>(&lv.dy);  // dy dz syz dense
+    const uint32_t cx = (uint32_t)(kx - b0.x), cy = (uint32_t)(ky - b0.y), cz = (uint32_t)(kz - b0.z);
+    if (cx >= (uint32_t)b0.w || cy >= b1.x || cz >= b1.y) return -1;
+    return __ldg(lv.grid + (cx * b1.z + cy * b1.y + cz));  // < 2^31 cells: 32-bit index
   }
   if (!key_in_range(kx) || !key_in_range(ky) || !key_in_range(kz)) return -1;
   return probe_hash(lv, pack_key(kx, ky, kz));

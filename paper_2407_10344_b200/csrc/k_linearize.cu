@@ -55,6 +55,7 @@ namespace {
 #define GVOX_LIN_G 4
 #endif
 
+
 constexpr int kThreads = GVOX_LIN_THREADS;
 constexpr int kWarps = kThreads / 32;
 
@@ -202,12 +203,25 @@ __device__ __forceinline__ void rcr(const float* R, const float4 a, const float4
   pd.s22 = fmaf(M22, R[8], fmaf(M21, R[7], M20 * R[6]));
 }
 
-// One (point, level) term of Eqs.3-8 in target-block form, accumulated.
-// v0 = {off.xyz, C.xx}, v1 = {C.xy, C.yy, C.xz, C.yz}, v2 = C.zz of the voxel.
+// Level folding.  B_k = [-(q)x, I] depends on the point only, so for one point
+//   sum_l B^T Omega_l B = B^T (sum_l Omega_l) B,   sum_l B^T Omega_l d_l = B^T (sum_l g_l)
+// with g_l = Omega_l d_l.  Each hit level therefore only adds its Omega_l and
+// g_l into per-point sums (level_term); the q-dependent target-block terms are
+// accumulated once per point (fold_point).  Exact algebra; only the fp32
+// summation order changes.
+struct LevelSum {
+  f2_t Oa, Oc;   // sum (o00, o01), sum (o02, o12)
+  float o11, o22;
+  f2_t G;        // sum (gx, gy)
+  float gz;
+};
+
+// One (point, level) term: Eq.3 fused covariance, Omega, residual, g = Omega d,
+// e = d^T g.  v0 = {off.xyz, C.xx}, v1 = {C.xy, C.yy, C.xz, C.yz}, v2 = C.zz.
 template <int MAXL>
-__device__ __forceinline__ void level_algebra(Acc<MAXL>& ac, const PointData& pd, const float4 v0,
-                                              const float4 v1, const float v2, const int l,
-                                              const float r0f, const bool error_only) {
+__device__ __forceinline__ void level_term(Acc<MAXL>& ac, LevelSum& ls, const PointData& pd,
+                                           const float4 v0, const float4 v1, const float v2,
+                                           const int l, const float r0f) {
   // fused covariance (Eq.3)
   const f2_t P = add2(pk(v1.x, v1.y), pd.Sp1);  // (cb, cd) = (xy, yy)
   const f2_t Q = add2(pk(v1.z, v1.w), pd.Sp2);  // (cc, ce) = (xz, yz)
@@ -230,7 +244,6 @@ __device__ __forceinline__ void level_algebra(Acc<MAXL>& ac, const PointData& pd
   const f2_t Om_b = mul2(pk(i01, i11), bc(id));  // (o01, o11) = column 1, rows 0-1
   const f2_t Om_c = mul2(pk(i02, i12), bc(id));  // (o02, o12) = column 2, rows 0-1
   const float o22 = i22 * id;
-  const float o02 = lo(Om_c), o12 = hi(Om_c);
 
   // d = mu~ - q = (centre_l - q) + offset (Q12): with k_l = k0 >> l,
   // centre_l - q = (centre_0 - q) + r0 (2^(l-1) - 1/2 - (k0 & (2^l - 1))).
@@ -248,24 +261,39 @@ __device__ __forceinline__ void level_algebra(Acc<MAXL>& ac, const PointData& pd
 
   // g = Omega d, e = d^T g
   const f2_t Gp = fma2(Om_c, bc(dz), fma2(Om_b, bc(dy), mul2(Om_a, bc(dx))));  // (gx, gy)
-  const float gz = fmaf(o02, dx, fmaf(o12, dy, o22 * dz));
+  const float gz = fmaf(lo(Om_c), dx, fmaf(hi(Om_c), dy, o22 * dz));
   ac.E = fma2(D, Gp, ac.E);
   ac.ez = fmaf(dz, gz, ac.ez);
-  if (error_only) return;
+  // per-point level sums
+  ls.Oa = add2(ls.Oa, Om_a);
+  ls.Oc = add2(ls.Oc, Om_c);
+  ls.o11 += hi(Om_b);
+  ls.o22 += o22;
+  ls.G = add2(ls.G, Gp);
+  ls.gz += gz;
+}
 
+// The target-block terms of one point from its level sums (Eqs.6-8 with
+// B = [-(q)x, I]): sum Omega, W = Omega [q]x, -[q]x W, q x g, g.
+template <int MAXL>
+__device__ __forceinline__ void fold_point(Acc<MAXL>& ac, const LevelSum& ls, const PointData& pd) {
   const float qx = pd.qx, qy = pd.qy, qz = pd.qz;
+  const f2_t Om_a = ls.Oa, Om_c = ls.Oc;                  // (o00, o01), (o02, o12)
+  const f2_t Om_b = pk(hi(ls.Oa), ls.o11);                  // (o01, o11)
+  const float o22 = ls.o22, o02 = lo(Om_c), o12 = hi(Om_c);
+  const f2_t Gp = ls.G;
+  const float gz = ls.gz, gx = lo(Gp), gy = hi(Gp);
   ac.G = add2(ac.G, Gp);
   ac.gz += gz;
   // b_rot = q x g, with X = sum qz (gx, gy), Y = sum gz (qy, qx):
   // brx = Y.x - X.y, bry = X.x - Y.y (combined at the tile reduction)
-  const float gx = lo(Gp), gy = hi(Gp);
   ac.X = fma2(bc(qz), Gp, ac.X);
   ac.Y = fma2(bc(gz), pk(qy, qx), ac.Y);
   ac.rz = fmaf(qx, gy, fmaf(-qy, gx, ac.rz));
   // sum Omega
   ac.A = add2(ac.A, Om_a);
   ac.C = add2(ac.C, Om_c);
-  ac.o11 += hi(Om_b);
+  ac.o11 += ls.o11;
   ac.o22 += o22;
   // W = Omega [q]x by columns: W[:,0] = qz Om[:,1] - qy Om[:,2],
   // W[:,1] = qx Om[:,2] - qz Om[:,0], W[:,2] = qy Om[:,0] - qx Om[:,1]
@@ -356,26 +384,29 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
   const float r0f = (float)sh.r0;
   const bool validate = sh.validate;
   const bool error_only = sh.error_only;
-  const int64_t begin = sh.begin, end = sh.end;
-  const float4* __restrict__ Ap = sh.A;
-  const float4* __restrict__ Bp = sh.B;
-  const float4* __restrict__ Np = sh.N;
+  // 32-bit point index within the tile; the source planes pre-offset to its start
+  const int64_t begin = sh.begin;
+  const int32_t npts = (int32_t)(sh.end - sh.begin);
+  const float4* __restrict__ Ap = sh.A + begin;
+  const float4* __restrict__ Bp = sh.B + begin;
+  const float4* __restrict__ Np = sh.N + begin;
+  int64_t* const corr_t = corr ? corr + sh.corr_base + begin * L : nullptr;
   Acc<MAXL> ac;
 
   // software pipeline: the next point's 48 B source record is in flight while
   // the current one is processed
 #if GVOX_LIN_PREFETCH
   float4 na, nb, nc;
-  if (begin + tid < end) {
-    na = __ldg(Ap + begin + tid);
-    nb = __ldg(Bp + begin + tid);
-    nc = __ldg(Np + begin + tid);
+  if (tid < npts) {
+    na = __ldg(Ap + tid);
+    nb = __ldg(Bp + tid);
+    nc = __ldg(Np + tid);
   }
 #endif
-  for (int64_t k = begin + tid; k < end; k += kThreads) {
+  for (int32_t k = tid; k < npts; k += kThreads) {
 #if GVOX_LIN_PREFETCH
     const float4 a = na, b = nb, c = nc;
-    if (k + kThreads < end) {
+    if (k + kThreads < npts) {
       na = __ldg(Ap + k + kThreads);
       nb = __ldg(Bp + k + kThreads);
       nc = __ldg(Np + k + kThreads);
@@ -386,12 +417,15 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     if (validate && invisible(sh, a, c)) {
       ++ac.n_invisible;
       if (corr)
-        for (int l = 0; l < L; ++l) corr[sh.corr_base + k * L + l] = -2;
+        for (int l = 0; l < L; ++l) corr_t[k * L + l] = -2;
       continue;
     }
     PointData pd;
     transform_point(sh, a, dyadic, r0, inv_r0, r0f, pd);
     bool have_rcr = false;
+    LevelSum ls;
+    ls.Oa = ls.Oc = ls.G = 0;
+    ls.o11 = ls.o22 = ls.gz = 0.f;
     // levels are processed in groups of G (all loads of a group in flight together)
     constexpr int G = MAXL < GVOX_LIN_G ? MAXL : GVOX_LIN_G;
 #pragma unroll
@@ -406,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       if (corr) {
         for (int j = 0; j < G && lb + j < L; ++j) {
           const int l = lb + j;
-          corr[sh.corr_base + k * L + l] =
+          corr_t[k * L + l] =
               vid[j] >= 0 ? (int64_t)pack_key(pd.k0x >> l, pd.k0y >> l, pd.k0z >> l) : -1;
         }
       }
@@ -431,8 +465,9 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       }
 #pragma unroll
       for (int j = 0; j < G; ++j)
-        if (vid[j] >= 0) level_algebra<MAXL>(ac, pd, v0[j], v1[j], v2[j], lb + j, r0f, error_only);
+        if (vid[j] >= 0) level_term<MAXL>(ac, ls, pd, v0[j], v1[j], v2[j], lb + j, r0f);
     }
+    if (have_rcr && !error_only) fold_point<MAXL>(ac, ls, pd);
   }
   tile_reduce<MAXL>(ac, red, partials, tile);
 }
