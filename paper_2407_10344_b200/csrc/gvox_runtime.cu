@@ -615,10 +615,11 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   int64_t vacc = 0;
   for (int64_t s = 0; s < count; ++s) {
     const gvox_cloud* c = clouds[s];
-    // fixed-point: F fraction bits so that n * 2^F <= 2^61
+    // fixed-point: F fraction bits so that n * 2^F <= 2^61 (voxel sums fit in
+    // int64) and F <= 46 (one value fits the kernel's two 32-bit REDUX chunks)
     int nb = 0;
     while ((1ll << nb) <= c->n) ++nb;  // 2^nb > n
-    int F = 61 - nb;
+    const int F = std::min(61 - nb, 46);
     int ec = 0;
     if (c->cmax > 0.f) {
       std::frexp((double)c->cmax, &ec);  // cmax < 2^ec

@@ -88,6 +88,8 @@ __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restri
 
 // Grids are 2D: blockIdx.y = segment (cloud), blockIdx.x * blockDim.x +
 // threadIdx.x = point within it, so a block never straddles two maps.
+constexpr int kMaxL = GVOX_MAX_LEVELS;
+
 __global__ void k_build_insert(const BuildSeg* __restrict__ segs, int levels, double r0,
                                double inv_r0, int dyadic, int32_t* __restrict__ pslot,
                                int32_t* __restrict__ err) {
@@ -103,36 +105,52 @@ __global__ void k_build_insert(const BuildSeg* __restrict__ segs, int levels, do
     k0y = voxel_coord0((double)a.y, r0, inv_r0, dyadic);
     k0z = voxel_coord0((double)a.z, r0, inv_r0, dyadic);
   }
-  for (int l = 0; l < levels; ++l) {
+  // 1) keys and warp groups of every level; 2) the group leaders' first CAS of
+  // every level issued back to back (independent L2 round trips in flight
+  // together); 3) collisions resolved by linear probing; 4) new voxels take
+  // consecutive indices with one atomicAdd per warp and level.
+  uint64_t key[kMaxL];
+  uint64_t h[kMaxL];
+  unsigned long long prev[kMaxL];
+  bool lead[kMaxL];
+  int leader[kMaxL];
+#pragma unroll
+  for (int l = 0; l < kMaxL; ++l) {
+    lead[l] = false;
+    leader[l] = 0;
+    if (l >= levels) continue;
     // floor(x / r_l) = floor(x / r0) >> l exactly (r_l = r0 2^l)
     const int32_t kx = k0x >> l, ky = k0y >> l, kz = k0z >> l;
     const bool inr = valid && key_in_range(kx) && key_in_range(ky) && key_in_range(kz);
     if (valid && !inr) atomicOr(err, 1);
     // real keys are < 2^63; dummies (~0 - lane) are distinct and never inserted
-    const uint64_t key = inr ? pack_key(kx, ky, kz) : ~0ull - (uint64_t)lane;
-    const unsigned grp = __match_any_sync(0xffffffffu, key);
-    const int leader = __ffs(grp) - 1;
-    // leaders claim their key's slot: CAS first (one L2 round trip when the
-    // slot is empty or already holds the key), linear probing on collision
-    int32_t h_out = -1;
-    bool is_new = false;
-    if (lane == leader && inr) {
-      ulonglong2* slots = sg.tmp_slots[l];
-      uint64_t h = hash_slot(key, sg.tmp_shift);
-      for (;;) {
-        unsigned long long* kp = reinterpret_cast<unsigned long long*>(&slots[h].x);
-        const unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
-        if (prev == kEmptyKey) {
-          is_new = true;
-          break;
-        }
-        if (prev == key) break;
-        h = (h + 1) & sg.tmp_mask;
-      }
-      h_out = (int32_t)h;
+    key[l] = inr ? pack_key(kx, ky, kz) : ~0ull - (uint64_t)lane;
+    const unsigned grp = __match_any_sync(0xffffffffu, key[l]);
+    leader[l] = __ffs(grp) - 1;
+    lead[l] = lane == leader[l] && inr;
+  }
+#pragma unroll
+  for (int l = 0; l < kMaxL; ++l) {
+    if (lead[l]) {
+      h[l] = hash_slot(key[l], sg.tmp_shift);
+      prev[l] = atomicCAS(reinterpret_cast<unsigned long long*>(&sg.tmp_slots[l][h[l]].x), kEmptyKey,
+                          key[l]);
     }
-    // new voxels take consecutive indices: one atomicAdd per warp (all lanes of
-    // a block belong to the same map and level)
+  }
+#pragma unroll
+  for (int l = 0; l < kMaxL; ++l) {
+    if (l >= levels) break;
+    bool is_new = false;
+    int32_t h_out = -1;
+    if (lead[l]) {
+      while (prev[l] != kEmptyKey && prev[l] != key[l]) {
+        h[l] = (h[l] + 1) & sg.tmp_mask;
+        prev[l] = atomicCAS(reinterpret_cast<unsigned long long*>(&sg.tmp_slots[l][h[l]].x),
+                            kEmptyKey, key[l]);
+      }
+      is_new = prev[l] == kEmptyKey;
+      h_out = (int32_t)h[l];
+    }
     const unsigned new_mask = __ballot_sync(0xffffffffu, is_new);
     if (new_mask) {
       int32_t base = 0;
@@ -142,25 +160,17 @@ __global__ void k_build_insert(const BuildSeg* __restrict__ segs, int levels, do
       if (is_new) {
         const int32_t idx = base + __popc(new_mask & ((1u << lane) - 1u));
         sg.tmp_slots[l][h_out].y = (unsigned long long)(uint32_t)idx | 0xFFFFFFFF00000000ull;
-        sg.keys_by_idx[l][idx] = key;
+        sg.keys_by_idx[l][idx] = key[l];
       }
     }
-    h_out = __shfl_sync(0xffffffffu, h_out, leader);
+    h_out = __shfl_sync(0xffffffffu, h_out, leader[l]);
+    const bool inr = key[l] < (1ull << 63);
     if (valid) pslot[sg.pl_offset + k * levels + l] = inr ? h_out : -1;
   }
 }
 
 __device__ inline unsigned long long to_fixed(double x) {
   return (unsigned long long)__double2ll_rn(x);
-}
-
-// Sum of a 64-bit integer over the lanes of `grp` (two's complement, mod 2^64)
-// with 32-bit REDUX on three 22-bit chunks (<= 32 * 2^22 < 2^32: no overflow).
-__device__ inline unsigned long long group_sum_u64(unsigned grp, unsigned long long v) {
-  const unsigned c0 = __reduce_add_sync(grp, (unsigned)(v & 0x3FFFFFull));
-  const unsigned c1 = __reduce_add_sync(grp, (unsigned)((v >> 22) & 0x3FFFFFull));
-  const unsigned c2 = __reduce_add_sync(grp, (unsigned)(v >> 44));
-  return (unsigned long long)c0 + ((unsigned long long)c1 << 22) + ((unsigned long long)c2 << 44);
 }
 
 __global__ void k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg* __restrict__ segs,
@@ -188,7 +198,6 @@ __global__ void k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg
     const int32_t sl = valid ? pslot[sg.pl_offset + k * levels + l] : -1;
     const int32_t idx = sl >= 0 ? (int32_t)(uint32_t)bs.tmp_slots[l][sl].y : -1 - lane;
     const unsigned grp = __match_any_sync(0xffffffffu, idx);
-    const int leader = __ffs(grp) - 1;
     unsigned long long v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (sl >= 0) {
       const double r = ldexp(r0, l);
@@ -200,14 +209,36 @@ __global__ void k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg
 #pragma unroll
       for (int j = 0; j < 6; ++j) v[3 + j] = to_fixed((double)cv[j] * sg.cov_scale);
     }
-    unsigned long long sum[9];
+    // group sums: one iteration per distinct group of the warp, each a set of
+    // full-mask REDUX.SUM (uniform mask: the fast path) over two 32-bit chunks
+    // of the fixed-point values (|v| < 2^46: low 24 bits unsigned, high part
+    // signed; 32 lanes cannot overflow either chunk)
+    unsigned lo_c[9];
+    int hi_c[9];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) sum[j] = group_sum_u64(grp, v[j]);
-    if (lane == leader && sl >= 0) {
-      unsigned long long* dst = acc + (sg.acc_offset[l] + idx) * 10;
+    for (int j = 0; j < 9; ++j) {
+      lo_c[j] = (unsigned)(v[j] & 0xFFFFFFull);
+      hi_c[j] = (int)((long long)v[j] >> 24);
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, sl >= 0);
+    while (todo) {
+      const int ld = __ffs(todo) - 1;
+      const unsigned g = __shfl_sync(0xffffffffu, grp, ld);
+      const bool in = (g >> lane) & 1u;
+      unsigned long long sum[9];
 #pragma unroll
-      for (int j = 0; j < 9; ++j) atomicAdd(dst + j, sum[j]);
-      atomicAdd(dst + 9, (unsigned long long)__popc(grp));
+      for (int j = 0; j < 9; ++j) {
+        const unsigned sl_ = __reduce_add_sync(0xffffffffu, in ? lo_c[j] : 0u);
+        const int sh_ = __reduce_add_sync(0xffffffffu, in ? hi_c[j] : 0);
+        sum[j] = (unsigned long long)((long long)sh_ * (1ll << 24)) + (unsigned long long)sl_;
+      }
+      if (lane == ld) {
+        unsigned long long* dst = acc + (sg.acc_offset[l] + idx) * 10;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) atomicAdd(dst + j, sum[j]);
+        atomicAdd(dst + 9, (unsigned long long)__popc(g));
+      }
+      todo &= ~g;
     }
   }
 }
