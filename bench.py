@@ -42,6 +42,7 @@ WORKLOADS = {
     "C4": "C4 global: 500 submaps x 50k points, overlap-selected factors, r = 0.5/1/2 m",
     "C3": "C3 smoother window: 30 frames x 10 keyframe factors x 20k points, r = 0.25/0.5/1 m",
     "C2": "C2 odometry step: one 20k frame vs 10 keyframe maps, r = 0.25/0.5/1 m",
+    "C1": "C1 single factor: 1k-point source vs 1k-point map, r = 1.0 m, L = 1",
 }
 
 
@@ -55,7 +56,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C5", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="C5", choices=sorted(WORKLOADS),
+                    help="workload; the bench line is C5 (the metric's config), the others "
+                         "report per-call latency of the small configs")
     ap.add_argument("--submaps", type=int, default=None, help="override the submap count (tests)")
     ap.add_argument("--order", default="morton", choices=["morton", "random"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -151,11 +154,12 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- oracle legs
-def oracle_sample(sc, selected_pairs_mask=None, budget_s=12.0, threads=None):
+def oracle_sample(sc, select=True, budget_s=12.0, threads=None):
     """The oracle, as it stands, on a bounded sample of the same step: all rows
-    (map build, overlap, selection, linearize) for a contiguous block of target
-    submaps, so the mix of work matches the full step.  Returns (points, seconds,
-    description, cores)."""
+    (map build, overlap, selection, linearize) for a random subset of target
+    maps, so the mix of work matches the full step.  select: C4/C5 factors are
+    the candidates with 20 * count > N; otherwise the config's factor list.
+    Returns (points, seconds, description, cores)."""
     from oracle import oracle
     import synth
     cores = threads or synth.host_threads()
@@ -170,19 +174,24 @@ def oracle_sample(sc, selected_pairs_mask=None, budget_s=12.0, threads=None):
     used = []
     for t in order:
         pr = sc.pairs[sc.pairs[:, 1] == t]
-        if len(pr) == 0:
+        fr = sc.factors[sc.factors[:, 1] == t]
+        if len(pr) == 0 and len(fr) == 0:
             continue
         mu_t, cov_t, _ = sc.cloud(int(sc.map_clouds[t]))
         om = oracle.VoxelMap(mu_t, cov_t, sc.r0, sc.levels)                     # S1
-        srcs = sorted(set(int(p[0]) for p in pr))
-        idx = {s: k for k, s in enumerate(srcs)}
-        pairs = np.array([[idx[int(p[0])], 0, int(p[2]), int(p[3])] for p in pr], np.int64)
-        counts = oracle.overlap_batch([sc.cloud(s)[0] for s in srcs], [om], pairs, sc.poses,
+        srcs = sorted(set(int(p[0]) for p in pr) | set(int(f[0]) for f in fr))
+        idx = {s_: k for k, s_ in enumerate(srcs)}
+        pairs = np.array([[idx[int(p[0])], 0, int(p[2]), int(p[3])] for p in pr], np.int64).reshape(-1, 4)
+        counts = oracle.overlap_batch([sc.cloud(s_)[0] for s_ in srcs], [om], pairs, sc.poses,
                                       sc.overlap_level, cores)                  # S2
-        sel = 20 * counts > n[[srcs[int(p[0])] for p in pairs]]
-        fac = np.concatenate([pairs[sel], np.zeros((int(sel.sum()), 1), np.int64)], 1)
+        if select:
+            sel = 20 * counts > n[[srcs[int(p[0])] for p in pairs]]
+            fac = np.concatenate([pairs[sel], np.zeros((int(sel.sum()), 1), np.int64)], 1)
+        else:
+            fac = np.array([[idx[int(f[0])], 0, int(f[2]), int(f[3]), int(f[4])] for f in fr],
+                           np.int64).reshape(-1, 5)
         if len(fac):
-            oracle.linearize_batch([sc.cloud(s) for s in srcs], [om], fac, sc.poses, cores)  # S3-7
+            oracle.linearize_batch([sc.cloud(s_) for s_ in srcs], [om], fac, sc.poses, cores)  # S3-7
         pts += int(n[[srcs[int(f[0])] for f in fac]].sum()) if len(fac) else 0
         nf += len(fac)
         npairs += len(pairs)
@@ -190,8 +199,8 @@ def oracle_sample(sc, selected_pairs_mask=None, budget_s=12.0, threads=None):
         if time.perf_counter() - t0 >= budget_s:
             break
     dt = time.perf_counter() - t0
-    desc = (f"{len(used)} of {M} target submaps (random, seed 12345) with all their rows: "
-            f"{len(used)} map builds, {npairs} overlap pairs, {nf} selected factors "
+    desc = (f"{len(used)} of {M} target maps (random, seed 12345) with all their rows: "
+            f"{len(used)} map builds, {npairs} overlap pairs, {nf} factors "
             f"({pts} source points)")
     return pts, dt, desc, cores
 
@@ -206,7 +215,7 @@ def run_reference(args):
     cores = None
     for i in range(args.warmup + args.steps):
         budget = max(2.0, 120.0 / max(1, args.warmup + args.steps))
-        pts, dt, desc, cores = oracle_sample(sc, budget_s=budget)
+        pts, dt, desc, cores = oracle_sample(sc, args.config in ("C4", "C5"), budget_s=budget)
         if i >= args.warmup:
             samples.append((pts, dt))
     tot_p = sum(p for p, _ in samples)
@@ -280,10 +289,18 @@ def main():
     pairs_s = gv.as_pairs(my_pairs)
     src_n = n_pts[my_pairs[:, 0]]
     my_target_clouds = [clouds[int(sc.map_clouds[t])] for t in my_targets]
+    # C4/C5: factors = candidate pairs whose overlap exceeds 5 %, no
+    # validation (Q7).  C1-C3: the config's own factor list (odometry factors,
+    # validation on); the overlap of their pairs is still screened.
+    select = args.config in ("C4", "C5")
+    if not select:
+        fm = (sc.factors[:, 1] >= t_lo) & (sc.factors[:, 1] < t_hi)
+        fixed = gv.as_factors(sc.factors[fm])
+        fixed["target_map"] -= t_lo
     flags = 0
 
     # device buffers reused across steps
-    acc_out = gv.device_records(ctx, max(len(my_pairs), 1), gv.FACTOR_ACCUM_DTYPE)
+    acc_out = gv.device_records(ctx, max(len(my_pairs), len(sc.factors), 1), gv.FACTOR_ACCUM_DTYPE)
     counts_h = np.zeros(len(my_pairs), np.int32)
 
     state = {}
@@ -292,13 +309,16 @@ def main():
         maps = gv.create_voxelmaps(ctx, my_target_clouds, sc.r0, sc.levels)        # S1
         marr = gv.HandleArray(maps)
         gv.overlap(ctx, cloud_arr, marr, pairs_s, poses, sc.overlap_level, out=counts_h)  # S2
-        sel = 20 * counts_h.astype(np.int64) > src_n
-        fac = np.empty(int(sel.sum()), gv.FACTOR_DTYPE)
-        fac["source_cloud"] = my_pairs[sel, 0]
-        fac["target_map"] = my_pairs[sel, 1]
-        fac["pose_i"] = my_pairs[sel, 2]
-        fac["pose_j"] = my_pairs[sel, 3]
-        fac["flags"] = flags
+        if select:
+            sel = 20 * counts_h.astype(np.int64) > src_n
+            fac = np.empty(int(sel.sum()), gv.FACTOR_DTYPE)
+            fac["source_cloud"] = my_pairs[sel, 0]
+            fac["target_map"] = my_pairs[sel, 1]
+            fac["pose_i"] = my_pairs[sel, 2]
+            fac["pose_j"] = my_pairs[sel, 3]
+            fac["flags"] = flags
+        else:
+            fac = fixed
         out = acc_out[:len(fac)]
         gv.linearize_batch_accum(ctx, cloud_arr, marr, fac, poses, out=out)         # S3-S7
         if world > 1:
@@ -306,7 +326,7 @@ def main():
             state["gathered"], _ = gdist.gather_records(acc_out, len(fac), state["fmax"])
         state["maps"] = maps                  # keep alive until the next step replaces them
         state["fac"] = fac
-        return int(src_n[sel].sum()), len(fac)
+        return int(n_pts[fac["source_cloud"]].sum()), len(fac)
 
     # ---- warm-up (also sizes the gather)
     if world > 1:
@@ -416,7 +436,7 @@ def main():
         cov_h = torch.from_numpy(sc.cov).pin_memory()
         nrm_h = torch.from_numpy(sc.nrm).pin_memory()
         k_e2e = max(1, min(args.steps, 3))
-        pin_out = np.zeros(len(my_pairs), gv.LINEAR_FACTOR_DTYPE)
+        pin_out = np.zeros(max(len(my_pairs), len(sc.factors)), gv.LINEAR_FACTOR_DTYPE)
         h2d = 0
         d2h = 0
 
@@ -438,17 +458,20 @@ def main():
                                          sc.r0, sc.levels)
             marr = gv.HandleArray(maps_e)
             cnt = gv.overlap(ctx, carr, marr, pairs_s, poses, sc.overlap_level)
-            sel = 20 * cnt.astype(np.int64) > src_n
-            fe = np.empty(int(sel.sum()), gv.FACTOR_DTYPE)
-            fe["source_cloud"] = my_pairs[sel, 0]
-            fe["target_map"] = my_pairs[sel, 1]
-            fe["pose_i"] = my_pairs[sel, 2]
-            fe["pose_j"] = my_pairs[sel, 3]
-            fe["flags"] = flags
+            if select:
+                sel = 20 * cnt.astype(np.int64) > src_n
+                fe = np.empty(int(sel.sum()), gv.FACTOR_DTYPE)
+                fe["source_cloud"] = my_pairs[sel, 0]
+                fe["target_map"] = my_pairs[sel, 1]
+                fe["pose_i"] = my_pairs[sel, 2]
+                fe["pose_j"] = my_pairs[sel, 3]
+                fe["flags"] = flags
+            else:
+                fe = fixed
             res = gv.linearize_batch(ctx, carr, marr, fe, poses, out=pin_out[:len(fe)])
             h2d = h2d_b + poses.nbytes * 2 + pairs_s.nbytes + fe.nbytes
             d2h = cnt.nbytes + res.nbytes
-            return int(src_n[sel].sum())
+            return int(n_pts[fe["source_cloud"]].sum())
 
         e2e_step()
         torch.cuda.synchronize()
@@ -479,7 +502,7 @@ def main():
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        pts_o, dt_o, desc, cores = oracle_sample(sc, budget_s=args.cpu_seconds)
+        pts_o, dt_o, desc, cores = oracle_sample(sc, select, budget_s=args.cpu_seconds)
         cpu = {"value": pts_o / dt_o, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": desc, "seconds": dt_o}
 
