@@ -37,8 +37,8 @@ struct CloudDev {
 
 // One level of a map.  Voxel lookup uses either
 //  * a DENSE index grid over the level's key bounding box (int32 voxel index
-//    or -1 per cell; chosen when the box has at most kDenseRatio cells per
-//    voxel): one predicated load, no probing; or
+//    or -1 per cell; chosen before the build when the box has at most
+//    kDenseBuildRatio cells per point): one predicated load, no probing; or
 //  * the open-addressing HASH table (sparse / very large extents).
 struct __align__(16) MapLevelDev {
   // dense-grid fields first, 16 B aligned: two vector loads per lookup
@@ -58,7 +58,7 @@ struct __align__(16) MapLevelDev {
   int32_t pad;
 };
 
-constexpr int kDenseRatio = 256;  // max cells per voxel for a dense grid level
+constexpr int kDenseBuildRatio = 48;  // max cells per POINT for a dense grid level
 
 struct MapDev {
   int32_t levels;
@@ -123,20 +123,30 @@ __host__ __device__ inline float ordered_to_float(int32_t i) {
 #endif
 }
 
-// voxelmap build, phase 1: insert keys of every (cloud point, level) into the
-// per-(map, level) temporary tables; assign compact voxel indices.
+// voxelmap build.  A level is DENSE (an int32 index grid over its key box,
+// decided before the build from the cloud's bounding box) or HASH (sparse
+// extents).  Phase 1 assigns each new voxel a compact index: dense levels CAS
+// the final grid cell directly; hash levels insert into a temporary table and
+// record per (point, level) the slot of their key.
+struct LevelBox {
+  int32_t x0, y0, z0;
+  uint32_t dx, dy, dz, syz;
+  int32_t dense;
+  int32_t* grid;            // dense: the map's final grid (0xFF-filled), else nullptr
+};
 struct BuildSeg {
   const float4* A;          // cloud means (+C.xx)
   int64_t n;                // points
   int64_t pl_offset;        // offset of this cloud's (point, level) records
-  ulonglong2* tmp_slots[GVOX_MAX_LEVELS];  // temp tables (capacity tmp_mask+1)
+  ulonglong2* tmp_slots[GVOX_MAX_LEVELS];  // hash levels: temp tables (capacity tmp_mask+1)
   uint64_t tmp_mask;
   int32_t tmp_shift;
   int32_t pad;
   uint64_t* keys_by_idx[GVOX_MAX_LEVELS];  // [n] workspace: key of voxel idx
   int32_t* counter;         // [levels] voxel counts (atomic)
-  // phase 1 records, per (point, level), the temp-table SLOT of its key;
-  // phase 2 reads the voxel index from that slot (all indices assigned by then).
+  LevelBox box[GVOX_MAX_LEVELS];
+  // hash levels: phase 1 records, per (point, level), the temp-table SLOT of its
+  // key; phase 2 reads the voxel index from that slot (all assigned by then).
 };
 void launch_build_insert(const BuildSeg* segs_dev, int64_t num_segs, int64_t max_seg_points,
                          int levels, double r0, int dyadic, int32_t* pslot, int32_t* err,

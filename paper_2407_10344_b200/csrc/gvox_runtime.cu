@@ -156,7 +156,8 @@ struct gvox_cloud {
 };
 
 struct gvox_map {
-  std::shared_ptr<DevBuf> arena;
+  std::shared_ptr<DevBuf> arena;       // descriptors, hash tables, voxel records, keys
+  std::shared_ptr<DevBuf> grid_arena;  // dense index grids
   MapDev desc{};         // host copy
   MapDev* dev = nullptr;
   int levels = 0;
@@ -467,29 +468,82 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
                         int levels, gvox_map** maps_out) {
   const int dyadic = is_dyadic(r0);
   const int L = levels;
-  // ---- phase 1 layout (workspace 0)
   std::vector<int64_t> seg_start(count + 1, 0);
   for (int64_t s = 0; s < count; ++s) seg_start[s + 1] = seg_start[s] + clouds[s]->n;
   const int64_t total = seg_start[count];
   int64_t max_pts = 0;
   for (int64_t s = 0; s < count; ++s) max_pts = std::max<int64_t>(max_pts, clouds[s]->n);
+
+  // ---- level plans from the clouds' bounding boxes (before any voxel exists).
+  // Dense: an int32 grid over the level's key box when it has at most
+  // kDenseBuildRatio cells per point (memory <= 4 kDenseBuildRatio B per
+  // point and level), every dimension < 2^30 (the lookups rely on it) and
+  // < 2^31 cells.  Otherwise a hash table sized after the voxel count is known.
+  struct LevelPlan {
+    bool dense = false;
+    int32_t x0 = 0, y0 = 0, z0 = 0;
+    uint32_t dx = 0, dy = 0, dz = 0;
+    uint64_t cells = 0;
+    uint64_t cap = 0;  // hash capacity
+    size_t o_grid = 0, o_slots = 0, o_vox = 0, o_keys = 0;
+  };
+  std::vector<LevelPlan> plan((size_t)count * L);
+  Layout gl;  // grid arena
+  for (int64_t s = 0; s < count; ++s) {
+    const gvox_cloud* c = clouds[s];
+    int32_t k0lo[3] = {0, 0, 0}, k0hi[3] = {0, 0, 0};
+    for (int a = 0; a < 3; ++a) {
+      // the device key formula (voxel_coord0), evaluated on the host; clamped
+      double slo = dyadic ? (double)c->lo[a] * (1.0 / r0) : (double)c->lo[a] / r0;
+      double shi = dyadic ? (double)c->hi[a] * (1.0 / r0) : (double)c->hi[a] / r0;
+      double flo = std::floor(slo), fhi = std::floor(shi);
+      k0lo[a] = (int32_t)std::min(std::max(flo, -1073741824.0), 1073741824.0);
+      k0hi[a] = (int32_t)std::min(std::max(fhi, -1073741824.0), 1073741824.0);
+    }
+    for (int l = 0; l < L; ++l) {
+      LevelPlan& p = plan[s * L + l];
+      uint64_t cells = 1;
+      int32_t lo3[3], n3[3];
+      for (int a = 0; a < 3; ++a) {
+        lo3[a] = k0lo[a] >> l;
+        n3[a] = (k0hi[a] >> l) - lo3[a] + 1;
+        cells *= (uint64_t)n3[a];
+      }
+      const bool dims_ok = n3[0] < (1 << 30) && n3[1] < (1 << 30) && n3[2] < (1 << 30);
+      if (c->n > 0 && dims_ok && cells <= (uint64_t)kDenseBuildRatio * (uint64_t)c->n &&
+          cells < (1ull << 31)) {
+        p.dense = true;
+        p.x0 = lo3[0]; p.y0 = lo3[1]; p.z0 = lo3[2];
+        p.dx = n3[0]; p.dy = n3[1]; p.dz = n3[2];
+        p.cells = cells;
+        p.o_grid = gl.add(cells * 4);
+      }
+    }
+  }
+  std::shared_ptr<DevBuf> grid_arena;
+  gvox_status st = devbuf_alloc(gl.size, ctx->device, ctx->stream, &grid_arena);
+  if (st) return st;
+  char* gb = (char*)grid_arena->ptr;
+  if (gl.size) CK(cudaMemsetAsync(gb, 0xFF, gl.size, ctx->stream));  // every cell -1 (empty)
+
+  // ---- phase 1 workspace (workspace 0): hash-level temp tables, keys, slots
   std::vector<uint64_t> tcap(count);
   Layout lay;
   std::vector<size_t> o_tmp(count), o_keys(count);
-  // all temporary tables first (one contiguous region -> one memset)
+  std::vector<int> nhash(count, 0);
   for (int64_t s = 0; s < count; ++s) {
     tcap[s] = pow2_at_least(std::max<uint64_t>(16, 2 * (uint64_t)clouds[s]->n));
-    o_tmp[s] = lay.add(tcap[s] * 16 * L);
+    for (int l = 0; l < L; ++l) nhash[s] += !plan[s * L + l].dense;
+    o_tmp[s] = lay.add(tcap[s] * 16 * nhash[s]);
   }
-  const size_t tmp_bytes = lay.size;
+  const size_t tmp_bytes = lay.size;  // temp tables first: one 0xFF memset
   for (int64_t s = 0; s < count; ++s) o_keys[s] = lay.add((size_t)clouds[s]->n * 8 * L);
   size_t o_pslot = lay.add((size_t)total * L * 4);
   size_t o_cnt = lay.add((size_t)count * L * 4 + 4);
   size_t o_bseg = lay.add(sizeof(BuildSeg) * count);
   size_t o_aseg = lay.add(sizeof(AccumSeg) * count);
-  size_t o_start = lay.add(8 * (count + 1));
   void* ws0 = nullptr;
-  gvox_status st = ws_reserve(ctx, 0, lay.size, &ws0);
+  st = ws_reserve(ctx, 0, lay.size, &ws0);
   if (st) return st;
   char* b0 = (char*)ws0;
   int32_t* d_cnt = (int32_t*)(b0 + o_cnt);
@@ -504,18 +558,26 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     g.pl_offset = seg_start[s] * L;
     g.tmp_mask = tcap[s] - 1;
     g.tmp_shift = shift_for_capacity(tcap[s]);
+    int hslot = 0;
     for (int l = 0; l < L; ++l) {
-      g.tmp_slots[l] = (ulonglong2*)(b0 + o_tmp[s]) + tcap[s] * l;
+      const LevelPlan& p = plan[s * L + l];
+      LevelBox& bx = g.box[l];
+      bx.dense = p.dense;
+      if (p.dense) {
+        bx.x0 = p.x0; bx.y0 = p.y0; bx.z0 = p.z0;
+        bx.dx = p.dx; bx.dy = p.dy; bx.dz = p.dz;
+        bx.syz = p.dy * p.dz;
+        bx.grid = (int32_t*)(gb + p.o_grid);
+      } else {
+        g.tmp_slots[l] = (ulonglong2*)(b0 + o_tmp[s]) + tcap[s] * hslot++;
+      }
       g.keys_by_idx[l] = (uint64_t*)(b0 + o_keys[s]) + (size_t)clouds[s]->n * l;
     }
     g.counter = d_cnt + s * L;
   }
-  // tables -> EMPTY (all 0xFF: key ~0, idx -1), counters + err -> 0
-  CK(cudaMemsetAsync(b0, 0xFF, tmp_bytes, ctx->stream));
+  if (tmp_bytes) CK(cudaMemsetAsync(b0, 0xFF, tmp_bytes, ctx->stream));
   CK(cudaMemsetAsync(d_cnt, 0, (size_t)count * L * 4 + 4, ctx->stream));
   CK(cudaMemcpyAsync(b0 + o_bseg, bseg.data(), sizeof(BuildSeg) * count, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  CK(cudaMemcpyAsync(b0 + o_start, seg_start.data(), 8 * (count + 1), cudaMemcpyHostToDevice,
                      ctx->stream));
   {
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
@@ -531,59 +593,20 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     return fail(GVOX_ERR_RANGE,
                 "gvox_create_voxelmap: a voxel key is outside [-2^20, 2^20) (r0 = %g)", r0);
 
-  // ---- final arena (exact sizes).  Per level: a dense index grid over the
-  // key box of the cloud when it has at most kDenseRatio cells per voxel,
-  // else a hash table with capacity 2^k >= 2V.
-  struct LevelPlan {
-    uint64_t cap = 0;  // hash capacity (0 = dense)
-    int32_t x0 = 0, y0 = 0, z0 = 0;
-    uint32_t dx = 0, dy = 0, dz = 0;
-    uint64_t cells = 0;
-    size_t o_slots = 0, o_grid = 0, o_vox = 0, o_keys = 0;
-  };
+  // ---- record arena (exact sizes): descriptors, hash tables, voxel records, keys
   Layout al;
   std::vector<size_t> o_desc(count);
-  std::vector<LevelPlan> plan((size_t)count * L);
   int64_t total_vox = 0;
   for (int64_t s = 0; s < count; ++s) o_desc[s] = al.add(sizeof(MapDev));
-  // index structures (grids, hash slots) first: one contiguous 0xFF memset
-  const size_t idx_begin = al.size;
-  for (int64_t s = 0; s < count; ++s) {
-    const gvox_cloud* c = clouds[s];
-    int32_t k0lo[3] = {0, 0, 0}, k0hi[3] = {0, 0, 0};
-    for (int a = 0; a < 3; ++a) {
-      // the device key formula (voxel_coord0), evaluated on the host; clamped
-      double slo = dyadic ? (double)c->lo[a] * (1.0 / r0) : (double)c->lo[a] / r0;
-      double shi = dyadic ? (double)c->hi[a] * (1.0 / r0) : (double)c->hi[a] / r0;
-      double flo = std::floor(slo), fhi = std::floor(shi);
-      k0lo[a] = (int32_t)std::min(std::max(flo, -1073741824.0), 1073741824.0);
-      k0hi[a] = (int32_t)std::min(std::max(fhi, -1073741824.0), 1073741824.0);
-    }
+  const size_t idx_begin = al.size;  // final hash tables: one 0xFF memset
+  for (int64_t s = 0; s < count; ++s)
     for (int l = 0; l < L; ++l) {
-      int64_t V = hcnt[s * L + l];
       LevelPlan& p = plan[s * L + l];
-      uint64_t cells = 1;
-      int32_t lo3[3], n3[3];
-      for (int a = 0; a < 3; ++a) {
-        lo3[a] = k0lo[a] >> l;
-        n3[a] = (k0hi[a] >> l) - lo3[a] + 1;
-        cells *= (uint64_t)n3[a];
-      }
-      // dense grid: each dimension < 2^30 (the kernels rely on it to skip
-      // clamping saturated coordinates) and at most kDenseRatio cells per voxel
-      const bool dims_ok = n3[0] < (1 << 30) && n3[1] < (1 << 30) && n3[2] < (1 << 30);
-      if (V > 0 && dims_ok && cells <= (uint64_t)kDenseRatio * (uint64_t)V && cells < (1ull << 31)) {
-        p.x0 = lo3[0]; p.y0 = lo3[1]; p.z0 = lo3[2];
-        p.dx = n3[0]; p.dy = n3[1]; p.dz = n3[2];
-        p.cells = cells;
-        p.o_grid = al.add(cells * 4);
-      } else {
-        p.cap = pow2_at_least(std::max<uint64_t>(2, 2 * (uint64_t)V));
+      if (!p.dense) {
+        p.cap = pow2_at_least(std::max<uint64_t>(2, 2 * (uint64_t)hcnt[s * L + l]));
         p.o_slots = al.add(p.cap * 16);
       }
-      total_vox += V;
     }
-  }
   const size_t idx_end = al.size;
   for (int64_t s = 0; s < count; ++s)
     for (int l = 0; l < L; ++l) {
@@ -591,6 +614,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       LevelPlan& p = plan[s * L + l];
       p.o_vox = al.add((size_t)V * 48);
       p.o_keys = al.add((size_t)V * 8);
+      total_vox += V;
     }
   std::shared_ptr<DevBuf> arena;
   st = devbuf_alloc(al.size, ctx->device, ctx->stream, &arena);
@@ -600,17 +624,15 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   Layout l1;
   size_t o_acc = l1.add((size_t)total_vox * 80);
   size_t o_fseg = l1.add(sizeof(FinalSeg) * count * L);
-  size_t o_vstart = l1.add(8 * ((size_t)count * L + 1));
   void* ws1 = nullptr;
   st = ws_reserve(ctx, 1, l1.size, &ws1);
   if (st) return st;
   char* b1 = (char*)ws1;
   CK(cudaMemsetAsync(b1 + o_acc, 0, (size_t)total_vox * 80, ctx->stream));
-  CK(cudaMemsetAsync(ab + idx_begin, 0xFF, idx_end - idx_begin, ctx->stream));
+  if (idx_end > idx_begin) CK(cudaMemsetAsync(ab + idx_begin, 0xFF, idx_end - idx_begin, ctx->stream));
 
   std::vector<AccumSeg> aseg(count);
   std::vector<FinalSeg> fseg((size_t)count * L);
-  std::vector<int64_t> vstart((size_t)count * L + 1, 0);
   std::vector<MapDev> mdesc(count);
   int64_t vacc = 0;
   for (int64_t s = 0; s < count; ++s) {
@@ -639,38 +661,36 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     md.r0 = r0;
     md.inv_r0 = 1.0 / r0;
     for (int l = 0; l < L; ++l) {
-      int64_t V = hcnt[s * L + l];
-      double r = std::ldexp(r0, l);
+      const int64_t V = hcnt[s * L + l];
+      const double r = std::ldexp(r0, l);
+      const LevelPlan& p = plan[s * L + l];
       a.acc_offset[l] = vacc;
       a.mu_scale[l] = std::ldexp(1.0, F) / r;
       FinalSeg& f = fseg[s * L + l];
+      std::memset(&f, 0, sizeof(f));
       f.acc_offset = vacc;
       f.nvox = V;
       f.keys_by_idx = bseg[s].keys_by_idx[l];
       f.r = r;
       f.mu_scale = a.mu_scale[l];
       f.cov_scale = a.cov_scale;
-      const LevelPlan& p = plan[s * L + l];
-      f.slots = p.cap ? (ulonglong2*)(ab + p.o_slots) : nullptr;
-      f.mask = p.cap ? p.cap - 1 : 0;
-      f.shift = p.cap ? shift_for_capacity(p.cap) : 64;
-      f.dense = p.cap == 0;
-      f.grid = p.cap ? nullptr : (int32_t*)(ab + p.o_grid);
-      f.x0 = p.x0; f.y0 = p.y0; f.z0 = p.z0;
-      f.dx = p.dx; f.dy = p.dy; f.dz = p.dz;
+      f.slots = p.dense ? nullptr : (ulonglong2*)(ab + p.o_slots);  // dense: grid built in phase 1
+      f.mask = p.dense ? 0 : p.cap - 1;
+      f.shift = p.dense ? 64 : shift_for_capacity(p.cap);
+      f.dense = p.dense;
+      f.grid = nullptr;
       f.vox = (float4*)(ab + p.o_vox);
       f.keys_out = (uint64_t*)(ab + p.o_keys);
-      vstart[s * L + l + 1] = vstart[s * L + l] + V;
       MapLevelDev& lv = md.lv[l];
       lv.slots = f.slots;
       lv.vox = f.vox;
       lv.mask = f.mask;
       lv.shift = f.shift;
-      lv.grid = f.grid;
-      lv.dense = f.dense;
-      lv.x0 = f.x0; lv.y0 = f.y0; lv.z0 = f.z0;
-      lv.dx = f.dx; lv.dy = f.dy; lv.dz = f.dz;
-      lv.syz = f.dy * f.dz;
+      lv.grid = p.dense ? (const int32_t*)(gb + p.o_grid) : nullptr;
+      lv.dense = p.dense;
+      lv.x0 = p.x0; lv.y0 = p.y0; lv.z0 = p.z0;
+      lv.dx = p.dx; lv.dy = p.dy; lv.dz = p.dz;
+      lv.syz = p.dy * p.dz;
       lv.r = r;
       lv.inv_r = 1.0 / r;
       lv.nvox = V;
@@ -680,8 +700,6 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   CK(cudaMemcpyAsync(b0 + o_aseg, aseg.data(), sizeof(AccumSeg) * count, cudaMemcpyHostToDevice,
                      ctx->stream));
   CK(cudaMemcpyAsync(b1 + o_fseg, fseg.data(), sizeof(FinalSeg) * count * L,
-                     cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(b1 + o_vstart, vstart.data(), 8 * ((size_t)count * L + 1),
                      cudaMemcpyHostToDevice, ctx->stream));
   {
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
@@ -707,6 +725,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   for (int64_t s = 0; s < count; ++s) {
     auto* m = new gvox_map;
     m->arena = arena;
+    m->grid_arena = grid_arena;
     m->desc = mdesc[s];
     m->dev = (MapDev*)(ab + o_desc[s]);
     m->levels = L;

@@ -132,9 +132,18 @@ __global__ void k_build_insert(const BuildSeg* __restrict__ segs, int levels, do
 #pragma unroll
   for (int l = 0; l < kMaxL; ++l) {
     if (lead[l]) {
-      h[l] = hash_slot(key[l], sg.tmp_shift);
-      prev[l] = atomicCAS(reinterpret_cast<unsigned long long*>(&sg.tmp_slots[l][h[l]].x), kEmptyKey,
-                          key[l]);
+      if (sg.box[l].dense) {
+        // dense level: claim the final grid cell (-1 -> -2); h = cell
+        const LevelBox& bx = sg.box[l];
+        h[l] = (uint64_t)((uint32_t)((k0x >> l) - bx.x0) * bx.syz +
+                          (uint32_t)((k0y >> l) - bx.y0) * bx.dz + (uint32_t)((k0z >> l) - bx.z0));
+        const int old = atomicCAS(bx.grid + h[l], -1, -2);
+        prev[l] = old == -1 ? kEmptyKey : key[l];  // "empty" = new voxel, else found
+      } else {
+        h[l] = hash_slot(key[l], sg.tmp_shift);
+        prev[l] = atomicCAS(reinterpret_cast<unsigned long long*>(&sg.tmp_slots[l][h[l]].x),
+                            kEmptyKey, key[l]);
+      }
     }
   }
 #pragma unroll
@@ -159,7 +168,10 @@ __global__ void k_build_insert(const BuildSeg* __restrict__ segs, int levels, do
       base = __shfl_sync(0xffffffffu, base, first);
       if (is_new) {
         const int32_t idx = base + __popc(new_mask & ((1u << lane) - 1u));
-        sg.tmp_slots[l][h_out].y = (unsigned long long)(uint32_t)idx | 0xFFFFFFFF00000000ull;
+        if (sg.box[l].dense)
+          sg.box[l].grid[h_out] = idx;
+        else
+          sg.tmp_slots[l][h_out].y = (unsigned long long)(uint32_t)idx | 0xFFFFFFFF00000000ull;
         sg.keys_by_idx[l][idx] = key[l];
       }
     }
@@ -195,8 +207,14 @@ __global__ void k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg
   const int32_t k0z = voxel_coord0(z, r0, inv_r0, dyadic);
   const float cv[6] = {a.w, b.x, b.y, b.z, b.w, c.x};
   for (int l = 0; l < levels; ++l) {
-    const int32_t sl = valid ? pslot[sg.pl_offset + k * levels + l] : -1;
-    const int32_t idx = sl >= 0 ? (int32_t)(uint32_t)bs.tmp_slots[l][sl].y : -1 - lane;
+    int32_t sl = valid ? pslot[sg.pl_offset + k * levels + l] : -1;
+    int32_t idx;
+    if (bs.box[l].dense) {
+      // dense level: the final grid holds the voxel index (phase 1 is complete)
+      idx = sl >= 0 ? __ldg(bs.box[l].grid + sl) : -1 - lane;
+    } else {
+      idx = sl >= 0 ? (int32_t)(uint32_t)bs.tmp_slots[l][sl].y : -1 - lane;
+    }
     const unsigned grp = __match_any_sync(0xffffffffu, idx);
     unsigned long long v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (sl >= 0) {
