@@ -299,28 +299,38 @@ def main():
         fixed["target_map"] -= t_lo
     flags = 0
 
+    all_fac = np.zeros(len(my_pairs), gv.FACTOR_DTYPE)  # every candidate as a factor
+    for i_, name_ in enumerate(("source_cloud", "target_map", "pose_i", "pose_j")):
+        all_fac[name_] = my_pairs[:, i_]
     # device buffers reused across steps
     acc_out = gv.device_records(ctx, max(len(my_pairs), len(sc.factors), 1), gv.FACTOR_ACCUM_DTYPE)
     counts_h = np.zeros(len(my_pairs), np.int32)
 
     state = {}
 
+    host_ms = {"build_call": 0.0, "overlap_call": 0.0, "select": 0.0, "linearize_call": 0.0,
+               "gather": 0.0}
+
     def step(timed_maps=None):
+        t0 = time.perf_counter()
         maps = gv.create_voxelmaps(ctx, my_target_clouds, sc.r0, sc.levels)        # S1
         marr = gv.HandleArray(maps)
+        t1 = time.perf_counter()
         gv.overlap(ctx, cloud_arr, marr, pairs_s, poses, sc.overlap_level, out=counts_h)  # S2
+        t2 = time.perf_counter()
         if select:
             sel = 20 * counts_h.astype(np.int64) > src_n
-            fac = np.empty(int(sel.sum()), gv.FACTOR_DTYPE)
-            fac["source_cloud"] = my_pairs[sel, 0]
-            fac["target_map"] = my_pairs[sel, 1]
-            fac["pose_i"] = my_pairs[sel, 2]
-            fac["pose_j"] = my_pairs[sel, 3]
-            fac["flags"] = flags
+            fac = all_fac[sel]
         else:
             fac = fixed
         out = acc_out[:len(fac)]
+        t3 = time.perf_counter()
         gv.linearize_batch_accum(ctx, cloud_arr, marr, fac, poses, out=out)         # S3-S7
+        t4 = time.perf_counter()
+        host_ms["build_call"] += 1e3 * (t1 - t0)
+        host_ms["overlap_call"] += 1e3 * (t2 - t1)
+        host_ms["select"] += 1e3 * (t3 - t2)
+        host_ms["linearize_call"] += 1e3 * (t4 - t3)
         if world > 1:
             # the one exchange: all-gather of the compact per-factor records
             state["gathered"], _ = gdist.gather_records(acc_out, len(fac), state["fmax"])
@@ -359,6 +369,8 @@ def main():
     ctx.enable_timing(True)
     ctx.timing(reset=True)
     gv.launch_count(reset=True)
+    for k_ in host_ms:
+        host_ms[k_] = 0.0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -427,6 +439,7 @@ def main():
         except (ValueError, KeyError):
             traffic = None
     stages = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for k, v in tm.items()}
+    stages["host_wall_ms_per_step"] = {k: v / args.steps for k, v in host_ms.items()}
     dominant = max(tm, key=lambda k: tm[k][0])
 
     # ---- e2e through the public API with host buffers (rank-local, N GPUs)
@@ -518,7 +531,8 @@ def main():
                        "factors_per_step": fac_all / args.steps, "levels": sc.levels, "r0": sc.r0,
                        "overlap_level": sc.overlap_level, "point_order": args.order,
                        "parallelism": f"factor-sharded x{world} (targets), NCCL all_gather",
-                       "l2": "inputs larger than L2 (clouds %.1f GB + maps %.1f GB on rank 0)"
+                       "l2": "inputs larger than L2 (clouds %.1f GB + voxel records %.1f GB + "
+                             "index grids on rank 0)"
                              % (len(sc.mu) * 48 / 1e9,
                                 sum(64 * v for v in n_levels_vox.values()) / 1e9),
                        "step": "S1 build all target maps + S2 overlap of all candidate pairs + "

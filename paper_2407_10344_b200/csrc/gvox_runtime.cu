@@ -595,9 +595,8 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
 
   // ---- record arena (exact sizes): descriptors, hash tables, voxel records, keys
   Layout al;
-  std::vector<size_t> o_desc(count);
   int64_t total_vox = 0;
-  for (int64_t s = 0; s < count; ++s) o_desc[s] = al.add(sizeof(MapDev));
+  const size_t o_descs = al.add(sizeof(MapDev) * count);  // contiguous: one H2D
   const size_t idx_begin = al.size;  // final hash tables: one 0xFF memset
   for (int64_t s = 0; s < count; ++s)
     for (int l = 0; l < L; ++l) {
@@ -716,18 +715,16 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
                           (const unsigned long long*)(b1 + o_acc), ctx->stream);
   }
   CK_LAUNCH("voxelmap finalize");
-  for (int64_t s = 0; s < count; ++s)
-    CK(cudaMemcpyAsync(ab + o_desc[s], &mdesc[s], sizeof(MapDev), cudaMemcpyHostToDevice,
-                       ctx->stream));
-  // the host vectors above are pageable: cudaMemcpyAsync has staged them on return,
-  // but keep the stream ordered before the next chunk reuses the workspaces.
-  CK(cudaStreamSynchronize(ctx->stream));
+  // (pageable sources: cudaMemcpyAsync has staged them when it returns; the
+  // stream orders the next chunk's reuse of the workspaces after this one)
+  CK(cudaMemcpyAsync(ab + o_descs, mdesc.data(), sizeof(MapDev) * count, cudaMemcpyHostToDevice,
+                     ctx->stream));
   for (int64_t s = 0; s < count; ++s) {
     auto* m = new gvox_map;
     m->arena = arena;
     m->grid_arena = grid_arena;
     m->desc = mdesc[s];
-    m->dev = (MapDev*)(ab + o_desc[s]);
+    m->dev = (MapDev*)(ab + o_descs) + s;
     m->levels = L;
     m->r0 = r0;
     m->device = ctx->device;

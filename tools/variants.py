@@ -11,16 +11,12 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "paper_2407_10344_b200", "build", "variants")
 VARIANTS = {
+    # linearize kernel (C5, r01 results in k_linearize.cu's knob comment)
     "base": [],
     "t256_b2": ["GVOX_LIN_THREADS=256", "GVOX_LIN_MINB=2"],
-    "nopf": ["GVOX_LIN_PREFETCH=0"],
-    "g1": ["GVOX_LIN_G=1"],
-    "g1_nopf_b3": ["GVOX_LIN_G=1", "GVOX_LIN_PREFETCH=0", "GVOX_LIN_MINB=3"],
-    "nopf_b3": ["GVOX_LIN_PREFETCH=0", "GVOX_LIN_MINB=3"],
-    "t128_b5": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=5", "GVOX_LIN_PREFETCH=0"],
-    "t128_b4": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=4"],
-    "nopf": ["GVOX_LIN_PREFETCH=0"],
     "t128_b3": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=3"],
+    "g1": ["GVOX_LIN_G=1"],
+    # overlap kernel (stage times from a full bench run)
     "ovl_u1_b8": ["GVOX_OVL_U=1", "GVOX_OVL_MINB=8"],
     "ovl_u2_b6": ["GVOX_OVL_U=2", "GVOX_OVL_MINB=6"],
     "ovl_u4_b4": ["GVOX_OVL_U=4", "GVOX_OVL_MINB=4"],
