@@ -82,21 +82,26 @@ def make_scene(args, rank, world, dist):
         kw = {}
     if world == 1:
         return synth.make(args.config, **kw)
-    path = f"/dev/shm/gvox_bench_{args.config}_{args.submaps}_{args.order}_{os.getppid()}.npz"
+    # rank 0 writes one .npy per array to /dev/shm; every rank maps them
+    # read-only (shared page cache, no per-rank copies of the 9 GB clouds)
+    base = f"/dev/shm/gvox_bench_{args.config}_{args.submaps}_{args.order}_{os.getppid()}"
+    names = ("mu", "cov", "nrm", "offsets", "map_clouds", "factors", "poses", "gt_poses", "pairs")
     if rank == 0:
         sc = synth.make(args.config, **kw)
-        np.savez(path, **{k: getattr(sc, k) for k in ("mu", "cov", "nrm", "offsets", "map_clouds",
-                                                      "factors", "poses", "gt_poses", "pairs")},
-                 meta=np.array([sc.r0, sc.levels, sc.overlap_level]), name=np.array(sc.name))
+        for k in names:
+            np.save(f"{base}_{k}.npy", getattr(sc, k))
+        np.save(f"{base}_meta.npy", np.array([sc.r0, sc.levels, sc.overlap_level]))
     dist.barrier()
-    z = np.load(path)
-    meta = z["meta"]
-    sc = synth.Scene(str(z["name"]), z["mu"], z["cov"], z["nrm"], z["offsets"], z["map_clouds"],
-                     float(meta[0]), int(meta[1]), z["factors"], z["poses"], z["gt_poses"],
-                     z["pairs"], int(meta[2]))
+    arr = {k: np.load(f"{base}_{k}.npy", mmap_mode="r") for k in names}
+    meta = np.load(f"{base}_meta.npy")
+    sc = synth.Scene(args.config, arr["mu"], arr["cov"], arr["nrm"], np.array(arr["offsets"]),
+                     np.array(arr["map_clouds"]), float(meta[0]), int(meta[1]),
+                     np.array(arr["factors"]), np.array(arr["poses"]), np.array(arr["gt_poses"]),
+                     np.array(arr["pairs"]), int(meta[2]))
     dist.barrier()
-    if rank == 0:
-        os.unlink(path)
+    if rank == 0:  # unlink: the mappings stay valid until every rank exits
+        for k in names + ("meta",):
+            os.unlink(f"{base}_{k}.npy")
     return sc
 
 
@@ -445,9 +450,23 @@ def main():
     # ---- e2e through the public API with host buffers (rank-local, N GPUs)
     e2e = None
     if not args.no_e2e:
-        mu_h = torch.from_numpy(sc.mu).pin_memory()
-        cov_h = torch.from_numpy(sc.cov).pin_memory()
-        nrm_h = torch.from_numpy(sc.nrm).pin_memory()
+        # host inputs of this rank's shard (sources of its pairs and factors + its
+        # targets), packed back to back in pinned memory
+        need = set(int(c) for c in my_pairs[:, 0]) | set(int(sc.map_clouds[t]) for t in my_targets)
+        if not select:
+            need |= set(int(c) for c in fixed["source_cloud"])
+        need = sorted(need)
+        need_n = n_pts[need]
+        loc_off = np.concatenate([[0], np.cumsum(need_n)]).astype(np.int64)
+        tot_n = int(loc_off[-1])
+        mu_h = torch.empty((tot_n, 3), dtype=torch.float32).pin_memory()
+        cov_h = torch.empty((tot_n, 6), dtype=torch.float32).pin_memory()
+        nrm_h = torch.empty((tot_n, 3), dtype=torch.float32).pin_memory()
+        for j_, c_ in enumerate(need):
+            a_, b_ = int(sc.offsets[c_]), int(sc.offsets[c_ + 1])
+            mu_h[loc_off[j_]:loc_off[j_ + 1]] = torch.from_numpy(np.asarray(sc.mu[a_:b_]))
+            cov_h[loc_off[j_]:loc_off[j_ + 1]] = torch.from_numpy(np.asarray(sc.cov[a_:b_]))
+            nrm_h[loc_off[j_]:loc_off[j_ + 1]] = torch.from_numpy(np.asarray(sc.nrm[a_:b_]))
         k_e2e = max(1, min(args.steps, 3))
         pin_out = np.zeros(max(len(my_pairs), len(sc.factors)), gv.LINEAR_FACTOR_DTYPE)
         h2d = 0
@@ -455,30 +474,18 @@ def main():
 
         def e2e_step():
             nonlocal h2d, d2h
-            # clouds needed by this rank's shard come from pinned host memory
-            need = sorted(set(int(c) for c in my_pairs[:, 0]) |
-                          set(int(sc.map_clouds[t]) for t in my_targets))
-            cl_all = gv.create_clouds(ctx, mu_h.numpy(), cov_h.numpy(), nrm_h.numpy(), sc.offsets) \
-                if len(need) > 0.5 * sc.num_clouds else None
-            if cl_all is None:
-                cl_all = [None] * sc.num_clouds
-                for c in need:
-                    a, b = int(sc.offsets[c]), int(sc.offsets[c + 1])
-                    cl_all[c] = gv.Cloud(ctx, mu_h.numpy()[a:b], cov_h.numpy()[a:b], nrm_h.numpy()[a:b])
-            h2d_b = 48 * int(sum(n_pts[c] for c in need)) if cl_all[0] is None else 48 * int(n_pts.sum())
-            carr = gv.HandleArray([c if c is not None else clouds[0] for c in cl_all])
+            cl_loc = gv.create_clouds(ctx, mu_h.numpy(), cov_h.numpy(), nrm_h.numpy(), loc_off)
+            cl_all = [cl_loc[0]] * sc.num_clouds  # placeholders for clouds not used here
+            for j_, c_ in enumerate(need):
+                cl_all[c_] = cl_loc[j_]
+            h2d_b = 48 * tot_n
+            carr = gv.HandleArray(cl_all)
             maps_e = gv.create_voxelmaps(ctx, [cl_all[int(sc.map_clouds[t])] for t in my_targets],
                                          sc.r0, sc.levels)
             marr = gv.HandleArray(maps_e)
             cnt = gv.overlap(ctx, carr, marr, pairs_s, poses, sc.overlap_level)
             if select:
-                sel = 20 * cnt.astype(np.int64) > src_n
-                fe = np.empty(int(sel.sum()), gv.FACTOR_DTYPE)
-                fe["source_cloud"] = my_pairs[sel, 0]
-                fe["target_map"] = my_pairs[sel, 1]
-                fe["pose_i"] = my_pairs[sel, 2]
-                fe["pose_j"] = my_pairs[sel, 3]
-                fe["flags"] = flags
+                fe = all_fac[20 * cnt.astype(np.int64) > src_n]
             else:
                 fe = fixed
             res = gv.linearize_batch(ctx, carr, marr, fe, poses, out=pin_out[:len(fe)])

@@ -15,9 +15,27 @@
 #include <string>
 #include <vector>
 
+#include <chrono>
+#include <cstdlib>
+
 #include "gvox_internal.h"
 
 using namespace gvox;
+
+namespace {
+// GVOX_DEBUG_TIMING=1: host-side phase timings of the map build on stderr
+struct DebugClock {
+  bool on = std::getenv("GVOX_DEBUG_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what) {
+    if (!on) return;
+    auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[gvox build] %-22s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+}  // namespace
 
 // ------------------------------------------------------------------ errors
 namespace {
@@ -462,7 +480,7 @@ void gvox_cloud_destroy(gvox_cloud* cloud) { delete cloud; }
 // ------------------------------------------------------------------ voxelmaps
 namespace {
 
-constexpr int64_t kBuildChunkPoints = 32 << 20;
+constexpr int64_t kBuildChunkPoints = 256 << 20;
 
 gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t count, double r0,
                         int levels, gvox_map** maps_out) {
@@ -520,8 +538,11 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       }
     }
   }
+  DebugClock dbg;
+  dbg.lap("plan");
   std::shared_ptr<DevBuf> grid_arena;
   gvox_status st = devbuf_alloc(gl.size, ctx->device, ctx->stream, &grid_arena);
+  dbg.lap("grid alloc");
   if (st) return st;
   char* gb = (char*)grid_arena->ptr;
   if (gl.size) CK(cudaMemsetAsync(gb, 0xFF, gl.size, ctx->stream));  // every cell -1 (empty)
@@ -545,6 +566,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   void* ws0 = nullptr;
   st = ws_reserve(ctx, 0, lay.size, &ws0);
   if (st) return st;
+  dbg.lap("ws0");
   char* b0 = (char*)ws0;
   int32_t* d_cnt = (int32_t*)(b0 + o_cnt);
   int32_t* d_err = d_cnt + count * L;
@@ -588,7 +610,9 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   std::vector<int32_t> hcnt((size_t)count * L + 1);
   CK(cudaMemcpyAsync(hcnt.data(), d_cnt, ((size_t)count * L + 1) * 4, cudaMemcpyDeviceToHost,
                      ctx->stream));
+  dbg.lap("insert enqueued");
   CK(cudaStreamSynchronize(ctx->stream));
+  dbg.lap("insert sync");
   if (hcnt[(size_t)count * L])
     return fail(GVOX_ERR_RANGE,
                 "gvox_create_voxelmap: a voxel key is outside [-2^20, 2^20) (r0 = %g)", r0);
@@ -618,6 +642,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   std::shared_ptr<DevBuf> arena;
   st = devbuf_alloc(al.size, ctx->device, ctx->stream, &arena);
   if (st) return st;
+  dbg.lap("record alloc");
   char* ab = (char*)arena->ptr;
   // ---- phase 2/3 workspace (workspace 1): acc [total_vox][10] + seg tables
   Layout l1;
@@ -626,6 +651,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   void* ws1 = nullptr;
   st = ws_reserve(ctx, 1, l1.size, &ws1);
   if (st) return st;
+  dbg.lap("ws1");
   char* b1 = (char*)ws1;
   CK(cudaMemsetAsync(b1 + o_acc, 0, (size_t)total_vox * 80, ctx->stream));
   if (idx_end > idx_begin) CK(cudaMemsetAsync(ab + idx_begin, 0xFF, idx_end - idx_begin, ctx->stream));
@@ -719,6 +745,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   // stream orders the next chunk's reuse of the workspaces after this one)
   CK(cudaMemcpyAsync(ab + o_descs, mdesc.data(), sizeof(MapDev) * count, cudaMemcpyHostToDevice,
                      ctx->stream));
+  dbg.lap("accum/finalize enqueued");
   for (int64_t s = 0; s < count; ++s) {
     auto* m = new gvox_map;
     m->arena = arena;
