@@ -5,8 +5,9 @@ on B200, in the driver's JSON-line contract.
 A STEP is one pass of every hot-path row of SURVEY.md Sec.8(a) over the
 workload (default C5: 2000 submaps x 100k points):
   S1  gvox_create_voxelmaps  -- multi-resolution voxelmaps of every target submap
-  S2  gvox_overlap           -- overlap counts of every candidate submap pair
-      host: a pair becomes a factor iff 20 * count > N_src ("exceeds 5 %")
+  S2  gvox_overlap_select    -- screening decision of every candidate submap pair:
+      a pair becomes a factor iff 20 * count > N_src ("exceeds 5 %"), exact,
+      each pair stopping as soon as its decision is certain (C1-C3: gvox_overlap counts)
   S3-S7 gvox_linearize_batch(_accum) -- every selected factor, one batch
   (N > 1: factors sharded by target submap; one NCCL all_gather of the compact
    per-factor records)
@@ -310,6 +311,7 @@ def main():
     # device buffers reused across steps
     acc_out = gv.device_records(ctx, max(len(my_pairs), len(sc.factors), 1), gv.FACTOR_ACCUM_DTYPE)
     counts_h = np.zeros(len(my_pairs), np.int32)
+    sel_h = np.zeros(len(my_pairs), np.uint8)
 
     state = {}
 
@@ -321,11 +323,14 @@ def main():
         maps = gv.create_voxelmaps(ctx, my_target_clouds, sc.r0, sc.levels)        # S1
         marr = gv.HandleArray(maps)
         t1 = time.perf_counter()
-        gv.overlap(ctx, cloud_arr, marr, pairs_s, poses, sc.overlap_level, out=counts_h)  # S2
+        if select:  # S2 as the screening decision: overlap exceeds 5 %
+            gv.overlap_select(ctx, cloud_arr, marr, pairs_s, poses, sc.overlap_level, 1, 20,
+                              out=sel_h)
+        else:       # S2 as overlap counts of the config's pairs
+            gv.overlap(ctx, cloud_arr, marr, pairs_s, poses, sc.overlap_level, out=counts_h)
         t2 = time.perf_counter()
         if select:
-            sel = 20 * counts_h.astype(np.int64) > src_n
-            fac = all_fac[sel]
+            fac = all_fac[sel_h.view(bool)]
         else:
             fac = fixed
         out = acc_out[:len(fac)]
@@ -483,10 +488,11 @@ def main():
             maps_e = gv.create_voxelmaps(ctx, [cl_all[int(sc.map_clouds[t])] for t in my_targets],
                                          sc.r0, sc.levels)
             marr = gv.HandleArray(maps_e)
-            cnt = gv.overlap(ctx, carr, marr, pairs_s, poses, sc.overlap_level)
             if select:
-                fe = all_fac[20 * cnt.astype(np.int64) > src_n]
+                cnt = gv.overlap_select(ctx, carr, marr, pairs_s, poses, sc.overlap_level, 1, 20)
+                fe = all_fac[cnt.view(bool)]
             else:
+                cnt = gv.overlap(ctx, carr, marr, pairs_s, poses, sc.overlap_level)
                 fe = fixed
             res = gv.linearize_batch(ctx, carr, marr, fe, poses, out=pin_out[:len(fe)])
             h2d = h2d_b + poses.nbytes * 2 + pairs_s.nbytes + fe.nbytes

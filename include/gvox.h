@@ -213,6 +213,20 @@ gvox_status gvox_overlap(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t
                          int64_t num_pairs, const double* poses, int64_t num_poses, int level,
                          int32_t* counts, int mem);
 
+/* Screening decision for factor creation ("a matching cost factor
+   between each submap pair with an overlap rate that exceeds a small threshold
+   (e.g., 5 %)"): selected[p] = 1 iff count * den > n * num, with count and n as
+   in gvox_overlap (e.g. num = 1, den = 20 for "exceeds 5 %").  Every pair stops
+   as soon as its decision is certain (enough hits, or too few points left), so
+   the decision is exactly the one the full count gives with fewer lookups.
+   num >= 0, den > 0.  selected: uint8 [num_pairs] in `mem`.  Same transfers as
+   gvox_overlap. */
+gvox_status gvox_overlap_select(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                int64_t num_clouds, const gvox_map* const* maps, int64_t num_maps,
+                                const gvox_pair* pairs, int64_t num_pairs, const double* poses,
+                                int64_t num_poses, int level, int32_t num, int32_t den,
+                                uint8_t* selected, int mem);
+
 /* ------------------------------------------------------------- linearize */
 
 /* Batched linearization of matching cost factors (Eqs. 2-8; Fig. 4 / P:224:

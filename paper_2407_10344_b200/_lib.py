@@ -42,7 +42,7 @@ SYMBOLS = [
     "gvox_cloud_destroy",
     "gvox_create_voxelmap", "gvox_create_voxelmaps", "gvox_voxelmap_info", "gvox_voxelmap_levels",
     "gvox_voxelmap_export", "gvox_voxelmap_lookup", "gvox_map_destroy",
-    "gvox_overlap", "gvox_linearize_batch", "gvox_linearize_batch_accum", "gvox_expand",
+    "gvox_overlap", "gvox_overlap_select", "gvox_linearize_batch", "gvox_linearize_batch_accum", "gvox_expand",
     "gvox_status_string", "gvox_last_error", "gvox_launch_count", "gvox_version",
 ]
 
@@ -84,6 +84,7 @@ def lib():
         "gvox_voxelmap_lookup": (I32, [P, P, I32, P, I64, P, I32]),
         "gvox_map_destroy": (None, [P]),
         "gvox_overlap": (I32, [P, P, I64, P, I64, P, I64, P, I64, I32, P, I32]),
+        "gvox_overlap_select": (I32, [P, P, I64, P, I64, P, I64, P, I64, I32, I32, I32, P, I32]),
         "gvox_linearize_batch": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32, P]),
         "gvox_linearize_batch_accum": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32]),
         "gvox_expand": (I32, [P, P, I64, P, I64, P, P, I32]),

@@ -262,6 +262,22 @@ def overlap(ctx: Context, clouds, maps, pairs, poses, level: int, out=None):
     return out
 
 
+def overlap_select(ctx: Context, clouds, maps, pairs, poses, level: int, num: int = 1,
+                   den: int = 20, out=None):
+    """gvox_overlap_select: uint8 decisions count * den > n * num per pair (default:
+    overlap rate exceeds 5 %), exact, with early termination per pair."""
+    C, M = _handles(clouds), _handles(maps)
+    pairs = as_pairs(pairs)
+    poses = as_poses(poses)
+    if out is None:
+        out = np.empty(pairs.shape[0], np.uint8)
+    po, mem = _ptr(out)
+    check(lib().gvox_overlap_select(ctx.handle, C.arr, C.n, M.arr, M.n, _ptr(pairs)[0],
+                                    pairs.shape[0], _ptr(poses)[0], poses.shape[0], int(level),
+                                    int(num), int(den), po, mem))
+    return out
+
+
 def device_records(ctx: Context, n: int, dtype: np.dtype):
     torch = _torch()
     return torch.empty((n, dtype.itemsize), dtype=torch.uint8, device=ctx.device)

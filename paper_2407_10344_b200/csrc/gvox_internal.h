@@ -203,6 +203,11 @@ void launch_overlap(const CloudDev* const* clouds, const MapDev* const* maps, co
                     const double* poses, int level, int32_t* tile_pair, int32_t* counts,
                     bool all_dense, cudaStream_t stream);
 
+void launch_overlap_select(const CloudDev* const* clouds, const MapDev* const* maps,
+                           const PairDev* pairs, int64_t num_pairs, const double* poses, int level,
+                           int32_t num, int32_t den, uint8_t* selected, bool all_dense,
+                           cudaStream_t stream);
+
 // linearize
 struct FactorDev {
   int32_t src, tgt, pi, pj;

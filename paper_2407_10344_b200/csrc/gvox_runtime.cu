@@ -892,55 +892,69 @@ gvox_status gvox_voxelmap_lookup(gvox_ctx* ctx, const gvox_map* map, int level, 
 void gvox_map_destroy(gvox_map* map) { delete map; }
 
 // ------------------------------------------------------------------ overlap
-gvox_status gvox_overlap(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t num_clouds,
-                         const gvox_map* const* maps, int64_t num_maps, const gvox_pair* pairs,
-                         int64_t num_pairs, const double* poses, int64_t num_poses, int level,
-                         int32_t* counts, int mem) {
-  if (!ctx) return fail(GVOX_ERR_INVALID, "gvox_overlap: ctx is NULL");
-  if (num_pairs < 0) return fail(GVOX_ERR_INVALID, "gvox_overlap: num_pairs < 0");
+namespace {
+
+// Shared by gvox_overlap (counts) and gvox_overlap_select (decisions).
+gvox_status overlap_impl(const char* fn, gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                         int64_t num_clouds, const gvox_map* const* maps, int64_t num_maps,
+                         const gvox_pair* pairs, int64_t num_pairs, const double* poses,
+                         int64_t num_poses, int level, int32_t* counts, uint8_t* selected,
+                         int32_t num, int32_t den, int mem) {
+  if (!ctx) return fail(GVOX_ERR_INVALID, "%s: ctx is NULL", fn);
+  if (num_pairs < 0) return fail(GVOX_ERR_INVALID, "%s: num_pairs < 0", fn);
   if (num_pairs == 0) return GVOX_OK;
-  if (!clouds || !maps || !pairs || !poses || !counts)
-    return fail(GVOX_ERR_INVALID, "gvox_overlap: NULL argument");
+  if (!clouds || !maps || !pairs || !poses || !(counts || selected))
+    return fail(GVOX_ERR_INVALID, "%s: NULL argument", fn);
+  if (mem != GVOX_HOST && mem != GVOX_DEVICE)
+    return fail(GVOX_ERR_INVALID, "%s: mem must be GVOX_HOST or GVOX_DEVICE", fn);
+  if (selected && (num < 0 || den <= 0))
+    return fail(GVOX_ERR_INVALID, "%s: threshold num = %d, den = %d (need num >= 0, den > 0)", fn,
+                num, den);
+  if (num_pairs > INT32_MAX) return fail(GVOX_ERR_INVALID, "%s: more than 2^31 pairs", fn);
   for (int64_t p = 0; p < num_pairs; ++p) {
     const gvox_pair& q = pairs[p];
     if (q.source_cloud < 0 || q.source_cloud >= num_clouds || !clouds[q.source_cloud])
-      return fail(GVOX_ERR_INVALID, "gvox_overlap: pair %lld: source_cloud %d out of range [0, %lld)",
+      return fail(GVOX_ERR_INVALID, "%s: pair %lld: source_cloud %d out of range [0, %lld)", fn,
                   (long long)p, q.source_cloud, (long long)num_clouds);
     if (q.target_map < 0 || q.target_map >= num_maps || !maps[q.target_map])
-      return fail(GVOX_ERR_INVALID, "gvox_overlap: pair %lld: target_map %d out of range [0, %lld)",
+      return fail(GVOX_ERR_INVALID, "%s: pair %lld: target_map %d out of range [0, %lld)", fn,
                   (long long)p, q.target_map, (long long)num_maps);
     if (q.pose_i < 0 || q.pose_i >= num_poses || q.pose_j < 0 || q.pose_j >= num_poses)
-      return fail(GVOX_ERR_INVALID, "gvox_overlap: pair %lld: pose index out of range [0, %lld)",
+      return fail(GVOX_ERR_INVALID, "%s: pair %lld: pose index out of range [0, %lld)", fn,
                   (long long)p, (long long)num_poses);
     if (level < 0 || level >= maps[q.target_map]->levels)
-      return fail(GVOX_ERR_INVALID, "gvox_overlap: pair %lld: level %d outside the target map's [0, %d)",
+      return fail(GVOX_ERR_INVALID, "%s: pair %lld: level %d outside the target map's [0, %d)", fn,
                   (long long)p, level, maps[q.target_map]->levels);
   }
   for (int64_t i = 0; i < num_poses; ++i)
     if (!finite_pose(poses + 12 * i))
-      return fail(GVOX_ERR_INVALID, "gvox_overlap: pose %lld is not finite", (long long)i);
+      return fail(GVOX_ERR_INVALID, "%s: pose %lld is not finite", fn, (long long)i);
   DeviceGuard g(ctx->device);
-  // tiles of 256 * ppt source points: >= ~8 waves of 8 CTAs per SM
   int64_t total_pts = 0;
   bool all_dense = true;
   for (int64_t p = 0; p < num_pairs; ++p) {
     total_pts += clouds[pairs[p].source_cloud]->n;
     all_dense = all_dense && maps[pairs[p].target_map]->desc.lv[level].dense;
   }
-  int ppt = 4;  // the kernel handles 4 points per thread per iteration
+  // counts: tiles of 256 * ppt source points, >= ~8 waves of 8 CTAs per SM
+  // (selection: one CTA per pair, no tiles)
+  int ppt = 4;  // the kernel handles U points per thread per iteration
   while (ppt < 32 && total_pts / ((int64_t)256 * ppt * 2) >= 148 * 8 * 8) ppt *= 2;
   const int tile_pts = 256 * ppt;
-  std::vector<int32_t> tstart(num_pairs + 1, 0);
-  for (int64_t p = 0; p < num_pairs; ++p) {
-    int64_t n = clouds[pairs[p].source_cloud]->n;
-    tstart[p + 1] = tstart[p] + (int32_t)((n + tile_pts - 1) / tile_pts);
-  }
-  const int64_t T = tstart[num_pairs];
+  std::vector<int32_t> tstart(counts ? num_pairs + 1 : 1, 0);
+  if (counts)
+    for (int64_t p = 0; p < num_pairs; ++p) {
+      int64_t n = clouds[pairs[p].source_cloud]->n;
+      int64_t nt = tstart[p] + (n + tile_pts - 1) / tile_pts;
+      if (nt > INT32_MAX) return fail(GVOX_ERR_INVALID, "%s: more than 2^31 tiles", fn);
+      tstart[p + 1] = (int32_t)nt;
+    }
+  const int64_t T = tstart.back();
   // ---- one serialized input block
   Layout lay;
   size_t o_pose = lay.add(96 * num_poses);
   size_t o_pair = lay.add(sizeof(PairDev) * num_pairs);
-  size_t o_ts = lay.add(4 * (num_pairs + 1));
+  size_t o_ts = lay.add(4 * tstart.size());
   size_t o_cl = lay.add(8 * num_clouds);
   size_t o_mp = lay.add(8 * num_maps);
   size_t in_bytes = lay.size;
@@ -950,13 +964,13 @@ gvox_status gvox_overlap(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t
   char* hp = (char*)pin;
   std::memcpy(hp + o_pose, poses, 96 * num_poses);
   std::memcpy(hp + o_pair, pairs, sizeof(PairDev) * num_pairs);
-  std::memcpy(hp + o_ts, tstart.data(), 4 * (num_pairs + 1));
+  std::memcpy(hp + o_ts, tstart.data(), 4 * tstart.size());
   for (int64_t i = 0; i < num_clouds; ++i) ((const CloudDev**)(hp + o_cl))[i] = clouds[i] ? clouds[i]->dev : nullptr;
   for (int64_t i = 0; i < num_maps; ++i) ((const MapDev**)(hp + o_mp))[i] = maps[i] ? maps[i]->dev : nullptr;
   Layout wl;
   size_t o_in = wl.add(in_bytes);
   size_t o_tp = wl.add(4 * (size_t)std::max<int64_t>(T, 1));
-  size_t o_cnt = wl.add(4 * num_pairs);
+  size_t o_out = wl.add(4 * num_pairs);
   void* ws = nullptr;
   st = ws_reserve(ctx, 0, wl.size, &ws);
   if (st) return st;
@@ -964,22 +978,58 @@ gvox_status gvox_overlap(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t
   st = h2d_block(ctx, wb + o_in, hp, in_bytes);
   if (st) return st;
   char* din = wb + o_in;
-  int32_t* dcounts = mem == GVOX_DEVICE ? counts : (int32_t*)(wb + o_cnt);
-  CK(cudaMemsetAsync(dcounts, 0, 4 * num_pairs, ctx->stream));
-  launch_tile_map((const int32_t*)(din + o_ts), num_pairs, (int32_t*)(wb + o_tp), ctx->stream);
-  {
+  const CloudDev* const* dcl = (const CloudDev* const*)(din + o_cl);
+  const MapDev* const* dmp = (const MapDev* const*)(din + o_mp);
+  const PairDev* dpairs = (const PairDev*)(din + o_pair);
+  const double* dposes = (const double*)(din + o_pose);
+  size_t out_bytes;
+  void* dout;
+  if (counts) {
+    int32_t* dcounts = mem == GVOX_DEVICE ? counts : (int32_t*)(wb + o_out);
+    CK(cudaMemsetAsync(dcounts, 0, 4 * num_pairs, ctx->stream));
+    launch_tile_map((const int32_t*)(din + o_ts), num_pairs, (int32_t*)(wb + o_tp), ctx->stream);
     TimerScope ts(ctx, GVOX_TIMER_OVERLAP);
-    launch_overlap((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
-                   (const PairDev*)(din + o_pair), (const int32_t*)(din + o_ts), num_pairs, T,
-                   tile_pts, (const double*)(din + o_pose), level, (int32_t*)(wb + o_tp), dcounts,
-                   all_dense, ctx->stream);
+    launch_overlap(dcl, dmp, dpairs, (const int32_t*)(din + o_ts), num_pairs, T, tile_pts, dposes,
+                   level, (int32_t*)(wb + o_tp), dcounts, all_dense, ctx->stream);
+    dout = dcounts;
+    out_bytes = 4 * num_pairs;
+  } else {
+    uint8_t* dsel = mem == GVOX_DEVICE ? selected : (uint8_t*)(wb + o_out);
+    TimerScope ts(ctx, GVOX_TIMER_OVERLAP);
+    launch_overlap_select(dcl, dmp, dpairs, num_pairs, dposes, level, num, den, dsel, all_dense,
+                          ctx->stream);
+    dout = dsel;
+    out_bytes = num_pairs;
   }
-  CK_LAUNCH("gvox_overlap");
+  CK_LAUNCH(fn);
   if (mem == GVOX_HOST) {
-    CK(cudaMemcpyAsync(counts, dcounts, 4 * num_pairs, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(counts ? (void*)counts : (void*)selected, dout, out_bytes,
+                       cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   }
   return GVOX_OK;
+}
+
+}  // namespace
+
+gvox_status gvox_overlap(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t num_clouds,
+                         const gvox_map* const* maps, int64_t num_maps, const gvox_pair* pairs,
+                         int64_t num_pairs, const double* poses, int64_t num_poses, int level,
+                         int32_t* counts, int mem) {
+  if (!counts && num_pairs > 0) return fail(GVOX_ERR_INVALID, "gvox_overlap: counts is NULL");
+  return overlap_impl("gvox_overlap", ctx, clouds, num_clouds, maps, num_maps, pairs, num_pairs,
+                      poses, num_poses, level, counts, nullptr, 0, 1, mem);
+}
+
+gvox_status gvox_overlap_select(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                int64_t num_clouds, const gvox_map* const* maps, int64_t num_maps,
+                                const gvox_pair* pairs, int64_t num_pairs, const double* poses,
+                                int64_t num_poses, int level, int32_t num, int32_t den,
+                                uint8_t* selected, int mem) {
+  if (!selected && num_pairs > 0)
+    return fail(GVOX_ERR_INVALID, "gvox_overlap_select: selected is NULL");
+  return overlap_impl("gvox_overlap_select", ctx, clouds, num_clouds, maps, num_maps, pairs,
+                      num_pairs, poses, num_poses, level, nullptr, selected, num, den, mem);
 }
 
 // ------------------------------------------------------------------ linearize

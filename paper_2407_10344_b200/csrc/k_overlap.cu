@@ -106,6 +106,94 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   }
 }
 
+// Screening decision (a factor for each pair whose overlap rate
+// "exceeds a small threshold"): selected[p] = (count * den > n * num).  One CTA
+// per pair walks its source points in blocks of kThreads * U and stops as soon
+// as the decision is certain -- enough hits (count >= need) or too few points
+// left to reach `need` -- so the decision equals the one from the exact count
+// while accepted pairs cost only the points it takes to accept them.
+template <bool ALL_DENSE>
+__global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
+    k_overlap_select(const CloudDev* const* __restrict__ clouds,
+                     const MapDev* const* __restrict__ maps, const PairDev* __restrict__ pairs,
+                     const double* __restrict__ poses, int level, int32_t num, int32_t den,
+                     uint8_t* __restrict__ selected) {
+  __shared__ double pose_s[24];
+  __shared__ double R[9], t[3];
+  __shared__ const float4* A_s;
+  __shared__ int64_t n_s;
+  __shared__ MapLevelDev lv_s;
+  __shared__ int dyadic_s;
+  __shared__ int warp_cnt[2][kThreads / 32];
+  const int tid = threadIdx.x;
+  const int32_t p = blockIdx.x;
+  const PairDev pd = pairs[p];
+  if (tid < 24) {
+    pose_s[tid] = __ldg(poses + 12 * (int64_t)(tid < 12 ? pd.pi : pd.pj) + (tid % 12));
+  } else if (tid == 32) {
+    const CloudDev* cd = clouds[pd.src];
+    A_s = cd->A;
+    n_s = cd->n;
+  } else if (tid == 64) {
+    const MapDev* md = maps[pd.tgt];
+    lv_s = md->lv[level];
+    dyadic_s = md->dyadic;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double v[3];
+    relative_pose_dev(pose_s, pose_s + 12, R, t, v);
+  }
+  __syncthreads();
+  const MapLevelDev lv = lv_s;
+  const int dyadic = dyadic_s;
+  const float4* __restrict__ A = A_s;
+  const int64_t n = n_s;
+  // count * den > n * num  <=>  count >= need
+  const int64_t need = (n * (int64_t)num) / den + 1;
+  constexpr int U = GVOX_OVL_U;
+  int64_t total = 0;
+  int buf = 0;
+  bool sel = false;
+  for (int64_t k0 = 0; k0 < n; k0 += (int64_t)U * kThreads) {
+    int cnt = 0;
+    float4 a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + u * kThreads + tid;
+      if (k < n) a[u] = __ldg(A + k);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (k0 + u * kThreads + tid < n) {
+        const double mx = a[u].x, my = a[u].y, mz = a[u].z;
+        const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
+        const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
+        const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
+        const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
+        const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
+        const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
+        cnt += lookup_level<ALL_DENSE>(lv, kx, ky, kz) >= 0;
+      }
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((tid & 31) == 0) warp_cnt[buf][tid >> 5] = cnt;
+    __syncthreads();
+    int blk = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) blk += warp_cnt[buf][w];
+    buf ^= 1;  // double buffer: no second barrier needed before the next write
+    total += blk;
+    const int64_t left = n - (k0 + (int64_t)U * kThreads);
+    if (total >= need) {
+      sel = true;
+      break;
+    }
+    if (total + (left > 0 ? left : 0) < need) break;
+  }
+  if (tid == 0) selected[p] = sel ? 1 : 0;
+}
+
 }  // namespace
 
 void launch_overlap(const CloudDev* const* clouds, const MapDev* const* maps, const PairDev* pairs,
@@ -122,4 +210,20 @@ void launch_overlap(const CloudDev* const* clouds, const MapDev* const* maps, co
   note_launch();
 }
 
+}  // namespace gvox
+
+namespace gvox {
+void launch_overlap_select(const CloudDev* const* clouds, const MapDev* const* maps,
+                           const PairDev* pairs, int64_t num_pairs, const double* poses, int level,
+                           int32_t num, int32_t den, uint8_t* selected, bool all_dense,
+                           cudaStream_t stream) {
+  if (num_pairs <= 0) return;
+  if (all_dense)
+    k_overlap_select<true><<<(unsigned)num_pairs, kThreads, 0, stream>>>(
+        clouds, maps, pairs, poses, level, num, den, selected);
+  else
+    k_overlap_select<false><<<(unsigned)num_pairs, kThreads, 0, stream>>>(
+        clouds, maps, pairs, poses, level, num, den, selected);
+  note_launch();
+}
 }  // namespace gvox

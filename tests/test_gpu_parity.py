@@ -142,6 +142,24 @@ def test_overlap_parity_random_poses(gv, ctx, oracle):
             assert int(g) == want
 
 
+@pytest.mark.parametrize("num,den", [(1, 20), (0, 1), (1, 2), (19, 20), (1, 1), (3, 7)])
+def test_overlap_select_matches_exact_decision(gv, ctx, oracle, num, den):
+    """gvox_overlap_select stops early but must reproduce count * den > n * num."""
+    rs = np.random.default_rng(17)
+    mu, cov, nrm = rand_scene(rs, 8000, 12.0)
+    srcs = [rand_scene(rs, n, 12.0)[0] for n in (9000, 2049, 1, 0, 4096, 777)]
+    clouds = [gv.Cloud(ctx, s_, np.tile(cov[:1], (len(s_), 1))) for s_ in srcs]
+    maps = gv.create_voxelmaps(ctx, [gv.Cloud(ctx, mu, cov)], 0.5, 3)
+    om = oracle.VoxelMap(mu, cov, 0.5, 3)
+    poses = [to12(np.eye(4))] + [random_pose(rs, 0.1 * k, 2.0 * k) for k in range(1, 9)]
+    pairs = [[s_, 0, 1 + (s_ + k) % 8, 0] for s_ in range(len(srcs)) for k in range(4)]
+    for level in (0, 1):
+        got = gv.overlap_select(ctx, clouds, maps, pairs, poses, level, num, den)
+        for p, g in zip(pairs, got):
+            cnt = oracle.overlap(srcs[p[0]], om, poses[p[2]], poses[p[3]], level)
+            assert int(g) == int(cnt * den > len(srcs[p[0]]) * num), (p, cnt, len(srcs[p[0]]))
+
+
 def test_overlap_c2(gv, ctx, oracle):
     sc = synth.make("C2")
     clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
@@ -367,6 +385,9 @@ def test_full_size_submaps_sampled(gv, ctx, oracle):
         mu, cov, nrm = sc.cloud(int(f[0]))
         ref = oracle.linearize(mu, cov, nrm, omaps[t], sc.poses[f[2]], sc.poses[f[3]])
         compare_factor(out[k], ref, sc.levels, what=f"C5-size factor {k}")
+    sel = gv.overlap_select(ctx, clouds, maps, sc.pairs, sc.poses, sc.overlap_level, 1, 20)
+    n = np.diff(sc.offsets)
+    assert np.array_equal(sel.astype(bool), 20 * cnt.astype(np.int64) > n[sc.pairs[:, 0]])
     for k in rs.choice(len(sc.pairs), 6, replace=False):
         p = sc.pairs[k]
         t = int(p[1])
@@ -374,6 +395,7 @@ def test_full_size_submaps_sampled(gv, ctx, oracle):
         want = oracle.overlap(sc.cloud(int(p[0]))[0], omaps[t], sc.poses[p[2]], sc.poses[p[3]],
                               sc.overlap_level)
         assert int(cnt[k]) == want
+        assert int(sel[k]) == int(20 * want > n[int(p[0])])
     # one sampled map, exported and compared bit-exactly on keys/counts
     t = int(sc.factors[0][1])
     omaps.setdefault(t, oracle.VoxelMap(*sc.cloud(t)[:2], sc.r0, sc.levels))
