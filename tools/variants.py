@@ -16,6 +16,8 @@ VARIANTS = {
     "t256_b2": ["GVOX_LIN_THREADS=256", "GVOX_LIN_MINB=2"],
     "t128_b3": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=3"],
     "g1": ["GVOX_LIN_G=1"],
+    "t128_b2": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=2"],
+    "t256_b1": ["GVOX_LIN_THREADS=256", "GVOX_LIN_MINB=1"],
     # overlap kernel (stage times from a full bench run)
     "ovl_u1_b8": ["GVOX_OVL_U=1", "GVOX_OVL_MINB=8"],
     "ovl_u2_b6": ["GVOX_OVL_U=2", "GVOX_OVL_MINB=6"],
