@@ -48,9 +48,6 @@ namespace {
 #ifndef GVOX_LIN_MINB
 #define GVOX_LIN_MINB 4
 #endif
-#ifndef GVOX_LIN_PREFETCH
-#define GVOX_LIN_PREFETCH 1
-#endif
 #ifndef GVOX_LIN_G
 #define GVOX_LIN_G 4
 #endif
@@ -73,6 +70,20 @@ struct FactorShared {
   int L, dyadic, validate, error_only;
   MapLevelDev lv[GVOX_MAX_LEVELS];
 };
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// 1/x for x > 0 finite (MUFU.RCP, ~1 ulp)
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 __global__ void k_tile_map(const int32_t* __restrict__ tile_start, int64_t num_factors,
                            int32_t* __restrict__ tile_factor) {
@@ -236,8 +247,9 @@ __device__ __forceinline__ void level_term(Acc<MAXL>& ac, LevelSum& ls, const Po
   const float i22 = fmaf(ca, cd, -cb * cb);
   const float det = fmaf(ca, i00, fmaf(cb, i01, cc * i02));
   // Q16: a fused covariance that is not positive definite contributes nothing
-  const bool ok = det > 0.f && det < INFINITY;
-  const float id = ok ? __fdividef(1.0f, det) : 0.f;
+  // det > 0 and finite  <=>  bits(det) - 1 < bits(FLT_MAX)  (unsigned)
+  const bool ok = __float_as_uint(det) - 1u < 0x7F7FFFFFu;
+  const float id = ok ? rcp_approx(det) : 0.f;
   ac.n_degenerate += !ok;
   ac.inl[l] += ok;
   const f2_t Om_a = mul2(pk(i00, i01), bc(id));  // (o00, o01) = column 0, rows 0-1
@@ -393,27 +405,25 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
   int64_t* const corr_t = corr ? corr + sh.corr_base + begin * L : nullptr;
   Acc<MAXL> ac;
 
-  // software pipeline: the next point's 48 B source record is in flight while
-  // the current one is processed
-#if GVOX_LIN_PREFETCH
-  float4 na, nb, nc;
-  if (tid < npts) {
-    na = __ldg(Ap + tid);
-    nb = __ldg(Bp + tid);
-    nc = __ldg(Np + tid);
-  }
-#endif
-  for (int32_t k = tid; k < npts; k += kThreads) {
-#if GVOX_LIN_PREFETCH
-    const float4 a = na, b = nb, c = nc;
-    if (k + kThreads < npts) {
-      na = __ldg(Ap + k + kThreads);
-      nb = __ldg(Bp + k + kThreads);
-      nc = __ldg(Np + k + kThreads);
+  // software pipeline: the next point's 48 B source record is copied into a
+  // per-thread double buffer in shared memory by cp.async (LDGSTS) while the
+  // current one is processed -- no registers held, no register copies.  Each
+  // thread only reads its own slots, so no block barrier is needed.
+  __shared__ float4 src_buf[2][3][kThreads];
+  auto issue = [&](int32_t kk, int buf) {
+    if (kk < npts) {
+      cp_async16(&src_buf[buf][0][tid], Ap + kk);
+      cp_async16(&src_buf[buf][1][tid], Bp + kk);
+      cp_async16(&src_buf[buf][2][tid], Np + kk);
     }
-#else
-    const float4 a = __ldg(Ap + k), b = __ldg(Bp + k), c = __ldg(Np + k);
-#endif
+    cp_async_commit();
+  };
+  issue(tid, 0);
+  int buf = 0;
+  for (int32_t k = tid; k < npts; k += kThreads, buf ^= 1) {
+    issue(k + kThreads, buf ^ 1);
+    cp_async_wait_1();  // this point's group has landed (the next one may be in flight)
+    const float4 a = src_buf[buf][0][tid], b = src_buf[buf][1][tid], c = src_buf[buf][2][tid];
     if (validate && invisible(sh, a, c)) {
       ++ac.n_invisible;
       if (corr)
