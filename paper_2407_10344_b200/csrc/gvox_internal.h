@@ -30,10 +30,14 @@ struct CloudDev {
   const float4* A;
   const float4* B;
   const float4* N;
+  // bounding box of every 32 consecutive points (a warp's worth):
+  // [chunk] = {min.x, min.y, min.z, max.x, max.y, max.z}, ceil(n / 32) chunks
+  const float* chunk_box;
   int64_t n;
   int32_t has_normals;
   int32_t pad;
 };
+constexpr int kChunk = 32;
 
 // One level of a map.  Voxel lookup uses either
 //  * a DENSE index grid over the level's key bounding box (int32 voxel index
@@ -65,6 +69,10 @@ struct MapDev {
   int32_t dyadic;  // r0 is a power of two: floor(q * inv_r0) == floor(q / r0)
   double r0;
   double inv_r0;
+  // conservative box of every voxel of every level: the source cloud's box
+  // grown by the coarsest resolution (a point q can only hit a voxel whose
+  // cell contains a map point p, so |q - p| < r_l per axis).  Empty map: lo > hi.
+  float box_lo[4], box_hi[4];
   MapLevelDev lv[GVOX_MAX_LEVELS];
 };
 
@@ -101,7 +109,8 @@ __host__ __device__ inline bool key_in_range(int32_t k) { return k >= -kKeyHalf 
 // [2..4] = min mu, [5..7] = max mu (order-preserving int encoding of floats;
 // initialise [2..4] to INT_MAX and [5..7] to INT_MIN).
 void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* A,
-                       float4* B, float4* N, int32_t* stats, cudaStream_t stream);
+                       float4* B, float4* N, float* chunk_box, int32_t* stats,
+                       cudaStream_t stream);
 
 __host__ __device__ inline int32_t float_to_ordered(float f) {
 #ifdef __CUDA_ARCH__

@@ -381,6 +381,12 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
   size_t o_desc = lay.add(sizeof(CloudDev) * count);
   size_t o_a = lay.add(16 * (size_t)n), o_b = lay.add(16 * (size_t)n), o_n = lay.add(16 * (size_t)n);
   size_t o_flags = lay.add(32 * (size_t)count);
+  // per-cloud chunk boxes (6 floats per 32 points), each cloud's run starting
+  // at its own chunk 0
+  std::vector<int64_t> cb_off(count + 1, 0);
+  for (int64_t k = 0; k < count; ++k)
+    cb_off[k + 1] = cb_off[k] + 6 * ((offsets[k + 1] - offsets[k] + kChunk - 1) / kChunk);
+  size_t o_cbox = lay.add(4 * (size_t)cb_off[count]);
   std::shared_ptr<DevBuf> buf;
   gvox_status st = devbuf_alloc(lay.size, ctx->device, ctx->stream, &buf);
   if (st) return st;
@@ -388,6 +394,7 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
   float4* A = (float4*)(base + o_a);
   float4* B = (float4*)(base + o_b);
   float4* N = (float4*)(base + o_n);
+  float* cbox = (float*)(base + o_cbox);
   // per-cloud statistics (see launch_cloud_pack): flag, max |C_ij|, min / max mean
   int32_t* dflags = (int32_t*)(base + o_flags);
   std::vector<int32_t> hflags(8 * (size_t)count);
@@ -420,7 +427,7 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
       int64_t a = offsets[k], m = offsets[k + 1] - offsets[k];
       if (m == 0) continue;
       launch_cloud_pack(dmu + 3 * a, dcov + 6 * a, dnrm ? dnrm + 3 * a : nullptr, m, A + a, B + a,
-                        N + a, dflags + 8 * k, ctx->stream);
+                        N + a, cbox + cb_off[k], dflags + 8 * k, ctx->stream);
     }
     CK_LAUNCH("gvox_cloud_create: pack");
   }
@@ -441,6 +448,7 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
     d.A = m ? A + a : nullptr;
     d.B = m ? B + a : nullptr;
     d.N = m ? N + a : nullptr;
+    d.chunk_box = m ? cbox + cb_off[k] : nullptr;
   }
   CK(cudaMemcpyAsync(base + o_desc, descs.data(), sizeof(CloudDev) * count, cudaMemcpyHostToDevice,
                      ctx->stream));
@@ -685,6 +693,14 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     md.dyadic = dyadic;
     md.r0 = r0;
     md.inv_r0 = 1.0 / r0;
+    {
+      const float rmax = (float)std::ldexp(r0, L - 1);
+      for (int a3 = 0; a3 < 3; ++a3) {
+        md.box_lo[a3] = c->n > 0 ? c->lo[a3] - rmax : INFINITY;
+        md.box_hi[a3] = c->n > 0 ? c->hi[a3] + rmax : -INFINITY;
+      }
+      md.box_lo[3] = md.box_hi[3] = 0.f;
+    }
     for (int l = 0; l < L; ++l) {
       const int64_t V = hcnt[s * L + l];
       const double r = std::ldexp(r0, l);

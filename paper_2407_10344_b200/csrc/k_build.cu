@@ -31,7 +31,7 @@ __device__ inline bool finite3(float a, float b, float c) {
 __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restrict__ cov,
                              const float* __restrict__ nrm, int64_t n, float4* __restrict__ A,
                              float4* __restrict__ B, float4* __restrict__ N,
-                             int32_t* __restrict__ stats) {
+                             float* __restrict__ chunk_box, int32_t* __restrict__ stats) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float cm = 0.f;
   bool bad = false;
@@ -68,6 +68,28 @@ __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restri
       lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
       hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
     }
+  }
+  // per-32-point chunk boxes (blocks are 256 threads from the cloud start, so
+  // every warp is exactly one chunk)
+  {
+    float lo3[3], hi3[3];
+    const bool in = i < n;
+    for (int a = 0; a < 3; ++a) {
+      const float v = in ? (a == 0 ? mu[3 * i] : a == 1 ? mu[3 * i + 1] : mu[3 * i + 2]) : 0.f;
+      lo3[a] = in ? v : INFINITY;
+      hi3[a] = in ? v : -INFINITY;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        lo3[a] = fminf(lo3[a], __shfl_xor_sync(0xffffffffu, lo3[a], o));
+        hi3[a] = fmaxf(hi3[a], __shfl_xor_sync(0xffffffffu, hi3[a], o));
+      }
+    const int64_t chunk = i / kChunk;
+    if ((threadIdx.x & 31) < 6 && chunk * kChunk < n)
+      chunk_box[6 * chunk + (threadIdx.x & 31)] =
+          (threadIdx.x & 31) < 3 ? lo3[threadIdx.x & 31] : hi3[(threadIdx.x & 31) - 3];
   }
   unsigned anybad = __ballot_sync(0xffffffffu, bad);
   if ((threadIdx.x & 31) == 0) {
@@ -324,9 +346,10 @@ inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 
 }  // namespace
 
 void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* A,
-                       float4* B, float4* N, int32_t* stats, cudaStream_t stream) {
+                       float4* B, float4* N, float* chunk_box, int32_t* stats,
+                       cudaStream_t stream) {
   if (n <= 0) return;
-  k_cloud_pack<<<grid_for(n, 256), 256, 0, stream>>>(mu, cov, nrm, n, A, B, N, stats);
+  k_cloud_pack<<<grid_for(n, 256), 256, 0, stream>>>(mu, cov, nrm, n, A, B, N, chunk_box, stats);
   note_launch();
 }
 

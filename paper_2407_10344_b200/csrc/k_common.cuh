@@ -70,6 +70,45 @@ __device__ inline int32_t clamp_coord(int32_t k) {
   return min(max(k, -(1 << 30)), 1 << 30);
 }
 
+// Exact culling: true if no point of the source chunk (box lo/hi in the source
+// frame) can fall inside the map's conservative box after q = R mu + t.
+// Interval arithmetic in fp32 plus a 1 mm margin (far above its rounding).
+__device__ inline bool chunk_culled(const float* box, const float* Rf, const double* t,
+                                    const float* map_lo, const float* map_hi) {
+  const float cx = 0.5f * (box[0] + box[3]), cy = 0.5f * (box[1] + box[4]), cz = 0.5f * (box[2] + box[5]);
+  const float hx = 0.5f * (box[3] - box[0]), hy = 0.5f * (box[4] - box[1]), hz = 0.5f * (box[5] - box[2]);
+  bool out = false;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float qc = fmaf(Rf[3 * a], cx, fmaf(Rf[3 * a + 1], cy, fmaf(Rf[3 * a + 2], cz, (float)t[a])));
+    // half-extent of the rotated box, plus 1 mm and a relative term bounding the
+    // fp32 rounding of Rf, t and the products (|terms| summed, not |qc|)
+    const float mag = fabsf(Rf[3 * a]) * fabsf(cx) + fabsf(Rf[3 * a + 1]) * fabsf(cy) +
+                      fabsf(Rf[3 * a + 2]) * fabsf(cz) + fabsf((float)t[a]);
+    const float qh = fabsf(Rf[3 * a]) * hx + fabsf(Rf[3 * a + 1]) * hy + fabsf(Rf[3 * a + 2]) * hz +
+                     1e-3f + 1e-6f * (mag + hx + hy + hz);
+    out |= (qc + qh < map_lo[a]) || (qc - qh > map_hi[a]);
+  }
+  return out;
+}
+
+// Culling bits for 32 chunks at once (whole warp, all lanes): lane j tests
+// chunk c0 + j * stride of the cloud (chunks at or past `nchunks` count as
+// culled: they hold no points).  Bit j of the result = chunk culled.
+__device__ inline uint32_t cull_ballot(const float* __restrict__ chunk_box, int64_t c0, int stride,
+                                       int64_t nchunks, const float* Rf, const double* t,
+                                       const float* map_lo, const float* map_hi) {
+  const int64_t c = c0 + (int64_t)(threadIdx.x & 31) * stride;
+  bool cul = true;
+  if (c < nchunks) {
+    float box[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) box[j] = __ldg(chunk_box + 6 * c + j);
+    cul = chunk_culled(box, Rf, t, map_lo, map_hi);
+  }
+  return __ballot_sync(0xffffffffu, cul);
+}
+
 __device__ inline double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

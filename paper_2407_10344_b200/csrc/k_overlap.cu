@@ -38,6 +38,8 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   __shared__ MapLevelDev lv_s;
   __shared__ int dyadic_s;
   __shared__ int warp_cnt[kThreads / 32];
+  __shared__ float Rf[9], map_lo[4], map_hi[4];
+  __shared__ const float* cbox_s;
   const int tid = threadIdx.x;
   const int64_t tile = blockIdx.x;
   const int32_t p = __ldg(tile_pair + tile);
@@ -49,17 +51,23 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
     int64_t b = (int64_t)(tile - __ldg(tile_start + p)) * tile_pts;
     int64_t e = b + tile_pts;
     A_s = cd->A;
+    cbox_s = cd->chunk_box;
     range_s[0] = b;
     range_s[1] = e < cd->n ? e : cd->n;
   } else if (tid == 64) {
     const MapDev* md = maps[pd.tgt];
     lv_s = md->lv[level];
     dyadic_s = md->dyadic;
+    for (int j = 0; j < 4; ++j) {
+      map_lo[j] = md->box_lo[j];
+      map_hi[j] = md->box_hi[j];
+    }
   }
   __syncthreads();
   if (tid == 0) {
     double v[3];
     relative_pose_dev(pose_s, pose_s + 12, R, t, v);
+    for (int j = 0; j < 9; ++j) Rf[j] = (float)R[j];
   }
   __syncthreads();
   const MapLevelDev lv = lv_s;
@@ -69,18 +77,25 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   const int64_t kb = range_s[0], ke = range_s[1];
   // U points per thread per iteration: their loads are in flight together
   constexpr int U = GVOX_OVL_U;
-  for (int64_t k0 = kb + tid; k0 < ke; k0 += U * kThreads) {
+  // exact chunk culling: sub-iteration m = it * U + u of warp w covers tile
+  // chunk 8 m + w; m < tile_pts / 256 <= 32, so one ballot covers the tile
+  const uint32_t cull =
+      cbox_s ? cull_ballot(cbox_s, (kb >> 5) + (tid >> 5), kThreads / 32, (ke + 31) >> 5, Rf, t,
+                           map_lo, map_hi)
+             : 0u;
+  int m = 0;
+  for (int64_t k0 = kb + tid; k0 < ke; k0 += U * kThreads, m += U) {
     float4 a[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t k = k0 + u * kThreads;
-      if (k < ke) a[u] = __ldg(A + k);
+      if (k < ke && !((cull >> (m + u)) & 1u)) a[u] = __ldg(A + k);
     }
     int32_t hit[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       hit[u] = -1;
-      if (k0 + u * kThreads < ke) {
+      if (k0 + u * kThreads < ke && !((cull >> (m + u)) & 1u)) {
         const double mx = a[u].x, my = a[u].y, mz = a[u].z;
         const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
         const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
@@ -125,6 +140,8 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   __shared__ MapLevelDev lv_s;
   __shared__ int dyadic_s;
   __shared__ int warp_cnt[2][kThreads / 32];
+  __shared__ float Rf[9], map_lo[4], map_hi[4];
+  __shared__ const float* cbox_s;
   const int tid = threadIdx.x;
   const int32_t p = blockIdx.x;
   const PairDev pd = pairs[p];
@@ -133,39 +150,54 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   } else if (tid == 32) {
     const CloudDev* cd = clouds[pd.src];
     A_s = cd->A;
+    cbox_s = cd->chunk_box;
     n_s = cd->n;
   } else if (tid == 64) {
     const MapDev* md = maps[pd.tgt];
     lv_s = md->lv[level];
     dyadic_s = md->dyadic;
+    for (int j = 0; j < 4; ++j) {
+      map_lo[j] = md->box_lo[j];
+      map_hi[j] = md->box_hi[j];
+    }
   }
   __syncthreads();
   if (tid == 0) {
     double v[3];
     relative_pose_dev(pose_s, pose_s + 12, R, t, v);
+    for (int j = 0; j < 9; ++j) Rf[j] = (float)R[j];
   }
   __syncthreads();
   const MapLevelDev lv = lv_s;
   const int dyadic = dyadic_s;
   const float4* __restrict__ A = A_s;
   const int64_t n = n_s;
+  const float* cbox = cbox_s;
+  const int64_t nchunks = (n + 31) >> 5;
+  uint32_t cull = 0;  // bits for sub-iterations m .. m + 31 (chunk 8 m + warp)
   // count * den > n * num  <=>  count >= need
   const int64_t need = (n * (int64_t)num) / den + 1;
   constexpr int U = GVOX_OVL_U;
   int64_t total = 0;
   int buf = 0;
   bool sel = false;
-  for (int64_t k0 = 0; k0 < n; k0 += (int64_t)U * kThreads) {
+  static_assert(32 % U == 0, "ballot refresh");
+  int m = 0;
+  for (int64_t k0 = 0; k0 < n; k0 += (int64_t)U * kThreads, m += U) {
+    if (cbox && (m & 31) == 0)  // uniform over the CTA: every warp refreshes
+      cull = cull_ballot(cbox, (int64_t)m * (kThreads / 32) + (tid >> 5), kThreads / 32, nchunks,
+                         Rf, t, map_lo, map_hi);
+    const uint32_t cm = cull >> (m & 31);
     int cnt = 0;
     float4 a[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t k = k0 + u * kThreads + tid;
-      if (k < n) a[u] = __ldg(A + k);
+      if (k < n && !((cm >> u) & 1u)) a[u] = __ldg(A + k);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (k0 + u * kThreads + tid < n) {
+      if (k0 + u * kThreads + tid < n && !((cm >> u) & 1u)) {
         const double mx = a[u].x, my = a[u].y, mz = a[u].z;
         const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
         const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));

@@ -160,6 +160,50 @@ def test_overlap_select_matches_exact_decision(gv, ctx, oracle, num, den):
             assert int(g) == int(cnt * den > len(srcs[p[0]]) * num), (p, cnt, len(srcs[p[0]]))
 
 
+def test_chunk_culling_exact(gv, ctx, oracle):
+    """Spatially ordered sources sweeping across the map's edge: whole 32-point
+    chunks are culled by their transformed bounding box (K2/K3).  The
+    culled result must equal the oracle and, bit for bit, the unculled path
+    (the correspondence dump disables culling), including points just inside
+    the coarsest voxels that stick out of the map's own extent."""
+    import torch
+    rs = np.random.default_rng(23)
+    # map: points on the slab x in [0, 10] (r0 = 0.5, L = 3: coarsest voxel 2 m)
+    nm = 12000
+    mu_m = np.stack([rs.uniform(0, 10, nm), rs.uniform(-5, 5, nm), rs.uniform(-1, 1, nm)], 1)
+    mu_m[:5] = [10.0001, 0.5, 0.5]  # x max just past 10: level-2 voxel [10, 12) reaches 12.0001
+    cov = np.tile(plane_cov(np.array([0.0, 0.0, 1.0]))[None], (nm, 1)).astype(np.float32)
+    srcs = []
+    for n, (a, b) in ((6000, (-20, 30)), (4000, (9.0, 12.5)), (3001, (-2.5, 1.0)), (700, (20, 40))):
+        x = np.sort(rs.uniform(a, b, n))
+        srcs.append(np.stack([x, rs.uniform(-6, 6, n), rs.uniform(-1.5, 1.5, n)], 1).astype(np.float32))
+    # at the map box edge (x max + 2 m): x = 11.999 hits voxel [10, 12) of level 2
+    srcs.append(np.array([[11.999, 0.1, 0.1]] * 40 + [[12.001, 0.1, 0.1]] * 40, np.float32))
+    clouds = [gv.Cloud(ctx, s_, cov[:len(s_)] if len(s_) <= nm else np.tile(cov[:1], (len(s_), 1)))
+              for s_ in srcs]
+    m_cloud = gv.Cloud(ctx, mu_m.astype(np.float32), cov)
+    maps = gv.create_voxelmaps(ctx, [m_cloud], 0.5, 3)
+    om = oracle.VoxelMap(mu_m.astype(np.float32), cov, 0.5, 3)
+    poses = [to12(np.eye(4))] + [random_pose(rs, 0.05, 0.5) for _ in range(4)]
+    pairs = [[s_, 0, k % 5, 0] for s_ in range(len(srcs)) for k in range(3)]
+    for level in range(3):
+        got = gv.overlap(ctx, clouds, maps, pairs, poses, level)
+        for p, g in zip(pairs, got):
+            assert int(g) == oracle.overlap(srcs[p[0]], om, poses[p[2]], poses[p[3]], level), (p, level)
+        sel = gv.overlap_select(ctx, clouds, maps, pairs, poses, level, 1, 4)
+        n = np.array([len(srcs[p[0]]) for p in pairs])
+        assert np.array_equal(sel.astype(bool), 4 * got.astype(np.int64) > n)
+    fac = np.array([[p[0], 0, p[2], 0, 0] for p in pairs], np.int64)
+    out = gv.linearize_batch(ctx, clouds, maps, fac, poses)
+    corr = torch.empty(gv.corr_dump_size(clouds, maps, fac), dtype=torch.int64, device=ctx.device)
+    nocull = gv.linearize_batch(ctx, clouds, maps, fac, poses, corr_dump=corr)
+    assert out.tobytes() == nocull.tobytes()
+    assert list(out["inliers"][-3, :3]) == [0, 0, 40]  # identity pose: level 2 only
+    for k, f in enumerate(fac):
+        ref = oracle.linearize(srcs[f[0]], cov[:len(srcs[f[0]])], None, om, poses[f[2]], poses[f[3]])
+        compare_factor(out[k], ref, 3, what=f"cull factor {k}")
+
+
 def test_overlap_c2(gv, ctx, oracle):
     sc = synth.make("C2")
     clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
