@@ -229,7 +229,7 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
                       const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
                       int64_t num_tiles, int tile_pts, int max_levels, const double* poses,
                       double* partials, int32_t* tile_factor, int64_t* corr_dump,
-                      bool all_dense, cudaStream_t stream);
+                      bool all_dense, bool fast, cudaStream_t stream);
 // reduce tile partials per factor in fixed order; write full or compact records.
 void launch_reduce(const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
                    const double* poses, const double* partials, gvox_linear_factor* out_full,

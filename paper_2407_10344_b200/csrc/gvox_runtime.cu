@@ -1103,11 +1103,14 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
   int64_t total_pf = 0;
   int max_levels = 1;
   bool all_dense = true;
+  bool fast = corr_dump == nullptr && std::getenv("GVOX_LIN_GENERIC") == nullptr;
   for (int64_t f = 0; f < num_factors; ++f) {
     total_pf += clouds[factors[f].source_cloud]->n;
     const gvox_map* m = maps[factors[f].target_map];
     max_levels = std::max(max_levels, m->levels);
     for (int l = 0; l < m->levels; ++l) all_dense = all_dense && m->desc.lv[l].dense;
+    // the specialised kernel: exactly 3 dyadic levels, no visibility test
+    fast = fast && m->levels == 3 && m->desc.dyadic && !(factors[f].flags & GVOX_F_VALIDATE_SURFACE);
   }
   std::vector<int32_t> tstart(num_factors + 1, 0);
   std::vector<FactorDev> fdev(num_factors);
@@ -1173,7 +1176,7 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
     launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
                      (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
                      0, max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
-                     (int32_t*)(wb + o_tf), corr_dump, all_dense, ctx->stream);
+                     (int32_t*)(wb + o_tf), corr_dump, all_dense, fast, ctx->stream);
   }
   CK_LAUNCH("linearize");
   {

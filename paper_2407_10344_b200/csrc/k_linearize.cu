@@ -48,13 +48,15 @@ namespace {
 #ifndef GVOX_LIN_MINB
 #define GVOX_LIN_MINB 4
 #endif
-// largest tile = 256 * 64 points (runtime tile plan: ppt <= 64)
-#define GVOX_LIN_MAX_PPT 64
-#ifndef GVOX_LIN_CULL
-#define GVOX_LIN_CULL 0  // measured: C5 selected factors have ~no culled chunks (+3% time)
-#endif
 #ifndef GVOX_LIN_G
 #define GVOX_LIN_G 4
+#endif
+// source prefetch: 0 = per-thread cp.async (LDGSTS), 1 = per-warp bulk copy + mbarrier
+#ifndef GVOX_LIN_BULK
+#define GVOX_LIN_BULK 0
+#endif
+#ifndef GVOX_LIN_STAGES
+#define GVOX_LIN_STAGES 2
 #endif
 
 
@@ -66,8 +68,6 @@ struct FactorShared {
   double t[3];
   double v[3];
   float Rf[9];
-  float map_lo[4], map_hi[4];  // conservative map box (chunk culling)
-  const float* cbox;           // source chunk boxes
   const float4* A;
   const float4* B;
   const float4* N;
@@ -83,7 +83,56 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+// all but the newest N groups have landed
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// mbarrier + bulk copy (async proxy) helpers
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+// Dense-grid probe without branches: the load is predicated on the bounds test.
+__device__ __forceinline__ int32_t lookup_dense_pred(const MapLevelDev& lv, int32_t kx, int32_t ky,
+                                                     int32_t kz) {
+  const int4 b0 = *reinterpret_cast<const int4*>(&lv.x0);   // x0 y0 z0 dx
+  const uint4 b1 = *reinterpret_cast<const uint4*>(&lv.dy);  // dy dz syz dense
+  const uint32_t cx = (uint32_t)(kx - b0.x), cy = (uint32_t)(ky - b0.y), cz = (uint32_t)(kz - b0.z);
+  const bool in = (cx < (uint32_t)b0.w) & (cy < b1.x) & (cz < b1.y);
+  int32_t v = -1;
+  if (in) v = __ldg(lv.grid + (cx * b1.z + cy * b1.y + cz));
+  return v;
+}
 
 // 1/x for x > 0 finite (MUFU.RCP, ~1 ulp)
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -152,7 +201,6 @@ __device__ __forceinline__ void stage_factor(FactorShared& sh, double* pose_s,
     sh.A = cd->A;
     sh.B = cd->B;
     sh.N = cd->N;
-    sh.cbox = cd->chunk_box;
     sh.begin = b;
     sh.end = e < n ? e : n;
     sh.validate = (fd.flags & GVOX_F_VALIDATE_SURFACE) && cd->has_normals;
@@ -164,11 +212,6 @@ __device__ __forceinline__ void stage_factor(FactorShared& sh, double* pose_s,
     sh.dyadic = md->dyadic;
     sh.r0 = md->r0;
     sh.inv_r0 = md->inv_r0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      sh.map_lo[j] = md->box_lo[j];
-      sh.map_hi[j] = md->box_hi[j];
-    }
   } else if (tid >= 96 && tid < 96 + MAXL) {
     const MapDev* md = maps[fd.tgt];
     sh.lv[tid - 96] = md->lv[tid - 96];
@@ -388,8 +431,14 @@ __device__ __forceinline__ void tile_reduce(const Acc<MAXL>& ac, double (*red)[k
   }
 }
 
-// ---------------------------------------------------------------- K3: register version
-template <int MAXL, bool ALL_DENSE>
+// ---------------------------------------------------------------- K3
+// Source records are prefetched S - 1 iterations ahead into a per-warp ring in
+// shared memory: per-thread cp.async (LDGSTS, default) or, with GVOX_LIN_BULK,
+// one lane per warp arming an mbarrier and issuing three cp.async.bulk copies
+// (the A, B, N planes of the warp's next 32 points).  FAST is the specialisation for the common
+// batch (exactly MAXL dyadic levels, no visibility test, no correspondence
+// dump): no runtime level / flag tests and branch-free grid probes.
+template <int MAXL, bool ALL_DENSE, bool FAST>
 __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     k_linearize(const CloudDev* const* __restrict__ clouds, const MapDev* const* __restrict__ maps,
                 const FactorDev* __restrict__ factors, const int32_t* __restrict__ tile_start,
@@ -399,65 +448,74 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
   __shared__ FactorShared sh;
   __shared__ double red[kWarps][kPartialStride];
   __shared__ double pose_s[24];
+  constexpr int S = GVOX_LIN_STAGES;
+  __shared__ __align__(128) float4 sbuf[kWarps][S][3][32];
+  __shared__ __align__(8) uint64_t mbar[kWarps][S];
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int64_t tile = blockIdx.x;
+  if (GVOX_LIN_BULK && lane == 0) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) mbar_init(&mbar[warp][j], 1);
+    fence_mbar_init();
+  }
   stage_factor<MAXL>(sh, pose_s, clouds, maps, factors, tile_start, tile_factor, tile_pts, poses,
                      tile);
-  const int L = sh.L;
-  const int dyadic = sh.dyadic;
+  const int L = FAST ? MAXL : sh.L;
+  const int dyadic = FAST ? 1 : sh.dyadic;
   const double r0 = sh.r0, inv_r0 = sh.inv_r0;
   const float r0f = (float)sh.r0;
-  const bool validate = sh.validate;
+  const bool validate = FAST ? false : (bool)sh.validate;
   const bool error_only = sh.error_only;
+  if (FAST) corr = nullptr;
   // 32-bit point index within the tile; the source planes pre-offset to its start
   const int64_t begin = sh.begin;
   const int32_t npts = (int32_t)(sh.end - sh.begin);
-  const float4* __restrict__ Ap = sh.A + begin;
-  const float4* __restrict__ Bp = sh.B + begin;
-  const float4* __restrict__ Np = sh.N + begin;
   int64_t* const corr_t = corr ? corr + sh.corr_base + begin * L : nullptr;
   Acc<MAXL> ac;
 
-  // software pipeline: the next point's 48 B source record is copied into a
-  // per-thread double buffer in shared memory by cp.async (LDGSTS) while the
-  // current one is processed -- no registers held, no register copies.  Each
-  // thread only reads its own slots, so no block barrier is needed.
-  __shared__ float4 src_buf[2][3][kThreads];
-  // Exact chunk culling (K3): iteration i of warp w covers tile chunk
-  // 4 i + w (32 consecutive points); a chunk whose transformed box misses the
-  // map box has no correspondence at any level, so it is skipped whole.  Not
-  // with the visibility test (its invisible count) or the correspondence dump.
-  __shared__ uint32_t cull_s[kWarps][(GVOX_LIN_MAX_PPT * 256 / kThreads + 31) / 32];
-  const int warp = tid >> 5;
-  const bool cull_on = GVOX_LIN_CULL && !validate && !corr && sh.cbox != nullptr;
-  const int32_t iters = (npts + kThreads - 1) / kThreads;
-  if (cull_on) {
-    const int64_t nchunks = (sh.end + 31) >> 5;
-    for (int32_t i0 = 0; i0 < iters; i0 += 32)
-      cull_s[warp][i0 >> 5] = cull_ballot(sh.cbox, (begin >> 5) + (int64_t)i0 * kWarps + warp,
-                                          kWarps, nchunks, sh.Rf,
-                                          sh.t, sh.map_lo, sh.map_hi);
-    __syncwarp();
-  }
-  auto culled = [&](int32_t i) -> bool {
-    return cull_on && ((cull_s[warp][i >> 5] >> (i & 31)) & 1u);
-  };
-  auto issue = [&](int32_t kk, int buf) {
-    if (kk < npts && !culled(kk / kThreads)) {
-      cp_async16(&src_buf[buf][0][tid], Ap + kk);
-      cp_async16(&src_buf[buf][1][tid], Bp + kk);
-      cp_async16(&src_buf[buf][2][tid], Np + kk);
+  // prefetch of iteration i (points i * kThreads + 32 warp + lane) into stage st
+  auto issue = [&](int32_t i, int st) {
+    const int32_t base = i * kThreads + 32 * warp;
+    if (GVOX_LIN_BULK) {
+      if (lane == 0 && base < npts) {
+        const int32_t cnt = npts - base < 32 ? npts - base : 32;
+        const unsigned bytes = 16u * (unsigned)cnt;
+        uint64_t* bar = &mbar[warp][st];
+        mbar_expect_tx(bar, 3u * bytes);
+        bulk_g2s(&sbuf[warp][st][0][0], sh.A + begin + base, bytes, bar);
+        bulk_g2s(&sbuf[warp][st][1][0], sh.B + begin + base, bytes, bar);
+        bulk_g2s(&sbuf[warp][st][2][0], sh.N + begin + base, bytes, bar);
+      }
+    } else {
+      if (base + lane < npts) {
+        cp_async16(&sbuf[warp][st][0][lane], sh.A + begin + base + lane);
+        cp_async16(&sbuf[warp][st][1][lane], sh.B + begin + base + lane);
+        cp_async16(&sbuf[warp][st][2][lane], sh.N + begin + base + lane);
+      }
+      cp_async_commit();
     }
-    cp_async_commit();
   };
-  issue(tid, 0);
-  int buf = 0;
-  for (int32_t k = tid; k < npts; k += kThreads, buf ^= 1) {
-    issue(k + kThreads, buf ^ 1);
-    cp_async_wait_1();  // this point's group has landed (the next one may be in flight)
-    if (culled(k / kThreads)) continue;
-    const float4 a = src_buf[buf][0][tid], b = src_buf[buf][1][tid], c = src_buf[buf][2][tid];
-    if (validate && invisible(sh, a, c)) {
+#pragma unroll
+  for (int j = 0; j < S - 1; ++j) issue(j, j);
+  int st = 0, ph = 0;  // stage of iteration i and its mbarrier phase
+  for (int32_t i = 0; i * kThreads + 32 * warp < npts; ++i) {
+    __syncwarp();  // every lane is done with the stage refilled below (read at i - 1)
+    issue(i + S - 1, st == 0 ? S - 1 : st - 1);
+    if (GVOX_LIN_BULK)
+      mbar_wait(&mbar[warp][st], (unsigned)ph);
+    else
+      cp_async_wait<S - 1>();
+    const int cur = st;
+    if (++st == S) {
+      st = 0;
+      ph ^= 1;
+    }
+    const int32_t k = i * kThreads + 32 * warp + lane;
+    if (k >= npts) continue;
+    const float4 a = sbuf[warp][cur][0][lane], b = sbuf[warp][cur][1][lane],
+                 c = sbuf[warp][cur][2][lane];
+    if (!FAST && validate && invisible(sh, a, c)) {
       ++ac.n_invisible;
       if (corr)
         for (int l = 0; l < L; ++l) corr_t[k * L + l] = -2;
@@ -473,12 +531,16 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     constexpr int G = MAXL < GVOX_LIN_G ? MAXL : GVOX_LIN_G;
 #pragma unroll
     for (int lb = 0; lb < MAXL; lb += G) {
-      if (lb >= L) break;
+      if (!FAST && lb >= L) break;
       int32_t vid[G];
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const int l = lb + j;
-        vid[j] = l < L ? lookup_level<ALL_DENSE>(sh.lv[l], pd.k0x >> l, pd.k0y >> l, pd.k0z >> l) : -1;
+        if (FAST)
+          vid[j] = lookup_dense_pred(sh.lv[l], pd.k0x >> l, pd.k0y >> l, pd.k0z >> l);
+        else
+          vid[j] = l < L ? lookup_level<ALL_DENSE>(sh.lv[l], pd.k0x >> l, pd.k0y >> l, pd.k0z >> l)
+                         : -1;
       }
       if (corr) {
         for (int j = 0; j < G && lb + j < L; ++j) {
@@ -687,20 +749,21 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
                       const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
                       int64_t num_tiles, int tile_pts, int max_levels, const double* poses,
                       double* partials, int32_t* tile_factor, int64_t* corr_dump,
-                      bool all_dense, cudaStream_t stream) {
+                      bool all_dense, bool fast, cudaStream_t stream) {
   if (num_tiles <= 0) return;
   const unsigned grid = (unsigned)num_tiles;
-  if (max_levels <= 3) {
+  if (fast && max_levels == 3 && all_dense) {
+    k_linearize<3, true, true><<<grid, kThreads, 0, stream>>>(
+        clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, nullptr);
+  } else if (max_levels <= 3) {
     if (all_dense)
-      k_linearize<3, true><<<grid, kThreads, 0, stream>>>(clouds, maps, factors, tile_start,
-                                                          tile_factor, tile_pts, poses, partials,
-                                                          corr_dump);
+      k_linearize<3, true, false><<<grid, kThreads, 0, stream>>>(
+          clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
     else
-      k_linearize<3, false><<<grid, kThreads, 0, stream>>>(clouds, maps, factors, tile_start,
-                                                           tile_factor, tile_pts, poses, partials,
-                                                           corr_dump);
+      k_linearize<3, false, false><<<grid, kThreads, 0, stream>>>(
+          clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
   } else {
-    k_linearize<GVOX_MAX_LEVELS, false><<<grid, kThreads, 0, stream>>>(
+    k_linearize<GVOX_MAX_LEVELS, false, false><<<grid, kThreads, 0, stream>>>(
         clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
   }
   note_launch();

@@ -381,6 +381,21 @@ def test_batch_equals_serial_and_determinism(gv, ctx):
     assert all(r[k].tobytes() == r[0].tobytes() for k in range(5))
 
 
+def test_fast_kernel_equals_generic(gv, ctx, monkeypatch):
+    """The specialised kernel (3 dyadic dense levels, no visibility test, no
+    dump) performs the same arithmetic in the same order as the generic one."""
+    sc = synth.make("C2")
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    f = sc.factors.copy()
+    f[:, 4] = 0
+    fast = gv.linearize_batch(ctx, clouds, maps, f, sc.poses)
+    monkeypatch.setenv("GVOX_LIN_GENERIC", "1")
+    generic = gv.linearize_batch(ctx, clouds, maps, f, sc.poses)
+    assert fast.tobytes() == generic.tobytes()
+    assert fast["inliers"].sum() > 0
+
+
 def test_compact_expand_equals_full(gv, ctx):
     import torch
     sc = synth.make("C2")

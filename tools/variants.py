@@ -13,7 +13,10 @@ OUT = os.path.join(ROOT, "paper_2407_10344_b200", "build", "variants")
 VARIANTS = {
     # linearize kernel (C5, r01 results in k_linearize.cu's knob comment)
     "base": [],
-    "nocull": ["GVOX_LIN_CULL=0"],
+    "s3": ["GVOX_LIN_STAGES=3"],
+    "bulk2": ["GVOX_LIN_BULK=1"],
+    "bulk3": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=3"],
+    "bulk4": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=4"],
     "t256_b2": ["GVOX_LIN_THREADS=256", "GVOX_LIN_MINB=2"],
     "t128_b3": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=3"],
     "g1": ["GVOX_LIN_G=1"],
