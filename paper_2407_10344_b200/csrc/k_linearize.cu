@@ -55,8 +55,11 @@ namespace {
 #ifndef GVOX_LIN_BULK
 #define GVOX_LIN_BULK 0
 #endif
+#ifndef GVOX_LIN_PIPE
+#define GVOX_LIN_PIPE 1
+#endif
 #ifndef GVOX_LIN_STAGES
-#define GVOX_LIN_STAGES 2
+#define GVOX_LIN_STAGES (GVOX_LIN_PIPE ? 3 : 2)
 #endif
 
 
@@ -80,6 +83,9 @@ struct FactorShared {
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16_s(unsigned s, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -474,6 +480,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
   int64_t* const corr_t = corr ? corr + sh.corr_base + begin * L : nullptr;
   Acc<MAXL> ac;
 
+  const unsigned s_lane = smem_addr(&sbuf[warp][0][0][lane]);
   // prefetch of iteration i (points i * kThreads + 32 warp + lane) into stage st
   auto issue = [&](int32_t i, int st) {
     const int32_t base = i * kThreads + 32 * warp;
@@ -488,19 +495,88 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
         bulk_g2s(&sbuf[warp][st][2][0], sh.N + begin + base, bytes, bar);
       }
     } else {
+      // each thread copies (and later reads) only its own slots: no warp sync
       if (base + lane < npts) {
-        cp_async16(&sbuf[warp][st][0][lane], sh.A + begin + base + lane);
-        cp_async16(&sbuf[warp][st][1][lane], sh.B + begin + base + lane);
-        cp_async16(&sbuf[warp][st][2][lane], sh.N + begin + base + lane);
+        const unsigned sa = s_lane + (unsigned)st * (unsigned)sizeof(sbuf[0][0]);
+        cp_async16_s(sa, sh.A + begin + base + lane);
+        cp_async16_s(sa + 512u, sh.B + begin + base + lane);
+        cp_async16_s(sa + 1024u, sh.N + begin + base + lane);
       }
       cp_async_commit();
     }
   };
+#if GVOX_LIN_PIPE
+  if constexpr (FAST) {
+    // Software pipeline over points (FAST only): the next point is transformed
+    // and its grid probes issued before the current point's voxel records are
+    // gathered, so the two dependent memory round trips of consecutive points
+    // overlap.  Needs a 3-stage ring: current (B, C planes), next (A plane),
+    // and the copy in flight.
+    static_assert(S >= 3, "GVOX_LIN_PIPE needs GVOX_LIN_STAGES >= 3");
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j) issue(j, j);
+    cp_async_wait<S - 2>();  // iteration 0 landed
+    PointData pn;
+    int32_t vn[MAXL];
+    auto prep = [&](int32_t kk, int stg) {
+#pragma unroll
+      for (int l = 0; l < MAXL; ++l) vn[l] = -1;
+      if (kk < npts) {
+        const float4 a = sbuf[warp][stg][0][lane];
+        transform_point(sh, a, 1, r0, inv_r0, r0f, pn);
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l)
+          vn[l] = lookup_dense_pred(sh.lv[l], pn.k0x >> l, pn.k0y >> l, pn.k0z >> l);
+      }
+    };
+    prep(tid, 0);
+    int st = 0;
+    for (int32_t i = 0; i * kThreads + 32 * warp < npts; ++i) {
+      issue(i + S - 1, st == 0 ? S - 1 : st - 1);
+      cp_async_wait<S - 2>();  // iteration i + 1 landed
+      const int cur = st;
+      if (++st == S) st = 0;
+      const int32_t k = i * kThreads + tid;
+      PointData pd = pn;
+      int32_t vid[MAXL];
+#pragma unroll
+      for (int l = 0; l < MAXL; ++l) vid[l] = vn[l];
+      prep(k + kThreads, st);
+      bool any = false;
+#pragma unroll
+      for (int l = 0; l < MAXL; ++l) any |= vid[l] >= 0;
+      if (k >= npts || !any) continue;
+      float4 v0[MAXL], v1[MAXL];
+      float v2[MAXL];
+#pragma unroll
+      for (int l = 0; l < MAXL; ++l) {
+        if (vid[l] >= 0) {
+          const float4* vp = sh.lv[l].vox + 3 * (int64_t)vid[l];
+          v0[l] = __ldg(vp);
+          v1[l] = __ldg(vp + 1);
+          v2[l] = __ldg(&vp[2].x);
+        }
+      }
+      const float4 a = sbuf[warp][cur][0][lane], b = sbuf[warp][cur][1][lane],
+                   c = sbuf[warp][cur][2][lane];
+      rcr(sh.Rf, a, b, c, pd);
+      LevelSum ls;
+      ls.Oa = ls.Oc = ls.G = 0;
+      ls.o11 = ls.o22 = ls.gz = 0.f;
+#pragma unroll
+      for (int l = 0; l < MAXL; ++l)
+        if (vid[l] >= 0) level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, r0f);
+      if (!error_only) fold_point<MAXL>(ac, ls, pd);
+    }
+    tile_reduce<MAXL>(ac, red, partials, tile);
+    return;
+  }
+#endif
 #pragma unroll
   for (int j = 0; j < S - 1; ++j) issue(j, j);
   int st = 0, ph = 0;  // stage of iteration i and its mbarrier phase
   for (int32_t i = 0; i * kThreads + 32 * warp < npts; ++i) {
-    __syncwarp();  // every lane is done with the stage refilled below (read at i - 1)
+    if (GVOX_LIN_BULK) __syncwarp();  // all lanes done with the stage refilled below
     issue(i + S - 1, st == 0 ? S - 1 : st - 1);
     if (GVOX_LIN_BULK)
       mbar_wait(&mbar[warp][st], (unsigned)ph);

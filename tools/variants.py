@@ -14,6 +14,8 @@ VARIANTS = {
     # linearize kernel (C5, r01 results in k_linearize.cu's knob comment)
     "base": [],
     "s3": ["GVOX_LIN_STAGES=3"],
+    "nopipe": ["GVOX_LIN_PIPE=0"],
+    "pipe_s4": ["GVOX_LIN_STAGES=4"],
     "bulk2": ["GVOX_LIN_BULK=1"],
     "bulk3": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=3"],
     "bulk4": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=4"],
