@@ -2,11 +2,14 @@
 // (gvox_runtime.cu) and the kernels (k_*.cu).  Not part of the ABI.
 //
 // HBM layout:
-//  * cloud: three planar float4 arrays of n points (48 B/point):
+//  * cloud: 48 B/point in chunks of 32 points (1536 B): each chunk holds the
+//    three float4 planes of its 32 points back to back,
 //      A[k] = {mu.x, mu.y, mu.z, C.xx}
 //      B[k] = {C.xy, C.xz, C.yy, C.yz}
 //      N[k] = {C.zz, n.x, n.y, n.z}
-//    the overlap kernel streams only A (16 B/point); linearize streams all 3.
+//    at float4 offset pt_off(k) from A, B = A + 32, N = A + 64 (so one pointer
+//    plus immediates reaches all three planes of a warp's 32 points); the
+//    overlap kernel streams only A (512 B runs, 16 B/point); linearize all 3.
 //  * map level: open-addressing hash of 16 B slots {u64 packed key, i32 voxel
 //    index, pad} (capacity 2^k >= 2V, EMPTY key = ~0) + compact voxel records
 //    of 48 B: {off.x, off.y, off.z, C.xx}, {C.xy, C.yy, C.xz, C.yz},
@@ -26,6 +29,12 @@ constexpr uint64_t kEmptyKey = ~0ull;
 constexpr int kKeyBits = 21;
 constexpr int32_t kKeyHalf = 1 << 20;
 
+constexpr int kChunk = 32;  // points per layout chunk (also the culling box granularity)
+// float4 offset of point k's A record from the cloud's A pointer (B, N: + 32, + 64)
+__host__ __device__ __forceinline__ int64_t pt_off(int64_t k) { return (k >> 5) * 96 + (k & 31); }
+// float4 slots a cloud of n points occupies
+__host__ __device__ __forceinline__ int64_t pt_slots(int64_t n) { return ((n + 31) >> 5) * 96; }
+
 struct CloudDev {
   const float4* A;
   const float4* B;
@@ -37,7 +46,6 @@ struct CloudDev {
   int32_t has_normals;
   int32_t pad;
 };
-constexpr int kChunk = 32;
 
 // One level of a map.  Voxel lookup uses either
 //  * a DENSE index grid over the level's key bounding box (int32 voxel index
@@ -108,9 +116,8 @@ __host__ __device__ inline bool key_in_range(int32_t k) { return k >= -kKeyHalf 
 // (8 int32): [0] |= 1 on non-finite input, [1] = max |C_ij| (float bits),
 // [2..4] = min mu, [5..7] = max mu (order-preserving int encoding of floats;
 // initialise [2..4] to INT_MAX and [5..7] to INT_MIN).
-void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* A,
-                       float4* B, float4* N, float* chunk_box, int32_t* stats,
-                       cudaStream_t stream);
+void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* P,
+                       float* chunk_box, int32_t* stats, cudaStream_t stream);
 
 __host__ __device__ inline int32_t float_to_ordered(float f) {
 #ifdef __CUDA_ARCH__

@@ -379,7 +379,10 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
   DeviceGuard g(ctx->device);
   Layout lay;
   size_t o_desc = lay.add(sizeof(CloudDev) * count);
-  size_t o_a = lay.add(16 * (size_t)n), o_b = lay.add(16 * (size_t)n), o_n = lay.add(16 * (size_t)n);
+  // chunked point records (gvox_internal.h): each cloud starts on a chunk
+  std::vector<int64_t> co(count + 1, 0);
+  for (int64_t k = 0; k < count; ++k) co[k + 1] = co[k] + pt_slots(offsets[k + 1] - offsets[k]);
+  size_t o_pts = lay.add(16 * (size_t)co[count]);
   size_t o_flags = lay.add(32 * (size_t)count);
   // per-cloud chunk boxes (6 floats per 32 points), each cloud's run starting
   // at its own chunk 0
@@ -391,9 +394,7 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
   gvox_status st = devbuf_alloc(lay.size, ctx->device, ctx->stream, &buf);
   if (st) return st;
   char* base = (char*)buf->ptr;
-  float4* A = (float4*)(base + o_a);
-  float4* B = (float4*)(base + o_b);
-  float4* N = (float4*)(base + o_n);
+  float4* P = (float4*)(base + o_pts);
   float* cbox = (float*)(base + o_cbox);
   // per-cloud statistics (see launch_cloud_pack): flag, max |C_ij|, min / max mean
   int32_t* dflags = (int32_t*)(base + o_flags);
@@ -426,8 +427,8 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
     for (int64_t k = 0; k < count; ++k) {
       int64_t a = offsets[k], m = offsets[k + 1] - offsets[k];
       if (m == 0) continue;
-      launch_cloud_pack(dmu + 3 * a, dcov + 6 * a, dnrm ? dnrm + 3 * a : nullptr, m, A + a, B + a,
-                        N + a, cbox + cb_off[k], dflags + 8 * k, ctx->stream);
+      launch_cloud_pack(dmu + 3 * a, dcov + 6 * a, dnrm ? dnrm + 3 * a : nullptr, m, P + co[k],
+                        cbox + cb_off[k], dflags + 8 * k, ctx->stream);
     }
     CK_LAUNCH("gvox_cloud_create: pack");
   }
@@ -445,9 +446,9 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
     d.n = m;
     d.has_normals = normals != nullptr;
     d.pad = 0;
-    d.A = m ? A + a : nullptr;
-    d.B = m ? B + a : nullptr;
-    d.N = m ? N + a : nullptr;
+    d.A = m ? P + co[k] : nullptr;
+    d.B = m ? P + co[k] + 32 : nullptr;
+    d.N = m ? P + co[k] + 64 : nullptr;
     d.chunk_box = m ? cbox + cb_off[k] : nullptr;
   }
   CK(cudaMemcpyAsync(base + o_desc, descs.data(), sizeof(CloudDev) * count, cudaMemcpyHostToDevice,

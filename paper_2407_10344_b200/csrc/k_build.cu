@@ -29,8 +29,7 @@ __device__ inline bool finite3(float a, float b, float c) {
 }
 
 __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restrict__ cov,
-                             const float* __restrict__ nrm, int64_t n, float4* __restrict__ A,
-                             float4* __restrict__ B, float4* __restrict__ N,
+                             const float* __restrict__ nrm, int64_t n, float4* __restrict__ P,
                              float* __restrict__ chunk_box, int32_t* __restrict__ stats) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float cm = 0.f;
@@ -47,9 +46,10 @@ __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restri
       nz = nrm[3 * i + 2];
     }
     bad = !(finite3(x, y, z) && finite3(c0, c1, c2) && finite3(c3, c4, c5) && finite3(nx, ny, nz));
-    A[i] = make_float4(x, y, z, c0);
-    B[i] = make_float4(c1, c2, c3, c4);
-    N[i] = make_float4(c5, nx, ny, nz);
+    float4* r = P + pt_off(i);
+    r[0] = make_float4(x, y, z, c0);
+    r[32] = make_float4(c1, c2, c3, c4);
+    r[64] = make_float4(c5, nx, ny, nz);
     cm = fmaxf(fmaxf(fmaxf(fabsf(c0), fabsf(c1)), fmaxf(fabsf(c2), fabsf(c3))),
                fmaxf(fabsf(c4), fabsf(c5)));
     if (!bad) {
@@ -122,7 +122,7 @@ __global__ void k_build_insert(const BuildSeg* __restrict__ segs, int levels, do
   if (__all_sync(0xffffffffu, !valid)) return;
   int32_t k0x = 0, k0y = 0, k0z = 0;
   if (valid) {
-    const float4 a = __ldg(sg.A + k);
+    const float4 a = __ldg(sg.A + pt_off(k));
     k0x = voxel_coord0((double)a.x, r0, inv_r0, dyadic);
     k0y = voxel_coord0((double)a.y, r0, inv_r0, dyadic);
     k0z = voxel_coord0((double)a.z, r0, inv_r0, dyadic);
@@ -219,9 +219,10 @@ __global__ void k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg
   if (__all_sync(0xffffffffu, !valid)) return;
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, c = a;
   if (valid) {
-    a = __ldg(sg.A + k);
-    b = __ldg(sg.B + k);
-    c = __ldg(sg.N + k);
+    const float4* r = sg.A + pt_off(k);
+    a = __ldg(r);
+    b = __ldg(r + 32);
+    c = __ldg(r + 64);
   }
   const double x = a.x, y = a.y, z = a.z;
   const int32_t k0x = voxel_coord0(x, r0, inv_r0, dyadic);
@@ -345,11 +346,10 @@ inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 
 
 }  // namespace
 
-void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* A,
-                       float4* B, float4* N, float* chunk_box, int32_t* stats,
-                       cudaStream_t stream) {
+void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* P,
+                       float* chunk_box, int32_t* stats, cudaStream_t stream) {
   if (n <= 0) return;
-  k_cloud_pack<<<grid_for(n, 256), 256, 0, stream>>>(mu, cov, nrm, n, A, B, N, chunk_box, stats);
+  k_cloud_pack<<<grid_for(n, 256), 256, 0, stream>>>(mu, cov, nrm, n, P, chunk_box, stats);
   note_launch();
 }
 

@@ -71,9 +71,7 @@ struct FactorShared {
   double t[3];
   double v[3];
   float Rf[9];
-  const float4* A;
-  const float4* B;
-  const float4* N;
+  const float4* A;  // the tile's chunked point records (B = A + 32, N = A + 64 per chunk)
   int64_t begin, end;
   int64_t corr_base;
   double r0, inv_r0;
@@ -204,9 +202,7 @@ __device__ __forceinline__ void stage_factor(FactorShared& sh, double* pose_s,
     int64_t b = (int64_t)(tile - __ldg(tile_start + f)) * fd.tile_pts;
     int64_t e = b + fd.tile_pts;
     int64_t n = cd->n;
-    sh.A = cd->A;
-    sh.B = cd->B;
-    sh.N = cd->N;
+    sh.A = cd->A + pt_off(b);  // the tile's first chunk (tiles are chunk-aligned)
     sh.begin = b;
     sh.end = e < n ? e : n;
     sh.validate = (fd.flags & GVOX_F_VALIDATE_SURFACE) && cd->has_normals;
@@ -485,22 +481,21 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
   auto issue = [&](int32_t i, int st) {
     const int32_t base = i * kThreads + 32 * warp;
     if (GVOX_LIN_BULK) {
+      // the warp's 32 points are one layout chunk: one 1536 B copy (a partial
+      // last chunk copies its unused slots too, inside the allocation)
       if (lane == 0 && base < npts) {
-        const int32_t cnt = npts - base < 32 ? npts - base : 32;
-        const unsigned bytes = 16u * (unsigned)cnt;
         uint64_t* bar = &mbar[warp][st];
-        mbar_expect_tx(bar, 3u * bytes);
-        bulk_g2s(&sbuf[warp][st][0][0], sh.A + begin + base, bytes, bar);
-        bulk_g2s(&sbuf[warp][st][1][0], sh.B + begin + base, bytes, bar);
-        bulk_g2s(&sbuf[warp][st][2][0], sh.N + begin + base, bytes, bar);
+        mbar_expect_tx(bar, (unsigned)sizeof(sbuf[0][0]));
+        bulk_g2s(&sbuf[warp][st][0][0], sh.A + (base >> 5) * 96, (unsigned)sizeof(sbuf[0][0]), bar);
       }
     } else {
       // each thread copies (and later reads) only its own slots: no warp sync
       if (base + lane < npts) {
         const unsigned sa = s_lane + (unsigned)st * (unsigned)sizeof(sbuf[0][0]);
-        cp_async16_s(sa, sh.A + begin + base + lane);
-        cp_async16_s(sa + 512u, sh.B + begin + base + lane);
-        cp_async16_s(sa + 1024u, sh.N + begin + base + lane);
+        const float4* g = sh.A + ((base >> 5) * 96 + lane);
+        cp_async16_s(sa, g);
+        cp_async16_s(sa + 512u, g + 32);
+        cp_async16_s(sa + 1024u, g + 64);
       }
       cp_async_commit();
     }
@@ -515,7 +510,10 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     static_assert(S >= 3, "GVOX_LIN_PIPE needs GVOX_LIN_STAGES >= 3");
 #pragma unroll
     for (int j = 0; j < S - 1; ++j) issue(j, j);
-    cp_async_wait<S - 2>();  // iteration 0 landed
+    if (GVOX_LIN_BULK) {
+      if (32 * warp < npts) mbar_wait(&mbar[warp][0], 0u);  // (issued only if so)
+    } else
+      cp_async_wait<S - 2>();  // iteration 0 landed
     PointData pn;
     int32_t vn[MAXL];
     auto prep = [&](int32_t kk, int stg) {
@@ -530,12 +528,20 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       }
     };
     prep(tid, 0);
-    int st = 0;
+    int st = 0, ph = 0;  // stage of iteration i + 1 below, and its mbarrier phase
     for (int32_t i = 0; i * kThreads + 32 * warp < npts; ++i) {
+      if (GVOX_LIN_BULK) __syncwarp();  // all lanes done with the stage refilled below
       issue(i + S - 1, st == 0 ? S - 1 : st - 1);
-      cp_async_wait<S - 2>();  // iteration i + 1 landed
       const int cur = st;
-      if (++st == S) st = 0;
+      if (++st == S) {
+        st = 0;
+        ph ^= 1;
+      }
+      if (GVOX_LIN_BULK) {
+        if ((i + 1) * kThreads + 32 * warp < npts) mbar_wait(&mbar[warp][st], (unsigned)ph);
+      } else {
+        cp_async_wait<S - 2>();  // iteration i + 1 landed
+      }
       const int32_t k = i * kThreads + tid;
       PointData pd = pn;
       int32_t vid[MAXL];

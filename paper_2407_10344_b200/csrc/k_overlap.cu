@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t k = k0 + u * kThreads;
-      if (k < ke && !((cull >> (m + u)) & 1u)) a[u] = __ldg(A + k);
+      if (k < ke && !((cull >> (m + u)) & 1u)) a[u] = __ldg(A + pt_off(k));
     }
     int32_t hit[U];
 #pragma unroll
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t k = k0 + u * kThreads + tid;
-      if (k < n && !((cm >> u) & 1u)) a[u] = __ldg(A + k);
+      if (k < n && !((cm >> u) & 1u)) a[u] = __ldg(A + pt_off(k));
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {

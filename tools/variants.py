@@ -16,6 +16,8 @@ VARIANTS = {
     "s3": ["GVOX_LIN_STAGES=3"],
     "nopipe": ["GVOX_LIN_PIPE=0"],
     "pipe_s4": ["GVOX_LIN_STAGES=4"],
+    "pbulk3": ["GVOX_LIN_BULK=1"],
+    "pbulk4": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=4"],
     "bulk2": ["GVOX_LIN_BULK=1"],
     "bulk3": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=3"],
     "bulk4": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=4"],
@@ -58,9 +60,14 @@ def run(names, extra, stage="linearize"):
             except Exception:
                 res[n] = p.stderr[-500:]
         else:
-            p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--linearize-only",
-                                "--no-e2e", "--no-cpu-baseline", "--steps", "6", *extra], env=env,
-                               capture_output=True, text=True)
+            try:
+                p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--linearize-only",
+                                    "--no-e2e", "--no-cpu-baseline", "--steps", "6", *extra], env=env,
+                                   capture_output=True, text=True, timeout=240)
+            except subprocess.TimeoutExpired:
+                res[n] = "TIMEOUT"
+                print(n, "TIMEOUT", flush=True)
+                continue
             line = [l for l in p.stderr.splitlines() if "linearize-only" in l]
             res[n] = line[-1] if line else p.stderr[-500:]
         print(n, res[n], flush=True)
