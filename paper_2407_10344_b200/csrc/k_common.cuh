@@ -92,19 +92,76 @@ __device__ inline bool chunk_culled(const float* box, const float* Rf, const dou
   return out;
 }
 
+// Exact culling against the occupancy of a map's COARSEST level (dense grid):
+// levels nest (a level-l voxel holding a map point lies inside that point's
+// coarsest-level voxel), so a source point can hit a voxel at any level only if
+// its coarsest-level cell is occupied.  The chunk's transformed box (fp32
+// interval arithmetic, margins as chunk_culled) is mapped to a cell range; the
+// chunk is culled if the range misses the grid or every cell in it is empty.
+// Ranges wider than 3 cells on an axis, or coordinates beyond 2^22 cells, are
+// not culled.
+__device__ inline bool chunk_culled_grid(const float* box, const float* Rf, const double* t,
+                                         const MapLevelDev& cv) {
+  const float cx = 0.5f * (box[0] + box[3]), cy = 0.5f * (box[1] + box[4]), cz = 0.5f * (box[2] + box[5]);
+  const float hx = 0.5f * (box[3] - box[0]), hy = 0.5f * (box[4] - box[1]), hz = 0.5f * (box[5] - box[2]);
+  const float inv = (float)cv.inv_r;
+  const int32_t org[3] = {cv.x0, cv.y0, cv.z0};
+  const uint32_t dim[3] = {cv.dx, cv.dy, cv.dz};
+  int32_t c0[3], nc[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float qc = fmaf(Rf[3 * a], cx, fmaf(Rf[3 * a + 1], cy, fmaf(Rf[3 * a + 2], cz, (float)t[a])));
+    const float mag = fabsf(Rf[3 * a]) * fabsf(cx) + fabsf(Rf[3 * a + 1]) * fabsf(cy) +
+                      fabsf(Rf[3 * a + 2]) * fabsf(cz) + fabsf((float)t[a]);
+    const float qh = fabsf(Rf[3 * a]) * hx + fabsf(Rf[3 * a + 1]) * hy + fabsf(Rf[3 * a + 2]) * hz +
+                     1e-3f + 1e-6f * (mag + hx + hy + hz);
+    const float vlo = (qc - qh) * inv, vhi = (qc + qh) * inv;
+    const float flo = floorf(vlo - (1e-5f * fabsf(vlo) + 1e-3f));
+    const float fhi = floorf(vhi + (1e-5f * fabsf(vhi) + 1e-3f));
+    if (!(fabsf(flo) < 4194304.f && fabsf(fhi) < 4194304.f)) return false;  // also NaN
+    const int32_t lo = max((int32_t)flo - org[a], 0);
+    const int32_t hi = min((int32_t)fhi - org[a], (int32_t)dim[a] - 1);
+    if (lo > hi) return true;  // the range misses the grid: every cell empty
+    c0[a] = lo;
+    nc[a] = hi - lo + 1;
+  }
+  if (nc[0] > 3 || nc[1] > 3 || nc[2] > 3) return false;
+  // up to 3 x 3 x 3 cells, probed four at a time (loads in flight together)
+  const int total = nc[0] * nc[1] * nc[2], n12 = nc[1] * nc[2];
+  for (int t0 = 0; t0 < total; t0 += 4) {
+    int32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int f = t0 + u;
+      v[u] = -1;
+      if (f < total) {
+        const int i = f / n12, r = f - i * n12, j = r / nc[2], k = r - j * nc[2];
+        v[u] = __ldg(cv.grid + ((uint32_t)(c0[0] + i) * cv.syz + (uint32_t)(c0[1] + j) * cv.dz +
+                                (uint32_t)(c0[2] + k)));
+      }
+    }
+    // all empty <=> every value is -1 <=> their AND is -1 (an index >= 0 clears the sign bit)
+    if ((v[0] & v[1] & v[2] & v[3]) != -1) return false;
+  }
+  return true;
+}
+
 // Culling bits for 32 chunks at once (whole warp, all lanes): lane j tests
 // chunk c0 + j * stride of the cloud (chunks at or past `nchunks` count as
 // culled: they hold no points).  Bit j of the result = chunk culled.
+// cv: the map's coarsest level if its index is a dense grid, else nullptr (then
+// only the map box test applies).
 __device__ inline uint32_t cull_ballot(const float* __restrict__ chunk_box, int64_t c0, int stride,
                                        int64_t nchunks, const float* Rf, const double* t,
-                                       const float* map_lo, const float* map_hi) {
+                                       const float* map_lo, const float* map_hi,
+                                       const MapLevelDev* cv) {
   const int64_t c = c0 + (int64_t)(threadIdx.x & 31) * stride;
   bool cul = true;
   if (c < nchunks) {
     float box[6];
 #pragma unroll
     for (int j = 0; j < 6; ++j) box[j] = __ldg(chunk_box + 6 * c + j);
-    cul = chunk_culled(box, Rf, t, map_lo, map_hi);
+    cul = cv ? chunk_culled_grid(box, Rf, t, *cv) : chunk_culled(box, Rf, t, map_lo, map_hi);
   }
   return __ballot_sync(0xffffffffu, cul);
 }

@@ -58,6 +58,10 @@ namespace {
 #ifndef GVOX_LIN_PIPE
 #define GVOX_LIN_PIPE 1
 #endif
+// exact chunk culling against the coarsest level's occupancy (FAST pipeline)
+#ifndef GVOX_LIN_CULL
+#define GVOX_LIN_CULL 1
+#endif
 #ifndef GVOX_LIN_STAGES
 #define GVOX_LIN_STAGES (GVOX_LIN_PIPE ? 3 : 2)
 #endif
@@ -72,6 +76,7 @@ struct FactorShared {
   double v[3];
   float Rf[9];
   const float4* A;  // the tile's chunked point records (B = A + 32, N = A + 64 per chunk)
+  const float* cbox;  // the tile's first chunk box (6 floats per chunk)
   int64_t begin, end;
   int64_t corr_base;
   double r0, inv_r0;
@@ -182,7 +187,8 @@ struct PointData {
   float ex, ey, ez;   // centre_0 - q (level-0 residual base)
   f2_t Sp1, Sp2;      // (s01, s11), (s02, s12) of R C R^T
   float s00, s22;
-  int32_t k0x, k0y, k0z;  // level-0 key (low bits give the level-l residual base)
+  int32_t k0x, k0y, k0z;  // level-0 key (the grid probes)
+  uint32_t kb;            // low 8 bits of k0x | k0y << 8 | k0z << 16 (level residual bases)
 };
 
 // Stage the factor of `tile` in shared memory (pose, cloud, map levels).
@@ -203,6 +209,7 @@ __device__ __forceinline__ void stage_factor(FactorShared& sh, double* pose_s,
     int64_t e = b + fd.tile_pts;
     int64_t n = cd->n;
     sh.A = cd->A + pt_off(b);  // the tile's first chunk (tiles are chunk-aligned)
+    sh.cbox = cd->chunk_box ? cd->chunk_box + 6 * (b >> 5) : nullptr;
     sh.begin = b;
     sh.end = e < n ? e : n;
     sh.validate = (fd.flags & GVOX_F_VALIDATE_SURFACE) && cd->has_normals;
@@ -249,6 +256,8 @@ __device__ __forceinline__ void transform_point(const FactorShared& sh, const fl
   pd.qx = (float)qx;
   pd.qy = (float)qy;
   pd.qz = (float)qz;
+  pd.kb = ((uint32_t)pd.k0x & 0xffu) | (((uint32_t)pd.k0y & 0xffu) << 8) |
+          (((uint32_t)pd.k0z & 0xffu) << 16);
   pd.ex = 0.5f * r0f - (float)(qx - (double)pd.k0x * r0);
   pd.ey = 0.5f * r0f - (float)(qy - (double)pd.k0y * r0);
   pd.ez = 0.5f * r0f - (float)(qz - (double)pd.k0z * r0);
@@ -321,9 +330,9 @@ __device__ __forceinline__ void level_term(Acc<MAXL>& ac, LevelSum& ls, const Po
   if (l > 0) {
     const int mlo = (1 << l) - 1;
     const float sh_l = 0.5f * (float)(1 << l) - 0.5f;
-    bx = fmaf(r0f, sh_l - (float)(pd.k0x & mlo), pd.ex);
-    by = fmaf(r0f, sh_l - (float)(pd.k0y & mlo), pd.ey);
-    bz = fmaf(r0f, sh_l - (float)(pd.k0z & mlo), pd.ez);
+    bx = fmaf(r0f, sh_l - (float)(pd.kb & mlo), pd.ex);
+    by = fmaf(r0f, sh_l - (float)((pd.kb >> 8) & mlo), pd.ey);
+    bz = fmaf(r0f, sh_l - (float)((pd.kb >> 16) & mlo), pd.ez);
   }
   const f2_t D = add2(pk(bx, by), pk(v0.x, v0.y));  // (dx, dy)
   const float dz = bz + v0.z;
@@ -500,26 +509,67 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       cp_async_commit();
     }
   };
-#if GVOX_LIN_PIPE
+#if GVOX_LIN_PIPE && !GVOX_LIN_BULK
   if constexpr (FAST) {
     // Software pipeline over points (FAST only): the next point is transformed
     // and its grid probes issued before the current point's voxel records are
     // gathered, so the two dependent memory round trips of consecutive points
     // overlap.  Needs a 3-stage ring: current (B, C planes), next (A plane),
     // and the copy in flight.
-    static_assert(S >= 3, "GVOX_LIN_PIPE needs GVOX_LIN_STAGES >= 3");
+    static_assert(S == 3, "GVOX_LIN_PIPE uses a 3-stage ring");
+    // Exact chunk culling (k_common.cuh chunk_culled_grid): iteration i of warp
+    // w covers tile chunk 4 i + w; a chunk whose transformed box meets no
+    // occupied coarsest-level cell has no correspondence at any level.  The warp
+    // walks only its LIVE iterations (identical results: culled points add
+    // nothing), so culled chunks are neither copied nor touched.
+    constexpr int kWords = (64 * 256 / kThreads + 31) / 32;  // tiles <= 64 * 256 points
+    constexpr int kNone = 1 << 30;
+    __shared__ uint32_t live_s[kWarps][kWords];
+    const int32_t iters = (npts - 32 * warp + kThreads - 1) / kThreads;
+    const MapLevelDev& cv = sh.lv[MAXL - 1];
+    const bool cull_on = GVOX_LIN_CULL && sh.cbox != nullptr && cv.grid != nullptr;
 #pragma unroll
-    for (int j = 0; j < S - 1; ++j) issue(j, j);
-    if (GVOX_LIN_BULK) {
-      if (32 * warp < npts) mbar_wait(&mbar[warp][0], 0u);  // (issued only if so)
-    } else
-      cp_async_wait<S - 2>();  // iteration 0 landed
+    for (int i0 = 0; i0 < kWords * 32; i0 += 32) {
+      const int32_t i = i0 + lane;
+      bool live = i < iters;
+      if (cull_on && i0 < iters && live) {
+        const float* bx = sh.cbox + 6 * (i * kWarps + warp);
+        float box[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) box[j] = __ldg(bx + j);
+        live = !chunk_culled_grid(box, sh.Rf, sh.t, cv);
+      }
+      live_s[warp][i0 >> 5] = __ballot_sync(0xffffffffu, live);
+    }
+    __syncwarp();
+    // smallest live iteration > i (kNone if none)
+    auto next_live = [&](int32_t i) -> int32_t {
+      int w = (i + 1) >> 5;
+      if (w >= kWords) return kNone;
+      uint32_t m = live_s[warp][w] & (0xffffffffu << ((i + 1) & 31));
+      while (!m) {
+        if (++w >= kWords) return kNone;
+        m = live_s[warp][w];
+      }
+      return (w << 5) + __ffs(m) - 1;
+    };
+    // stages follow the live SEQUENCE: the j-th live iteration uses stage j % S
+    auto issue_l = [&](int32_t i, int stg) {
+      if (i != kNone) issue(i, stg);
+      else cp_async_commit();  // keep one group per sequence slot
+    };
+    int32_t i_cur = next_live(-1);
+    int32_t i_nxt = i_cur == kNone ? kNone : next_live(i_cur);
+    int32_t i_nx2 = i_nxt == kNone ? kNone : next_live(i_nxt);
+    issue_l(i_cur, 0);
+    issue_l(i_nxt, 1);
+    cp_async_wait<S - 2>();  // the first live iteration landed
     PointData pn;
     int32_t vn[MAXL];
-    auto prep = [&](int32_t kk, int stg) {
+    auto prep = [&](int32_t i, int stg) {
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) vn[l] = -1;
-      if (kk < npts) {
+      if (i != kNone && i * kThreads + tid < npts) {
         const float4 a = sbuf[warp][stg][0][lane];
         transform_point(sh, a, 1, r0, inv_r0, r0f, pn);
 #pragma unroll
@@ -527,27 +577,22 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
           vn[l] = lookup_dense_pred(sh.lv[l], pn.k0x >> l, pn.k0y >> l, pn.k0z >> l);
       }
     };
-    prep(tid, 0);
-    int st = 0, ph = 0;  // stage of iteration i + 1 below, and its mbarrier phase
-    for (int32_t i = 0; i * kThreads + 32 * warp < npts; ++i) {
-      if (GVOX_LIN_BULK) __syncwarp();  // all lanes done with the stage refilled below
-      issue(i + S - 1, st == 0 ? S - 1 : st - 1);
+    prep(i_cur, 0);
+    int st = 0;  // stage of the current live iteration
+    while (i_cur != kNone) {
+      issue_l(i_nx2, st == 0 ? S - 1 : st - 1);  // sequence slot j + 2
+      cp_async_wait<S - 2>();                    // slot j + 1 landed
       const int cur = st;
-      if (++st == S) {
-        st = 0;
-        ph ^= 1;
-      }
-      if (GVOX_LIN_BULK) {
-        if ((i + 1) * kThreads + 32 * warp < npts) mbar_wait(&mbar[warp][st], (unsigned)ph);
-      } else {
-        cp_async_wait<S - 2>();  // iteration i + 1 landed
-      }
-      const int32_t k = i * kThreads + tid;
+      if (++st == S) st = 0;
+      const int32_t k = i_cur * kThreads + tid;
       PointData pd = pn;
       int32_t vid[MAXL];
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) vid[l] = vn[l];
-      prep(k + kThreads, st);
+      prep(i_nxt, st);
+      i_cur = i_nxt;
+      i_nxt = i_nx2;
+      i_nx2 = i_nx2 == kNone ? kNone : next_live(i_nx2);
       bool any = false;
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) any |= vid[l] >= 0;

@@ -18,11 +18,11 @@ namespace gvox {
 namespace {
 
 constexpr int kThreads = 256;
-#ifndef GVOX_OVL_U
-#define GVOX_OVL_U 2
-#endif
 #ifndef GVOX_OVL_MINB
-#define GVOX_OVL_MINB 4
+#define GVOX_OVL_MINB 6
+#endif
+#ifndef GVOX_OVL_CULL
+#define GVOX_OVL_CULL 1
 #endif
 
 template <bool ALL_DENSE>
@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   __shared__ int warp_cnt[kThreads / 32];
   __shared__ float Rf[9], map_lo[4], map_hi[4];
   __shared__ const float* cbox_s;
+  __shared__ MapLevelDev cv_s;  // coarsest level (culling), valid if cv_dense
   const int tid = threadIdx.x;
   const int64_t tile = blockIdx.x;
   const int32_t p = __ldg(tile_pair + tile);
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
       map_lo[j] = md->box_lo[j];
       map_hi[j] = md->box_hi[j];
     }
+    cv_s = md->lv[md->levels - 1];
   }
   __syncthreads();
   if (tid == 0) {
@@ -75,39 +77,40 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   const float4* __restrict__ A = A_s;
   int cnt = 0;
   const int64_t kb = range_s[0], ke = range_s[1];
-  // U points per thread per iteration: their loads are in flight together
-  constexpr int U = GVOX_OVL_U;
-  // exact chunk culling: sub-iteration m = it * U + u of warp w covers tile
-  // chunk 8 m + w; m < tile_pts / 256 <= 32, so one ballot covers the tile
+  const int warp = tid >> 5, lane = tid & 31;
+  // Warp w owns tile chunks 8 m + w (32 consecutive points each), m < tile_pts /
+  // 256 <= 32.  Exact chunk culling (k_common.cuh): one ballot marks the chunks
+  // that cannot hit; the warp visits only the live ones, two at a time.
   const uint32_t cull =
-      cbox_s ? cull_ballot(cbox_s, (kb >> 5) + (tid >> 5), kThreads / 32, (ke + 31) >> 5, Rf, t,
-                           map_lo, map_hi)
-             : 0u;
-  int m = 0;
-  for (int64_t k0 = kb + tid; k0 < ke; k0 += U * kThreads, m += U) {
-    float4 a[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t k = k0 + u * kThreads;
-      if (k < ke && !((cull >> (m + u)) & 1u)) a[u] = __ldg(A + pt_off(k));
+      (GVOX_OVL_CULL && cbox_s)
+          ? cull_ballot(cbox_s, (kb >> 5) + warp, kThreads / 32, (ke + 31) >> 5, Rf, t, map_lo,
+                        map_hi, (cv_s.dense && cv_s.grid) ? &cv_s : nullptr)
+          : 0u;
+  const int nm = (int)((ke - kb + kThreads - 1) / kThreads);
+  uint32_t live = ~cull & (nm >= 32 ? 0xffffffffu : ((1u << nm) - 1u));
+  auto probe = [&](int m) -> int {
+    const int64_t k = kb + (int64_t)m * kThreads + 32 * warp + lane;
+    if (k >= ke) return 0;
+    const float4 a = __ldg(A + pt_off(k));
+    const double mx = a.x, my = a.y, mz = a.z;
+    const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
+    const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
+    const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
+    const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
+    const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
+    const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
+    return lookup_level<ALL_DENSE>(lv, kx, ky, kz) >= 0;
+  };
+  while (live) {
+    const int m0 = __ffs(live) - 1;
+    live &= live - 1;
+    if (live) {
+      const int m1 = __ffs(live) - 1;
+      live &= live - 1;
+      cnt += probe(m0) + probe(m1);
+    } else {
+      cnt += probe(m0);
     }
-    int32_t hit[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      hit[u] = -1;
-      if (k0 + u * kThreads < ke && !((cull >> (m + u)) & 1u)) {
-        const double mx = a[u].x, my = a[u].y, mz = a[u].z;
-        const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
-        const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
-        const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
-        const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
-        const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
-        const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
-        hit[u] = lookup_level<ALL_DENSE>(lv, kx, ky, kz);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) cnt += hit[u] >= 0;
   }
   // warp counts, then one atomic per CTA
 #pragma unroll
@@ -142,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   __shared__ int warp_cnt[2][kThreads / 32];
   __shared__ float Rf[9], map_lo[4], map_hi[4];
   __shared__ const float* cbox_s;
+  __shared__ MapLevelDev cv_s;  // coarsest level (culling), valid if cv_dense
   const int tid = threadIdx.x;
   const int32_t p = blockIdx.x;
   const PairDev pd = pairs[p];
@@ -160,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
       map_lo[j] = md->box_lo[j];
       map_hi[j] = md->box_hi[j];
     }
+    cv_s = md->lv[md->levels - 1];
   }
   __syncthreads();
   if (tid == 0) {
@@ -174,49 +179,62 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   const int64_t n = n_s;
   const float* cbox = cbox_s;
   const int64_t nchunks = (n + 31) >> 5;
-  uint32_t cull = 0;  // bits for sub-iterations m .. m + 31 (chunk 8 m + warp)
   // count * den > n * num  <=>  count >= need
   const int64_t need = (n * (int64_t)num) / den + 1;
-  constexpr int U = GVOX_OVL_U;
+  const int warp = tid >> 5, lane = tid & 31;
+  auto probe = [&](int64_t m) -> int {
+    const int64_t k = m * kThreads + 32 * warp + lane;
+    if (k >= n) return 0;
+    const float4 a = __ldg(A + pt_off(k));
+    const double mx = a.x, my = a.y, mz = a.z;
+    const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
+    const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
+    const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
+    const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
+    const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
+    const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
+    return lookup_level<ALL_DENSE>(lv, kx, ky, kz) >= 0;
+  };
+  // Windows of kWin sub-steps m (kThreads points each; warp w owns chunk 8 m + w):
+  // each warp probes its live (non-culled) chunks of the window without
+  // barriers, then one block reduction decides.  Culled chunks hold no hit.
+  constexpr int kWin = 8;
+  const int64_t msteps = (n + kThreads - 1) / kThreads;
   int64_t total = 0;
   int buf = 0;
   bool sel = false;
-  static_assert(32 % U == 0, "ballot refresh");
-  int m = 0;
-  for (int64_t k0 = 0; k0 < n; k0 += (int64_t)U * kThreads, m += U) {
-    if (cbox && (m & 31) == 0)  // uniform over the CTA: every warp refreshes
-      cull = cull_ballot(cbox, (int64_t)m * (kThreads / 32) + (tid >> 5), kThreads / 32, nchunks,
-                         Rf, t, map_lo, map_hi);
-    const uint32_t cm = cull >> (m & 31);
-    int cnt = 0;
-    float4 a[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t k = k0 + u * kThreads + tid;
-      if (k < n && !((cm >> u) & 1u)) a[u] = __ldg(A + pt_off(k));
+  uint32_t live = 0;  // bits for sub-steps mb .. mb + 31
+  for (int64_t mw = 0; mw < msteps; mw += kWin) {
+    if ((mw & 31) == 0) {
+      uint32_t cull = 0;
+      if (GVOX_OVL_CULL && cbox)
+        cull = cull_ballot(cbox, mw * (kThreads / 32) + warp, kThreads / 32, nchunks, Rf, t, map_lo,
+                           map_hi, (cv_s.dense && cv_s.grid) ? &cv_s : nullptr);
+      live = ~cull;
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (k0 + u * kThreads + tid < n && !((cm >> u) & 1u)) {
-        const double mx = a[u].x, my = a[u].y, mz = a[u].z;
-        const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
-        const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
-        const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
-        const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
-        const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
-        const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
-        cnt += lookup_level<ALL_DENSE>(lv, kx, ky, kz) >= 0;
+    uint32_t w = (live >> (mw & 31)) & ((1u << kWin) - 1u);
+    int cnt = 0;
+    while (w) {
+      const int j0 = __ffs(w) - 1;
+      w &= w - 1;
+      if (w) {
+        const int j1 = __ffs(w) - 1;
+        w &= w - 1;
+        cnt += probe(mw + j0) + probe(mw + j1);
+      } else {
+        cnt += probe(mw + j0);
       }
     }
     cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if ((tid & 31) == 0) warp_cnt[buf][tid >> 5] = cnt;
+    if (lane == 0) warp_cnt[buf][warp] = cnt;
     __syncthreads();
     int blk = 0;
 #pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) blk += warp_cnt[buf][w];
+    for (int q = 0; q < kThreads / 32; ++q) blk += warp_cnt[buf][q];
     buf ^= 1;  // double buffer: no second barrier needed before the next write
     total += blk;
-    const int64_t left = n - (k0 + (int64_t)U * kThreads);
+    const int64_t done = (mw + kWin) * kThreads;
+    const int64_t left = n - done;
     if (total >= need) {
       sel = true;
       break;

@@ -15,9 +15,7 @@ VARIANTS = {
     "base": [],
     "s3": ["GVOX_LIN_STAGES=3"],
     "nopipe": ["GVOX_LIN_PIPE=0"],
-    "pipe_s4": ["GVOX_LIN_STAGES=4"],
-    "pbulk3": ["GVOX_LIN_BULK=1"],
-    "pbulk4": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=4"],
+    "nocull": ["GVOX_LIN_CULL=0"],
     "bulk2": ["GVOX_LIN_BULK=1"],
     "bulk3": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=3"],
     "bulk4": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=4"],
@@ -27,10 +25,9 @@ VARIANTS = {
     "t128_b2": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=2"],
     "t256_b1": ["GVOX_LIN_THREADS=256", "GVOX_LIN_MINB=1"],
     # overlap kernel (stage times from a full bench run)
-    "ovl_u1_b8": ["GVOX_OVL_U=1", "GVOX_OVL_MINB=8"],
-    "ovl_u2_b6": ["GVOX_OVL_U=2", "GVOX_OVL_MINB=6"],
-    "ovl_u4_b4": ["GVOX_OVL_U=4", "GVOX_OVL_MINB=4"],
-    "ovl_u2_b4": ["GVOX_OVL_U=2", "GVOX_OVL_MINB=4"],
+    "ovl_base": [],
+    "ovl_b6": ["GVOX_OVL_MINB=6"],
+    "ovl_nocull": ["GVOX_OVL_CULL=0"],
 }
 
 
@@ -56,9 +53,10 @@ def run(names, extra, stage="linearize"):
                                capture_output=True, text=True)
             try:
                 d = json.loads(p.stdout.strip().splitlines()[-1])
-                res[n] = {k: round(v["ms_per_step"], 2) for k, v in d["stages"].items()}
+                res[n] = {k: round(v["ms_per_step"], 2) for k, v in d["stages"].items()
+                          if "ms_per_step" in v}
             except Exception:
-                res[n] = p.stderr[-500:]
+                res[n] = (p.stdout[-300:], p.stderr[-700:])
         else:
             try:
                 p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--linearize-only",
