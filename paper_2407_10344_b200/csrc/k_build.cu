@@ -110,16 +110,23 @@ __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restri
 
 // Grids are 2D: blockIdx.y = segment (cloud), blockIdx.x * blockDim.x +
 // threadIdx.x = point within it, so a block never straddles two maps.
-constexpr int kMaxL = GVOX_MAX_LEVELS;
+#ifndef GVOX_INS_MINB
+#define GVOX_INS_MINB 4
+#endif
+#ifndef GVOX_ACC_MINB
+#define GVOX_ACC_MINB 3
+#endif
 
-__global__ void k_build_insert(const BuildSeg* __restrict__ segs, int levels, double r0,
+template <int kMaxL>
+__global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const BuildSeg* __restrict__ segs, int levels, double r0,
                                double inv_r0, int dyadic, int32_t* __restrict__ pslot,
                                int32_t* __restrict__ err) {
   const int lane = threadIdx.x & 31;
   const BuildSeg& sg = segs[blockIdx.y];
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = k < sg.n;
-  if (__all_sync(0xffffffffu, !valid)) return;
+  // (block-uniform exit only: the index allocation below uses block barriers)
+  if ((int64_t)blockIdx.x * blockDim.x >= sg.n) return;
   int32_t k0x = 0, k0y = 0, k0z = 0;
   if (valid) {
     const float4 a = __ldg(sg.A + pt_off(k));
@@ -168,38 +175,58 @@ __global__ void k_build_insert(const BuildSeg* __restrict__ segs, int levels, do
       }
     }
   }
+  // probing (hash levels only), then the index allocation aggregated over the
+  // block: warp counts -> shared-memory offsets -> one global atomicAdd per
+  // block and level (the per-map counters are the contended addresses)
+  __shared__ int32_t blk_cnt[kMaxL], blk_base[kMaxL];
+  bool is_new[kMaxL];
+  int32_t h_out[kMaxL];
+  unsigned new_mask[kMaxL];
+  int32_t woff[kMaxL];
+  if (threadIdx.x < kMaxL) blk_cnt[threadIdx.x] = 0;
+  __syncthreads();
 #pragma unroll
   for (int l = 0; l < kMaxL; ++l) {
-    if (l >= levels) break;
-    bool is_new = false;
-    int32_t h_out = -1;
+    is_new[l] = false;
+    h_out[l] = -1;
+    new_mask[l] = 0;
+    woff[l] = 0;
+    if (l >= levels) continue;
     if (lead[l]) {
       while (prev[l] != kEmptyKey && prev[l] != key[l]) {
         h[l] = (h[l] + 1) & sg.tmp_mask;
         prev[l] = atomicCAS(reinterpret_cast<unsigned long long*>(&sg.tmp_slots[l][h[l]].x),
                             kEmptyKey, key[l]);
       }
-      is_new = prev[l] == kEmptyKey;
-      h_out = (int32_t)h[l];
+      is_new[l] = prev[l] == kEmptyKey;
+      h_out[l] = (int32_t)h[l];
     }
-    const unsigned new_mask = __ballot_sync(0xffffffffu, is_new);
-    if (new_mask) {
-      int32_t base = 0;
-      const int first = __ffs(new_mask) - 1;
-      if (lane == first) base = atomicAdd(sg.counter + l, __popc(new_mask));
-      base = __shfl_sync(0xffffffffu, base, first);
-      if (is_new) {
-        const int32_t idx = base + __popc(new_mask & ((1u << lane) - 1u));
+    new_mask[l] = __ballot_sync(0xffffffffu, is_new[l]);
+    if (new_mask[l] && lane == __ffs(new_mask[l]) - 1)
+      woff[l] = atomicAdd(&blk_cnt[l], __popc(new_mask[l]));
+  }
+  __syncthreads();
+  if (threadIdx.x < levels && blk_cnt[threadIdx.x] > 0)
+    blk_base[threadIdx.x] = atomicAdd(sg.counter + threadIdx.x, blk_cnt[threadIdx.x]);
+  __syncthreads();
+#pragma unroll
+  for (int l = 0; l < kMaxL; ++l) {
+    if (l >= levels) break;
+    if (new_mask[l]) {
+      const int32_t b =
+          blk_base[l] + __shfl_sync(0xffffffffu, woff[l], __ffs(new_mask[l]) - 1);
+      if (is_new[l]) {
+        const int32_t idx = b + __popc(new_mask[l] & ((1u << lane) - 1u));
         if (sg.box[l].dense)
-          sg.box[l].grid[h_out] = idx;
+          sg.box[l].grid[h_out[l]] = idx;
         else
-          sg.tmp_slots[l][h_out].y = (unsigned long long)(uint32_t)idx | 0xFFFFFFFF00000000ull;
+          sg.tmp_slots[l][h_out[l]].y = (unsigned long long)(uint32_t)idx | 0xFFFFFFFF00000000ull;
         sg.keys_by_idx[l][idx] = key[l];
       }
     }
-    h_out = __shfl_sync(0xffffffffu, h_out, leader[l]);
+    const int32_t hl = __shfl_sync(0xffffffffu, h_out[l], leader[l]);
     const bool inr = key[l] < (1ull << 63);
-    if (valid) pslot[sg.pl_offset + k * levels + l] = inr ? h_out : -1;
+    if (valid) pslot[sg.pl_offset + k * levels + l] = inr ? hl : -1;
   }
 }
 
@@ -207,7 +234,7 @@ __device__ inline unsigned long long to_fixed(double x) {
   return (unsigned long long)__double2ll_rn(x);
 }
 
-__global__ void k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg* __restrict__ segs,
+__global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildSeg* __restrict__ bsegs, const AccumSeg* __restrict__ segs,
                               int levels, double r0, double inv_r0, int dyadic,
                               const int32_t* __restrict__ pslot,
                               unsigned long long* __restrict__ acc) {
@@ -358,7 +385,11 @@ void launch_build_insert(const BuildSeg* segs_dev, int64_t num_segs, int64_t max
                          cudaStream_t stream) {
   if (num_segs <= 0 || max_seg_points <= 0) return;
   dim3 grid(grid_for(max_seg_points, 256), (unsigned)num_segs);
-  k_build_insert<<<grid, 256, 0, stream>>>(segs_dev, levels, r0, 1.0 / r0, dyadic, pslot, err);
+  if (levels <= 3)
+    k_build_insert<3><<<grid, 256, 0, stream>>>(segs_dev, levels, r0, 1.0 / r0, dyadic, pslot, err);
+  else
+    k_build_insert<GVOX_MAX_LEVELS><<<grid, 256, 0, stream>>>(segs_dev, levels, r0, 1.0 / r0,
+                                                              dyadic, pslot, err);
   note_launch();
 }
 
