@@ -116,6 +116,10 @@ __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restri
 #ifndef GVOX_ACC_MINB
 #define GVOX_ACC_MINB 3
 #endif
+// accumulation: segmented run sums when a warp has more than this many groups
+#ifndef GVOX_ACC_SEG_MIN
+#define GVOX_ACC_SEG_MIN 1
+#endif
 
 template <int kMaxL>
 __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const BuildSeg* __restrict__ segs, int levels, double r0,
@@ -289,6 +293,43 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
       hi_c[j] = (int)((long long)v[j] >> 24);
     }
     unsigned todo = __ballot_sync(0xffffffffu, sl >= 0);
+    // many groups (fine levels): segmented suffix sums over RUNS of equal index
+    // in lane order (shuffles; cost independent of the group count), one set
+    // of atomics per run head.  A voxel split over several runs gets several
+    // atomic contributions -- integer sums, so the result is the same.
+    const int ngroups = __popc(__ballot_sync(0xffffffffu, sl >= 0 && lane == __ffs(grp) - 1));
+    if (ngroups > GVOX_ACC_SEG_MIN) {
+      const int32_t idx_prev = __shfl_up_sync(0xffffffffu, idx, 1);
+      const bool head = lane == 0 || idx != idx_prev;
+      const unsigned H = __ballot_sync(0xffffffffu, head);
+      const unsigned after = lane == 31 ? 0u : (H & (0xffffffffu << (lane + 1)));
+      const int run_end = after ? __ffs(after) - 2 : 31;
+      int cnt = sl >= 0 ? 1 : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const bool take = lane + off <= run_end;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+          const unsigned ol = __shfl_down_sync(0xffffffffu, lo_c[j], off);
+          const int oh = __shfl_down_sync(0xffffffffu, hi_c[j], off);
+          if (take) {
+            lo_c[j] += ol;
+            hi_c[j] += oh;
+          }
+        }
+        const int oc = __shfl_down_sync(0xffffffffu, cnt, off);
+        if (take) cnt += oc;
+      }
+      if (head && sl >= 0) {
+        unsigned long long* dst = acc + (sg.acc_offset[l] + idx) * 10;
+#pragma unroll
+        for (int j = 0; j < 9; ++j)
+          atomicAdd(dst + j, (unsigned long long)((long long)hi_c[j] * (1ll << 24)) +
+                                 (unsigned long long)lo_c[j]);
+        atomicAdd(dst + 9, (unsigned long long)cnt);
+      }
+      continue;
+    }
     while (todo) {
       const int ld = __ffs(todo) - 1;
       const unsigned g = __shfl_sync(0xffffffffu, grp, ld);

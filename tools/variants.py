@@ -26,6 +26,9 @@ VARIANTS = {
     "t256_b1": ["GVOX_LIN_THREADS=256", "GVOX_LIN_MINB=1"],
     # overlap kernel (stage times from a full bench run)
     "ovl_base": [],
+    "acc_seg1": ["GVOX_ACC_SEG_MIN=1"],
+    "acc_seg6": ["GVOX_ACC_SEG_MIN=6"],
+    "acc_noseg": ["GVOX_ACC_SEG_MIN=99"],
     "ovl_b6": ["GVOX_OVL_MINB=6"],
     "ovl_nocull": ["GVOX_OVL_CULL=0"],
 }
@@ -47,7 +50,7 @@ def run(names, extra, stage="linearize"):
     res = {}
     for n in names:
         env = dict(os.environ, GVOX_LIB=os.path.join(OUT, f"libgvox_{n}.so"))
-        if n.startswith("ovl"):
+        if n.startswith("ovl") or n.startswith("acc"):
             p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--no-e2e",
                                 "--no-cpu-baseline", "--steps", "3", *extra], env=env,
                                capture_output=True, text=True)
