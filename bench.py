@@ -442,12 +442,26 @@ def main():
     lin_avg_s = (lin_ms / max(lin_n, 1)) / 1e3
     achieved = alg_bytes / lin_avg_s / 1e9 if lin_n else None
     traffic = None
+    inst_pf = None
     prof = os.path.join(ROOT, "profiles", "linearize_dram_bytes_per_pf.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof))["dram_bytes_per_point_factor"] * pf
+            pj = json.load(open(prof))
+            traffic = pj["dram_bytes_per_point_factor"] * pf
+            inst_pf = pj.get("warp_instructions_per_point_factor")
         except (ValueError, KeyError):
             traffic = None
+    # issue-slot view of the same kernel (it is instruction-issue bound): warp
+    # instructions per point-factor from the committed full-size ncu capture,
+    # against 4 schedulers x SMs x the SM clock sampled during the timed region
+    issue = None
+    if inst_pf and lin_n and clk and clk.get("sm_mhz"):
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_i = 4 * sms * clk["sm_mhz"] * 1e6
+        ach_i = inst_pf * pf / lin_avg_s
+        issue = {"unit": "warp-instructions/s", "achieved": ach_i, "peak": peak_i,
+                 "frac": ach_i / peak_i, "warp_instructions_per_point_factor": inst_pf,
+                 "source": "profiles/linearize_dram_bytes_per_pf.json (ncu smsp__inst_executed)"}
     stages = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for k, v in tm.items()}
     stages["host_wall_ms_per_step"] = {k: v / args.steps for k, v in host_ms.items()}
     dominant = max(tm, key=lambda k: tm[k][0])
@@ -560,7 +574,8 @@ def main():
                          "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes, "point_factors_per_launch": pf,
                          "avg_launch_ms": lin_avg_s * 1e3,
-                         "dominant_kernel_group": dominant},
+                         "dominant_kernel_group": dominant,
+                         "issue": issue},
             "e2e": e2e,
             "gpu_launches": launches_all,
             "clocks": clk,

@@ -67,8 +67,10 @@ def main(rep, out, pf=None):
             u = units[i]
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         b = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+        inst = val("smsp__inst_executed.sum")
         json.dump({"dram_bytes_per_point_factor": b / pf, "source": os.path.basename(rep),
-                   "point_factors": pf, "dram_bytes": b},
+                   "point_factors": pf, "dram_bytes": b,
+                   "warp_instructions_per_point_factor": inst / pf},
                   open(os.path.join(os.path.dirname(out), "linearize_dram_bytes_per_pf.json"), "w"),
                   indent=1)
 
