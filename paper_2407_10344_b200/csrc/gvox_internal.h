@@ -70,6 +70,16 @@ struct __align__(16) MapLevelDev {
   int32_t pad;
 };
 
+// linearize tile plan: tiles of 256 * ppt points of one factor, ppt = the
+// largest power of two <= GVOX_TILE_MAX_PPT with n >= 256 * MIN_TILES * ppt
+// (a function of the factor alone: batch == serial bit for bit)
+#ifndef GVOX_TILE_MAX_PPT
+#define GVOX_TILE_MAX_PPT 128
+#endif
+#ifndef GVOX_TILE_MIN_TILES
+#define GVOX_TILE_MIN_TILES 2
+#endif
+
 constexpr int kDenseBuildRatio = 48;  // max cells per POINT for a dense grid level
 
 struct MapDev {

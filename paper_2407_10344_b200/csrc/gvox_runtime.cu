@@ -1122,7 +1122,7 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
     // tile = 256 * ppt points, ppt = pow2 <= n / 2048 in [1, 64]: ~8-16 tiles per
     // factor; depends on the factor alone (bitwise batch/shard independence)
     int ppt = 1;
-    while (ppt < 64 && (int64_t)256 * 8 * (ppt * 2) <= n) ppt *= 2;
+    while (ppt < GVOX_TILE_MAX_PPT && (int64_t)256 * GVOX_TILE_MIN_TILES * (ppt * 2) <= n) ppt *= 2;
     const int tile_pts = 256 * ppt;
     const int64_t nt = (n + tile_pts - 1) / tile_pts;
     if ((int64_t)tstart[f] + nt > INT32_MAX)

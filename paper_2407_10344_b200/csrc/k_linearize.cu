@@ -522,13 +522,13 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     // occupied coarsest-level cell has no correspondence at any level.  The warp
     // walks only its LIVE iterations (identical results: culled points add
     // nothing), so culled chunks are neither copied nor touched.
-    constexpr int kWords = (64 * 256 / kThreads + 31) / 32;  // tiles <= 64 * 256 points
+    constexpr int kWords = (GVOX_TILE_MAX_PPT * 256 / kThreads + 31) / 32;  // bits per iteration
     constexpr int kNone = 1 << 30;
     __shared__ uint32_t live_s[kWarps][kWords];
     const int32_t iters = (npts - 32 * warp + kThreads - 1) / kThreads;
     const MapLevelDev& cv = sh.lv[MAXL - 1];
     const bool cull_on = GVOX_LIN_CULL && sh.cbox != nullptr && cv.grid != nullptr;
-#pragma unroll
+#pragma unroll 1
     for (int i0 = 0; i0 < kWords * 32; i0 += 32) {
       const int32_t i = i0 + lane;
       bool live = i < iters;

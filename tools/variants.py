@@ -16,6 +16,10 @@ VARIANTS = {
     "s3": ["GVOX_LIN_STAGES=3"],
     "nopipe": ["GVOX_LIN_PIPE=0"],
     "nocull": ["GVOX_LIN_CULL=0"],
+    "tile4": ["GVOX_TILE_MIN_TILES=4"],
+    "tile2": ["GVOX_TILE_MIN_TILES=2", "GVOX_TILE_MAX_PPT=128"],
+    "tile1": ["GVOX_TILE_MIN_TILES=1", "GVOX_TILE_MAX_PPT=256"],
+    "tile2_256": ["GVOX_TILE_MIN_TILES=2", "GVOX_TILE_MAX_PPT=256"],
     "bulk2": ["GVOX_LIN_BULK=1"],
     "bulk3": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=3"],
     "bulk4": ["GVOX_LIN_BULK=1", "GVOX_LIN_STAGES=4"],
