@@ -126,23 +126,18 @@ __device__ inline bool chunk_culled_grid(const float* box, const float* Rf, cons
     nc[a] = hi - lo + 1;
   }
   if (nc[0] > 3 || nc[1] > 3 || nc[2] > 3) return false;
-  // up to 3 x 3 x 3 cells, probed four at a time (loads in flight together)
-  const int total = nc[0] * nc[1] * nc[2], n12 = nc[1] * nc[2];
-  for (int t0 = 0; t0 < total; t0 += 4) {
-    int32_t v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int f = t0 + u;
-      v[u] = -1;
-      if (f < total) {
-        const int i = f / n12, r = f - i * n12, j = r / nc[2], k = r - j * nc[2];
-        v[u] = __ldg(cv.grid + ((uint32_t)(c0[0] + i) * cv.syz + (uint32_t)(c0[1] + j) * cv.dz +
-                                (uint32_t)(c0[2] + k)));
-      }
+  // up to 3 x 3 x 3 cells: one row of <= 3 cells along z per step, its loads
+  // in flight together
+  for (int i = 0; i < nc[0]; ++i)
+    for (int j = 0; j < nc[1]; ++j) {
+      const int32_t* row = cv.grid + ((uint32_t)(c0[0] + i) * cv.syz +
+                                      (uint32_t)(c0[1] + j) * cv.dz + (uint32_t)c0[2]);
+      const int32_t v0 = __ldg(row);
+      const int32_t v1 = nc[2] > 1 ? __ldg(row + 1) : -1;
+      const int32_t v2 = nc[2] > 2 ? __ldg(row + 2) : -1;
+      // all empty <=> each is -1 <=> their AND is -1 (an index >= 0 clears the sign bit)
+      if ((v0 & v1 & v2) != -1) return false;
     }
-    // all empty <=> every value is -1 <=> their AND is -1 (an index >= 0 clears the sign bit)
-    if ((v[0] & v[1] & v[2] & v[3]) != -1) return false;
-  }
   return true;
 }
 
