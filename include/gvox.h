@@ -135,7 +135,8 @@ enum {
   GVOX_TIMER_OVERLAP = 1,   /* overlap kernel */
   GVOX_TIMER_LINEARIZE = 2, /* fused correspondence + linearization kernel */
   GVOX_TIMER_REDUCE = 3,    /* per-factor reduction / expansion kernel */
-  GVOX_TIMER_COUNT = 4
+  GVOX_TIMER_REGISTER = 4,  /* one gvox_register_batch graph launch (all iterations) */
+  GVOX_TIMER_COUNT = 5
 };
 gvox_status gvox_ctx_enable_timing(gvox_ctx* ctx, int enable);
 gvox_status gvox_ctx_timing(gvox_ctx* ctx, double* ms, int64_t* launches, int reset);
@@ -259,6 +260,68 @@ gvox_status gvox_linearize_batch_accum(gvox_ctx* ctx, const gvox_cloud* const* c
 gvox_status gvox_expand(gvox_ctx* ctx, const gvox_factor* factors, int64_t num_factors,
                         const double* poses, int64_t num_poses, const gvox_factor_accum* accum,
                         gvox_linear_factor* out, int mem);
+
+/* ------------------------------------------------------ on-device registration */
+
+/* Iterated re-linearization with a pose update on the device, no host round
+   trip between iterations (the paper re-evaluates every
+   matching cost factor in each optimization iteration, with Omega fixed
+   at the linearization point).
+
+   Every factor's pose_i is a VARIABLE pose; every pose_j is FIXED.  A pose may
+   not be both (that couples poses into a joint system: GVOX_ERR_INVALID), and
+   pose_i != pose_j.  The variable poses are therefore independent problems,
+   solved together in one batch.  For a variable pose v, iteration k:
+     1. linearize all factors with pose_i = v at (T_v^k, T_j) (Eqs. 2-8);
+     2. H = sum_f H_ii(f), b = sum_f b_i(f), e_k = sum_f error(f), summed in
+        ascending factor order;
+     3. solve (H + lambda I) delta = -b by Cholesky (fp64); if the matrix is not
+        positive definite the pose stops with GVOX_REG_SINGULAR, unchanged;
+     4. T_v^(k+1) = T_v^k Exp(delta) (right perturbation, rotation-first
+        delta = [w; rho], full SE(3) exponential);
+     5. stop with GVOX_REG_CONVERGED when |w| <= eps_rot and |rho| <= eps_trans,
+        or with GVOX_REG_MAX_ITER after max_iterations linearizations.
+   The returned pose is the one after the last step, error_final the error at
+   the last linearization.  One loop iteration = linearize + per-factor reduce
+   + solve/update kernels, run as the body of a CUDA graph WHILE node whose
+   condition the solve kernel sets (any pose still active): one graph launch
+   per call, one H2D and (host outputs) one D2H.
+   Converged poses stay frozen while others iterate. */
+typedef struct gvox_register_params {
+  int32_t max_iterations; /* linearizations per variable pose, in [1, 1000] */
+  int32_t reserved;       /* 0 */
+  double lambda;          /* >= 0; 0 = Gauss-Newton */
+  double eps_rot;         /* >= 0 [rad] */
+  double eps_trans;       /* >= 0 [m] */
+} gvox_register_params;
+
+enum {
+  GVOX_REG_FIXED = 0,     /* not a variable pose (no factor has it as pose_i) */
+  GVOX_REG_MAX_ITER = 1,
+  GVOX_REG_CONVERGED = 2,
+  GVOX_REG_SINGULAR = 3
+};
+
+typedef struct gvox_register_result {
+  int32_t status;        /* GVOX_REG_* */
+  int32_t iterations;    /* linearizations performed */
+  int32_t inliers;       /* correspondences (all factors, all levels) at the last linearization */
+  int32_t reserved;
+  double error_initial;  /* e at the first linearization */
+  double error_final;    /* e at the last linearization */
+  double last_step[6];   /* the last delta applied (zeros when singular) */
+} gvox_register_result;
+
+/* factors, poses, params: host.  poses_out [num_poses x 12] (fixed poses copied
+   unchanged), results [num_poses] (indexed by pose) and error_history
+   (optional, [max_iterations x num_poses], e_k of pose v at [k * num_poses + v],
+   0 after the pose stopped) live in `mem`. */
+gvox_status gvox_register_batch(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                int64_t num_clouds, const gvox_map* const* maps, int64_t num_maps,
+                                const gvox_factor* factors, int64_t num_factors,
+                                const double* poses, int64_t num_poses,
+                                const gvox_register_params* params, double* poses_out,
+                                gvox_register_result* results, double* error_history, int mem);
 
 /* ------------------------------------------------------------- utilities */
 

@@ -6,20 +6,22 @@ Importing this package loads libgvox.so and raises if it is missing; there is
 no CPU fallback.
 """
 from ._lib import (FACTOR_ACCUM_DTYPE, FACTOR_DTYPE, F_ERROR_ONLY, F_VALIDATE_SURFACE,
-                   GVOX_DEVICE, GVOX_HOST, LINEAR_FACTOR_DTYPE, MAX_LEVELS, PAIR_DTYPE, GvoxError,
-                   launch_count, lib, version)
+                   GVOX_DEVICE, GVOX_HOST, LINEAR_FACTOR_DTYPE, MAX_LEVELS, PAIR_DTYPE,
+                   REG_CONVERGED, REG_FIXED, REG_MAX_ITER, REG_SINGULAR, REGISTER_PARAMS_DTYPE,
+                   REGISTER_RESULT_DTYPE, GvoxError, launch_count, lib, version)
 from .api import (Cloud, Context, HandleArray, VoxelMap, as_factors, as_pairs, as_poses,
                   corr_dump_size, create_clouds, create_voxelmap, create_voxelmaps, device_records, expand,
                   full_blocks, linearize_batch, linearize_batch_accum, overlap, overlap_select,
-                  records_to_numpy)
+                  records_to_numpy, register_batch)
 
 lib()  # fail loudly at import if the CUDA library is absent
 
 __all__ = [
     "Cloud", "Context", "VoxelMap", "HandleArray", "create_clouds", "create_voxelmap", "create_voxelmaps",
     "overlap", "overlap_select", "linearize_batch", "linearize_batch_accum", "expand", "device_records",
-    "records_to_numpy", "full_blocks", "corr_dump_size", "as_factors", "as_pairs", "as_poses",
+    "records_to_numpy", "register_batch", "full_blocks", "corr_dump_size", "as_factors", "as_pairs", "as_poses",
     "FACTOR_DTYPE", "PAIR_DTYPE", "LINEAR_FACTOR_DTYPE", "FACTOR_ACCUM_DTYPE", "MAX_LEVELS",
     "F_VALIDATE_SURFACE", "F_ERROR_ONLY", "GVOX_HOST", "GVOX_DEVICE", "GvoxError",
-    "launch_count", "version", "lib",
+    "launch_count", "version", "lib", "REG_FIXED", "REG_MAX_ITER", "REG_CONVERGED", "REG_SINGULAR",
+    "REGISTER_PARAMS_DTYPE", "REGISTER_RESULT_DTYPE",
 ]

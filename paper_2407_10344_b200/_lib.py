@@ -17,7 +17,7 @@ GVOX_HOST = 0
 GVOX_DEVICE = 1
 F_VALIDATE_SURFACE = 1
 F_ERROR_ONLY = 2
-TIMERS = ("build", "overlap", "linearize", "reduce")
+TIMERS = ("build", "overlap", "linearize", "reduce", "register")
 
 STATUS = {0: "GVOX_OK", 1: "GVOX_ERR_INVALID", 2: "GVOX_ERR_RANGE", 3: "GVOX_ERR_CUDA",
           4: "GVOX_ERR_NOMEM"}
@@ -34,6 +34,12 @@ LINEAR_FACTOR_DTYPE = np.dtype([("H_ii", "<f8", (36,)), ("H_ij", "<f8", (36,)),
 FACTOR_ACCUM_DTYPE = np.dtype([("terms", "<f8", (28,)), ("inliers", "<i4", (MAX_LEVELS,)),
                                ("num_invisible", "<i4"), ("num_degenerate", "<i4"),
                                ("reserved", "<i4", (6,))])
+REGISTER_PARAMS_DTYPE = np.dtype([("max_iterations", "<i4"), ("reserved", "<i4"), ("lambda", "<f8"),
+                                  ("eps_rot", "<f8"), ("eps_trans", "<f8")])
+REGISTER_RESULT_DTYPE = np.dtype([("status", "<i4"), ("iterations", "<i4"), ("inliers", "<i4"),
+                                  ("reserved", "<i4"), ("error_initial", "<f8"),
+                                  ("error_final", "<f8"), ("last_step", "<f8", (6,))])
+REG_FIXED, REG_MAX_ITER, REG_CONVERGED, REG_SINGULAR = 0, 1, 2, 3
 
 # exported symbols (tests check every one declared in include/gvox.h is here)
 SYMBOLS = [
@@ -43,6 +49,7 @@ SYMBOLS = [
     "gvox_create_voxelmap", "gvox_create_voxelmaps", "gvox_voxelmap_info", "gvox_voxelmap_levels",
     "gvox_voxelmap_export", "gvox_voxelmap_lookup", "gvox_map_destroy",
     "gvox_overlap", "gvox_overlap_select", "gvox_linearize_batch", "gvox_linearize_batch_accum", "gvox_expand",
+    "gvox_register_batch",
     "gvox_status_string", "gvox_last_error", "gvox_launch_count", "gvox_version",
 ]
 
@@ -88,6 +95,7 @@ def lib():
         "gvox_linearize_batch": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32, P]),
         "gvox_linearize_batch_accum": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32]),
         "gvox_expand": (I32, [P, P, I64, P, I64, P, P, I32]),
+        "gvox_register_batch": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, P, P, P, I32]),
         "gvox_status_string": (ctypes.c_char_p, [I32]),
         "gvox_last_error": (ctypes.c_char_p, []),
         "gvox_launch_count": (I64, [I32]),

@@ -14,7 +14,7 @@ from typing import Sequence
 import numpy as np
 
 from ._lib import (FACTOR_ACCUM_DTYPE, FACTOR_DTYPE, GVOX_DEVICE, GVOX_HOST, LINEAR_FACTOR_DTYPE,
-                   PAIR_DTYPE, check, lib)
+                   PAIR_DTYPE, REGISTER_PARAMS_DTYPE, REGISTER_RESULT_DTYPE, check, lib)
 
 
 def _torch():
@@ -336,6 +336,39 @@ def expand(ctx: Context, factors, poses, accum, out=None):
     check(lib().gvox_expand(ctx.handle, _ptr(factors)[0], F, _ptr(poses)[0], poses.shape[0],
                             ctypes.c_void_p(accum.data_ptr()), po, mem))
     return out
+
+
+def register_batch(ctx: Context, clouds, maps, factors, poses, max_iterations: int = 10,
+                   lam: float = 0.0, eps_rot: float = 1e-6, eps_trans: float = 1e-6,
+                   history: bool = False, device: bool = False):
+    """gvox_register_batch: on-device Gauss-Newton over every factor's pose_i
+    (variable) with pose_j fixed.  Returns (poses_out [P,12] f64, results
+    [P] REGISTER_RESULT_DTYPE, history [max_iterations, P] f64 or None); with
+    device=True the three are CUDA tensors (results as uint8 [P, 80])."""
+    C, M = _handles(clouds), _handles(maps)
+    factors = as_factors(factors)
+    poses = as_poses(poses)
+    NPz = poses.shape[0]
+    prm = np.zeros(1, REGISTER_PARAMS_DTYPE)
+    prm["max_iterations"], prm["lambda"] = int(max_iterations), float(lam)
+    prm["eps_rot"], prm["eps_trans"] = float(eps_rot), float(eps_trans)
+    if device:
+        torch = _torch()
+        dev = ctx.device
+        pout = torch.empty((NPz, 12), dtype=torch.float64, device=dev)
+        res = torch.empty((NPz, REGISTER_RESULT_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+        hist = torch.empty((max_iterations, NPz), dtype=torch.float64, device=dev) if history else None
+        mem = GVOX_DEVICE
+    else:
+        pout = np.zeros((NPz, 12), np.float64)
+        res = np.zeros(NPz, REGISTER_RESULT_DTYPE)
+        hist = np.zeros((max_iterations, NPz), np.float64) if history else None
+        mem = GVOX_HOST
+    check(lib().gvox_register_batch(ctx.handle, C.arr, C.n, M.arr, M.n, _ptr(factors)[0],
+                                    factors.shape[0], _ptr(poses)[0], NPz, _ptr(prm)[0],
+                                    _ptr(pout)[0], _ptr(res)[0],
+                                    None if hist is None else _ptr(hist)[0], mem))
+    return pout, res, hist
 
 
 def corr_dump_size(clouds: Sequence[Cloud], maps: Sequence[VoxelMap], factors) -> int:

@@ -254,6 +254,24 @@ void launch_reduce(const FactorDev* factors, const int32_t* tile_start, int64_t 
 void launch_expand(const FactorDev* factors, int64_t num_factors, const double* poses,
                    const gvox_factor_accum* accum, gvox_linear_factor* out, cudaStream_t stream);
 
+// on-device registration (gvox_register_batch): one problem per variable pose,
+// its factors at reg_factors[f0, f1) in ascending factor order.
+struct RegProblem {
+  int32_t pose, f0, f1, pad;
+};
+struct RegControl {
+  int32_t iter;          // loop iterations completed
+  int32_t max_iter;
+  int32_t any_active;    // per-iteration count (reset by the last block)
+  uint32_t blocks_done;  // per-iteration block ticket (reset by the last block)
+  double lambda, eps_rot, eps_trans;
+};
+void launch_gn_step(const RegProblem* problems, int32_t num_problems, const int32_t* reg_factors,
+                    const FactorDev* factors, const gvox_factor_accum* accum, double* poses,
+                    gvox_register_result* results, int32_t* active, RegControl* ctrl,
+                    double* history, int64_t num_poses, cudaGraphConditionalHandle cond,
+                    cudaStream_t stream);
+
 // tile -> owning item (factor or pair) table from the tile prefix sums
 void launch_tile_map(const int32_t* tile_start, int64_t num_items, int32_t* tile_owner,
                      cudaStream_t stream);

@@ -161,6 +161,10 @@ struct gvox_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_open[GVOX_TIMER_COUNT];
   double timer_ms[GVOX_TIMER_COUNT] = {};
   int64_t timer_launches[GVOX_TIMER_COUNT] = {};
+  // gvox_register_batch: capture stream for the loop graph, pinned D2H staging
+  cudaStream_t cap_stream = nullptr;
+  void* pin_out = nullptr;
+  size_t pin_out_bytes = 0;
 };
 
 struct gvox_cloud {
@@ -316,6 +320,8 @@ void gvox_ctx_destroy(gvox_ctx* ctx) {
     if (ctx->ws[i]) cudaFreeAsync(ctx->ws[i], ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->pin) cudaFreeHost(ctx->pin);
+  if (ctx->pin_out) cudaFreeHost(ctx->pin_out);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->pin_done) cudaEventDestroy(ctx->pin_done);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (int t = 0; t < GVOX_TIMER_COUNT; ++t)
@@ -1083,6 +1089,52 @@ gvox_status validate_factors(const char* fn, const gvox_cloud* const* clouds, in
   return GVOX_OK;
 }
 
+// Tile plan of a linearization batch: tiles of tile_pts consecutive points of
+// one factor; tile_pts = 256 * ppt, ppt = pow2 <= n / 2048 in [1, 128] (a
+// function of the factor alone: bitwise batch/shard independence).
+struct LinPlan {
+  std::vector<int32_t> tstart;
+  std::vector<FactorDev> fdev;
+  int max_levels = 1;
+  bool all_dense = true;
+  bool fast = true;  // the specialised kernel: exactly 3 dyadic dense levels, no visibility test
+};
+
+gvox_status plan_linearize(const char* fn, const gvox_cloud* const* clouds,
+                           const gvox_map* const* maps, const gvox_factor* factors,
+                           int64_t num_factors, bool fast_allowed, LinPlan* p,
+                           int min_tiles = GVOX_TILE_MIN_TILES) {
+  p->fast = fast_allowed;
+  p->tstart.assign(num_factors + 1, 0);
+  p->fdev.resize(num_factors);
+  int64_t corr_off = 0;
+  for (int64_t f = 0; f < num_factors; ++f) {
+    const gvox_factor& q = factors[f];
+    const gvox_map* m = maps[q.target_map];
+    p->max_levels = std::max(p->max_levels, m->levels);
+    for (int l = 0; l < m->levels; ++l) p->all_dense = p->all_dense && m->desc.lv[l].dense;
+    p->fast = p->fast && m->levels == 3 && m->desc.dyadic && !(q.flags & GVOX_F_VALIDATE_SURFACE);
+    const int64_t n = clouds[q.source_cloud]->n;
+    int ppt = 1;
+    while (ppt < GVOX_TILE_MAX_PPT && (int64_t)256 * min_tiles * (ppt * 2) <= n) ppt *= 2;
+    const int tile_pts = 256 * ppt;
+    const int64_t nt = (n + tile_pts - 1) / tile_pts;
+    if ((int64_t)p->tstart[f] + nt > INT32_MAX)
+      return fail(GVOX_ERR_INVALID, "%s: batch too large (more than 2^31 tiles)", fn);
+    p->tstart[f + 1] = p->tstart[f] + (int32_t)nt;
+    FactorDev& d = p->fdev[f];
+    d.src = q.source_cloud;
+    d.tgt = q.target_map;
+    d.pi = q.pose_i;
+    d.pj = q.pose_j;
+    d.flags = q.flags;
+    d.tile_pts = tile_pts;
+    d.corr_offset = corr_off;
+    corr_off += n * m->levels;
+  }
+  return GVOX_OK;
+}
+
 gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t num_clouds,
                            const gvox_map* const* maps, int64_t num_maps,
                            const gvox_factor* factors, int64_t num_factors, const double* poses,
@@ -1100,44 +1152,14 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
                                     poses, num_poses);
   if (st) return st;
   DeviceGuard g(ctx->device);
-  // ---- tile plan: tiles of tile_pts consecutive points of one factor
-  int64_t total_pf = 0;
-  int max_levels = 1;
-  bool all_dense = true;
-  bool fast = corr_dump == nullptr && std::getenv("GVOX_LIN_GENERIC") == nullptr;
-  for (int64_t f = 0; f < num_factors; ++f) {
-    total_pf += clouds[factors[f].source_cloud]->n;
-    const gvox_map* m = maps[factors[f].target_map];
-    max_levels = std::max(max_levels, m->levels);
-    for (int l = 0; l < m->levels; ++l) all_dense = all_dense && m->desc.lv[l].dense;
-    // the specialised kernel: exactly 3 dyadic levels, no visibility test
-    fast = fast && m->levels == 3 && m->desc.dyadic && !(factors[f].flags & GVOX_F_VALIDATE_SURFACE);
-  }
-  std::vector<int32_t> tstart(num_factors + 1, 0);
-  std::vector<FactorDev> fdev(num_factors);
-  int64_t corr_off = 0;
-  for (int64_t f = 0; f < num_factors; ++f) {
-    const gvox_factor& q = factors[f];
-    const int64_t n = clouds[q.source_cloud]->n;
-    // tile = 256 * ppt points, ppt = pow2 <= n / 2048 in [1, 64]: ~8-16 tiles per
-    // factor; depends on the factor alone (bitwise batch/shard independence)
-    int ppt = 1;
-    while (ppt < GVOX_TILE_MAX_PPT && (int64_t)256 * GVOX_TILE_MIN_TILES * (ppt * 2) <= n) ppt *= 2;
-    const int tile_pts = 256 * ppt;
-    const int64_t nt = (n + tile_pts - 1) / tile_pts;
-    if ((int64_t)tstart[f] + nt > INT32_MAX)
-      return fail(GVOX_ERR_INVALID, "%s: batch too large (more than 2^31 tiles)", fn);
-    tstart[f + 1] = tstart[f] + (int32_t)nt;
-    FactorDev& d = fdev[f];
-    d.src = q.source_cloud;
-    d.tgt = q.target_map;
-    d.pi = q.pose_i;
-    d.pj = q.pose_j;
-    d.flags = q.flags;
-    d.tile_pts = tile_pts;
-    d.corr_offset = corr_off;
-    corr_off += n * maps[q.target_map]->levels;
-  }
+  LinPlan plan;
+  st = plan_linearize(fn, clouds, maps, factors, num_factors,
+                      corr_dump == nullptr && std::getenv("GVOX_LIN_GENERIC") == nullptr, &plan);
+  if (st) return st;
+  const std::vector<int32_t>& tstart = plan.tstart;
+  const std::vector<FactorDev>& fdev = plan.fdev;
+  const int max_levels = plan.max_levels;
+  const bool all_dense = plan.all_dense, fast = plan.fast;
   const int64_t T = tstart[num_factors];
   // ---- the single serialized input block
   Layout lay;
@@ -1260,6 +1282,202 @@ gvox_status gvox_expand(gvox_ctx* ctx, const gvox_factor* factors, int64_t num_f
                        cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   }
+  return GVOX_OK;
+}
+
+// ------------------------------------------------------------ registration
+namespace {
+constexpr int kRegMinTiles = 32;
+}
+gvox_status gvox_register_batch(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                int64_t num_clouds, const gvox_map* const* maps, int64_t num_maps,
+                                const gvox_factor* factors, int64_t num_factors,
+                                const double* poses, int64_t num_poses,
+                                const gvox_register_params* params, double* poses_out,
+                                gvox_register_result* results, double* error_history, int mem) {
+  const char* fn = "gvox_register_batch";
+  if (!ctx) return fail(GVOX_ERR_INVALID, "%s: ctx is NULL", fn);
+  if (num_factors < 0 || num_poses < 0) return fail(GVOX_ERR_INVALID, "%s: negative size", fn);
+  if (!params || !poses_out || !results || (num_factors > 0 && (!clouds || !maps || !factors || !poses)))
+    return fail(GVOX_ERR_INVALID, "%s: NULL argument", fn);
+  if (mem != GVOX_HOST && mem != GVOX_DEVICE)
+    return fail(GVOX_ERR_INVALID, "%s: mem must be GVOX_HOST or GVOX_DEVICE", fn);
+  const gvox_register_params P = *params;
+  if (P.max_iterations < 1 || P.max_iterations > 1000)
+    return fail(GVOX_ERR_INVALID, "%s: max_iterations %d outside [1, 1000]", fn, P.max_iterations);
+  if (!(P.lambda >= 0.0) || !std::isfinite(P.lambda) || !(P.eps_rot >= 0.0) ||
+      !(P.eps_trans >= 0.0) || std::isnan(P.eps_rot) || std::isnan(P.eps_trans))
+    return fail(GVOX_ERR_INVALID, "%s: lambda, eps_rot, eps_trans must be >= 0 (lambda finite)", fn);
+  gvox_status st = validate_factors(fn, clouds, num_clouds, maps, num_maps, factors, num_factors,
+                                    poses, num_poses);
+  if (st) return st;
+  // ---- problems: one per variable pose (a factor's pose_i), ascending pose
+  std::vector<int32_t> nf(num_poses, 0);
+  for (int64_t f = 0; f < num_factors; ++f) {
+    if (factors[f].flags & GVOX_F_ERROR_ONLY)
+      return fail(GVOX_ERR_INVALID, "%s: factor %lld has GVOX_F_ERROR_ONLY (the solve needs H, b)",
+                  fn, (long long)f);
+    if (factors[f].pose_i == factors[f].pose_j)
+      return fail(GVOX_ERR_INVALID, "%s: factor %lld has pose_i == pose_j", fn, (long long)f);
+    ++nf[factors[f].pose_i];
+  }
+  for (int64_t f = 0; f < num_factors; ++f)
+    if (nf[factors[f].pose_j])
+      return fail(GVOX_ERR_INVALID,
+                  "%s: factor %lld: pose_j %d is the variable pose of another factor (joint "
+                  "multi-pose systems are not supported)", fn, (long long)f, factors[f].pose_j);
+  std::vector<RegProblem> probs;
+  std::vector<int32_t> pstart(num_poses + 1, 0);
+  for (int64_t v = 0; v < num_poses; ++v) pstart[v + 1] = pstart[v] + nf[v];
+  std::vector<int32_t> reg_f(std::max<int64_t>(num_factors, 1));
+  {
+    std::vector<int32_t> fill(pstart.begin(), pstart.end() - 1);
+    for (int64_t f = 0; f < num_factors; ++f) reg_f[fill[factors[f].pose_i]++] = (int32_t)f;
+  }
+  for (int64_t v = 0; v < num_poses; ++v)
+    if (nf[v]) probs.push_back(RegProblem{(int32_t)v, pstart[v], pstart[v + 1], 0});
+  const int64_t NP = (int64_t)probs.size();
+  DeviceGuard g(ctx->device);
+  LinPlan plan;
+  if (num_factors > 0) {
+    // registration batches are small (one odometry step: ~10 factors): tiles
+    // of >= 32 per factor keep every SM busy in the latency-bound loop
+    st = plan_linearize(fn, clouds, maps, factors, num_factors,
+                        std::getenv("GVOX_LIN_GENERIC") == nullptr, &plan, kRegMinTiles);
+    if (st) return st;
+  }
+  const int64_t T = num_factors > 0 ? plan.tstart[num_factors] : 0;
+  // ---- initial state
+  std::vector<gvox_register_result> res0(std::max<int64_t>(num_poses, 1));
+  std::memset(res0.data(), 0, sizeof(gvox_register_result) * res0.size());
+  for (const RegProblem& q : probs) res0[q.pose].status = GVOX_REG_MAX_ITER;
+  RegControl c0{};
+  c0.iter = 0;
+  c0.max_iter = P.max_iterations;
+  c0.lambda = P.lambda;
+  c0.eps_rot = P.eps_rot;
+  c0.eps_trans = P.eps_trans;
+  const int64_t HN = error_history ? (int64_t)P.max_iterations * num_poses : 0;
+  // ---- one serialized input block; the OUTPUT regions (poses, results,
+  // history) are contiguous at its start so a host D2H is one copy
+  Layout lay;
+  size_t o_pose = lay.add(96 * num_poses);
+  size_t o_res = lay.add(sizeof(gvox_register_result) * num_poses);
+  size_t o_hist = lay.add(8 * HN);
+  const size_t out_bytes = lay.size;
+  size_t o_ctrl = lay.add(sizeof(RegControl));
+  size_t o_act = lay.add(4 * std::max<int64_t>(NP, 1));
+  size_t o_prob = lay.add(sizeof(RegProblem) * std::max<int64_t>(NP, 1));
+  size_t o_rf = lay.add(4 * reg_f.size());
+  size_t o_fac = lay.add(sizeof(FactorDev) * num_factors);
+  size_t o_ts = lay.add(4 * (num_factors + 1));
+  size_t o_cl = lay.add(8 * num_clouds);
+  size_t o_mp = lay.add(8 * num_maps);
+  const size_t in_bytes = lay.size;
+  void* pin = nullptr;
+  st = pin_reserve(ctx, in_bytes, &pin);
+  if (st) return st;
+  char* hp = (char*)pin;
+  std::memset(hp, 0, in_bytes);
+  if (num_poses) std::memcpy(hp + o_pose, poses, 96 * num_poses);
+  if (num_poses) std::memcpy(hp + o_res, res0.data(), sizeof(gvox_register_result) * num_poses);
+  std::memcpy(hp + o_ctrl, &c0, sizeof(c0));
+  for (int64_t k = 0; k < NP; ++k) ((int32_t*)(hp + o_act))[k] = 1;
+  if (NP) std::memcpy(hp + o_prob, probs.data(), sizeof(RegProblem) * NP);
+  std::memcpy(hp + o_rf, reg_f.data(), 4 * reg_f.size());
+  if (num_factors) {
+    std::memcpy(hp + o_fac, plan.fdev.data(), sizeof(FactorDev) * num_factors);
+    std::memcpy(hp + o_ts, plan.tstart.data(), 4 * (num_factors + 1));
+  }
+  for (int64_t i = 0; i < num_clouds; ++i) ((const CloudDev**)(hp + o_cl))[i] = clouds[i] ? clouds[i]->dev : nullptr;
+  for (int64_t i = 0; i < num_maps; ++i) ((const MapDev**)(hp + o_mp))[i] = maps[i] ? maps[i]->dev : nullptr;
+  Layout wl;
+  size_t o_in = wl.add(in_bytes);
+  size_t o_part = wl.add(8 * kPartialStride * (size_t)std::max<int64_t>(T, 1));
+  size_t o_tf = wl.add(4 * (size_t)std::max<int64_t>(T, 1));
+  size_t o_acc = wl.add(sizeof(gvox_factor_accum) * std::max<int64_t>(num_factors, 1));
+  void* ws = nullptr;
+  st = ws_reserve(ctx, 0, wl.size, &ws);
+  if (st) return st;
+  char* wb = (char*)ws;
+  char* din = wb + o_in;
+  st = h2d_block(ctx, din, hp, in_bytes);
+  if (st) return st;
+  if (NP > 0) {
+    launch_tile_map((const int32_t*)(din + o_ts), num_factors, (int32_t*)(wb + o_tf), ctx->stream);
+    CK_LAUNCH("register tile map");
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    // ---- the loop: a WHILE node whose body is linearize -> reduce -> solve
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CK(cudaGraphCreate(&graph, 0));
+    std::unique_ptr<CUgraph_st, void (*)(cudaGraph_t)> graph_guard(graph, [](cudaGraph_t gr) { cudaGraphDestroy(gr); });
+    cudaGraphConditionalHandle cond;
+    CK(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(ctx->cap_stream, body, nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
+                     (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
+                     0, plan.max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
+                     (int32_t*)(wb + o_tf), nullptr, plan.all_dense, plan.fast, ctx->cap_stream);
+    launch_reduce((const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors,
+                  (const double*)(din + o_pose), (const double*)(wb + o_part), nullptr,
+                  (gvox_factor_accum*)(wb + o_acc), ctx->cap_stream);
+    launch_gn_step((const RegProblem*)(din + o_prob), (int32_t)NP, (const int32_t*)(din + o_rf),
+                   (const FactorDev*)(din + o_fac), (const gvox_factor_accum*)(wb + o_acc),
+                   (double*)(din + o_pose), (gvox_register_result*)(din + o_res),
+                   (int32_t*)(din + o_act), (RegControl*)(din + o_ctrl),
+                   HN ? (double*)(din + o_hist) : nullptr, num_poses, cond, ctx->cap_stream);
+    cudaGraph_t captured = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &captured);
+    if (ce != cudaSuccess) return cuda_fail(ce, "register loop capture");
+    CK_LAUNCH("register loop capture");
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    {
+      TimerScope ts(ctx, GVOX_TIMER_REGISTER);
+      cudaError_t le = cudaGraphLaunch(exec, ctx->stream);
+      if (le != cudaSuccess) {
+        cudaGraphExecDestroy(exec);
+        return cuda_fail(le, "register loop launch");
+      }
+    }
+    note_launch();
+    CK(cudaGraphExecDestroy(exec));  // freed asynchronously once the launch completes
+  }
+  // ---- outputs
+  if (mem == GVOX_DEVICE) {
+    if (num_poses) {
+      CK(cudaMemcpyAsync(poses_out, din + o_pose, 96 * num_poses, cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(results, din + o_res, sizeof(gvox_register_result) * num_poses,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (HN) CK(cudaMemcpyAsync(error_history, din + o_hist, 8 * HN, cudaMemcpyDeviceToDevice, ctx->stream));
+    return GVOX_OK;
+  }
+  if (ctx->pin_out_bytes < out_bytes) {
+    if (ctx->pin_out) CK(cudaFreeHost(ctx->pin_out));
+    ctx->pin_out = nullptr;
+    size_t nb = align_up(std::max(out_bytes, ctx->pin_out_bytes * 3 / 2), 1 << 16);
+    cudaError_t e = cudaHostAlloc(&ctx->pin_out, nb, cudaHostAllocDefault);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
+    ctx->pin_out_bytes = nb;
+  }
+  CK(cudaMemcpyAsync(ctx->pin_out, din, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const char* ho = (const char*)ctx->pin_out;
+  if (num_poses) {
+    std::memcpy(poses_out, ho + o_pose, 96 * num_poses);
+    std::memcpy(results, ho + o_res, sizeof(gvox_register_result) * num_poses);
+  }
+  if (HN) std::memcpy(error_history, ho + o_hist, 8 * HN);
   return GVOX_OK;
 }
 

@@ -1,0 +1,243 @@
+// k_register.cu -- the solve/update step of the on-device registration loop
+// (gvox_register_batch, include/gvox.h).  One loop
+// iteration is k_linearize -> k_reduce (compact records) -> k_gn_step, the
+// body of a CUDA graph WHILE node; k_gn_step sets the node's condition.
+//
+// Per variable pose v (a "problem"), one warp:
+//   H = sum_f H_ii(f), b = sum_f b_i(f), e = sum_f e(f) over v's factors in
+//   ascending factor order, with H_ii = Ad^T H_jj Ad and b_i = -Ad^T b_j
+//   (Ad = Ad(T_ij); exact since A = -B Ad(T_ij), Eqs. 4-8);
+//   (H + lambda I) delta = -b by fp64 Cholesky; T_v <- T_v Exp(delta).
+#include <cuda_runtime.h>
+
+#include "k_common.cuh"
+
+namespace gvox {
+namespace {
+
+constexpr int kStepWarps = 8;
+
+// Ad(T) for rotation-first tangents: [[R, 0], [t^ R, R]] (row-major 6x6).
+__device__ inline void adjoint6_r(const double* R, const double* t, double* Ad) {
+  for (int i = 0; i < 36; ++i) Ad[i] = 0.0;
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      Ad[a * 6 + b] = R[a * 3 + b];
+      Ad[(a + 3) * 6 + (b + 3)] = R[a * 3 + b];
+    }
+  const double T[9] = {0, -t[2], t[1], t[2], 0, -t[0], -t[1], t[0], 0};
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      double s = 0;
+      for (int c = 0; c < 3; ++c) s += T[a * 3 + c] * R[c * 3 + b];
+      Ad[(a + 3) * 6 + b] = s;
+    }
+}
+
+// SE(3) exponential, rotation-first xi = [w; rho]:
+//   R = I + A K + B K^2,  t = (I + B K + C K^2) rho,  K = w^,
+//   A = sin(th)/th, B = (1 - cos th)/th^2, C = (th - sin th)/th^3.
+__device__ inline void se3_exp_dev(const double* xi, double* R, double* t) {
+  const double w0 = xi[0], w1 = xi[1], w2 = xi[2];
+  const double th2 = w0 * w0 + w1 * w1 + w2 * w2;
+  const double th = sqrt(th2);
+  double A, B, C;
+  if (th < 1e-4) {  // series; the truncation error is below 1e-17
+    A = 1.0 - th2 / 6.0 + th2 * th2 / 120.0;
+    B = 0.5 - th2 / 24.0 + th2 * th2 / 720.0;
+    C = 1.0 / 6.0 - th2 / 120.0 + th2 * th2 / 5040.0;
+  } else {
+    double s, c;
+    sincos(th, &s, &c);
+    A = s / th;
+    B = (1.0 - c) / th2;
+    C = (th - s) / (th2 * th);
+  }
+  const double K[9] = {0, -w2, w1, w2, 0, -w0, -w1, w0, 0};
+  double K2[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      double s = 0;
+      for (int c = 0; c < 3; ++c) s += K[a * 3 + c] * K[c * 3 + b];
+      K2[a * 3 + b] = s;
+    }
+  double V[9];
+  for (int i = 0; i < 9; ++i) {
+    const double I = (i % 4 == 0) ? 1.0 : 0.0;
+    R[i] = I + A * K[i] + B * K2[i];
+    V[i] = I + B * K[i] + C * K2[i];
+  }
+  for (int a = 0; a < 3; ++a) t[a] = V[a * 3 + 0] * xi[3] + V[a * 3 + 1] * xi[4] + V[a * 3 + 2] * xi[5];
+}
+
+// In-place Cholesky of a 6x6 SPD matrix (row-major, lower factor) and solve
+// L L^T x = rhs.  False if a pivot is not positive and finite.
+__device__ inline bool chol6_solve(double* M, const double* rhs, double* x) {
+  for (int j = 0; j < 6; ++j) {
+    double d = M[j * 6 + j];
+    for (int k = 0; k < j; ++k) d -= M[j * 6 + k] * M[j * 6 + k];
+    if (!(d > 0.0) || !isfinite(d)) return false;
+    const double ljj = sqrt(d);
+    M[j * 6 + j] = ljj;
+    for (int i = j + 1; i < 6; ++i) {
+      double s = M[i * 6 + j];
+      for (int k = 0; k < j; ++k) s -= M[i * 6 + k] * M[j * 6 + k];
+      M[i * 6 + j] = s / ljj;
+    }
+  }
+  double y[6];
+  for (int i = 0; i < 6; ++i) {
+    double s = rhs[i];
+    for (int k = 0; k < i; ++k) s -= M[i * 6 + k] * y[k];
+    y[i] = s / M[i * 6 + i];
+  }
+  for (int i = 5; i >= 0; --i) {
+    double s = y[i];
+    for (int k = i + 1; k < 6; ++k) s -= M[k * 6 + i] * x[k];
+    x[i] = s / M[i * 6 + i];
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(32 * kStepWarps)
+    k_gn_step(const RegProblem* __restrict__ problems, int32_t num_problems,
+              const int32_t* __restrict__ reg_factors, const FactorDev* __restrict__ factors,
+              const gvox_factor_accum* __restrict__ accum, double* __restrict__ poses,
+              gvox_register_result* __restrict__ results, int32_t* __restrict__ active,
+              RegControl* __restrict__ ctrl, double* __restrict__ history, int64_t num_poses,
+              cudaGraphConditionalHandle cond) {
+  __shared__ double Ti_s[kStepWarps][12];
+  __shared__ double Ad_s[kStepWarps][36];
+  __shared__ double Hj_s[kStepWarps][36];
+  __shared__ double M_s[kStepWarps][36];
+  __shared__ double H_s[kStepWarps][36];
+  __shared__ double b_s[kStepWarps][6];
+  __shared__ int32_t still_active;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) still_active = 0;
+  __syncthreads();
+  const int32_t iter = ctrl->iter;
+  const int32_t p = blockIdx.x * kStepWarps + w;
+  if (p < num_problems && active[p]) {
+    const RegProblem pr = problems[p];
+    const int32_t v = pr.pose;
+    if (lane < 12) Ti_s[w][lane] = poses[12 * (int64_t)v + lane];
+    for (int e = lane; e < 36; e += 32) H_s[w][e] = 0.0;
+    if (lane < 6) b_s[w][lane] = 0.0;
+    double err = 0.0;
+    int32_t inl = 0;
+    __syncwarp();
+    for (int32_t q = pr.f0; q < pr.f1; ++q) {
+      const int32_t f = reg_factors[q];
+      const FactorDev fd = factors[f];
+      const gvox_factor_accum* a = accum + f;
+      if (lane == 0) {
+        double Tj[12];
+        for (int i = 0; i < 12; ++i) Tj[i] = poses[12 * (int64_t)fd.pj + i];
+        double R[9], t[3], vv[3];
+        relative_pose_dev(Ti_s[w], Tj, R, t, vv);
+        adjoint6_r(R, t, Ad_s[w]);
+        int k = 0;
+        for (int r = 0; r < 6; ++r)
+          for (int c = r; c < 6; ++c) {
+            Hj_s[w][r * 6 + c] = a->terms[k];
+            Hj_s[w][c * 6 + r] = a->terms[k];
+            ++k;
+          }
+        err += a->terms[27];
+        for (int l = 0; l < GVOX_MAX_LEVELS; ++l) inl += a->inliers[l];
+      }
+      __syncwarp();
+      for (int e = lane; e < 36; e += 32) {  // M = H_jj Ad
+        const int r = e / 6, c = e % 6;
+        double s = 0;
+        for (int k = 0; k < 6; ++k) s += Hj_s[w][r * 6 + k] * Ad_s[w][k * 6 + c];
+        M_s[w][e] = s;
+      }
+      __syncwarp();
+      for (int e = lane; e < 36; e += 32) {  // H += Ad^T M
+        const int r = e / 6, c = e % 6;
+        double s = 0;
+        for (int k = 0; k < 6; ++k) s += Ad_s[w][k * 6 + r] * M_s[w][k * 6 + c];
+        H_s[w][e] += s;
+      }
+      if (lane < 6) {  // b += -Ad^T b_j
+        double s = 0;
+        for (int k = 0; k < 6; ++k) s += Ad_s[w][k * 6 + lane] * a->terms[21 + k];
+        b_s[w][lane] -= s;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      gvox_register_result& res = results[v];
+      if (iter == 0) res.error_initial = err;
+      res.error_final = err;
+      res.inliers = inl;
+      res.iterations = iter + 1;
+      if (history) history[(int64_t)iter * num_poses + v] = err;
+      double Mx[36], rhs[6], delta[6];
+      for (int e = 0; e < 36; ++e) Mx[e] = H_s[w][e] + ((e % 7 == 0) ? ctrl->lambda : 0.0);
+      for (int i = 0; i < 6; ++i) rhs[i] = -b_s[w][i];
+      bool go = true;
+      if (!chol6_solve(Mx, rhs, delta)) {
+        res.status = GVOX_REG_SINGULAR;
+        for (int i = 0; i < 6; ++i) res.last_step[i] = 0.0;
+        go = false;
+      } else {
+        double dR[9], dt[3];
+        se3_exp_dev(delta, dR, dt);
+        const double* T = Ti_s[w];
+        double Tn[12];
+        for (int a = 0; a < 3; ++a) {
+          for (int b = 0; b < 3; ++b)
+            Tn[a * 4 + b] = T[a * 4 + 0] * dR[0 * 3 + b] + T[a * 4 + 1] * dR[1 * 3 + b] +
+                            T[a * 4 + 2] * dR[2 * 3 + b];
+          Tn[a * 4 + 3] = T[a * 4 + 0] * dt[0] + T[a * 4 + 1] * dt[1] + T[a * 4 + 2] * dt[2] + T[a * 4 + 3];
+        }
+        for (int i = 0; i < 12; ++i) poses[12 * (int64_t)v + i] = Tn[i];
+        for (int i = 0; i < 6; ++i) res.last_step[i] = delta[i];
+        const double nw = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]);
+        const double nr = sqrt(delta[3] * delta[3] + delta[4] * delta[4] + delta[5] * delta[5]);
+        if (nw <= ctrl->eps_rot && nr <= ctrl->eps_trans) {
+          res.status = GVOX_REG_CONVERGED;
+          go = false;
+        } else if (iter + 1 >= ctrl->max_iter) {
+          res.status = GVOX_REG_MAX_ITER;
+          go = false;
+        }
+      }
+      if (!go) active[p] = 0;
+      else atomicAdd(&still_active, 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (still_active) atomicAdd(&ctrl->any_active, still_active);
+    __threadfence();
+    const unsigned ticket = atomicAdd(&ctrl->blocks_done, 1u);
+    if (ticket == gridDim.x - 1) {  // last block: all counts are in
+      __threadfence();
+      const int32_t any = atomicAdd(&ctrl->any_active, 0);
+      ctrl->any_active = 0;
+      ctrl->blocks_done = 0;
+      ctrl->iter = iter + 1;
+      cudaGraphSetConditional(cond, any > 0 ? 1u : 0u);
+    }
+  }
+}
+
+}  // namespace
+
+void launch_gn_step(const RegProblem* problems, int32_t num_problems, const int32_t* reg_factors,
+                    const FactorDev* factors, const gvox_factor_accum* accum, double* poses,
+                    gvox_register_result* results, int32_t* active, RegControl* ctrl,
+                    double* history, int64_t num_poses, cudaGraphConditionalHandle cond,
+                    cudaStream_t stream) {
+  const unsigned blocks = (unsigned)((num_problems + kStepWarps - 1) / kStepWarps);
+  k_gn_step<<<blocks, 32 * kStepWarps, 0, stream>>>(problems, num_problems, reg_factors, factors,
+                                                     accum, poses, results, active, ctrl, history,
+                                                     num_poses, cond);
+  note_launch();
+}
+
+}  // namespace gvox

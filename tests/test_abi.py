@@ -47,7 +47,9 @@ def test_struct_layouts_match_header(tmp_path, L):
     c.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "gvox.h"\nint main(void){'
                  'printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(gvox_factor), sizeof(gvox_pair),'
                  'sizeof(gvox_linear_factor), sizeof(gvox_factor_accum),'
-                 'offsetof(gvox_linear_factor, error), offsetof(gvox_linear_factor, inliers));return 0;}')
+                 'offsetof(gvox_linear_factor, error), offsetof(gvox_linear_factor, inliers));'
+                 'printf("%zu %zu %zu %zu\\n", sizeof(gvox_register_params), sizeof(gvox_register_result),'
+                 'offsetof(gvox_register_result, error_initial), offsetof(gvox_register_params, lambda));return 0;}')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)])
     got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
@@ -57,6 +59,10 @@ def test_struct_layouts_match_header(tmp_path, L):
     assert got[3] == L.FACTOR_ACCUM_DTYPE.itemsize == 288
     assert got[4] == L.LINEAR_FACTOR_DTYPE.fields["error"][1]
     assert got[5] == L.LINEAR_FACTOR_DTYPE.fields["inliers"][1]
+    assert got[6] == L.REGISTER_PARAMS_DTYPE.itemsize == 32
+    assert got[7] == L.REGISTER_RESULT_DTYPE.itemsize == 80
+    assert got[8] == L.REGISTER_RESULT_DTYPE.fields["error_initial"][1]
+    assert got[9] == L.REGISTER_PARAMS_DTYPE.fields["lambda"][1]
 
 
 def test_status_strings_and_null_errors(L):
