@@ -228,6 +228,49 @@ gvox_status gvox_overlap_select(gvox_ctx* ctx, const gvox_cloud* const* clouds,
                                 int64_t num_poses, int level, int32_t num, int32_t den,
                                 uint8_t* selected, int mem);
 
+/* ------------------------------------------------------------- keyframes */
+
+/* Overlap with a UNION of maps ("we evaluate the overlap rate between
+   that frame and the union of all keyframes, and if the overlap is smaller
+   than a threshold (e.g., 90%), we insert that frame into the keyframe
+   list").  Query q: counts[q] = number of points of clouds[queries[q].source_cloud]
+   at pose queries[q].pose_i whose key at `level` is occupied in AT LEAST ONE
+   of the maps members[first .. first + count) (each at its own pose_j; keys
+   and poses as in gvox_overlap).  The rate is counts[q] / n; the insertion
+   test "smaller than 90 %" is 10 * count < 9 * n.  count = 0 gives 0.
+   queries, members, poses: host arrays; counts: int32 [num_queries] in `mem`.
+   One H2D; one D2H when mem == GVOX_HOST. */
+typedef struct gvox_union_query {
+  int32_t source_cloud;
+  int32_t pose_i;
+  int32_t first; /* into members[] */
+  int32_t count; /* >= 0 */
+} gvox_union_query;
+typedef struct gvox_union_member {
+  int32_t target_map;
+  int32_t pose_j;
+} gvox_union_member;
+gvox_status gvox_overlap_union(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t num_clouds,
+                               const gvox_map* const* maps, int64_t num_maps,
+                               const gvox_union_query* queries, int64_t num_queries,
+                               const gvox_union_member* members, int64_t num_members,
+                               const double* poses, int64_t num_poses, int level,
+                               int32_t* counts, int mem);
+
+/* Keyframe removal rule (host only, no GPU work).  Keyframes
+   0 .. K-1 in list order, K-1 = the latest keyframe; overlap[i * K + j] =
+   o(i, j), the overlap rate of keyframe i's points in keyframe j's voxels
+   (gvox_overlap counts / n_i).  remove[i] (K bytes out) is set to 1 for
+     1. every i < K-1 with o(i, K-1) < min_overlap ("overlap the latest
+        keyframe by less than a certain threshold (e.g., 5%)");
+     2. then, if more than n_odom keyframes remain, the ONE remaining i < K-1
+        minimising s(i) = o(i, K-1) * sum_{j remaining, j != i, j < K-1} (1 - o(i, j))
+        (ties: the smallest i).  Reading R25: the paper's
+        j in [1, N_odom - 1] \ {i} is every other non-latest keyframe.
+   The latest keyframe is never removed.  K >= 1, n_odom >= 1. */
+gvox_status gvox_keyframe_update(const double* overlap, int32_t K, int32_t n_odom,
+                                 double min_overlap, uint8_t* remove);
+
 /* ------------------------------------------------------------- linearize */
 
 /* Batched linearization of matching cost factors (Eqs. 2-8; Fig. 4 / P:224:

@@ -486,6 +486,31 @@ void oracle_overlap_batch(const float* const* mus, const int64_t* npts,
   for (auto& th : pool) th.join();
 }
 
+// P:280 "the overlap rate between that frame and the union of all keyframes":
+// the number of points of the source (at pose Ti) whose key at `level` is
+// occupied in at least one of the K maps (map k at pose Tjs + 12 k).
+int64_t oracle_overlap_union(const float* mu, int64_t n, const OracleMap* const* maps,
+                             const double* Tjs, int64_t K, const double* Ti, int level) {
+  std::vector<Pose> T(K);
+  Pose pi = load_pose(Ti);
+  for (int64_t j = 0; j < K; ++j) {
+    double v[3];
+    relative_pose(pi, load_pose(Tjs + 12 * j), &T[j], v);
+  }
+  int64_t count = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    double p[3] = {mu[3 * k], mu[3 * k + 1], mu[3 * k + 2]};
+    bool hit = false;
+    for (int64_t j = 0; j < K && !hit; ++j) {
+      double q[3];
+      transform_point(T[j], p, q);
+      hit = find_voxel(maps[j], level, q) != nullptr;
+    }
+    if (hit) ++count;
+  }
+  return count;
+}
+
 int oracle_sizeof_factor(void) { return (int)sizeof(OracleFactor); }
 
 }  // extern "C"

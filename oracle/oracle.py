@@ -73,6 +73,8 @@ def lib():
         L.oracle_linearize_batch.argtypes = [P, P, P, P, P, P, ctypes.c_int64, P, ctypes.c_int, P]
         L.oracle_overlap_batch.argtypes = [P, P, P, P, ctypes.c_int64, P, ctypes.c_int,
                                            ctypes.c_int, P]
+        L.oracle_overlap_union.restype = ctypes.c_int64
+        L.oracle_overlap_union.argtypes = [P, ctypes.c_int64, P, P, ctypes.c_int64, P, ctypes.c_int]
         L.oracle_sizeof_factor.restype = ctypes.c_int
         assert L.oracle_sizeof_factor() == ctypes.sizeof(OracleFactor)
         _lib = L
@@ -156,6 +158,18 @@ def overlap(mu, vmap: VoxelMap, Ti, Tj, level: int) -> int:
     Tj = _f64(Tj, 12)
     return int(lib().oracle_overlap(_ptr(mu), mu.shape[0], vmap.handle, _ptr(Ti), _ptr(Tj),
                                     int(level)))
+
+
+def overlap_union(mu, vmaps, Ti, Tjs, level: int) -> int:
+    """Points of mu (at Ti) falling in a voxel of ANY of vmaps (map k at Tjs[k])."""
+    mu = _f32(mu, 3)
+    Ti = _f64(Ti, 12)
+    K = len(vmaps)
+    Tjs = _f64(np.asarray(Tjs, np.float64).reshape(-1), 12 * K)
+    P = ctypes.c_void_p
+    mh = (P * max(K, 1))(*[m.handle.value for m in vmaps])
+    return int(lib().oracle_overlap_union(_ptr(mu), mu.shape[0], mh, _ptr(Tjs), K, _ptr(Ti),
+                                          int(level)))
 
 
 def _factor_dict(f: OracleFactor, levels: int):

@@ -39,6 +39,9 @@ REGISTER_PARAMS_DTYPE = np.dtype([("max_iterations", "<i4"), ("reserved", "<i4")
 REGISTER_RESULT_DTYPE = np.dtype([("status", "<i4"), ("iterations", "<i4"), ("inliers", "<i4"),
                                   ("reserved", "<i4"), ("error_initial", "<f8"),
                                   ("error_final", "<f8"), ("last_step", "<f8", (6,))])
+UNION_QUERY_DTYPE = np.dtype([("source_cloud", "<i4"), ("pose_i", "<i4"), ("first", "<i4"),
+                              ("count", "<i4")])
+UNION_MEMBER_DTYPE = np.dtype([("target_map", "<i4"), ("pose_j", "<i4")])
 REG_FIXED, REG_MAX_ITER, REG_CONVERGED, REG_SINGULAR = 0, 1, 2, 3
 
 # exported symbols (tests check every one declared in include/gvox.h is here)
@@ -49,7 +52,7 @@ SYMBOLS = [
     "gvox_create_voxelmap", "gvox_create_voxelmaps", "gvox_voxelmap_info", "gvox_voxelmap_levels",
     "gvox_voxelmap_export", "gvox_voxelmap_lookup", "gvox_map_destroy",
     "gvox_overlap", "gvox_overlap_select", "gvox_linearize_batch", "gvox_linearize_batch_accum", "gvox_expand",
-    "gvox_register_batch",
+    "gvox_register_batch", "gvox_overlap_union", "gvox_keyframe_update",
     "gvox_status_string", "gvox_last_error", "gvox_launch_count", "gvox_version",
 ]
 
@@ -95,6 +98,8 @@ def lib():
         "gvox_linearize_batch": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32, P]),
         "gvox_linearize_batch_accum": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32]),
         "gvox_expand": (I32, [P, P, I64, P, I64, P, P, I32]),
+        "gvox_overlap_union": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I64, I32, P, I32]),
+        "gvox_keyframe_update": (I32, [P, I32, I32, D, P]),
         "gvox_register_batch": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, P, P, P, I32]),
         "gvox_status_string": (ctypes.c_char_p, [I32]),
         "gvox_last_error": (ctypes.c_char_p, []),

@@ -14,7 +14,8 @@ from typing import Sequence
 import numpy as np
 
 from ._lib import (FACTOR_ACCUM_DTYPE, FACTOR_DTYPE, GVOX_DEVICE, GVOX_HOST, LINEAR_FACTOR_DTYPE,
-                   PAIR_DTYPE, REGISTER_PARAMS_DTYPE, REGISTER_RESULT_DTYPE, check, lib)
+                   PAIR_DTYPE, REGISTER_PARAMS_DTYPE, REGISTER_RESULT_DTYPE, UNION_MEMBER_DTYPE,
+                   UNION_QUERY_DTYPE, check, lib)
 
 
 def _torch():
@@ -336,6 +337,80 @@ def expand(ctx: Context, factors, poses, accum, out=None):
     check(lib().gvox_expand(ctx.handle, _ptr(factors)[0], F, _ptr(poses)[0], poses.shape[0],
                             ctypes.c_void_p(accum.data_ptr()), po, mem))
     return out
+
+
+def overlap_union(ctx: Context, clouds, maps, queries, members, poses, level: int, out=None):
+    """gvox_overlap_union: queries [Q,4] {source_cloud, pose_i, first, count},
+    members [M,2] {target_map, pose_j}.  Returns int32 counts [Q] (host) or
+    fills the int32 CUDA tensor `out`."""
+    C, Mh = _handles(clouds), _handles(maps)
+    q = np.ascontiguousarray(np.asarray(queries, np.int64).reshape(-1, 4).astype(np.int32)).view(
+        UNION_QUERY_DTYPE).reshape(-1)
+    m = np.ascontiguousarray(np.asarray(members, np.int64).reshape(-1, 2).astype(np.int32)).view(
+        UNION_MEMBER_DTYPE).reshape(-1)
+    poses = as_poses(poses)
+    if out is None:
+        out = np.zeros(len(q), np.int32)
+    po, mem = _ptr(out)
+    check(lib().gvox_overlap_union(ctx.handle, C.arr, C.n, Mh.arr, Mh.n, _ptr(q)[0], len(q),
+                                   _ptr(m)[0] if len(m) else None, len(m), _ptr(poses)[0],
+                                   poses.shape[0], int(level), po, mem))
+    return out
+
+
+def keyframe_update(overlap_rates, n_odom: int = 20, min_overlap: float = 0.05) -> np.ndarray:
+    """gvox_keyframe_update (host): overlap_rates [K,K] o(i, j), row/col K-1 =
+    the latest keyframe.  Returns a bool mask of the keyframes to remove."""
+    o = np.ascontiguousarray(np.asarray(overlap_rates, np.float64))
+    K = o.shape[0]
+    rm = np.zeros(K, np.uint8)
+    check(lib().gvox_keyframe_update(_ptr(o)[0], K, int(n_odom), float(min_overlap), _ptr(rm)[0]))
+    return rm.astype(bool)
+
+
+class KeyframeList:
+    """The P:280-288 keyframe mechanism driven through the library: for each
+    new frame, one gvox_overlap_union (insertion test "overlap with the union
+    of all keyframes smaller than 90 %", decided in integers), and on insertion
+    one gvox_overlap of the new keyframe against the others (both directions)
+    followed by gvox_keyframe_update.  Holds only bookkeeping: cloud/map/pose
+    indices of the keyframes and their o(i, j) matrix."""
+
+    def __init__(self, ctx: Context, level: int, n_odom: int = 20, insert_num: int = 9,
+                 insert_den: int = 10, min_overlap: float = 0.05):
+        self.ctx, self.level, self.n_odom = ctx, int(level), int(n_odom)
+        self.insert_num, self.insert_den, self.min_overlap = int(insert_num), int(insert_den), min_overlap
+        self.frames = []          # frame ids of the keyframes, list order
+        self.o = np.zeros((0, 0))
+
+    def add_frame(self, frame: int, clouds, maps, poses):
+        """frame indexes clouds/maps/poses (its cloud, its voxelmap, its pose).
+        Returns (inserted, removed frame ids)."""
+        n = len(clouds[frame])
+        if self.frames:
+            members = [[f, f] for f in self.frames]
+            cnt = int(overlap_union(self.ctx, clouds, maps, [[frame, frame, 0, len(members)]], members,
+                                    poses, self.level)[0])
+            if not self.insert_den * cnt < self.insert_num * n:
+                return False, []
+        ks = self.frames + [frame]
+        K = len(ks)
+        o = np.zeros((K, K))
+        o[:K - 1, :K - 1] = self.o
+        o[K - 1, K - 1] = 1.0 if n else 0.0
+        if K > 1:
+            pairs = [[f, frame, f, frame] for f in self.frames] + [[frame, f, frame, f] for f in self.frames]
+            c = overlap(self.ctx, clouds, maps, pairs, poses, self.level)
+            for a, f in enumerate(self.frames):
+                nf = len(clouds[f])
+                o[a, K - 1] = c[a] / nf if nf else 0.0
+                o[K - 1, a] = c[K - 1 + a] / n if n else 0.0
+        rm = keyframe_update(o, self.n_odom, self.min_overlap)
+        keep = ~rm
+        removed = [ks[a] for a in range(K) if rm[a]]
+        self.frames = [ks[a] for a in range(K) if keep[a]]
+        self.o = o[np.ix_(keep, keep)]
+        return True, removed
 
 
 def register_batch(ctx: Context, clouds, maps, factors, poses, max_iterations: int = 10,

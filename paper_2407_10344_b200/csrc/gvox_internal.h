@@ -234,6 +234,21 @@ void launch_overlap_select(const CloudDev* const* clouds, const MapDev* const* m
                            int32_t num, int32_t den, uint8_t* selected, bool all_dense,
                            cudaStream_t stream);
 
+// union overlap (P:280 keyframe insertion): query q = source cloud at pose pi
+// against members[first, first + count) = {target map, pose_j}
+struct UnionQueryDev {
+  int32_t src, pi, first, count;
+};
+struct UnionMemberDev {
+  int32_t tgt, pj;
+};
+// tiles of tile_pts <= 256 * 32 points
+void launch_overlap_union(const CloudDev* const* clouds, const MapDev* const* maps,
+                          const UnionQueryDev* queries, const UnionMemberDev* members,
+                          const int32_t* tile_start, const int32_t* tile_query, int64_t num_tiles,
+                          int tile_pts, const double* poses, int level, int32_t* counts,
+                          cudaStream_t stream);
+
 // linearize
 struct FactorDev {
   int32_t src, tgt, pi, pj;
@@ -246,7 +261,7 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
                       const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
                       int64_t num_tiles, int tile_pts, int max_levels, const double* poses,
                       double* partials, int32_t* tile_factor, int64_t* corr_dump,
-                      bool all_dense, bool fast, cudaStream_t stream);
+                      bool all_dense, bool fast, bool validate, cudaStream_t stream);
 // reduce tile partials per factor in fixed order; write full or compact records.
 void launch_reduce(const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
                    const double* poses, const double* partials, gvox_linear_factor* out_full,

@@ -1097,7 +1097,8 @@ struct LinPlan {
   std::vector<FactorDev> fdev;
   int max_levels = 1;
   bool all_dense = true;
-  bool fast = true;  // the specialised kernel: exactly 3 dyadic dense levels, no visibility test
+  bool fast = true;       // the specialised kernel: exactly 3 dyadic dense levels, no dump
+  bool validate = false;  // some factor has GVOX_F_VALIDATE_SURFACE (FAST: the VALID variant)
 };
 
 gvox_status plan_linearize(const char* fn, const gvox_cloud* const* clouds,
@@ -1113,7 +1114,8 @@ gvox_status plan_linearize(const char* fn, const gvox_cloud* const* clouds,
     const gvox_map* m = maps[q.target_map];
     p->max_levels = std::max(p->max_levels, m->levels);
     for (int l = 0; l < m->levels; ++l) p->all_dense = p->all_dense && m->desc.lv[l].dense;
-    p->fast = p->fast && m->levels == 3 && m->desc.dyadic && !(q.flags & GVOX_F_VALIDATE_SURFACE);
+    p->fast = p->fast && m->levels == 3 && m->desc.dyadic;
+    p->validate = p->validate || (q.flags & GVOX_F_VALIDATE_SURFACE);
     const int64_t n = clouds[q.source_cloud]->n;
     int ppt = 1;
     while (ppt < GVOX_TILE_MAX_PPT && (int64_t)256 * min_tiles * (ppt * 2) <= n) ppt *= 2;
@@ -1199,7 +1201,8 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
     launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
                      (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
                      0, max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
-                     (int32_t*)(wb + o_tf), corr_dump, all_dense, fast, ctx->stream);
+                     (int32_t*)(wb + o_tf), corr_dump, all_dense, fast, plan.validate,
+                     ctx->stream);
   }
   CK_LAUNCH("linearize");
   {
@@ -1285,6 +1288,151 @@ gvox_status gvox_expand(gvox_ctx* ctx, const gvox_factor* factors, int64_t num_f
   return GVOX_OK;
 }
 
+// ------------------------------------------------------------ keyframes
+gvox_status gvox_overlap_union(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t num_clouds,
+                               const gvox_map* const* maps, int64_t num_maps,
+                               const gvox_union_query* queries, int64_t num_queries,
+                               const gvox_union_member* members, int64_t num_members,
+                               const double* poses, int64_t num_poses, int level,
+                               int32_t* counts, int mem) {
+  const char* fn = "gvox_overlap_union";
+  if (!ctx) return fail(GVOX_ERR_INVALID, "%s: ctx is NULL", fn);
+  if (num_queries < 0 || num_members < 0) return fail(GVOX_ERR_INVALID, "%s: negative size", fn);
+  if (num_queries == 0) return GVOX_OK;
+  if (!clouds || !queries || !poses || !counts || (num_members > 0 && (!members || !maps)))
+    return fail(GVOX_ERR_INVALID, "%s: NULL argument", fn);
+  if (mem != GVOX_HOST && mem != GVOX_DEVICE)
+    return fail(GVOX_ERR_INVALID, "%s: mem must be GVOX_HOST or GVOX_DEVICE", fn);
+  if (num_queries > INT32_MAX || num_members > INT32_MAX)
+    return fail(GVOX_ERR_INVALID, "%s: more than 2^31 queries or members", fn);
+  for (int64_t m = 0; m < num_members; ++m) {
+    const gvox_union_member& u = members[m];
+    if (u.target_map < 0 || u.target_map >= num_maps || !maps[u.target_map])
+      return fail(GVOX_ERR_INVALID, "%s: member %lld: target_map %d out of range [0, %lld)", fn,
+                  (long long)m, u.target_map, (long long)num_maps);
+    if (u.pose_j < 0 || u.pose_j >= num_poses)
+      return fail(GVOX_ERR_INVALID, "%s: member %lld: pose_j %d out of range [0, %lld)", fn,
+                  (long long)m, u.pose_j, (long long)num_poses);
+    if (level < 0 || level >= maps[u.target_map]->levels)
+      return fail(GVOX_ERR_INVALID, "%s: member %lld: level %d outside the map's [0, %d)", fn,
+                  (long long)m, level, maps[u.target_map]->levels);
+  }
+  for (int64_t q = 0; q < num_queries; ++q) {
+    const gvox_union_query& u = queries[q];
+    if (u.source_cloud < 0 || u.source_cloud >= num_clouds || !clouds[u.source_cloud])
+      return fail(GVOX_ERR_INVALID, "%s: query %lld: source_cloud %d out of range [0, %lld)", fn,
+                  (long long)q, u.source_cloud, (long long)num_clouds);
+    if (u.pose_i < 0 || u.pose_i >= num_poses)
+      return fail(GVOX_ERR_INVALID, "%s: query %lld: pose_i %d out of range [0, %lld)", fn,
+                  (long long)q, u.pose_i, (long long)num_poses);
+    if (u.count < 0 || u.first < 0 || (int64_t)u.first + u.count > num_members)
+      return fail(GVOX_ERR_INVALID, "%s: query %lld: members [%d, %d + %d) outside [0, %lld)", fn,
+                  (long long)q, u.first, u.first, u.count, (long long)num_members);
+  }
+  for (int64_t i = 0; i < num_poses; ++i)
+    if (!finite_pose(poses + 12 * i))
+      return fail(GVOX_ERR_INVALID, "%s: pose %lld is not finite", fn, (long long)i);
+  DeviceGuard g(ctx->device);
+  // tiles of 256 * ppt points (ppt <= 32: one hit bit per point and thread)
+  int64_t total = 0;
+  for (int64_t q = 0; q < num_queries; ++q)
+    if (queries[q].count > 0) total += clouds[queries[q].source_cloud]->n;
+  int ppt = 1;
+  while (ppt < 32 && total / ((int64_t)256 * ppt * 2) >= 148 * 8) ppt *= 2;
+  const int tile_pts = 256 * ppt;
+  std::vector<int32_t> tstart(num_queries + 1, 0);
+  for (int64_t q = 0; q < num_queries; ++q) {
+    const int64_t n = queries[q].count > 0 ? clouds[queries[q].source_cloud]->n : 0;
+    const int64_t nt = tstart[q] + (n + tile_pts - 1) / tile_pts;
+    if (nt > INT32_MAX) return fail(GVOX_ERR_INVALID, "%s: more than 2^31 tiles", fn);
+    tstart[q + 1] = (int32_t)nt;
+  }
+  const int64_t T = tstart.back();
+  Layout lay;
+  size_t o_pose = lay.add(96 * num_poses);
+  size_t o_q = lay.add(sizeof(UnionQueryDev) * num_queries);
+  size_t o_m = lay.add(sizeof(UnionMemberDev) * std::max<int64_t>(num_members, 1));
+  size_t o_ts = lay.add(4 * tstart.size());
+  size_t o_cl = lay.add(8 * num_clouds);
+  size_t o_mp = lay.add(8 * std::max<int64_t>(num_maps, 1));
+  const size_t in_bytes = lay.size;
+  void* pin = nullptr;
+  gvox_status st = pin_reserve(ctx, in_bytes, &pin);
+  if (st) return st;
+  char* hp = (char*)pin;
+  std::memcpy(hp + o_pose, poses, 96 * num_poses);
+  static_assert(sizeof(UnionQueryDev) == sizeof(gvox_union_query), "layout");
+  static_assert(sizeof(UnionMemberDev) == sizeof(gvox_union_member), "layout");
+  std::memcpy(hp + o_q, queries, sizeof(UnionQueryDev) * num_queries);
+  if (num_members) std::memcpy(hp + o_m, members, sizeof(UnionMemberDev) * num_members);
+  std::memcpy(hp + o_ts, tstart.data(), 4 * tstart.size());
+  for (int64_t i = 0; i < num_clouds; ++i) ((const CloudDev**)(hp + o_cl))[i] = clouds[i] ? clouds[i]->dev : nullptr;
+  for (int64_t i = 0; i < num_maps; ++i) ((const MapDev**)(hp + o_mp))[i] = maps[i] ? maps[i]->dev : nullptr;
+  Layout wl;
+  size_t o_in = wl.add(in_bytes);
+  size_t o_tq = wl.add(4 * (size_t)std::max<int64_t>(T, 1));
+  size_t o_out = wl.add(4 * num_queries);
+  void* ws = nullptr;
+  st = ws_reserve(ctx, 0, wl.size, &ws);
+  if (st) return st;
+  char* wb = (char*)ws;
+  char* din = wb + o_in;
+  st = h2d_block(ctx, din, hp, in_bytes);
+  if (st) return st;
+  int32_t* dcounts = mem == GVOX_DEVICE ? counts : (int32_t*)(wb + o_out);
+  CK(cudaMemsetAsync(dcounts, 0, 4 * num_queries, ctx->stream));
+  if (T > 0) {
+    launch_tile_map((const int32_t*)(din + o_ts), num_queries, (int32_t*)(wb + o_tq), ctx->stream);
+    TimerScope ts(ctx, GVOX_TIMER_OVERLAP);
+    launch_overlap_union((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
+                         (const UnionQueryDev*)(din + o_q), (const UnionMemberDev*)(din + o_m),
+                         (const int32_t*)(din + o_ts), (const int32_t*)(wb + o_tq), T, tile_pts,
+                         (const double*)(din + o_pose), level, dcounts, ctx->stream);
+  }
+  CK_LAUNCH(fn);
+  if (mem == GVOX_HOST) {
+    CK(cudaMemcpyAsync(counts, dcounts, 4 * num_queries, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return GVOX_OK;
+}
+
+gvox_status gvox_keyframe_update(const double* overlap, int32_t K, int32_t n_odom,
+                                 double min_overlap, uint8_t* remove) {
+  const char* fn = "gvox_keyframe_update";
+  if (K < 1 || n_odom < 1) return fail(GVOX_ERR_INVALID, "%s: need K >= 1 and n_odom >= 1", fn);
+  if (!overlap || !remove) return fail(GVOX_ERR_INVALID, "%s: NULL argument", fn);
+  for (int64_t i = 0; i < (int64_t)K * K; ++i)
+    if (!std::isfinite(overlap[i]))
+      return fail(GVOX_ERR_INVALID, "%s: overlap[%lld] is not finite", fn, (long long)i);
+  const int latest = K - 1;
+  std::vector<uint8_t> rm(K, 0);
+  // 1. keyframes overlapping the latest one by less than min_overlap
+  for (int i = 0; i < latest; ++i)
+    if (overlap[(int64_t)i * K + latest] < min_overlap) rm[i] = 1;
+  // 2. one score-based removal while more than n_odom keyframes remain
+  int remaining = 0;
+  for (int i = 0; i < K; ++i) remaining += !rm[i];
+  if (remaining > n_odom) {
+    int best = -1;
+    double best_s = 0.0;
+    for (int i = 0; i < latest; ++i) {
+      if (rm[i]) continue;
+      double sum = 0.0;
+      for (int j = 0; j < latest; ++j)
+        if (j != i && !rm[j]) sum += 1.0 - overlap[(int64_t)i * K + j];
+      const double s = overlap[(int64_t)i * K + latest] * sum;
+      if (best < 0 || s < best_s) {
+        best = i;
+        best_s = s;
+      }
+    }
+    if (best >= 0) rm[best] = 1;
+  }
+  std::memcpy(remove, rm.data(), K);
+  return GVOX_OK;
+}
+
 // ------------------------------------------------------------ registration
 namespace {
 constexpr int kRegMinTiles = 32;
@@ -1343,7 +1491,9 @@ gvox_status gvox_register_batch(gvox_ctx* ctx, const gvox_cloud* const* clouds,
     // registration batches are small (one odometry step: ~10 factors): tiles
     // of >= 32 per factor keep every SM busy in the latency-bound loop
     st = plan_linearize(fn, clouds, maps, factors, num_factors,
-                        std::getenv("GVOX_LIN_GENERIC") == nullptr, &plan, kRegMinTiles);
+                        std::getenv("GVOX_LIN_GENERIC") == nullptr, &plan,
+                        std::getenv("GVOX_REG_MIN_TILES") ? std::max(1, std::atoi(std::getenv("GVOX_REG_MIN_TILES")))
+                                                          : kRegMinTiles);
     if (st) return st;
   }
   const int64_t T = num_factors > 0 ? plan.tstart[num_factors] : 0;
@@ -1406,6 +1556,28 @@ gvox_status gvox_register_batch(gvox_ctx* ctx, const gvox_cloud* const* clouds,
   if (NP > 0) {
     launch_tile_map((const int32_t*)(din + o_ts), num_factors, (int32_t*)(wb + o_tf), ctx->stream);
     CK_LAUNCH("register tile map");
+    auto body = [&](cudaStream_t sm, cudaGraphConditionalHandle cond) {
+      launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
+                       (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
+                       0, plan.max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
+                       (int32_t*)(wb + o_tf), nullptr, plan.all_dense, plan.fast, plan.validate, sm);
+      launch_reduce((const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors,
+                    (const double*)(din + o_pose), (const double*)(wb + o_part), nullptr,
+                    (gvox_factor_accum*)(wb + o_acc), sm);
+      launch_gn_step((const RegProblem*)(din + o_prob), (int32_t)NP, (const int32_t*)(din + o_rf),
+                     (const FactorDev*)(din + o_fac), (const gvox_factor_accum*)(wb + o_acc),
+                     (double*)(din + o_pose), (gvox_register_result*)(din + o_res),
+                     (int32_t*)(din + o_act), (RegControl*)(din + o_ctrl),
+                     HN ? (double*)(din + o_hist) : nullptr, num_poses, cond, sm);
+    };
+    if (std::getenv("GVOX_REG_EAGER")) {
+      // profiling aid (ncu does not see kernels inside conditional graph
+      // nodes): max_iterations plain launches; stopped problems are skipped
+      // by the solve kernel, so results are identical
+      TimerScope ts(ctx, GVOX_TIMER_REGISTER);
+      for (int it = 0; it < P.max_iterations; ++it) body(ctx->stream, 0);
+      CK_LAUNCH("register loop (eager)");
+    } else {
     if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
     // ---- the loop: a WHILE node whose body is linearize -> reduce -> solve
     cudaGraph_t graph = nullptr;
@@ -1421,21 +1593,10 @@ gvox_status gvox_register_batch(gvox_ctx* ctx, const gvox_cloud* const* clouds,
     cp.conditional.size = 1;
     cudaGraphNode_t node;
     CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    CK(cudaStreamBeginCaptureToGraph(ctx->cap_stream, body, nullptr, nullptr, 0,
+    cudaGraph_t body_graph = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(ctx->cap_stream, body_graph, nullptr, nullptr, 0,
                                      cudaStreamCaptureModeThreadLocal));
-    launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
-                     (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
-                     0, plan.max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
-                     (int32_t*)(wb + o_tf), nullptr, plan.all_dense, plan.fast, ctx->cap_stream);
-    launch_reduce((const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors,
-                  (const double*)(din + o_pose), (const double*)(wb + o_part), nullptr,
-                  (gvox_factor_accum*)(wb + o_acc), ctx->cap_stream);
-    launch_gn_step((const RegProblem*)(din + o_prob), (int32_t)NP, (const int32_t*)(din + o_rf),
-                   (const FactorDev*)(din + o_fac), (const gvox_factor_accum*)(wb + o_acc),
-                   (double*)(din + o_pose), (gvox_register_result*)(din + o_res),
-                   (int32_t*)(din + o_act), (RegControl*)(din + o_ctrl),
-                   HN ? (double*)(din + o_hist) : nullptr, num_poses, cond, ctx->cap_stream);
+    body(ctx->cap_stream, cond);
     cudaGraph_t captured = nullptr;
     cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &captured);
     if (ce != cudaSuccess) return cuda_fail(ce, "register loop capture");
@@ -1451,6 +1612,7 @@ gvox_status gvox_register_batch(gvox_ctx* ctx, const gvox_cloud* const* clouds,
     }
     note_launch();
     CK(cudaGraphExecDestroy(exec));  // freed asynchronously once the launch completes
+    }
   }
   // ---- outputs
   if (mem == GVOX_DEVICE) {

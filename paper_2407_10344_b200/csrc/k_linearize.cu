@@ -449,7 +449,7 @@ __device__ __forceinline__ void tile_reduce(const Acc<MAXL>& ac, double (*red)[k
 // (the A, B, N planes of the warp's next 32 points).  FAST is the specialisation for the common
 // batch (exactly MAXL dyadic levels, no visibility test, no correspondence
 // dump): no runtime level / flag tests and branch-free grid probes.
-template <int MAXL, bool ALL_DENSE, bool FAST>
+template <int MAXL, bool ALL_DENSE, bool FAST, bool VALID = false>
 __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     k_linearize(const CloudDev* const* __restrict__ clouds, const MapDev* const* __restrict__ maps,
                 const FactorDev* __restrict__ factors, const int32_t* __restrict__ tile_start,
@@ -476,7 +476,8 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
   const int dyadic = FAST ? 1 : sh.dyadic;
   const double r0 = sh.r0, inv_r0 = sh.inv_r0;
   const float r0f = (float)sh.r0;
-  const bool validate = FAST ? false : (bool)sh.validate;
+  // FAST: the visibility test only in the VALID instantiation
+  const bool validate = FAST ? (VALID && sh.validate) : (bool)sh.validate;
   const bool error_only = sh.error_only;
   if (FAST) corr = nullptr;
   // 32-bit point index within the tile; the source planes pre-offset to its start
@@ -527,7 +528,8 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     __shared__ uint32_t live_s[kWarps][kWords];
     const int32_t iters = (npts - 32 * warp + kThreads - 1) / kThreads;
     const MapLevelDev& cv = sh.lv[MAXL - 1];
-    const bool cull_on = GVOX_LIN_CULL && sh.cbox != nullptr && cv.grid != nullptr;
+    // (no culling when validating: discarded points are counted, culled or not)
+    const bool cull_on = GVOX_LIN_CULL && sh.cbox != nullptr && cv.grid != nullptr && !validate;
 #pragma unroll 1
     for (int i0 = 0; i0 < kWords * 32; i0 += 32) {
       const int32_t i = i0 + lane;
@@ -566,15 +568,22 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     cp_async_wait<S - 2>();  // the first live iteration landed
     PointData pn;
     int32_t vn[MAXL];
+    bool inv_n = false;  // VALID: the next point is discarded by the P:197 test
     auto prep = [&](int32_t i, int stg) {
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) vn[l] = -1;
+      inv_n = false;
       if (i != kNone && i * kThreads + tid < npts) {
         const float4 a = sbuf[warp][stg][0][lane];
+        if (VALID && validate && invisible(sh, a, sbuf[warp][stg][2][lane])) {
+          inv_n = true;
+          return;
+        }
         transform_point(sh, a, 1, r0, inv_r0, r0f, pn);
 #pragma unroll
         for (int l = 0; l < MAXL; ++l)
-          vn[l] = lookup_dense_pred(sh.lv[l], pn.k0x >> l, pn.k0y >> l, pn.k0z >> l);
+          vn[l] = ALL_DENSE ? lookup_dense_pred(sh.lv[l], pn.k0x >> l, pn.k0y >> l, pn.k0z >> l)
+                            : lookup_level<false>(sh.lv[l], pn.k0x >> l, pn.k0y >> l, pn.k0z >> l);
       }
     };
     prep(i_cur, 0);
@@ -589,10 +598,15 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       int32_t vid[MAXL];
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) vid[l] = vn[l];
+      const bool inv = VALID && inv_n;
       prep(i_nxt, st);
       i_cur = i_nxt;
       i_nxt = i_nx2;
       i_nx2 = i_nx2 == kNone ? kNone : next_live(i_nx2);
+      if (VALID && inv) {  // (k < npts: only real points are marked)
+        ++ac.n_invisible;
+        continue;
+      }
       bool any = false;
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) any |= vid[l] >= 0;
@@ -816,11 +830,20 @@ __global__ void k_reduce(const FactorDev* __restrict__ factors, const int32_t* _
   const int64_t f = (int64_t)blockIdx.x * kReduceWarps + w;
   if (f >= num_factors) return;
   const int32_t t0 = tile_start[f], t1 = tile_start[f + 1];
-  // fixed tile order -> deterministic sums
+  // fixed order (4 interleaved partial sums over the tiles, then combined) ->
+  // deterministic; the 4 chains keep 4 loads in flight per lane
   for (int j = lane; j < kPartialStride; j += 32) {
-    double s = 0.0;
-    for (int32_t t = t0; t < t1; ++t) s += partials[(int64_t)t * kPartialStride + j];
-    sum_s[w][j] = s;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int32_t t = t0;
+    for (; t + 4 <= t1; t += 4) {
+      const double* q = partials + (int64_t)t * kPartialStride + j;
+      s0 += q[0];
+      s1 += q[kPartialStride];
+      s2 += q[2 * kPartialStride];
+      s3 += q[3 * kPartialStride];
+    }
+    for (; t < t1; ++t) s0 += partials[(int64_t)t * kPartialStride + j];
+    sum_s[w][j] = (s0 + s1) + (s2 + s3);
   }
   __syncwarp();
   if (lane == 0) {
@@ -876,12 +899,16 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
                       const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
                       int64_t num_tiles, int tile_pts, int max_levels, const double* poses,
                       double* partials, int32_t* tile_factor, int64_t* corr_dump,
-                      bool all_dense, bool fast, cudaStream_t stream) {
+                      bool all_dense, bool fast, bool validate, cudaStream_t stream) {
   if (num_tiles <= 0) return;
   const unsigned grid = (unsigned)num_tiles;
-  if (fast && max_levels == 3 && all_dense) {
-    k_linearize<3, true, true><<<grid, kThreads, 0, stream>>>(
-        clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, nullptr);
+  // FAST (3 dyadic levels, no dump): dense grids or hash levels, with or
+  // without the P:197 visibility test
+  if (fast && max_levels == 3) {
+    auto* k = all_dense ? (validate ? k_linearize<3, true, true, true> : k_linearize<3, true, true, false>)
+                        : (validate ? k_linearize<3, false, true, true> : k_linearize<3, false, true, false>);
+    k<<<grid, kThreads, 0, stream>>>(clouds, maps, factors, tile_start, tile_factor, tile_pts, poses,
+                                     partials, nullptr);
   } else if (max_levels <= 3) {
     if (all_dense)
       k_linearize<3, true, false><<<grid, kThreads, 0, stream>>>(

@@ -277,3 +277,101 @@ void launch_overlap_select(const CloudDev* const* clouds, const MapDev* const* m
   note_launch();
 }
 }  // namespace gvox
+
+// ------------------------------------------------------------ union overlap
+namespace gvox {
+namespace {
+
+constexpr int kUnionChunk = 32;  // members staged in shared memory at a time
+
+// P:280 keyframe insertion test: "the overlap rate between that frame and the
+// union of all keyframes".  One CTA per tile of a query's source points; each
+// thread owns up to 32 points (bit m of `hit`: point kb + m * 256 + tid) and
+// tests them against the members in chunks of kUnionChunk (poses composed
+// in fp64 with the pinned order, Q10), stopping at the first member whose
+// voxel at `level` is occupied.  Integer counts: exact, order-independent.
+__global__ void __launch_bounds__(kThreads)
+    k_overlap_union(const CloudDev* const* __restrict__ clouds, const MapDev* const* __restrict__ maps,
+                    const UnionQueryDev* __restrict__ queries, const UnionMemberDev* __restrict__ members,
+                    const int32_t* __restrict__ tile_start, const int32_t* __restrict__ tile_query,
+                    int tile_pts, const double* __restrict__ poses, int level,
+                    int32_t* __restrict__ counts) {
+  __shared__ double Rt_s[kUnionChunk][12];  // R (9), t (3) of T_j^-1 T_i
+  __shared__ MapLevelDev lv_s[kUnionChunk];
+  __shared__ int32_t dy_s[kUnionChunk];
+  __shared__ int warp_cnt[kThreads / 32];
+  const int tid = threadIdx.x;
+  const int64_t tile = blockIdx.x;
+  const int32_t qi = __ldg(tile_query + tile);
+  const UnionQueryDev q = queries[qi];
+  const CloudDev* cd = clouds[q.src];
+  const float4* __restrict__ A = cd->A;
+  const int64_t kb = (int64_t)(tile - __ldg(tile_start + qi)) * tile_pts;
+  const int64_t ke = kb + tile_pts < cd->n ? kb + tile_pts : cd->n;
+  const int nm = (int)((ke - kb + kThreads - 1) / kThreads);  // <= 32
+  const double* Ti = poses + 12 * (int64_t)q.pi;
+  uint32_t hit = 0;
+  for (int c0 = 0; c0 < q.count; c0 += kUnionChunk) {
+    const int nc = q.count - c0 < kUnionChunk ? q.count - c0 : kUnionChunk;
+    __syncthreads();  // previous chunk no longer in use
+    if (tid < nc) {
+      const UnionMemberDev mb = members[q.first + c0 + tid];
+      const MapDev* md = maps[mb.tgt];
+      double Tj[12], Tl[12], v[3];
+      for (int j = 0; j < 12; ++j) {
+        Tj[j] = __ldg(poses + 12 * (int64_t)mb.pj + j);
+        Tl[j] = __ldg(Ti + j);
+      }
+      relative_pose_dev(Tl, Tj, Rt_s[tid], Rt_s[tid] + 9, v);
+      lv_s[tid] = md->lv[level];
+      dy_s[tid] = md->dyadic;
+    }
+    __syncthreads();
+    for (int m = 0; m < nm; ++m) {
+      if (hit >> m & 1u) continue;
+      const int64_t k = kb + (int64_t)m * kThreads + tid;
+      if (k >= ke) break;
+      const float4 a = __ldg(A + pt_off(k));
+      const double mx = a.x, my = a.y, mz = a.z;
+      for (int j = 0; j < nc; ++j) {
+        const double* R = Rt_s[j];
+        const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, R[9])));
+        const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, R[10])));
+        const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, R[11])));
+        const MapLevelDev& lv = lv_s[j];
+        const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dy_s[j]);
+        const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dy_s[j]);
+        const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dy_s[j]);
+        if (lookup_level<false>(lv, kx, ky, kz) >= 0) {
+          hit |= 1u << m;
+          break;
+        }
+      }
+    }
+  }
+  int cnt = __popc(hit);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((tid & 31) == 0) warp_cnt[tid >> 5] = cnt;
+  __syncthreads();
+  if (tid == 0) {
+    int s = 0;
+    for (int w = 0; w < kThreads / 32; ++w) s += warp_cnt[w];
+    if (s) atomicAdd(counts + qi, s);
+  }
+}
+
+}  // namespace
+
+void launch_overlap_union(const CloudDev* const* clouds, const MapDev* const* maps,
+                          const UnionQueryDev* queries, const UnionMemberDev* members,
+                          const int32_t* tile_start, const int32_t* tile_query, int64_t num_tiles,
+                          int tile_pts, const double* poses, int level, int32_t* counts,
+                          cudaStream_t stream) {
+  if (num_tiles <= 0) return;
+  k_overlap_union<<<(unsigned)num_tiles, kThreads, 0, stream>>>(
+      clouds, maps, queries, members, tile_start, tile_query, tile_pts, poses, level, counts);
+  note_launch();
+}
+
+}  // namespace gvox

@@ -4,8 +4,9 @@
 // body of a CUDA graph WHILE node; k_gn_step sets the node's condition.
 //
 // Per variable pose v (a "problem"), one warp:
-//   H = sum_f H_ii(f), b = sum_f b_i(f), e = sum_f e(f) over v's factors in
-//   ascending factor order, with H_ii = Ad^T H_jj Ad and b_i = -Ad^T b_j
+//   H = sum_f H_ii(f), b = sum_f b_i(f), e = sum_f e(f) over v's factors (lane
+//   l takes factors l, l + 32, ...; then a fixed xor-tree sum over lanes, so
+//   the result depends only on the problem's factor list), with H_ii = Ad^T H_jj Ad and b_i = -Ad^T b_j
 //   (Ad = Ad(T_ij); exact since A = -B Ad(T_ij), Eqs. 4-8);
 //   (H + lambda I) delta = -b by fp64 Cholesky; T_v <- T_v Exp(delta).
 #include <cuda_runtime.h>
@@ -107,9 +108,6 @@ __global__ void __launch_bounds__(32 * kStepWarps)
               RegControl* __restrict__ ctrl, double* __restrict__ history, int64_t num_poses,
               cudaGraphConditionalHandle cond) {
   __shared__ double Ti_s[kStepWarps][12];
-  __shared__ double Ad_s[kStepWarps][36];
-  __shared__ double Hj_s[kStepWarps][36];
-  __shared__ double M_s[kStepWarps][36];
   __shared__ double H_s[kStepWarps][36];
   __shared__ double b_s[kStepWarps][6];
   __shared__ int32_t still_active;
@@ -122,52 +120,85 @@ __global__ void __launch_bounds__(32 * kStepWarps)
     const RegProblem pr = problems[p];
     const int32_t v = pr.pose;
     if (lane < 12) Ti_s[w][lane] = poses[12 * (int64_t)v + lane];
-    for (int e = lane; e < 36; e += 32) H_s[w][e] = 0.0;
-    if (lane < 6) b_s[w][lane] = 0.0;
-    double err = 0.0;
-    int32_t inl = 0;
     __syncwarp();
-    for (int32_t q = pr.f0; q < pr.f1; ++q) {
+    // lane l expands the factors pr.f0 + l, pr.f0 + l + 32, ... (H_ii = Ad^T H_jj Ad,
+    // b_i = -Ad^T b_j, upper triangle); then a fixed xor-tree sum over lanes
+    double hs[21], bs[6], err = 0.0;
+    int32_t inl = 0;
+#pragma unroll
+    for (int i = 0; i < 21; ++i) hs[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) bs[i] = 0.0;
+    for (int32_t q = pr.f0 + lane; q < pr.f1; q += 32) {
       const int32_t f = reg_factors[q];
       const FactorDev fd = factors[f];
       const gvox_factor_accum* a = accum + f;
-      if (lane == 0) {
-        double Tj[12];
-        for (int i = 0; i < 12; ++i) Tj[i] = poses[12 * (int64_t)fd.pj + i];
-        double R[9], t[3], vv[3];
-        relative_pose_dev(Ti_s[w], Tj, R, t, vv);
-        adjoint6_r(R, t, Ad_s[w]);
-        int k = 0;
-        for (int r = 0; r < 6; ++r)
-          for (int c = r; c < 6; ++c) {
-            Hj_s[w][r * 6 + c] = a->terms[k];
-            Hj_s[w][c * 6 + r] = a->terms[k];
-            ++k;
-          }
-        err += a->terms[27];
-        for (int l = 0; l < GVOX_MAX_LEVELS; ++l) inl += a->inliers[l];
+      double Tj[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) Tj[i] = poses[12 * (int64_t)fd.pj + i];
+      double R[9], t[3], vv[3], Ad[36], Hj[36];
+      relative_pose_dev(Ti_s[w], Tj, R, t, vv);
+      adjoint6_r(R, t, Ad);
+      int k = 0;
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = r; c < 6; ++c) {
+          const double x = a->terms[k++];
+          Hj[r * 6 + c] = x;
+          Hj[c * 6 + r] = x;
+        }
+      double M[36];  // H_jj Ad
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          double s2 = 0;
+#pragma unroll
+          for (int j = 0; j < 6; ++j) s2 += Hj[r * 6 + j] * Ad[j * 6 + c];
+          M[r * 6 + c] = s2;
+        }
+      k = 0;
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = r; c < 6; ++c) {
+          double s2 = 0;
+#pragma unroll
+          for (int j = 0; j < 6; ++j) s2 += Ad[j * 6 + r] * M[j * 6 + c];
+          hs[k++] += s2;
+        }
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        double s2 = 0;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) s2 += Ad[j * 6 + c] * a->terms[21 + j];
+        bs[c] -= s2;
       }
-      __syncwarp();
-      for (int e = lane; e < 36; e += 32) {  // M = H_jj Ad
-        const int r = e / 6, c = e % 6;
-        double s = 0;
-        for (int k = 0; k < 6; ++k) s += Hj_s[w][r * 6 + k] * Ad_s[w][k * 6 + c];
-        M_s[w][e] = s;
-      }
-      __syncwarp();
-      for (int e = lane; e < 36; e += 32) {  // H += Ad^T M
-        const int r = e / 6, c = e % 6;
-        double s = 0;
-        for (int k = 0; k < 6; ++k) s += Ad_s[w][k * 6 + r] * M_s[w][k * 6 + c];
-        H_s[w][e] += s;
-      }
-      if (lane < 6) {  // b += -Ad^T b_j
-        double s = 0;
-        for (int k = 0; k < 6; ++k) s += Ad_s[w][k * 6 + lane] * a->terms[21 + k];
-        b_s[w][lane] -= s;
-      }
-      __syncwarp();
+      err += a->terms[27];
+#pragma unroll
+      for (int l = 0; l < GVOX_MAX_LEVELS; ++l) inl += a->inliers[l];
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int i = 0; i < 21; ++i) hs[i] += __shfl_xor_sync(0xffffffffu, hs[i], o);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) bs[i] += __shfl_xor_sync(0xffffffffu, bs[i], o);
+      err += __shfl_xor_sync(0xffffffffu, err, o);
+      inl += __shfl_xor_sync(0xffffffffu, inl, o);
+    }
+    if (lane == 0) {
+      int k = 0;
+      for (int r = 0; r < 6; ++r)
+        for (int c = r; c < 6; ++c) {
+          H_s[w][r * 6 + c] = hs[k];
+          H_s[w][c * 6 + r] = hs[k];
+          ++k;
+        }
+      for (int i = 0; i < 6; ++i) b_s[w][i] = bs[i];
+    }
+    __syncwarp();
     if (lane == 0) {
       gvox_register_result& res = results[v];
       if (iter == 0) res.error_initial = err;
@@ -221,7 +252,7 @@ __global__ void __launch_bounds__(32 * kStepWarps)
       ctrl->any_active = 0;
       ctrl->blocks_done = 0;
       ctrl->iter = iter + 1;
-      cudaGraphSetConditional(cond, any > 0 ? 1u : 0u);
+      if (cond) cudaGraphSetConditional(cond, any > 0 ? 1u : 0u);  // 0: eager (profiling) mode
     }
   }
 }

@@ -381,19 +381,30 @@ def test_batch_equals_serial_and_determinism(gv, ctx):
     assert all(r[k].tobytes() == r[0].tobytes() for k in range(5))
 
 
-def test_fast_kernel_equals_generic(gv, ctx, monkeypatch):
-    """The specialised kernel (3 dyadic dense levels, no visibility test, no
-    dump) performs the same arithmetic in the same order as the generic one."""
-    sc = synth.make("C2")
+@pytest.fixture(scope="module")
+def dense_scene():
+    # submaps (C4 recipe, small): every level gets a dense index grid
+    return synth.global_scene(n_submaps=8, n_points=30000, half_blocks=2, factor_dist=40.0,
+                              cand_dist=60.0)
+
+
+@pytest.mark.parametrize("which", ["C2-hash", "C4-dense"])
+@pytest.mark.parametrize("flags", [0, 1])
+def test_fast_kernel_equals_generic(gv, ctx, monkeypatch, flags, which, request):
+    """The specialised kernel (3 dyadic levels, no dump; dense-grid or hash
+    levels; its VALID variant with the P:197 visibility test) performs the same
+    arithmetic in the same order as the generic one."""
+    sc = synth.make("C2") if which == "C2-hash" else request.getfixturevalue("dense_scene")
     clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
     maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
     f = sc.factors.copy()
-    f[:, 4] = 0
+    f[:, 4] = flags
     fast = gv.linearize_batch(ctx, clouds, maps, f, sc.poses)
     monkeypatch.setenv("GVOX_LIN_GENERIC", "1")
     generic = gv.linearize_batch(ctx, clouds, maps, f, sc.poses)
     assert fast.tobytes() == generic.tobytes()
     assert fast["inliers"].sum() > 0
+    assert (fast["num_invisible"].sum() > 0) == bool(flags)
 
 
 def test_compact_expand_equals_full(gv, ctx):
