@@ -136,7 +136,8 @@ enum {
   GVOX_TIMER_LINEARIZE = 2, /* fused correspondence + linearization kernel */
   GVOX_TIMER_REDUCE = 3,    /* per-factor reduction / expansion kernel */
   GVOX_TIMER_REGISTER = 4,  /* one gvox_register_batch graph launch (all iterations) */
-  GVOX_TIMER_COUNT = 5
+  GVOX_TIMER_PREPROCESS = 5, /* k-NN (count, scan, scatter, query) / covariance kernels */
+  GVOX_TIMER_COUNT = 6
 };
 gvox_status gvox_ctx_enable_timing(gvox_ctx* ctx, int enable);
 gvox_status gvox_ctx_timing(gvox_ctx* ctx, double* ms, int64_t* launches, int reset);
@@ -227,6 +228,40 @@ gvox_status gvox_overlap_select(gvox_ctx* ctx, const gvox_cloud* const* clouds,
                                 const gvox_pair* pairs, int64_t num_pairs, const double* poses,
                                 int64_t num_poses, int level, int32_t num, int32_t den,
                                 uint8_t* selected, int mem);
+
+/* ---------------------------------------------------------- preprocessing */
+
+/* Exact k nearest neighbours ("C_k is calculated from neighboring
+   points of p_k given by a k-nearest-neighbor search"; "the costly
+   exact nearest neighbor search is only performed in the preprocessing
+   step").  A batch of `count` independent clouds stored back to back:
+   cloud c = points [offsets[c], offsets[c+1]) of `points` (n x 3 floats).
+   neighbors (n x k int32): row i lists the k points of i's cloud nearest to i
+   (self included) as LOCAL indices within the cloud, ordered by (squared
+   distance, index) ascending; -1 pads rows of clouds with fewer than k
+   points.  Distances: fp64 d2 = (dx*dx + dy*dy) + dz*dz from the fp32 inputs
+   with no fused multiply-add (reading R26), so the result is unique.
+   cell_size (> 0, metres): the search grid pitch; speed only, never the
+   result (about twice the downsampling resolution works well).
+   1 <= k <= 32.  offsets: host int64 [count + 1], offsets[0] = 0.  points and
+   neighbors live in `mem`.  Synchronizes once (to size the grids).
+   Errors: GVOX_ERR_INVALID for bad sizes or a non-finite coordinate. */
+gvox_status gvox_knn(gvox_ctx* ctx, const float* points, const int64_t* offsets, int64_t count,
+                     int32_t k, double cell_size, int32_t* neighbors, int mem);
+
+/* Per-point covariance from a neighbour table (reading R27): the
+   sample covariance of the point's neighbours (fp64), the unit eigenvector n
+   of its smallest eigenvalue oriented toward the cloud origin (n . mu <= 0),
+   and the GICP plane model C = I - (1 - 1e-3) n n^T (eigenvalues 1e-3, 1, 1).
+   A zero sample covariance gives C = 1e-6 I and n = 0 (R28).  neighbors as
+   produced by gvox_knn (local indices, -1 = none; other values are rejected
+   for host arrays and undefined behaviour for device arrays).  cov (n x 6:
+   xx xy xz yy yz zz) and normals (n x 3) are fp32 in `mem`, like points and
+   neighbors.  The neighbour table may come from an earlier pose of the same
+   points (reused after deskewing). */
+gvox_status gvox_estimate_covariances(gvox_ctx* ctx, const float* points, const int64_t* offsets,
+                                      int64_t count, const int32_t* neighbors, int32_t k,
+                                      float* cov, float* normals, int mem);
 
 /* ------------------------------------------------------------- keyframes */
 

@@ -17,7 +17,7 @@ GVOX_HOST = 0
 GVOX_DEVICE = 1
 F_VALIDATE_SURFACE = 1
 F_ERROR_ONLY = 2
-TIMERS = ("build", "overlap", "linearize", "reduce", "register")
+TIMERS = ("build", "overlap", "linearize", "reduce", "register", "preprocess")
 
 STATUS = {0: "GVOX_OK", 1: "GVOX_ERR_INVALID", 2: "GVOX_ERR_RANGE", 3: "GVOX_ERR_CUDA",
           4: "GVOX_ERR_NOMEM"}
@@ -52,7 +52,8 @@ SYMBOLS = [
     "gvox_create_voxelmap", "gvox_create_voxelmaps", "gvox_voxelmap_info", "gvox_voxelmap_levels",
     "gvox_voxelmap_export", "gvox_voxelmap_lookup", "gvox_map_destroy",
     "gvox_overlap", "gvox_overlap_select", "gvox_linearize_batch", "gvox_linearize_batch_accum", "gvox_expand",
-    "gvox_register_batch", "gvox_overlap_union", "gvox_keyframe_update",
+    "gvox_register_batch", "gvox_overlap_union", "gvox_keyframe_update", "gvox_knn",
+    "gvox_estimate_covariances",
     "gvox_status_string", "gvox_last_error", "gvox_launch_count", "gvox_version",
 ]
 
@@ -98,6 +99,8 @@ def lib():
         "gvox_linearize_batch": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32, P]),
         "gvox_linearize_batch_accum": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32]),
         "gvox_expand": (I32, [P, P, I64, P, I64, P, P, I32]),
+        "gvox_knn": (I32, [P, P, P, I64, I32, D, P, I32]),
+        "gvox_estimate_covariances": (I32, [P, P, P, I64, P, I32, P, P, I32]),
         "gvox_overlap_union": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I64, I32, P, I32]),
         "gvox_keyframe_update": (I32, [P, I32, I32, D, P]),
         "gvox_register_batch": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, P, P, P, I32]),

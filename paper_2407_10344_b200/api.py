@@ -339,6 +339,54 @@ def expand(ctx: Context, factors, poses, accum, out=None):
     return out
 
 
+def _points_batch(points, offsets):
+    if _is_cuda_tensor(points):
+        pts = points.to(_torch().float32).reshape(-1, 3).contiguous()
+    else:
+        pts = np.ascontiguousarray(np.asarray(points, np.float32).reshape(-1, 3))
+    n = pts.shape[0]
+    off = np.array([0, n] if offsets is None else offsets, np.int64)
+    return pts, off
+
+
+def knn(ctx: Context, points, k: int = 10, cell_size: float = 0.5, offsets=None):
+    """gvox_knn: exact k nearest neighbours (local indices, -1 pad) of each
+    point within its cloud.  points: float32 [N,3] numpy (-> numpy result) or
+    CUDA tensor (-> int32 CUDA tensor); offsets: cloud boundaries [C+1]
+    (default: one cloud)."""
+    pts, off = _points_batch(points, offsets)
+    n = pts.shape[0]
+    if _is_cuda_tensor(pts):
+        out = _torch().empty((n, k), dtype=_torch().int32, device=pts.device)
+    else:
+        out = np.empty((n, k), np.int32)
+    pp_, mem = _ptr(pts)
+    check(lib().gvox_knn(ctx.handle, pp_, _ptr(off)[0], len(off) - 1, int(k), float(cell_size),
+                         _ptr(out)[0], mem))
+    return out
+
+
+def estimate_covariances(ctx: Context, points, neighbors, offsets=None):
+    """gvox_estimate_covariances: (cov [N,6] fp32, normals [N,3] fp32), numpy
+    or CUDA tensors like the inputs."""
+    pts, off = _points_batch(points, offsets)
+    n = pts.shape[0]
+    k = int(neighbors.shape[1])
+    if _is_cuda_tensor(pts):
+        torch = _torch()
+        nb = neighbors.to(torch.int32).contiguous()
+        cov = torch.empty((n, 6), dtype=torch.float32, device=pts.device)
+        nrm = torch.empty((n, 3), dtype=torch.float32, device=pts.device)
+    else:
+        nb = np.ascontiguousarray(np.asarray(neighbors, np.int32))
+        cov = np.empty((n, 6), np.float32)
+        nrm = np.empty((n, 3), np.float32)
+    pp_, mem = _ptr(pts)
+    check(lib().gvox_estimate_covariances(ctx.handle, pp_, _ptr(off)[0], len(off) - 1, _ptr(nb)[0],
+                                          k, _ptr(cov)[0], _ptr(nrm)[0], mem))
+    return cov, nrm
+
+
 def overlap_union(ctx: Context, clouds, maps, queries, members, poses, level: int, out=None):
     """gvox_overlap_union: queries [Q,4] {source_cloud, pose_i, first, count},
     members [M,2] {target_map, pose_j}.  Returns int32 counts [Q] (host) or

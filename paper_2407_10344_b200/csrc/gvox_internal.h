@@ -249,6 +249,35 @@ void launch_overlap_union(const CloudDev* const* clouds, const MapDev* const* ma
                           int tile_pts, const double* poses, int level, int32_t* counts,
                           cudaStream_t stream);
 
+// preprocessing (k_knn.cu): per cloud, a uniform cell grid over its bounding
+// box; the cloud's points are [first, first + n) of the batch arrays and its
+// cells [cell0, cell0 + dim0 * dim1 * dim2) of the global cell arrays
+struct KnnCloudDev {
+  int64_t first, n;
+  double lo[3];
+  double s, inv_s;
+  int32_t dim[3];
+  int32_t cell0;
+};
+void launch_knn_bbox(const float* pts, const KnnCloudDev* clouds, const int32_t* tile_start,
+                     const int32_t* tile_cloud, int64_t num_tiles, int tile_pts, int32_t* box,
+                     int32_t* bad, cudaStream_t stream);
+void launch_knn_count(const float* pts, const KnnCloudDev* clouds, const int32_t* tile_start,
+                      const int32_t* tile_cloud, int64_t num_tiles, int tile_pts, int32_t* cell_of,
+                      int32_t* count, cudaStream_t stream);
+void launch_exclusive_scan(const int32_t* in, int64_t n, int32_t* out, int32_t* scratch,
+                           cudaStream_t stream);
+void launch_knn_scatter(const float* pts, const KnnCloudDev* clouds, const int32_t* tile_start,
+                        const int32_t* tile_cloud, int64_t num_tiles, int tile_pts,
+                        const int32_t* cell_of, const int32_t* cell_start, int32_t* fill,
+                        float4* sorted, cudaStream_t stream);
+void launch_knn_query(const KnnCloudDev* clouds, const int32_t* tile_start, const int32_t* tile_cloud,
+                      int64_t num_tiles, int tile_pts, const float4* sorted,
+                      const int32_t* cell_start, int k, int32_t* out, cudaStream_t stream);
+void launch_covariance(const float* pts, const KnnCloudDev* clouds, const int32_t* tile_start,
+                       const int32_t* tile_cloud, int64_t num_tiles, int tile_pts, const int32_t* nbr,
+                       int k, float* cov, float* nrm, cudaStream_t stream);
+
 // linearize
 struct FactorDev {
   int32_t src, tgt, pi, pj;

@@ -201,7 +201,11 @@ gvox_status ws_reserve(gvox_ctx* ctx, int which, size_t bytes, void** out) {
       ctx->ws_bytes[which] = 0;
     }
     cudaError_t e = cudaMallocAsync(&ctx->ws[which], nb, ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMallocAsync");
+    if (e != cudaSuccess) {
+      char where[96];
+      snprintf(where, sizeof(where), "workspace %d cudaMallocAsync(%zu bytes)", which, nb);
+      return cuda_fail(e, where);
+    }
     ctx->ws_bytes[which] = nb;
   }
   *out = ctx->ws[which];
@@ -1283,6 +1287,262 @@ gvox_status gvox_expand(gvox_ctx* ctx, const gvox_factor* factors, int64_t num_f
   if (mem == GVOX_HOST) {
     CK(cudaMemcpyAsync(out, dout, sizeof(gvox_linear_factor) * num_factors,
                        cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return GVOX_OK;
+}
+
+// ------------------------------------------------------------ preprocessing
+namespace {
+
+// common validation + point upload + per-cloud tile plan for the
+// preprocessing calls
+struct PrepBatch {
+  const float* dpts = nullptr;          // device points
+  std::vector<KnnCloudDev> cl;
+  std::vector<int32_t> tstart;
+  int tile_pts = 256;  // one query per thread or two: a single frame still fills the GPU
+  int64_t n = 0, T = 0;
+};
+
+gvox_status prep_batch(const char* fn, gvox_ctx* ctx, const float* points, const int64_t* offsets,
+                       int64_t count, int mem, void* dev_points_ws, PrepBatch* b) {
+  if (count < 0) return fail(GVOX_ERR_INVALID, "%s: count < 0", fn);
+  if (!offsets) return fail(GVOX_ERR_INVALID, "%s: offsets is NULL", fn);
+  if (offsets[0] != 0) return fail(GVOX_ERR_INVALID, "%s: offsets[0] != 0", fn);
+  for (int64_t c = 0; c < count; ++c)
+    if (offsets[c + 1] < offsets[c])
+      return fail(GVOX_ERR_INVALID, "%s: offsets not non-decreasing at cloud %lld", fn, (long long)c);
+  b->n = offsets[count];
+  if (b->n > INT32_MAX) return fail(GVOX_ERR_INVALID, "%s: more than 2^31 points", fn);
+  if (b->n > 0 && !points) return fail(GVOX_ERR_INVALID, "%s: points is NULL", fn);
+  b->cl.resize(count);
+  b->tstart.assign(count + 1, 0);
+  for (int64_t c = 0; c < count; ++c) {
+    KnnCloudDev& d = b->cl[c];
+    std::memset(&d, 0, sizeof(d));
+    d.first = offsets[c];
+    d.n = offsets[c + 1] - offsets[c];
+    b->tstart[c + 1] = b->tstart[c] + (int32_t)((d.n + b->tile_pts - 1) / b->tile_pts);
+  }
+  b->T = b->tstart[count];
+  if (mem == GVOX_DEVICE || b->n == 0) {
+    b->dpts = points;
+  } else {
+    CK(cudaMemcpyAsync(dev_points_ws, points, 12 * b->n, cudaMemcpyHostToDevice, ctx->stream));
+    b->dpts = (const float*)dev_points_ws;
+  }
+  return GVOX_OK;
+}
+
+}  // namespace
+
+gvox_status gvox_knn(gvox_ctx* ctx, const float* points, const int64_t* offsets, int64_t count,
+                     int32_t k, double cell_size, int32_t* neighbors, int mem) {
+  const char* fn = "gvox_knn";
+  if (!ctx) return fail(GVOX_ERR_INVALID, "%s: ctx is NULL", fn);
+  if (k < 1 || k > 32) return fail(GVOX_ERR_INVALID, "%s: k = %d outside [1, 32]", fn, k);
+  if (!(cell_size > 0.0) || !std::isfinite(cell_size))
+    return fail(GVOX_ERR_INVALID, "%s: cell_size must be finite and > 0", fn);
+  if (mem != GVOX_HOST && mem != GVOX_DEVICE)
+    return fail(GVOX_ERR_INVALID, "%s: mem must be GVOX_HOST or GVOX_DEVICE", fn);
+  if (count < 0 || !offsets) return fail(GVOX_ERR_INVALID, "%s: bad count / offsets", fn);
+  const int64_t n_all = count > 0 ? offsets[count] : 0;
+  if (n_all > 0 && !neighbors) return fail(GVOX_ERR_INVALID, "%s: neighbors is NULL", fn);
+  DeviceGuard g(ctx->device);
+  // workspace 1: uploaded points (host input), bbox, the cloud / tile tables
+  void* ws1 = nullptr;
+  Layout l1;
+  size_t o_pts = l1.add(mem == GVOX_HOST ? 12 * (size_t)std::max<int64_t>(n_all, 0) : 0);
+  size_t o_box = l1.add(4 * 6 * (size_t)std::max<int64_t>(count, 1) + 16);
+  size_t o_cl = l1.add(sizeof(KnnCloudDev) * (size_t)std::max<int64_t>(count, 1));
+  size_t o_ts = l1.add(4 * (size_t)(count + 1));
+  size_t o_tc = l1.add(4 * (size_t)(n_all / 256 + count + 1));
+  gvox_status st = ws_reserve(ctx, 1, l1.size, &ws1);
+  if (st) return st;
+  char* w1 = (char*)ws1;
+  PrepBatch b;
+  st = prep_batch(fn, ctx, points, offsets, count, mem, w1 + o_pts, &b);
+  if (st) return st;
+  if (b.n == 0) return GVOX_OK;
+  // ---- bounding boxes (one sync: the grids are sized on the host)
+  {
+    void* pin = nullptr;
+    Layout lp;
+    size_t p_cl = lp.add(sizeof(KnnCloudDev) * count);
+    size_t p_ts = lp.add(4 * (count + 1));
+    size_t p_box = lp.add(4 * 6 * count + 16);
+    st = pin_reserve(ctx, lp.size, &pin);
+    if (st) return st;
+    char* hp = (char*)pin;
+    std::memcpy(hp + p_cl, b.cl.data(), sizeof(KnnCloudDev) * count);
+    std::memcpy(hp + p_ts, b.tstart.data(), 4 * (count + 1));
+    int32_t* hb = (int32_t*)(hp + p_box);
+    for (int64_t c = 0; c < count; ++c)
+      for (int a = 0; a < 3; ++a) {
+        hb[6 * c + a] = INT32_MAX;
+        hb[6 * c + 3 + a] = INT32_MIN;
+      }
+    hb[6 * count] = 0;  // non-finite flag
+    CK(cudaMemcpyAsync(w1 + o_cl, hp + p_cl, sizeof(KnnCloudDev) * count, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(w1 + o_ts, hp + p_ts, 4 * (count + 1), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(w1 + o_box, hp + p_box, 4 * (6 * count + 1), cudaMemcpyHostToDevice, ctx->stream));
+    launch_tile_map((const int32_t*)(w1 + o_ts), count, (int32_t*)(w1 + o_tc), ctx->stream);
+    launch_knn_bbox(b.dpts, (const KnnCloudDev*)(w1 + o_cl), (const int32_t*)(w1 + o_ts),
+                    (const int32_t*)(w1 + o_tc), b.T, b.tile_pts, (int32_t*)(w1 + o_box),
+                    (int32_t*)(w1 + o_box) + 6 * count, ctx->stream);
+    CK_LAUNCH(fn);
+    CK(cudaMemcpyAsync(hb, w1 + o_box, 4 * (6 * count + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->pin_pending = false;
+    if (hb[6 * count]) return fail(GVOX_ERR_INVALID, "%s: non-finite point coordinate", fn);
+    if (std::getenv("GVOX_DEBUG_KNN"))
+      for (int64_t c = 0; c < count; ++c)
+        fprintf(stderr, "[gvox_knn] cloud %lld n %lld box %g %g %g .. %g %g %g (mem %d, pts %p)\n",
+                (long long)c, (long long)b.cl[c].n, ordered_to_float(hb[6 * c]),
+                ordered_to_float(hb[6 * c + 1]), ordered_to_float(hb[6 * c + 2]),
+                ordered_to_float(hb[6 * c + 3]), ordered_to_float(hb[6 * c + 4]),
+                ordered_to_float(hb[6 * c + 5]), mem, (const void*)b.dpts);
+    // ---- per-cloud grids: pitch cell_size, doubled while the grid would
+    // hold more than 32 cells per point (sparse extents)
+    int64_t cells = 0;
+    for (int64_t c = 0; c < count; ++c) {
+      KnnCloudDev& d = b.cl[c];
+      if (d.n == 0) {
+        d.s = cell_size;
+        d.inv_s = 1.0 / cell_size;
+        d.dim[0] = d.dim[1] = d.dim[2] = 1;
+        d.cell0 = (int32_t)cells;
+        cells += 1;
+        continue;
+      }
+      double lo[3], hi[3];
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = ordered_to_float(hb[6 * c + a]);
+        hi[a] = ordered_to_float(hb[6 * c + 3 + a]);
+        if (!(hi[a] >= lo[a]) || !std::isfinite(hi[a] - lo[a]))
+          return fail(GVOX_ERR_INVALID, "%s: cloud %lld: bad bounding box [%g, %g] on axis %d", fn,
+                      (long long)c, lo[a], hi[a], a);
+      }
+      double s = cell_size;
+      int64_t dims[3], nc;
+      for (;;) {
+        nc = 1;
+        for (int a = 0; a < 3; ++a) {
+          dims[a] = (int64_t)std::floor((hi[a] - lo[a]) / s) + 1;
+          nc *= dims[a];
+        }
+        if (nc <= std::max<int64_t>(32 * d.n, 4096) && nc < (1ll << 30)) break;
+        s *= 2.0;
+      }
+      for (int a = 0; a < 3; ++a) {
+        d.lo[a] = lo[a];
+        d.dim[a] = (int32_t)dims[a];
+      }
+      d.s = s;
+      d.inv_s = 1.0 / s;
+      d.cell0 = (int32_t)cells;
+      cells += nc;
+      if (cells >= INT32_MAX) return fail(GVOX_ERR_INVALID, "%s: search grids exceed 2^31 cells", fn);
+    }
+    CK(cudaMemcpyAsync(w1 + o_cl, b.cl.data(), sizeof(KnnCloudDev) * count, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    // (pageable copy of a host vector: synchronous with respect to the host)
+    Layout l2;
+    size_t o_cnt = l2.add(4 * (size_t)(cells + 1));
+    size_t o_start = l2.add(4 * (size_t)(cells + 1));
+    size_t o_fill = l2.add(4 * (size_t)(cells + 1));
+    size_t o_scr = l2.add(4 * (size_t)(cells / 4096 + 2));
+    size_t o_cell = l2.add(4 * (size_t)b.n);
+    size_t o_sorted = l2.add(16 * (size_t)b.n);
+    size_t o_out = l2.add(mem == GVOX_HOST ? 4 * (size_t)b.n * k : 0);
+    void* ws2 = nullptr;
+    st = ws_reserve(ctx, 2, l2.size, &ws2);
+    if (st) return st;
+    char* w2 = (char*)ws2;
+    CK(cudaMemsetAsync(w2 + o_cnt, 0, 4 * (size_t)(cells + 1), ctx->stream));
+    CK(cudaMemsetAsync(w2 + o_fill, 0, 4 * (size_t)(cells + 1), ctx->stream));
+    const KnnCloudDev* dcl = (const KnnCloudDev*)(w1 + o_cl);
+    const int32_t* dts = (const int32_t*)(w1 + o_ts);
+    const int32_t* dtc = (const int32_t*)(w1 + o_tc);
+    int32_t* dout = mem == GVOX_DEVICE ? neighbors : (int32_t*)(w2 + o_out);
+    TimerScope ts(ctx, GVOX_TIMER_PREPROCESS);
+    launch_knn_count(b.dpts, dcl, dts, dtc, b.T, b.tile_pts, (int32_t*)(w2 + o_cell),
+                     (int32_t*)(w2 + o_cnt), ctx->stream);
+    launch_exclusive_scan((const int32_t*)(w2 + o_cnt), cells, (int32_t*)(w2 + o_start),
+                          (int32_t*)(w2 + o_scr), ctx->stream);
+    launch_knn_scatter(b.dpts, dcl, dts, dtc, b.T, b.tile_pts, (const int32_t*)(w2 + o_cell),
+                       (const int32_t*)(w2 + o_start), (int32_t*)(w2 + o_fill),
+                       (float4*)(w2 + o_sorted), ctx->stream);
+    launch_knn_query(dcl, dts, dtc, b.T, b.tile_pts, (const float4*)(w2 + o_sorted),
+                     (const int32_t*)(w2 + o_start), k, dout, ctx->stream);
+    CK_LAUNCH(fn);
+    if (mem == GVOX_HOST) {
+      CK(cudaMemcpyAsync(neighbors, dout, 4 * (size_t)b.n * k, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+  }
+  return GVOX_OK;
+}
+
+gvox_status gvox_estimate_covariances(gvox_ctx* ctx, const float* points, const int64_t* offsets,
+                                      int64_t count, const int32_t* neighbors, int32_t k,
+                                      float* cov, float* normals, int mem) {
+  const char* fn = "gvox_estimate_covariances";
+  if (!ctx) return fail(GVOX_ERR_INVALID, "%s: ctx is NULL", fn);
+  if (k < 1 || k > 32) return fail(GVOX_ERR_INVALID, "%s: k = %d outside [1, 32]", fn, k);
+  if (mem != GVOX_HOST && mem != GVOX_DEVICE)
+    return fail(GVOX_ERR_INVALID, "%s: mem must be GVOX_HOST or GVOX_DEVICE", fn);
+  if (count < 0 || !offsets) return fail(GVOX_ERR_INVALID, "%s: bad count / offsets", fn);
+  const int64_t n_all = count > 0 ? offsets[count] : 0;
+  if (n_all > 0 && (!neighbors || !cov || !normals)) return fail(GVOX_ERR_INVALID, "%s: NULL argument", fn);
+  if (mem == GVOX_HOST)
+    for (int64_t c = 0; c < count; ++c)
+      for (int64_t i = offsets[c]; i < offsets[c + 1]; ++i)
+        for (int j = 0; j < k; ++j) {
+          const int32_t q = neighbors[i * k + j];
+          if (q < -1 || q >= offsets[c + 1] - offsets[c])
+            return fail(GVOX_ERR_INVALID, "%s: neighbors[%lld][%d] = %d outside [-1, %lld)", fn,
+                        (long long)i, j, q, (long long)(offsets[c + 1] - offsets[c]));
+        }
+  DeviceGuard g(ctx->device);
+  Layout l1;
+  size_t o_pts = l1.add(mem == GVOX_HOST ? 12 * (size_t)n_all : 0);
+  size_t o_nb = l1.add(mem == GVOX_HOST ? 4 * (size_t)n_all * k : 0);
+  size_t o_cov = l1.add(mem == GVOX_HOST ? 24 * (size_t)n_all : 0);
+  size_t o_nrm = l1.add(mem == GVOX_HOST ? 12 * (size_t)n_all : 0);
+  size_t o_cl = l1.add(sizeof(KnnCloudDev) * (size_t)std::max<int64_t>(count, 1));
+  size_t o_ts = l1.add(4 * (size_t)(count + 1));
+  size_t o_tc = l1.add(4 * (size_t)(n_all / 256 + count + 1));
+  void* ws = nullptr;
+  gvox_status st = ws_reserve(ctx, 1, l1.size, &ws);
+  if (st) return st;
+  char* w = (char*)ws;
+  PrepBatch b;
+  st = prep_batch(fn, ctx, points, offsets, count, mem, w + o_pts, &b);
+  if (st) return st;
+  if (b.n == 0) return GVOX_OK;
+  const int32_t* dnb = neighbors;
+  float* dcov = cov;
+  float* dnrm = normals;
+  if (mem == GVOX_HOST) {
+    CK(cudaMemcpyAsync(w + o_nb, neighbors, 4 * (size_t)b.n * k, cudaMemcpyHostToDevice, ctx->stream));
+    dnb = (const int32_t*)(w + o_nb);
+    dcov = (float*)(w + o_cov);
+    dnrm = (float*)(w + o_nrm);
+  }
+  CK(cudaMemcpyAsync(w + o_cl, b.cl.data(), sizeof(KnnCloudDev) * count, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(w + o_ts, b.tstart.data(), 4 * (count + 1), cudaMemcpyHostToDevice, ctx->stream));
+  launch_tile_map((const int32_t*)(w + o_ts), count, (int32_t*)(w + o_tc), ctx->stream);
+  {
+    TimerScope ts(ctx, GVOX_TIMER_PREPROCESS);
+    launch_covariance(b.dpts, (const KnnCloudDev*)(w + o_cl), (const int32_t*)(w + o_ts),
+                      (const int32_t*)(w + o_tc), b.T, b.tile_pts, dnb, k, dcov, dnrm, ctx->stream);
+  }
+  CK_LAUNCH(fn);
+  if (mem == GVOX_HOST) {
+    CK(cudaMemcpyAsync(cov, dcov, 24 * (size_t)b.n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(normals, dnrm, 12 * (size_t)b.n, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   }
   return GVOX_OK;
