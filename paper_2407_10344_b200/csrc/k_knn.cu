@@ -131,51 +131,75 @@ __global__ void __launch_bounds__(kKnnThreads)
       bi[j] = INT32_MAX;
     }
     int found = 0;
-    const int64_t n = cd.n;
+    double kth = __longlong_as_double(0x7ff0000000000000ll);  // (bd, bi)[k - 1]: the insertion gate
+    int32_t kidx = INT32_MAX;
+    // slack for the cell assignment's rounding (floor((x - lo) / s) in fp64)
+    const double slack = 1e-9 * (fabs(cd.lo[0]) + fabs(cd.lo[1]) + fabs(cd.lo[2]) +
+                                 cd.s * (cd.dim[0] + cd.dim[1] + cd.dim[2]) + 1.0);
+    const double s = cd.s;
     for (int R = 0;; ++R) {
       const int32_t x0 = max(cx - R, 0), x1 = min(cx + R, cd.dim[0] - 1);
       const int32_t y0 = max(cy - R, 0), y1 = min(cy + R, cd.dim[1] - 1);
       const int32_t z0 = max(cz - R, 0), z1 = min(cz + R, cd.dim[2] - 1);
-      for (int32_t x = x0; x <= x1; ++x)
-        for (int32_t y = y0; y <= y1; ++y) {
-          const bool face = (x == cx - R) | (x == cx + R) | (y == cy - R) | (y == cy + R);
-          // cells at Chebyshev distance exactly R: all z on an x/y face, else z = cz +- R
-          const int32_t zstep = face ? 1 : 2 * R;
-          for (int32_t z = face ? z0 : cz - R; z <= (face ? z1 : cz + R); z += (zstep > 0 ? zstep : 1)) {
-            if (z < z0 || z > z1) continue;
-            const int32_t cell = cd.cell0 + (x * cd.dim[1] + y) * cd.dim[2] + z;
-            const int32_t s0 = __ldg(cell_start + cell), s1 = __ldg(cell_start + cell + 1);
-            for (int32_t s = s0; s < s1; ++s) {
-              const float4 p = __ldg(sorted + s);
-              const double d2 = sq_dist_pinned(q.x, q.y, q.z, p.x, p.y, p.z);
-              const int32_t pi = __float_as_int(p.w);
-              if (d2 < bd[MAXK - 1] || (d2 == bd[MAXK - 1] && pi < bi[MAXK - 1])) {
-                // insertion into the (d2, index)-sorted list (registers: unrolled)
-                double cd2 = d2;
-                int32_t ci = pi;
+      // the cells of one (x, y) column are consecutive in the grid and so are
+      // their points in `sorted`: a column's new cells are one or two runs
+      auto scan_run = [&](int32_t c0, int32_t c1) {  // cells [c0, c1] of one column
+        const int32_t s0 = __ldg(cell_start + c0), s1 = __ldg(cell_start + c1 + 1);
+        for (int32_t si = s0; si < s1; ++si) {
+          const float4 p = __ldg(sorted + si);
+          const double d2 = sq_dist_pinned(q.x, q.y, q.z, p.x, p.y, p.z);
+          const int32_t pi = __float_as_int(p.w);
+          ++found;
+          if (d2 < kth || (d2 == kth && pi < kidx)) {
+            // insertion into the (d2, index)-sorted list (registers: unrolled)
+            double cd2 = d2;
+            int32_t ci = pi;
 #pragma unroll
-                for (int j = 0; j < MAXK; ++j) {
-                  const bool lt = cd2 < bd[j] || (cd2 == bd[j] && ci < bi[j]);
-                  const double td = bd[j];
-                  const int32_t ti = bi[j];
-                  bd[j] = lt ? cd2 : td;
-                  bi[j] = lt ? ci : ti;
-                  cd2 = lt ? td : cd2;
-                  ci = lt ? ti : ci;
-                }
-                ++found;
-              }
+            for (int j = 0; j < MAXK; ++j) {
+              const bool lt = cd2 < bd[j] || (cd2 == bd[j] && ci < bi[j]);
+              const double td = bd[j];
+              const int32_t ti = bi[j];
+              bd[j] = lt ? cd2 : td;
+              bi[j] = lt ? ci : ti;
+              cd2 = lt ? td : cd2;
+              ci = lt ? ti : ci;
             }
+#pragma unroll
+            for (int j = 0; j < MAXK; ++j)
+              if (j == k - 1) {
+                kth = bd[j];
+                kidx = bi[j];
+              }
           }
         }
+      };
+      for (int32_t x = x0; x <= x1; ++x) {
+        const double bx0 = cd.lo[0] + (double)x * s;
+        const double ex = fmax(fmax(bx0 - (double)q.x, (double)q.x - (bx0 + s)), 0.0);
+        for (int32_t y = y0; y <= y1; ++y) {
+          const bool face = (x == cx - R) | (x == cx + R) | (y == cy - R) | (y == cy + R);
+          if (found >= k) {  // exact pruning of the whole column by its xy distance
+            const double by0 = cd.lo[1] + (double)y * s;
+            const double ey = fmax(fmax(by0 - (double)q.y, (double)q.y - (by0 + s)), 0.0);
+            const double em = fmax(sqrt(ex * ex + ey * ey) - slack, 0.0);
+            if (em * em > kth * (1.0 + 1e-9)) continue;
+          }
+          const int32_t col = cd.cell0 + (x * cd.dim[1] + y) * cd.dim[2];
+          if (face) {
+            scan_run(col + z0, col + z1);
+          } else {  // interior column: only z = cz - R and cz + R are new
+            if (cz - R >= z0) scan_run(col + cz - R, col + cz - R);
+            if (cz + R <= z1) scan_run(col + cz + R, col + cz + R);
+          }
+        }
+      }
       // every unsearched point lies beyond the searched cube's faces that are
       // inside the grid; stop once the k-th distance is certainly below that
       const bool all = x0 == 0 && y0 == 0 && z0 == 0 && x1 == cd.dim[0] - 1 &&
                        y1 == cd.dim[1] - 1 && z1 == cd.dim[2] - 1;
       if (all) break;
-      if (found >= k || found >= n) {
+      if (found >= k) {
         double b = __longlong_as_double(0x7ff0000000000000ll);
-        const double s = cd.s;
         const int32_t cc[3] = {cx, cy, cz};
         const float qq[3] = {q.x, q.y, q.z};
 #pragma unroll
@@ -183,12 +207,7 @@ __global__ void __launch_bounds__(kKnnThreads)
           if (cc[a] - R > 0) b = fmin(b, (double)qq[a] - (cd.lo[a] + (double)(cc[a] - R) * s));
           if (cc[a] + R < cd.dim[a] - 1) b = fmin(b, cd.lo[a] + (double)(cc[a] + R + 1) * s - (double)qq[a]);
         }
-        double kth = bd[0];
-#pragma unroll
-        for (int j = 0; j < MAXK; ++j)
-          if (j == k - 1) kth = bd[j];
-        // slack for the cell assignment's rounding (floor((x - lo) / s) in fp64)
-        b -= 1e-9 * (fabs(cd.lo[0]) + fabs(cd.lo[1]) + fabs(cd.lo[2]) + s * (cd.dim[0] + cd.dim[1] + cd.dim[2]) + 1.0);
+        b -= slack;
         if (b > 0.0 && kth < b * b * (1.0 - 1e-9)) break;
       }
     }

@@ -23,7 +23,7 @@ def main():
     ctx = gv.Context(0)
     sc = synth.make("C3")
     reps = int(os.environ.get("REPS", "20"))
-    cell = float(os.environ.get("CELL", "1.0"))
+    cell = float(os.environ.get("CELL", "1.5"))
     for name, ncl in (("frame", 1), ("C3-batch", sc.num_clouds)):
         off = sc.offsets[: ncl + 1]
         pts = torch.from_numpy(sc.mu[: off[-1]]).cuda()
