@@ -137,7 +137,8 @@ enum {
   GVOX_TIMER_REDUCE = 3,    /* per-factor reduction / expansion kernel */
   GVOX_TIMER_REGISTER = 4,  /* one gvox_register_batch graph launch (all iterations) */
   GVOX_TIMER_PREPROCESS = 5, /* k-NN (count, scan, scatter, query) / covariance kernels */
-  GVOX_TIMER_COUNT = 6
+  GVOX_TIMER_SOLVE = 6,     /* gvox_solve_global: expand, assemble, PCG, scatter */
+  GVOX_TIMER_COUNT = 7
 };
 gvox_status gvox_ctx_enable_timing(gvox_ctx* ctx, int enable);
 gvox_status gvox_ctx_timing(gvox_ctx* ctx, double* ms, int64_t* launches, int reset);
@@ -400,6 +401,49 @@ gvox_status gvox_register_batch(gvox_ctx* ctx, const gvox_cloud* const* clouds,
                                 const double* poses, int64_t num_poses,
                                 const gvox_register_params* params, double* poses_out,
                                 gvox_register_result* results, double* error_history, int mem);
+
+/* ---------------------------------------------------------- global system */
+
+/* One Gauss-Newton step of a whole factor graph of matching cost factors
+   (global mapping; the solver the paper runs on the CPU, P:814;
+   SURVEY §8(f) NEXT-4).  Poses with fixed[v] != 0 are constants (at least one
+   is needed to remove the 6-dof gauge freedom, unless lambda > 0); the others
+   are the variables, ordered by pose index.  With every factor's full blocks
+   (H_ii, H_ij, H_jj, b_i, b_j; from its compact record `accum` and the poses,
+   as gvox_expand) scattered onto its variable poses,
+       H = sum_f scatter(H_f) + lambda I,   b = sum_f scatter(b_f),
+   the step solves H delta = -b by block-Jacobi preconditioned conjugate
+   gradients in fp64 until |r| <= tol |b| or max_iterations (the PCG loop runs
+   on the device as a CUDA-graph WHILE node).  delta [num_poses x 6]
+   (rotation-first, right perturbation: T_v <- T_v Exp(delta_v); 0 for fixed
+   poses).  Every block and right-hand-side entry is summed in ascending
+   factor order: results are bitwise reproducible.
+   factors, poses, fixed, params: host.  accum [num_factors] and delta live in
+   `mem`; H_dense [(6V)^2] and b_dense [6V] (optional, HOST, row-major, V =
+   variables) receive the assembled system for inspection.
+   Errors: GVOX_ERR_INVALID for bad indices / sizes, no fixed pose with
+   lambda = 0, or a diagonal block that is not positive definite. */
+typedef struct gvox_global_params {
+  int32_t max_iterations; /* PCG iterations, >= 1 */
+  int32_t reserved;
+  double tol;             /* relative residual, >= 0 */
+  double lambda;          /* >= 0, added to the diagonal */
+} gvox_global_params;
+
+typedef struct gvox_global_result {
+  int32_t iterations;     /* PCG iterations run */
+  int32_t converged;      /* |r| <= tol |b| */
+  int32_t num_variables;
+  int32_t num_blocks;     /* stored 6x6 blocks (both triangles) */
+  double residual_initial; /* |b| */
+  double residual_final;   /* |r| (recurrence) */
+} gvox_global_result;
+
+gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t num_factors,
+                              const gvox_factor_accum* accum, const double* poses,
+                              int64_t num_poses, const uint8_t* fixed,
+                              const gvox_global_params* params, double* delta, double* H_dense,
+                              double* b_dense, gvox_global_result* result, int mem);
 
 /* ------------------------------------------------------------- utilities */
 

@@ -17,7 +17,7 @@ GVOX_HOST = 0
 GVOX_DEVICE = 1
 F_VALIDATE_SURFACE = 1
 F_ERROR_ONLY = 2
-TIMERS = ("build", "overlap", "linearize", "reduce", "register", "preprocess")
+TIMERS = ("build", "overlap", "linearize", "reduce", "register", "preprocess", "solve")
 
 STATUS = {0: "GVOX_OK", 1: "GVOX_ERR_INVALID", 2: "GVOX_ERR_RANGE", 3: "GVOX_ERR_CUDA",
           4: "GVOX_ERR_NOMEM"}
@@ -42,6 +42,11 @@ REGISTER_RESULT_DTYPE = np.dtype([("status", "<i4"), ("iterations", "<i4"), ("in
 UNION_QUERY_DTYPE = np.dtype([("source_cloud", "<i4"), ("pose_i", "<i4"), ("first", "<i4"),
                               ("count", "<i4")])
 UNION_MEMBER_DTYPE = np.dtype([("target_map", "<i4"), ("pose_j", "<i4")])
+GLOBAL_PARAMS_DTYPE = np.dtype([("max_iterations", "<i4"), ("reserved", "<i4"), ("tol", "<f8"),
+                                ("lambda", "<f8")])
+GLOBAL_RESULT_DTYPE = np.dtype([("iterations", "<i4"), ("converged", "<i4"), ("num_variables", "<i4"),
+                                ("num_blocks", "<i4"), ("residual_initial", "<f8"),
+                                ("residual_final", "<f8")])
 REG_FIXED, REG_MAX_ITER, REG_CONVERGED, REG_SINGULAR = 0, 1, 2, 3
 
 # exported symbols (tests check every one declared in include/gvox.h is here)
@@ -53,7 +58,7 @@ SYMBOLS = [
     "gvox_voxelmap_export", "gvox_voxelmap_lookup", "gvox_map_destroy",
     "gvox_overlap", "gvox_overlap_select", "gvox_linearize_batch", "gvox_linearize_batch_accum", "gvox_expand",
     "gvox_register_batch", "gvox_overlap_union", "gvox_keyframe_update", "gvox_knn",
-    "gvox_estimate_covariances",
+    "gvox_estimate_covariances", "gvox_solve_global",
     "gvox_status_string", "gvox_last_error", "gvox_launch_count", "gvox_version",
 ]
 
@@ -99,6 +104,7 @@ def lib():
         "gvox_linearize_batch": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32, P]),
         "gvox_linearize_batch_accum": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32]),
         "gvox_expand": (I32, [P, P, I64, P, I64, P, P, I32]),
+        "gvox_solve_global": (I32, [P, P, I64, P, P, I64, P, P, P, P, P, P, I32]),
         "gvox_knn": (I32, [P, P, P, I64, I32, D, P, I32]),
         "gvox_estimate_covariances": (I32, [P, P, P, I64, P, I32, P, P, I32]),
         "gvox_overlap_union": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I64, I32, P, I32]),

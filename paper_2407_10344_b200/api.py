@@ -15,7 +15,7 @@ import numpy as np
 
 from ._lib import (FACTOR_ACCUM_DTYPE, FACTOR_DTYPE, GVOX_DEVICE, GVOX_HOST, LINEAR_FACTOR_DTYPE,
                    PAIR_DTYPE, REGISTER_PARAMS_DTYPE, REGISTER_RESULT_DTYPE, UNION_MEMBER_DTYPE,
-                   UNION_QUERY_DTYPE, check, lib)
+                   UNION_QUERY_DTYPE, GLOBAL_PARAMS_DTYPE, GLOBAL_RESULT_DTYPE, check, lib)
 
 
 def _torch():
@@ -459,6 +459,37 @@ class KeyframeList:
         self.frames = [ks[a] for a in range(K) if keep[a]]
         self.o = o[np.ix_(keep, keep)]
         return True, removed
+
+
+def solve_global(ctx: Context, factors, accum, poses, fixed, max_iterations: int = 500,
+                 tol: float = 1e-10, lam: float = 0.0, dense: bool = False):
+    """gvox_solve_global: one Gauss-Newton step of the whole factor graph.
+    accum: compact records (numpy FACTOR_ACCUM_DTYPE, or a uint8 CUDA tensor
+    [F, 288] -> delta is then a CUDA tensor).  Returns (delta [P,6], result,
+    H [6V,6V] or None, b [6V] or None)."""
+    factors = as_factors(factors)
+    poses = as_poses(poses)
+    NPz = poses.shape[0]
+    fx = np.ascontiguousarray(np.asarray(fixed, np.uint8).reshape(-1))
+    assert fx.size == NPz
+    prm = np.zeros(1, GLOBAL_PARAMS_DTYPE)
+    prm["max_iterations"], prm["tol"], prm["lambda"] = int(max_iterations), float(tol), float(lam)
+    res = np.zeros(1, GLOBAL_RESULT_DTYPE)
+    if _is_cuda_tensor(accum):
+        delta = _torch().empty((NPz, 6), dtype=_torch().float64, device=accum.device)
+        mem = GVOX_DEVICE
+    else:
+        accum = np.ascontiguousarray(accum)
+        delta = np.zeros((NPz, 6), np.float64)
+        mem = GVOX_HOST
+    V = int(NPz - np.count_nonzero(fx))
+    H = np.zeros((6 * V, 6 * V)) if dense else None
+    b = np.zeros(6 * V) if dense else None
+    check(lib().gvox_solve_global(ctx.handle, _ptr(factors)[0], factors.shape[0], _ptr(accum)[0],
+                                  _ptr(poses)[0], NPz, _ptr(fx)[0], _ptr(prm)[0], _ptr(delta)[0],
+                                  None if H is None else _ptr(H)[0], None if b is None else _ptr(b)[0],
+                                  _ptr(res)[0], mem))
+    return delta, res[0], H, b
 
 
 def register_batch(ctx: Context, clouds, maps, factors, poses, max_iterations: int = 10,

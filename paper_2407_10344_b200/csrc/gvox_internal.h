@@ -316,6 +316,25 @@ void launch_gn_step(const RegProblem* problems, int32_t num_problems, const int3
                     double* history, int64_t num_poses, cudaGraphConditionalHandle cond,
                     cudaStream_t stream);
 
+// global system (k_global.cu): BSR assembly + block-Jacobi PCG
+struct PcgState {
+  double rz, r0, res;
+  int32_t iter, done;
+};
+void launch_assemble(const gvox_linear_factor* rec, const int32_t* contrib_start,
+                     const int32_t* contrib, int64_t num_blocks, const uint8_t* is_diag,
+                     double lambda, double* blocks, const int32_t* g_start, const int32_t* g_list,
+                     int64_t num_vars, double* rhs, const int32_t* diag_block, double* minv,
+                     int32_t* bad, cudaStream_t stream);
+void launch_pcg_init(const double* rhs, const double* minv, int64_t num_vars, double* x, double* r,
+                     double* z, double* p, PcgState* st, cudaStream_t stream);
+void launch_pcg_iteration(const double* blocks, const int32_t* row_start, const int32_t* col,
+                          int64_t num_vars, const double* minv, double* x, double* r, double* z,
+                          double* p, double* q, double* pq_part, PcgState* st, int32_t max_iter,
+                          double tol, cudaGraphConditionalHandle cond, cudaStream_t stream);
+void launch_scatter_delta(const double* x, const int32_t* var_of_pose, int64_t num_poses,
+                          double* delta, cudaStream_t stream);
+
 // tile -> owning item (factor or pair) table from the tile prefix sums
 void launch_tile_map(const int32_t* tile_start, int64_t num_items, int32_t* tile_owner,
                      cudaStream_t stream);

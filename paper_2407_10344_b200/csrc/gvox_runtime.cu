@@ -1903,6 +1903,235 @@ gvox_status gvox_register_batch(gvox_ctx* ctx, const gvox_cloud* const* clouds,
   return GVOX_OK;
 }
 
+// ------------------------------------------------------------ global system
+gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t num_factors,
+                              const gvox_factor_accum* accum, const double* poses,
+                              int64_t num_poses, const uint8_t* fixed,
+                              const gvox_global_params* params, double* delta, double* H_dense,
+                              double* b_dense, gvox_global_result* result, int mem) {
+  const char* fn = "gvox_solve_global";
+  if (!ctx) return fail(GVOX_ERR_INVALID, "%s: ctx is NULL", fn);
+  if (num_factors < 0 || num_poses < 0) return fail(GVOX_ERR_INVALID, "%s: negative size", fn);
+  if (!params || !fixed || !delta || !result || (num_poses > 0 && !poses) ||
+      (num_factors > 0 && (!factors || !accum)))
+    return fail(GVOX_ERR_INVALID, "%s: NULL argument", fn);
+  if (mem != GVOX_HOST && mem != GVOX_DEVICE)
+    return fail(GVOX_ERR_INVALID, "%s: mem must be GVOX_HOST or GVOX_DEVICE", fn);
+  const gvox_global_params P = *params;
+  if (P.max_iterations < 1 || !(P.tol >= 0.0) || !(P.lambda >= 0.0) || !std::isfinite(P.lambda))
+    return fail(GVOX_ERR_INVALID, "%s: need max_iterations >= 1, tol >= 0, finite lambda >= 0", fn);
+  gvox_status st = validate_factors(fn, nullptr, 0, nullptr, 0, factors, num_factors, poses, num_poses);
+  if (st) return st;
+  // ---- variables and the block pattern (host)
+  std::vector<int32_t> var_of(num_poses, -1);
+  int32_t V = 0;
+  bool any_fixed = false;
+  for (int64_t i = 0; i < num_poses; ++i) {
+    if (fixed[i]) any_fixed = true;
+    else var_of[i] = V++;
+  }
+  std::memset(result, 0, sizeof(*result));
+  result->num_variables = V;
+  if (V > 0 && !any_fixed && P.lambda == 0.0)
+    return fail(GVOX_ERR_INVALID, "%s: no fixed pose and lambda = 0 (the gauge is free)", fn);
+  struct Ent {
+    int32_t row, col, code;
+  };
+  std::vector<Ent> ent;
+  ent.reserve(4 * num_factors + V);
+  for (int32_t v = 0; v < V; ++v) ent.push_back({v, v, -1});  // every variable has its diagonal block
+  std::vector<std::vector<int32_t>> g(V);
+  for (int64_t f = 0; f < num_factors; ++f) {
+    const int32_t vi = var_of[factors[f].pose_i], vj = var_of[factors[f].pose_j];
+    const int32_t c = (int32_t)(f << 2);
+    if (vi >= 0) {
+      ent.push_back({vi, vi, c | 0});
+      g[vi].push_back((int32_t)(f << 1) | 0);
+    }
+    if (vi >= 0 && vj >= 0) {
+      ent.push_back({vi, vj, c | 1});
+      ent.push_back({vj, vi, c | 2});
+    }
+    if (vj >= 0) {
+      ent.push_back({vj, vj, c | 3});
+      g[vj].push_back((int32_t)(f << 1) | 1);
+    }
+  }
+  if (num_factors > (1 << 28)) return fail(GVOX_ERR_INVALID, "%s: too many factors", fn);
+  std::stable_sort(ent.begin(), ent.end(), [](const Ent& a, const Ent& b) {
+    return a.row != b.row ? a.row < b.row : a.col < b.col;
+  });
+  std::vector<int32_t> row_start(V + 1, 0), col, cstart, contrib, diag_block(V, -1);
+  std::vector<uint8_t> is_diag;
+  for (size_t k = 0; k < ent.size();) {
+    size_t e = k;
+    const int32_t nb = (int32_t)col.size();
+    col.push_back(ent[k].col);
+    is_diag.push_back(ent[k].row == ent[k].col);
+    if (ent[k].row == ent[k].col) diag_block[ent[k].row] = nb;
+    cstart.push_back((int32_t)contrib.size());
+    while (e < ent.size() && ent[e].row == ent[k].row && ent[e].col == ent[k].col) {
+      if (ent[e].code >= 0) contrib.push_back(ent[e].code);
+      ++e;
+    }
+    row_start[ent[k].row + 1] = nb + 1;
+    k = e;
+  }
+  for (int32_t v = 0; v < V; ++v) row_start[v + 1] = std::max(row_start[v + 1], row_start[v]);
+  const int64_t NB = (int64_t)col.size();
+  cstart.push_back((int32_t)contrib.size());
+  std::vector<int32_t> gstart(V + 1, 0), glist;
+  for (int32_t v = 0; v < V; ++v) {
+    glist.insert(glist.end(), g[v].begin(), g[v].end());
+    gstart[v + 1] = (int32_t)glist.size();
+  }
+  result->num_blocks = (int32_t)NB;
+  DeviceGuard dg(ctx->device);
+  // ---- one input block
+  std::vector<FactorDev> fdev(num_factors);
+  for (int64_t f = 0; f < num_factors; ++f)
+    fdev[f] = FactorDev{factors[f].source_cloud, factors[f].target_map, factors[f].pose_i,
+                        factors[f].pose_j, factors[f].flags, 0, 0};
+  Layout lay;
+  size_t o_pose = lay.add(96 * num_poses);
+  size_t o_fac = lay.add(sizeof(FactorDev) * num_factors);
+  size_t o_rs = lay.add(4 * row_start.size());
+  size_t o_col = lay.add(4 * col.size());
+  size_t o_cs = lay.add(4 * cstart.size());
+  size_t o_ct = lay.add(4 * std::max<size_t>(contrib.size(), 1));
+  size_t o_gs = lay.add(4 * gstart.size());
+  size_t o_gl = lay.add(4 * std::max<size_t>(glist.size(), 1));
+  size_t o_dg = lay.add(4 * std::max<int32_t>(V, 1));
+  size_t o_isd = lay.add(std::max<size_t>(is_diag.size(), 1));
+  size_t o_vo = lay.add(4 * std::max<int64_t>(num_poses, 1));
+  size_t o_acc = lay.add(mem == GVOX_HOST ? sizeof(gvox_factor_accum) * num_factors : 0);
+  const size_t in_bytes = lay.size;
+  void* pin = nullptr;
+  st = pin_reserve(ctx, in_bytes, &pin);
+  if (st) return st;
+  char* hp = (char*)pin;
+  if (num_poses) std::memcpy(hp + o_pose, poses, 96 * num_poses);
+  if (num_factors) std::memcpy(hp + o_fac, fdev.data(), sizeof(FactorDev) * num_factors);
+  std::memcpy(hp + o_rs, row_start.data(), 4 * row_start.size());
+  if (!col.empty()) std::memcpy(hp + o_col, col.data(), 4 * col.size());
+  std::memcpy(hp + o_cs, cstart.data(), 4 * cstart.size());
+  if (!contrib.empty()) std::memcpy(hp + o_ct, contrib.data(), 4 * contrib.size());
+  std::memcpy(hp + o_gs, gstart.data(), 4 * gstart.size());
+  if (!glist.empty()) std::memcpy(hp + o_gl, glist.data(), 4 * glist.size());
+  if (V) std::memcpy(hp + o_dg, diag_block.data(), 4 * V);
+  if (!is_diag.empty()) std::memcpy(hp + o_isd, is_diag.data(), is_diag.size());
+  if (num_poses) std::memcpy(hp + o_vo, var_of.data(), 4 * num_poses);
+  if (mem == GVOX_HOST && num_factors) std::memcpy(hp + o_acc, accum, sizeof(gvox_factor_accum) * num_factors);
+  Layout wl;
+  size_t o_in = wl.add(in_bytes);
+  size_t o_rec = wl.add(sizeof(gvox_linear_factor) * std::max<int64_t>(num_factors, 1));
+  size_t o_blk = wl.add(8 * 36 * std::max<int64_t>(NB, 1));
+  const int64_t n6 = 6 * (int64_t)std::max<int32_t>(V, 1);
+  size_t o_rhs = wl.add(8 * n6), o_x = wl.add(8 * n6), o_r = wl.add(8 * n6), o_z = wl.add(8 * n6);
+  size_t o_p = wl.add(8 * n6), o_q = wl.add(8 * n6), o_pq = wl.add(8 * (n6 / 6));
+  size_t o_minv = wl.add(8 * 36 * (n6 / 6));
+  size_t o_st = wl.add(sizeof(PcgState) + 16);
+  size_t o_dl = wl.add(mem == GVOX_HOST ? 48 * (size_t)std::max<int64_t>(num_poses, 1) : 0);
+  void* ws = nullptr;
+  st = ws_reserve(ctx, 0, wl.size, &ws);
+  if (st) return st;
+  char* wb = (char*)ws;
+  char* din = wb + o_in;
+  st = h2d_block(ctx, din, hp, in_bytes);
+  if (st) return st;
+  int32_t* dbad = (int32_t*)(wb + o_st + sizeof(PcgState));
+  PcgState* dst = (PcgState*)(wb + o_st);
+  CK(cudaMemsetAsync(wb + o_st, 0, sizeof(PcgState) + 16, ctx->stream));
+  const gvox_factor_accum* dacc = mem == GVOX_HOST ? (const gvox_factor_accum*)(din + o_acc) : accum;
+  double* ddelta = mem == GVOX_DEVICE ? delta : (double*)(wb + o_dl);
+  {
+    TimerScope ts(ctx, GVOX_TIMER_SOLVE);
+    launch_expand((const FactorDev*)(din + o_fac), num_factors, (const double*)(din + o_pose), dacc,
+                  (gvox_linear_factor*)(wb + o_rec), ctx->stream);
+    launch_assemble((const gvox_linear_factor*)(wb + o_rec), (const int32_t*)(din + o_cs),
+                    (const int32_t*)(din + o_ct), NB, (const uint8_t*)(din + o_isd), P.lambda,
+                    (double*)(wb + o_blk), (const int32_t*)(din + o_gs), (const int32_t*)(din + o_gl),
+                    V, (double*)(wb + o_rhs), (const int32_t*)(din + o_dg), (double*)(wb + o_minv),
+                    dbad, ctx->stream);
+    CK_LAUNCH("global assemble");
+    if (V > 0) {
+      launch_pcg_init((const double*)(wb + o_rhs), (const double*)(wb + o_minv), V, (double*)(wb + o_x),
+                      (double*)(wb + o_r), (double*)(wb + o_z), (double*)(wb + o_p), dst, ctx->stream);
+      if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+      cudaGraph_t graph = nullptr;
+      cudaGraphExec_t exec = nullptr;
+      CK(cudaGraphCreate(&graph, 0));
+      std::unique_ptr<CUgraph_st, void (*)(cudaGraph_t)> guard(graph, [](cudaGraph_t gr) { cudaGraphDestroy(gr); });
+      cudaGraphConditionalHandle cond;
+      CK(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = cond;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+      CK(cudaStreamBeginCaptureToGraph(ctx->cap_stream, cp.conditional.phGraph_out[0], nullptr, nullptr,
+                                       0, cudaStreamCaptureModeThreadLocal));
+      launch_pcg_iteration((const double*)(wb + o_blk), (const int32_t*)(din + o_rs),
+                           (const int32_t*)(din + o_col), V, (const double*)(wb + o_minv),
+                           (double*)(wb + o_x), (double*)(wb + o_r), (double*)(wb + o_z),
+                           (double*)(wb + o_p), (double*)(wb + o_q), (double*)(wb + o_pq), dst,
+                           P.max_iterations, P.tol, cond, ctx->cap_stream);
+      cudaGraph_t captured = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &captured);
+      if (ce != cudaSuccess) return cuda_fail(ce, "PCG loop capture");
+      CK(cudaGraphInstantiate(&exec, graph, 0));
+      cudaError_t le = cudaGraphLaunch(exec, ctx->stream);
+      cudaGraphExecDestroy(exec);
+      if (le != cudaSuccess) return cuda_fail(le, "PCG loop launch");
+      note_launch();
+    }
+    if (num_poses > 0) {
+      if (V > 0) {
+        launch_scatter_delta((const double*)(wb + o_x), (const int32_t*)(din + o_vo), num_poses,
+                             ddelta, ctx->stream);
+      } else {
+        CK(cudaMemsetAsync(ddelta, 0, 48 * num_poses, ctx->stream));
+      }
+    }
+  }
+  CK_LAUNCH(fn);
+  // ---- results (always synchronizes: the result struct is host memory)
+  PcgState hs{};
+  int32_t hbad = 0;
+  CK(cudaMemcpyAsync(&hs, dst, sizeof(PcgState), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&hbad, dbad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (mem == GVOX_HOST && num_poses)
+    CK(cudaMemcpyAsync(delta, ddelta, 48 * num_poses, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<double> hblk, hrhs;
+  if (H_dense && V > 0) {
+    hblk.resize(36 * NB);
+    CK(cudaMemcpyAsync(hblk.data(), wb + o_blk, 8 * 36 * NB, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (b_dense && V > 0) {
+    hrhs.resize(6 * V);
+    CK(cudaMemcpyAsync(hrhs.data(), wb + o_rhs, 8 * 6 * V, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hbad) return fail(GVOX_ERR_INVALID, "%s: a diagonal block is not positive definite", fn);
+  result->iterations = hs.iter;
+  result->residual_initial = hs.r0;
+  result->residual_final = hs.res;
+  result->converged = V == 0 || hs.res <= P.tol * hs.r0;
+  if (H_dense && V > 0) {
+    const int64_t D = 6 * (int64_t)V;
+    std::memset(H_dense, 0, 8 * D * D);
+    for (int32_t v = 0; v < V; ++v)
+      for (int32_t b = row_start[v]; b < row_start[v + 1]; ++b)
+        for (int e = 0; e < 36; ++e)
+          H_dense[(6 * (int64_t)v + e / 6) * D + 6 * (int64_t)col[b] + e % 6] = hblk[36 * b + e];
+  }
+  if (b_dense && V > 0)
+    for (int64_t t = 0; t < 6 * (int64_t)V; ++t) b_dense[t] = -hrhs[t];
+  return GVOX_OK;
+}
+
 // ------------------------------------------------------------------ utilities
 const char* gvox_status_string(gvox_status s) {
   switch (s) {

@@ -1,0 +1,297 @@
+// k_global.cu -- global Gauss-Newton system of a factor graph of matching cost
+// factors and its GPU solve (global mapping P:391, the
+// CPU solver's share of the optimisation P:814).
+//
+//   H = sum_f scatter(H_f),  b = sum_f scatter(b_f)  over the VARIABLE poses,
+//   (H + lambda I) delta = -b  by block-Jacobi preconditioned conjugate
+//   gradients in fp64.
+//
+// Layout: block-sparse rows (BSR, 6x6 fp64 blocks, both (i, j) and (j, i)
+// stored, columns ascending per row).  Every block and every right-hand-side
+// entry is summed by one warp / thread over its contribution list in
+// ascending factor order: the system is bitwise deterministic.  The PCG loop
+// runs as the body of a CUDA graph WHILE node (k_spmv_dot -> k_pcg_update, the
+// latter sets the condition), like the registration loop.
+#include <cuda_runtime.h>
+
+#include "k_common.cuh"
+
+namespace gvox {
+namespace {
+
+constexpr int kUpdThreads = 1024;
+
+// one warp per block: sum its contributions (factor, kind) in order
+__global__ void k_assemble_blocks(const gvox_linear_factor* __restrict__ rec,
+                                  const int32_t* __restrict__ contrib_start,
+                                  const int32_t* __restrict__ contrib, int64_t num_blocks,
+                                  const uint8_t* __restrict__ is_diag, double lambda,
+                                  double* __restrict__ blocks) {
+  const int lane = threadIdx.x & 31;
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (b >= num_blocks) return;
+  for (int e = lane; e < 36; e += 32) {
+    double s = 0.0;
+    for (int32_t c = contrib_start[b]; c < contrib_start[b + 1]; ++c) {
+      const int32_t v = contrib[c];
+      const int32_t f = v >> 2, kind = v & 3;
+      const gvox_linear_factor& r = rec[f];
+      const int rr = e / 6, cc = e % 6;
+      s += kind == 0 ? r.H_ii[e] : kind == 1 ? r.H_ij[e] : kind == 2 ? r.H_ij[cc * 6 + rr] : r.H_jj[e];
+    }
+    if (is_diag[b] && (e % 7) == 0) s += lambda;
+    blocks[36 * b + e] = s;
+  }
+}
+
+// one thread per (variable, component): rhs = -sum of the factors' b_i / b_j
+__global__ void k_assemble_rhs(const gvox_linear_factor* __restrict__ rec,
+                               const int32_t* __restrict__ g_start, const int32_t* __restrict__ g_list,
+                               int64_t num_vars, double* __restrict__ rhs) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 6 * num_vars) return;
+  const int64_t v = t / 6;
+  const int e = (int)(t % 6);
+  double s = 0.0;
+  for (int32_t c = g_start[v]; c < g_start[v + 1]; ++c) {
+    const int32_t x = g_list[c];
+    const gvox_linear_factor& r = rec[x >> 1];
+    s += (x & 1) ? r.b_j[e] : r.b_i[e];
+  }
+  rhs[t] = -s;
+}
+
+// block-Jacobi preconditioner: Minv_v = (diag block)^-1 by Cholesky (fp64)
+__global__ void k_block_jacobi(const double* __restrict__ blocks, const int32_t* __restrict__ diag_block,
+                               int64_t num_vars, double* __restrict__ minv, int32_t* __restrict__ bad) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= num_vars) return;
+  double L[36];
+  const double* A = blocks + 36 * (int64_t)diag_block[v];
+  for (int i = 0; i < 36; ++i) L[i] = A[i];
+  for (int j = 0; j < 6; ++j) {
+    double d = L[j * 6 + j];
+    for (int k = 0; k < j; ++k) d -= L[j * 6 + k] * L[j * 6 + k];
+    if (!(d > 0.0) || !isfinite(d)) {
+      atomicOr(bad, 1);
+      for (int i = 0; i < 36; ++i) minv[36 * v + i] = (i % 7 == 0) ? 1.0 : 0.0;
+      return;
+    }
+    const double ljj = sqrt(d);
+    L[j * 6 + j] = ljj;
+    for (int i = j + 1; i < 6; ++i) {
+      double s = L[i * 6 + j];
+      for (int k = 0; k < j; ++k) s -= L[i * 6 + k] * L[j * 6 + k];
+      L[i * 6 + j] = s / ljj;
+    }
+  }
+  // columns of the inverse: solve L L^T x = e_c
+  for (int c = 0; c < 6; ++c) {
+    double y[6], x[6];
+    for (int i = 0; i < 6; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= L[i * 6 + k] * y[k];
+      y[i] = s / L[i * 6 + i];
+    }
+    for (int i = 5; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < 6; ++k) s -= L[k * 6 + i] * x[k];
+      x[i] = s / L[i * 6 + i];
+    }
+    for (int i = 0; i < 6; ++i) minv[36 * v + i * 6 + c] = x[i];
+  }
+}
+
+// deterministic block-wide sum (fixed strided order, then a fixed tree)
+__device__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (w == 0) {
+    s = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[32] = s;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+__device__ inline void precond(const double* __restrict__ minv, const double* __restrict__ r,
+                               double* __restrict__ z, int64_t n6) {
+  for (int64_t t = threadIdx.x; t < n6; t += blockDim.x) {
+    const int64_t v = t / 6;
+    const int i = (int)(t % 6);
+    double s = 0.0;
+    for (int k = 0; k < 6; ++k) s += minv[36 * v + i * 6 + k] * r[6 * v + k];
+    z[t] = s;
+  }
+}
+
+// PCG start: x = 0, r = rhs, z = M^-1 r, p = z, rz = r.z, r0 = |r|
+__global__ void __launch_bounds__(kUpdThreads)
+    k_pcg_init(const double* __restrict__ rhs, const double* __restrict__ minv, int64_t num_vars,
+               double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+               double* __restrict__ p, PcgState* __restrict__ st) {
+  __shared__ double red[33];
+  const int64_t n6 = 6 * num_vars;
+  for (int64_t t = threadIdx.x; t < n6; t += blockDim.x) {
+    x[t] = 0.0;
+    r[t] = rhs[t];
+  }
+  __syncthreads();
+  precond(minv, r, z, n6);
+  __syncthreads();
+  double rz = 0.0, rr = 0.0;
+  for (int64_t t = threadIdx.x; t < n6; t += blockDim.x) {
+    p[t] = z[t];
+    rz += r[t] * z[t];
+    rr += r[t] * r[t];
+  }
+  rz = block_sum(rz, red);
+  rr = block_sum(rr, red);
+  if (threadIdx.x == 0) {
+    st->rz = rz;
+    st->r0 = sqrt(rr);
+    st->res = sqrt(rr);
+    st->iter = 0;
+  }
+}
+
+// q = A p (one warp per block row; lane l takes the row's blocks l, l + 32, ...
+// then a fixed xor tree), and per-row partials of p . q
+__global__ void k_spmv_dot(const double* __restrict__ blocks, const int32_t* __restrict__ row_start,
+                           const int32_t* __restrict__ col, int64_t num_vars,
+                           const double* __restrict__ p, double* __restrict__ q,
+                           double* __restrict__ pq_part) {
+  const int lane = threadIdx.x & 31;
+  const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (v >= num_vars) return;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int32_t b = row_start[v] + lane; b < row_start[v + 1]; b += 32) {
+    const double* B = blocks + 36 * (int64_t)b;
+    const double* pc = p + 6 * (int64_t)col[b];
+    double pv[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) pv[k] = pc[k];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) acc[i] += B[i * 6 + k] * pv[k];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 6; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+  if (lane == 0) {
+    double d = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      q[6 * v + i] = acc[i];
+      d += p[6 * v + i] * acc[i];
+    }
+    pq_part[v] = d;
+  }
+}
+
+// one block: alpha, x, r, z, beta, p; sets the WHILE condition
+__global__ void __launch_bounds__(kUpdThreads)
+    k_pcg_update(const double* __restrict__ minv, int64_t num_vars, const double* __restrict__ q,
+                 const double* __restrict__ pq_part, double* __restrict__ x, double* __restrict__ r,
+                 double* __restrict__ z, double* __restrict__ p, PcgState* __restrict__ st,
+                 int32_t max_iter, double tol, cudaGraphConditionalHandle cond) {
+  __shared__ double red[33];
+  const int64_t n6 = 6 * num_vars;
+  double pq = 0.0;
+  for (int64_t v = threadIdx.x; v < num_vars; v += blockDim.x) pq += pq_part[v];
+  pq = block_sum(pq, red);
+  const double rz = st->rz;
+  const double alpha = pq > 0.0 ? rz / pq : 0.0;
+  for (int64_t t = threadIdx.x; t < n6; t += blockDim.x) {
+    x[t] += alpha * p[t];
+    r[t] -= alpha * q[t];
+  }
+  __syncthreads();
+  precond(minv, r, z, n6);
+  __syncthreads();
+  double rzn = 0.0, rr = 0.0;
+  for (int64_t t = threadIdx.x; t < n6; t += blockDim.x) {
+    rzn += r[t] * z[t];
+    rr += r[t] * r[t];
+  }
+  rzn = block_sum(rzn, red);
+  rr = block_sum(rr, red);
+  const double beta = rz > 0.0 ? rzn / rz : 0.0;
+  for (int64_t t = threadIdx.x; t < n6; t += blockDim.x) p[t] = z[t] + beta * p[t];
+  if (threadIdx.x == 0) {
+    st->rz = rzn;
+    st->res = sqrt(rr);
+    st->iter += 1;
+    const bool go = st->res > tol * st->r0 && st->iter < max_iter && pq > 0.0;
+    if (cond) cudaGraphSetConditional(cond, go ? 1u : 0u);
+    st->done = go ? 0 : 1;
+  }
+}
+
+// delta of every pose: the solution for variables, 0 for fixed poses
+__global__ void k_scatter_delta(const double* __restrict__ x, const int32_t* __restrict__ var_of_pose,
+                                int64_t num_poses, double* __restrict__ delta) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 6 * num_poses) return;
+  const int32_t v = var_of_pose[t / 6];
+  delta[t] = v >= 0 ? x[6 * (int64_t)v + t % 6] : 0.0;
+}
+
+}  // namespace
+
+void launch_assemble(const gvox_linear_factor* rec, const int32_t* contrib_start,
+                     const int32_t* contrib, int64_t num_blocks, const uint8_t* is_diag,
+                     double lambda, double* blocks, const int32_t* g_start, const int32_t* g_list,
+                     int64_t num_vars, double* rhs, const int32_t* diag_block, double* minv,
+                     int32_t* bad, cudaStream_t stream) {
+  if (num_blocks > 0) {
+    k_assemble_blocks<<<(unsigned)((num_blocks * 32 + 255) / 256), 256, 0, stream>>>(
+        rec, contrib_start, contrib, num_blocks, is_diag, lambda, blocks);
+    note_launch();
+  }
+  if (num_vars > 0) {
+    k_assemble_rhs<<<(unsigned)((6 * num_vars + 255) / 256), 256, 0, stream>>>(rec, g_start, g_list,
+                                                                              num_vars, rhs);
+    k_block_jacobi<<<(unsigned)((num_vars + 127) / 128), 128, 0, stream>>>(blocks, diag_block, num_vars,
+                                                                          minv, bad);
+    note_launch();
+    note_launch();
+  }
+}
+
+void launch_pcg_init(const double* rhs, const double* minv, int64_t num_vars, double* x, double* r,
+                     double* z, double* p, PcgState* st, cudaStream_t stream) {
+  k_pcg_init<<<1, kUpdThreads, 0, stream>>>(rhs, minv, num_vars, x, r, z, p, st);
+  note_launch();
+}
+
+void launch_pcg_iteration(const double* blocks, const int32_t* row_start, const int32_t* col,
+                          int64_t num_vars, const double* minv, double* x, double* r, double* z,
+                          double* p, double* q, double* pq_part, PcgState* st, int32_t max_iter,
+                          double tol, cudaGraphConditionalHandle cond, cudaStream_t stream) {
+  k_spmv_dot<<<(unsigned)((num_vars * 32 + 255) / 256), 256, 0, stream>>>(blocks, row_start, col,
+                                                                          num_vars, p, q, pq_part);
+  k_pcg_update<<<1, kUpdThreads, 0, stream>>>(minv, num_vars, q, pq_part, x, r, z, p, st, max_iter,
+                                              tol, cond);
+  note_launch();
+  note_launch();
+}
+
+void launch_scatter_delta(const double* x, const int32_t* var_of_pose, int64_t num_poses,
+                          double* delta, cudaStream_t stream) {
+  if (num_poses <= 0) return;
+  k_scatter_delta<<<(unsigned)((6 * num_poses + 255) / 256), 256, 0, stream>>>(x, var_of_pose,
+                                                                              num_poses, delta);
+  note_launch();
+}
+
+}  // namespace gvox
