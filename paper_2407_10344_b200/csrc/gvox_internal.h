@@ -332,6 +332,11 @@ void launch_pcg_iteration(const double* blocks, const int32_t* row_start, const 
                           int64_t num_vars, const double* minv, double* x, double* r, double* z,
                           double* p, double* q, double* pq_part, PcgState* st, int32_t max_iter,
                           double tol, cudaGraphConditionalHandle cond, cudaStream_t stream);
+void launch_pcg_persistent(const double* blocks, const int32_t* row_start, const int32_t* col,
+                           int64_t num_vars, const double* minv, const double* rhs, double* x,
+                           double* r, double* z, double* p, double* q, double* part_a,
+                           double* part_b, PcgState* st, int32_t max_iter, double tol,
+                           cudaStream_t stream);
 void launch_scatter_delta(const double* x, const int32_t* var_of_pose, int64_t num_poses,
                           double* delta, cudaStream_t stream);
 

@@ -1301,7 +1301,7 @@ struct PrepBatch {
   const float* dpts = nullptr;          // device points
   std::vector<KnnCloudDev> cl;
   std::vector<int32_t> tstart;
-  int tile_pts = 256;  // one query per thread or two: a single frame still fills the GPU
+  int tile_pts = 64;  // one query per thread (64-thread CTAs): a single frame spreads over all SMs
   int64_t n = 0, T = 0;
 };
 
@@ -1357,7 +1357,7 @@ gvox_status gvox_knn(gvox_ctx* ctx, const float* points, const int64_t* offsets,
   size_t o_box = l1.add(4 * 6 * (size_t)std::max<int64_t>(count, 1) + 16);
   size_t o_cl = l1.add(sizeof(KnnCloudDev) * (size_t)std::max<int64_t>(count, 1));
   size_t o_ts = l1.add(4 * (size_t)(count + 1));
-  size_t o_tc = l1.add(4 * (size_t)(n_all / 256 + count + 1));
+  size_t o_tc = l1.add(4 * (size_t)(n_all / 64 + count + 1));
   gvox_status st = ws_reserve(ctx, 1, l1.size, &ws1);
   if (st) return st;
   char* w1 = (char*)ws1;
@@ -1513,7 +1513,7 @@ gvox_status gvox_estimate_covariances(gvox_ctx* ctx, const float* points, const 
   size_t o_nrm = l1.add(mem == GVOX_HOST ? 12 * (size_t)n_all : 0);
   size_t o_cl = l1.add(sizeof(KnnCloudDev) * (size_t)std::max<int64_t>(count, 1));
   size_t o_ts = l1.add(4 * (size_t)(count + 1));
-  size_t o_tc = l1.add(4 * (size_t)(n_all / 256 + count + 1));
+  size_t o_tc = l1.add(4 * (size_t)(n_all / 64 + count + 1));
   void* ws = nullptr;
   gvox_status st = ws_reserve(ctx, 1, l1.size, &ws);
   if (st) return st;
@@ -2029,6 +2029,7 @@ gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t
   const int64_t n6 = 6 * (int64_t)std::max<int32_t>(V, 1);
   size_t o_rhs = wl.add(8 * n6), o_x = wl.add(8 * n6), o_r = wl.add(8 * n6), o_z = wl.add(8 * n6);
   size_t o_p = wl.add(8 * n6), o_q = wl.add(8 * n6), o_pq = wl.add(8 * (n6 / 6));
+  size_t o_pb = wl.add(8 * (n6 / 6));
   size_t o_minv = wl.add(8 * 36 * (n6 / 6));
   size_t o_st = wl.add(sizeof(PcgState) + 16);
   size_t o_dl = wl.add(mem == GVOX_HOST ? 48 * (size_t)std::max<int64_t>(num_poses, 1) : 0);
@@ -2054,7 +2055,16 @@ gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t
                     V, (double*)(wb + o_rhs), (const int32_t*)(din + o_dg), (double*)(wb + o_minv),
                     dbad, ctx->stream);
     CK_LAUNCH("global assemble");
-    if (V > 0) {
+    if (V > 0 && std::getenv("GVOX_PCG_GRAPH") == nullptr) {
+      // one cooperative persistent kernel runs the whole PCG (grid barriers)
+      launch_pcg_persistent((const double*)(wb + o_blk), (const int32_t*)(din + o_rs),
+                            (const int32_t*)(din + o_col), V, (const double*)(wb + o_minv),
+                            (const double*)(wb + o_rhs), (double*)(wb + o_x), (double*)(wb + o_r),
+                            (double*)(wb + o_z), (double*)(wb + o_p), (double*)(wb + o_q),
+                            (double*)(wb + o_pq), (double*)(wb + o_pb), dst, P.max_iterations,
+                            P.tol, ctx->stream);
+      CK_LAUNCH("PCG (persistent)");
+    } else if (V > 0) {
       launch_pcg_init((const double*)(wb + o_rhs), (const double*)(wb + o_minv), V, (double*)(wb + o_x),
                       (double*)(wb + o_r), (double*)(wb + o_z), (double*)(wb + o_p), dst, ctx->stream);
       if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));

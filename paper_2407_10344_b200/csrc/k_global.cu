@@ -9,12 +9,19 @@
 // Layout: block-sparse rows (BSR, 6x6 fp64 blocks, both (i, j) and (j, i)
 // stored, columns ascending per row).  Every block and every right-hand-side
 // entry is summed by one warp / thread over its contribution list in
-// ascending factor order: the system is bitwise deterministic.  The PCG loop
-// runs as the body of a CUDA graph WHILE node (k_spmv_dot -> k_pcg_update, the
-// latter sets the condition), like the registration loop.
+// ascending factor order: the system is bitwise deterministic.  The PCG runs
+// as ONE cooperative persistent kernel (k_pcg_persistent: grid barriers
+// between SpMV, update and direction phases); the two-kernel version as the
+// body of a CUDA graph WHILE node (k_spmv_dot -> k_pcg_update, the latter
+// sets the condition) is kept behind GVOX_PCG_GRAPH=1 for comparison.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "k_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gvox {
 namespace {
@@ -246,7 +253,147 @@ __global__ void k_scatter_delta(const double* __restrict__ x, const int32_t* __r
   delta[t] = v >= 0 ? x[6 * (int64_t)v + t % 6] : 0.0;
 }
 
+// Persistent PCG: one cooperative launch runs every iteration; three grid
+// barriers per iteration (after q = A p; after x, r, z; after p).  Every CTA
+// sums the per-row partials itself in the same fixed order, so all CTAs hold
+// bitwise identical alpha, beta and stopping decisions (and the run is
+// reproducible).  Rows are grid-strided warp by warp.
+constexpr int kPcgThreads = 256;
+
+__device__ double sum_parts(const double* __restrict__ part, int64_t n, double* red) {
+  double s = 0.0;
+  for (int64_t v = threadIdx.x; v < n; v += blockDim.x) s += part[v];
+  return block_sum(s, red);
+}
+
+__global__ void __launch_bounds__(kPcgThreads)
+    k_pcg_persistent(const double* __restrict__ blocks, const int32_t* __restrict__ row_start,
+                     const int32_t* __restrict__ col, int64_t num_vars, const double* __restrict__ minv,
+                     const double* __restrict__ rhs, double* __restrict__ x, double* __restrict__ r,
+                     double* __restrict__ z, double* __restrict__ p, double* __restrict__ q,
+                     double* __restrict__ part_a, double* __restrict__ part_b, PcgState* __restrict__ st,
+                     int32_t max_iter, double tol) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[33];
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // z = M^-1 r for the rows of this warp; returns (r.z, r.r) partials per row
+  auto precond_rows = [&]() {
+    for (int64_t v = gwarp; v < num_vars; v += nwarps) {
+      double zi = 0.0, rv = 0.0;
+      if (lane < 6) {
+        rv = r[6 * v + lane];
+        for (int k = 0; k < 6; ++k) zi += minv[36 * v + lane * 6 + k] * r[6 * v + k];
+        z[6 * v + lane] = zi;
+      }
+      double rz = lane < 6 ? rv * zi : 0.0, rr = lane < 6 ? rv * rv : 0.0;
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        rz += __shfl_xor_sync(0xffffffffu, rz, o);
+        rr += __shfl_xor_sync(0xffffffffu, rr, o);
+      }
+      if (lane == 0) {
+        part_a[v] = rz;
+        part_b[v] = rr;
+      }
+    }
+  };
+  // ---- start: x = 0, r = rhs, z = M^-1 r, p = z
+  for (int64_t v = gwarp; v < num_vars; v += nwarps)
+    if (lane < 6) {
+      x[6 * v + lane] = 0.0;
+      r[6 * v + lane] = rhs[6 * v + lane];
+    }
+  __syncwarp();
+  precond_rows();
+  for (int64_t v = gwarp; v < num_vars; v += nwarps)
+    if (lane < 6) p[6 * v + lane] = z[6 * v + lane];
+  grid.sync();
+  double rz = sum_parts(part_a, num_vars, red);
+  const double r0 = sqrt(sum_parts(part_b, num_vars, red));
+  double res = r0;
+  int32_t it = 0;
+  bool go = r0 > 0.0 && !(r0 <= tol * r0);
+  while (go) {
+    // q = A p (warp per block row, lane-strided blocks, fixed xor tree)
+    for (int64_t v = gwarp; v < num_vars; v += nwarps) {
+      double acc[6] = {0, 0, 0, 0, 0, 0};
+      for (int32_t b = row_start[v] + lane; b < row_start[v + 1]; b += 32) {
+        const double* B = blocks + 36 * (int64_t)b;
+        const double* pc = p + 6 * (int64_t)col[b];
+        double pv[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) pv[k] = pc[k];
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+          for (int k = 0; k < 6; ++k) acc[i] += B[i * 6 + k] * pv[k];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < 6; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+      if (lane == 0) {
+        double d = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          q[6 * v + i] = acc[i];
+          d += p[6 * v + i] * acc[i];
+        }
+        part_a[v] = d;
+      }
+    }
+    grid.sync();
+    const double pq = sum_parts(part_a, num_vars, red);
+    const double alpha = pq > 0.0 ? rz / pq : 0.0;
+    grid.sync();  // every CTA has read part_a before it is overwritten
+    for (int64_t v = gwarp; v < num_vars; v += nwarps)
+      if (lane < 6) {
+        x[6 * v + lane] += alpha * p[6 * v + lane];
+        r[6 * v + lane] -= alpha * q[6 * v + lane];
+      }
+    __syncwarp();
+    precond_rows();
+    grid.sync();
+    const double rzn = sum_parts(part_a, num_vars, red);
+    res = sqrt(sum_parts(part_b, num_vars, red));
+    const double beta = rz > 0.0 ? rzn / rz : 0.0;
+    rz = rzn;
+    ++it;
+    for (int64_t v = gwarp; v < num_vars; v += nwarps)
+      if (lane < 6) p[6 * v + lane] = z[6 * v + lane] + beta * p[6 * v + lane];
+    go = res > tol * r0 && it < max_iter && pq > 0.0;
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->rz = rz;
+    st->r0 = r0;
+    st->res = res;
+    st->iter = it;
+    st->done = 1;
+  }
+}
+
 }  // namespace
+
+void launch_pcg_persistent(const double* blocks, const int32_t* row_start, const int32_t* col,
+                           int64_t num_vars, const double* minv, const double* rhs, double* x,
+                           double* r, double* z, double* p, double* q, double* part_a,
+                           double* part_b, PcgState* st, int32_t max_iter, double tol,
+                           cudaStream_t stream) {
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_persistent, kPcgThreads, 0);
+  const int64_t want = (num_vars * 32 + kPcgThreads - 1) / kPcgThreads;  // one warp per row
+  int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)sms * std::max(per_sm, 1));
+  void* args[] = {(void*)&blocks, (void*)&row_start, (void*)&col, (void*)&num_vars, (void*)&minv,
+                  (void*)&rhs, (void*)&x, (void*)&r, (void*)&z, (void*)&p, (void*)&q,
+                  (void*)&part_a, (void*)&part_b, (void*)&st, (void*)&max_iter, (void*)&tol};
+  cudaLaunchCooperativeKernel((void*)k_pcg_persistent, grid, kPcgThreads, args, 0, stream);
+  note_launch();
+}
 
 void launch_assemble(const gvox_linear_factor* rec, const int32_t* contrib_start,
                      const int32_t* contrib, int64_t num_blocks, const uint8_t* is_diag,

@@ -19,7 +19,7 @@
 namespace gvox {
 namespace {
 
-constexpr int kKnnThreads = 128;
+constexpr int kKnnThreads = 64;
 
 __device__ __forceinline__ double sq_dist_pinned(float px, float py, float pz, float qx, float qy,
                                                  float qz) {
@@ -41,7 +41,7 @@ __global__ void k_knn_count(const float* __restrict__ pts, const KnnCloudDev* __
   const int32_t c = __ldg(tile_cloud + blockIdx.x);
   const KnnCloudDev cd = clouds[c];
   const int64_t k = cd.first + (int64_t)(blockIdx.x - __ldg(tile_start + c)) * tile_pts + threadIdx.x;
-  for (int64_t i = k; i < cd.first + cd.n && i < k + tile_pts; i += blockDim.x) {
+  for (int64_t i = k; i < cd.first + cd.n && i < k - threadIdx.x + tile_pts; i += blockDim.x) {
     const float x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
     const int32_t cx = cell_coord(x, cd.lo[0], cd.inv_s, cd.dim[0]);
     const int32_t cy = cell_coord(y, cd.lo[1], cd.inv_s, cd.dim[1]);
@@ -61,7 +61,7 @@ __global__ void k_knn_scatter(const float* __restrict__ pts, const KnnCloudDev* 
   const int32_t c = __ldg(tile_cloud + blockIdx.x);
   const KnnCloudDev cd = clouds[c];
   const int64_t k = cd.first + (int64_t)(blockIdx.x - __ldg(tile_start + c)) * tile_pts + threadIdx.x;
-  for (int64_t i = k; i < cd.first + cd.n && i < k + tile_pts; i += blockDim.x) {
+  for (int64_t i = k; i < cd.first + cd.n && i < k - threadIdx.x + tile_pts; i += blockDim.x) {
     const int32_t cell = cell_of[i];
     const int32_t slot = cell_start[cell] + atomicAdd(fill + cell, 1);
     sorted[slot] = make_float4(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2],
@@ -79,7 +79,7 @@ __global__ void k_knn_bbox(const float* __restrict__ pts, const KnnCloudDev* __r
   const int64_t k = cd.first + (int64_t)(blockIdx.x - __ldg(tile_start + c)) * tile_pts + threadIdx.x;
   int32_t mn[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, mx[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
   int nonfinite = 0;
-  for (int64_t i = k; i < cd.first + cd.n && i < k + tile_pts; i += blockDim.x) {
+  for (int64_t i = k; i < cd.first + cd.n && i < k - threadIdx.x + tile_pts; i += blockDim.x) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const float x = pts[3 * i + a];
@@ -267,7 +267,7 @@ __global__ void k_covariance(const float* __restrict__ pts, const KnnCloudDev* _
   const int32_t c = __ldg(tile_cloud + blockIdx.x);
   const KnnCloudDev cd = clouds[c];
   const int64_t k0 = cd.first + (int64_t)(blockIdx.x - __ldg(tile_start + c)) * tile_pts + threadIdx.x;
-  for (int64_t i = k0; i < cd.first + cd.n && i < k0 + tile_pts; i += blockDim.x) {
+  for (int64_t i = k0; i < cd.first + cd.n && i < k0 - threadIdx.x + tile_pts; i += blockDim.x) {
     const int32_t* row = nbr + i * (int64_t)k;
     double m[3] = {0, 0, 0};
     int cnt = 0;
@@ -464,7 +464,7 @@ void launch_covariance(const float* pts, const KnnCloudDev* clouds, const int32_
                        const int32_t* tile_cloud, int64_t num_tiles, int tile_pts, const int32_t* nbr,
                        int k, float* cov, float* nrm, cudaStream_t stream) {
   if (num_tiles <= 0) return;
-  k_covariance<<<(unsigned)num_tiles, 128, 0, stream>>>(pts, clouds, tile_start, tile_cloud, tile_pts,
+  k_covariance<<<(unsigned)num_tiles, 64, 0, stream>>>(pts, clouds, tile_start, tile_cloud, tile_pts,
                                                        nbr, k, cov, nrm);
   note_launch();
 }

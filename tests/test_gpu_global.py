@@ -91,3 +91,18 @@ def test_device_records_and_errors(gv, ctx, graph):
     # everything fixed: zero step
     d4, r4, _, _ = gv.solve_global(ctx, f, acc, poses, np.ones(P, np.uint8))
     assert not d4.any() and r4["num_variables"] == 0
+
+
+def test_persistent_and_graph_pcg_agree(gv, ctx, graph, monkeypatch):
+    """The cooperative persistent PCG and the WHILE-node two-kernel PCG run the
+    same recurrence (different dot-product partitions): same solution to the
+    solver tolerance, same iteration count within one."""
+    sc, f, poses, acc, lin, clouds, maps = graph
+    P = len(poses)
+    fixed = np.zeros(P, np.uint8)
+    fixed[0] = 1
+    d1, r1, _, _ = gv.solve_global(ctx, f, acc, poses, fixed, tol=1e-12, max_iterations=2000)
+    monkeypatch.setenv("GVOX_PCG_GRAPH", "1")
+    d2, r2, _, _ = gv.solve_global(ctx, f, acc, poses, fixed, tol=1e-12, max_iterations=2000)
+    assert np.linalg.norm(d1 - d2) <= 1e-8 * np.linalg.norm(d1)
+    assert abs(int(r1["iterations"]) - int(r2["iterations"])) <= 1
