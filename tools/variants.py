@@ -28,6 +28,8 @@ VARIANTS = {
     "g1": ["GVOX_LIN_G=1"],
     "t128_b2": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=2"],
     "t256_b1": ["GVOX_LIN_THREADS=256", "GVOX_LIN_MINB=1"],
+    "t128_b5": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=5"],
+    "t64_b8": ["GVOX_LIN_THREADS=64", "GVOX_LIN_MINB=8"],
     # overlap kernel (stage times from a full bench run)
     "ovl_base": [],
     "acc_seg1": ["GVOX_ACC_SEG_MIN=1"],
