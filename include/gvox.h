@@ -445,6 +445,42 @@ gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t
                               const gvox_global_params* params, double* delta, double* H_dense,
                               double* b_dense, gvox_global_result* result, int mem);
 
+/* Gauss-Newton optimisation of the whole graph (the global mapping loop,
+   P:391, with every factor re-linearized at every iteration).  Each
+   iteration: gvox_linearize_batch_accum at the current poses (device
+   records), gvox_solve_global (params' PCG settings), T_v <- T_v Exp(delta_v)
+   on the device; stop when max_v |w_v| <= eps_rot and max_v |rho_v| <=
+   eps_trans, or after max_iterations.  error_history (optional, HOST,
+   [max_iterations]) receives the total error at each linearization.
+   clouds, maps, factors, poses, fixed, params: as in gvox_linearize_batch /
+   gvox_solve_global (host); poses_out [num_poses x 12] in `mem`. */
+typedef struct gvox_optimize_params {
+  int32_t max_iterations;      /* Gauss-Newton iterations, >= 1 */
+  int32_t pcg_max_iterations;  /* per solve, >= 1 */
+  double pcg_tol;
+  double lambda;
+  double eps_rot;              /* rad */
+  double eps_trans;            /* m */
+} gvox_optimize_params;
+
+typedef struct gvox_optimize_result {
+  int32_t iterations;          /* linearizations performed */
+  int32_t converged;
+  int32_t pcg_iterations;      /* summed over the solves */
+  int32_t reserved;
+  double error_initial;        /* total error at the first linearization */
+  double error_final;          /* ... at the last one */
+  double last_step_rot;        /* max |w| of the last step */
+  double last_step_trans;      /* max |rho| of the last step */
+} gvox_optimize_result;
+
+gvox_status gvox_optimize_global(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                 int64_t num_clouds, const gvox_map* const* maps, int64_t num_maps,
+                                 const gvox_factor* factors, int64_t num_factors,
+                                 const double* poses, int64_t num_poses, const uint8_t* fixed,
+                                 const gvox_optimize_params* params, double* poses_out,
+                                 double* error_history, gvox_optimize_result* result, int mem);
+
 /* ------------------------------------------------------------- utilities */
 
 const char* gvox_status_string(gvox_status s);

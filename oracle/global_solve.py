@@ -44,3 +44,34 @@ def assemble(factors, lin, num_poses, fixed, lam=0.0):
 
 def solve(H, b):
     return np.linalg.solve(H, -b)
+
+
+def optimize(clouds, maps, factors, poses, fixed, max_iterations=10, lam=0.0, eps_rot=1e-6,
+             eps_trans=1e-6, num_threads=1):
+    """Gauss-Newton over the whole graph (P:391 global mapping; every factor
+    re-linearized each iteration): linearize all factors (oracle.cpp),
+    assemble, solve, T_v <- T_v Exp(delta_v) for the variables; stop when the
+    largest |w| and |rho| of a step are within eps.  Returns (poses, errors,
+    converged)."""
+    from . import oracle as _o
+    from .register import se3_exp
+    poses = np.array(np.asarray(poses, np.float64).reshape(-1, 12))
+    P = len(poses)
+    errs = []
+    for _ in range(max_iterations):
+        lin = _o.linearize_batch(clouds, maps, factors, poses, num_threads=num_threads)
+        errs.append(sum(d["e"] for d in lin))
+        H, b, var = assemble(factors, lin, P, fixed, lam)
+        x = solve(H, b)
+        mw = mr = 0.0
+        for v in range(P):
+            if var[v] < 0:
+                continue
+            d = x[6 * var[v]: 6 * var[v] + 6]
+            mw, mr = max(mw, float(np.linalg.norm(d[:3]))), max(mr, float(np.linalg.norm(d[3:])))
+            T = np.eye(4)
+            T[:3, :] = poses[v].reshape(3, 4)
+            poses[v] = (T @ se3_exp(d))[:3, :].reshape(12)
+        if mw <= eps_rot and mr <= eps_trans:
+            return poses, errs, True
+    return poses, errs, False

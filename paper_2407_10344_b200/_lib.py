@@ -47,6 +47,12 @@ GLOBAL_PARAMS_DTYPE = np.dtype([("max_iterations", "<i4"), ("reserved", "<i4"), 
 GLOBAL_RESULT_DTYPE = np.dtype([("iterations", "<i4"), ("converged", "<i4"), ("num_variables", "<i4"),
                                 ("num_blocks", "<i4"), ("residual_initial", "<f8"),
                                 ("residual_final", "<f8")])
+OPTIMIZE_PARAMS_DTYPE = np.dtype([("max_iterations", "<i4"), ("pcg_max_iterations", "<i4"),
+                                  ("pcg_tol", "<f8"), ("lambda", "<f8"), ("eps_rot", "<f8"),
+                                  ("eps_trans", "<f8")])
+OPTIMIZE_RESULT_DTYPE = np.dtype([("iterations", "<i4"), ("converged", "<i4"), ("pcg_iterations", "<i4"),
+                                  ("reserved", "<i4"), ("error_initial", "<f8"), ("error_final", "<f8"),
+                                  ("last_step_rot", "<f8"), ("last_step_trans", "<f8")])
 REG_FIXED, REG_MAX_ITER, REG_CONVERGED, REG_SINGULAR = 0, 1, 2, 3
 
 # exported symbols (tests check every one declared in include/gvox.h is here)
@@ -58,7 +64,7 @@ SYMBOLS = [
     "gvox_voxelmap_export", "gvox_voxelmap_lookup", "gvox_map_destroy",
     "gvox_overlap", "gvox_overlap_select", "gvox_linearize_batch", "gvox_linearize_batch_accum", "gvox_expand",
     "gvox_register_batch", "gvox_overlap_union", "gvox_keyframe_update", "gvox_knn",
-    "gvox_estimate_covariances", "gvox_solve_global",
+    "gvox_estimate_covariances", "gvox_solve_global", "gvox_optimize_global",
     "gvox_status_string", "gvox_last_error", "gvox_launch_count", "gvox_version",
 ]
 
@@ -105,6 +111,7 @@ def lib():
         "gvox_linearize_batch_accum": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32]),
         "gvox_expand": (I32, [P, P, I64, P, I64, P, P, I32]),
         "gvox_solve_global": (I32, [P, P, I64, P, P, I64, P, P, P, P, P, P, I32]),
+        "gvox_optimize_global": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, P, P, P, P, I32]),
         "gvox_knn": (I32, [P, P, P, I64, I32, D, P, I32]),
         "gvox_estimate_covariances": (I32, [P, P, P, I64, P, I32, P, P, I32]),
         "gvox_overlap_union": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I64, I32, P, I32]),

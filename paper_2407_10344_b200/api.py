@@ -15,7 +15,8 @@ import numpy as np
 
 from ._lib import (FACTOR_ACCUM_DTYPE, FACTOR_DTYPE, GVOX_DEVICE, GVOX_HOST, LINEAR_FACTOR_DTYPE,
                    PAIR_DTYPE, REGISTER_PARAMS_DTYPE, REGISTER_RESULT_DTYPE, UNION_MEMBER_DTYPE,
-                   UNION_QUERY_DTYPE, GLOBAL_PARAMS_DTYPE, GLOBAL_RESULT_DTYPE, check, lib)
+                   UNION_QUERY_DTYPE, GLOBAL_PARAMS_DTYPE, GLOBAL_RESULT_DTYPE,
+                   OPTIMIZE_PARAMS_DTYPE, OPTIMIZE_RESULT_DTYPE, check, lib)
 
 
 def _torch():
@@ -490,6 +491,29 @@ def solve_global(ctx: Context, factors, accum, poses, fixed, max_iterations: int
                                   None if H is None else _ptr(H)[0], None if b is None else _ptr(b)[0],
                                   _ptr(res)[0], mem))
     return delta, res[0], H, b
+
+
+def optimize_global(ctx: Context, clouds, maps, factors, poses, fixed, max_iterations: int = 10,
+                    pcg_max_iterations: int = 2000, pcg_tol: float = 1e-10, lam: float = 0.0,
+                    eps_rot: float = 1e-6, eps_trans: float = 1e-6):
+    """gvox_optimize_global: Gauss-Newton over the whole graph on the device.
+    Returns (poses_out [P,12], result, error_history [iterations])."""
+    C, M = _handles(clouds), _handles(maps)
+    factors = as_factors(factors)
+    poses = as_poses(poses)
+    NPz = poses.shape[0]
+    fx = np.ascontiguousarray(np.asarray(fixed, np.uint8).reshape(-1))
+    prm = np.zeros(1, OPTIMIZE_PARAMS_DTYPE)
+    prm["max_iterations"], prm["pcg_max_iterations"] = int(max_iterations), int(pcg_max_iterations)
+    prm["pcg_tol"], prm["lambda"] = float(pcg_tol), float(lam)
+    prm["eps_rot"], prm["eps_trans"] = float(eps_rot), float(eps_trans)
+    res = np.zeros(1, OPTIMIZE_RESULT_DTYPE)
+    out = np.zeros((NPz, 12), np.float64)
+    hist = np.zeros(max_iterations, np.float64)
+    check(lib().gvox_optimize_global(ctx.handle, C.arr, C.n, M.arr, M.n, _ptr(factors)[0],
+                                     factors.shape[0], _ptr(poses)[0], NPz, _ptr(fx)[0], _ptr(prm)[0],
+                                     _ptr(out)[0], _ptr(hist)[0], _ptr(res)[0], GVOX_HOST))
+    return out, res[0], hist[: int(res[0]["iterations"])]
 
 
 def register_batch(ctx: Context, clouds, maps, factors, poses, max_iterations: int = 10,

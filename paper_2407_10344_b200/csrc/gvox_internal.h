@@ -340,6 +340,10 @@ void launch_pcg_persistent(const double* blocks, const int32_t* row_start, const
 void launch_scatter_delta(const double* x, const int32_t* var_of_pose, int64_t num_poses,
                           double* delta, cudaStream_t stream);
 
+void launch_apply_delta(double* poses, const double* delta, int64_t num_poses, double* out_max,
+                        cudaStream_t stream);
+void launch_sum_error(const gvox_factor_accum* acc, int64_t n, double* out, cudaStream_t stream);
+
 // tile -> owning item (factor or pair) table from the tile prefix sums
 void launch_tile_map(const int32_t* tile_start, int64_t num_items, int32_t* tile_owner,
                      cudaStream_t stream);

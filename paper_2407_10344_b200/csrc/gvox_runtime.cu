@@ -2142,6 +2142,78 @@ gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t
   return GVOX_OK;
 }
 
+gvox_status gvox_optimize_global(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                 int64_t num_clouds, const gvox_map* const* maps, int64_t num_maps,
+                                 const gvox_factor* factors, int64_t num_factors,
+                                 const double* poses, int64_t num_poses, const uint8_t* fixed,
+                                 const gvox_optimize_params* params, double* poses_out,
+                                 double* error_history, gvox_optimize_result* result, int mem) {
+  const char* fn = "gvox_optimize_global";
+  if (!ctx) return fail(GVOX_ERR_INVALID, "%s: ctx is NULL", fn);
+  if (!params || !result || !poses_out || !fixed || (num_poses > 0 && !poses))
+    return fail(GVOX_ERR_INVALID, "%s: NULL argument", fn);
+  if (num_poses < 0 || num_factors < 0) return fail(GVOX_ERR_INVALID, "%s: negative size", fn);
+  if (mem != GVOX_HOST && mem != GVOX_DEVICE)
+    return fail(GVOX_ERR_INVALID, "%s: mem must be GVOX_HOST or GVOX_DEVICE", fn);
+  const gvox_optimize_params P = *params;
+  if (P.max_iterations < 1 || P.max_iterations > 1000 || P.pcg_max_iterations < 1 ||
+      !(P.eps_rot >= 0.0) || !(P.eps_trans >= 0.0))
+    return fail(GVOX_ERR_INVALID, "%s: bad iteration counts or tolerances", fn);
+  std::memset(result, 0, sizeof(*result));
+  DeviceGuard g(ctx->device);
+  // device state: records, step, poses, two scalars (error, max |w|, max |rho|);
+  // a dedicated allocation (the linearize / solve calls reuse the workspaces)
+  const size_t acc_b = sizeof(gvox_factor_accum) * (size_t)std::max<int64_t>(num_factors, 1);
+  const size_t pose_b = 96 * (size_t)std::max<int64_t>(num_poses, 1);
+  std::shared_ptr<DevBuf> buf;
+  gvox_status st = devbuf_alloc(acc_b + pose_b + 48 * (size_t)std::max<int64_t>(num_poses, 1) + 64,
+                                ctx->device, ctx->stream, &buf);
+  if (st) return st;
+  char* b0 = (char*)buf->ptr;
+  gvox_factor_accum* dacc = (gvox_factor_accum*)b0;
+  double* dposes = (double*)(b0 + acc_b);
+  double* ddelta = (double*)(b0 + acc_b + pose_b);
+  double* dscal = (double*)(b0 + acc_b + pose_b + 48 * (size_t)std::max<int64_t>(num_poses, 1));
+  std::vector<double> ph(poses, poses + 12 * num_poses);
+  gvox_global_params gp{P.pcg_max_iterations, 0, P.pcg_tol, P.lambda};
+  for (int it = 0; it < P.max_iterations; ++it) {
+    st = linearize_impl(ctx, clouds, num_clouds, maps, num_maps, factors, num_factors, ph.data(),
+                        num_poses, nullptr, dacc, GVOX_DEVICE, nullptr);
+    if (st) return st;
+    launch_sum_error(dacc, num_factors, dscal, ctx->stream);
+    gvox_global_result gr;
+    st = gvox_solve_global(ctx, factors, num_factors, dacc, ph.data(), num_poses, fixed, &gp, ddelta,
+                           nullptr, nullptr, &gr, GVOX_DEVICE);
+    if (st) return st;
+    if (num_poses) {
+      CK(cudaMemcpyAsync(dposes, ph.data(), 96 * num_poses, cudaMemcpyHostToDevice, ctx->stream));
+      launch_apply_delta(dposes, ddelta, num_poses, dscal + 1, ctx->stream);
+      CK(cudaMemcpyAsync(ph.data(), dposes, 96 * num_poses, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    double sc[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(sc, dscal, num_poses ? 24 : 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK_LAUNCH(fn);
+    if (it == 0) result->error_initial = sc[0];
+    result->error_final = sc[0];
+    if (error_history) error_history[it] = sc[0];
+    result->iterations = it + 1;
+    result->pcg_iterations += gr.iterations;
+    result->last_step_rot = sc[1];
+    result->last_step_trans = sc[2];
+    if (sc[1] <= P.eps_rot && sc[2] <= P.eps_trans) {
+      result->converged = 1;
+      break;
+    }
+  }
+  if (num_poses) {
+    if (mem == GVOX_HOST) std::memcpy(poses_out, ph.data(), 96 * num_poses);
+    else CK(cudaMemcpyAsync(poses_out, dposes, 96 * num_poses, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return GVOX_OK;
+}
+
 // ------------------------------------------------------------------ utilities
 const char* gvox_status_string(gvox_status s) {
   switch (s) {

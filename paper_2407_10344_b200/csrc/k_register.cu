@@ -257,7 +257,71 @@ __global__ void __launch_bounds__(32 * kStepWarps)
   }
 }
 
+// Global loop helpers (gvox_optimize_global): T_v <- T_v Exp(delta_v) for every
+// pose (fixed poses carry delta = 0: Exp(0) = I leaves them bit-identical),
+// and the largest |w| and |rho| of the step; one block, fixed-order maxima.
+__global__ void __launch_bounds__(256)
+    k_apply_delta(double* __restrict__ poses, const double* __restrict__ delta, int64_t num_poses,
+                  double* __restrict__ out_max) {
+  __shared__ double mw[256], mr[256];
+  double aw = 0.0, ar = 0.0;
+  for (int64_t v = threadIdx.x; v < num_poses; v += blockDim.x) {
+    const double* d = delta + 6 * v;
+    aw = fmax(aw, sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]));
+    ar = fmax(ar, sqrt(d[3] * d[3] + d[4] * d[4] + d[5] * d[5]));
+    double dR[9], dt[3], T[12];
+    se3_exp_dev(d, dR, dt);
+    for (int i = 0; i < 12; ++i) T[i] = poses[12 * v + i];
+    for (int a = 0; a < 3; ++a) {
+      for (int b = 0; b < 3; ++b)
+        poses[12 * v + a * 4 + b] = T[a * 4 + 0] * dR[0 * 3 + b] + T[a * 4 + 1] * dR[1 * 3 + b] +
+                                    T[a * 4 + 2] * dR[2 * 3 + b];
+      poses[12 * v + a * 4 + 3] = T[a * 4 + 0] * dt[0] + T[a * 4 + 1] * dt[1] + T[a * 4 + 2] * dt[2] + T[a * 4 + 3];
+    }
+  }
+  mw[threadIdx.x] = aw;
+  mr[threadIdx.x] = ar;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      mw[threadIdx.x] = fmax(mw[threadIdx.x], mw[threadIdx.x + o]);
+      mr[threadIdx.x] = fmax(mr[threadIdx.x], mr[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out_max[0] = mw[0];
+    out_max[1] = mr[0];
+  }
+}
+
+// total error of a batch of compact records, fixed order (one block)
+__global__ void __launch_bounds__(256)
+    k_sum_error(const gvox_factor_accum* __restrict__ acc, int64_t n, double* __restrict__ out) {
+  __shared__ double part[256];
+  double s = 0.0;
+  for (int64_t f = threadIdx.x; f < n; f += blockDim.x) s += acc[f].terms[27];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) part[threadIdx.x] += part[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = part[0];
+}
+
 }  // namespace
+
+void launch_apply_delta(double* poses, const double* delta, int64_t num_poses, double* out_max,
+                        cudaStream_t stream) {
+  k_apply_delta<<<1, 256, 0, stream>>>(poses, delta, num_poses, out_max);
+  note_launch();
+}
+
+void launch_sum_error(const gvox_factor_accum* acc, int64_t n, double* out, cudaStream_t stream) {
+  k_sum_error<<<1, 256, 0, stream>>>(acc, n, out);
+  note_launch();
+}
 
 void launch_gn_step(const RegProblem* problems, int32_t num_problems, const int32_t* reg_factors,
                     const FactorDev* factors, const gvox_factor_accum* accum, double* poses,

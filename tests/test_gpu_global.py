@@ -106,3 +106,27 @@ def test_persistent_and_graph_pcg_agree(gv, ctx, graph, monkeypatch):
     d2, r2, _, _ = gv.solve_global(ctx, f, acc, poses, fixed, tol=1e-12, max_iterations=2000)
     assert np.linalg.norm(d1 - d2) <= 1e-8 * np.linalg.norm(d1)
     assert abs(int(r1["iterations"]) - int(r2["iterations"])) <= 1
+
+
+def test_optimize_global_matches_oracle_loop(gv, ctx, oracle, graph):
+    """gvox_optimize_global (relinearize -> assemble -> PCG -> update, on the
+    device) against the oracle's dense loop: same iteration count, errors per
+    iteration within 1e-4, final poses within 1e-4 m / rad (fp32 per-point
+    algebra and PCG tolerance move the fixed point by far less)."""
+    from oracle import global_solve as og
+    sc, f, poses, acc, lin, clouds, maps = graph
+    P = len(poses)
+    fixed = np.zeros(P, np.uint8)
+    fixed[0] = 1
+    out, res, hist = gv.optimize_global(ctx, clouds, maps, f, poses, fixed, max_iterations=8,
+                                        eps_rot=1e-6, eps_trans=1e-5)
+    ocl = [sc.cloud(c) for c in range(sc.num_clouds)]
+    omp = [oracle.VoxelMap(*sc.cloud(int(c))[:2], sc.r0, sc.levels) for c in sc.map_clouds]
+    op, oerr, oconv = og.optimize(ocl, omp, f, poses, fixed.astype(bool), max_iterations=8,
+                                  eps_rot=1e-6, eps_trans=1e-5, num_threads=8)
+    assert int(res["converged"]) == 1 and oconv
+    assert int(res["iterations"]) == len(oerr)
+    np.testing.assert_allclose(hist, oerr, rtol=1e-4)
+    assert np.abs(out[:, 3::4] - op[:, 3::4]).max() <= 1e-4
+    assert np.abs(out[:, [0, 1, 2, 4, 5, 6, 8, 9, 10]] - op[:, [0, 1, 2, 4, 5, 6, 8, 9, 10]]).max() <= 1e-4
+    np.testing.assert_array_equal(out[0], poses[0])  # the fixed pose is untouched

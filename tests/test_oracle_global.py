@@ -80,3 +80,24 @@ def test_two_pose_graph_is_registration_step(oracle, graph):
     np.testing.assert_array_equal(H, lin[0]["H_ii"])
     np.testing.assert_allclose(og.solve(H, b), -np.linalg.solve(lin[0]["H_ii"], lin[0]["b_i"]),
                                rtol=1e-12, atol=1e-15)
+
+
+def test_optimize_converges_to_ground_truth(oracle, graph):
+    """The loop's fixed point: the graph error drops (GN on a re-linearized,
+    re-associated objective is not strictly monotone near the optimum:
+    allow 1e-5 relative wobble per step) and the poses end close to the ground
+    truth they were perturbed from."""
+    sc, clouds, maps, f = graph
+    P = len(sc.poses)
+    fixed = np.zeros(P, bool)
+    fixed[0] = True
+    poses = sc.poses.copy()
+    poses[0] = sc.gt_poses[0]
+    out, errs, conv = og.optimize(clouds, maps, f, poses, fixed, max_iterations=8, eps_rot=1e-7,
+                                  eps_trans=1e-6, num_threads=8)
+    assert conv
+    assert all(b <= a * (1 + 1e-5) for a, b in zip(errs, errs[1:]))
+    assert errs[-1] < 0.1 * errs[0]
+    dt = np.linalg.norm(out[1:, 3::4] - sc.gt_poses[1:, 3::4], axis=1)
+    dt0 = np.linalg.norm(poses[1:, 3::4] - sc.gt_poses[1:, 3::4], axis=1)
+    assert dt.mean() < 0.2 * dt0.mean() and dt.max() < 0.02
