@@ -79,6 +79,15 @@ struct __align__(16) MapLevelDev {
 #ifndef GVOX_TILE_MIN_TILES
 #define GVOX_TILE_MIN_TILES 2
 #endif
+// factors below GVOX_TILE_SMALL_N points (odometry frames, ~20k) are cut into
+// at least GVOX_TILE_MIN_TILES_SMALL tiles: their batches are small, so the
+// tiles must spread over the SMs (still a function of the factor alone)
+#ifndef GVOX_TILE_SMALL_N
+#define GVOX_TILE_SMALL_N 32768
+#endif
+#ifndef GVOX_TILE_MIN_TILES_SMALL
+#define GVOX_TILE_MIN_TILES_SMALL 16
+#endif
 
 constexpr int kDenseBuildRatio = 48;  // max cells per POINT for a dense grid level
 

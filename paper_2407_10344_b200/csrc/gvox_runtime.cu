@@ -1121,8 +1121,9 @@ gvox_status plan_linearize(const char* fn, const gvox_cloud* const* clouds,
     p->fast = p->fast && m->levels == 3 && m->desc.dyadic;
     p->validate = p->validate || (q.flags & GVOX_F_VALIDATE_SURFACE);
     const int64_t n = clouds[q.source_cloud]->n;
+    const int mt = n < GVOX_TILE_SMALL_N ? std::max(min_tiles, GVOX_TILE_MIN_TILES_SMALL) : min_tiles;
     int ppt = 1;
-    while (ppt < GVOX_TILE_MAX_PPT && (int64_t)256 * min_tiles * (ppt * 2) <= n) ppt *= 2;
+    while (ppt < GVOX_TILE_MAX_PPT && (int64_t)256 * mt * (ppt * 2) <= n) ppt *= 2;
     const int tile_pts = 256 * ppt;
     const int64_t nt = (n + tile_pts - 1) / tile_pts;
     if ((int64_t)p->tstart[f] + nt > INT32_MAX)

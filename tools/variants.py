@@ -29,6 +29,11 @@ VARIANTS = {
     "t128_b2": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=2"],
     "t256_b1": ["GVOX_LIN_THREADS=256", "GVOX_LIN_MINB=1"],
     "t128_b5": ["GVOX_LIN_THREADS=128", "GVOX_LIN_MINB=5"],
+    "small2": ["GVOX_TILE_MIN_TILES_SMALL=2"],
+    "small4": ["GVOX_TILE_MIN_TILES_SMALL=4"],
+    "small8": ["GVOX_TILE_MIN_TILES_SMALL=8"],
+    "small16": ["GVOX_TILE_MIN_TILES_SMALL=16"],
+    "small32": ["GVOX_TILE_MIN_TILES_SMALL=32"],
     "t64_b8": ["GVOX_LIN_THREADS=64", "GVOX_LIN_MINB=8"],
     # overlap kernel (stage times from a full bench run)
     "ovl_base": [],
