@@ -463,6 +463,23 @@ def main():
                  "frac": ach_i / peak_i, "warp_instructions_per_point_factor": inst_pf,
                  "source": "profiles/linearize_dram_bytes_per_pf.json (ncu smsp__inst_executed)"}
     stages = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for k, v in tm.items()}
+    # SURVEY §8(d) secondary rates (rank-local): per-row throughputs of the step
+    rates = None
+    if lin_n and tm["overlap"][1] and tm["build"][1]:
+        try:
+            inl = gv.records_to_numpy(acc_out[:len(fac)], gv.FACTOR_ACCUM_DTYPE)["inliers"]
+            corr = int(inl.sum())
+        except Exception:  # pragma: no cover
+            corr = None
+        tgt_pts = int(sum(n_pts[int(sc.map_clouds[t])] for t in my_targets))
+        ovl_s = tm["overlap"][0] / tm["overlap"][1] / 1e3
+        bld_s = tm["build"][0] / args.steps / 1e3
+        rates = {"point_factors_per_s_linearize": pf / lin_avg_s,
+                 "point_levels_per_s_linearize": pf * sc.levels / lin_avg_s,
+                 "correspondences_per_s_linearize": (corr / lin_avg_s) if corr is not None else None,
+                 "overlap_pairs_per_s": len(my_pairs) / ovl_s,
+                 "overlap_points_per_s": float(src_n.sum()) / ovl_s,
+                 "build_points_per_s": tgt_pts / bld_s}
     stages["host_wall_ms_per_step"] = {k: v / args.steps for k, v in host_ms.items()}
     dominant = max(tm, key=lambda k: tm[k][0])
 
@@ -568,6 +585,7 @@ def main():
             "precision": "per-point fp32 algebra; fp64 transform, voxel keys, residual base "
                          "and cross-thread accumulation",
             "stages": stages,
+            "rates": rates,
             "roofline": {"kernel": "k_linearize", "bound": "hbm",
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": (achieved / hbm_peak) if achieved else None,
