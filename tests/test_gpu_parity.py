@@ -473,3 +473,51 @@ def test_full_size_submaps_sampled(gv, ctx, oracle):
         keys, means, covs, counts = maps[t].export(ctx, l)
         okeys, omeans, ocovs, ocounts = omaps[t].export(l)
         assert np.array_equal(keys, okeys) and np.array_equal(counts.astype(np.int64), ocounts)
+
+
+@pytest.mark.slow
+def test_full_c5_bench_configuration_sampled(gv, ctx, oracle):
+    """The bench's own workload and launch configuration (BASELINE C5: 2000
+    submaps x 100k points, 204,949 candidate pairs, one gvox_overlap_select
+    over all of them, one gvox_linearize_batch_accum over the ~1.1e5 selected
+    factors, FAST all-dense kernel), checked on sampled outputs the oracle
+    computes one by one: screening decisions against the oracle's exact counts,
+    compact records (expanded) against the oracle's factors."""
+    import torch
+    sc = synth.make("C5")
+    clouds = gv.create_clouds(ctx, torch.from_numpy(sc.mu).cuda(), torch.from_numpy(sc.cov).cuda(),
+                              torch.from_numpy(sc.nrm).cuda(), sc.offsets)
+    maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    sel = gv.overlap_select(ctx, clouds, maps, sc.pairs, sc.poses, sc.overlap_level, 1, 20)
+    fac = np.zeros(len(sc.pairs), gv.FACTOR_DTYPE)
+    for i, name in enumerate(("source_cloud", "target_map", "pose_i", "pose_j")):
+        fac[name] = sc.pairs[:, i]
+    fac = fac[sel.view(bool)]
+    assert len(fac) > 100000
+    acc = gv.device_records(ctx, len(fac), gv.FACTOR_ACCUM_DTYPE)
+    gv.linearize_batch_accum(ctx, clouds, maps, fac, sc.poses, out=acc)
+    rs = np.random.default_rng(7)
+    n = np.diff(sc.offsets)
+    omaps = {}
+
+    def omap(t):
+        if t not in omaps:
+            omaps[t] = oracle.VoxelMap(*sc.cloud(int(sc.map_clouds[t]))[:2], sc.r0, sc.levels)
+        return omaps[t]
+
+    for k in rs.choice(len(sc.pairs), 12, replace=False):
+        p = sc.pairs[k]
+        want = oracle.overlap(sc.cloud(int(p[0]))[0], omap(int(p[1])), sc.poses[p[2]], sc.poses[p[3]],
+                              sc.overlap_level)
+        assert int(sel[k]) == int(20 * want > n[int(p[0])]), k
+    pick = rs.choice(len(fac), 8, replace=False)
+    sub = gv.device_records(ctx, len(pick), gv.FACTOR_ACCUM_DTYPE)
+    sub.copy_(acc[torch.from_numpy(pick).cuda()])
+    full = gv.records_to_numpy(gv.expand(ctx, fac[pick], sc.poses, sub,
+                                         out=gv.device_records(ctx, len(pick), gv.LINEAR_FACTOR_DTYPE)))
+    for j, k in enumerate(pick):
+        f = fac[k]
+        mu, cov, nrm = sc.cloud(int(f["source_cloud"]))
+        ref = oracle.linearize(mu, cov, None, omap(int(f["target_map"])), sc.poses[f["pose_i"]],
+                               sc.poses[f["pose_j"]])
+        compare_factor(full[j], ref, sc.levels, what=f"C5 factor {k}")
