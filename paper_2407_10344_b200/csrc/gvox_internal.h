@@ -89,7 +89,10 @@ struct __align__(16) MapLevelDev {
 #define GVOX_TILE_MIN_TILES_SMALL 16
 #endif
 
-constexpr int kDenseBuildRatio = 48;  // max cells per POINT for a dense grid level
+#ifndef GVOX_DENSE_RATIO
+#define GVOX_DENSE_RATIO 192
+#endif
+constexpr int kDenseBuildRatio = GVOX_DENSE_RATIO;  // max cells per POINT for a dense grid level
 
 struct MapDev {
   int32_t levels;

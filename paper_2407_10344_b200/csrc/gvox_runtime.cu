@@ -165,6 +165,7 @@ struct gvox_ctx {
   cudaStream_t cap_stream = nullptr;
   void* pin_out = nullptr;
   size_t pin_out_bytes = 0;
+  uint64_t dense_budget = 16ull << 30;  // bytes of dense index grids per build chunk
 };
 
 struct gvox_cloud {
@@ -295,6 +296,10 @@ gvox_status gvox_ctx_create(int device, void* cuda_stream, gvox_ctx** out) {
   DeviceGuard g(device);
   auto* c = new gvox_ctx;
   c->device = device;
+  {
+    size_t free_b = 0, tot_b = 0;
+    if (cudaMemGetInfo(&free_b, &tot_b) == cudaSuccess) c->dense_budget = tot_b / 4;
+  }
   c->stream = (cudaStream_t)cuda_stream;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -515,7 +520,8 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   // Dense: an int32 grid over the level's key box when it has at most
   // kDenseBuildRatio cells per point (memory <= 4 kDenseBuildRatio B per
   // point and level), every dimension < 2^30 (the lookups rely on it) and
-  // < 2^31 cells.  Otherwise a hash table sized after the voxel count is known.
+  // < 2^31 cells, within the chunk's dense budget (below).  Otherwise a hash
+  // table sized after the voxel count is known.
   struct LevelPlan {
     bool dense = false;
     int32_t x0 = 0, y0 = 0, z0 = 0;
@@ -553,9 +559,31 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
         p.x0 = lo3[0]; p.y0 = lo3[1]; p.z0 = lo3[2];
         p.dx = n3[0]; p.dy = n3[1]; p.dz = n3[2];
         p.cells = cells;
-        p.o_grid = gl.add(cells * 4);
       }
     }
+  }
+  // Dense grids trade HBM for one-load lookups; keep the chunk's grids within
+  // a budget (a quarter of the device memory, GVOX_DENSE_BUDGET_MB overrides)
+  // by demoting the largest grids to hash levels.
+  {
+    uint64_t total_cells = 0;
+    for (const LevelPlan& p : plan)
+      if (p.dense) total_cells += p.cells;
+    uint64_t budget = ctx->dense_budget;
+    if (const char* e = std::getenv("GVOX_DENSE_BUDGET_MB")) budget = (uint64_t)std::atoll(e) << 20;
+    if (4 * total_cells > budget) {
+      std::vector<size_t> idx;
+      for (size_t i = 0; i < plan.size(); ++i)
+        if (plan[i].dense) idx.push_back(i);
+      std::sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return plan[a].cells > plan[b].cells; });
+      for (size_t i : idx) {
+        if (4 * total_cells <= budget) break;
+        total_cells -= plan[i].cells;
+        plan[i] = LevelPlan{};
+      }
+    }
+    for (LevelPlan& p : plan)
+      if (p.dense) p.o_grid = gl.add(p.cells * 4);
   }
   DebugClock dbg;
   dbg.lap("plan");

@@ -521,3 +521,29 @@ def test_full_c5_bench_configuration_sampled(gv, ctx, oracle):
         ref = oracle.linearize(mu, cov, None, omap(int(f["target_map"])), sc.poses[f["pose_i"]],
                                sc.poses[f["pose_j"]])
         compare_factor(full[j], ref, sc.levels, what=f"C5 factor {k}")
+
+
+def test_dense_and_hash_levels_agree(gv, ctx, monkeypatch):
+    """The two voxel index structures (dense grids, hash tables) give identical
+    maps and bitwise identical linearizations and overlap counts: the build is
+    forced to hash every level with a zero dense budget."""
+    sc = synth.global_scene(n_submaps=6, n_points=20000, half_blocks=2, factor_dist=40.0,
+                            cand_dist=60.0)
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    f = sc.factors.copy()
+    f[:, 4] = 0
+    dense = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    monkeypatch.setenv("GVOX_DENSE_BUDGET_MB", "0")
+    hashed = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    monkeypatch.delenv("GVOX_DENSE_BUDGET_MB")
+    for m1, m2 in zip(dense, hashed):
+        for l in range(sc.levels):
+            a, b = m1.export(ctx, l), m2.export(ctx, l)
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y)
+    r1 = gv.linearize_batch(ctx, clouds, dense, f, sc.poses)
+    r2 = gv.linearize_batch(ctx, clouds, hashed, f, sc.poses)
+    assert r1.tobytes() == r2.tobytes()
+    c1 = gv.overlap(ctx, clouds, dense, sc.pairs, sc.poses, sc.overlap_level)
+    c2 = gv.overlap(ctx, clouds, hashed, sc.pairs, sc.poses, sc.overlap_level)
+    assert np.array_equal(c1, c2)

@@ -34,6 +34,9 @@ VARIANTS = {
     "small8": ["GVOX_TILE_MIN_TILES_SMALL=8"],
     "small16": ["GVOX_TILE_MIN_TILES_SMALL=16"],
     "small32": ["GVOX_TILE_MIN_TILES_SMALL=32"],
+    "dense48": ["GVOX_DENSE_RATIO=48"],
+    "dense96": ["GVOX_DENSE_RATIO=96"],
+    "dense192": ["GVOX_DENSE_RATIO=192"],
     "t64_b8": ["GVOX_LIN_THREADS=64", "GVOX_LIN_MINB=8"],
     # overlap kernel (stage times from a full bench run)
     "ovl_base": [],
