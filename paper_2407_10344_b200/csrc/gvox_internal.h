@@ -90,7 +90,7 @@ struct __align__(16) MapLevelDev {
 #endif
 
 #ifndef GVOX_DENSE_RATIO
-#define GVOX_DENSE_RATIO 192
+#define GVOX_DENSE_RATIO 2048
 #endif
 constexpr int kDenseBuildRatio = GVOX_DENSE_RATIO;  // max cells per POINT for a dense grid level
 

@@ -532,6 +532,8 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   };
   std::vector<LevelPlan> plan((size_t)count * L);
   Layout gl;  // grid arena
+  uint64_t dense_ratio = kDenseBuildRatio;  // GVOX_DENSE_RATIO env: experiments
+  if (const char* e = std::getenv("GVOX_DENSE_RATIO")) dense_ratio = (uint64_t)std::max(0ll, std::atoll(e));
   for (int64_t s = 0; s < count; ++s) {
     const gvox_cloud* c = clouds[s];
     int32_t k0lo[3] = {0, 0, 0}, k0hi[3] = {0, 0, 0};
@@ -553,7 +555,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
         cells *= (uint64_t)n3[a];
       }
       const bool dims_ok = n3[0] < (1 << 30) && n3[1] < (1 << 30) && n3[2] < (1 << 30);
-      if (c->n > 0 && dims_ok && cells <= (uint64_t)kDenseBuildRatio * (uint64_t)c->n &&
+      if (c->n > 0 && dims_ok && cells <= dense_ratio * (uint64_t)c->n &&
           cells < (1ull << 31)) {
         p.dense = true;
         p.x0 = lo3[0]; p.y0 = lo3[1]; p.z0 = lo3[2];

@@ -396,7 +396,10 @@ def test_fast_kernel_equals_generic(gv, ctx, monkeypatch, flags, which, request)
     arithmetic in the same order as the generic one."""
     sc = synth.make("C2") if which == "C2-hash" else request.getfixturevalue("dense_scene")
     clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    if which == "C2-hash":  # every level a hash table (zero dense-grid budget)
+        monkeypatch.setenv("GVOX_DENSE_BUDGET_MB", "0")
     maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    monkeypatch.delenv("GVOX_DENSE_BUDGET_MB", raising=False)
     f = sc.factors.copy()
     f[:, 4] = flags
     fast = gv.linearize_batch(ctx, clouds, maps, f, sc.poses)
