@@ -312,6 +312,7 @@ def main():
     acc_out = gv.device_records(ctx, max(len(my_pairs), len(sc.factors), 1), gv.FACTOR_ACCUM_DTYPE)
     counts_h = np.zeros(len(my_pairs), np.int32)
     sel_h = np.zeros(len(my_pairs), np.uint8)
+    sel_d = torch.empty(max(len(my_pairs), 1), dtype=torch.uint8, device=dev)
 
     state = {}
 
@@ -323,24 +324,34 @@ def main():
         maps = gv.create_voxelmaps(ctx, my_target_clouds, sc.r0, sc.levels)        # S1
         marr = gv.HandleArray(maps)
         t1 = time.perf_counter()
-        if select:  # S2 as the screening decision: overlap exceeds 5 %
-            gv.overlap_select(ctx, cloud_arr, marr, pairs_s, poses, sc.overlap_level, 1, 20,
-                              out=sel_h)
-        else:       # S2 as overlap counts of the config's pairs
-            gv.overlap(ctx, cloud_arr, marr, pairs_s, poses, sc.overlap_level, out=counts_h)
-        t2 = time.perf_counter()
         if select:
-            fac = all_fac[sel_h.view(bool)]
+            # S2 as the screening decision (overlap exceeds 5 %), kept on
+            # the device; S3-S7 over the selected candidates, compacted on the
+            # device (one 8-byte readback of the batch size, no host round trip
+            # of the decisions before the launch)
+            gv.overlap_select(ctx, cloud_arr, marr, pairs_s, poses, sc.overlap_level, 1, 20,
+                              out=sel_d)
+            t2 = time.perf_counter()
+            ns = gv.linearize_batch_accum_select(ctx, cloud_arr, marr, all_fac, sel_d, poses,
+                                                 acc_out, selected_host=sel_h)
+            t3 = time.perf_counter()
+            fac = all_fac[sel_h.view(bool)]  # host bookkeeping, overlaps the linearization
+            assert len(fac) == ns
+            t4 = time.perf_counter()
+            dt_sel, dt_lin = t4 - t3, t3 - t2
         else:
+            # S2 as overlap counts of the config's pairs, then S3-S7
+            gv.overlap(ctx, cloud_arr, marr, pairs_s, poses, sc.overlap_level, out=counts_h)
+            t2 = time.perf_counter()
             fac = fixed
-        out = acc_out[:len(fac)]
-        t3 = time.perf_counter()
-        gv.linearize_batch_accum(ctx, cloud_arr, marr, fac, poses, out=out)         # S3-S7
-        t4 = time.perf_counter()
+            t3 = time.perf_counter()
+            gv.linearize_batch_accum(ctx, cloud_arr, marr, fac, poses, out=acc_out[:len(fac)])
+            t4 = time.perf_counter()
+            dt_sel, dt_lin = t3 - t2, t4 - t3
         host_ms["build_call"] += 1e3 * (t1 - t0)
         host_ms["overlap_call"] += 1e3 * (t2 - t1)
-        host_ms["select"] += 1e3 * (t3 - t2)
-        host_ms["linearize_call"] += 1e3 * (t4 - t3)
+        host_ms["select"] += 1e3 * dt_sel
+        host_ms["linearize_call"] += 1e3 * dt_lin
         if world > 1:
             # the one exchange: all-gather of the compact per-factor records
             state["gathered"], _ = gdist.gather_records(acc_out, len(fac), state["fmax"])

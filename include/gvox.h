@@ -333,6 +333,28 @@ gvox_status gvox_linearize_batch_accum(gvox_ctx* ctx, const gvox_cloud* const* c
                                        int64_t num_factors, const double* poses, int64_t num_poses,
                                        gvox_factor_accum* out, int mem);
 
+/* Screened batch (P:391 factor creation followed by the Fig. 4 / P:224 batched
+   linearization, with the screening decision kept on the device):
+   candidates[p] (host, num_candidates) is a factor for every candidate pair;
+   selected (DEVICE, uint8 [num_candidates]) is e.g. gvox_overlap_select's
+   output with mem = GVOX_DEVICE.  The selected candidates, in candidate order,
+   are compacted ON THE DEVICE and linearized exactly as
+   gvox_linearize_batch_accum would linearize that list (the same records
+   bitwise: a factor's result depends on the factor alone): out[k] (DEVICE,
+   capacity num_candidates) is the k-th selected candidate's record,
+   k < *num_selected (host out).  selected_host (optional, HOST,
+   num_candidates bytes) receives a copy of the decisions.  One H2D (the
+   candidate table), one 8-byte D2H of the selected and tile counts (plus the
+   optional decision copy) before the launch; returns with the linearization
+   enqueued on ctx's stream.  Errors as gvox_linearize_batch_accum. */
+gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                              int64_t num_clouds, const gvox_map* const* maps,
+                                              int64_t num_maps, const gvox_factor* candidates,
+                                              int64_t num_candidates, const uint8_t* selected,
+                                              const double* poses, int64_t num_poses,
+                                              gvox_factor_accum* out, int64_t* num_selected,
+                                              uint8_t* selected_host);
+
 /* Expand compact records (DEVICE, e.g. after an all-gather) into full records:
    accum[k] belongs to factors[k]; poses as in gvox_linearize_batch (host).
    out in `mem`. */

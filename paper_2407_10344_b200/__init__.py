@@ -11,7 +11,8 @@ from ._lib import (FACTOR_ACCUM_DTYPE, FACTOR_DTYPE, F_ERROR_ONLY, F_VALIDATE_SU
                    REGISTER_RESULT_DTYPE, GvoxError, launch_count, lib, version)
 from .api import (Cloud, Context, HandleArray, VoxelMap, as_factors, as_pairs, as_poses,
                   corr_dump_size, create_clouds, create_voxelmap, create_voxelmaps, device_records, expand,
-                  full_blocks, linearize_batch, linearize_batch_accum, overlap, overlap_select,
+                  full_blocks, linearize_batch, linearize_batch_accum, linearize_batch_accum_select,
+                  overlap, overlap_select,
                   records_to_numpy, register_batch, overlap_union, keyframe_update,
                   KeyframeList, knn, estimate_covariances, solve_global,
                   optimize_global)
@@ -20,7 +21,8 @@ lib()  # fail loudly at import if the CUDA library is absent
 
 __all__ = [
     "Cloud", "Context", "VoxelMap", "HandleArray", "create_clouds", "create_voxelmap", "create_voxelmaps",
-    "overlap", "overlap_select", "linearize_batch", "linearize_batch_accum", "expand", "device_records",
+    "overlap", "overlap_select", "linearize_batch", "linearize_batch_accum",
+    "linearize_batch_accum_select", "expand", "device_records",
     "records_to_numpy", "register_batch", "overlap_union", "keyframe_update", "KeyframeList", "knn", "estimate_covariances", "solve_global", "optimize_global", "full_blocks", "corr_dump_size", "as_factors", "as_pairs", "as_poses",
     "FACTOR_DTYPE", "PAIR_DTYPE", "LINEAR_FACTOR_DTYPE", "FACTOR_ACCUM_DTYPE", "MAX_LEVELS",
     "F_VALIDATE_SURFACE", "F_ERROR_ONLY", "GVOX_HOST", "GVOX_DEVICE", "GvoxError",

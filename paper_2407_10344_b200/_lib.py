@@ -62,7 +62,8 @@ SYMBOLS = [
     "gvox_cloud_destroy",
     "gvox_create_voxelmap", "gvox_create_voxelmaps", "gvox_voxelmap_info", "gvox_voxelmap_levels",
     "gvox_voxelmap_export", "gvox_voxelmap_lookup", "gvox_map_destroy",
-    "gvox_overlap", "gvox_overlap_select", "gvox_linearize_batch", "gvox_linearize_batch_accum", "gvox_expand",
+    "gvox_overlap", "gvox_overlap_select", "gvox_linearize_batch", "gvox_linearize_batch_accum",
+    "gvox_linearize_batch_accum_select", "gvox_expand",
     "gvox_register_batch", "gvox_overlap_union", "gvox_keyframe_update", "gvox_knn",
     "gvox_estimate_covariances", "gvox_solve_global", "gvox_optimize_global",
     "gvox_status_string", "gvox_last_error", "gvox_launch_count", "gvox_version",
@@ -109,6 +110,7 @@ def lib():
         "gvox_overlap_select": (I32, [P, P, I64, P, I64, P, I64, P, I64, I32, I32, I32, P, I32]),
         "gvox_linearize_batch": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32, P]),
         "gvox_linearize_batch_accum": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32]),
+        "gvox_linearize_batch_accum_select": (I32, [P, P, I64, P, I64, P, I64, P, P, I64, P, P, P]),
         "gvox_expand": (I32, [P, P, I64, P, I64, P, P, I32]),
         "gvox_solve_global": (I32, [P, P, I64, P, P, I64, P, P, P, P, P, P, I32]),
         "gvox_optimize_global": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, P, P, P, P, I32]),

@@ -326,6 +326,32 @@ def linearize_batch_accum(ctx: Context, clouds, maps, factors, poses, out=None):
     return out
 
 
+def linearize_batch_accum_select(ctx: Context, clouds, maps, candidates, selected, poses, out,
+                                 selected_host=None):
+    """gvox_linearize_batch_accum_select: linearize the candidates whose device
+    decision `selected` (uint8 CUDA tensor, e.g. overlap_select(..., out=<CUDA
+    tensor>)) is set, compacted on the device in candidate order, into the
+    uint8 CUDA tensor `out` ([>= len(candidates), 288]).  Returns the number
+    selected; `selected_host` (optional uint8 numpy array) receives the
+    decisions."""
+    C, M = _handles(clouds), _handles(maps)
+    candidates = as_factors(candidates)
+    poses = as_poses(poses)
+    F = candidates.shape[0]
+    assert _is_cuda_tensor(selected) and _is_cuda_tensor(out)
+    assert selected.numel() >= F and out.shape[0] >= F
+    ns = ctypes.c_int64(0)
+    sh = None
+    if selected_host is not None:
+        assert selected_host.dtype == np.uint8 and selected_host.shape[0] >= F
+        sh = _ptr(selected_host)[0]
+    check(lib().gvox_linearize_batch_accum_select(
+        ctx.handle, C.arr, C.n, M.arr, M.n, _ptr(candidates)[0], F,
+        ctypes.c_void_p(selected.data_ptr()), _ptr(poses)[0], poses.shape[0],
+        ctypes.c_void_p(out.data_ptr()), ctypes.byref(ns), sh))
+    return int(ns.value)
+
+
 def expand(ctx: Context, factors, poses, accum, out=None):
     """gvox_expand: compact records (uint8 CUDA tensor [F, 288]) -> full records."""
     factors = as_factors(factors)

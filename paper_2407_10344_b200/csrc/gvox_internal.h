@@ -359,6 +359,10 @@ void launch_sum_error(const gvox_factor_accum* acc, int64_t n, double* out, cuda
 // tile -> owning item (factor or pair) table from the tile prefix sums
 void launch_tile_map(const int32_t* tile_start, int64_t num_items, int32_t* tile_owner,
                      cudaStream_t stream);
+// compact the selected candidates (device plan of gvox_linearize_batch_accum_select)
+void launch_select_plan(const uint8_t* selected, const int32_t* ntiles, const FactorDev* factors,
+                        int64_t num_cand, FactorDev* factors_c, int32_t* tile_start_c,
+                        int32_t* counts, cudaStream_t stream);
 
 void note_launch();
 

@@ -165,6 +165,7 @@ struct gvox_ctx {
   cudaStream_t cap_stream = nullptr;
   void* pin_out = nullptr;
   size_t pin_out_bytes = 0;
+  int32_t* pin_counts = nullptr;  // pinned {S, T} of gvox_linearize_batch_accum_select
   uint64_t dense_budget = 16ull << 30;  // bytes of dense index grids per build chunk
 };
 
@@ -330,6 +331,7 @@ void gvox_ctx_destroy(gvox_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   if (ctx->pin) cudaFreeHost(ctx->pin);
   if (ctx->pin_out) cudaFreeHost(ctx->pin_out);
+  if (ctx->pin_counts) cudaFreeHost(ctx->pin_counts);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->pin_done) cudaEventDestroy(ctx->pin_done);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1276,6 +1278,103 @@ gvox_status gvox_linearize_batch_accum(gvox_ctx* ctx, const gvox_cloud* const* c
   if (!out && num_factors > 0) return fail(GVOX_ERR_INVALID, "gvox_linearize_batch_accum: out is NULL");
   return linearize_impl(ctx, clouds, num_clouds, maps, num_maps, factors, num_factors, poses,
                         num_poses, nullptr, out, mem, nullptr);
+}
+
+gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* const* clouds,
+                                              int64_t num_clouds, const gvox_map* const* maps,
+                                              int64_t num_maps, const gvox_factor* candidates,
+                                              int64_t num_candidates, const uint8_t* selected,
+                                              const double* poses, int64_t num_poses,
+                                              gvox_factor_accum* out, int64_t* num_selected,
+                                              uint8_t* selected_host) {
+  const char* fn = "gvox_linearize_batch_accum_select";
+  if (!ctx) return fail(GVOX_ERR_INVALID, "%s: ctx is NULL", fn);
+  if (num_candidates < 0) return fail(GVOX_ERR_INVALID, "%s: num_candidates < 0", fn);
+  if (!num_selected) return fail(GVOX_ERR_INVALID, "%s: num_selected is NULL", fn);
+  *num_selected = 0;
+  if (num_candidates == 0) return GVOX_OK;
+  if (!clouds || !maps || !candidates || !selected || !poses || !out)
+    return fail(GVOX_ERR_INVALID, "%s: NULL argument", fn);
+  if (num_candidates > INT32_MAX) return fail(GVOX_ERR_INVALID, "%s: more than 2^31 candidates", fn);
+  gvox_status st = validate_factors(fn, clouds, num_clouds, maps, num_maps, candidates,
+                                    num_candidates, poses, num_poses);
+  if (st) return st;
+  DeviceGuard g(ctx->device);
+  // host plan of every candidate (tiles are a function of the factor alone, so
+  // the selected subset's tiles are exactly gvox_linearize_batch_accum's)
+  LinPlan plan;
+  st = plan_linearize(fn, clouds, maps, candidates, num_candidates,
+                      std::getenv("GVOX_LIN_GENERIC") == nullptr, &plan);
+  if (st) return st;
+  const int64_t T_all = plan.tstart[num_candidates];
+  std::vector<int32_t> ntiles(num_candidates);
+  for (int64_t p = 0; p < num_candidates; ++p) ntiles[p] = plan.tstart[p + 1] - plan.tstart[p];
+  // ---- the single serialized input block
+  Layout lay;
+  size_t o_pose = lay.add(96 * num_poses);
+  size_t o_fac = lay.add(sizeof(FactorDev) * num_candidates);
+  size_t o_nt = lay.add(4 * num_candidates);
+  size_t o_cl = lay.add(8 * num_clouds);
+  size_t o_mp = lay.add(8 * num_maps);
+  const size_t in_bytes = lay.size;
+  void* pin = nullptr;
+  st = pin_reserve(ctx, in_bytes, &pin);
+  if (st) return st;
+  char* hp = (char*)pin;
+  std::memcpy(hp + o_pose, poses, 96 * num_poses);
+  std::memcpy(hp + o_fac, plan.fdev.data(), sizeof(FactorDev) * num_candidates);
+  std::memcpy(hp + o_nt, ntiles.data(), 4 * num_candidates);
+  for (int64_t i = 0; i < num_clouds; ++i) ((const CloudDev**)(hp + o_cl))[i] = clouds[i] ? clouds[i]->dev : nullptr;
+  for (int64_t i = 0; i < num_maps; ++i) ((const MapDev**)(hp + o_mp))[i] = maps[i] ? maps[i]->dev : nullptr;
+  // ---- device workspace (partials and tile map sized for every candidate)
+  Layout wl;
+  size_t o_in = wl.add(in_bytes);
+  size_t o_part = wl.add(8 * kPartialStride * (size_t)std::max<int64_t>(T_all, 1));
+  size_t o_tf = wl.add(4 * (size_t)std::max<int64_t>(T_all, 1));
+  size_t o_fc = wl.add(sizeof(FactorDev) * num_candidates);
+  size_t o_tsc = wl.add(4 * (num_candidates + 1));
+  size_t o_cnt = wl.add(8);
+  void* ws = nullptr;
+  st = ws_reserve(ctx, 0, wl.size, &ws);
+  if (st) return st;
+  char* wb = (char*)ws;
+  st = h2d_block(ctx, wb + o_in, hp, in_bytes);
+  if (st) return st;
+  char* din = wb + o_in;
+  FactorDev* fc = (FactorDev*)(wb + o_fc);
+  int32_t* tsc = (int32_t*)(wb + o_tsc);
+  int32_t* dcnt = (int32_t*)(wb + o_cnt);
+  launch_select_plan(selected, (const int32_t*)(din + o_nt), (const FactorDev*)(din + o_fac),
+                     num_candidates, fc, tsc, dcnt, ctx->stream);
+  CK_LAUNCH("select plan");
+  // the one readback before the launch: {S, T} (the grid size)
+  if (!ctx->pin_counts) {
+    cudaError_t e = cudaHostAlloc((void**)&ctx->pin_counts, 64, cudaHostAllocDefault);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
+  }
+  CK(cudaMemcpyAsync(ctx->pin_counts, dcnt, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (selected_host)
+    CK(cudaMemcpyAsync(selected_host, selected, num_candidates, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int64_t S = ctx->pin_counts[0], T = ctx->pin_counts[1];
+  *num_selected = S;
+  if (S == 0) return GVOX_OK;
+  launch_tile_map(tsc, S, (int32_t*)(wb + o_tf), ctx->stream);
+  {
+    TimerScope ts(ctx, GVOX_TIMER_LINEARIZE);
+    launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp), fc,
+                     tsc, S, T, 0, plan.max_levels, (const double*)(din + o_pose),
+                     (double*)(wb + o_part), (int32_t*)(wb + o_tf), nullptr, plan.all_dense,
+                     plan.fast, plan.validate, ctx->stream);
+  }
+  CK_LAUNCH("linearize");
+  {
+    TimerScope ts(ctx, GVOX_TIMER_REDUCE);
+    launch_reduce(fc, tsc, S, (const double*)(din + o_pose), (const double*)(wb + o_part), nullptr,
+                  out, ctx->stream);
+  }
+  CK_LAUNCH("linearize reduce");
+  return GVOX_OK;
 }
 
 gvox_status gvox_expand(gvox_ctx* ctx, const gvox_factor* factors, int64_t num_factors,

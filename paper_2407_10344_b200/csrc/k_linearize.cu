@@ -931,6 +931,61 @@ void launch_tile_map(const int32_t* tile_start, int64_t num_items, int32_t* tile
   note_launch();
 }
 
+// Device-side plan of a screened batch (gvox_linearize_batch_accum_select):
+// compact the candidates whose selected[p] != 0, in candidate order, into
+// factors_c[0..S), their tile starts tile_start_c[0..S] (tiles per candidate
+// from the host plan, a function of the factor alone) and counts = {S, T}.
+// One CTA: each thread owns a contiguous candidate range; two block scans.
+constexpr int kPlanThreads = 1024;
+__global__ void __launch_bounds__(kPlanThreads)
+    k_select_plan(const uint8_t* __restrict__ selected, const int32_t* __restrict__ ntiles,
+                  const FactorDev* __restrict__ factors, int64_t num_cand,
+                  FactorDev* __restrict__ factors_c, int32_t* __restrict__ tile_start_c,
+                  int32_t* __restrict__ counts) {
+  __shared__ int32_t s_f[kPlanThreads], s_t[kPlanThreads];
+  const int tid = threadIdx.x;
+  const int64_t per = (num_cand + kPlanThreads - 1) / kPlanThreads;
+  const int64_t b = min((int64_t)tid * per, num_cand), e = min(b + per, num_cand);
+  int32_t nf = 0, ntl = 0;
+  for (int64_t p = b; p < e; ++p)
+    if (selected[p]) {
+      ++nf;
+      ntl += ntiles[p];
+    }
+  s_f[tid] = nf;
+  s_t[tid] = ntl;
+  __syncthreads();
+  // inclusive Hillis-Steele scans of the per-thread counts
+  for (int o = 1; o < kPlanThreads; o <<= 1) {
+    const int32_t af = tid >= o ? s_f[tid - o] : 0, at = tid >= o ? s_t[tid - o] : 0;
+    __syncthreads();
+    s_f[tid] += af;
+    s_t[tid] += at;
+    __syncthreads();
+  }
+  int32_t f = s_f[tid] - nf, t = s_t[tid] - ntl;  // exclusive starts
+  for (int64_t p = b; p < e; ++p)
+    if (selected[p]) {
+      factors_c[f] = factors[p];
+      tile_start_c[f] = t;
+      ++f;
+      t += ntiles[p];
+    }
+  if (tid == kPlanThreads - 1) {
+    tile_start_c[f] = t;
+    counts[0] = f;
+    counts[1] = t;
+  }
+}
+
+void launch_select_plan(const uint8_t* selected, const int32_t* ntiles, const FactorDev* factors,
+                        int64_t num_cand, FactorDev* factors_c, int32_t* tile_start_c,
+                        int32_t* counts, cudaStream_t stream) {
+  k_select_plan<<<1, kPlanThreads, 0, stream>>>(selected, ntiles, factors, num_cand, factors_c,
+                                                tile_start_c, counts);
+  note_launch();
+}
+
 void launch_reduce(const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
                    const double* poses, const double* partials, gvox_linear_factor* out_full,
                    gvox_factor_accum* out_accum, cudaStream_t stream) {

@@ -495,10 +495,22 @@ def test_full_c5_bench_configuration_sampled(gv, ctx, oracle):
     fac = np.zeros(len(sc.pairs), gv.FACTOR_DTYPE)
     for i, name in enumerate(("source_cloud", "target_map", "pose_i", "pose_j")):
         fac[name] = sc.pairs[:, i]
+    cand = fac
     fac = fac[sel.view(bool)]
     assert len(fac) > 100000
     acc = gv.device_records(ctx, len(fac), gv.FACTOR_ACCUM_DTYPE)
     gv.linearize_batch_accum(ctx, clouds, maps, fac, sc.poses, out=acc)
+    # the bench's call sequence: device decisions -> device-compacted batch,
+    # bitwise the two-call path's records
+    dsel = torch.empty(len(sc.pairs), dtype=torch.uint8, device=ctx.device)
+    gv.overlap_select(ctx, clouds, maps, sc.pairs, sc.poses, sc.overlap_level, 1, 20, out=dsel)
+    acc2 = gv.device_records(ctx, len(cand), gv.FACTOR_ACCUM_DTYPE)
+    sel_h = np.zeros(len(cand), np.uint8)
+    ns = gv.linearize_batch_accum_select(ctx, clouds, maps, cand, dsel, sc.poses, acc2,
+                                         selected_host=sel_h)
+    assert ns == len(fac) and np.array_equal(sel_h, sel)
+    assert torch.equal(acc2[:ns], acc)
+    del acc2
     rs = np.random.default_rng(7)
     n = np.diff(sc.offsets)
     omaps = {}
@@ -524,6 +536,44 @@ def test_full_c5_bench_configuration_sampled(gv, ctx, oracle):
         ref = oracle.linearize(mu, cov, None, omap(int(f["target_map"])), sc.poses[f["pose_i"]],
                                sc.poses[f["pose_j"]])
         compare_factor(full[j], ref, sc.levels, what=f"C5 factor {k}")
+
+
+@pytest.mark.parametrize("num,den", [(1, 20), (0, 1), (1, 1)])
+def test_linearize_select_equals_two_calls(gv, ctx, num, den):
+    """gvox_linearize_batch_accum_select (decisions stay on the device, the
+    batch is compacted there) gives bitwise the records of gvox_overlap_select
+    to the host + gvox_linearize_batch_accum over the selected list, including
+    all / none selected, and repeated calls are bitwise reproducible."""
+    import torch
+    sc = synth.make("C5", n_submaps=48, half_blocks=4)
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    maps = gv.create_voxelmaps(ctx, clouds, sc.r0, sc.levels)
+    cand = np.zeros(len(sc.pairs), gv.FACTOR_DTYPE)
+    for i, name in enumerate(("source_cloud", "target_map", "pose_i", "pose_j")):
+        cand[name] = sc.pairs[:, i]
+    sel = gv.overlap_select(ctx, clouds, maps, sc.pairs, sc.poses, sc.overlap_level, num, den)
+    fac = cand[sel.view(bool)]
+    dsel = torch.from_numpy(sel).cuda()
+    out = gv.device_records(ctx, len(cand), gv.FACTOR_ACCUM_DTYPE)
+    sel_h = np.full(len(cand), 7, np.uint8)
+    ns = gv.linearize_batch_accum_select(ctx, clouds, maps, cand, dsel, sc.poses, out,
+                                         selected_host=sel_h)
+    assert ns == len(fac) and np.array_equal(sel_h, sel)
+    if num == 1 and den == 1:
+        assert ns == 0
+    if ns:
+        ref = gv.device_records(ctx, ns, gv.FACTOR_ACCUM_DTYPE)
+        gv.linearize_batch_accum(ctx, clouds, maps, fac, sc.poses, out=ref)
+        assert torch.equal(out[:ns], ref)
+        out2 = gv.device_records(ctx, len(cand), gv.FACTOR_ACCUM_DTYPE)
+        assert gv.linearize_batch_accum_select(ctx, clouds, maps, cand, dsel, sc.poses, out2) == ns
+        assert torch.equal(out2[:ns], out[:ns])
+    # errors: a candidate out of range, no candidates
+    bad = cand.copy()
+    bad["target_map"][0] = len(maps)
+    with pytest.raises(gv.GvoxError):
+        gv.linearize_batch_accum_select(ctx, clouds, maps, bad, dsel, sc.poses, out)
+    assert gv.linearize_batch_accum_select(ctx, clouds, maps, cand[:0], dsel, sc.poses, out) == 0
 
 
 def test_dense_and_hash_levels_agree(gv, ctx, monkeypatch):
