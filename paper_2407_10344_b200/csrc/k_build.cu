@@ -120,6 +120,14 @@ __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restri
 #ifndef GVOX_ACC_SEG_MIN
 #define GVOX_ACC_SEG_MIN 1
 #endif
+// accumulation: level-independent covariance terms converted once per point
+#ifndef GVOX_ACC_HOIST
+#define GVOX_ACC_HOIST 1
+#endif
+// segmented sums: only as many doubling rounds as the warp's longest run
+#ifndef GVOX_ACC_MAXRUN
+#define GVOX_ACC_MAXRUN 1
+#endif
 
 template <int kMaxL>
 __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const BuildSeg* __restrict__ segs, int levels, double r0,
@@ -260,6 +268,19 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
   const int32_t k0y = voxel_coord0(y, r0, inv_r0, dyadic);
   const int32_t k0z = voxel_coord0(z, r0, inv_r0, dyadic);
   const float cv[6] = {a.w, b.x, b.y, b.z, b.w, c.x};
+#if GVOX_ACC_HOIST
+  // the covariance terms do not depend on the level: converted and split once.
+  // (Lanes without a voxel need no zeroing: their index is unique to the lane,
+  // so no run or group that is summed contains them.)
+  unsigned cov_lo[6];
+  int cov_hi[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    const unsigned long long f = to_fixed((double)cv[j] * sg.cov_scale);
+    cov_lo[j] = (unsigned)(f & 0xFFFFFFull);
+    cov_hi[j] = (int)((long long)f >> 24);
+  }
+#endif
   for (int l = 0; l < levels; ++l) {
     int32_t sl = valid ? pslot[sg.pl_offset + k * levels + l] : -1;
     int32_t idx;
@@ -270,6 +291,27 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
       idx = sl >= 0 ? (int32_t)(uint32_t)bs.tmp_slots[l][sl].y : -1 - lane;
     }
     const unsigned grp = __match_any_sync(0xffffffffu, idx);
+#if GVOX_ACC_HOIST
+    unsigned lo_c[9];
+    int hi_c[9];
+    {
+      const double r = ldexp(r0, l);
+      const double S = sg.mu_scale[l];
+      const unsigned long long o[3] = {to_fixed((x - (double)(k0x >> l) * r) * S),
+                                       to_fixed((y - (double)(k0y >> l) * r) * S),
+                                       to_fixed((z - (double)(k0z >> l) * r) * S)};
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        lo_c[j] = (unsigned)(o[j] & 0xFFFFFFull);
+        hi_c[j] = (int)((long long)o[j] >> 24);
+      }
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        lo_c[3 + j] = cov_lo[j];
+        hi_c[3 + j] = cov_hi[j];
+      }
+    }
+#else
     unsigned long long v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (sl >= 0) {
       const double r = ldexp(r0, l);
@@ -292,6 +334,7 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
       lo_c[j] = (unsigned)(v[j] & 0xFFFFFFull);
       hi_c[j] = (int)((long long)v[j] >> 24);
     }
+#endif
     unsigned todo = __ballot_sync(0xffffffffu, sl >= 0);
     // many groups (fine levels): segmented suffix sums over RUNS of equal index
     // in lane order (shuffles; cost independent of the group count), one set
@@ -305,8 +348,10 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
       const unsigned after = lane == 31 ? 0u : (H & (0xffffffffu << (lane + 1)));
       const int run_end = after ? __ffs(after) - 2 : 31;
       int cnt = sl >= 0 ? 1 : 0;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
+      // only as many doubling rounds as the warp's longest run needs
+      const int max_run = GVOX_ACC_MAXRUN ? __reduce_max_sync(0xffffffffu, head ? (unsigned)(run_end - lane + 1) : 0u) : 32;
+#pragma unroll 1
+      for (int off = 1; off < max_run; off <<= 1) {
         const bool take = lane + off <= run_end;
 #pragma unroll
         for (int j = 0; j < 9; ++j) {

@@ -25,7 +25,10 @@ for r in rows[2:]:
         continue
     op = toks[1] if toks[0].startswith("@") else toks[0]
     op = op.split(".")[0]
-    n = int(r[iex] or 0)
+    try:
+        n = int(r[iex] or 0)
+    except ValueError:
+        continue
     c[op] += n
     st[op] += int(r[ist] or 0)
     tot += n

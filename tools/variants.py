@@ -43,6 +43,12 @@ VARIANTS = {
     "acc_seg1": ["GVOX_ACC_SEG_MIN=1"],
     "acc_seg6": ["GVOX_ACC_SEG_MIN=6"],
     "acc_noseg": ["GVOX_ACC_SEG_MIN=99"],
+    "acc_base": [],
+    "acc_seg2": ["GVOX_ACC_SEG_MIN=2"],
+    "acc_seg3": ["GVOX_ACC_SEG_MIN=3"],
+    "acc_nohoist": ["GVOX_ACC_HOIST=0"],
+    "acc_nomaxrun": ["GVOX_ACC_MAXRUN=0"],
+    "acc_r01f": ["GVOX_ACC_HOIST=0", "GVOX_ACC_MAXRUN=0"],
     "ovl_b6": ["GVOX_OVL_MINB=6"],
     "ovl_nocull": ["GVOX_OVL_CULL=0"],
 }
