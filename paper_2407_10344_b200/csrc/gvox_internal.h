@@ -362,7 +362,8 @@ void launch_tile_map(const int32_t* tile_start, int64_t num_items, int32_t* tile
 // compact the selected candidates (device plan of gvox_linearize_batch_accum_select)
 void launch_select_plan(const uint8_t* selected, const int32_t* ntiles, const FactorDev* factors,
                         int64_t num_cand, FactorDev* factors_c, int32_t* tile_start_c,
-                        int32_t* counts, cudaStream_t stream);
+                        int32_t* counts, int2* block_tot /* ceil(num_cand / 1024) */,
+                        cudaStream_t stream);
 
 void note_launch();
 

@@ -1334,6 +1334,7 @@ gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* c
   size_t o_fc = wl.add(sizeof(FactorDev) * num_candidates);
   size_t o_tsc = wl.add(4 * (num_candidates + 1));
   size_t o_cnt = wl.add(8);
+  size_t o_bt = wl.add(8 * ((num_candidates + 1023) / 1024));
   void* ws = nullptr;
   st = ws_reserve(ctx, 0, wl.size, &ws);
   if (st) return st;
@@ -1345,7 +1346,7 @@ gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* c
   int32_t* tsc = (int32_t*)(wb + o_tsc);
   int32_t* dcnt = (int32_t*)(wb + o_cnt);
   launch_select_plan(selected, (const int32_t*)(din + o_nt), (const FactorDev*)(din + o_fac),
-                     num_candidates, fc, tsc, dcnt, ctx->stream);
+                     num_candidates, fc, tsc, dcnt, (int2*)(wb + o_bt), ctx->stream);
   CK_LAUNCH("select plan");
   // the one readback before the launch: {S, T} (the grid size)
   if (!ctx->pin_counts) {

@@ -111,10 +111,10 @@ __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restri
 // Grids are 2D: blockIdx.y = segment (cloud), blockIdx.x * blockDim.x +
 // threadIdx.x = point within it, so a block never straddles two maps.
 #ifndef GVOX_INS_MINB
-#define GVOX_INS_MINB 4
+#define GVOX_INS_MINB 8
 #endif
 #ifndef GVOX_ACC_MINB
-#define GVOX_ACC_MINB 3
+#define GVOX_ACC_MINB 4
 #endif
 // accumulation: segmented run sums when a warp has more than this many groups
 #ifndef GVOX_ACC_SEG_MIN
@@ -397,7 +397,10 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
   }
 }
 
-__global__ void k_build_finalize(const FinalSeg* __restrict__ segs,
+#ifndef GVOX_FIN_MINB
+#define GVOX_FIN_MINB 8
+#endif
+__global__ void __launch_bounds__(256, GVOX_FIN_MINB) k_build_finalize(const FinalSeg* __restrict__ segs,
                                  const unsigned long long* __restrict__ acc) {
   const FinalSeg& sg = segs[blockIdx.y];  // one (segment, level) per grid row
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

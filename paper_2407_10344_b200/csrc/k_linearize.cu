@@ -935,54 +935,101 @@ void launch_tile_map(const int32_t* tile_start, int64_t num_items, int32_t* tile
 // compact the candidates whose selected[p] != 0, in candidate order, into
 // factors_c[0..S), their tile starts tile_start_c[0..S] (tiles per candidate
 // from the host plan, a function of the factor alone) and counts = {S, T}.
-// One CTA: each thread owns a contiguous candidate range; two block scans.
+// Two coalesced passes of one thread per candidate: per-block totals, then
+// each block's offset (sum of the earlier blocks' totals), a block scan and
+// the scatter.
 constexpr int kPlanThreads = 1024;
-__global__ void __launch_bounds__(kPlanThreads)
-    k_select_plan(const uint8_t* __restrict__ selected, const int32_t* __restrict__ ntiles,
-                  const FactorDev* __restrict__ factors, int64_t num_cand,
-                  FactorDev* __restrict__ factors_c, int32_t* __restrict__ tile_start_c,
-                  int32_t* __restrict__ counts) {
-  __shared__ int32_t s_f[kPlanThreads], s_t[kPlanThreads];
-  const int tid = threadIdx.x;
-  const int64_t per = (num_cand + kPlanThreads - 1) / kPlanThreads;
-  const int64_t b = min((int64_t)tid * per, num_cand), e = min(b + per, num_cand);
-  int32_t nf = 0, ntl = 0;
-  for (int64_t p = b; p < e; ++p)
-    if (selected[p]) {
-      ++nf;
-      ntl += ntiles[p];
+
+// inclusive block scan of (a, b) over the block's threads; returns the totals
+__device__ __forceinline__ int2 block_scan2(int32_t& a, int32_t& b, int2* s_w) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t xa = __shfl_up_sync(0xffffffffu, a, o), xb = __shfl_up_sync(0xffffffffu, b, o);
+    if (lane >= o) {
+      a += xa;
+      b += xb;
     }
-  s_f[tid] = nf;
-  s_t[tid] = ntl;
+  }
+  if (lane == 31) s_w[warp] = make_int2(a, b);
   __syncthreads();
-  // inclusive Hillis-Steele scans of the per-thread counts
-  for (int o = 1; o < kPlanThreads; o <<= 1) {
-    const int32_t af = tid >= o ? s_f[tid - o] : 0, at = tid >= o ? s_t[tid - o] : 0;
-    __syncthreads();
-    s_f[tid] += af;
-    s_t[tid] += at;
+  if (warp == 0) {
+    int2 v = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t xa = __shfl_up_sync(0xffffffffu, v.x, o), xb = __shfl_up_sync(0xffffffffu, v.y, o);
+      if (lane >= o) {
+        v.x += xa;
+        v.y += xb;
+      }
+    }
+    s_w[lane] = v;  // inclusive warp-total prefix
+  }
+  __syncthreads();
+  if (warp > 0) {
+    a += s_w[warp - 1].x;
+    b += s_w[warp - 1].y;
+  }
+  return s_w[31];
+}
+
+__global__ void __launch_bounds__(kPlanThreads)
+    k_select_count(const uint8_t* __restrict__ selected, const int32_t* __restrict__ ntiles,
+                   int64_t num_cand, int2* __restrict__ block_tot) {
+  __shared__ int2 s_w[32];
+  const int64_t p = (int64_t)blockIdx.x * kPlanThreads + threadIdx.x;
+  int32_t f = p < num_cand && selected[p] ? 1 : 0;
+  int32_t t = f ? ntiles[p] : 0;
+  const int2 tot = block_scan2(f, t, s_w);
+  if (threadIdx.x == 0) block_tot[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kPlanThreads)
+    k_select_scatter(const uint8_t* __restrict__ selected, const int32_t* __restrict__ ntiles,
+                     const FactorDev* __restrict__ factors, int64_t num_cand,
+                     const int2* __restrict__ block_tot, FactorDev* __restrict__ factors_c,
+                     int32_t* __restrict__ tile_start_c, int32_t* __restrict__ counts) {
+  __shared__ int2 s_w[32];
+  __shared__ int2 s_off;
+  // this block's offset: the totals of the blocks before it
+  int32_t of = 0, ot = 0;
+  for (int j = threadIdx.x; j < (int)blockIdx.x; j += kPlanThreads) {
+    const int2 v = block_tot[j];
+    of += v.x;
+    ot += v.y;
+  }
+  {
+    int32_t a = of, b = ot;
+    const int2 tot = block_scan2(a, b, s_w);
+    if (threadIdx.x == 0) s_off = tot;
     __syncthreads();
   }
-  int32_t f = s_f[tid] - nf, t = s_t[tid] - ntl;  // exclusive starts
-  for (int64_t p = b; p < e; ++p)
-    if (selected[p]) {
-      factors_c[f] = factors[p];
-      tile_start_c[f] = t;
-      ++f;
-      t += ntiles[p];
-    }
-  if (tid == kPlanThreads - 1) {
-    tile_start_c[f] = t;
-    counts[0] = f;
-    counts[1] = t;
+  const int2 off = s_off;
+  const int64_t p = (int64_t)blockIdx.x * kPlanThreads + threadIdx.x;
+  const bool sel = p < num_cand && selected[p];
+  const int32_t nt = sel ? ntiles[p] : 0;
+  int32_t f = sel ? 1 : 0, t = nt;
+  const int2 tot = block_scan2(f, t, s_w);
+  if (sel) {
+    const int32_t k = off.x + f - 1;  // exclusive position
+    factors_c[k] = factors[p];
+    tile_start_c[k] = off.y + t - nt;
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    tile_start_c[off.x + tot.x] = off.y + tot.y;
+    counts[0] = off.x + tot.x;
+    counts[1] = off.y + tot.y;
   }
 }
 
 void launch_select_plan(const uint8_t* selected, const int32_t* ntiles, const FactorDev* factors,
                         int64_t num_cand, FactorDev* factors_c, int32_t* tile_start_c,
-                        int32_t* counts, cudaStream_t stream) {
-  k_select_plan<<<1, kPlanThreads, 0, stream>>>(selected, ntiles, factors, num_cand, factors_c,
-                                                tile_start_c, counts);
+                        int32_t* counts, int2* block_tot, cudaStream_t stream) {
+  const unsigned nb = (unsigned)((num_cand + kPlanThreads - 1) / kPlanThreads);
+  k_select_count<<<nb, kPlanThreads, 0, stream>>>(selected, ntiles, num_cand, block_tot);
+  note_launch();
+  k_select_scatter<<<nb, kPlanThreads, 0, stream>>>(selected, ntiles, factors, num_cand, block_tot,
+                                                    factors_c, tile_start_c, counts);
   note_launch();
 }
 

@@ -19,7 +19,10 @@ namespace {
 
 constexpr int kThreads = 256;
 #ifndef GVOX_OVL_MINB
-#define GVOX_OVL_MINB 6
+#define GVOX_OVL_MINB 7
+#endif
+#ifndef GVOX_OVL_LV_SMEM
+#define GVOX_OVL_LV_SMEM 0
 #endif
 #ifndef GVOX_OVL_CULL
 #define GVOX_OVL_CULL 1
@@ -173,7 +176,11 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
     for (int j = 0; j < 9; ++j) Rf[j] = (float)R[j];
   }
   __syncthreads();
+#if GVOX_OVL_LV_SMEM
+  const MapLevelDev& lv = lv_s;  // level descriptor read from shared memory (registers)
+#else
   const MapLevelDev lv = lv_s;
+#endif
   const int dyadic = dyadic_s;
   const float4* __restrict__ A = A_s;
   const int64_t n = n_s;

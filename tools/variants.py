@@ -51,6 +51,19 @@ VARIANTS = {
     "acc_r01f": ["GVOX_ACC_HOIST=0", "GVOX_ACC_MAXRUN=0"],
     "ovl_b6": ["GVOX_OVL_MINB=6"],
     "ovl_nocull": ["GVOX_OVL_CULL=0"],
+    "ovl_b5": ["GVOX_OVL_MINB=5"],
+    "ovl_lvs": ["GVOX_OVL_LV_SMEM=1"],
+    "ovl_b5_lvs": ["GVOX_OVL_MINB=5", "GVOX_OVL_LV_SMEM=1"],
+    "ovl_b8_lvs": ["GVOX_OVL_MINB=8", "GVOX_OVL_LV_SMEM=1"],
+    "ovl_b7": ["GVOX_OVL_MINB=7"],
+    "ovl_b8": ["GVOX_OVL_MINB=8"],
+    "acc_ins6": ["GVOX_INS_MINB=6"],
+    "acc_ins8": ["GVOX_INS_MINB=8"],
+    "acc_acc4": ["GVOX_ACC_MINB=4"],
+    "acc_acc4_ins6": ["GVOX_ACC_MINB=4", "GVOX_INS_MINB=6"],
+    "acc_acc5": ["GVOX_ACC_MINB=5"],
+    "acc_acc4_ins8": ["GVOX_ACC_MINB=4", "GVOX_INS_MINB=8"],
+    "acc_acc4_ins6_fin": ["GVOX_ACC_MINB=4", "GVOX_INS_MINB=6", "GVOX_FIN_MINB=8"],
 }
 
 
