@@ -62,6 +62,11 @@ namespace {
 #ifndef GVOX_LIN_CULL
 #define GVOX_LIN_CULL 1
 #endif
+// FAST pipeline: every level's term evaluated branch-free and masked (ILP across
+// levels) instead of one branch per level
+#ifndef GVOX_LIN_BRANCHLESS
+#define GVOX_LIN_BRANCHLESS 1
+#endif
 #ifndef GVOX_LIN_STAGES
 #define GVOX_LIN_STAGES (GVOX_LIN_PIPE ? 3 : 2)
 #endif
@@ -299,7 +304,7 @@ struct LevelSum {
 template <int MAXL>
 __device__ __forceinline__ void level_term(Acc<MAXL>& ac, LevelSum& ls, const PointData& pd,
                                            const float4 v0, const float4 v1, const float v2,
-                                           const int l, const float r0f) {
+                                           const int l, const float r0f, const bool hit = true) {
   // fused covariance (Eq.3)
   const f2_t P = add2(pk(v1.x, v1.y), pd.Sp1);  // (cb, cd) = (xy, yy)
   const f2_t Q = add2(pk(v1.z, v1.w), pd.Sp2);  // (cc, ce) = (xz, yz)
@@ -315,9 +320,12 @@ __device__ __forceinline__ void level_term(Acc<MAXL>& ac, LevelSum& ls, const Po
   const float det = fmaf(ca, i00, fmaf(cb, i01, cc * i02));
   // Q16: a fused covariance that is not positive definite contributes nothing
   // det > 0 and finite  <=>  bits(det) - 1 < bits(FLT_MAX)  (unsigned)
-  const bool ok = __float_as_uint(det) - 1u < 0x7F7FFFFFu;
+  const bool pd_ok = __float_as_uint(det) - 1u < 0x7F7FFFFFu;
+  // (hit = false: a level without a correspondence, evaluated branch-free and
+  // masked out -- Omega = 0 makes every contribution below exactly zero)
+  const bool ok = pd_ok && hit;
   const float id = ok ? rcp_approx(det) : 0.f;
-  ac.n_degenerate += !ok;
+  ac.n_degenerate += hit && !pd_ok;
   ac.inl[l] += ok;
   const f2_t Om_a = mul2(pk(i00, i01), bc(id));  // (o00, o01) = column 0, rows 0-1
   const f2_t Om_b = mul2(pk(i01, i11), bc(id));  // (o01, o11) = column 1, rows 0-1
@@ -615,6 +623,10 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       float v2[MAXL];
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) {
+        if (GVOX_LIN_BRANCHLESS) {
+          v0[l] = v1[l] = make_float4(0.f, 0.f, 0.f, 0.f);
+          v2[l] = 0.f;
+        }
         if (vid[l] >= 0) {
           const float4* vp = sh.lv[l].vox + 3 * (int64_t)vid[l];
           v0[l] = __ldg(vp);
@@ -629,8 +641,12 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       ls.Oa = ls.Oc = ls.G = 0;
       ls.o11 = ls.o22 = ls.gz = 0.f;
 #pragma unroll
-      for (int l = 0; l < MAXL; ++l)
-        if (vid[l] >= 0) level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, r0f);
+      for (int l = 0; l < MAXL; ++l) {
+        if (GVOX_LIN_BRANCHLESS)
+          level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, r0f, vid[l] >= 0);
+        else if (vid[l] >= 0)
+          level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, r0f);
+      }
       if (!error_only) fold_point<MAXL>(ac, ls, pd);
     }
     tile_reduce<MAXL>(ac, red, partials, tile);

@@ -38,6 +38,7 @@ VARIANTS = {
     "dense96": ["GVOX_DENSE_RATIO=96"],
     "dense192": ["GVOX_DENSE_RATIO=192"],
     "t64_b8": ["GVOX_LIN_THREADS=64", "GVOX_LIN_MINB=8"],
+    "branchless": ["GVOX_LIN_BRANCHLESS=1"],
     # overlap kernel (stage times from a full bench run)
     "ovl_base": [],
     "acc_seg1": ["GVOX_ACC_SEG_MIN=1"],
