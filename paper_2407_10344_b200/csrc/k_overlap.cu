@@ -21,6 +21,11 @@ constexpr int kThreads = 256;
 #ifndef GVOX_OVL_MINB
 #define GVOX_OVL_MINB 7
 #endif
+// screening: sub-steps (256 points each) per decision window (one barrier each);
+// a window is a slice of the 32-bit live-chunk word, so <= 32
+#ifndef GVOX_OVL_WIN
+#define GVOX_OVL_WIN 32
+#endif
 #ifndef GVOX_OVL_LV_SMEM
 #define GVOX_OVL_LV_SMEM 0
 #endif
@@ -205,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   // Windows of kWin sub-steps m (kThreads points each; warp w owns chunk 8 m + w):
   // each warp probes its live (non-culled) chunks of the window without
   // barriers, then one block reduction decides.  Culled chunks hold no hit.
-  constexpr int kWin = 8;
+  constexpr int kWin = GVOX_OVL_WIN;
   const int64_t msteps = (n + kThreads - 1) / kThreads;
   int64_t total = 0;
   int buf = 0;
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
                            map_hi, (cv_s.dense && cv_s.grid) ? &cv_s : nullptr);
       live = ~cull;
     }
-    uint32_t w = (live >> (mw & 31)) & ((1u << kWin) - 1u);
+    uint32_t w = (live >> (mw & 31)) & (kWin >= 32 ? 0xffffffffu : ((1u << (kWin & 31)) - 1u));
     int cnt = 0;
     while (w) {
       const int j0 = __ffs(w) - 1;

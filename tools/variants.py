@@ -58,6 +58,9 @@ VARIANTS = {
     "ovl_b8_lvs": ["GVOX_OVL_MINB=8", "GVOX_OVL_LV_SMEM=1"],
     "ovl_b7": ["GVOX_OVL_MINB=7"],
     "ovl_b8": ["GVOX_OVL_MINB=8"],
+    "ovl_win4": ["GVOX_OVL_WIN=4"],
+    "ovl_win16": ["GVOX_OVL_WIN=16"],
+    "ovl_win32": ["GVOX_OVL_WIN=32"],
     "acc_ins6": ["GVOX_INS_MINB=6"],
     "acc_ins8": ["GVOX_INS_MINB=8"],
     "acc_acc4": ["GVOX_ACC_MINB=4"],
