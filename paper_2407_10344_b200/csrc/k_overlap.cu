@@ -22,7 +22,8 @@ constexpr int kThreads = 256;
 #define GVOX_OVL_MINB 7
 #endif
 // screening: sub-steps (256 points each) per decision window (one barrier each);
-// a window is a slice of the 32-bit live-chunk word, so <= 32
+// (a power of two: windows <= 32 are slices of one 32-bit live-chunk word,
+// larger ones several words)
 #ifndef GVOX_OVL_WIN
 #define GVOX_OVL_WIN 32
 #endif
@@ -216,25 +217,29 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   int buf = 0;
   bool sel = false;
   uint32_t live = 0;  // bits for sub-steps mb .. mb + 31
+  constexpr int kSub = kWin < 32 ? kWin : 32;  // sub-steps per live-word slice
   for (int64_t mw = 0; mw < msteps; mw += kWin) {
-    if ((mw & 31) == 0) {
-      uint32_t cull = 0;
-      if (GVOX_OVL_CULL && cbox)
-        cull = cull_ballot(cbox, mw * (kThreads / 32) + warp, kThreads / 32, nchunks, Rf, t, map_lo,
-                           map_hi, (cv_s.dense && cv_s.grid) ? &cv_s : nullptr);
-      live = ~cull;
-    }
-    uint32_t w = (live >> (mw & 31)) & (kWin >= 32 ? 0xffffffffu : ((1u << (kWin & 31)) - 1u));
     int cnt = 0;
-    while (w) {
-      const int j0 = __ffs(w) - 1;
-      w &= w - 1;
-      if (w) {
-        const int j1 = __ffs(w) - 1;
+#pragma unroll 1
+    for (int64_t mb = mw; mb < mw + kWin && mb < msteps; mb += kSub) {
+      if ((mb & 31) == 0) {
+        uint32_t cull = 0;
+        if (GVOX_OVL_CULL && cbox)
+          cull = cull_ballot(cbox, mb * (kThreads / 32) + warp, kThreads / 32, nchunks, Rf, t,
+                             map_lo, map_hi, (cv_s.dense && cv_s.grid) ? &cv_s : nullptr);
+        live = ~cull;
+      }
+      uint32_t w = (live >> (mb & 31)) & (kSub >= 32 ? 0xffffffffu : ((1u << (kSub & 31)) - 1u));
+      while (w) {
+        const int j0 = __ffs(w) - 1;
         w &= w - 1;
-        cnt += probe(mw + j0) + probe(mw + j1);
-      } else {
-        cnt += probe(mw + j0);
+        if (w) {
+          const int j1 = __ffs(w) - 1;
+          w &= w - 1;
+          cnt += probe(mb + j0) + probe(mb + j1);
+        } else {
+          cnt += probe(mb + j0);
+        }
       }
     }
     cnt = __reduce_add_sync(0xffffffffu, cnt);

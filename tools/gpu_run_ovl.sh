@@ -1,3 +1,3 @@
 # Screening-kernel variants (stage times from full C5 bench runs).
 set -x
-timeout 1200 python tools/variants.py run ovl_base,ovl_win4,ovl_win16,ovl_win32 > gpurun_out/variants_ovl.log 2>&1
+timeout 1200 python tools/variants.py run ovl_base,ovl_win64,ovl_win128 > gpurun_out/variants_ovl.log 2>&1

@@ -61,6 +61,8 @@ VARIANTS = {
     "ovl_win4": ["GVOX_OVL_WIN=4"],
     "ovl_win16": ["GVOX_OVL_WIN=16"],
     "ovl_win32": ["GVOX_OVL_WIN=32"],
+    "ovl_win64": ["GVOX_OVL_WIN=64"],
+    "ovl_win128": ["GVOX_OVL_WIN=128"],
     "acc_ins6": ["GVOX_INS_MINB=6"],
     "acc_ins8": ["GVOX_INS_MINB=8"],
     "acc_acc4": ["GVOX_ACC_MINB=4"],
