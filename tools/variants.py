@@ -39,6 +39,7 @@ VARIANTS = {
     "dense192": ["GVOX_DENSE_RATIO=192"],
     "t64_b8": ["GVOX_LIN_THREADS=64", "GVOX_LIN_MINB=8"],
     "branchless": ["GVOX_LIN_BRANCHLESS=1"],
+    "t160_b3": ["GVOX_LIN_THREADS=160", "GVOX_LIN_MINB=3"],
     # overlap kernel (stage times from a full bench run)
     "ovl_base": [],
     "acc_seg1": ["GVOX_ACC_SEG_MIN=1"],
