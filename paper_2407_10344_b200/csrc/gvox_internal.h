@@ -140,6 +140,18 @@ __host__ __device__ inline bool key_in_range(int32_t k) { return k >= -kKeyHalf 
 // initialise [2..4] to INT_MAX and [5..7] to INT_MIN).
 void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* P,
                        float* chunk_box, int32_t* stats, cudaStream_t stream);
+// the same for every cloud of a batch in one launch (count <= 65535)
+struct PackSeg {
+  const float* mu;
+  const float* cov;
+  const float* nrm;  // or nullptr
+  int64_t n;
+  float4* P;
+  float* chunk_box;
+  int32_t* stats;    // 8 int32 as above
+};
+void launch_cloud_pack_batch(const PackSeg* segs_dev, int64_t count, int64_t max_n,
+                             cudaStream_t stream);
 
 __host__ __device__ inline int32_t float_to_ordered(float f) {
 #ifdef __CUDA_ARCH__

@@ -407,6 +407,7 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
   for (int64_t k = 0; k < count; ++k)
     cb_off[k + 1] = cb_off[k] + 6 * ((offsets[k + 1] - offsets[k] + kChunk - 1) / kChunk);
   size_t o_cbox = lay.add(4 * (size_t)cb_off[count]);
+  size_t o_pseg = lay.add(sizeof(PackSeg) * count);
   std::shared_ptr<DevBuf> buf;
   gvox_status st = devbuf_alloc(lay.size, ctx->device, ctx->stream, &buf);
   if (st) return st;
@@ -441,11 +442,26 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
       dcov = (const float*)(p + n * 12);
       dnrm = normals ? (const float*)(p + n * 36) : nullptr;
     }
-    for (int64_t k = 0; k < count; ++k) {
-      int64_t a = offsets[k], m = offsets[k + 1] - offsets[k];
-      if (m == 0) continue;
-      launch_cloud_pack(dmu + 3 * a, dcov + 6 * a, dnrm ? dnrm + 3 * a : nullptr, m, P + co[k],
-                        cbox + cb_off[k], dflags + 8 * k, ctx->stream);
+    if (count <= 65535) {  // one launch for the batch (grid y = cloud)
+      std::vector<PackSeg> ps(count);
+      int64_t max_n = 0;
+      for (int64_t k = 0; k < count; ++k) {
+        const int64_t a = offsets[k], m = offsets[k + 1] - offsets[k];
+        ps[k] = PackSeg{dmu + 3 * a, dcov + 6 * a, dnrm ? dnrm + 3 * a : nullptr, m, P + co[k],
+                        cbox + cb_off[k], dflags + 8 * k};
+        max_n = std::max(max_n, m);
+      }
+      CK(cudaMemcpyAsync(base + o_pseg, ps.data(), sizeof(PackSeg) * count,
+                         cudaMemcpyHostToDevice, ctx->stream));
+      launch_cloud_pack_batch((const PackSeg*)(base + o_pseg), count, max_n, ctx->stream);
+      CK(cudaStreamSynchronize(ctx->stream));  // ps is a host temporary
+    } else {
+      for (int64_t k = 0; k < count; ++k) {
+        int64_t a = offsets[k], m = offsets[k + 1] - offsets[k];
+        if (m == 0) continue;
+        launch_cloud_pack(dmu + 3 * a, dcov + 6 * a, dnrm ? dnrm + 3 * a : nullptr, m, P + co[k],
+                          cbox + cb_off[k], dflags + 8 * k, ctx->stream);
+      }
     }
     CK_LAUNCH("gvox_cloud_create: pack");
   }

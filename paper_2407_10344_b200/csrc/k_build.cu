@@ -28,9 +28,12 @@ __device__ inline bool finite3(float a, float b, float c) {
   return isfinite(a) && isfinite(b) && isfinite(c);
 }
 
-__global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restrict__ cov,
-                             const float* __restrict__ nrm, int64_t n, float4* __restrict__ P,
-                             float* __restrict__ chunk_box, int32_t* __restrict__ stats) {
+__device__ __forceinline__ void cloud_pack_body(const float* __restrict__ mu,
+                                                const float* __restrict__ cov,
+                                                const float* __restrict__ nrm, int64_t n,
+                                                float4* __restrict__ P,
+                                                float* __restrict__ chunk_box,
+                                                int32_t* __restrict__ stats) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float cm = 0.f;
   bool bad = false;
@@ -100,6 +103,20 @@ __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restri
       if (hi[a] != INT_MIN) atomicMax(stats + 5 + a, hi[a]);
     }
   }
+}
+
+__global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restrict__ cov,
+                             const float* __restrict__ nrm, int64_t n, float4* __restrict__ P,
+                             float* __restrict__ chunk_box, int32_t* __restrict__ stats) {
+  cloud_pack_body(mu, cov, nrm, n, P, chunk_box, stats);
+}
+
+// All clouds of a batch in one launch: blockIdx.y = cloud (blocks past a
+// cloud's end exit; the body has no block barrier).
+__global__ void k_cloud_pack_batch(const PackSeg* __restrict__ segs) {
+  const PackSeg sg = segs[blockIdx.y];
+  if ((int64_t)blockIdx.x * blockDim.x >= sg.n) return;
+  cloud_pack_body(sg.mu, sg.cov, sg.nrm, sg.n, sg.P, sg.chunk_box, sg.stats);
 }
 
 // Both passes aggregate within a warp: lanes holding the same (map, key) --
@@ -466,6 +483,14 @@ void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int6
                        float* chunk_box, int32_t* stats, cudaStream_t stream) {
   if (n <= 0) return;
   k_cloud_pack<<<grid_for(n, 256), 256, 0, stream>>>(mu, cov, nrm, n, P, chunk_box, stats);
+  note_launch();
+}
+
+void launch_cloud_pack_batch(const PackSeg* segs_dev, int64_t count, int64_t max_n,
+                             cudaStream_t stream) {
+  if (count <= 0 || max_n <= 0) return;
+  dim3 grid(grid_for(max_n, 256), (unsigned)count);
+  k_cloud_pack_batch<<<grid, 256, 0, stream>>>(segs_dev);
   note_launch();
 }
 
