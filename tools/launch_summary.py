@@ -19,7 +19,7 @@ for r in rows:
     scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(r[ui], 1e-6)
     tot[name] += float(r[vi].replace(",", "")) * scale
     cnt[name] += 1
-setup = {"k_cloud_pack"}
+setup = {"k_cloud_pack", "k_cloud_pack_batch"}
 hot = sum(v for k, v in tot.items() if k not in setup)
 lines = [f"# {title}", "", "| kernel | launches | total ms | ms / step | share of hot path |",
          "|---|---|---|---|---|"]
