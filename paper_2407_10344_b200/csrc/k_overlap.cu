@@ -27,6 +27,10 @@ constexpr int kThreads = 256;
 #ifndef GVOX_OVL_WIN
 #define GVOX_OVL_WIN 32
 #endif
+// screening: live chunks probed together per thread (2 or 4)
+#ifndef GVOX_OVL_ILP
+#define GVOX_OVL_ILP 4
+#endif
 #ifndef GVOX_OVL_LV_SMEM
 #define GVOX_OVL_LV_SMEM 0
 #endif
@@ -230,6 +234,20 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
         live = ~cull;
       }
       uint32_t w = (live >> (mb & 31)) & (kSub >= 32 ? 0xffffffffu : ((1u << (kSub & 31)) - 1u));
+#if GVOX_OVL_ILP >= 4
+      // up to four live chunks' lookups in flight per thread
+      while (__popc(w) >= 4) {
+        const int j0 = __ffs(w) - 1;
+        w &= w - 1;
+        const int j1 = __ffs(w) - 1;
+        w &= w - 1;
+        const int j2 = __ffs(w) - 1;
+        w &= w - 1;
+        const int j3 = __ffs(w) - 1;
+        w &= w - 1;
+        cnt += (probe(mb + j0) + probe(mb + j1)) + (probe(mb + j2) + probe(mb + j3));
+      }
+#endif
       while (w) {
         const int j0 = __ffs(w) - 1;
         w &= w - 1;

@@ -63,6 +63,8 @@ VARIANTS = {
     "ovl_win16": ["GVOX_OVL_WIN=16"],
     "ovl_win32": ["GVOX_OVL_WIN=32"],
     "ovl_win64": ["GVOX_OVL_WIN=64"],
+    "ovl_ilp4": ["GVOX_OVL_ILP=4"],
+    "ovl_ilp4_b6": ["GVOX_OVL_ILP=4", "GVOX_OVL_MINB=6"],
     "ovl_win128": ["GVOX_OVL_WIN=128"],
     "acc_ins6": ["GVOX_INS_MINB=6"],
     "acc_ins8": ["GVOX_INS_MINB=8"],
