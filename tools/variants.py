@@ -65,6 +65,7 @@ VARIANTS = {
     "ovl_win64": ["GVOX_OVL_WIN=64"],
     "ovl_ilp4": ["GVOX_OVL_ILP=4"],
     "ovl_ilp4_b6": ["GVOX_OVL_ILP=4", "GVOX_OVL_MINB=6"],
+    "ovl_ilp4_lvs": ["GVOX_OVL_LV_SMEM=1"],
     "ovl_win128": ["GVOX_OVL_WIN=128"],
     "acc_ins6": ["GVOX_INS_MINB=6"],
     "acc_ins8": ["GVOX_INS_MINB=8"],
