@@ -74,3 +74,72 @@ def test_union_overlap_pins(oracle):
         assert oracle.overlap_union(src, [mL, mL], Ti, np.stack([I, I]), level) == \
             oracle.overlap(src, mL, Ti, I, level)
         assert oracle.overlap_union(src, [], Ti, np.zeros((0, 12)), level) == 0
+
+
+# ---------------------------------------------------------------------------
+# run_keyframes on a hand-worked sequence (P:280 insertion, P:282-283 removal).
+# Frame f covers the unit cells x in SEQ_CELLS[f] (y = z = 0) of the world,
+# one point per cell centre; it is stored in its own sensor frame under the
+# pose POSE(f) (a multiple of 90 degrees of yaw and an integer translation,
+# so every coordinate is exact).  With r = 1 the overlap o(a, b) is
+# |cells_a & cells_b| / |cells_a| and the union overlap of a frame is
+# |cells_f & (union of the keyframes' cells)| / |cells_f|.  n_odom = 3.
+#
+# f0  0..9   (10)  first frame: inserted.                         kf [0]
+# f1  0..9   (10)  union 10/10 = 100 %: not inserted.             kf [0]
+# f2  5..14  (10)  union 5/10: inserted; o(0,2) = 5/10.           kf [0, 2]
+# f3  9..28  (20)  union {0..14}: 6/20: inserted; 3 <= n_odom.     kf [0, 2, 3]
+# f4  14..33 (20)  union {0..28}: 15/20: inserted.  Rule 1: o(0,4) = 0 -> remove 0;
+#                  o(2,4) = 1/10, o(3,4) = 15/20 stay; 3 remain.   kf [2, 3, 4]
+# f5  16..35 (20)  union {5..33}: 18/20 = 90 % exactly: "smaller than 90 %" is
+#                  false -> not inserted (10 * 18 < 9 * 20 is false).
+# f6  10..39 (30)  union {5..33}: 24/30: inserted.  Rule 1: o(2,6) = 5/10,
+#                  o(3,6) = 19/20, o(4,6) = 20/20 stay; 4 > 3 -> rule 2:
+#                  s(2) = o(2,6)[(1 - o(2,3)) + (1 - o(2,4))] = .5 (.4 + .9)   = .65
+#                  s(3) = o(3,6)[(1 - o(3,2)) + (1 - o(3,4))] = .95 (.7 + .25) = .9025
+#                  s(4) = o(4,6)[(1 - o(4,2)) + (1 - o(4,3))] = 1 (.95 + .25)  = 1.2
+#                  -> remove 2.                                    kf [3, 4, 6]
+# f7  0..25  (26)  union {9..39}: 17/26: inserted.  o(3,7) = 17/20, o(4,7) = 12/20,
+#                  o(6,7) = 16/30: no rule 1.  Rule 2 (4 > 3):
+#                  s(3) = .85 [(1 - o(3,4)) + (1 - o(3,6))] = .85 (.25 + .05)  = .255
+#                  s(4) = .6  [(1 - o(4,3)) + (1 - o(4,6))] = .6 (.25 + 0)     = .15
+#                  s(6) = 16/30 [(1 - 19/30) + (1 - 20/30)] = 16/30 * 21/30    = .373
+#                  -> remove 4.  (With o transposed, s'(i) = o(7,i) sum(1 - o(j,i)),
+#                  the removal would differ.)                      kf [3, 6, 7]
+# f8  28..41 (14)  union {0..39}: 12/14: inserted.  Rule 1: o(3,8) = 1/20 = 5 %
+#                  exactly is NOT below 5 % (kept); o(6,8) = 12/30; o(7,8) = 0 ->
+#                  remove 7.  3 remain.                            kf [3, 6, 8]
+SEQ_CELLS = [range(0, 10), range(0, 10), range(5, 15), range(9, 29), range(14, 34),
+             range(16, 36), range(10, 40), range(0, 26), range(28, 42)]
+SEQ_EVENTS = [(True, []), (False, []), (True, []), (True, []), (True, [0]), (False, []),
+              (True, [2]), (True, [4]), (True, [7])]
+SEQ_FINAL = [3, 6, 8]
+
+
+def _seq_pose(f):
+    c, s = [(1, 0), (0, 1), (-1, 0), (0, -1)][f % 4]
+    T = np.eye(4)
+    T[:3, :3] = [[c, -s, 0], [s, c, 0], [0, 0, 1]]
+    T[:3, 3] = [f - 3, 2 * f, -1]
+    return T
+
+
+def keyframe_sequence():
+    """(clouds [(mu, cov)], poses [F,12]) of the hand-worked sequence."""
+    clouds, poses = [], []
+    for f, cells in enumerate(SEQ_CELLS):
+        T = _seq_pose(f)
+        w = np.array([[x + 0.5, 0.5, 0.5] for x in cells])
+        local = (w - T[:3, 3]) @ T[:3, :3]          # R^T (w - t), exact
+        clouds.append((local.astype(np.float32),
+                       np.tile(np.array([1, 0, 0, 1, 0, 1], np.float32), (len(cells), 1))))
+        poses.append(T[:3].reshape(12))
+    return clouds, np.stack(poses)
+
+
+def test_run_keyframes_hand_worked_sequence(oracle):
+    clouds, poses = keyframe_sequence()
+    maps = [oracle.VoxelMap(mu, cov, 1.0, 1) for mu, cov in clouds]
+    kf, events = okf.run_keyframes(clouds, maps, poses, list(range(len(clouds))), 0, n_odom=3)
+    assert events == SEQ_EVENTS
+    assert kf == SEQ_FINAL
