@@ -306,12 +306,16 @@ def smoother_window(seed=3, n_frames=30, n_kf=20, per_frame=10, n_points=20000, 
 
 
 def submap_scene(name, seed, n_submaps, n_points, half_blocks, factor_dist, cand_dist,
-                 spacing=3.0, frames_per_submap=15, rings=128, az=256, ds_res=0.1,
+                 spacing=3.0, frames_per_submap=15, rings=128, az=1024, ds_res=0.1,
                  order_random=False, threads=None):
     """C4/C5: submaps (15 frames merged in the centre-frame origin) every 3 m
     along a street random walk; factors = pairs (newer source, older target) with
-    ground-truth origin distance < factor_dist; overlap candidates = pairs within
-    cand_dist (stand-in for an AABB prefilter).  r = 0.5/1.0/2.0 m (Q14)."""
+    origin distance < factor_dist; overlap candidates = pairs within cand_dist
+    (stand-in for an AABB prefilter).  Both distances are taken between the
+    LINEARIZATION poses (the perturbed estimates a mapping system holds), not
+    the ground truth.  Submap frames use the sensor's full 1024 azimuth steps
+    (SURVEY 8(d)), enough returns for exactly n_points per submap after the
+    0.1 m downsampling.  r = 0.5/1.0/2.0 m (Q14)."""
     path = StreetPath(seed, n_submaps * spacing + 10.0, half_blocks)
     world = _World(half_blocks)
     s_c = np.array([5.0 + spacing * i for i in range(n_submaps)])
@@ -327,7 +331,8 @@ def submap_scene(name, seed, n_submaps, n_points, half_blocks, factor_dist, cand
     frames = np.stack(frames)
     mu, cov, nrm, off = _make_clouds(world.h, frames, origins, frames_per_submap, rings, az,
                                      ds_res, n_points, seed, 0, order_random, threads)
-    pos = origins.reshape(-1, 3, 4)[:, :, 3]
+    lin = perturb_poses(origins, seed + 100)
+    pos = lin.reshape(-1, 3, 4)[:, :, 3]
     fl, pl = [], []
     for i in range(n_submaps):
         d = np.linalg.norm(pos[:i] - pos[i], axis=1)
@@ -338,7 +343,7 @@ def submap_scene(name, seed, n_submaps, n_points, half_blocks, factor_dist, cand
     factors = np.array(fl, np.int64).reshape(-1, 5)
     pairs = np.array(pl, np.int64).reshape(-1, 4)
     return Scene(name, mu, cov, nrm, off, np.arange(n_submaps, dtype=np.int64), 0.5, 3, factors,
-                 perturb_poses(origins, seed + 100), origins, pairs, 1)
+                 lin, origins, pairs, 1)
 
 
 def global_scene(seed=4, **kw):

@@ -45,3 +45,38 @@ def compare_factor(rec, ref, levels, what=""):
         errs["e"] = 0.0
     assert errs["e"] <= E_TOL, f"{what} e rel err {errs['e']:.3g}"
     return errs
+
+
+class Margins:
+    """Worst relative errors (H blocks, b, e) and integer mismatches over the
+    factors compared in one parity test.  When GVOX_MARGINS_OUT names a file,
+    `save` appends one JSON line per test (tools/parity_margins.py turns them
+    into profiles/*_parity_margins.md); otherwise it only prints."""
+
+    def __init__(self, config):
+        self.config = config
+        self.worst = {"H_ii": 0.0, "H_ij": 0.0, "H_jj": 0.0, "b": 0.0, "e": 0.0}
+        self.factors = 0
+        self.int_compared = {}
+        self.int_mismatch = {}
+
+    def add_factor(self, errs):
+        self.factors += 1
+        for k, v in errs.items():
+            self.worst[k] = max(self.worst.get(k, 0.0), float(v))
+
+    def add_ints(self, what, compared, mismatches=0):
+        self.int_compared[what] = self.int_compared.get(what, 0) + int(compared)
+        self.int_mismatch[what] = self.int_mismatch.get(what, 0) + int(mismatches)
+
+    def save(self, test):
+        import json
+        import os
+        rec = {"test": test, "config": self.config, "factors": self.factors, "worst": self.worst,
+               "int_compared": self.int_compared, "int_mismatch": self.int_mismatch,
+               "tolerances": {"H": H_TOL, "b": B_TOL, "e": E_TOL}}
+        print("parity margins:", json.dumps(rec))
+        path = os.environ.get("GVOX_MARGINS_OUT")
+        if path:
+            with open(path, "a") as fh:
+                fh.write(json.dumps(rec) + "\n")

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import synth
-from tests.parity import compare_factor
+from tests.parity import Margins, compare_factor
 from tests.se3 import plane_cov, random_pose, rel_pose, right_perturb, to12, to44
 
 pytestmark = pytest.mark.gpu
@@ -224,7 +224,7 @@ def test_overlap_c2(gv, ctx, oracle):
 
 
 # ---------------------------------------------------------------------- linearize
-def _scene_parity(gv, ctx, oracle, sc, check_corr=True):
+def _scene_parity(gv, ctx, oracle, sc, check_corr=True, margins=None):
     clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
     maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
     import torch
@@ -236,7 +236,7 @@ def _scene_parity(gv, ctx, oracle, sc, check_corr=True):
     corr_h = corr.cpu().numpy() if check_corr else None
     omaps = {}
     off = 0
-    worst = {}
+    mg = margins if margins is not None else Margins(sc.name)
     for k, f in enumerate(sc.factors):
         t = int(f[1])
         if t not in omaps:
@@ -244,30 +244,31 @@ def _scene_parity(gv, ctx, oracle, sc, check_corr=True):
         mu, cov, nrm = sc.cloud(int(f[0]))
         ref = oracle.linearize(mu, cov, nrm, omaps[t], sc.poses[f[2]], sc.poses[f[3]],
                                validate=bool(f[4] & 1), return_corr=check_corr)
-        errs = compare_factor(out[k], ref, sc.levels, what=f"{sc.name} factor {k}")
-        for a, b in errs.items():
-            worst[a] = max(worst.get(a, 0.0), b)
+        mg.add_ints("inliers", sc.levels, int((out[k]["inliers"][:sc.levels] != ref["inliers"]).sum()))
+        mg.add_factor(compare_factor(out[k], ref, sc.levels, what=f"{sc.name} factor {k}"))
         if check_corr:
             n = len(mu) * sc.levels
-            assert np.array_equal(corr_h[off:off + n], ref["corr"].reshape(-1)), f"factor {k} corr"
+            bad = int((corr_h[off:off + n] != ref["corr"].reshape(-1)).sum())
+            mg.add_ints("correspondences", n, bad)
+            assert bad == 0, f"factor {k} corr: {bad} mismatches"
             off += n
-    return out, worst
+    return out, mg.worst, mg
 
 
 def test_linearize_c1(gv, ctx, oracle):
-    _scene_parity(gv, ctx, oracle, synth.make("C1"))
+    _scene_parity(gv, ctx, oracle, synth.make("C1"))[2].save("test_linearize_c1")
 
 
 def test_linearize_c2_validation(gv, ctx, oracle):
-    out, worst = _scene_parity(gv, ctx, oracle, synth.make("C2"))
+    out, worst, mg = _scene_parity(gv, ctx, oracle, synth.make("C2"))
     assert out["inliers"][:, :3].min() > 0
-    print("C2 worst relative errors:", worst)
+    mg.save("test_linearize_c2_validation")
 
 
 def test_linearize_c3_subset(gv, ctx, oracle):
     sc = synth.make("C3")
     sc.factors = sc.factors[::7].copy()  # 43 of 300 factors, all 50 clouds uploaded
-    _scene_parity(gv, ctx, oracle, sc)
+    _scene_parity(gv, ctx, oracle, sc)[2].save("test_linearize_c3_subset")
 
 
 def test_linearize_random_factors_nondyadic(gv, ctx, oracle):
@@ -277,6 +278,7 @@ def test_linearize_random_factors_nondyadic(gv, ctx, oracle):
     clouds = [transform_cloud(mu_w[k * 1500:(k + 1) * 1500 + 777], cov_w[k * 1500:(k + 1) * 1500 + 777],
                               n_w[k * 1500:(k + 1) * 1500 + 777], Ts[k]) for k in range(5)]
     poses = np.stack([right_perturb(T, rs.normal(0, 0.01, 6)) for T in Ts])
+    mg = Margins("random non-dyadic (r0 0.3/0.7/0.25, L 3/1/5)")
     for r0, L in ((0.3, 3), (0.7, 1), (0.25, 5)):
         sc = synth.Scene("rand", np.concatenate([c[0] for c in clouds]),
                          np.concatenate([c[1] for c in clouds]), np.concatenate([c[2] for c in clouds]),
@@ -284,7 +286,8 @@ def test_linearize_random_factors_nondyadic(gv, ctx, oracle):
                          np.arange(5, dtype=np.int64), r0, L,
                          np.array([[i, j, i, j, (i + j) % 2] for i in range(5) for j in range(5) if i != j],
                                   np.int64), poses, poses, np.zeros((0, 4), np.int64), 0)
-        _scene_parity(gv, ctx, oracle, sc)
+        _scene_parity(gv, ctx, oracle, sc, margins=mg)
+    mg.save("test_linearize_random_factors_nondyadic")
 
 
 def test_linearize_zero_at_ground_truth_lattice(gv, ctx):
@@ -479,25 +482,36 @@ def test_full_size_submaps_sampled(gv, ctx, oracle):
 
 
 @pytest.mark.slow
-def test_full_c5_bench_configuration_sampled(gv, ctx, oracle):
-    """The bench's own workload and launch configuration (BASELINE C5: 2000
-    submaps x 100k points, 204,949 candidate pairs, one gvox_overlap_select
-    over all of them, one gvox_linearize_batch_accum over the ~1.1e5 selected
-    factors, FAST all-dense kernel), checked on sampled outputs the oracle
-    computes one by one: screening decisions against the oracle's exact counts,
-    compact records (expanded) against the oracle's factors."""
+@pytest.mark.parametrize("config", ["C4", "C5"])
+def test_full_bench_configuration_sampled(gv, ctx, oracle, config):
+    """The bench's own workload and launch configuration at full size (C5:
+    2000 submaps x 100k points, ~2e5 candidate pairs; C4: 500 x 50k), one
+    gvox_overlap_select over every candidate, one gvox_linearize_batch_accum
+    over the ~1e5 selected factors (FAST all-dense kernel), the device-compacted
+    select path bitwise equal to it, and sampled outputs the oracle computes one
+    by one: 32 target submaps (the 16 farthest from the world origin + 16
+    random), >= 256 screening decisions against the oracle's exact counts,
+    64 factors (records expanded from the big batch) against the oracle's
+    factors, and the same 64 factors' correspondences (packed voxel keys of
+    every point at every level) dumped at these coordinates and
+    compared bit for bit; the FAST kernel's records for them equal the generic
+    (dumping) kernel's bitwise."""
     import torch
-    sc = synth.make("C5")
+    from concurrent.futures import ThreadPoolExecutor
+    sc = synth.make(config)
     clouds = gv.create_clouds(ctx, torch.from_numpy(sc.mu).cuda(), torch.from_numpy(sc.cov).cuda(),
                               torch.from_numpy(sc.nrm).cuda(), sc.offsets)
     maps = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
     sel = gv.overlap_select(ctx, clouds, maps, sc.pairs, sc.poses, sc.overlap_level, 1, 20)
+    cnt = gv.overlap(ctx, clouds, maps, sc.pairs, sc.poses, sc.overlap_level)
+    n = np.diff(sc.offsets)
+    assert np.array_equal(sel.astype(bool), 20 * cnt.astype(np.int64) > n[sc.pairs[:, 0]])
     fac = np.zeros(len(sc.pairs), gv.FACTOR_DTYPE)
     for i, name in enumerate(("source_cloud", "target_map", "pose_i", "pose_j")):
         fac[name] = sc.pairs[:, i]
     cand = fac
     fac = fac[sel.view(bool)]
-    assert len(fac) > 100000
+    assert len(fac) > (100000 if config == "C5" else 10000)
     acc = gv.device_records(ctx, len(fac), gv.FACTOR_ACCUM_DTYPE)
     gv.linearize_batch_accum(ctx, clouds, maps, fac, sc.poses, out=acc)
     # the bench's call sequence: device decisions -> device-compacted batch,
@@ -511,31 +525,77 @@ def test_full_c5_bench_configuration_sampled(gv, ctx, oracle):
     assert ns == len(fac) and np.array_equal(sel_h, sel)
     assert torch.equal(acc2[:ns], acc)
     del acc2
+
+    mg = Margins(f"{config} full size (sampled)")
     rs = np.random.default_rng(7)
-    n = np.diff(sc.offsets)
-    omaps = {}
+    pos = sc.poses.reshape(-1, 3, 4)[:, :, 3]
+    tsel = np.unique(fac["target_map"])
+    far = tsel[np.argsort(-np.linalg.norm(pos[sc.map_clouds[tsel]], axis=1), kind="stable")[:16]]
+    rest = rs.choice(np.setdiff1d(tsel, far), 16, replace=False)
+    targets = [int(t) for t in np.concatenate([far, rest])]
+    with ThreadPoolExecutor(16) as ex:
+        ol = list(ex.map(lambda t: oracle.VoxelMap(*sc.cloud(int(sc.map_clouds[t]))[:2], sc.r0,
+                                                   sc.levels), targets))
+    local = {t: k for k, t in enumerate(targets)}
 
-    def omap(t):
-        if t not in omaps:
-            omaps[t] = oracle.VoxelMap(*sc.cloud(int(sc.map_clouds[t]))[:2], sc.r0, sc.levels)
-        return omaps[t]
+    # >= 256 screening decisions: 8 candidate pairs per sampled target, half
+    # selected where possible
+    dk = []
+    for t in targets:
+        idx = np.nonzero(sc.pairs[:, 1] == t)[0]
+        on, off = idx[sel[idx] == 1], idx[sel[idx] == 0]
+        k_off = min(4, len(off))
+        dk += rs.choice(on, min(8 - k_off, len(on)), replace=False).tolist()
+        dk += rs.choice(off, k_off, replace=False).tolist() if k_off else []
+    dk = np.array(sorted(dk))
+    assert len(dk) >= 256
+    lp = sc.pairs[dk].copy()
+    lp[:, 1] = [local[int(t)] for t in lp[:, 1]]
+    want = oracle.overlap_batch([sc.cloud(c)[0] for c in range(sc.num_clouds)], ol, lp, sc.poses,
+                                sc.overlap_level, num_threads=16)
+    assert np.array_equal(cnt[dk].astype(np.int64), want)
+    wsel = (20 * want > n[sc.pairs[dk, 0]]).astype(np.uint8)
+    mg.add_ints("overlap counts", len(dk), int((cnt[dk] != want).sum()))
+    mg.add_ints("screening decisions", len(dk), int((sel[dk] != wsel).sum()))
+    assert np.array_equal(sel[dk], wsel)
 
-    for k in rs.choice(len(sc.pairs), 12, replace=False):
-        p = sc.pairs[k]
-        want = oracle.overlap(sc.cloud(int(p[0]))[0], omap(int(p[1])), sc.poses[p[2]], sc.poses[p[3]],
-                              sc.overlap_level)
-        assert int(sel[k]) == int(20 * want > n[int(p[0])]), k
-    pick = rs.choice(len(fac), 8, replace=False)
+    # 64 factors: two selected factors per sampled target
+    pick = []
+    for t in targets:
+        idx = np.nonzero(fac["target_map"] == t)[0]
+        pick += rs.choice(idx, min(2, len(idx)), replace=False).tolist()
+    pick = np.array(sorted(pick))
+    assert len(pick) >= 64
     sub = gv.device_records(ctx, len(pick), gv.FACTOR_ACCUM_DTYPE)
     sub.copy_(acc[torch.from_numpy(pick).cuda()])
     full = gv.records_to_numpy(gv.expand(ctx, fac[pick], sc.poses, sub,
                                          out=gv.device_records(ctx, len(pick), gv.LINEAR_FACTOR_DTYPE)))
-    for j, k in enumerate(pick):
-        f = fac[k]
-        mu, cov, nrm = sc.cloud(int(f["source_cloud"]))
-        ref = oracle.linearize(mu, cov, None, omap(int(f["target_map"])), sc.poses[f["pose_i"]],
-                               sc.poses[f["pose_j"]])
-        compare_factor(full[j], ref, sc.levels, what=f"C5 factor {k}")
+    fsub = fac[pick]
+    corr = torch.empty(gv.corr_dump_size(clouds, maps, fsub), dtype=torch.int64, device=ctx.device)
+    dumped = gv.linearize_batch(ctx, clouds, maps, fsub, sc.poses, corr_dump=corr)   # generic kernel
+    fast = gv.linearize_batch(ctx, clouds, maps, fsub, sc.poses)                     # FAST kernel
+    assert dumped.tobytes() == fast.tobytes()
+    assert fast.tobytes() == full.tobytes()      # a factor's result is independent of its batch
+    corr_h = corr.cpu().numpy()
+
+    def ref_of(f):
+        mu, cov, _ = sc.cloud(int(f["source_cloud"]))
+        return oracle.linearize(mu, cov, None, ol[local[int(f["target_map"])]], sc.poses[f["pose_i"]],
+                                sc.poses[f["pose_j"]], return_corr=True)
+
+    with ThreadPoolExecutor(16) as ex:
+        refs = list(ex.map(ref_of, fsub))
+    off = 0
+    for j, (f, ref) in enumerate(zip(fsub, refs)):
+        mg.add_ints("inliers", sc.levels, int((full[j]["inliers"][:sc.levels] != ref["inliers"]).sum()))
+        mg.add_factor(compare_factor(full[j], ref, sc.levels, what=f"{config} factor {pick[j]}"))
+        m = n[int(f["source_cloud"])] * sc.levels
+        bad = int((corr_h[off:off + m] != ref["corr"].reshape(-1)).sum())
+        mg.add_ints("correspondences", m, bad)
+        assert bad == 0, f"{config} factor {pick[j]}: {bad} correspondence mismatches"
+        off += m
+    assert off == len(corr_h)
+    mg.save(f"test_full_bench_configuration_sampled[{config}]")
 
 
 @pytest.mark.parametrize("num,den", [(1, 20), (0, 1), (1, 1)])
