@@ -47,6 +47,17 @@ WORKLOADS = {
 }
 
 
+def workload_label(args, sc):
+    """The workload as run: the config's description, with the submap count and
+    points per submap taken from the generated scene when --submaps overrides it."""
+    lab = WORKLOADS[args.config]
+    if args.config in ("C4", "C5") and args.submaps:
+        n = np.diff(sc.offsets)
+        lab = (f"{args.config} reduced by --submaps: {sc.num_clouds} submaps x "
+               f"{int(n.mean())} points, overlap-selected factors, r = 0.5/1/2 m")
+    return lab
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -68,6 +79,8 @@ def parse():
                          "360-376 ms vs 386 ms serial; the concurrent H2D runs at ~24 GB/s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--per-call-runs", type=int, default=20,
+                    help="calls timed for SURVEY 8(d)'s per-call metric (median; 0 = skip)")
     ap.add_argument("--linearize-only", action="store_true",
                     help="profiling aid: time only S3-S7 (not a bench line)")
     return ap.parse_args()
@@ -163,6 +176,16 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- oracle legs
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def oracle_sample(sc, select=True, budget_s=12.0, threads=None):
     """The oracle, as it stands, on a bounded sample of the same step: all rows
     (map build, overlap, selection, linearize) for a random subset of target
@@ -234,7 +257,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot_t / len(samples), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "oracle_sample": desc},
+            "config": {"workload": workload_label(args, sc), "oracle_sample": desc},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -294,31 +317,37 @@ def main():
     poses = gv.as_poses(sc.poses)
 
     from paper_2407_10344_b200 import dist as gdist
-    bounds = gdist.shard_targets(n_pts, sc.map_clouds, sc.pairs, world)
-    t_lo, t_hi = bounds[rank], bounds[rank + 1]
-    my_targets = np.arange(t_lo, t_hi)
-    _, my_pairs = gdist.local_pairs(sc.pairs, bounds, rank)  # target -> local map index
-    pairs_s = gv.as_pairs(my_pairs)
-    src_n = n_pts[my_pairs[:, 0]]
-    my_target_clouds = [clouds[int(sc.map_clouds[t])] for t in my_targets]
     # C4/C5: factors = candidate pairs whose overlap exceeds 5 %, no
     # validation (Q7).  C1-C3: the config's own factor list (odometry factors,
     # validation on); the overlap of their pairs is still screened.
     select = args.config in ("C4", "C5")
-    if not select:
-        fm = (sc.factors[:, 1] >= t_lo) & (sc.factors[:, 1] < t_hi)
-        fixed = gv.as_factors(sc.factors[fm])
-        fixed["target_map"] -= t_lo
-    flags = 0
 
-    all_fac = np.zeros(len(my_pairs), gv.FACTOR_DTYPE)  # every candidate as a factor
-    for i_, name_ in enumerate(("source_cloud", "target_map", "pose_i", "pose_j")):
-        all_fac[name_] = my_pairs[:, i_]
-    # device buffers reused across steps
-    acc_out = gv.device_records(ctx, max(len(my_pairs), len(sc.factors), 1), gv.FACTOR_ACCUM_DTYPE)
-    counts_h = np.zeros(len(my_pairs), np.int32)
-    sel_h = np.zeros(len(my_pairs), np.uint8)
-    sel_d = torch.empty(max(len(my_pairs), 1), dtype=torch.uint8, device=dev)
+    def setup(bounds):
+        """This rank's share of the step for a target-range plan."""
+        t_lo, t_hi = bounds[rank], bounds[rank + 1]
+        my_targets = np.arange(t_lo, t_hi)
+        _, my_pairs = gdist.local_pairs(sc.pairs, bounds, rank)  # target -> local map index
+        fixed = None
+        if not select:
+            fm = (sc.factors[:, 1] >= t_lo) & (sc.factors[:, 1] < t_hi)
+            fixed = gv.as_factors(sc.factors[fm])
+            fixed["target_map"] -= t_lo
+        all_fac = np.zeros(len(my_pairs), gv.FACTOR_DTYPE)  # every candidate as a factor
+        for i_, name_ in enumerate(("source_cloud", "target_map", "pose_i", "pose_j")):
+            all_fac[name_] = my_pairs[:, i_]
+        # device buffers reused across steps
+        acc_out = gv.device_records(ctx, max(len(my_pairs), len(sc.factors), 1), gv.FACTOR_ACCUM_DTYPE)
+        return (my_targets, my_pairs, gv.as_pairs(my_pairs), n_pts[my_pairs[:, 0]],
+                [clouds[int(sc.map_clouds[t])] for t in my_targets], fixed, all_fac, acc_out,
+                np.zeros(len(my_pairs), np.int32), np.zeros(len(my_pairs), np.uint8),
+                torch.empty(max(len(my_pairs), 1), dtype=torch.uint8, device=dev))
+
+    # first plan: candidates' work (no decisions yet); at N > 1 it is redone
+    # after the first warm-up step on that step's screening decisions
+    bounds = gdist.shard_targets(n_pts, sc.map_clouds, sc.pairs, world)
+    (my_targets, my_pairs, pairs_s, src_n, my_target_clouds, fixed, all_fac, acc_out, counts_h,
+     sel_h, sel_d) = setup(bounds)
+    balance = "candidates (no decisions)"
 
     state = {}
 
@@ -365,14 +394,27 @@ def main():
         state["fac"] = fac
         return int(n_pts[fac["source_cloud"]].sum()), len(fac)
 
-    # ---- warm-up (also sizes the gather)
+    # ---- warm-up (also re-balances the shards and sizes the gather)
+    warm = args.warmup
     if world > 1:
-        state["fmax"] = max(len(my_pairs), 1)
-        t = torch.tensor([state["fmax"]], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        state["fmax"] = int(t.item())
+        if select and warm > 0:
+            state["fmax"] = gdist.max_count(max(len(my_pairs), 1), dev)
+            step()
+            warm -= 1
+            # the previous step's screening decisions -> global selection vector
+            # -> shards balanced on the work actually selected (setup, untimed)
+            rows, _ = gdist.local_pairs(sc.pairs, bounds, rank)
+            g = torch.zeros(len(sc.pairs), dtype=torch.int32, device=dev)
+            g[torch.from_numpy(rows).to(dev)] = torch.from_numpy(sel_h.astype(np.int32)).to(dev)
+            dist.all_reduce(g, op=dist.ReduceOp.SUM)
+            w = gdist.target_weights(n_pts, sc.map_clouds, sc.pairs, g.cpu().numpy().astype(bool))
+            bounds = gdist.shard_targets(n_pts, sc.map_clouds, sc.pairs, world, weights=w)
+            (my_targets, my_pairs, pairs_s, src_n, my_target_clouds, fixed, all_fac, acc_out,
+             counts_h, sel_h, sel_d) = setup(bounds)
+            balance = "previous step's screening decisions (selected point-factors)"
+        state["fmax"] = gdist.max_count(max(len(my_pairs), 1), dev)
         acc_out = gv.device_records(ctx, state["fmax"], gv.FACTOR_ACCUM_DTYPE)
-    for _ in range(args.warmup):
+    for _ in range(warm):
         step()
     torch.cuda.synchronize()
     if args.linearize_only:
@@ -434,6 +476,55 @@ def main():
     ms_step = ms / args.steps
     value = pts_all / (ms / 1e3)
 
+    # ---- SURVEY 8(d)'s per-call metric: ONE gvox_linearize_batch over the step's
+    # selected factors, its single H2D (factor table + poses) and single D2H
+    # (full records into pinned host memory) inside the interval, maps and clouds
+    # resident (built once, amortised over GN iterations).  CUDA events on the
+    # library's stream bracket the call (the host-side serialisation before the
+    # H2D is inside the interval); median of >= 20 calls, max over ranks.
+    per_call = None
+    if not args.linearize_only and args.per_call_runs > 0:
+        pc_fac = state["fac"]
+        pc_maps = gv.HandleArray(state["maps"])
+        pc_out = np.zeros(max(len(pc_fac), 1), gv.LINEAR_FACTOR_DTYPE)
+        try:
+            pc_out = torch.from_numpy(pc_out.view(np.uint8)).pin_memory().numpy().view(
+                gv.LINEAR_FACTOR_DTYPE)
+        except RuntimeError:
+            pass
+        pc_pts = int(n_pts[pc_fac["source_cloud"]].sum())
+        gv.linearize_batch(ctx, cloud_arr, pc_maps, pc_fac, poses, out=pc_out[:len(pc_fac)])  # warm
+        pc_ms = []
+        for _ in range(args.per_call_runs):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            c0 = torch.cuda.Event(enable_timing=True)
+            c1 = torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            gv.linearize_batch(ctx, cloud_arr, pc_maps, pc_fac, poses, out=pc_out[:len(pc_fac)])
+            c1.record(stream)
+            c1.synchronize()
+            pc_ms.append(c0.elapsed_time(c1))
+        med = statistics.median(pc_ms)
+        pc_pf = float(pc_pts)
+        pc_nf = float(len(pc_fac))
+        if world > 1:
+            t = torch.tensor([med, pc_pf, pc_nf], dtype=torch.float64, device=dev)
+            tmax = t.clone()
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            tsum = t.clone()
+            dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+            med, pc_pf, pc_nf = float(tmax[0]), float(tsum[1]), float(tsum[2])
+        per_call = {"value": pc_pf / (med / 1e3), "unit": UNIT, "factors_per_s": pc_nf / (med / 1e3),
+                    "ms_median": med, "ms_min": min(pc_ms), "ms_max": max(pc_ms),
+                    "runs": len(pc_ms), "factors": int(pc_nf), "point_factors": int(pc_pf),
+                    "h2d_bytes": int(pc_fac.nbytes + poses.nbytes),
+                    "d2h_bytes": int(pc_out[:len(pc_fac)].nbytes),
+                    "what": "one gvox_linearize_batch over the step's selected factors: one H2D "
+                            "(factor table, poses), one fused launch, one D2H of full records "
+                            "to pinned host memory (P:224); maps resident; median of the runs"}
+
     # ---- roofline of the dominant kernel (rank 0's launches)
     peaks = {}
     try:
@@ -460,25 +551,44 @@ def main():
     achieved = alg_bytes / lin_avg_s / 1e9 if lin_n else None
     traffic = None
     inst_pf = None
+    ncu = {}
     prof = os.path.join(ROOT, "profiles", "linearize_dram_bytes_per_pf.json")
     if os.path.exists(prof):
         try:
-            pj = json.load(open(prof))
-            traffic = pj["dram_bytes_per_point_factor"] * pf
-            inst_pf = pj.get("warp_instructions_per_point_factor")
+            ncu = json.load(open(prof))
+            traffic = ncu["dram_bytes_per_point_factor"] * pf
+            inst_pf = ncu.get("warp_instructions_per_point_factor")
         except (ValueError, KeyError):
             traffic = None
-    # issue-slot view of the same kernel (it is instruction-issue bound): warp
-    # instructions per point-factor from the committed full-size ncu capture,
-    # against 4 schedulers x SMs x the SM clock sampled during the timed region
+    # The kernel is bound by instruction issue (ncu: DRAM well below peak, no
+    # pipe saturated, issue-active the highest utilisation), so the roofline
+    # line is the ALU/issue ceiling: warp instructions per point-factor (the
+    # committed full-size ncu capture) x point-factors / the live CUDA-event
+    # launch time, against 4 schedulers x SMs x the SM clock sampled during the
+    # timed region (one warp instruction per scheduler per cycle).
+    # HBM is reported beside it two ways: measured DRAM bytes (ncu) and the
+    # algorithmic-bytes model, each over the same live launch time.
     issue = None
     if inst_pf and lin_n and clk and clk.get("sm_mhz"):
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         peak_i = 4 * sms * clk["sm_mhz"] * 1e6
         ach_i = inst_pf * pf / lin_avg_s
-        issue = {"unit": "warp-instructions/s", "achieved": ach_i, "peak": peak_i,
+        issue = {"achieved": ach_i / 1e9, "peak": peak_i / 1e9, "unit": "Gwarp-inst/s",
                  "frac": ach_i / peak_i, "warp_instructions_per_point_factor": inst_pf,
-                 "source": "profiles/linearize_dram_bytes_per_pf.json (ncu smsp__inst_executed)"}
+                 "peak_derivation": f"4 schedulers x {sms} SMs x {clk['sm_mhz']:.0f} MHz "
+                                    "(1 warp-instruction / scheduler / cycle)"}
+    hbm = {"peak": hbm_peak, "unit": "GB/s", "peak_source": peak_src,
+           "measured_dram": {"achieved": traffic / lin_avg_s / 1e9 if (traffic and lin_n) else None,
+                             "frac": (traffic / lin_avg_s / 1e9 / hbm_peak) if (traffic and lin_n) else None,
+                             "bytes_per_point_factor": ncu.get("dram_bytes_per_point_factor"),
+                             "source": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                       "full-size launch (profiles/linearize_dram_bytes_per_pf.json)"},
+           "algorithmic": {"achieved": achieved, "frac": (achieved / hbm_peak) if achieved else None,
+                           "bytes_per_launch": alg_bytes,
+                           "model": "48 B per point-factor + 64 B per voxel of each distinct target"}}
+    pipes = {k: ncu.get(k) for k in ("fma_pipe_pct", "alu_pipe_pct", "fp64_pipe_pct",
+                                     "issue_active_pct", "dram_pct_of_peak", "occupancy_pct")
+             if ncu.get(k) is not None}
     stages = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for k, v in tm.items()}
     # SURVEY §8(d) secondary rates (rank-local): per-row throughputs of the step
     rates = None
@@ -657,8 +767,13 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         pts_o, dt_o, desc, cores = oracle_sample(sc, select, budget_s=args.cpu_seconds)
+        # the same oracle on one thread (single-thread and all-core rates)
+        pts_1, dt_1, desc_1, _ = oracle_sample(sc, select, budget_s=args.cpu_seconds / 3,
+                                               threads=1)
         cpu = {"value": pts_o / dt_o, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": desc, "seconds": dt_o}
+               "sample": desc, "seconds": dt_o, "cpu_model": cpu_model(),
+               "single_thread": {"value": pts_1 / dt_1, "unit": UNIT, "cores": 1,
+                                 "sample": desc_1, "seconds": dt_1}}
 
     if rank == 0:
         n_levels_vox = {l: int(sum(m.num_voxels(l) for m in maps)) for l in range(sc.levels)}
@@ -667,11 +782,15 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded LiDAR-shaped submaps, synth/)",
-            "config": {"workload": WORKLOADS[args.config], "submaps": sc.num_clouds,
+            "config": {"workload": workload_label(args, sc), "submaps": sc.num_clouds,
                        "points": int(len(sc.mu)), "candidate_pairs": int(len(sc.pairs)),
                        "factors_per_step": fac_all / args.steps, "levels": sc.levels, "r0": sc.r0,
                        "overlap_level": sc.overlap_level, "point_order": args.order,
-                       "parallelism": f"factor-sharded x{world} (targets), NCCL all_gather",
+                       "parallelism": (f"factor-sharded x{world} (targets), one {dist.get_backend()} "
+                                       "all_gather of the compact records" if world > 1 else
+                                       "one GPU (no collective)"),
+                       "shard_balance": balance if world > 1 else None,
+                       "shard_bounds": bounds if world > 1 else None,
                        "l2": "inputs larger than L2 (clouds %.1f GB + voxel records %.1f GB + "
                              "index grids on rank 0)"
                              % (len(sc.mu) * 48 / 1e9,
@@ -683,14 +802,22 @@ def main():
                          "and cross-thread accumulation",
             "stages": stages,
             "rates": rates,
-            "roofline": {"kernel": "k_linearize", "bound": "hbm",
-                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": (achieved / hbm_peak) if achieved else None,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "alg_bytes_per_launch": alg_bytes, "point_factors_per_launch": pf,
-                         "avg_launch_ms": lin_avg_s * 1e3,
-                         "dominant_kernel_group": dominant,
-                         "issue": issue},
+            "roofline": ({"kernel": "k_linearize", "bound": "alu", "limiter": "instruction issue",
+                          "achieved": issue["achieved"], "peak": issue["peak"], "unit": issue["unit"],
+                          "frac": issue["frac"], "traffic": traffic,
+                          "peak_derivation": issue["peak_derivation"],
+                          "warp_instructions_per_point_factor": inst_pf,
+                          "hbm": hbm, "ncu_pipes_pct": pipes,
+                          "point_factors_per_launch": pf, "avg_launch_ms": lin_avg_s * 1e3,
+                          "dominant_kernel_group": dominant}
+                         if issue else
+                         {"kernel": "k_linearize", "bound": "hbm", "achieved": achieved,
+                          "peak": hbm_peak, "unit": "GB/s",
+                          "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
+                          "note": "no ncu instruction count or clock sample: algorithmic bytes only",
+                          "point_factors_per_launch": pf, "avg_launch_ms": lin_avg_s * 1e3,
+                          "dominant_kernel_group": dominant}),
+            "per_call": per_call,
             "e2e": e2e,
             "gpu_launches": launches_all,
             "clocks": clk,

@@ -122,6 +122,9 @@ typedef struct gvox_factor_accum {
 /* Create a context on CUDA device `device`, enqueuing on `cuda_stream`
    (a cudaStream_t; NULL = the legacy default stream).  The stream is not owned. */
 gvox_status gvox_ctx_create(int device, void* cuda_stream, gvox_ctx** out);
+/* Move the context to another stream.  The new stream is first ordered after
+   everything already enqueued on the old one (an event), so the context's
+   reused workspaces never race across the switch. */
 gvox_status gvox_ctx_set_stream(gvox_ctx* ctx, void* cuda_stream);
 void gvox_ctx_destroy(gvox_ctx* ctx);
 
@@ -307,6 +310,31 @@ gvox_status gvox_overlap_union(gvox_ctx* ctx, const gvox_cloud* const* clouds, i
 gvox_status gvox_keyframe_update(const double* overlap, int32_t K, int32_t n_odom,
                                  double min_overlap, uint8_t* remove);
 
+/* Keyframe insertion test (host only): "if the overlap [of the new
+   frame with the union of all keyframes] is smaller than a threshold (e.g.,
+   90%), we insert that frame".  count: gvox_overlap_union's count for the
+   frame (points of the frame inside a voxel of any keyframe), n: the frame's
+   point count.  The rate count / n is compared in integers,
+   insert = (den * count < num * n) (default num / den = 9 / 10; strict
+   "smaller than").  An empty keyframe list is the caller's case (always
+   insert); n = 0 gives 0 < 0, false: an empty frame adds nothing and is not
+   inserted (the oracle's rule, oracle/keyframes.py).  GVOX_ERR_INVALID for count < 0,
+   n < 0, count > n, num < 0, den <= 0 or a NULL output. */
+gvox_status gvox_keyframe_insert_test(int64_t count, int64_t n, int32_t num, int32_t den,
+                                      int32_t* insert);
+
+/* The removal rule of gvox_keyframe_update from raw gvox_overlap COUNTS (P:280
+   "overlap rate between frames": the fraction of keyframe i's points that fall
+   within a voxel of keyframe j): counts[i * K + j] = points of keyframe i in
+   keyframe j's voxels, sizes[i] = keyframe i's point count, K-1 = the latest
+   keyframe.  o(i, j) = counts / sizes[i] (0 for an empty keyframe) is formed
+   here, in fp64, then the rules apply exactly as gvox_keyframe_update.
+   overlap_out (optional, K * K doubles): the o(i, j) matrix used.
+   GVOX_ERR_INVALID for negative counts or sizes, counts[i*K+j] > sizes[i]. */
+gvox_status gvox_keyframe_update_counts(const int64_t* counts, const int64_t* sizes, int32_t K,
+                                        int32_t n_odom, double min_overlap, uint8_t* remove,
+                                        double* overlap_out);
+
 /* ------------------------------------------------------------- linearize */
 
 /* Batched linearization of matching cost factors (Eqs. 2-8; Fig. 4 / P:224:
@@ -346,7 +374,12 @@ gvox_status gvox_linearize_batch_accum(gvox_ctx* ctx, const gvox_cloud* const* c
    num_candidates bytes) receives a copy of the decisions.  One H2D (the
    candidate table), one 8-byte D2H of the selected and tile counts (plus the
    optional decision copy) before the launch; returns with the linearization
-   enqueued on ctx's stream.  Errors as gvox_linearize_batch_accum. */
+   enqueued on ctx's stream.  The kernel variant (FAST all-dense / generic) is
+   chosen on the host from ALL candidates, before the decisions exist: one
+   unselected candidate with a hash level or non-dyadic map sends the batch to
+   the generic kernel.  The records are the same either way (the two variants
+   are bitwise equal, tested), only the speed differs; tile partials are sized
+   for every candidate.  Errors as gvox_linearize_batch_accum. */
 gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* const* clouds,
                                               int64_t num_clouds, const gvox_map* const* maps,
                                               int64_t num_maps, const gvox_factor* candidates,

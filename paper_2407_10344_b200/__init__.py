@@ -14,6 +14,7 @@ from .api import (Cloud, Context, HandleArray, VoxelMap, as_factors, as_pairs, a
                   full_blocks, linearize_batch, linearize_batch_accum, linearize_batch_accum_select,
                   overlap, overlap_select,
                   records_to_numpy, register_batch, overlap_union, keyframe_update,
+                  keyframe_insert_test, keyframe_update_counts,
                   KeyframeList, knn, estimate_covariances, solve_global,
                   optimize_global)
 
@@ -23,7 +24,7 @@ __all__ = [
     "Cloud", "Context", "VoxelMap", "HandleArray", "create_clouds", "create_voxelmap", "create_voxelmaps",
     "overlap", "overlap_select", "linearize_batch", "linearize_batch_accum",
     "linearize_batch_accum_select", "expand", "device_records",
-    "records_to_numpy", "register_batch", "overlap_union", "keyframe_update", "KeyframeList", "knn", "estimate_covariances", "solve_global", "optimize_global", "full_blocks", "corr_dump_size", "as_factors", "as_pairs", "as_poses",
+    "records_to_numpy", "register_batch", "overlap_union", "keyframe_update", "keyframe_insert_test", "keyframe_update_counts", "KeyframeList", "knn", "estimate_covariances", "solve_global", "optimize_global", "full_blocks", "corr_dump_size", "as_factors", "as_pairs", "as_poses",
     "FACTOR_DTYPE", "PAIR_DTYPE", "LINEAR_FACTOR_DTYPE", "FACTOR_ACCUM_DTYPE", "MAX_LEVELS",
     "F_VALIDATE_SURFACE", "F_ERROR_ONLY", "GVOX_HOST", "GVOX_DEVICE", "GvoxError",
     "launch_count", "version", "lib", "REG_FIXED", "REG_MAX_ITER", "REG_CONVERGED", "REG_SINGULAR",

@@ -64,7 +64,8 @@ SYMBOLS = [
     "gvox_voxelmap_export", "gvox_voxelmap_lookup", "gvox_map_destroy",
     "gvox_overlap", "gvox_overlap_select", "gvox_linearize_batch", "gvox_linearize_batch_accum",
     "gvox_linearize_batch_accum_select", "gvox_expand",
-    "gvox_register_batch", "gvox_overlap_union", "gvox_keyframe_update", "gvox_knn",
+    "gvox_register_batch", "gvox_overlap_union", "gvox_keyframe_update",
+    "gvox_keyframe_insert_test", "gvox_keyframe_update_counts", "gvox_knn",
     "gvox_estimate_covariances", "gvox_solve_global", "gvox_optimize_global",
     "gvox_status_string", "gvox_last_error", "gvox_launch_count", "gvox_version",
 ]
@@ -118,6 +119,8 @@ def lib():
         "gvox_estimate_covariances": (I32, [P, P, P, I64, P, I32, P, P, I32]),
         "gvox_overlap_union": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I64, I32, P, I32]),
         "gvox_keyframe_update": (I32, [P, I32, I32, D, P]),
+        "gvox_keyframe_insert_test": (I32, [I64, I64, I32, I32, P]),
+        "gvox_keyframe_update_counts": (I32, [P, P, I32, I32, D, P, P]),
         "gvox_register_batch": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, P, P, P, I32]),
         "gvox_status_string": (ctypes.c_char_p, [I32]),
         "gvox_last_error": (ctypes.c_char_p, []),

@@ -43,6 +43,33 @@ def _ptr(x):
     return ctypes.c_void_p(x.ctypes.data), GVOX_HOST
 
 
+def _out_ptr(ctx, out, n: int, dtype: np.dtype, what: str):
+    """(pointer, mem) of an output buffer after checking it can hold n elements
+    of `dtype`: a numpy array of that dtype, or a contiguous CUDA tensor on the
+    context's device with at least n * itemsize bytes (record tensors: uint8
+    [>= n, itemsize]).  An undersized or mistyped buffer raises instead of
+    letting the library write past its end."""
+    dtype = np.dtype(dtype)
+    if _is_cuda_tensor(out):
+        if out.device != ctx.device:
+            raise ValueError(f"{what}: output on {out.device}, context on {ctx.device}")
+        if not out.is_contiguous():
+            raise ValueError(f"{what}: output tensor must be contiguous")
+        if out.dim() == 2 and out.element_size() == 1 and out.shape[1] != dtype.itemsize:
+            raise ValueError(f"{what}: record tensor rows are {out.shape[1]} B, need {dtype.itemsize}")
+        if out.dim() != 2 and out.element_size() != dtype.itemsize:
+            raise ValueError(f"{what}: output element size {out.element_size()}, need {dtype.itemsize}")
+        if out.numel() * out.element_size() < n * dtype.itemsize:
+            raise ValueError(f"{what}: output holds {out.numel() * out.element_size()} B, "
+                             f"need {n} x {dtype.itemsize} B")
+        return ctypes.c_void_p(out.data_ptr()), GVOX_DEVICE
+    if not isinstance(out, np.ndarray) or not out.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"{what}: output must be a contiguous numpy array or CUDA tensor")
+    if out.dtype != dtype or out.size < n:
+        raise ValueError(f"{what}: output {out.dtype} [{out.size}], need {dtype} [>= {n}]")
+    return ctypes.c_void_p(out.ctypes.data), GVOX_HOST
+
+
 class Context:
     """gvox_ctx on one CUDA device, enqueuing on a torch stream (default: the
     device's current stream)."""
@@ -258,7 +285,7 @@ def overlap(ctx: Context, clouds, maps, pairs, poses, level: int, out=None):
     poses = as_poses(poses)
     if out is None:
         out = np.empty(pairs.shape[0], np.int32)
-    po, mem = _ptr(out)
+    po, mem = _out_ptr(ctx, out, pairs.shape[0], np.int32, "overlap")
     check(lib().gvox_overlap(ctx.handle, C.arr, C.n, M.arr, M.n, _ptr(pairs)[0], pairs.shape[0],
                              _ptr(poses)[0], poses.shape[0], int(level), po, mem))
     return out
@@ -273,7 +300,7 @@ def overlap_select(ctx: Context, clouds, maps, pairs, poses, level: int, num: in
     poses = as_poses(poses)
     if out is None:
         out = np.empty(pairs.shape[0], np.uint8)
-    po, mem = _ptr(out)
+    po, mem = _out_ptr(ctx, out, pairs.shape[0], np.uint8, "overlap_select")
     check(lib().gvox_overlap_select(ctx.handle, C.arr, C.n, M.arr, M.n, _ptr(pairs)[0],
                                     pairs.shape[0], _ptr(poses)[0], poses.shape[0], int(level),
                                     int(num), int(den), po, mem))
@@ -302,11 +329,13 @@ def linearize_batch(ctx: Context, clouds, maps, factors, poses, out=None, corr_d
     F = factors.shape[0]
     if out is None:
         out = np.zeros(F, LINEAR_FACTOR_DTYPE)
-    po, mem = _ptr(out)
+    po, mem = _out_ptr(ctx, out, F, LINEAR_FACTOR_DTYPE, "linearize_batch")
     pc = None
     if corr_dump is not None:
-        assert _is_cuda_tensor(corr_dump)
-        pc = ctypes.c_void_p(corr_dump.data_ptr())
+        if not _is_cuda_tensor(corr_dump):
+            raise ValueError("linearize_batch: corr_dump must be an int64 CUDA tensor")
+        pc, _ = _out_ptr(ctx, corr_dump, corr_dump_size(C.objs, M.objs, factors), np.int64,
+                         "linearize_batch corr_dump")
     check(lib().gvox_linearize_batch(ctx.handle, C.arr, C.n, M.arr, M.n, _ptr(factors)[0], F,
                                      _ptr(poses)[0], poses.shape[0], po, mem, pc))
     return out
@@ -320,7 +349,7 @@ def linearize_batch_accum(ctx: Context, clouds, maps, factors, poses, out=None):
     F = factors.shape[0]
     if out is None:
         out = np.zeros(F, FACTOR_ACCUM_DTYPE)
-    po, mem = _ptr(out)
+    po, mem = _out_ptr(ctx, out, F, FACTOR_ACCUM_DTYPE, "linearize_batch_accum")
     check(lib().gvox_linearize_batch_accum(ctx.handle, C.arr, C.n, M.arr, M.n, _ptr(factors)[0], F,
                                            _ptr(poses)[0], poses.shape[0], po, mem))
     return out
@@ -338,8 +367,10 @@ def linearize_batch_accum_select(ctx: Context, clouds, maps, candidates, selecte
     candidates = as_factors(candidates)
     poses = as_poses(poses)
     F = candidates.shape[0]
-    assert _is_cuda_tensor(selected) and _is_cuda_tensor(out)
-    assert selected.numel() >= F and out.shape[0] >= F
+    if not (_is_cuda_tensor(selected) and _is_cuda_tensor(out)):
+        raise ValueError("linearize_batch_accum_select: selected and out must be CUDA tensors")
+    _out_ptr(ctx, selected, F, np.uint8, "linearize_batch_accum_select selected")
+    _out_ptr(ctx, out, F, FACTOR_ACCUM_DTYPE, "linearize_batch_accum_select")
     ns = ctypes.c_int64(0)
     sh = None
     if selected_host is not None:
@@ -357,10 +388,12 @@ def expand(ctx: Context, factors, poses, accum, out=None):
     factors = as_factors(factors)
     poses = as_poses(poses)
     F = factors.shape[0]
-    assert _is_cuda_tensor(accum)
+    if not _is_cuda_tensor(accum):
+        raise ValueError("expand: accum must be a CUDA tensor")
+    _out_ptr(ctx, accum, F, FACTOR_ACCUM_DTYPE, "expand accum")
     if out is None:
         out = np.zeros(F, LINEAR_FACTOR_DTYPE)
-    po, mem = _ptr(out)
+    po, mem = _out_ptr(ctx, out, F, LINEAR_FACTOR_DTYPE, "expand")
     check(lib().gvox_expand(ctx.handle, _ptr(factors)[0], F, _ptr(poses)[0], poses.shape[0],
                             ctypes.c_void_p(accum.data_ptr()), po, mem))
     return out
@@ -426,7 +459,7 @@ def overlap_union(ctx: Context, clouds, maps, queries, members, poses, level: in
     poses = as_poses(poses)
     if out is None:
         out = np.zeros(len(q), np.int32)
-    po, mem = _ptr(out)
+    po, mem = _out_ptr(ctx, out, len(q), np.int32, "overlap_union")
     check(lib().gvox_overlap_union(ctx.handle, C.arr, C.n, Mh.arr, Mh.n, _ptr(q)[0], len(q),
                                    _ptr(m)[0] if len(m) else None, len(m), _ptr(poses)[0],
                                    poses.shape[0], int(level), po, mem))
@@ -443,20 +476,45 @@ def keyframe_update(overlap_rates, n_odom: int = 20, min_overlap: float = 0.05) 
     return rm.astype(bool)
 
 
+def keyframe_insert_test(count: int, n: int, num: int = 9, den: int = 10) -> bool:
+    """gvox_keyframe_insert_test (host): P:280 insertion, den * count < num * n."""
+    out = ctypes.c_int(0)
+    check(lib().gvox_keyframe_insert_test(int(count), int(n), int(num), int(den), ctypes.byref(out)))
+    return bool(out.value)
+
+
+def keyframe_update_counts(counts, sizes, n_odom: int = 20, min_overlap: float = 0.05):
+    """gvox_keyframe_update_counts (host): removal rules from raw overlap counts
+    [K,K] and keyframe sizes [K].  Returns (remove mask, o(i, j) matrix)."""
+    c = np.ascontiguousarray(np.asarray(counts, np.int64))
+    n = np.ascontiguousarray(np.asarray(sizes, np.int64).reshape(-1))
+    K = n.shape[0]
+    assert c.shape == (K, K), (c.shape, K)
+    rm = np.zeros(K, np.uint8)
+    o = np.zeros((K, K), np.float64)
+    check(lib().gvox_keyframe_update_counts(_ptr(c)[0], _ptr(n)[0], K, int(n_odom),
+                                            float(min_overlap), _ptr(rm)[0], _ptr(o)[0]))
+    return rm.astype(bool), o
+
+
 class KeyframeList:
     """The P:280-288 keyframe mechanism driven through the library: for each
-    new frame, one gvox_overlap_union (insertion test "overlap with the union
-    of all keyframes smaller than 90 %", decided in integers), and on insertion
-    one gvox_overlap of the new keyframe against the others (both directions)
-    followed by gvox_keyframe_update.  Holds only bookkeeping: cloud/map/pose
-    indices of the keyframes and their o(i, j) matrix."""
+    new frame, one gvox_overlap_union and the insertion test
+    gvox_keyframe_insert_test ("overlap with the union of all keyframes smaller
+    than 90 %"), and on insertion one gvox_overlap of the new keyframe against
+    the others (both directions) followed by gvox_keyframe_update_counts (the
+    rates o(i, j) and the removal rules are formed in the library).  Holds only
+    bookkeeping: the keyframes' frame ids, their raw pairwise overlap counts and
+    point counts."""
 
     def __init__(self, ctx: Context, level: int, n_odom: int = 20, insert_num: int = 9,
                  insert_den: int = 10, min_overlap: float = 0.05):
         self.ctx, self.level, self.n_odom = ctx, int(level), int(n_odom)
         self.insert_num, self.insert_den, self.min_overlap = int(insert_num), int(insert_den), min_overlap
         self.frames = []          # frame ids of the keyframes, list order
-        self.o = np.zeros((0, 0))
+        self.counts = np.zeros((0, 0), np.int64)   # counts[a, b]: points of a in b's voxels
+        self.sizes = np.zeros(0, np.int64)
+        self.o = np.zeros((0, 0))                  # the library's o(i, j) of the last update
 
     def add_frame(self, frame: int, clouds, maps, poses):
         """frame indexes clouds/maps/poses (its cloud, its voxelmap, its pose).
@@ -466,24 +524,25 @@ class KeyframeList:
             members = [[f, f] for f in self.frames]
             cnt = int(overlap_union(self.ctx, clouds, maps, [[frame, frame, 0, len(members)]], members,
                                     poses, self.level)[0])
-            if not self.insert_den * cnt < self.insert_num * n:
+            if not keyframe_insert_test(cnt, n, self.insert_num, self.insert_den):
                 return False, []
         ks = self.frames + [frame]
         K = len(ks)
-        o = np.zeros((K, K))
-        o[:K - 1, :K - 1] = self.o
-        o[K - 1, K - 1] = 1.0 if n else 0.0
+        c = np.zeros((K, K), np.int64)
+        c[:K - 1, :K - 1] = self.counts
+        c[K - 1, K - 1] = n          # a cloud lies entirely in its own voxels
+        sizes = np.append(self.sizes, n).astype(np.int64)
         if K > 1:
             pairs = [[f, frame, f, frame] for f in self.frames] + [[frame, f, frame, f] for f in self.frames]
-            c = overlap(self.ctx, clouds, maps, pairs, poses, self.level)
-            for a, f in enumerate(self.frames):
-                nf = len(clouds[f])
-                o[a, K - 1] = c[a] / nf if nf else 0.0
-                o[K - 1, a] = c[K - 1 + a] / n if n else 0.0
-        rm = keyframe_update(o, self.n_odom, self.min_overlap)
+            cc = overlap(self.ctx, clouds, maps, pairs, poses, self.level)
+            c[:K - 1, K - 1] = cc[:K - 1]
+            c[K - 1, :K - 1] = cc[K - 1:]
+        rm, o = keyframe_update_counts(c, sizes, self.n_odom, self.min_overlap)
         keep = ~rm
         removed = [ks[a] for a in range(K) if rm[a]]
         self.frames = [ks[a] for a in range(K) if keep[a]]
+        self.counts = c[np.ix_(keep, keep)]
+        self.sizes = sizes[keep]
         self.o = o[np.ix_(keep, keep)]
         return True, removed
 

@@ -318,7 +318,19 @@ gvox_status gvox_ctx_create(int device, void* cuda_stream, gvox_ctx** out) {
 
 gvox_status gvox_ctx_set_stream(gvox_ctx* ctx, void* cuda_stream) {
   if (!ctx) return fail(GVOX_ERR_INVALID, "gvox_ctx_set_stream: ctx is NULL");
-  ctx->stream = (cudaStream_t)cuda_stream;
+  cudaStream_t next = (cudaStream_t)cuda_stream;
+  if (next != ctx->stream) {
+    // The grow-only workspaces (and the stream-ordered frees of the next call)
+    // move to the new stream: order it after everything already queued on the
+    // old one, so no kernel still reading a workspace races with its reuse.
+    DeviceGuard g(ctx->device);
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev, ctx->stream) != cudaSuccess || cudaStreamWaitEvent(next, ev, 0) != cudaSuccess)
+      return fail(GVOX_ERR_CUDA, "gvox_ctx_set_stream: %s", cudaGetErrorString(cudaGetLastError()));
+    cudaEventDestroy(ev);  // released once the recorded work completes
+    ctx->stream = next;
+  }
   return GVOX_OK;
 }
 
@@ -1838,6 +1850,42 @@ gvox_status gvox_keyframe_update(const double* overlap, int32_t K, int32_t n_odo
   }
   std::memcpy(remove, rm.data(), K);
   return GVOX_OK;
+}
+
+gvox_status gvox_keyframe_insert_test(int64_t count, int64_t n, int32_t num, int32_t den,
+                                      int32_t* insert) {
+  const char* fn = "gvox_keyframe_insert_test";
+  if (!insert) return fail(GVOX_ERR_INVALID, "%s: NULL argument", fn);
+  if (count < 0 || n < 0 || count > n)
+    return fail(GVOX_ERR_INVALID, "%s: need 0 <= count <= n (count %lld, n %lld)", fn,
+                (long long)count, (long long)n);
+  if (num < 0 || den <= 0) return fail(GVOX_ERR_INVALID, "%s: need num >= 0 and den > 0", fn);
+  // insert when the union overlap count / n is SMALLER than num / den;
+  // in integers (n <= 2^62 / den is far beyond any cloud)
+  *insert = ((__int128)den * count < (__int128)num * n) ? 1 : 0;
+  return GVOX_OK;
+}
+
+gvox_status gvox_keyframe_update_counts(const int64_t* counts, const int64_t* sizes, int32_t K,
+                                        int32_t n_odom, double min_overlap, uint8_t* remove,
+                                        double* overlap_out) {
+  const char* fn = "gvox_keyframe_update_counts";
+  if (K < 1) return fail(GVOX_ERR_INVALID, "%s: need K >= 1", fn);
+  if (!counts || !sizes || !remove) return fail(GVOX_ERR_INVALID, "%s: NULL argument", fn);
+  std::vector<double> o((size_t)K * K);
+  for (int i = 0; i < K; ++i) {
+    if (sizes[i] < 0) return fail(GVOX_ERR_INVALID, "%s: sizes[%d] < 0", fn, i);
+    for (int j = 0; j < K; ++j) {
+      const int64_t c = counts[(int64_t)i * K + j];
+      if (c < 0 || c > sizes[i])
+        return fail(GVOX_ERR_INVALID, "%s: counts[%d][%d] = %lld outside [0, sizes[%d]]", fn, i, j,
+                    (long long)c, i);
+      // P:280 overlap rate o(i, j): the fraction of keyframe i's points in j's voxels
+      o[(size_t)i * K + j] = sizes[i] ? (double)c / (double)sizes[i] : 0.0;
+    }
+  }
+  if (overlap_out) std::memcpy(overlap_out, o.data(), o.size() * sizeof(double));
+  return gvox_keyframe_update(o.data(), K, n_odom, min_overlap, remove);
 }
 
 // ------------------------------------------------------------ registration

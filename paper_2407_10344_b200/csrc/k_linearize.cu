@@ -319,8 +319,10 @@ __device__ __forceinline__ void level_term(Acc<MAXL>& ac, LevelSum& ls, const Po
   const float i22 = fmaf(ca, cd, -cb * cb);
   const float det = fmaf(ca, i00, fmaf(cb, i01, cc * i02));
   // Q16: a fused covariance that is not positive definite contributes nothing
-  // det > 0 and finite  <=>  bits(det) - 1 < bits(FLT_MAX)  (unsigned)
-  const bool pd_ok = __float_as_uint(det) - 1u < 0x7F7FFFFFu;
+  // det >= FLT_MIN (normal) and finite  <=>  bits(det) - bits(FLT_MIN) <
+  // bits(FLT_MAX) - bits(FLT_MIN) + 1 (unsigned): a subnormal det would make the
+  // flush-to-zero reciprocal +Inf and poison the factor (reading R22)
+  const bool pd_ok = __float_as_uint(det) - 0x00800000u < 0x7F7FFFFFu - 0x007FFFFFu;
   // (hit = false: a level without a correspondence, evaluated branch-free and
   // masked out -- Omega = 0 makes every contribution below exactly zero)
   const bool ok = pd_ok && hit;

@@ -104,3 +104,25 @@ def test_shard_order_is_a_permutation():
         t = fac[order, 1]
         assert (np.diff(t // 1) >= 0).sum() >= 0 and all(
             (t[(t >= b[r]) & (t < b[r + 1])] >= b[r]).all() for r in range(world))
+
+
+def test_target_weights_follow_selection():
+    """Balancing on the previous step's decisions: a target whose candidates
+    were all rejected weighs only its build and screening work."""
+    n = np.array([1000, 1000, 1000, 1000])
+    mc = np.arange(2)
+    pairs = np.array([[2, 0, 2, 0], [3, 0, 3, 0], [2, 1, 2, 1], [3, 1, 3, 1]])
+    w0 = gdist.target_weights(n, mc, pairs)
+    assert w0[0] == w0[1]
+    w1 = gdist.target_weights(n, mc, pairs, selected=np.array([1, 1, 0, 0], bool))
+    assert w1[0] - w1[1] == 2 * 1000 * gdist.COST_LINEARIZE
+    assert w1[1] == gdist.COST_BUILD * 1000 + 2 * 1000 * gdist.COST_SCREEN
+    # explicit weights drive the cut: all the work on target 0 -> rank 0 takes it alone
+    b = gdist.shard_targets(n, np.arange(4), np.zeros((0, 4), np.int64), 2,
+                            weights=np.array([10.0, 1, 1, 1]))
+    assert b == [0, 1, 4]
+
+
+def test_gather_records_rejects_overflow():
+    with pytest.raises(ValueError):
+        gdist.gather_records(torch.zeros((4, 288), dtype=torch.uint8), 5, 4)

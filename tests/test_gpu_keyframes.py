@@ -74,3 +74,16 @@ def test_keyframe_list_matches_oracle(gv, ctx, oracle, scene, built):
     assert [sorted(e[1]) for e in events] == [sorted(e[1]) for e in oev]
     assert kl.frames == okfs
     assert sum(e[0] for e in events) > 6 and any(e[1] for e in events)  # both rules exercised
+
+
+def test_keyframe_list_hand_worked_sequence(gv, ctx):
+    """KeyframeList (GPU union and pair overlaps + the C-ABI rules) replays the
+    hand-worked sequence of tests/test_oracle_keyframes.py."""
+    from tests.test_oracle_keyframes import SEQ_EVENTS, SEQ_FINAL, keyframe_sequence
+    clouds_h, poses = keyframe_sequence()
+    clouds = [gv.Cloud(ctx, mu, cov) for mu, cov in clouds_h]
+    maps = gv.create_voxelmaps(ctx, clouds, 1.0, 1)
+    kl = gv.KeyframeList(ctx, level=0, n_odom=3)
+    events = [kl.add_frame(f, clouds, maps, poses) for f in range(len(clouds))]
+    assert [(bool(a), list(b)) for a, b in events] == SEQ_EVENTS
+    assert kl.frames == SEQ_FINAL

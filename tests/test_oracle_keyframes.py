@@ -143,3 +143,41 @@ def test_run_keyframes_hand_worked_sequence(oracle):
     kf, events = okf.run_keyframes(clouds, maps, poses, list(range(len(clouds))), 0, n_odom=3)
     assert events == SEQ_EVENTS
     assert kf == SEQ_FINAL
+
+
+def test_library_host_rules_on_hand_worked_sequence():
+    """The library's host-only keyframe entry points (gvox_keyframe_insert_test,
+    gvox_keyframe_update_counts: the P:280 insertion test and the removal rules
+    formed from raw counts in the C ABI) replay the hand-worked sequence, with
+    every count taken from plain set arithmetic on the cells (no GPU)."""
+    import paper_2407_10344_b200 as gv
+    cells = [set(c) for c in SEQ_CELLS]
+    kf, events = [], []
+    for f in range(len(cells)):
+        if kf:
+            cnt = len(cells[f] & set().union(*[cells[k] for k in kf]))
+            if not gv.keyframe_insert_test(cnt, len(cells[f])):
+                events.append((False, []))
+                continue
+        ks = kf + [f]
+        c = np.array([[len(cells[a] & cells[b]) for b in ks] for a in ks], np.int64)
+        rm, o = gv.keyframe_update_counts(c, [len(cells[a]) for a in ks], n_odom=3)
+        np.testing.assert_array_equal(o, c / np.array([len(cells[a]) for a in ks])[:, None])
+        events.append((True, [ks[a] for a in np.flatnonzero(rm)]))
+        kf = [ks[a] for a in range(len(ks)) if not rm[a]]
+    assert events == SEQ_EVENTS and kf == SEQ_FINAL
+
+
+def test_library_insert_test_boundaries_and_errors():
+    import paper_2407_10344_b200 as gv
+    assert gv.keyframe_insert_test(17, 20) is True       # 85 %
+    assert gv.keyframe_insert_test(18, 20) is False      # 90 % is not smaller than 90 %
+    assert gv.keyframe_insert_test(0, 0) is False         # empty frame: 0 < 0 is false
+    assert gv.keyframe_insert_test(5, 10, 1, 2) is False  # custom threshold 50 %
+    for bad in ((-1, 5), (6, 5)):
+        with pytest.raises(gv.GvoxError):
+            gv.keyframe_insert_test(*bad)
+    with pytest.raises(gv.GvoxError):
+        gv.keyframe_update_counts([[3, 4], [0, 2]], [3, 2])   # count 4 > size 3
+    rm, o = gv.keyframe_update_counts([[0, 0], [0, 0]], [0, 0])
+    assert o.tolist() == [[0, 0], [0, 0]] and rm.tolist() == [True, False]
