@@ -714,7 +714,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     for (int l = 0; l < L; ++l) {
       const int64_t V = hcnt[s * L + l];
       LevelPlan& p = plan[s * L + l];
-      p.o_vox = al.add((size_t)V * 48);
+      p.o_vox = al.add((size_t)(V + 1) * 48);  // + the all-zero sentinel record at index -1
       p.o_keys = al.add((size_t)V * 8);
       total_vox += V;
     }
@@ -791,7 +791,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       f.shift = p.dense ? 64 : shift_for_capacity(p.cap);
       f.dense = p.dense;
       f.grid = nullptr;
-      f.vox = (float4*)(ab + p.o_vox);
+      f.vox = (float4*)(ab + p.o_vox) + 3;  // record -1: the zero sentinel (written by finalize)
       f.keys_out = (uint64_t*)(ab + p.o_keys);
       MapLevelDev& lv = md.lv[l];
       lv.slots = f.slots;

@@ -421,6 +421,9 @@ __global__ void __launch_bounds__(256, GVOX_FIN_MINB) k_build_finalize(const Fin
                                  const unsigned long long* __restrict__ acc) {
   const FinalSeg& sg = segs[blockIdx.y];  // one (segment, level) per grid row
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // record -1 of every level: all zeros, the record a lookup miss (index -1)
+  // gathers in the linearize kernel's unconditional loads
+  if (v < 3) sg.vox[v - 3] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (v >= sg.nvox) return;
   const unsigned long long* src = acc + (sg.acc_offset + v) * 10;
   double cnt = (double)(long long)src[9];
@@ -519,8 +522,8 @@ void launch_build_accum(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int
 
 void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs, int64_t max_seg_voxels,
                            const unsigned long long* acc, cudaStream_t stream) {
-  if (num_segs <= 0 || max_seg_voxels <= 0) return;
-  dim3 grid(grid_for(max_seg_voxels, 256), (unsigned)num_segs);
+  if (num_segs <= 0) return;  // (runs for empty maps too: it writes the sentinel records)
+  dim3 grid(grid_for(max_seg_voxels > 0 ? max_seg_voxels : 1, 256), (unsigned)num_segs);
   k_build_finalize<<<grid, 256, 0, stream>>>(segs_dev, acc);
   note_launch();
 }

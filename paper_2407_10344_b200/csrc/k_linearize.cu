@@ -62,11 +62,6 @@ namespace {
 #ifndef GVOX_LIN_CULL
 #define GVOX_LIN_CULL 1
 #endif
-// FAST pipeline: every level's term evaluated branch-free and masked (ILP across
-// levels) instead of one branch per level
-#ifndef GVOX_LIN_BRANCHLESS
-#define GVOX_LIN_BRANCHLESS 1
-#endif
 #ifndef GVOX_LIN_STAGES
 #define GVOX_LIN_STAGES (GVOX_LIN_PIPE ? 3 : 2)
 #endif
@@ -533,48 +528,56 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     // occupied coarsest-level cell has no correspondence at any level.  The warp
     // walks only its LIVE iterations (identical results: culled points add
     // nothing), so culled chunks are neither copied nor touched.
-    constexpr int kWords = (GVOX_TILE_MAX_PPT * 256 / kThreads + 31) / 32;  // bits per iteration
+    constexpr int kMaxIters = GVOX_TILE_MAX_PPT * 256 / kThreads;  // iterations per warp
+    static_assert(kMaxIters <= 256, "live iteration list holds 8-bit indices");
     constexpr int kNone = 1 << 30;
-    __shared__ uint32_t live_s[kWarps][kWords];
+    __shared__ uint8_t live_s[kWarps][kMaxIters];
     const int32_t iters = (npts - 32 * warp + kThreads - 1) / kThreads;
     const MapLevelDev& cv = sh.lv[MAXL - 1];
     // (no culling when validating: discarded points are counted, culled or not)
     const bool cull_on = GVOX_LIN_CULL && sh.cbox != nullptr && cv.grid != nullptr && !validate;
+    // the warp's LIVE iterations, compacted in order into live_s[warp][0 .. nlive)
+    int32_t nlive = 0;
 #pragma unroll 1
-    for (int i0 = 0; i0 < kWords * 32; i0 += 32) {
+    for (int i0 = 0; i0 < iters; i0 += 32) {
       const int32_t i = i0 + lane;
       bool live = i < iters;
-      if (cull_on && i0 < iters && live) {
+      if (cull_on && live) {
         const float* bx = sh.cbox + 6 * (i * kWarps + warp);
         float box[6];
 #pragma unroll
         for (int j = 0; j < 6; ++j) box[j] = __ldg(bx + j);
         live = !chunk_culled_grid(box, sh.Rf, sh.t, cv);
       }
-      live_s[warp][i0 >> 5] = __ballot_sync(0xffffffffu, live);
+      const uint32_t m = __ballot_sync(0xffffffffu, live);
+      if (live) live_s[warp][nlive + __popc(m & ((1u << lane) - 1u))] = (uint8_t)i;
+      nlive += __popc(m);
     }
     __syncwarp();
-    // smallest live iteration > i (kNone if none)
-    auto next_live = [&](int32_t i) -> int32_t {
-      int w = (i + 1) >> 5;
-      if (w >= kWords) return kNone;
-      uint32_t m = live_s[warp][w] & (0xffffffffu << ((i + 1) & 31));
-      while (!m) {
-        if (++w >= kWords) return kNone;
-        m = live_s[warp][w];
+    const uint8_t* live_w = live_s[warp];
+    auto live_at = [&](int32_t j) -> int32_t { return j < nlive ? (int32_t)live_w[j] : kNone; };
+    // Per-thread copy addresses: iteration i of this warp is tile chunk
+    // i * kWarps + warp, i.e. a fixed stride from the warp's first chunk; this
+    // lane's slots of stage s sit at s_lane + s * (one stage).
+    const float4* const g_lane = sh.A + (warp * 96 + lane);
+    constexpr int kChunkStride = kWarps * 96;  // float4 per iteration
+    constexpr unsigned kStageBytes = (unsigned)sizeof(sbuf[0][0]);
+    // the j-th live iteration's copy into stage j % S (one group per slot,
+    // empty when the iteration does not exist or this lane has no point)
+    auto issue_l = [&](int32_t i, unsigned sa) {
+      if (i != kNone && i * kThreads + tid < npts) {
+        const float4* g = g_lane + i * kChunkStride;
+        cp_async16_s(sa, g);
+        cp_async16_s(sa + 512u, g + 32);
+        cp_async16_s(sa + 1024u, g + 64);
       }
-      return (w << 5) + __ffs(m) - 1;
+      cp_async_commit();
     };
-    // stages follow the live SEQUENCE: the j-th live iteration uses stage j % S
-    auto issue_l = [&](int32_t i, int stg) {
-      if (i != kNone) issue(i, stg);
-      else cp_async_commit();  // keep one group per sequence slot
-    };
-    int32_t i_cur = next_live(-1);
-    int32_t i_nxt = i_cur == kNone ? kNone : next_live(i_cur);
-    int32_t i_nx2 = i_nxt == kNone ? kNone : next_live(i_nxt);
-    issue_l(i_cur, 0);
-    issue_l(i_nxt, 1);
+    int32_t i_cur = live_at(0);
+    int32_t i_nxt = live_at(1);
+    int32_t i_nx2 = live_at(2);
+    issue_l(i_cur, s_lane);
+    issue_l(i_nxt, s_lane + kStageBytes);
     cp_async_wait<S - 2>();  // the first live iteration landed
     PointData pn;
     int32_t vn[MAXL];
@@ -598,9 +601,10 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     };
     prep(i_cur, 0);
     int st = 0;  // stage of the current live iteration
-    while (i_cur != kNone) {
-      issue_l(i_nx2, st == 0 ? S - 1 : st - 1);  // sequence slot j + 2
-      cp_async_wait<S - 2>();                    // slot j + 1 landed
+#pragma unroll 1
+    for (int32_t j = 0; j < nlive; ++j) {
+      issue_l(i_nx2, s_lane + (unsigned)(st == 0 ? S - 1 : st - 1) * kStageBytes);  // slot j + 2
+      cp_async_wait<S - 2>();                                                        // slot j + 1 landed
       const int cur = st;
       if (++st == S) st = 0;
       const int32_t k = i_cur * kThreads + tid;
@@ -612,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       prep(i_nxt, st);
       i_cur = i_nxt;
       i_nxt = i_nx2;
-      i_nx2 = i_nx2 == kNone ? kNone : next_live(i_nx2);
+      i_nx2 = live_at(j + 3);
       if (VALID && inv) {  // (k < npts: only real points are marked)
         ++ac.n_invisible;
         continue;
@@ -621,20 +625,17 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) any |= vid[l] >= 0;
       if (k >= npts || !any) continue;
+      // every level's record is loaded unconditionally: a level without a
+      // correspondence (index -1) reads the level's all-zero sentinel record
+      // at index -1 (masked out in level_term, exactly as zeros)
       float4 v0[MAXL], v1[MAXL];
       float v2[MAXL];
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) {
-        if (GVOX_LIN_BRANCHLESS) {
-          v0[l] = v1[l] = make_float4(0.f, 0.f, 0.f, 0.f);
-          v2[l] = 0.f;
-        }
-        if (vid[l] >= 0) {
-          const float4* vp = sh.lv[l].vox + 3 * (int64_t)vid[l];
-          v0[l] = __ldg(vp);
-          v1[l] = __ldg(vp + 1);
-          v2[l] = __ldg(&vp[2].x);
-        }
+        const float4* vp = sh.lv[l].vox + 3 * vid[l];
+        v0[l] = __ldg(vp);
+        v1[l] = __ldg(vp + 1);
+        v2[l] = __ldg(&vp[2].x);
       }
       const float4 a = sbuf[warp][cur][0][lane], b = sbuf[warp][cur][1][lane],
                    c = sbuf[warp][cur][2][lane];
@@ -643,12 +644,8 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       ls.Oa = ls.Oc = ls.G = 0;
       ls.o11 = ls.o22 = ls.gz = 0.f;
 #pragma unroll
-      for (int l = 0; l < MAXL; ++l) {
-        if (GVOX_LIN_BRANCHLESS)
-          level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, r0f, vid[l] >= 0);
-        else if (vid[l] >= 0)
-          level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, r0f);
-      }
+      for (int l = 0; l < MAXL; ++l)
+        level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, r0f, vid[l] >= 0);
       if (!error_only) fold_point<MAXL>(ac, ls, pd);
     }
     tile_reduce<MAXL>(ac, red, partials, tile);

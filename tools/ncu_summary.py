@@ -68,9 +68,23 @@ def main(rep, out, pf=None):
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         b = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
         inst = val("smsp__inst_executed.sum")
+        def pct(k):
+            try:
+                return float(lin[hdr.index(k)])
+            except (ValueError, IndexError):
+                return None
         json.dump({"dram_bytes_per_point_factor": b / pf, "source": os.path.basename(rep),
                    "point_factors": pf, "dram_bytes": b,
-                   "warp_instructions_per_point_factor": inst / pf},
+                   "warp_instructions_per_point_factor": inst / pf,
+                   "fma_pipe_pct": pct("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "alu_pipe_pct": pct("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "fp64_pipe_pct": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                   "dram_pct_of_peak": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                   "occupancy_pct": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                   "duration_ms": float(lin[hdr.index("gpu__time_duration.sum")]) * {
+                       "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ms": 1.0, "us": 1e-3,
+                       "ns": 1e-6}.get(units[hdr.index("gpu__time_duration.sum")], float("nan"))},
                   open(os.path.join(os.path.dirname(out), "linearize_dram_bytes_per_pf.json"), "w"),
                   indent=1)
 
