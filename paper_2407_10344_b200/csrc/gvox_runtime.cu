@@ -578,13 +578,24 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     for (int l = 0; l < L; ++l) {
       LevelPlan& p = plan[s * L + l];
       uint64_t cells = 1;
-      int32_t lo3[3], n3[3];
+      int32_t lo3[3];
+      int64_t n3[3];
+      // NESTED boxes: every level's box is the coarsest level's key box refined
+      // (x0_l = x0_c * 2^(L-1-l), d_l = d_c * 2^(L-1-l)), so a level-0 key is
+      // inside the level-0 box iff its level-l key (k >> l) is inside the
+      // level-l box, for every l: the linearize kernel tests the bounds once
+      // per point (k_linearize.cu lookup_nested).  Costs at most 2^(L-1) - 1
+      // padding cells per side of the finer grids.
+      const int sc = L - 1 - l;
       for (int a = 0; a < 3; ++a) {
-        lo3[a] = k0lo[a] >> l;
-        n3[a] = (k0hi[a] >> l) - lo3[a] + 1;
-        cells *= (uint64_t)n3[a];
+        const int32_t clo = k0lo[a] >> (L - 1), chi = k0hi[a] >> (L - 1);
+        lo3[a] = clo * (1 << sc);  // |clo| <= 2^30 >> (L - 1): no overflow
+        n3[a] = ((int64_t)chi - clo + 1) << sc;
       }
       const bool dims_ok = n3[0] < (1 << 30) && n3[1] < (1 << 30) && n3[2] < (1 << 30);
+      // (saturating: a product above 2^62 is far beyond any dense grid)
+      for (int a = 0; a < 3; ++a)
+        cells = (dims_ok && cells <= (1ull << 32)) ? cells * (uint64_t)n3[a] : (1ull << 62);
       if (c->n > 0 && dims_ok && cells <= dense_ratio * (uint64_t)c->n &&
           cells < (1ull << 31)) {
         p.dense = true;

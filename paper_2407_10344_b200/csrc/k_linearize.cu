@@ -65,6 +65,16 @@ namespace {
 #ifndef GVOX_LIN_STAGES
 #define GVOX_LIN_STAGES (GVOX_LIN_PIPE ? 3 : 2)
 #endif
+// FAST all-dense probes: one bounds test per point on the nested grid boxes (1)
+// or one per level (0; both correct on nested boxes)
+#ifndef GVOX_LIN_NESTED
+#define GVOX_LIN_NESTED 1
+#endif
+// residual base of level l > 0 from level l - 1's (one select + add per axis, 1)
+// or from the level-0 base and the key's low bits (0)
+#ifndef GVOX_LIN_INCBASE
+#define GVOX_LIN_INCBASE 0
+#endif
 
 
 constexpr int kThreads = GVOX_LIN_THREADS;
@@ -141,6 +151,27 @@ __device__ __forceinline__ int32_t lookup_dense_pred(const MapLevelDev& lv, int3
   int32_t v = -1;
   if (in) v = __ldg(lv.grid + (cx * b1.z + cy * b1.y + cz));
   return v;
+}
+
+// All-dense maps of this library have NESTED grid boxes (gvox_runtime.cu build
+// plan: level l's box is the coarsest box refined, x0_l = x0_0 >> l, d_l =
+// d_0 >> l), so the level-0 bounds test decides every level and the level-l
+// cell is the level-0 cell offset shifted: one subtraction and one unsigned
+// compare per axis per POINT instead of per level.
+template <int MAXL>
+__device__ __forceinline__ void lookup_nested(const MapLevelDev* lv, int32_t kx, int32_t ky,
+                                              int32_t kz, int32_t* vid) {
+  const int4 b0 = *reinterpret_cast<const int4*>(&lv[0].x0);  // x0 y0 z0 dx
+  const uint4 b1 = *reinterpret_cast<const uint4*>(&lv[0].dy);  // dy dz syz dense
+  const uint32_t cx = (uint32_t)(kx - b0.x), cy = (uint32_t)(ky - b0.y), cz = (uint32_t)(kz - b0.z);
+  const bool in = (cx < (uint32_t)b0.w) & (cy < b1.x) & (cz < b1.y);
+#pragma unroll
+  for (int l = 0; l < MAXL; ++l) {
+    const uint4 bl = l == 0 ? b1 : *reinterpret_cast<const uint4*>(&lv[l].dy);
+    int32_t v = -1;
+    if (in) v = __ldg(lv[l].grid + ((cx >> l) * bl.z + (cy >> l) * bl.y + (cz >> l)));
+    vid[l] = v;
+  }
 }
 
 // 1/x for x > 0 finite (MUFU.RCP, ~1 ulp)
@@ -294,12 +325,37 @@ struct LevelSum {
   float gz;
 };
 
+// Residual base of level l, centre_l - q, in fp32 (reading Q12: the fp64 part
+// is the level-0 base pd.e = centre_0 - q).  Call for l = 0, 1, ... in order
+// with (bx, by, bz) = pd.e before level 0.
+//  INCBASE 0: with k_l = k0 >> l, centre_l - q = (centre_0 - q)
+//             + r0 (2^(l-1) - 1/2 - (k0 & (2^l - 1)))   (from level 0 each time)
+//  INCBASE 1: centre_l - centre_(l-1) = r_(l-1) (1/2 - bit_(l-1)(k0)), so each
+//             level adds +-r_(l-1)/2 to the previous level's base
+__device__ __forceinline__ void level_base(const PointData& pd, const int l, const float r0f,
+                                           float& bx, float& by, float& bz) {
+  if (l == 0) return;
+#if GVOX_LIN_INCBASE
+  const float h = 0.5f * r0f * (float)(1 << (l - 1));  // exact: a power-of-two multiple
+  bx += ((pd.kb >> (l - 1)) & 1u) ? -h : h;
+  by += ((pd.kb >> (l + 7)) & 1u) ? -h : h;
+  bz += ((pd.kb >> (l + 15)) & 1u) ? -h : h;
+#else
+  const int mlo = (1 << l) - 1;
+  const float sh_l = 0.5f * (float)(1 << l) - 0.5f;
+  bx = fmaf(r0f, sh_l - (float)(pd.kb & mlo), pd.ex);
+  by = fmaf(r0f, sh_l - (float)((pd.kb >> 8) & mlo), pd.ey);
+  bz = fmaf(r0f, sh_l - (float)((pd.kb >> 16) & mlo), pd.ez);
+#endif
+}
+
 // One (point, level) term: Eq.3 fused covariance, Omega, residual, g = Omega d,
 // e = d^T g.  v0 = {off.xyz, C.xx}, v1 = {C.xy, C.yy, C.xz, C.yz}, v2 = C.zz.
 template <int MAXL>
 __device__ __forceinline__ void level_term(Acc<MAXL>& ac, LevelSum& ls, const PointData& pd,
                                            const float4 v0, const float4 v1, const float v2,
-                                           const int l, const float r0f, const bool hit = true) {
+                                           const int l, const float bx, const float by,
+                                           const float bz, const bool hit = true) {
   // fused covariance (Eq.3)
   const f2_t P = add2(pk(v1.x, v1.y), pd.Sp1);  // (cb, cd) = (xy, yy)
   const f2_t Q = add2(pk(v1.z, v1.w), pd.Sp2);  // (cc, ce) = (xz, yz)
@@ -329,16 +385,8 @@ __device__ __forceinline__ void level_term(Acc<MAXL>& ac, LevelSum& ls, const Po
   const f2_t Om_c = mul2(pk(i02, i12), bc(id));  // (o02, o12) = column 2, rows 0-1
   const float o22 = i22 * id;
 
-  // d = mu~ - q = (centre_l - q) + offset (Q12): with k_l = k0 >> l,
-  // centre_l - q = (centre_0 - q) + r0 (2^(l-1) - 1/2 - (k0 & (2^l - 1))).
-  float bx = pd.ex, by = pd.ey, bz = pd.ez;
-  if (l > 0) {
-    const int mlo = (1 << l) - 1;
-    const float sh_l = 0.5f * (float)(1 << l) - 0.5f;
-    bx = fmaf(r0f, sh_l - (float)(pd.kb & mlo), pd.ex);
-    by = fmaf(r0f, sh_l - (float)((pd.kb >> 8) & mlo), pd.ey);
-    bz = fmaf(r0f, sh_l - (float)((pd.kb >> 16) & mlo), pd.ez);
-  }
+  // d = mu~ - q = (centre_l - q) + offset (Q12); (bx, by, bz) = centre_l - q
+  // from level_base
   const f2_t D = add2(pk(bx, by), pk(v0.x, v0.y));  // (dx, dy)
   const float dz = bz + v0.z;
   const float dx = lo(D), dy = hi(D);
@@ -529,9 +577,9 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     // walks only its LIVE iterations (identical results: culled points add
     // nothing), so culled chunks are neither copied nor touched.
     constexpr int kMaxIters = GVOX_TILE_MAX_PPT * 256 / kThreads;  // iterations per warp
-    static_assert(kMaxIters <= 256, "live iteration list holds 8-bit indices");
-    constexpr int kNone = 1 << 30;
-    __shared__ uint8_t live_s[kWarps][kMaxIters];
+    static_assert(kMaxIters < 65535, "live iteration list holds 16-bit indices");
+    constexpr int kNone = 0xFFFF;  // list padding: past every thread's last iteration
+    __shared__ uint16_t live_s[kWarps][kMaxIters + 3];
     const int32_t iters = (npts - 32 * warp + kThreads - 1) / kThreads;
     const MapLevelDev& cv = sh.lv[MAXL - 1];
     // (no culling when validating: discarded points are counted, culled or not)
@@ -550,12 +598,15 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
         live = !chunk_culled_grid(box, sh.Rf, sh.t, cv);
       }
       const uint32_t m = __ballot_sync(0xffffffffu, live);
-      if (live) live_s[warp][nlive + __popc(m & ((1u << lane) - 1u))] = (uint8_t)i;
+      if (live) live_s[warp][nlive + __popc(m & ((1u << lane) - 1u))] = (uint16_t)i;
       nlive += __popc(m);
     }
+    if (lane < 3) live_s[warp][nlive + lane] = (uint16_t)kNone;  // the pipeline reads up to j + 3
     __syncwarp();
-    const uint8_t* live_w = live_s[warp];
-    auto live_at = [&](int32_t j) -> int32_t { return j < nlive ? (int32_t)live_w[j] : kNone; };
+    const uint16_t* live_w = live_s[warp];
+    auto live_at = [&](int32_t j) -> int32_t { return (int32_t)live_w[j]; };
+    // this thread's point exists in iteration i  <=>  i < my_iters (kNone never)
+    const int32_t my_iters = npts > tid ? (npts - tid + kThreads - 1) / kThreads : 0;
     // Per-thread copy addresses: iteration i of this warp is tile chunk
     // i * kWarps + warp, i.e. a fixed stride from the warp's first chunk; this
     // lane's slots of stage s sit at s_lane + s * (one stage).
@@ -565,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     // the j-th live iteration's copy into stage j % S (one group per slot,
     // empty when the iteration does not exist or this lane has no point)
     auto issue_l = [&](int32_t i, unsigned sa) {
-      if (i != kNone && i * kThreads + tid < npts) {
+      if (i < my_iters) {
         const float4* g = g_lane + i * kChunkStride;
         cp_async16_s(sa, g);
         cp_async16_s(sa + 512u, g + 32);
@@ -586,17 +637,24 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) vn[l] = -1;
       inv_n = false;
-      if (i != kNone && i * kThreads + tid < npts) {
+      if (i < my_iters) {
         const float4 a = sbuf[warp][stg][0][lane];
         if (VALID && validate && invisible(sh, a, sbuf[warp][stg][2][lane])) {
           inv_n = true;
           return;
         }
         transform_point(sh, a, 1, r0, inv_r0, r0f, pn);
+        if (ALL_DENSE && GVOX_LIN_NESTED) {
+          lookup_nested<MAXL>(sh.lv, pn.k0x, pn.k0y, pn.k0z, vn);
+        } else if (ALL_DENSE) {
 #pragma unroll
-        for (int l = 0; l < MAXL; ++l)
-          vn[l] = ALL_DENSE ? lookup_dense_pred(sh.lv[l], pn.k0x >> l, pn.k0y >> l, pn.k0z >> l)
-                            : lookup_level<false>(sh.lv[l], pn.k0x >> l, pn.k0y >> l, pn.k0z >> l);
+          for (int l = 0; l < MAXL; ++l)
+            vn[l] = lookup_dense_pred(sh.lv[l], pn.k0x >> l, pn.k0y >> l, pn.k0z >> l);
+        } else {
+#pragma unroll
+          for (int l = 0; l < MAXL; ++l)
+            vn[l] = lookup_level<false>(sh.lv[l], pn.k0x >> l, pn.k0y >> l, pn.k0z >> l);
+        }
       }
     };
     prep(i_cur, 0);
@@ -607,7 +665,6 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       cp_async_wait<S - 2>();                                                        // slot j + 1 landed
       const int cur = st;
       if (++st == S) st = 0;
-      const int32_t k = i_cur * kThreads + tid;
       PointData pd = pn;
       int32_t vid[MAXL];
 #pragma unroll
@@ -624,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       bool any = false;
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) any |= vid[l] >= 0;
-      if (k >= npts || !any) continue;
+      if (!any) continue;  // (also every lane without a point: prep left its indices -1)
       // every level's record is loaded unconditionally: a level without a
       // correspondence (index -1) reads the level's all-zero sentinel record
       // at index -1 (masked out in level_term, exactly as zeros)
@@ -643,9 +700,12 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       LevelSum ls;
       ls.Oa = ls.Oc = ls.G = 0;
       ls.o11 = ls.o22 = ls.gz = 0.f;
+      float bx = pd.ex, by = pd.ey, bz = pd.ez;
 #pragma unroll
-      for (int l = 0; l < MAXL; ++l)
-        level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, r0f, vid[l] >= 0);
+      for (int l = 0; l < MAXL; ++l) {
+        level_base(pd, l, r0f, bx, by, bz);
+        level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, bx, by, bz, vid[l] >= 0);
+      }
       if (!error_only) fold_point<MAXL>(ac, ls, pd);
     }
     tile_reduce<MAXL>(ac, red, partials, tile);
@@ -679,6 +739,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     }
     PointData pd;
     transform_point(sh, a, dyadic, r0, inv_r0, r0f, pd);
+    float bx = pd.ex, by = pd.ey, bz = pd.ez;  // residual base, advanced level by level
     bool have_rcr = false;
     LevelSum ls;
     ls.Oa = ls.Oc = ls.G = 0;
@@ -708,7 +769,12 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       bool any = false;
 #pragma unroll
       for (int j = 0; j < G; ++j) any |= vid[j] >= 0;
-      if (!any) continue;
+      if (!any) {
+#pragma unroll
+        for (int j = 0; j < G; ++j)  // (the bases of the skipped levels still advance)
+          if (lb + j > 0) level_base(pd, lb + j, r0f, bx, by, bz);
+        continue;
+      }
       float4 v0[G], v1[G];
       float v2[G];
 #pragma unroll
@@ -725,8 +791,10 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
         rcr(sh.Rf, a, b, c, pd);
       }
 #pragma unroll
-      for (int j = 0; j < G; ++j)
-        if (vid[j] >= 0) level_term<MAXL>(ac, ls, pd, v0[j], v1[j], v2[j], lb + j, r0f);
+      for (int j = 0; j < G; ++j) {
+        if (lb + j > 0) level_base(pd, lb + j, r0f, bx, by, bz);
+        if (vid[j] >= 0) level_term<MAXL>(ac, ls, pd, v0[j], v1[j], v2[j], lb + j, bx, by, bz);
+      }
     }
     if (have_rcr && !error_only) fold_point<MAXL>(ac, ls, pd);
   }

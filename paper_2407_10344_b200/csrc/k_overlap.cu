@@ -37,6 +37,12 @@ constexpr int kThreads = 256;
 #ifndef GVOX_OVL_CULL
 #define GVOX_OVL_CULL 1
 #endif
+// screening without block barriers: warps publish (hits, points processed) into
+// one packed 64-bit shared counter and stop on a certain decision (1), or the
+// windowed block reductions (0)
+#ifndef GVOX_OVL_NOBAR
+#define GVOX_OVL_NOBAR 1
+#endif
 
 template <bool ALL_DENSE>
 __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
@@ -279,6 +285,168 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   if (tid == 0) selected[p] = sel ? 1 : 0;
 }
 
+// Barrier-free screening decision (same contract as k_overlap_select).  The
+// CTA keeps ONE packed shared counter prog = hits << 32 | points processed;
+// each warp walks its chunks (warp w owns chunk 8 m + w of sub-step m, the
+// chunks of a 32-sub-step word culled together as above), probes up to four
+// live chunks at a time, then adds its group's (hits, points) with a single
+// shared atomicAdd -- culled chunks count as processed with no hit -- and
+// reads back a consistent snapshot of both:
+//   hits >= need                      -> selected (hits only grow),
+//   hits + (n - processed) < need     -> rejected (every unprocessed point,
+//                                        in flight in other warps or not yet
+//                                        reached, could at most hit),
+// so every decision is the one the exact count gives, and no warp waits at a
+// barrier for the others.  A decided CTA's warps stop at their next check.
+template <bool ALL_DENSE>
+__global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
+    k_overlap_select_nb(const CloudDev* const* __restrict__ clouds,
+                        const MapDev* const* __restrict__ maps, const PairDev* __restrict__ pairs,
+                        const double* __restrict__ poses, int level, int32_t num, int32_t den,
+                        uint8_t* __restrict__ selected) {
+  __shared__ double pose_s[24];
+  __shared__ double R[9], t[3];
+  __shared__ const float4* A_s;
+  __shared__ int64_t n_s;
+  __shared__ MapLevelDev lv_s;
+  __shared__ int dyadic_s;
+  __shared__ float Rf[9], map_lo[4], map_hi[4];
+  __shared__ const float* cbox_s;
+  __shared__ MapLevelDev cv_s;
+  __shared__ unsigned long long prog;  // hits << 32 | processed points
+  __shared__ int decided;              // 0 open, 1 selected, 2 rejected
+  const int tid = threadIdx.x;
+  const int32_t p = blockIdx.x;
+  const PairDev pd = pairs[p];
+  if (tid < 24) {
+    pose_s[tid] = __ldg(poses + 12 * (int64_t)(tid < 12 ? pd.pi : pd.pj) + (tid % 12));
+  } else if (tid == 32) {
+    const CloudDev* cd = clouds[pd.src];
+    A_s = cd->A;
+    cbox_s = cd->chunk_box;
+    n_s = cd->n;
+  } else if (tid == 64) {
+    const MapDev* md = maps[pd.tgt];
+    lv_s = md->lv[level];
+    dyadic_s = md->dyadic;
+    for (int j = 0; j < 4; ++j) {
+      map_lo[j] = md->box_lo[j];
+      map_hi[j] = md->box_hi[j];
+    }
+    cv_s = md->lv[md->levels - 1];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double v[3];
+    relative_pose_dev(pose_s, pose_s + 12, R, t, v);
+    for (int j = 0; j < 9; ++j) Rf[j] = (float)R[j];
+    prog = 0ull;
+    decided = 0;
+  }
+  __syncthreads();
+  const MapLevelDev lv = lv_s;
+  const int dyadic = dyadic_s;
+  const float4* __restrict__ A = A_s;
+  const int64_t n = n_s;  // < 2^32 (cloud sizes are int32-indexed on the device)
+  const float* cbox = cbox_s;
+  const int64_t nchunks = (n + 31) >> 5;
+  const int64_t need = (n * (int64_t)num) / den + 1;  // count * den > n * num <=> count >= need
+  const int warp = tid >> 5, lane = tid & 31;
+  const int64_t msteps = (n + kThreads - 1) / kThreads;
+  const uint32_t tail_pts = (uint32_t)(n - 32 * (nchunks - 1));  // points of the last chunk
+  // points in the chunks of sub-steps mb + j, j in mask (all 32 but the tail chunk)
+  auto mask_pts = [&](int64_t mb, uint32_t mask) -> uint32_t {
+    uint32_t pts = 32u * (uint32_t)__popc(mask);
+    const int64_t jt = (nchunks - 1 - warp) / (kThreads / 32) - mb;  // sub-step of the tail chunk
+    if ((nchunks - 1 - warp) % (kThreads / 32) == 0 && jt >= 0 && jt < 32 && (mask >> jt & 1u))
+      pts -= 32u - tail_pts;
+    return pts;
+  };
+  auto probe = [&](int64_t m) -> int {
+    const int64_t k = m * kThreads + 32 * warp + lane;
+    if (k >= n) return 0;
+    const float4 a = __ldg(A + pt_off(k));
+    const double mx = a.x, my = a.y, mz = a.z;
+    const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
+    const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
+    const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
+    const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
+    const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
+    const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
+    return lookup_level<ALL_DENSE>(lv, kx, ky, kz) >= 0;
+  };
+  // publish (h, pts); true once the CTA's decision is certain
+  auto publish = [&](int h, uint32_t pts) -> bool {
+    int dec = 0;
+    if (lane == 0) {
+      const unsigned long long add = ((unsigned long long)(unsigned)h << 32) | pts;
+      const unsigned long long now = atomicAdd(&prog, add) + add;
+      const int64_t hits = (int64_t)(now >> 32), proc = (int64_t)(now & 0xffffffffull);
+      if (hits >= need) dec = 1;
+      else if (hits + (n - proc) < need) dec = 2;
+      if (dec) atomicExch(&decided, dec);
+      else dec = *((volatile int*)&decided);
+    }
+    return __shfl_sync(0xffffffffu, dec, 0) != 0;
+  };
+#pragma unroll 1
+  for (int64_t mb = 0; mb < msteps; mb += 32) {
+    uint32_t cull = 0;
+    if (GVOX_OVL_CULL && cbox)
+      cull = cull_ballot(cbox, mb * (kThreads / 32) + warp, kThreads / 32, nchunks, Rf, t, map_lo,
+                         map_hi, (cv_s.dense && cv_s.grid) ? &cv_s : nullptr);
+    // this warp's real chunks of the word (sub-steps whose chunk exists)
+    uint32_t real = 0;
+    {
+      const int64_t c0 = mb * (kThreads / 32) + warp;  // chunk of sub-step mb
+      const int64_t left = c0 < nchunks ? (nchunks - 1 - c0) / (kThreads / 32) + 1 : 0;
+      real = left >= 32 ? 0xffffffffu : ((1u << left) - 1u);
+    }
+    uint32_t w = ~cull & real;
+    const uint32_t culled = cull & real;
+    bool stop = culled && publish(0, mask_pts(mb, culled));  // culled: processed, no hit
+    while (w && !stop) {
+      uint32_t g = 0;  // the group's chunks (up to four)
+      int h;
+      const int j0 = __ffs(w) - 1;
+      w &= w - 1;
+      g |= 1u << j0;
+      if (w) {
+        const int j1 = __ffs(w) - 1;
+        w &= w - 1;
+        g |= 1u << j1;
+        if (w) {
+          const int j2 = __ffs(w) - 1;
+          w &= w - 1;
+          g |= 1u << j2;
+          if (w) {
+            const int j3 = __ffs(w) - 1;
+            w &= w - 1;
+            g |= 1u << j3;
+            h = (probe(mb + j0) + probe(mb + j1)) + (probe(mb + j2) + probe(mb + j3));
+          } else {
+            h = probe(mb + j0) + probe(mb + j1) + probe(mb + j2);
+          }
+        } else {
+          h = probe(mb + j0) + probe(mb + j1);
+        }
+      } else {
+        h = probe(mb + j0);
+      }
+      h = __reduce_add_sync(0xffffffffu, h);
+      stop = publish(h, mask_pts(mb, g));
+    }
+    if (stop) break;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // undecided only if every point was processed without a certain decision
+    // before the last publish (n = 0, or the final snapshot): decide on the count
+    const int dec = decided;
+    selected[p] = (dec == 1 || (dec == 0 && (int64_t)(prog >> 32) >= need)) ? 1 : 0;
+  }
+}
+
 }  // namespace
 
 void launch_overlap(const CloudDev* const* clouds, const MapDev* const* maps, const PairDev* pairs,
@@ -303,7 +471,14 @@ void launch_overlap_select(const CloudDev* const* clouds, const MapDev* const* m
                            int32_t num, int32_t den, uint8_t* selected, bool all_dense,
                            cudaStream_t stream) {
   if (num_pairs <= 0) return;
-  if (all_dense)
+  if (GVOX_OVL_NOBAR) {
+    if (all_dense)
+      k_overlap_select_nb<true><<<(unsigned)num_pairs, kThreads, 0, stream>>>(
+          clouds, maps, pairs, poses, level, num, den, selected);
+    else
+      k_overlap_select_nb<false><<<(unsigned)num_pairs, kThreads, 0, stream>>>(
+          clouds, maps, pairs, poses, level, num, den, selected);
+  } else if (all_dense)
     k_overlap_select<true><<<(unsigned)num_pairs, kThreads, 0, stream>>>(
         clouds, maps, pairs, poses, level, num, den, selected);
   else

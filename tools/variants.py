@@ -13,6 +13,8 @@ OUT = os.path.join(ROOT, "paper_2407_10344_b200", "build", "variants")
 VARIANTS = {
     # linearize kernel (C5, r01 results in k_linearize.cu's knob comment)
     "base": [],
+    "lin_nonest": ["GVOX_LIN_NESTED=0"],
+    "lin_incbase": ["GVOX_LIN_INCBASE=1"],
     "s3": ["GVOX_LIN_STAGES=3"],
     "nopipe": ["GVOX_LIN_PIPE=0"],
     "nocull": ["GVOX_LIN_CULL=0"],
@@ -42,6 +44,10 @@ VARIANTS = {
     "t160_b3": ["GVOX_LIN_THREADS=160", "GVOX_LIN_MINB=3"],
     # overlap kernel (stage times from a full bench run)
     "ovl_base": [],
+    "ovl_bar": ["GVOX_OVL_NOBAR=0"],
+    "ovl_nobar": ["GVOX_OVL_NOBAR=1"],
+    "ovl_nobar_b6": ["GVOX_OVL_NOBAR=1", "GVOX_OVL_MINB=6"],
+    "ovl_nobar_b8": ["GVOX_OVL_NOBAR=1", "GVOX_OVL_MINB=8"],
     "acc_seg1": ["GVOX_ACC_SEG_MIN=1"],
     "acc_seg6": ["GVOX_ACC_SEG_MIN=6"],
     "acc_noseg": ["GVOX_ACC_SEG_MIN=99"],
