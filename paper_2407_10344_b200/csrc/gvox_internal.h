@@ -240,6 +240,20 @@ void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs, int64_t m
 
 void launch_fill_u64(uint64_t* p, uint64_t value, int64_t count, cudaStream_t stream);
 
+// Recycling of dense index grids (gvox_runtime.cu GridArena): a dense level's
+// only non-empty cells are its voxels' cells, so writing -1 back into exactly
+// those cells returns the grid to the all-empty state a build expects -- V
+// scattered stores instead of a fill of the whole box.
+struct ResetSeg {
+  const uint64_t* keys;  // the level's packed voxel keys [nvox]
+  int32_t* grid;
+  int64_t nvox;
+  int32_t x0, y0, z0;
+  uint32_t dy, dz;
+};
+void launch_grid_reset(const ResetSeg* segs_dev, int64_t num_segs, int64_t max_seg_voxels,
+                       cudaStream_t stream);
+
 // lookup
 void launch_lookup(const MapDev* map, int level, const double* q, int64_t n, int64_t* out,
                    cudaStream_t stream);
@@ -256,7 +270,7 @@ void launch_overlap(const CloudDev* const* clouds, const MapDev* const* maps, co
 void launch_overlap_select(const CloudDev* const* clouds, const MapDev* const* maps,
                            const PairDev* pairs, int64_t num_pairs, const double* poses, int level,
                            int32_t num, int32_t den, uint8_t* selected, bool all_dense,
-                           cudaStream_t stream);
+                           bool all_dyadic, cudaStream_t stream);
 
 // union overlap (P:280 keyframe insertion): query q = source cloud at pose pi
 // against members[first, first + count) = {target map, pose_j}

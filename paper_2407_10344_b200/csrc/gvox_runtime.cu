@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -137,6 +138,114 @@ gvox_status devbuf_alloc(size_t bytes, int device, cudaStream_t stream,
   return GVOX_OK;
 }
 
+// Recycled dense index grids.  A build needs its grids all -1 (empty); a
+// fresh arena gets a full fill, a recycled one is already clean: when the last
+// map of a build goes, its GridArena writes -1 back into exactly the cells its
+// voxels set (launch_grid_reset: V scattered stores instead of a fill of the
+// whole key box -- at C5 ~6e7 cells instead of ~5e9) and parks the memory in
+// its context's pool, from which the next build of about the same size takes
+// it (stream-ordered after the reset by an event).  At most kGridPoolKeep
+// arenas are kept; the pool outlives its context while arenas refer to it.
+constexpr size_t kGridPoolKeep = 2;
+struct GridPool {
+  struct Entry {
+    void* ptr;
+    size_t bytes;
+    cudaStream_t stream;
+    cudaEvent_t ready;  // the reset that cleaned it has run
+  };
+  std::mutex mu;
+  std::vector<Entry> free;
+  int device = 0;
+  static void release(const Entry& e, int device) {
+    DeviceGuard g(device);
+    if (cudaFreeAsync(e.ptr, e.stream) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(e.ptr);
+    }
+    cudaEventDestroy(e.ready);
+  }
+  ~GridPool() {
+    for (const Entry& e : free) release(e, device);
+  }
+};
+
+struct GridArena {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::shared_ptr<GridPool> pool;  // null: freed, not recycled
+  std::shared_ptr<DevBuf> rec;     // record arena: keys + reset table, alive until the reset ran
+  const ResetSeg* reset = nullptr;
+  int64_t nreset = 0, max_vox = 0;
+  ~GridArena() {
+    if (!ptr) return;
+    DeviceGuard g(device);
+    cudaEvent_t ev = nullptr;
+    if (pool && reset && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+      launch_grid_reset(reset, nreset, max_vox, stream);
+      if (cudaGetLastError() == cudaSuccess && cudaEventRecord(ev, stream) == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(pool->mu);
+        pool->free.push_back({ptr, bytes, stream, ev});
+        while (pool->free.size() > kGridPoolKeep) {  // the oldest goes back to the device pool
+          GridPool::release(pool->free.front(), device);
+          pool->free.erase(pool->free.begin());
+        }
+        return;  // (rec is released after this: its stream-ordered free follows the reset)
+      }
+      cudaGetLastError();
+      cudaEventDestroy(ev);
+    }
+    if (cudaFreeAsync(ptr, stream) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(ptr);
+    }
+  }
+};
+
+// An all-empty grid arena of >= bytes: a recycled one (no fill needed, *fresh
+// = false) of at most twice the size, else a new allocation (*fresh = true:
+// the caller fills it with -1).
+gvox_status grid_arena_take(const std::shared_ptr<GridPool>& pool, size_t bytes, int device,
+                            cudaStream_t stream, std::shared_ptr<GridArena>* out, bool* fresh) {
+  auto a = std::make_shared<GridArena>();
+  a->device = device;
+  a->stream = stream;
+  a->bytes = bytes;
+  *fresh = true;
+  if (!bytes) {
+    *out = a;
+    *fresh = false;
+    return GVOX_OK;
+  }
+  {
+    std::lock_guard<std::mutex> lk(pool->mu);
+    size_t best = pool->free.size();
+    for (size_t i = 0; i < pool->free.size(); ++i) {
+      const size_t b = pool->free[i].bytes;
+      if (b >= bytes && b <= 2 * bytes && (best == pool->free.size() || b < pool->free[best].bytes))
+        best = i;
+    }
+    if (best < pool->free.size()) {
+      const GridPool::Entry e = pool->free[best];
+      pool->free.erase(pool->free.begin() + best);
+      CK(cudaStreamWaitEvent(stream, e.ready, 0));
+      cudaEventDestroy(e.ready);
+      a->ptr = e.ptr;
+      a->bytes = e.bytes;
+      *fresh = false;
+    }
+  }
+  if (*fresh) {
+    cudaError_t e = cudaMallocAsync(&a->ptr, bytes, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (grid arena)");
+  }
+  a->pool = pool;
+  *out = a;
+  return GVOX_OK;
+}
+
 }  // namespace
 
 namespace gvox {
@@ -167,6 +276,12 @@ struct gvox_ctx {
   size_t pin_out_bytes = 0;
   int32_t* pin_counts = nullptr;  // pinned {S, T} of gvox_linearize_batch_accum_select
   uint64_t dense_budget = 16ull << 30;  // bytes of dense index grids per build chunk
+  std::shared_ptr<GridPool> grid_pool = std::make_shared<GridPool>();
+  // pinned staging of the build's two descriptor uploads (pageable copies
+  // would wait for the stream to drain before they start)
+  void* pin_b[2] = {nullptr, nullptr};
+  size_t pin_b_bytes[2] = {0, 0};
+  cudaEvent_t pin_b_done[2] = {nullptr, nullptr};
 };
 
 struct gvox_cloud {
@@ -181,7 +296,7 @@ struct gvox_cloud {
 
 struct gvox_map {
   std::shared_ptr<DevBuf> arena;       // descriptors, hash tables, voxel records, keys
-  std::shared_ptr<DevBuf> grid_arena;  // dense index grids
+  std::shared_ptr<GridArena> grid_arena;  // dense index grids (recycled when the last map goes)
   MapDev desc{};         // host copy
   MapDev* dev = nullptr;
   int levels = 0;
@@ -238,6 +353,31 @@ gvox_status h2d_block(gvox_ctx* ctx, void* dst, const void* pinned_src, size_t b
   CK(cudaMemcpyAsync(dst, pinned_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaEventRecord(ctx->pin_done, ctx->stream));
   ctx->pin_pending = true;
+  return GVOX_OK;
+}
+
+// Pinned staging slot `slot` of the voxelmap build (>= bytes), once the
+// previous upload out of it has completed; pin_b_upload enqueues the H2D and
+// marks the slot busy until it lands.
+gvox_status pin_b_reserve(gvox_ctx* ctx, int slot, size_t bytes, void** out) {
+  if (!ctx->pin_b_done[slot])
+    CK(cudaEventCreateWithFlags(&ctx->pin_b_done[slot], cudaEventDisableTiming));
+  else
+    CK(cudaEventSynchronize(ctx->pin_b_done[slot]));
+  if (ctx->pin_b_bytes[slot] < bytes) {
+    if (ctx->pin_b[slot]) CK(cudaFreeHost(ctx->pin_b[slot]));
+    ctx->pin_b[slot] = nullptr;
+    const size_t nb = align_up(std::max(bytes, ctx->pin_b_bytes[slot] * 3 / 2), 1 << 16);
+    cudaError_t e = cudaHostAlloc(&ctx->pin_b[slot], nb, cudaHostAllocDefault);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
+    ctx->pin_b_bytes[slot] = nb;
+  }
+  *out = ctx->pin_b[slot];
+  return GVOX_OK;
+}
+gvox_status pin_b_upload(gvox_ctx* ctx, int slot, void* dst, size_t bytes) {
+  if (bytes) CK(cudaMemcpyAsync(dst, ctx->pin_b[slot], bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaEventRecord(ctx->pin_b_done[slot], ctx->stream));
   return GVOX_OK;
 }
 
@@ -302,6 +442,7 @@ gvox_status gvox_ctx_create(int device, void* cuda_stream, gvox_ctx** out) {
     if (cudaMemGetInfo(&free_b, &tot_b) == cudaSuccess) c->dense_budget = tot_b / 4;
   }
   c->stream = (cudaStream_t)cuda_stream;
+  c->grid_pool->device = device;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     uint64_t keep = UINT64_MAX;  // freed blocks stay in the pool for reuse
@@ -342,6 +483,11 @@ void gvox_ctx_destroy(gvox_ctx* ctx) {
     if (ctx->ws[i]) cudaFreeAsync(ctx->ws[i], ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->pin) cudaFreeHost(ctx->pin);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->pin_b_done[i]) cudaEventSynchronize(ctx->pin_b_done[i]);
+    if (ctx->pin_b[i]) cudaFreeHost(ctx->pin_b[i]);
+    if (ctx->pin_b_done[i]) cudaEventDestroy(ctx->pin_b_done[i]);
+  }
   if (ctx->pin_out) cudaFreeHost(ctx->pin_out);
   if (ctx->pin_counts) cudaFreeHost(ctx->pin_counts);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
@@ -630,12 +776,15 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   }
   DebugClock dbg;
   dbg.lap("plan");
-  std::shared_ptr<DevBuf> grid_arena;
-  gvox_status st = devbuf_alloc(gl.size, ctx->device, ctx->stream, &grid_arena);
+  std::shared_ptr<GridArena> grid_arena;
+  bool grid_fresh = true;
+  gvox_status st = grid_arena_take(ctx->grid_pool, gl.size, ctx->device, ctx->stream, &grid_arena,
+                                   &grid_fresh);
   dbg.lap("grid alloc");
   if (st) return st;
   char* gb = (char*)grid_arena->ptr;
-  if (gl.size) CK(cudaMemsetAsync(gb, 0xFF, gl.size, ctx->stream));  // every cell -1 (empty)
+  // every cell -1 (empty); a recycled arena already is
+  if (gl.size && grid_fresh) CK(cudaMemsetAsync(gb, 0xFF, gl.size, ctx->stream));
 
   // ---- phase 1 workspace (workspace 0): hash-level temp tables, keys, slots
   std::vector<uint64_t> tcap(count);
@@ -652,7 +801,6 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   size_t o_pslot = lay.add((size_t)total * L * 4);
   size_t o_cnt = lay.add((size_t)count * L * 4 + 4);
   size_t o_bseg = lay.add(sizeof(BuildSeg) * count);
-  size_t o_aseg = lay.add(sizeof(AccumSeg) * count);
   void* ws0 = nullptr;
   st = ws_reserve(ctx, 0, lay.size, &ws0);
   if (st) return st;
@@ -689,8 +837,14 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   }
   if (tmp_bytes) CK(cudaMemsetAsync(b0, 0xFF, tmp_bytes, ctx->stream));
   CK(cudaMemsetAsync(d_cnt, 0, (size_t)count * L * 4 + 4, ctx->stream));
-  CK(cudaMemcpyAsync(b0 + o_bseg, bseg.data(), sizeof(BuildSeg) * count, cudaMemcpyHostToDevice,
-                     ctx->stream));
+  {
+    void* hp = nullptr;
+    st = pin_b_reserve(ctx, 0, sizeof(BuildSeg) * count, &hp);
+    if (st) return st;
+    std::memcpy(hp, bseg.data(), sizeof(BuildSeg) * count);
+    st = pin_b_upload(ctx, 0, b0 + o_bseg, sizeof(BuildSeg) * count);
+    if (st) return st;
+  }
   {
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
     launch_build_insert((const BuildSeg*)(b0 + o_bseg), count, max_pts, L, r0, dyadic,
@@ -710,7 +864,13 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   // ---- record arena (exact sizes): descriptors, hash tables, voxel records, keys
   Layout al;
   int64_t total_vox = 0;
-  const size_t o_descs = al.add(sizeof(MapDev) * count);  // contiguous: one H2D
+  // build metadata first, uploaded as ONE pinned H2D: map descriptors, the
+  // grid-reset table (kept with the maps), accumulate and finalize segments
+  const size_t o_descs = al.add(sizeof(MapDev) * count);
+  const size_t o_reset = al.add(sizeof(ResetSeg) * count * L);
+  const size_t o_aseg = al.add(sizeof(AccumSeg) * count);
+  const size_t o_fseg = al.add(sizeof(FinalSeg) * count * L);
+  const size_t meta_end = al.size;
   const size_t idx_begin = al.size;  // final hash tables: one 0xFF memset
   for (int64_t s = 0; s < count; ++s)
     for (int l = 0; l < L; ++l) {
@@ -737,7 +897,6 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   // ---- phase 2/3 workspace (workspace 1): acc [total_vox][10] + seg tables
   Layout l1;
   size_t o_acc = l1.add((size_t)total_vox * 80);
-  size_t o_fseg = l1.add(sizeof(FinalSeg) * count * L);
   void* ws1 = nullptr;
   st = ws_reserve(ctx, 1, l1.size, &ws1);
   if (st) return st;
@@ -820,29 +979,51 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       vacc += V;
     }
   }
-  CK(cudaMemcpyAsync(b0 + o_aseg, aseg.data(), sizeof(AccumSeg) * count, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  CK(cudaMemcpyAsync(b1 + o_fseg, fseg.data(), sizeof(FinalSeg) * count * L,
-                     cudaMemcpyHostToDevice, ctx->stream));
+  int64_t max_vox = 0;
+  for (int64_t q = 0; q < count * L; ++q) max_vox = std::max<int64_t>(max_vox, hcnt[q]);
+  {
+    // reset table of the dense levels (GridArena: recycling the grids)
+    std::vector<ResetSeg> rseg((size_t)count * L);
+    for (int64_t q = 0; q < count * L; ++q) {
+      const LevelPlan& p = plan[q];
+      ResetSeg& r = rseg[q];
+      std::memset(&r, 0, sizeof(r));
+      if (!p.dense) continue;
+      r.keys = fseg[q].keys_out;
+      r.grid = (int32_t*)(gb + p.o_grid);
+      r.nvox = hcnt[q];
+      r.x0 = p.x0; r.y0 = p.y0; r.z0 = p.z0;
+      r.dy = p.dy; r.dz = p.dz;
+    }
+    void* hp = nullptr;
+    st = pin_b_reserve(ctx, 1, meta_end - o_descs, &hp);
+    if (st) return st;
+    char* h = (char*)hp - o_descs;  // the pinned block mirrors [o_descs, meta_end)
+    std::memcpy(h + o_descs, mdesc.data(), sizeof(MapDev) * count);
+    std::memcpy(h + o_reset, rseg.data(), sizeof(ResetSeg) * count * L);
+    std::memcpy(h + o_aseg, aseg.data(), sizeof(AccumSeg) * count);
+    std::memcpy(h + o_fseg, fseg.data(), sizeof(FinalSeg) * count * L);
+    st = pin_b_upload(ctx, 1, ab + o_descs, meta_end - o_descs);
+    if (st) return st;
+    grid_arena->rec = arena;
+    grid_arena->reset = (const ResetSeg*)(ab + o_reset);
+    grid_arena->nreset = count * L;
+    grid_arena->max_vox = max_vox;
+  }
   {
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
-    launch_build_accum((const BuildSeg*)(b0 + o_bseg), (const AccumSeg*)(b0 + o_aseg), count,
+    launch_build_accum((const BuildSeg*)(b0 + o_bseg), (const AccumSeg*)(ab + o_aseg), count,
                        max_pts, L, r0, dyadic, (const int32_t*)(b0 + o_pslot),
                        (unsigned long long*)(b1 + o_acc), ctx->stream);
   }
   CK_LAUNCH("voxelmap accumulate");
   {
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
-    int64_t max_vox = 0;
-    for (int64_t q = 0; q < count * L; ++q) max_vox = std::max<int64_t>(max_vox, hcnt[q]);
-    launch_build_finalize((const FinalSeg*)(b1 + o_fseg), count * L, max_vox,
+    launch_build_finalize((const FinalSeg*)(ab + o_fseg), count * L, max_vox,
                           (const unsigned long long*)(b1 + o_acc), ctx->stream);
   }
   CK_LAUNCH("voxelmap finalize");
-  // (pageable sources: cudaMemcpyAsync has staged them when it returns; the
-  // stream orders the next chunk's reuse of the workspaces after this one)
-  CK(cudaMemcpyAsync(ab + o_descs, mdesc.data(), sizeof(MapDev) * count, cudaMemcpyHostToDevice,
-                     ctx->stream));
+  // (the stream orders the next chunk's reuse of the workspaces after this one)
   dbg.lap("accum/finalize enqueued");
   for (int64_t s = 0; s < count; ++s) {
     auto* m = new gvox_map;
@@ -1029,9 +1210,10 @@ gvox_status overlap_impl(const char* fn, gvox_ctx* ctx, const gvox_cloud* const*
       return fail(GVOX_ERR_INVALID, "%s: pose %lld is not finite", fn, (long long)i);
   DeviceGuard g(ctx->device);
   int64_t total_pts = 0;
-  bool all_dense = true;
+  bool all_dense = true, all_dyadic = true;
   for (int64_t p = 0; p < num_pairs; ++p) {
     total_pts += clouds[pairs[p].source_cloud]->n;
+    all_dyadic = all_dyadic && maps[pairs[p].target_map]->desc.dyadic;
     all_dense = all_dense && maps[pairs[p].target_map]->desc.lv[level].dense;
   }
   // counts: tiles of 256 * ppt source points, >= ~8 waves of 8 CTAs per SM
@@ -1095,7 +1277,7 @@ gvox_status overlap_impl(const char* fn, gvox_ctx* ctx, const gvox_cloud* const*
     uint8_t* dsel = mem == GVOX_DEVICE ? selected : (uint8_t*)(wb + o_out);
     TimerScope ts(ctx, GVOX_TIMER_OVERLAP);
     launch_overlap_select(dcl, dmp, dpairs, num_pairs, dposes, level, num, den, dsel, all_dense,
-                          ctx->stream);
+                          all_dyadic, ctx->stream);
     dout = dsel;
     out_bytes = num_pairs;
   }

@@ -458,6 +458,18 @@ __global__ void __launch_bounds__(256, GVOX_FIN_MINB) k_build_finalize(const Fin
   }
 }
 
+// One (map, level) per grid row: cell of voxel v back to -1 (empty).
+__global__ void k_grid_reset(const ResetSeg* __restrict__ segs) {
+  const ResetSeg& sg = segs[blockIdx.y];
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= sg.nvox) return;
+  const uint64_t key = sg.keys[v];
+  const int32_t kx = (int32_t)((key >> 42) & 0x1FFFFF) - kKeyHalf;
+  const int32_t ky = (int32_t)((key >> 21) & 0x1FFFFF) - kKeyHalf;
+  const int32_t kz = (int32_t)(key & 0x1FFFFF) - kKeyHalf;
+  sg.grid[((size_t)(kx - sg.x0) * sg.dy + (ky - sg.y0)) * sg.dz + (kz - sg.z0)] = -1;
+}
+
 __global__ void k_fill_u64(uint64_t* p, uint64_t value, int64_t count) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -525,6 +537,14 @@ void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs, int64_t m
   if (num_segs <= 0) return;  // (runs for empty maps too: it writes the sentinel records)
   dim3 grid(grid_for(max_seg_voxels > 0 ? max_seg_voxels : 1, 256), (unsigned)num_segs);
   k_build_finalize<<<grid, 256, 0, stream>>>(segs_dev, acc);
+  note_launch();
+}
+
+void launch_grid_reset(const ResetSeg* segs_dev, int64_t num_segs, int64_t max_seg_voxels,
+                       cudaStream_t stream) {
+  if (num_segs <= 0 || max_seg_voxels <= 0) return;
+  dim3 grid(grid_for(max_seg_voxels, 256), (unsigned)num_segs);
+  k_grid_reset<<<grid, 256, 0, stream>>>(segs_dev);
   note_launch();
 }
 

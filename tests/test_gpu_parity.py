@@ -660,3 +660,39 @@ def test_dense_and_hash_levels_agree(gv, ctx, monkeypatch):
     c1 = gv.overlap(ctx, clouds, dense, sc.pairs, sc.poses, sc.overlap_level)
     c2 = gv.overlap(ctx, clouds, hashed, sc.pairs, sc.poses, sc.overlap_level)
     assert np.array_equal(c1, c2)
+
+
+def test_recycled_grid_arena_is_clean(gv, ctx):
+    """Dense index grids are recycled (gvox_runtime.cu GridArena): when the
+    last map of a build goes, exactly its voxels' cells are reset to -1 and the
+    arena serves the next build without a fill.  A build into a recycled arena
+    -- including one that previously held OTHER clouds -- gives the maps and
+    results of a build into a fresh one (a new context: empty pool)."""
+    import gc
+    sc = synth.global_scene(n_submaps=6, n_points=20000, half_blocks=2, factor_dist=40.0,
+                            cand_dist=60.0)
+    f = sc.factors.copy()
+    f[:, 4] = 0
+    shifted = sc.mu + np.float32(3.3)  # other cells, same sizes -> same arena size class
+    fresh = gv.Context(0)
+    c_ref = [gv.Cloud(fresh, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    m_ref = gv.create_voxelmaps(fresh, [c_ref[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    r_ref = gv.linearize_batch(fresh, c_ref, m_ref, f, sc.poses)
+    o_ref = gv.overlap(fresh, c_ref, m_ref, sc.pairs, sc.poses, sc.overlap_level)
+    k = gv.Context(0)
+    clouds = [gv.Cloud(k, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    other = [gv.Cloud(k, shifted[sc.offsets[c]:sc.offsets[c + 1]], *sc.cloud(c)[1:])
+             for c in range(sc.num_clouds)]
+    for rnd in range(3):
+        tmp = gv.create_voxelmaps(k, [other[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+        del tmp
+        gc.collect()                       # -> reset + parked in the pool
+        maps = gv.create_voxelmaps(k, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+        for a, b in zip(maps, m_ref):
+            for l in range(sc.levels):
+                for x, y in zip(a.export(k, l), b.export(fresh, l)):
+                    assert np.array_equal(x, y)
+        assert gv.linearize_batch(k, clouds, maps, f, sc.poses).tobytes() == r_ref.tobytes()
+        assert np.array_equal(gv.overlap(k, clouds, maps, sc.pairs, sc.poses, sc.overlap_level), o_ref)
+        del maps
+        gc.collect()
