@@ -194,6 +194,11 @@ struct BuildSeg {
   int32_t pad;
   uint64_t* keys_by_idx[GVOX_MAX_LEVELS];  // [n] workspace: key of voxel idx
   int32_t* counter;         // [levels] voxel counts (atomic)
+  // sync-free builds (acc sized by upper bounds before the insert): the
+  // thread that creates voxel idx of level l zeroes its 10 accumulators at
+  // acc + (acc_offset[l] + idx) * 10; nullptr: acc is zero-filled instead
+  unsigned long long* acc;
+  int64_t acc_offset[GVOX_MAX_LEVELS];
   LevelBox box[GVOX_MAX_LEVELS];
   // hash levels: phase 1 records, per (point, level), the temp-table SLOT of its
   // key; phase 2 reads the voxel index from that slot (all assigned by then).
@@ -220,7 +225,7 @@ void launch_build_accum(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int
 // phase 3: per voxel, finalize the record and insert into the final table.
 struct FinalSeg {
   int64_t acc_offset;       // first voxel in acc[] / keys
-  int64_t nvox;
+  const int32_t* nvox;      // device: the level's voxel count (the insert's counter)
   const uint64_t* keys_by_idx;
   double r;
   double mu_scale;
@@ -247,7 +252,7 @@ void launch_fill_u64(uint64_t* p, uint64_t value, int64_t count, cudaStream_t st
 struct ResetSeg {
   const uint64_t* keys;  // the level's packed voxel keys [nvox]
   int32_t* grid;
-  int64_t nvox;
+  const int32_t* nvox;   // device: the level's voxel count (nullptr: not a dense level)
   int32_t x0, y0, z0;
   uint32_t dy, dz;
 };

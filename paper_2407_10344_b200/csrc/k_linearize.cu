@@ -73,7 +73,22 @@ namespace {
 // residual base of level l > 0 from level l - 1's (one select + add per axis, 1)
 // or from the level-0 base and the key's low bits (0)
 #ifndef GVOX_LIN_INCBASE
-#define GVOX_LIN_INCBASE 0
+#define GVOX_LIN_INCBASE 1
+#endif
+// level term: 1/det folded into the level sums' FMAs and into g (1), or Omega
+// formed explicitly first (0)
+#ifndef GVOX_LIN_FUSEOM
+#define GVOX_LIN_FUSEOM 1
+#endif
+// FAST pipeline: a level no lane of the warp hits is skipped as a whole (one
+// vote per level; warp-uniform branch) (1), or evaluated masked (0)
+#ifndef GVOX_LIN_WSKIP
+#define GVOX_LIN_WSKIP 0
+#endif
+// FAST pipeline: the current point's record gathers are issued before the next
+// point's transform and probes (1; they land during prep) or after (0)
+#ifndef GVOX_LIN_EARLYGATHER
+#define GVOX_LIN_EARLYGATHER 0
 #endif
 
 
@@ -380,6 +395,28 @@ __device__ __forceinline__ void level_term(Acc<MAXL>& ac, LevelSum& ls, const Po
   const float id = ok ? rcp_approx(det) : 0.f;
   ac.n_degenerate += hit && !pd_ok;
   ac.inl[l] += ok;
+#if GVOX_LIN_FUSEOM
+  // d = mu~ - q = (centre_l - q) + offset (Q12); (bx, by, bz) = centre_l - q
+  // from level_base
+  const f2_t D = add2(pk(bx, by), pk(v0.x, v0.y));  // (dx, dy)
+  const float dz = bz + v0.z;
+  const float dx = lo(D), dy = hi(D);
+  // g = Omega d = (adj d) / det, e = d^T g; Omega = adj / det enters the level
+  // sums through one FMA per pair
+  const f2_t A01 = pk(i00, i01), A11 = pk(i01, i11), A12 = pk(i02, i12);
+  const f2_t Tp = fma2(A12, bc(dz), fma2(A11, bc(dy), mul2(A01, bc(dx))));
+  const float tz = fmaf(i02, dx, fmaf(i12, dy, i22 * dz));
+  const f2_t Gp = mul2(Tp, bc(id));  // (gx, gy)
+  const float gz = tz * id;
+  ac.E = fma2(D, Gp, ac.E);
+  ac.ez = fmaf(dz, gz, ac.ez);
+  ls.Oa = fma2(A01, bc(id), ls.Oa);
+  ls.Oc = fma2(A12, bc(id), ls.Oc);
+  ls.o11 = fmaf(i11, id, ls.o11);
+  ls.o22 = fmaf(i22, id, ls.o22);
+  ls.G = add2(ls.G, Gp);
+  ls.gz += gz;
+#else
   const f2_t Om_a = mul2(pk(i00, i01), bc(id));  // (o00, o01) = column 0, rows 0-1
   const f2_t Om_b = mul2(pk(i01, i11), bc(id));  // (o01, o11) = column 1, rows 0-1
   const f2_t Om_c = mul2(pk(i02, i12), bc(id));  // (o02, o12) = column 2, rows 0-1
@@ -403,6 +440,7 @@ __device__ __forceinline__ void level_term(Acc<MAXL>& ac, LevelSum& ls, const Po
   ls.o22 += o22;
   ls.G = add2(ls.G, Gp);
   ls.gz += gz;
+#endif
 }
 
 // The target-block terms of one point from its level sums (Eqs.6-8 with
@@ -669,7 +707,31 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       int32_t vid[MAXL];
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) vid[l] = vn[l];
+      // levels some lane of the warp hits (all lanes converged here)
+      uint32_t lany = (1u << MAXL) - 1u;
+      if (GVOX_LIN_WSKIP) {
+        lany = 0u;
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) lany |= (__any_sync(0xffffffffu, vid[l] >= 0) ? 1u : 0u) << l;
+      }
       const bool inv = VALID && inv_n;
+      // every level's record is loaded unconditionally: a level without a
+      // correspondence (index -1) reads the level's all-zero sentinel record
+      // at index -1 (masked out in level_term, exactly as zeros)
+      float4 v0[MAXL], v1[MAXL];
+      float v2[MAXL];
+      auto gather = [&]() {
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) {
+          if (lany >> l & 1u) {
+            const float4* vp = sh.lv[l].vox + 3 * vid[l];
+            v0[l] = __ldg(vp);
+            v1[l] = __ldg(vp + 1);
+            v2[l] = __ldg(&vp[2].x);
+          }
+        }
+      };
+      if (GVOX_LIN_EARLYGATHER) gather();
       prep(i_nxt, st);
       i_cur = i_nxt;
       i_nxt = i_nx2;
@@ -682,18 +744,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) any |= vid[l] >= 0;
       if (!any) continue;  // (also every lane without a point: prep left its indices -1)
-      // every level's record is loaded unconditionally: a level without a
-      // correspondence (index -1) reads the level's all-zero sentinel record
-      // at index -1 (masked out in level_term, exactly as zeros)
-      float4 v0[MAXL], v1[MAXL];
-      float v2[MAXL];
-#pragma unroll
-      for (int l = 0; l < MAXL; ++l) {
-        const float4* vp = sh.lv[l].vox + 3 * vid[l];
-        v0[l] = __ldg(vp);
-        v1[l] = __ldg(vp + 1);
-        v2[l] = __ldg(&vp[2].x);
-      }
+      if (!GVOX_LIN_EARLYGATHER) gather();
       const float4 a = sbuf[warp][cur][0][lane], b = sbuf[warp][cur][1][lane],
                    c = sbuf[warp][cur][2][lane];
       rcr(sh.Rf, a, b, c, pd);
@@ -704,7 +755,8 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) {
         level_base(pd, l, r0f, bx, by, bz);
-        level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, bx, by, bz, vid[l] >= 0);
+        if (lany >> l & 1u)
+          level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, bx, by, bz, vid[l] >= 0);
       }
       if (!error_only) fold_point<MAXL>(ac, ls, pd);
     }

@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
 //                                        reached, could at most hit),
 // so every decision is the one the exact count gives, and no warp waits at a
 // barrier for the others.  A decided CTA's warps stop at their next check.
-template <bool ALL_DENSE>
+template <bool ALL_DENSE, bool DYADIC>
 __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
     k_overlap_select_nb(const CloudDev* const* __restrict__ clouds,
                         const MapDev* const* __restrict__ maps, const PairDev* __restrict__ pairs,
@@ -362,17 +362,20 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
       pts -= 32u - tail_pts;
     return pts;
   };
-  auto probe = [&](int64_t m) -> int {
-    const int64_t k = m * kThreads + 32 * warp + lane;
-    if (k >= n) return 0;
-    const float4 a = __ldg(A + pt_off(k));
+  // point m * kThreads + 32 warp + lane (sub-step m's chunk of this warp) exists
+  // iff m < m_lim; its record sits a fixed stride from the lane's first one
+  const int32_t m_lim = (int32_t)((n - 32 * warp - lane + kThreads - 1) / kThreads);
+  const float4* __restrict__ A_lane = A + (warp * 96 + lane);
+  auto probe = [&](int32_t m) -> int {
+    if (m >= m_lim) return 0;
+    const float4 a = __ldg(A_lane + m * (kThreads / 32 * 96));
     const double mx = a.x, my = a.y, mz = a.z;
     const double qx = __fma_rn(R[0], mx, __fma_rn(R[1], my, __fma_rn(R[2], mz, t[0])));
     const double qy = __fma_rn(R[3], mx, __fma_rn(R[4], my, __fma_rn(R[5], mz, t[1])));
     const double qz = __fma_rn(R[6], mx, __fma_rn(R[7], my, __fma_rn(R[8], mz, t[2])));
-    const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, dyadic);
-    const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, dyadic);
-    const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, dyadic);
+    const int32_t kx = voxel_coord0(qx, lv.r, lv.inv_r, DYADIC);
+    const int32_t ky = voxel_coord0(qy, lv.r, lv.inv_r, DYADIC);
+    const int32_t kz = voxel_coord0(qz, lv.r, lv.inv_r, DYADIC);
     return lookup_level<ALL_DENSE>(lv, kx, ky, kz) >= 0;
   };
   // publish (h, pts); true once the CTA's decision is certain
@@ -469,15 +472,13 @@ namespace gvox {
 void launch_overlap_select(const CloudDev* const* clouds, const MapDev* const* maps,
                            const PairDev* pairs, int64_t num_pairs, const double* poses, int level,
                            int32_t num, int32_t den, uint8_t* selected, bool all_dense,
-                           cudaStream_t stream) {
+                           bool all_dyadic, cudaStream_t stream) {
   if (num_pairs <= 0) return;
   if (GVOX_OVL_NOBAR) {
-    if (all_dense)
-      k_overlap_select_nb<true><<<(unsigned)num_pairs, kThreads, 0, stream>>>(
-          clouds, maps, pairs, poses, level, num, den, selected);
-    else
-      k_overlap_select_nb<false><<<(unsigned)num_pairs, kThreads, 0, stream>>>(
-          clouds, maps, pairs, poses, level, num, den, selected);
+    auto* k = all_dense ? (all_dyadic ? k_overlap_select_nb<true, true> : k_overlap_select_nb<true, false>)
+                        : (all_dyadic ? k_overlap_select_nb<false, true> : k_overlap_select_nb<false, false>);
+    k<<<(unsigned)num_pairs, kThreads, 0, stream>>>(clouds, maps, pairs, poses, level, num, den,
+                                                    selected);
   } else if (all_dense)
     k_overlap_select<true><<<(unsigned)num_pairs, kThreads, 0, stream>>>(
         clouds, maps, pairs, poses, level, num, den, selected);
