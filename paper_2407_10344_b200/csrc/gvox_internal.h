@@ -375,6 +375,10 @@ void launch_pcg_iteration(const double* blocks, const int32_t* row_start, const 
                           int64_t num_vars, const double* minv, double* x, double* r, double* z,
                           double* p, double* q, double* pq_part, PcgState* st, int32_t max_iter,
                           double tol, cudaGraphConditionalHandle cond, cudaStream_t stream);
+bool launch_pcg_cluster(const double* blocks, const int32_t* row_start, const int32_t* col,
+                        int64_t num_vars, int64_t num_blocks, const double* minv, const double* rhs,
+                        double* x, double* r, double* z, double* p, double* q, PcgState* st,
+                        int32_t max_iter, double tol, cudaStream_t stream);
 void launch_pcg_persistent(const double* blocks, const int32_t* row_start, const int32_t* col,
                            int64_t num_vars, const double* minv, const double* rhs, double* x,
                            double* r, double* z, double* p, double* q, double* part_a,

@@ -259,11 +259,19 @@ struct gvox_ctx {
   // grow-only device workspaces
   void* ws[3] = {nullptr, nullptr, nullptr};
   size_t ws_bytes[3] = {0, 0, 0};
-  // pinned host staging for the single H2D input block
-  void* pin = nullptr;
-  size_t pin_bytes = 0;
-  cudaEvent_t pin_done = nullptr;  // last H2D out of `pin` has completed
-  bool pin_pending = false;
+  // pinned host staging of the calls' single H2D input blocks: a ring of
+  // slots, so a call only waits when the copy out of the slot it reuses (four
+  // calls back) has not landed -- consecutive calls do not serialise the host
+  // with the stream
+  static constexpr int kPinSlots = 4;
+  struct PinSlot {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t done = nullptr;  // the last H2D out of this slot has completed
+    bool pending = false;
+  };
+  PinSlot pin_ring[kPinSlots];
+  int pin_slot = 0;
   // optional device-side kernel timing (gvox_ctx_enable_timing)
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -301,7 +309,11 @@ struct gvox_map {
   MapDev* dev = nullptr;
   int levels = 0;
   double r0 = 0;
-  int64_t nvox[GVOX_MAX_LEVELS] = {};
+  // voxel counts per level: known on the host after a counted build; a
+  // sync-free build leaves them on the device (counts_dev) until first asked
+  mutable int64_t nvox[GVOX_MAX_LEVELS] = {};
+  mutable bool counts_known = true;
+  const int32_t* counts_dev = nullptr;
   const uint64_t* keys[GVOX_MAX_LEVELS] = {};
   int device = 0;
 };
@@ -332,27 +344,33 @@ gvox_status ws_reserve(gvox_ctx* ctx, int which, size_t bytes, void** out) {
 // Pinned staging for the single H2D block; waits for the previous H2D out of
 // it to finish before handing it out again.
 gvox_status pin_reserve(gvox_ctx* ctx, size_t bytes, void** out) {
-  if (ctx->pin_pending) {
-    CK(cudaEventSynchronize(ctx->pin_done));
-    ctx->pin_pending = false;
+  const int k = (ctx->pin_slot + 1) % gvox_ctx::kPinSlots;
+  gvox_ctx::PinSlot& sl = ctx->pin_ring[k];
+  if (!sl.done) CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+  if (sl.pending) {
+    CK(cudaEventSynchronize(sl.done));
+    sl.pending = false;
   }
-  if (ctx->pin_bytes < bytes) {
-    if (ctx->pin) CK(cudaFreeHost(ctx->pin));
-    ctx->pin = nullptr;
-    size_t nb = align_up(std::max(bytes, ctx->pin_bytes * 3 / 2), 1 << 16);
-    cudaError_t e = cudaHostAlloc(&ctx->pin, nb, cudaHostAllocDefault);
+  if (sl.bytes < bytes) {
+    if (sl.ptr) CK(cudaFreeHost(sl.ptr));
+    sl.ptr = nullptr;
+    size_t nb = align_up(std::max(bytes, sl.bytes * 3 / 2), 1 << 16);
+    cudaError_t e = cudaHostAlloc(&sl.ptr, nb, cudaHostAllocDefault);
     if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
-    ctx->pin_bytes = nb;
+    sl.bytes = nb;
   }
-  *out = ctx->pin;
+  ctx->pin_slot = k;
+  *out = sl.ptr;
   return GVOX_OK;
 }
 
+// H2D out of the slot pin_reserve handed out last
 gvox_status h2d_block(gvox_ctx* ctx, void* dst, const void* pinned_src, size_t bytes) {
   if (bytes == 0) return GVOX_OK;
+  gvox_ctx::PinSlot& sl = ctx->pin_ring[ctx->pin_slot];
   CK(cudaMemcpyAsync(dst, pinned_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaEventRecord(ctx->pin_done, ctx->stream));
-  ctx->pin_pending = true;
+  CK(cudaEventRecord(sl.done, ctx->stream));
+  sl.pending = true;
   return GVOX_OK;
 }
 
@@ -448,10 +466,12 @@ gvox_status gvox_ctx_create(int device, void* cuda_stream, gvox_ctx** out) {
     uint64_t keep = UINT64_MAX;  // freed blocks stay in the pool for reuse
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
-  e = cudaEventCreateWithFlags(&c->pin_done, cudaEventDisableTiming);
-  if (e != cudaSuccess) {
-    delete c;
-    return cuda_fail(e, "cudaEventCreate");
+  for (auto& sl : c->pin_ring) {
+    e = cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      delete c;
+      return cuda_fail(e, "cudaEventCreate");
+    }
   }
   *out = c;
   return GVOX_OK;
@@ -482,7 +502,10 @@ void gvox_ctx_destroy(gvox_ctx* ctx) {
   for (int i = 0; i < 3; ++i)
     if (ctx->ws[i]) cudaFreeAsync(ctx->ws[i], ctx->stream);
   cudaStreamSynchronize(ctx->stream);
-  if (ctx->pin) cudaFreeHost(ctx->pin);
+  for (auto& sl : ctx->pin_ring) {
+    if (sl.ptr) cudaFreeHost(sl.ptr);
+    if (sl.done) cudaEventDestroy(sl.done);
+  }
   for (int i = 0; i < 2; ++i) {
     if (ctx->pin_b_done[i]) cudaEventSynchronize(ctx->pin_b_done[i]);
     if (ctx->pin_b[i]) cudaFreeHost(ctx->pin_b[i]);
@@ -491,7 +514,6 @@ void gvox_ctx_destroy(gvox_ctx* ctx) {
   if (ctx->pin_out) cudaFreeHost(ctx->pin_out);
   if (ctx->pin_counts) cudaFreeHost(ctx->pin_counts);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
-  if (ctx->pin_done) cudaEventDestroy(ctx->pin_done);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (int t = 0; t < GVOX_TIMER_COUNT; ++t)
     for (auto& pr : ctx->ev_open[t]) {
@@ -681,6 +703,7 @@ void gvox_cloud_destroy(gvox_cloud* cloud) { delete cloud; }
 namespace {
 
 constexpr int64_t kBuildChunkPoints = 256 << 20;
+constexpr int64_t kNoSyncBuildPoints = 4 << 20;  // chunks up to this many points build sync-free
 
 gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t count, double r0,
                         int levels, gvox_map** maps_out) {
@@ -786,6 +809,28 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   // every cell -1 (empty); a recycled arena already is
   if (gl.size && grid_fresh) CK(cudaMemsetAsync(gb, 0xFF, gl.size, ctx->stream));
 
+  // ---- sync-free or counted.  A small chunk (odometry frames, keyframe maps:
+  // <= kNoSyncBuildPoints points) sizes every buffer by the bound "at most one
+  // voxel per point and level" before the insert, so the host never waits for
+  // the GPU: the accumulators are zeroed by the insert as voxels are created,
+  // finalize and the grid reset read the counts on the device, and the range
+  // error is decided from the clouds' bounding boxes on the host (the level-0
+  // keys are the widest; floor is monotone, so the box corners decide it
+  // exactly).  A large chunk reads the counts back once and sizes exactly.
+  bool nosync = total <= kNoSyncBuildPoints;
+  if (const char* e = std::getenv("GVOX_BUILD_NOSYNC")) nosync = std::atoi(e) != 0;
+  for (int64_t s = 0; s < count; ++s) {
+    const gvox_cloud* c = clouds[s];
+    if (c->n <= 0) continue;
+    for (int a = 0; a < 3; ++a) {
+      const double slo = dyadic ? (double)c->lo[a] * (1.0 / r0) : (double)c->lo[a] / r0;
+      const double shi = dyadic ? (double)c->hi[a] * (1.0 / r0) : (double)c->hi[a] / r0;
+      if (std::floor(slo) < -1048576.0 || std::floor(shi) >= 1048576.0)
+        return fail(GVOX_ERR_RANGE,
+                    "gvox_create_voxelmap: a voxel key is outside [-2^20, 2^20) (r0 = %g)", r0);
+    }
+  }
+
   // ---- phase 1 workspace (workspace 0): hash-level temp tables, keys, slots
   std::vector<uint64_t> tcap(count);
   Layout lay;
@@ -837,53 +882,65 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   }
   if (tmp_bytes) CK(cudaMemsetAsync(b0, 0xFF, tmp_bytes, ctx->stream));
   CK(cudaMemsetAsync(d_cnt, 0, (size_t)count * L * 4 + 4, ctx->stream));
-  {
+
+  // voxel capacity of every (map, level): the point count (sync-free) or the
+  // exact count (counted, after the readback)
+  std::vector<int64_t> vcap((size_t)count * L);
+  std::vector<int32_t> hcnt((size_t)count * L + 1, 0);
+  auto launch_insert = [&]() -> gvox_status {
     void* hp = nullptr;
-    st = pin_b_reserve(ctx, 0, sizeof(BuildSeg) * count, &hp);
-    if (st) return st;
+    gvox_status st2 = pin_b_reserve(ctx, 0, sizeof(BuildSeg) * count, &hp);
+    if (st2) return st2;
     std::memcpy(hp, bseg.data(), sizeof(BuildSeg) * count);
-    st = pin_b_upload(ctx, 0, b0 + o_bseg, sizeof(BuildSeg) * count);
-    if (st) return st;
-  }
-  {
+    st2 = pin_b_upload(ctx, 0, b0 + o_bseg, sizeof(BuildSeg) * count);
+    if (st2) return st2;
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
     launch_build_insert((const BuildSeg*)(b0 + o_bseg), count, max_pts, L, r0, dyadic,
                         (int32_t*)(b0 + o_pslot), d_err, ctx->stream);
+    CK_LAUNCH("voxelmap insert");
+    return GVOX_OK;
+  };
+  if (nosync) {
+    for (int64_t s = 0; s < count; ++s)
+      for (int l = 0; l < L; ++l) vcap[s * L + l] = clouds[s]->n;
+  } else {
+    st = launch_insert();
+    if (st) return st;
+    CK(cudaMemcpyAsync(hcnt.data(), d_cnt, ((size_t)count * L + 1) * 4, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    dbg.lap("insert enqueued");
+    CK(cudaStreamSynchronize(ctx->stream));
+    dbg.lap("insert sync");
+    if (hcnt[(size_t)count * L])
+      return fail(GVOX_ERR_RANGE,
+                  "gvox_create_voxelmap: a voxel key is outside [-2^20, 2^20) (r0 = %g)", r0);
+    for (int64_t q = 0; q < count * L; ++q) vcap[q] = hcnt[q];
   }
-  CK_LAUNCH("voxelmap insert");
-  std::vector<int32_t> hcnt((size_t)count * L + 1);
-  CK(cudaMemcpyAsync(hcnt.data(), d_cnt, ((size_t)count * L + 1) * 4, cudaMemcpyDeviceToHost,
-                     ctx->stream));
-  dbg.lap("insert enqueued");
-  CK(cudaStreamSynchronize(ctx->stream));
-  dbg.lap("insert sync");
-  if (hcnt[(size_t)count * L])
-    return fail(GVOX_ERR_RANGE,
-                "gvox_create_voxelmap: a voxel key is outside [-2^20, 2^20) (r0 = %g)", r0);
 
-  // ---- record arena (exact sizes): descriptors, hash tables, voxel records, keys
+  // ---- record arena: build metadata (uploaded as ONE pinned H2D: map
+  // descriptors, grid-reset table, accumulate / finalize segments, voxel
+  // counts), hash tables, voxel records, keys
   Layout al;
   int64_t total_vox = 0;
-  // build metadata first, uploaded as ONE pinned H2D: map descriptors, the
-  // grid-reset table (kept with the maps), accumulate and finalize segments
   const size_t o_descs = al.add(sizeof(MapDev) * count);
   const size_t o_reset = al.add(sizeof(ResetSeg) * count * L);
   const size_t o_aseg = al.add(sizeof(AccumSeg) * count);
   const size_t o_fseg = al.add(sizeof(FinalSeg) * count * L);
+  const size_t o_counts = al.add((size_t)count * L * 4);  // the maps' voxel counts
   const size_t meta_end = al.size;
   const size_t idx_begin = al.size;  // final hash tables: one 0xFF memset
   for (int64_t s = 0; s < count; ++s)
     for (int l = 0; l < L; ++l) {
       LevelPlan& p = plan[s * L + l];
       if (!p.dense) {
-        p.cap = pow2_at_least(std::max<uint64_t>(2, 2 * (uint64_t)hcnt[s * L + l]));
+        p.cap = pow2_at_least(std::max<uint64_t>(2, 2 * (uint64_t)vcap[s * L + l]));
         p.o_slots = al.add(p.cap * 16);
       }
     }
   const size_t idx_end = al.size;
   for (int64_t s = 0; s < count; ++s)
     for (int l = 0; l < L; ++l) {
-      const int64_t V = hcnt[s * L + l];
+      const int64_t V = vcap[s * L + l];
       LevelPlan& p = plan[s * L + l];
       p.o_vox = al.add((size_t)(V + 1) * 48);  // + the all-zero sentinel record at index -1
       p.o_keys = al.add((size_t)V * 8);
@@ -894,7 +951,8 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   if (st) return st;
   dbg.lap("record alloc");
   char* ab = (char*)arena->ptr;
-  // ---- phase 2/3 workspace (workspace 1): acc [total_vox][10] + seg tables
+  const int32_t* d_counts = (const int32_t*)(ab + o_counts);
+  // ---- phase 2/3 workspace (workspace 1): acc [total_vox][10]
   Layout l1;
   size_t o_acc = l1.add((size_t)total_vox * 80);
   void* ws1 = nullptr;
@@ -902,7 +960,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   if (st) return st;
   dbg.lap("ws1");
   char* b1 = (char*)ws1;
-  CK(cudaMemsetAsync(b1 + o_acc, 0, (size_t)total_vox * 80, ctx->stream));
+  if (!nosync) CK(cudaMemsetAsync(b1 + o_acc, 0, (size_t)total_vox * 80, ctx->stream));
   if (idx_end > idx_begin) CK(cudaMemsetAsync(ab + idx_begin, 0xFF, idx_end - idx_begin, ctx->stream));
 
   std::vector<AccumSeg> aseg(count);
@@ -943,15 +1001,19 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       md.box_lo[3] = md.box_hi[3] = 0.f;
     }
     for (int l = 0; l < L; ++l) {
-      const int64_t V = hcnt[s * L + l];
+      const int64_t V = vcap[s * L + l];
       const double r = std::ldexp(r0, l);
       const LevelPlan& p = plan[s * L + l];
       a.acc_offset[l] = vacc;
       a.mu_scale[l] = std::ldexp(1.0, F) / r;
+      if (nosync) {
+        bseg[s].acc = (unsigned long long*)(b1 + o_acc);
+        bseg[s].acc_offset[l] = vacc;
+      }
       FinalSeg& f = fseg[s * L + l];
       std::memset(&f, 0, sizeof(f));
       f.acc_offset = vacc;
-      f.nvox = V;
+      f.nvox = d_counts + s * L + l;
       f.keys_by_idx = bseg[s].keys_by_idx[l];
       f.r = r;
       f.mu_scale = a.mu_scale[l];
@@ -975,12 +1037,12 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       lv.syz = p.dy * p.dz;
       lv.r = r;
       lv.inv_r = 1.0 / r;
-      lv.nvox = V;
+      lv.nvox = nosync ? -1 : V;  // (host-side information only; -1: on the device)
       vacc += V;
     }
   }
   int64_t max_vox = 0;
-  for (int64_t q = 0; q < count * L; ++q) max_vox = std::max<int64_t>(max_vox, hcnt[q]);
+  for (int64_t q = 0; q < count * L; ++q) max_vox = std::max<int64_t>(max_vox, vcap[q]);
   {
     // reset table of the dense levels (GridArena: recycling the grids)
     std::vector<ResetSeg> rseg((size_t)count * L);
@@ -991,7 +1053,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       if (!p.dense) continue;
       r.keys = fseg[q].keys_out;
       r.grid = (int32_t*)(gb + p.o_grid);
-      r.nvox = hcnt[q];
+      r.nvox = d_counts + q;
       r.x0 = p.x0; r.y0 = p.y0; r.z0 = p.z0;
       r.dy = p.dy; r.dz = p.dz;
     }
@@ -1003,12 +1065,21 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     std::memcpy(h + o_reset, rseg.data(), sizeof(ResetSeg) * count * L);
     std::memcpy(h + o_aseg, aseg.data(), sizeof(AccumSeg) * count);
     std::memcpy(h + o_fseg, fseg.data(), sizeof(FinalSeg) * count * L);
+    std::memcpy(h + o_counts, hcnt.data(), (size_t)count * L * 4);  // counted: the exact counts
     st = pin_b_upload(ctx, 1, ab + o_descs, meta_end - o_descs);
     if (st) return st;
     grid_arena->rec = arena;
     grid_arena->reset = (const ResetSeg*)(ab + o_reset);
     grid_arena->nreset = count * L;
     grid_arena->max_vox = max_vox;
+  }
+  if (nosync) {
+    st = launch_insert();  // (its zeroing of the accumulators needs bseg's acc fields)
+    if (st) return st;
+    // the maps' counts: the insert's counters, copied into the record arena
+    CK(cudaMemcpyAsync(ab + o_counts, d_cnt, (size_t)count * L * 4, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    dbg.lap("insert enqueued (sync-free)");
   }
   {
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
@@ -1034,8 +1105,10 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     m->levels = L;
     m->r0 = r0;
     m->device = ctx->device;
+    m->counts_dev = d_counts + s * L;
+    m->counts_known = !nosync;
     for (int l = 0; l < L; ++l) {
-      m->nvox[l] = hcnt[s * L + l];
+      m->nvox[l] = nosync ? -1 : hcnt[s * L + l];
       m->keys[l] = fseg[s * L + l].keys_out;
     }
     maps_out[s] = m;
@@ -1086,12 +1159,29 @@ gvox_status gvox_create_voxelmap(gvox_ctx* ctx, const gvox_cloud* cloud, double 
   return gvox_create_voxelmaps(ctx, &cloud, 1, r0, levels, out);
 }
 
+// The voxel counts of a sync-free build live on the device until first asked.
+gvox_status resolve_counts(const gvox_map* map) {
+  if (map->counts_known) return GVOX_OK;
+  DeviceGuard g(map->device);
+  int32_t c[GVOX_MAX_LEVELS] = {};
+  const cudaStream_t st = map->arena->stream;  // the building stream: after the build
+  CK(cudaMemcpyAsync(c, map->counts_dev, 4 * map->levels, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int l = 0; l < map->levels; ++l) map->nvox[l] = c[l];
+  map->counts_known = true;
+  return GVOX_OK;
+}
+
 gvox_status gvox_voxelmap_info(const gvox_map* map, int level, int64_t* num_voxels,
                                double* resolution) {
   if (!map) return fail(GVOX_ERR_INVALID, "gvox_voxelmap_info: map is NULL");
   if (level < 0 || level >= map->levels)
     return fail(GVOX_ERR_INVALID, "gvox_voxelmap_info: level %d outside [0, %d)", level, map->levels);
-  if (num_voxels) *num_voxels = map->nvox[level];
+  if (num_voxels) {
+    gvox_status st = resolve_counts(map);
+    if (st) return st;
+    *num_voxels = map->nvox[level];
+  }
   if (resolution) *resolution = std::ldexp(map->r0, level);
   return GVOX_OK;
 }
@@ -1104,6 +1194,8 @@ gvox_status gvox_voxelmap_export(gvox_ctx* ctx, const gvox_map* map, int level, 
   if (level < 0 || level >= map->levels)
     return fail(GVOX_ERR_INVALID, "gvox_voxelmap_export: level %d outside [0, %d)", level, map->levels);
   DeviceGuard g(ctx->device);
+  gvox_status st0 = resolve_counts(map);
+  if (st0) return st0;
   const int64_t V = map->nvox[level];
   std::vector<uint64_t> k(V);
   std::vector<float4> v(3 * V);
@@ -1746,7 +1838,7 @@ gvox_status gvox_knn(gvox_ctx* ctx, const float* points, const int64_t* offsets,
     CK_LAUNCH(fn);
     CK(cudaMemcpyAsync(hb, w1 + o_box, 4 * (6 * count + 1), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    ctx->pin_pending = false;
+    ctx->pin_ring[ctx->pin_slot].pending = false;
     if (hb[6 * count]) return fail(GVOX_ERR_INVALID, "%s: non-finite point coordinate", fn);
     if (std::getenv("GVOX_DEBUG_KNN"))
       for (int64_t c = 0; c < count; ++c)
@@ -2443,7 +2535,15 @@ gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t
                     V, (double*)(wb + o_rhs), (const int32_t*)(din + o_dg), (double*)(wb + o_minv),
                     dbad, ctx->stream);
     CK_LAUNCH("global assemble");
-    if (V > 0 && std::getenv("GVOX_PCG_GRAPH") == nullptr) {
+    if (V > 0 && std::getenv("GVOX_PCG_GRAPH") == nullptr &&
+        launch_pcg_cluster((const double*)(wb + o_blk), (const int32_t*)(din + o_rs),
+                           (const int32_t*)(din + o_col), V, NB, (const double*)(wb + o_minv),
+                           (const double*)(wb + o_rhs), (double*)(wb + o_x), (double*)(wb + o_r),
+                           (double*)(wb + o_z), (double*)(wb + o_p), (double*)(wb + o_q), dst,
+                           P.max_iterations, P.tol, ctx->stream)) {
+      // (the whole PCG on one thread-block cluster: hardware cluster barriers)
+      CK_LAUNCH("PCG (cluster)");
+    } else if (V > 0 && std::getenv("GVOX_PCG_GRAPH") == nullptr) {
       // one cooperative persistent kernel runs the whole PCG (grid barriers)
       launch_pcg_persistent((const double*)(wb + o_blk), (const int32_t*)(din + o_rs),
                             (const int32_t*)(din + o_col), V, (const double*)(wb + o_minv),

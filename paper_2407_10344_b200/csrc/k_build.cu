@@ -251,6 +251,11 @@ __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const Build
         else
           sg.tmp_slots[l][h_out[l]].y = (unsigned long long)(uint32_t)idx | 0xFFFFFFFF00000000ull;
         sg.keys_by_idx[l][idx] = key[l];
+        if (sg.acc) {  // sync-free build: this voxel's accumulators start at zero
+          ulonglong2* a = reinterpret_cast<ulonglong2*>(sg.acc + (sg.acc_offset[l] + idx) * 10);
+#pragma unroll
+          for (int j = 0; j < 5; ++j) a[j] = make_ulonglong2(0ull, 0ull);
+        }
       }
     }
     const int32_t hl = __shfl_sync(0xffffffffu, h_out[l], leader[l]);
@@ -424,7 +429,7 @@ __global__ void __launch_bounds__(256, GVOX_FIN_MINB) k_build_finalize(const Fin
   // record -1 of every level: all zeros, the record a lookup miss (index -1)
   // gathers in the linearize kernel's unconditional loads
   if (v < 3) sg.vox[v - 3] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (v >= sg.nvox) return;
+  if (v >= *sg.nvox) return;
   const unsigned long long* src = acc + (sg.acc_offset + v) * 10;
   double cnt = (double)(long long)src[9];
   double inv = 1.0 / cnt;
@@ -462,7 +467,7 @@ __global__ void __launch_bounds__(256, GVOX_FIN_MINB) k_build_finalize(const Fin
 __global__ void k_grid_reset(const ResetSeg* __restrict__ segs) {
   const ResetSeg& sg = segs[blockIdx.y];
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= sg.nvox) return;
+  if (!sg.nvox || v >= *sg.nvox) return;
   const uint64_t key = sg.keys[v];
   const int32_t kx = (int32_t)((key >> 42) & 0x1FFFFF) - kKeyHalf;
   const int32_t ky = (int32_t)((key >> 21) & 0x1FFFFF) - kKeyHalf;

@@ -696,3 +696,34 @@ def test_recycled_grid_arena_is_clean(gv, ctx):
         assert np.array_equal(gv.overlap(k, clouds, maps, sc.pairs, sc.poses, sc.overlap_level), o_ref)
         del maps
         gc.collect()
+
+
+@pytest.mark.parametrize("hash_levels", [False, True])
+def test_sync_free_build_equals_counted(gv, ctx, monkeypatch, hash_levels):
+    """Small chunks build sync-free (buffers sized by one voxel per point and
+    level, accumulators zeroed by the insert, counts left on the device until
+    asked); the counted build (one count readback, exact sizes) gives the same
+    maps and bitwise the same linearization, with dense grids and with hash
+    levels; the range error is raised by the host box test either way."""
+    sc = synth.make("C2")
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    if hash_levels:
+        monkeypatch.setenv("GVOX_DENSE_BUDGET_MB", "0")
+    monkeypatch.setenv("GVOX_BUILD_NOSYNC", "1")
+    fast = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    monkeypatch.setenv("GVOX_BUILD_NOSYNC", "0")
+    counted = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    monkeypatch.delenv("GVOX_BUILD_NOSYNC")
+    for a, b in zip(fast, counted):
+        for l in range(sc.levels):
+            assert a.num_voxels(l) == b.num_voxels(l) > 0
+            for x, y in zip(a.export(ctx, l), b.export(ctx, l)):
+                assert np.array_equal(x, y)
+    r1 = gv.linearize_batch(ctx, clouds, fast, sc.factors, sc.poses)
+    r2 = gv.linearize_batch(ctx, clouds, counted, sc.factors, sc.poses)
+    assert r1.tobytes() == r2.tobytes()
+    far = gv.Cloud(ctx, np.array([[0, 0, 0], [2.5e6, 0, 0]], np.float32), np.ones((2, 6), np.float32))
+    for flag in ("0", "1"):
+        monkeypatch.setenv("GVOX_BUILD_NOSYNC", flag)
+        with pytest.raises(gv.GvoxError, match="GVOX_ERR_RANGE"):
+            gv.create_voxelmap(ctx, far, 1.0, 1)
