@@ -13,6 +13,7 @@
 // with a pinned, unfused operation order (R26), so the k-set and its order
 // are exactly the oracle's.
 #include <cstdint>
+#include <cstdlib>
 
 #include "k_common.cuh"
 
@@ -215,6 +216,188 @@ __global__ void __launch_bounds__(kKnnThreads)
 #pragma unroll
     for (int j = 0; j < MAXK; ++j)
       if (j < k) row[j] = bi[j] == INT32_MAX ? -1 : bi[j];
+  }
+}
+
+// Exact k-NN with G lanes per query (k <= MAXK): the same ring search and
+// pinned distances as k_knn_query, but each ring's candidate points are split
+// over the query's G lanes (lane g takes points g, g + G, ... of every cell
+// run), each lane keeping its own sorted (d2, index) list.  At the end of a
+// ring the group merges the lists -- k rounds of a group-wide minimum over the
+// lanes' heads, the winner popping its head -- into lane 0 (the other lanes
+// restart empty, so no point is counted twice), and every lane keeps the merged
+// k-th entry, the bound the next ring prunes and stops with.  A point set and
+// its order are unique under (d2, index), so the result is exactly
+// k_knn_query's (and the oracle's); only the in-ring column pruning uses the
+// previous ring's bound.  G x more threads per frame: the search of one
+// odometry frame no longer leaves the GPU nearly empty.
+template <int MAXK, int G>
+__global__ void __launch_bounds__(kKnnThreads)
+    k_knn_query_g(const KnnCloudDev* __restrict__ clouds, const int32_t* __restrict__ tile_start,
+                  const int32_t* __restrict__ tile_cloud, int tile_pts, const float4* __restrict__ sorted,
+                  const int32_t* __restrict__ cell_start, int k, int32_t* __restrict__ out) {
+  static_assert(G == 2 || G == 4 || G == 8 || G == 16 || G == 32, "G: a power of two <= 32");
+  // G CTAs per tile of the plan (one query per thread of a 64-thread CTA):
+  // CTA part p of tile T takes the tile's queries [p, p + 1) * tile_pts / G
+  const int64_t tile = blockIdx.x / G;
+  const int part = (int)(blockIdx.x % G);
+  const int32_t c = __ldg(tile_cloud + tile);
+  const KnnCloudDev cd = clouds[c];
+  const int per = tile_pts / G;
+  const int64_t t0 = cd.first + (int64_t)(tile - __ldg(tile_start + c)) * tile_pts + (int64_t)part * per;
+  const int lane = threadIdx.x & 31, sub = lane & (G - 1);
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane & ~(G - 1));
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const int64_t tend = min(cd.first + cd.n, t0 + (int64_t)per);
+  // (the G lanes of a query run the same iterations: the group stays converged
+  // at every merge)
+  for (int64_t t = t0 + threadIdx.x / G; t < tend; t += blockDim.x / G) {
+    const float4 q = sorted[t];
+    const int32_t qi = __float_as_int(q.w);
+    const int32_t cx = cell_coord(q.x, cd.lo[0], cd.inv_s, cd.dim[0]);
+    const int32_t cy = cell_coord(q.y, cd.lo[1], cd.inv_s, cd.dim[1]);
+    const int32_t cz = cell_coord(q.z, cd.lo[2], cd.inv_s, cd.dim[2]);
+    double bd[MAXK];
+    int32_t bi[MAXK];
+#pragma unroll
+    for (int j = 0; j < MAXK; ++j) {
+      bd[j] = kInf;
+      bi[j] = INT32_MAX;
+    }
+    int found_g = 0;    // candidates the group has scanned before this ring
+    double kth = kInf;  // the merged list's k-th (d2, index)
+    int32_t kidx = INT32_MAX;
+    const double slack = 1e-9 * (fabs(cd.lo[0]) + fabs(cd.lo[1]) + fabs(cd.lo[2]) +
+                                 cd.s * (cd.dim[0] + cd.dim[1] + cd.dim[2]) + 1.0);
+    const double s = cd.s;
+    for (int R = 0;; ++R) {
+      const int32_t x0 = max(cx - R, 0), x1 = min(cx + R, cd.dim[0] - 1);
+      const int32_t y0 = max(cy - R, 0), y1 = min(cy + R, cd.dim[1] - 1);
+      const int32_t z0 = max(cz - R, 0), z1 = min(cz + R, cd.dim[2] - 1);
+      int found = 0;
+      // the gate: the smaller of this lane's own k-th and the merged bound
+      double gth = kth;
+      int32_t gidx = kidx;
+      auto scan_run = [&](int32_t c0, int32_t c1) {
+        const int32_t s0 = __ldg(cell_start + c0), s1 = __ldg(cell_start + c1 + 1);
+        for (int32_t si = s0 + sub; si < s1; si += G) {
+          const float4 p = __ldg(sorted + si);
+          const double d2 = sq_dist_pinned(q.x, q.y, q.z, p.x, p.y, p.z);
+          const int32_t pi = __float_as_int(p.w);
+          ++found;
+          if (d2 < gth || (d2 == gth && pi < gidx)) {
+            double cd2 = d2;
+            int32_t ci = pi;
+#pragma unroll
+            for (int j = 0; j < MAXK; ++j) {
+              const bool lt = cd2 < bd[j] || (cd2 == bd[j] && ci < bi[j]);
+              const double td = bd[j];
+              const int32_t ti = bi[j];
+              bd[j] = lt ? cd2 : td;
+              bi[j] = lt ? ci : ti;
+              cd2 = lt ? td : cd2;
+              ci = lt ? ti : ci;
+            }
+#pragma unroll
+            for (int j = 0; j < MAXK; ++j)
+              if (j == k - 1 && (bd[j] < gth || (bd[j] == gth && bi[j] < gidx))) {
+                gth = bd[j];
+                gidx = bi[j];
+              }
+          }
+        }
+      };
+      for (int32_t x = x0; x <= x1; ++x) {
+        const double bx0 = cd.lo[0] + (double)x * s;
+        const double ex = fmax(fmax(bx0 - (double)q.x, (double)q.x - (bx0 + s)), 0.0);
+        for (int32_t y = y0; y <= y1; ++y) {
+          const bool face = (x == cx - R) | (x == cx + R) | (y == cy - R) | (y == cy + R);
+          if (found_g >= k) {  // exact pruning of the whole column by the merged bound
+            const double by0 = cd.lo[1] + (double)y * s;
+            const double ey = fmax(fmax(by0 - (double)q.y, (double)q.y - (by0 + s)), 0.0);
+            const double em = fmax(sqrt(ex * ex + ey * ey) - slack, 0.0);
+            if (em * em > kth * (1.0 + 1e-9)) continue;
+          }
+          const int32_t col = cd.cell0 + (x * cd.dim[1] + y) * cd.dim[2];
+          if (face) {
+            scan_run(col + z0, col + z1);
+          } else {
+            if (cz - R >= z0) scan_run(col + cz - R, col + cz - R);
+            if (cz + R <= z1) scan_run(col + cz + R, col + cz + R);
+          }
+        }
+      }
+      // ---- merge: round j takes the group minimum of the lanes' heads
+      __syncwarp(gmask);
+      double md[MAXK];
+      int32_t mi[MAXK];
+#pragma unroll
+      for (int j = 0; j < MAXK; ++j) {
+        md[j] = kInf;
+        mi[j] = INT32_MAX;
+        if (j < k) {
+          double hd = bd[0];
+          int32_t hi = bi[0];
+          int who = sub;
+#pragma unroll
+          for (int o = G / 2; o > 0; o >>= 1) {
+            const double od = __shfl_xor_sync(gmask, hd, o, G);
+            const int32_t oi = __shfl_xor_sync(gmask, hi, o, G);
+            const int ow = __shfl_xor_sync(gmask, who, o, G);
+            if (od < hd || (od == hd && oi < hi)) {
+              hd = od;
+              hi = oi;
+              who = ow;
+            }
+          }
+          if (who == sub) {  // the winner pops its head
+#pragma unroll
+            for (int m = 0; m < MAXK - 1; ++m) {
+              bd[m] = bd[m + 1];
+              bi[m] = bi[m + 1];
+            }
+            bd[MAXK - 1] = kInf;
+            bi[MAXK - 1] = INT32_MAX;
+          }
+          md[j] = hd;
+          mi[j] = hi;
+          if (j == k - 1) {
+            kth = hd;
+            kidx = hi;
+          }
+        }
+      }
+      // lane 0 holds the merged list, the others start the next ring empty
+#pragma unroll
+      for (int j = 0; j < MAXK; ++j) {
+        bd[j] = sub == 0 ? md[j] : kInf;
+        bi[j] = sub == 0 ? mi[j] : INT32_MAX;
+      }
+      found_g += __reduce_add_sync(gmask, found);
+      // every unsearched point lies beyond the searched cube's faces that are
+      // inside the grid; stop once the k-th distance is certainly below that
+      const bool all = x0 == 0 && y0 == 0 && z0 == 0 && x1 == cd.dim[0] - 1 &&
+                       y1 == cd.dim[1] - 1 && z1 == cd.dim[2] - 1;
+      if (all) break;
+      if (found_g >= k) {
+        double b = kInf;
+        const int32_t cc[3] = {cx, cy, cz};
+        const float qq[3] = {q.x, q.y, q.z};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (cc[a] - R > 0) b = fmin(b, (double)qq[a] - (cd.lo[a] + (double)(cc[a] - R) * s));
+          if (cc[a] + R < cd.dim[a] - 1) b = fmin(b, cd.lo[a] + (double)(cc[a] + R + 1) * s - (double)qq[a]);
+        }
+        b -= slack;
+        if (b > 0.0 && kth < b * b * (1.0 - 1e-9)) break;
+      }
+    }
+    if (sub == 0) {
+      int32_t* row = out + (cd.first + qi) * (int64_t)k;
+#pragma unroll
+      for (int j = 0; j < MAXK; ++j)
+        if (j < k) row[j] = bi[j] == INT32_MAX ? -1 : bi[j];
+    }
   }
 }
 
@@ -451,7 +634,20 @@ void launch_knn_query(const KnnCloudDev* clouds, const int32_t* tile_start, cons
                       int64_t num_tiles, int tile_pts, const float4* sorted,
                       const int32_t* cell_start, int k, int32_t* out, cudaStream_t stream) {
   if (num_tiles <= 0) return;
-  if (k <= 16)
+  // lanes per query: a batch of at most ~64k queries (one or a few odometry
+  // frames) leaves the GPU mostly idle at one thread per query, so it uses 4
+  // (r02m, one 15.6k-point frame: 193 -> 142 us, issue-active 20 -> 34 %);
+  // larger batches fill the GPU already and keep 1 (C3's 0.8 M points: 2.31 ms
+  // at G = 1, 4.21 at G = 4).  GVOX_KNN_GROUP overrides (1, 4, 8).
+  int kGroup = (int64_t)num_tiles * tile_pts <= (64 << 10) ? 4 : 1;
+  if (const char* e = std::getenv("GVOX_KNN_GROUP")) kGroup = std::atoi(e);
+  if (k <= 16 && kGroup == 8 && tile_pts % 8 == 0)
+    k_knn_query_g<16, 8><<<(unsigned)(num_tiles * 8), kKnnThreads, 0, stream>>>(
+        clouds, tile_start, tile_cloud, tile_pts, sorted, cell_start, k, out);
+  else if (k <= 16 && kGroup == 4 && tile_pts % 4 == 0)
+    k_knn_query_g<16, 4><<<(unsigned)(num_tiles * 4), kKnnThreads, 0, stream>>>(
+        clouds, tile_start, tile_cloud, tile_pts, sorted, cell_start, k, out);
+  else if (k <= 16)
     k_knn_query<16><<<(unsigned)num_tiles, kKnnThreads, 0, stream>>>(clouds, tile_start, tile_cloud,
                                                                      tile_pts, sorted, cell_start, k, out);
   else
