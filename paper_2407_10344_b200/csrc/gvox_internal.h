@@ -215,12 +215,18 @@ struct AccumSeg {
   int64_t n;
   int64_t pl_offset;
   int64_t acc_offset[GVOX_MAX_LEVELS];  // first voxel of (seg, level) in acc[]
-  double mu_scale[GVOX_MAX_LEVELS];     // S_l = 2^F / r_l
+  double mu_scale[GVOX_MAX_LEVELS];     // offset scale: 2^F / r_l, or (lifted builds) 2^F / r_(L-1) for every l
   double cov_scale;                     // 2^(F - e_c), 2^e_c >= max |C_ij| of the cloud
 };
 void launch_build_accum(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int64_t num_segs,
                         int64_t max_seg_points, int levels, double r0, int dyadic,
                         const int32_t* pslot, unsigned long long* acc, cudaStream_t stream);
+
+// phase 2b: coarser levels from finer ones (nested voxels; see k_build.cu)
+void launch_build_lift(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int64_t num_segs,
+                       int levels, const int64_t* max_level_voxels, double r0,
+                       unsigned long long* acc, cudaStream_t stream);
+bool build_lift_enabled();
 
 // phase 3: per voxel, finalize the record and insert into the final table.
 struct FinalSeg {

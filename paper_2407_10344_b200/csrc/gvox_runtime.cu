@@ -1005,7 +1005,9 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       const double r = std::ldexp(r0, l);
       const LevelPlan& p = plan[s * L + l];
       a.acc_offset[l] = vacc;
-      a.mu_scale[l] = std::ldexp(1.0, F) / r;
+      // lifted builds: one offset scale for every level (the coarsest level's),
+      // so k_build_lift moves a voxel's sums into its parent exactly
+      a.mu_scale[l] = std::ldexp(1.0, F) / (build_lift_enabled() ? std::ldexp(r0, L - 1) : r);
       if (nosync) {
         bseg[s].acc = (unsigned long long*)(b1 + o_acc);
         bseg[s].acc_offset[l] = vacc;
@@ -1088,6 +1090,15 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
                        (unsigned long long*)(b1 + o_acc), ctx->stream);
   }
   CK_LAUNCH("voxelmap accumulate");
+  {
+    std::vector<int64_t> maxv(L, 0);
+    for (int64_t s2 = 0; s2 < count; ++s2)
+      for (int l = 0; l < L; ++l) maxv[l] = std::max<int64_t>(maxv[l], vcap[s2 * L + l]);
+    TimerScope ts(ctx, GVOX_TIMER_BUILD);
+    launch_build_lift((const BuildSeg*)(b0 + o_bseg), (const AccumSeg*)(ab + o_aseg), count, L,
+                      maxv.data(), r0, (unsigned long long*)(b1 + o_acc), ctx->stream);
+  }
+  CK_LAUNCH("voxelmap lift");
   {
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
     launch_build_finalize((const FinalSeg*)(ab + o_fseg), count * L, max_vox,

@@ -145,6 +145,11 @@ __global__ void k_cloud_pack_batch(const PackSeg* __restrict__ segs) {
 #ifndef GVOX_ACC_MAXRUN
 #define GVOX_ACC_MAXRUN 1
 #endif
+// accumulate only level 0 from the points and derive every coarser level from
+// the one below it (k_build_lift), or every level from the points (0)
+#ifndef GVOX_ACC_LIFT
+#define GVOX_ACC_LIFT 1
+#endif
 
 template <int kMaxL>
 __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const BuildSeg* __restrict__ segs, int levels, double r0,
@@ -260,7 +265,8 @@ __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const Build
     }
     const int32_t hl = __shfl_sync(0xffffffffu, h_out[l], leader[l]);
     const bool inr = key[l] < (1ull << 63);
-    if (valid) pslot[sg.pl_offset + k * levels + l] = inr ? hl : -1;
+    // (lifted builds accumulate only level 0 from the points)
+    if (valid && (!GVOX_ACC_LIFT || l == 0)) pslot[sg.pl_offset + k * levels + l] = inr ? hl : -1;
   }
 }
 
@@ -303,7 +309,7 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
     cov_hi[j] = (int)((long long)f >> 24);
   }
 #endif
-  for (int l = 0; l < levels; ++l) {
+  for (int l = 0; l < (GVOX_ACC_LIFT ? 1 : levels); ++l) {
     int32_t sl = valid ? pslot[sg.pl_offset + k * levels + l] : -1;
     int32_t idx;
     if (bs.box[l].dense) {
@@ -422,6 +428,87 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
 #ifndef GVOX_FIN_MINB
 #define GVOX_FIN_MINB 8
 #endif
+// Level l -> l + 1 of the accumulation (nested voxels: a level-(l+1) voxel is
+// the union of the level-l voxels inside it).  The offsets are fixed
+// point at ONE scale for every level (AccumSeg::mu_scale, 2^F / r_(L-1)), so a
+// child's sums move to its parent's corner by adding count * (the child
+// corner's offset in the parent) * scale, an exact integer (r_l * scale is a
+// power of two); covariance sums and counts add as they are.  Integer sums:
+// the parent's sums are bitwise those of summing its points directly.  One
+// thread per level-l voxel, warp runs of equal parent summed by shuffles, one
+// set of atomics per run.
+__global__ void __launch_bounds__(256) k_build_lift(const BuildSeg* __restrict__ bsegs,
+                                                    const AccumSeg* __restrict__ segs, int levels,
+                                                    int l, double r0,
+                                                    unsigned long long* __restrict__ acc) {
+  const int lane = threadIdx.x & 31;
+  const AccumSeg& sg = segs[blockIdx.y];
+  const BuildSeg& bs = bsegs[blockIdx.y];
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nv = bs.counter[l];  // (final after the insert)
+  if (__all_sync(0xffffffffu, v >= nv)) return;
+  const bool valid = v < nv;
+  unsigned long long val[10];
+  int32_t pidx = -1 - lane;  // unique per lane unless a real parent is found
+  if (valid) {
+    const unsigned long long* src = acc + (sg.acc_offset[l] + v) * 10;
+#pragma unroll
+    for (int j = 0; j < 10; ++j) val[j] = src[j];
+    const uint64_t key = bs.keys_by_idx[l][v];
+    const int32_t kx = (int32_t)((key >> 42) & 0x1FFFFF) - kKeyHalf;
+    const int32_t ky = (int32_t)((key >> 21) & 0x1FFFFF) - kKeyHalf;
+    const int32_t kz = (int32_t)(key & 0x1FFFFF) - kKeyHalf;
+    // the child corner's offset inside the parent, in fixed-point units
+    const unsigned long long unit = (unsigned long long)(ldexp(r0, l) * sg.mu_scale[l]);
+    const unsigned long long cnt = val[9];
+    val[0] += cnt * unit * (unsigned long long)(kx & 1);
+    val[1] += cnt * unit * (unsigned long long)(ky & 1);
+    val[2] += cnt * unit * (unsigned long long)(kz & 1);
+    const int32_t px = kx >> 1, py = ky >> 1, pz = kz >> 1;
+    const LevelBox& bx = bs.box[l + 1];
+    if (bx.dense) {
+      pidx = bx.grid[(size_t)((uint32_t)(px - bx.x0) * bx.syz + (uint32_t)(py - bx.y0) * bx.dz +
+                              (uint32_t)(pz - bx.z0))];
+    } else {
+      const uint64_t pk = pack_key(px, py, pz);
+      uint64_t h = hash_slot(pk, bs.tmp_shift);
+      for (;;) {
+        const ulonglong2 e = bs.tmp_slots[l + 1][h];
+        if (e.x == pk) {
+          pidx = (int32_t)(uint32_t)e.y;
+          break;
+        }
+        h = (h + 1) & bs.tmp_mask;  // (the parent exists: its points are the child's)
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 10; ++j) val[j] = 0ull;
+  }
+  // runs of equal parent in lane order; suffix sums by doubling (64-bit values)
+  const int32_t prev = __shfl_up_sync(0xffffffffu, pidx, 1);
+  const bool head = lane == 0 || pidx != prev;
+  const unsigned H = __ballot_sync(0xffffffffu, head);
+  const unsigned after = lane == 31 ? 0u : (H & (0xffffffffu << (lane + 1)));
+  const int run_end = after ? __ffs(after) - 2 : 31;
+  const int max_run = __reduce_max_sync(0xffffffffu, head ? (unsigned)(run_end - lane + 1) : 0u);
+#pragma unroll 1
+  for (int off = 1; off < max_run; off <<= 1) {
+    const bool take = lane + off <= run_end;
+#pragma unroll
+    for (int j = 0; j < 10; ++j) {
+      const unsigned long long o = __shfl_down_sync(0xffffffffu, val[j], off);
+      if (take) val[j] += o;
+    }
+  }
+  if (head && valid) {
+    unsigned long long* dst = acc + (sg.acc_offset[l + 1] + pidx) * 10;
+#pragma unroll
+    for (int j = 0; j < 10; ++j) atomicAdd(dst + j, val[j]);
+  }
+  (void)levels;
+}
+
 __global__ void __launch_bounds__(256, GVOX_FIN_MINB) k_build_finalize(const FinalSeg* __restrict__ segs,
                                  const unsigned long long* __restrict__ acc) {
   const FinalSeg& sg = segs[blockIdx.y];  // one (segment, level) per grid row
@@ -536,6 +623,19 @@ void launch_build_accum(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int
                                           acc);
   note_launch();
 }
+
+void launch_build_lift(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int64_t num_segs,
+                       int levels, const int64_t* max_level_voxels, double r0,
+                       unsigned long long* acc, cudaStream_t stream) {
+  if (!GVOX_ACC_LIFT || num_segs <= 0) return;
+  for (int l = 0; l + 1 < levels; ++l) {
+    if (max_level_voxels[l] <= 0) continue;
+    dim3 grid(grid_for(max_level_voxels[l], 256), (unsigned)num_segs);
+    k_build_lift<<<grid, 256, 0, stream>>>(bsegs_dev, segs_dev, levels, l, r0, acc);
+    note_launch();
+  }
+}
+bool build_lift_enabled() { return GVOX_ACC_LIFT != 0; }
 
 void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs, int64_t max_seg_voxels,
                            const unsigned long long* acc, cudaStream_t stream) {
