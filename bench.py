@@ -74,9 +74,12 @@ def parse():
     ap.add_argument("--submaps", type=int, default=None, help="override the submap count (tests)")
     ap.add_argument("--order", default="morton", choices=["morton", "random"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-pipelined", action="store_true",
-                    help="e2e with step k+1's upload overlapping step k's compute (measured r01g: "
-                         "360-376 ms vs 386 ms serial; the concurrent H2D runs at ~24 GB/s)")
+    ap.add_argument("--e2e-mode", default="pipelined", choices=["pipelined", "serial"],
+                    help="e2e: step k+1's upload overlapping step k's compute (default; r02p: "
+                         "237 ms vs 367 ms serial per C5 step at 5 steps), or each step's "
+                         "upload inside it")
+    ap.add_argument("--e2e-steps", type=int, default=10,
+                    help="e2e steps timed (the first step's upload is never overlapped)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--per-call-runs", type=int, default=20,
@@ -644,19 +647,23 @@ def main():
             mu_h[loc_off[j_]:loc_off[j_ + 1]] = torch.from_numpy(np.asarray(sc.mu[a_:b_]))
             cov_h[loc_off[j_]:loc_off[j_ + 1]] = torch.from_numpy(np.asarray(sc.cov[a_:b_]))
             nrm_h[loc_off[j_]:loc_off[j_ + 1]] = torch.from_numpy(np.asarray(sc.nrm[a_:b_]))
-        k_e2e = max(1, min(args.steps, 5))
-        pin_out = np.zeros(max(len(my_pairs), len(sc.factors)), gv.LINEAR_FACTOR_DTYPE)
+        k_e2e = max(1, args.e2e_steps)
+        # full records land in pinned host memory (a pageable D2H is staged at a
+        # fraction of the PCIe rate)
+        n_out = max(len(my_pairs), len(sc.factors), 1)
+        pin_out = torch.empty(n_out * gv.LINEAR_FACTOR_DTYPE.itemsize, dtype=torch.uint8).pin_memory() \
+            .numpy().view(gv.LINEAR_FACTOR_DTYPE)
         h2d = 0
         d2h = 0
 
-        # Pipelined e2e (--e2e-pipelined): each step's inputs are copied from pinned host
+        # Pipelined e2e (default, --e2e-mode pipelined): each step's inputs are copied from pinned host
         # memory into one of two device staging buffers on a copy stream, the
         # copy of step k + 1 overlapping the compute of step k (the way a
         # streaming deployment feeds the GPU); step k's clouds are then created
         # from the staged device arrays through the same public call.  Every
         # copy, including the first step's, is inside the timed region.
         # Default (serial): the copy inside each step, nothing overlapped.
-        pipelined = args.e2e_pipelined
+        pipelined = args.e2e_mode == "pipelined"
         if pipelined:
             stage = [tuple(torch.empty(t_.shape, dtype=t_.dtype, device=dev) for t_ in (mu_h, cov_h, nrm_h))
                      for _ in range(2)]
@@ -664,12 +671,25 @@ def main():
             pack_ev = [None, None]
 
         def issue_h2d(k):
-            """Upload step k's inputs into staging buffer k % 2 from a helper
-            thread, in 16 MB pieces with at most two in flight: the copy engine
-            then never holds a long queue in front of the library's own small
-            per-call uploads.  Returns (thread, [final event])."""
+            """Upload step k's inputs into staging buffer k % 2 on the copy
+            stream: three whole-array copies (the library's own small per-call
+            inputs go through SM-driven copies, so they never queue behind
+            this bulk upload on the copy engines); GVOX_E2E_CHUNK_MB > 0 uses
+            pieces of that size from a helper thread, at most two in flight
+            (the r01 scheme).  Returns (thread or None, [final event])."""
             b_ = k % 2
             done_ = []
+            chunk_mb = float(os.environ.get("GVOX_E2E_CHUNK_MB", "0"))
+            if chunk_mb <= 0:
+                with torch.cuda.stream(cp_stream):
+                    if pack_ev[b_] is not None:
+                        cp_stream.wait_event(pack_ev[b_])
+                    for dst_, src_ in zip(stage[b_], (mu_h, cov_h, nrm_h)):
+                        dst_.copy_(src_, non_blocking=True)
+                    e_ = torch.cuda.Event()
+                    e_.record(cp_stream)
+                    done_.append(e_)
+                return None, done_
 
             def run_():
                 with torch.cuda.stream(cp_stream):
@@ -677,7 +697,7 @@ def main():
                         cp_stream.wait_event(pack_ev[b_])
                     inflight_ = []
                     for dst_, src_ in zip(stage[b_], (mu_h, cov_h, nrm_h)):
-                        rows_ = max(1, (16 << 20) // (src_.shape[1] * 4))
+                        rows_ = max(1, int(chunk_mb * (1 << 20)) // (src_.shape[1] * 4))
                         for r_ in range(0, src_.shape[0], rows_):
                             dst_[r_:r_ + rows_].copy_(src_[r_:r_ + rows_], non_blocking=True)
                             e_ = torch.cuda.Event()
@@ -708,7 +728,8 @@ def main():
             _dbg(f"step {k} start")
             ev_next = None
             if pipelined:
-                ev_in[0].join()  # every piece of step k's upload is enqueued
+                if ev_in[0] is not None:
+                    ev_in[0].join()  # every piece of step k's upload is enqueued
                 stream.wait_event(ev_in[1][0])
                 if not last:
                     ev_next = issue_h2d(k + 1)

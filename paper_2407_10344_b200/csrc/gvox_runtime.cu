@@ -364,11 +364,30 @@ gvox_status pin_reserve(gvox_ctx* ctx, size_t bytes, void** out) {
   return GVOX_OK;
 }
 
+// The calls' small H2D input blocks (<= 64 MiB) are read from the pinned
+// staging by an SM kernel over PCIe instead of a copy-engine DMA: a bulk upload
+// on another stream (the e2e pipeline's next clouds) then never delays them.
+// GVOX_H2D_DMA=1 restores cudaMemcpyAsync for every block.
+bool h2d_by_kernel(size_t bytes) {
+  static const bool dma = std::getenv("GVOX_H2D_DMA") != nullptr;
+  return !dma && bytes <= (64u << 20);
+}
+gvox_status h2d_small(gvox_ctx* ctx, void* dst, const void* pinned_src, size_t bytes) {
+  if (h2d_by_kernel(bytes)) {
+    launch_h2d_copy(dst, pinned_src, (int64_t)bytes, ctx->stream);
+    CK_LAUNCH("h2d copy");
+  } else {
+    CK(cudaMemcpyAsync(dst, pinned_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  return GVOX_OK;
+}
+
 // H2D out of the slot pin_reserve handed out last
 gvox_status h2d_block(gvox_ctx* ctx, void* dst, const void* pinned_src, size_t bytes) {
   if (bytes == 0) return GVOX_OK;
   gvox_ctx::PinSlot& sl = ctx->pin_ring[ctx->pin_slot];
-  CK(cudaMemcpyAsync(dst, pinned_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  gvox_status st = h2d_small(ctx, dst, pinned_src, bytes);
+  if (st) return st;
   CK(cudaEventRecord(sl.done, ctx->stream));
   sl.pending = true;
   return GVOX_OK;
@@ -394,7 +413,10 @@ gvox_status pin_b_reserve(gvox_ctx* ctx, int slot, size_t bytes, void** out) {
   return GVOX_OK;
 }
 gvox_status pin_b_upload(gvox_ctx* ctx, int slot, void* dst, size_t bytes) {
-  if (bytes) CK(cudaMemcpyAsync(dst, ctx->pin_b[slot], bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (bytes) {
+    gvox_status st = h2d_small(ctx, dst, ctx->pin_b[slot], bytes);
+    if (st) return st;
+  }
   CK(cudaEventRecord(ctx->pin_b_done[slot], ctx->stream));
   return GVOX_OK;
 }
@@ -603,9 +625,15 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
     st8[2] = st8[3] = st8[4] = INT32_MAX;
     st8[5] = st8[6] = st8[7] = INT32_MIN;
   }
-  CK(cudaMemcpyAsync(dflags, hflags.data(), 32 * (size_t)count, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));  // hflags is reused below
+  {
+    // (small inputs through the pinned ring: no copy-engine queueing, no sync)
+    void* hp = nullptr;
+    st = pin_reserve(ctx, 32 * (size_t)count, &hp);
+    if (st) return st;
+    std::memcpy(hp, hflags.data(), 32 * (size_t)count);
+    st = h2d_block(ctx, dflags, hp, 32 * (size_t)count);
+    if (st) return st;
+  }
   if (n > 0) {
     const float *dmu = mu, *dcov = cov, *dnrm = normals;
     if (mem == GVOX_HOST) {
@@ -631,10 +659,15 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
                         cbox + cb_off[k], dflags + 8 * k};
         max_n = std::max(max_n, m);
       }
-      CK(cudaMemcpyAsync(base + o_pseg, ps.data(), sizeof(PackSeg) * count,
-                         cudaMemcpyHostToDevice, ctx->stream));
+      {
+        void* hp = nullptr;
+        st = pin_reserve(ctx, sizeof(PackSeg) * count, &hp);
+        if (st) return st;
+        std::memcpy(hp, ps.data(), sizeof(PackSeg) * count);
+        st = h2d_block(ctx, base + o_pseg, hp, sizeof(PackSeg) * count);
+        if (st) return st;
+      }
       launch_cloud_pack_batch((const PackSeg*)(base + o_pseg), count, max_n, ctx->stream);
-      CK(cudaStreamSynchronize(ctx->stream));  // ps is a host temporary
     } else {
       for (int64_t k = 0; k < count; ++k) {
         int64_t a = offsets[k], m = offsets[k + 1] - offsets[k];
@@ -664,9 +697,14 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
     d.N = m ? P + co[k] + 64 : nullptr;
     d.chunk_box = m ? cbox + cb_off[k] : nullptr;
   }
-  CK(cudaMemcpyAsync(base + o_desc, descs.data(), sizeof(CloudDev) * count, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
+  {
+    void* hp = nullptr;
+    st = pin_reserve(ctx, sizeof(CloudDev) * count, &hp);
+    if (st) return st;
+    std::memcpy(hp, descs.data(), sizeof(CloudDev) * count);
+    st = h2d_block(ctx, base + o_desc, hp, sizeof(CloudDev) * count);
+    if (st) return st;
+  }
   for (int64_t k = 0; k < count; ++k) {
     auto* c = new gvox_cloud;
     c->buf = buf;

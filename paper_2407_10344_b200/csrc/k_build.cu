@@ -16,6 +16,7 @@
 //           offset-from-centre and fp32 covariance; insert into the final
 //           table (capacity 2^k >= 2V).
 #include <climits>
+#include <algorithm>
 #include <cstdint>
 
 #include "k_common.cuh"
@@ -562,6 +563,24 @@ __global__ void k_grid_reset(const ResetSeg* __restrict__ segs) {
   sg.grid[((size_t)(kx - sg.x0) * sg.dy + (ky - sg.y0)) * sg.dz + (kz - sg.z0)] = -1;
 }
 
+// Host -> device copy by the SMs: reads pinned (mapped) host memory over PCIe
+// directly (ld.global.cv: the staging slots are rewritten by the host between
+// uses, nothing may be cached), so the calls' small input blocks never queue on
+// the copy engines behind a bulk upload running on another stream.
+__global__ void k_h2d_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, int64_t bytes) {
+  const int64_t n16 = bytes >> 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  if (aligned) {
+    for (int64_t i = t0; i < n16; i += stride)
+      reinterpret_cast<int4*>(dst)[i] = __ldcv(reinterpret_cast<const int4*>(src) + i);
+    for (int64_t i = (n16 << 4) + t0; i < bytes; i += stride) dst[i] = *(const volatile uint8_t*)(src + i);
+  } else {
+    for (int64_t i = t0; i < bytes; i += stride) dst[i] = *(const volatile uint8_t*)(src + i);
+  }
+}
+
 __global__ void k_fill_u64(uint64_t* p, uint64_t value, int64_t count) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -650,6 +669,14 @@ void launch_grid_reset(const ResetSeg* segs_dev, int64_t num_segs, int64_t max_s
   if (num_segs <= 0 || max_seg_voxels <= 0) return;
   dim3 grid(grid_for(max_seg_voxels, 256), (unsigned)num_segs);
   k_grid_reset<<<grid, 256, 0, stream>>>(segs_dev);
+  note_launch();
+}
+
+void launch_h2d_copy(void* dst, const void* pinned_src, int64_t bytes, cudaStream_t stream) {
+  if (bytes <= 0) return;
+  int64_t blocks = ((bytes >> 4) + 255) / 256;
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 4));
+  k_h2d_copy<<<(unsigned)blocks, 256, 0, stream>>>((uint8_t*)dst, (const uint8_t*)pinned_src, bytes);
   note_launch();
 }
 
