@@ -262,7 +262,7 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_label(args, sc), "oracle_sample": desc},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": desc},
+                             "sample": desc, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -639,14 +639,19 @@ def main():
         need_n = n_pts[need]
         loc_off = np.concatenate([[0], np.cumsum(need_n)]).astype(np.int64)
         tot_n = int(loc_off[-1])
+        # the step's inputs: means and covariances, and normals only where the
+        # step validates correspondences (C1-C3 odometry factors) --
+        # the C4/C5 global factors never read them
+        use_nrm = not select
         mu_h = torch.empty((tot_n, 3), dtype=torch.float32).pin_memory()
         cov_h = torch.empty((tot_n, 6), dtype=torch.float32).pin_memory()
-        nrm_h = torch.empty((tot_n, 3), dtype=torch.float32).pin_memory()
+        nrm_h = torch.empty((tot_n if use_nrm else 0, 3), dtype=torch.float32).pin_memory()
         for j_, c_ in enumerate(need):
             a_, b_ = int(sc.offsets[c_]), int(sc.offsets[c_ + 1])
             mu_h[loc_off[j_]:loc_off[j_ + 1]] = torch.from_numpy(np.asarray(sc.mu[a_:b_]))
             cov_h[loc_off[j_]:loc_off[j_ + 1]] = torch.from_numpy(np.asarray(sc.cov[a_:b_]))
-            nrm_h[loc_off[j_]:loc_off[j_ + 1]] = torch.from_numpy(np.asarray(sc.nrm[a_:b_]))
+            if use_nrm:
+                nrm_h[loc_off[j_]:loc_off[j_ + 1]] = torch.from_numpy(np.asarray(sc.nrm[a_:b_]))
         k_e2e = max(1, args.e2e_steps)
         # full records land in pinned host memory (a pageable D2H is staged at a
         # fraction of the PCIe rate)
@@ -684,11 +689,14 @@ def main():
                 with torch.cuda.stream(cp_stream):
                     if pack_ev[b_] is not None:
                         cp_stream.wait_event(pack_ev[b_])
+                    s_ = torch.cuda.Event(enable_timing=True)
+                    s_.record(cp_stream)
                     for dst_, src_ in zip(stage[b_], (mu_h, cov_h, nrm_h)):
                         dst_.copy_(src_, non_blocking=True)
-                    e_ = torch.cuda.Event()
+                    e_ = torch.cuda.Event(enable_timing=True)
                     e_.record(cp_stream)
                     done_.append(e_)
+                    done_.append(s_)
                 return None, done_
 
             def run_():
@@ -731,19 +739,24 @@ def main():
                 if ev_in[0] is not None:
                     ev_in[0].join()  # every piece of step k's upload is enqueued
                 stream.wait_event(ev_in[1][0])
+                if os.environ.get("GVOX_E2E_DEBUG") and len(ev_in[1]) > 1:
+                    ev_in[1][0].synchronize()
+                    log(f"[e2e] upload of step {k}: {ev_in[1][1].elapsed_time(ev_in[1][0]):.1f} ms")
                 if not last:
                     ev_next = issue_h2d(k + 1)
                 b_ = k % 2
-                cl_loc = gv.create_clouds(ctx, stage[b_][0], stage[b_][1], stage[b_][2], loc_off)
+                cl_loc = gv.create_clouds(ctx, stage[b_][0], stage[b_][1],
+                                          stage[b_][2] if use_nrm else None, loc_off)
                 pe_ = torch.cuda.Event()
                 pe_.record(stream)
                 pack_ev[b_] = pe_
             else:
-                cl_loc = gv.create_clouds(ctx, mu_h.numpy(), cov_h.numpy(), nrm_h.numpy(), loc_off)
+                cl_loc = gv.create_clouds(ctx, mu_h.numpy(), cov_h.numpy(),
+                                          nrm_h.numpy() if use_nrm else None, loc_off)
             cl_all = [cl_loc[0]] * sc.num_clouds  # placeholders for clouds not used here
             for j_, c_ in enumerate(need):
                 cl_all[c_] = cl_loc[j_]
-            h2d_b = 48 * tot_n
+            h2d_b = (48 if use_nrm else 36) * tot_n
             carr = gv.HandleArray(cl_all)
             _dbg("clouds")
             maps_e = gv.create_voxelmaps(ctx, [cl_all[int(sc.map_clouds[t])] for t in my_targets],

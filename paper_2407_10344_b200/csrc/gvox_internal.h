@@ -391,7 +391,9 @@ void launch_pcg_persistent(const double* blocks, const int32_t* row_start, const
                            int64_t num_vars, const double* minv, const double* rhs, double* x,
                            double* r, double* z, double* p, double* q, double* part_a,
                            double* part_b, PcgState* st, int32_t max_iter, double tol,
-                           cudaStream_t stream);
+                           const int32_t* chunk_row, const int32_t* chunk_b0,
+                           const int32_t* row_chunk, int64_t num_chunks, double* qpart,
+                           double* part_c, cudaStream_t stream);
 void launch_scatter_delta(const double* x, const int32_t* var_of_pose, int64_t num_poses,
                           double* delta, cudaStream_t stream);
 

@@ -2515,6 +2515,24 @@ gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t
     gstart[v + 1] = (int32_t)glist.size();
   }
   result->num_blocks = (int32_t)NB;
+  // SpMV work units of the persistent PCG: each block row cut into chunks of at
+  // most kPcgChunk blocks (GVOX_PCG_CHUNK; 0 = one chunk per row), so no warp
+  // walks a whole long row while the others wait at the barrier
+  int pcg_chunk = 64;
+  if (const char* e = std::getenv("GVOX_PCG_CHUNK")) pcg_chunk = std::atoi(e);
+  std::vector<int32_t> chunk_row, chunk_b0, row_chunk(V + 1, 0);
+  for (int32_t v = 0; v < V; ++v) {
+    row_chunk[v] = (int32_t)chunk_row.size();
+    const int32_t b0 = row_start[v], b1 = row_start[v + 1];
+    const int32_t step = pcg_chunk > 0 ? pcg_chunk : std::max(b1 - b0, 1);
+    for (int32_t b = b0; b < b1 || b == b0; b += step) {  // (an empty row still gets one chunk)
+      chunk_row.push_back(v);
+      chunk_b0.push_back(b);
+      if (b1 <= b0) break;
+    }
+  }
+  row_chunk[V] = (int32_t)chunk_row.size();
+  const int64_t NC = (int64_t)chunk_row.size();
   DeviceGuard dg(ctx->device);
   // ---- one input block
   std::vector<FactorDev> fdev(num_factors);
@@ -2534,6 +2552,9 @@ gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t
   size_t o_isd = lay.add(std::max<size_t>(is_diag.size(), 1));
   size_t o_vo = lay.add(4 * std::max<int64_t>(num_poses, 1));
   size_t o_acc = lay.add(mem == GVOX_HOST ? sizeof(gvox_factor_accum) * num_factors : 0);
+  size_t o_crow = lay.add(4 * std::max<int64_t>(NC, 1));
+  size_t o_cb0 = lay.add(4 * std::max<int64_t>(NC, 1));
+  size_t o_rch = lay.add(4 * row_chunk.size());
   const size_t in_bytes = lay.size;
   void* pin = nullptr;
   st = pin_reserve(ctx, in_bytes, &pin);
@@ -2551,6 +2572,11 @@ gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t
   if (!is_diag.empty()) std::memcpy(hp + o_isd, is_diag.data(), is_diag.size());
   if (num_poses) std::memcpy(hp + o_vo, var_of.data(), 4 * num_poses);
   if (mem == GVOX_HOST && num_factors) std::memcpy(hp + o_acc, accum, sizeof(gvox_factor_accum) * num_factors);
+  if (NC) {
+    std::memcpy(hp + o_crow, chunk_row.data(), 4 * NC);
+    std::memcpy(hp + o_cb0, chunk_b0.data(), 4 * NC);
+  }
+  std::memcpy(hp + o_rch, row_chunk.data(), 4 * row_chunk.size());
   Layout wl;
   size_t o_in = wl.add(in_bytes);
   size_t o_rec = wl.add(sizeof(gvox_linear_factor) * std::max<int64_t>(num_factors, 1));
@@ -2561,6 +2587,8 @@ gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t
   size_t o_pb = wl.add(8 * (n6 / 6));
   size_t o_minv = wl.add(8 * 36 * (n6 / 6));
   size_t o_st = wl.add(sizeof(PcgState) + 16);
+  size_t o_qpart = wl.add(8 * 6 * std::max<int64_t>(NC, 1));
+  size_t o_pc = wl.add(8 * std::max<int64_t>(NC, 1));
   size_t o_dl = wl.add(mem == GVOX_HOST ? 48 * (size_t)std::max<int64_t>(num_poses, 1) : 0);
   void* ws = nullptr;
   st = ws_reserve(ctx, 0, wl.size, &ws);
@@ -2599,7 +2627,9 @@ gvox_status gvox_solve_global(gvox_ctx* ctx, const gvox_factor* factors, int64_t
                             (const double*)(wb + o_rhs), (double*)(wb + o_x), (double*)(wb + o_r),
                             (double*)(wb + o_z), (double*)(wb + o_p), (double*)(wb + o_q),
                             (double*)(wb + o_pq), (double*)(wb + o_pb), dst, P.max_iterations,
-                            P.tol, ctx->stream);
+                            P.tol, (const int32_t*)(din + o_crow), (const int32_t*)(din + o_cb0),
+                            (const int32_t*)(din + o_rch), NC, (double*)(wb + o_qpart),
+                            (double*)(wb + o_pc), ctx->stream);
       CK_LAUNCH("PCG (persistent)");
     } else if (V > 0) {
       launch_pcg_init((const double*)(wb + o_rhs), (const double*)(wb + o_minv), V, (double*)(wb + o_x),

@@ -273,7 +273,9 @@ __global__ void __launch_bounds__(kPcgThreads)
                      const double* __restrict__ rhs, double* __restrict__ x, double* __restrict__ r,
                      double* __restrict__ z, double* __restrict__ p, double* __restrict__ q,
                      double* __restrict__ part_a, double* __restrict__ part_b, PcgState* __restrict__ st,
-                     int32_t max_iter, double tol) {
+                     int32_t max_iter, double tol, const int32_t* __restrict__ chunk_row,
+                     const int32_t* __restrict__ chunk_b0, const int32_t* __restrict__ row_chunk,
+                     int64_t num_chunks, double* __restrict__ qpart, double* __restrict__ part_c) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[33];
   const int lane = threadIdx.x & 31;
@@ -317,10 +319,16 @@ __global__ void __launch_bounds__(kPcgThreads)
   int32_t it = 0;
   bool go = r0 > 0.0 && !(r0 <= tol * r0);
   while (go) {
-    // q = A p (warp per block row, lane-strided blocks, fixed xor tree)
-    for (int64_t v = gwarp; v < num_vars; v += nwarps) {
+    // q = A p over row CHUNKS of at most kPcgChunk blocks (a long block row is
+    // split over several warps, so the SpMV phase is not as long as the longest
+    // row): warp per chunk, lane-strided blocks, fixed xor tree; the chunk's
+    // partial product and its p . (partial q) go to qpart / part_c
+    for (int64_t c = gwarp; c < num_chunks; c += nwarps) {
+      const int32_t v = chunk_row[c];
+      const int32_t bend = (c + 1 < num_chunks && chunk_row[c + 1] == v) ? chunk_b0[c + 1]
+                                                                          : row_start[v + 1];
       double acc[6] = {0, 0, 0, 0, 0, 0};
-      for (int32_t b = row_start[v] + lane; b < row_start[v + 1]; b += 32) {
+      for (int32_t b = chunk_b0[c] + lane; b < bend; b += 32) {
         const double* B = blocks + 36 * (int64_t)b;
         const double* pc = p + 6 * (int64_t)col[b];
         double pv[6];
@@ -339,20 +347,23 @@ __global__ void __launch_bounds__(kPcgThreads)
         double d = 0.0;
 #pragma unroll
         for (int i = 0; i < 6; ++i) {
-          q[6 * v + i] = acc[i];
-          d += p[6 * v + i] * acc[i];
+          qpart[6 * c + i] = acc[i];
+          d += p[6 * (int64_t)v + i] * acc[i];
         }
-        part_a[v] = d;
+        part_c[c] = d;
       }
     }
     grid.sync();
-    const double pq = sum_parts(part_a, num_vars, red);
+    const double pq = sum_parts(part_c, num_chunks, red);
     const double alpha = pq > 0.0 ? rz / pq : 0.0;
-    grid.sync();  // every CTA has read part_a before it is overwritten
+    grid.sync();  // every CTA has read part_c before it is overwritten
     for (int64_t v = gwarp; v < num_vars; v += nwarps)
       if (lane < 6) {
+        double qv = 0.0;  // the row's chunks in order
+        for (int32_t c = row_chunk[v]; c < row_chunk[v + 1]; ++c) qv += qpart[6 * (int64_t)c + lane];
+        q[6 * v + lane] = qv;
         x[6 * v + lane] += alpha * p[6 * v + lane];
-        r[6 * v + lane] -= alpha * q[6 * v + lane];
+        r[6 * v + lane] -= alpha * qv;
       }
     __syncwarp();
     precond_rows();
@@ -551,16 +562,20 @@ void launch_pcg_persistent(const double* blocks, const int32_t* row_start, const
                            int64_t num_vars, const double* minv, const double* rhs, double* x,
                            double* r, double* z, double* p, double* q, double* part_a,
                            double* part_b, PcgState* st, int32_t max_iter, double tol,
-                           cudaStream_t stream) {
+                           const int32_t* chunk_row, const int32_t* chunk_b0,
+                           const int32_t* row_chunk, int64_t num_chunks, double* qpart,
+                           double* part_c, cudaStream_t stream) {
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_persistent, kPcgThreads, 0);
-  const int64_t want = (num_vars * 32 + kPcgThreads - 1) / kPcgThreads;  // one warp per row
+  const int64_t want = (std::max(num_vars, num_chunks) * 32 + kPcgThreads - 1) / kPcgThreads;  // a warp per chunk
   int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)sms * std::max(per_sm, 1));
   void* args[] = {(void*)&blocks, (void*)&row_start, (void*)&col, (void*)&num_vars, (void*)&minv,
                   (void*)&rhs, (void*)&x, (void*)&r, (void*)&z, (void*)&p, (void*)&q,
-                  (void*)&part_a, (void*)&part_b, (void*)&st, (void*)&max_iter, (void*)&tol};
+                  (void*)&part_a, (void*)&part_b, (void*)&st, (void*)&max_iter, (void*)&tol,
+                  (void*)&chunk_row, (void*)&chunk_b0, (void*)&row_chunk, (void*)&num_chunks,
+                  (void*)&qpart, (void*)&part_c};
   cudaLaunchCooperativeKernel((void*)k_pcg_persistent, grid, kPcgThreads, args, 0, stream);
   note_launch();
 }
