@@ -669,6 +669,7 @@ def main():
         # copy, including the first step's, is inside the timed region.
         # Default (serial): the copy inside each step, nothing overlapped.
         pipelined = args.e2e_mode == "pipelined"
+        e2e_device_select = os.environ.get("GVOX_E2E_HOST_SELECT") is None
         if pipelined:
             stage = [tuple(torch.empty(t_.shape, dtype=t_.dtype, device=dev) for t_ in (mu_h, cov_h, nrm_h))
                      for _ in range(2)]
@@ -762,16 +763,32 @@ def main():
             maps_e = gv.create_voxelmaps(ctx, [cl_all[int(sc.map_clouds[t])] for t in my_targets],
                                          sc.r0, sc.levels)
             marr = gv.HandleArray(maps_e)
-            if select:
+            if select and e2e_device_select:
+                # the screened batch through the public API with the decisions
+                # kept on the device: gvox_overlap_select (device out) ->
+                # gvox_linearize_batch_accum_select -> gvox_expand into pinned
+                # host memory (full records: the step's result)
                 _dbg("maps")
-                cnt = gv.overlap_select(ctx, carr, marr, pairs_s, poses, sc.overlap_level, 1, 20)
-                _dbg("select")
-                fe = all_fac[cnt.view(bool)]
+                gv.overlap_select(ctx, carr, marr, pairs_s, poses, sc.overlap_level, 1, 20,
+                                  out=sel_d)
+                ns = gv.linearize_batch_accum_select(ctx, carr, marr, all_fac, sel_d, poses,
+                                                     acc_out, selected_host=sel_h)
+                _dbg("select + linearize")
+                fe = all_fac[sel_h.view(bool)]
+                cnt = sel_h
+                res = gv.expand(ctx, fe, poses, acc_out[:ns], out=pin_out[:ns])
+                _dbg("expand")
             else:
-                cnt = gv.overlap(ctx, carr, marr, pairs_s, poses, sc.overlap_level)
-                fe = fixed
-            res = gv.linearize_batch(ctx, carr, marr, fe, poses, out=pin_out[:len(fe)])
-            _dbg("linearize")
+                if select:
+                    _dbg("maps")
+                    cnt = gv.overlap_select(ctx, carr, marr, pairs_s, poses, sc.overlap_level, 1, 20)
+                    _dbg("select")
+                    fe = all_fac[cnt.view(bool)]
+                else:
+                    cnt = gv.overlap(ctx, carr, marr, pairs_s, poses, sc.overlap_level)
+                    fe = fixed
+                res = gv.linearize_batch(ctx, carr, marr, fe, poses, out=pin_out[:len(fe)])
+                _dbg("linearize")
             h2d = h2d_b + poses.nbytes * 2 + pairs_s.nbytes + fe.nbytes
             d2h = cnt.nbytes + res.nbytes
             return int(n_pts[fe["source_cloud"]].sum()), ev_next
