@@ -596,6 +596,7 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
   if (mem != GVOX_HOST && mem != GVOX_DEVICE)
     return fail(GVOX_ERR_INVALID, "gvox_cloud_create: mem must be GVOX_HOST or GVOX_DEVICE");
   DeviceGuard g(ctx->device);
+  DebugClock dbg;
   Layout lay;
   size_t o_desc = lay.add(sizeof(CloudDev) * count);
   // chunked point records (gvox_internal.h): each cloud starts on a chunk
@@ -613,6 +614,7 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
   std::shared_ptr<DevBuf> buf;
   gvox_status st = devbuf_alloc(lay.size, ctx->device, ctx->stream, &buf);
   if (st) return st;
+  dbg.lap("clouds: alloc");
   char* base = (char*)buf->ptr;
   float4* P = (float4*)(base + o_pts);
   float* cbox = (float*)(base + o_cbox);
@@ -678,8 +680,10 @@ gvox_status gvox_clouds_create(gvox_ctx* ctx, const float* mu, const float* cov,
     }
     CK_LAUNCH("gvox_cloud_create: pack");
   }
+  dbg.lap("clouds: pack enqueued");
   CK(cudaMemcpyAsync(hflags.data(), dflags, 32 * (size_t)count, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  dbg.lap("clouds: stats read back");
   for (int64_t k = 0; k < count; ++k)
     if (hflags[8 * k] & 1)
       return fail(GVOX_ERR_INVALID,

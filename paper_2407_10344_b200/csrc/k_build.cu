@@ -29,95 +29,115 @@ __device__ inline bool finite3(float a, float b, float c) {
   return isfinite(a) && isfinite(b) && isfinite(c);
 }
 
+// Pack the cloud's points into the chunked layout (gvox_internal.h) and gather
+// its statistics: flag (non-finite input), max |C_ij|, min / max of the means
+// (order-preserving ints), and the per-32-point chunk boxes.  Every warp walks
+// whole 32-point chunks, grid-strided (a warp packs many chunks, so its stores
+// drain while it works on the next ones -- one point per thread left the warps
+// waiting at exit for their stores, r02u: 26.8 ms for C5's 2e8 points), and
+// keeps its statistics in registers: one set of atomics per warp at the end.
 __device__ __forceinline__ void cloud_pack_body(const float* __restrict__ mu,
                                                 const float* __restrict__ cov,
                                                 const float* __restrict__ nrm, int64_t n,
                                                 float4* __restrict__ P,
                                                 float* __restrict__ chunk_box,
-                                                int32_t* __restrict__ stats) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                                                int32_t* __restrict__ stats, int64_t warp0,
+                                                int64_t nwarps) {
+  const int lane = threadIdx.x & 31;
   float cm = 0.f;
   bool bad = false;
-  int32_t lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
-  if (i < n) {
-    float x = mu[3 * i], y = mu[3 * i + 1], z = mu[3 * i + 2];
-    float c0 = cov[6 * i], c1 = cov[6 * i + 1], c2 = cov[6 * i + 2];
-    float c3 = cov[6 * i + 3], c4 = cov[6 * i + 4], c5 = cov[6 * i + 5];
-    float nx = 0.f, ny = 0.f, nz = 0.f;
-    if (nrm) {
-      nx = nrm[3 * i];
-      ny = nrm[3 * i + 1];
-      nz = nrm[3 * i + 2];
+  int32_t lox = INT_MAX, loy = INT_MAX, loz = INT_MAX, hix = INT_MIN, hiy = INT_MIN, hiz = INT_MIN;
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  for (int64_t ch = warp0; ch < nchunks; ch += nwarps) {
+    const int64_t i = ch * kChunk + lane;
+    const bool in = i < n;
+    float x = 0.f, y = 0.f, z = 0.f;
+    if (in) {
+      x = mu[3 * i];
+      y = mu[3 * i + 1];
+      z = mu[3 * i + 2];
+      const float c0 = cov[6 * i], c1 = cov[6 * i + 1], c2 = cov[6 * i + 2];
+      const float c3 = cov[6 * i + 3], c4 = cov[6 * i + 4], c5 = cov[6 * i + 5];
+      float nx = 0.f, ny = 0.f, nz = 0.f;
+      if (nrm) {
+        nx = nrm[3 * i];
+        ny = nrm[3 * i + 1];
+        nz = nrm[3 * i + 2];
+      }
+      const bool b = !(finite3(x, y, z) && finite3(c0, c1, c2) && finite3(c3, c4, c5) &&
+                       finite3(nx, ny, nz));
+      bad |= b;
+      float4* r = P + pt_off(i);
+      r[0] = make_float4(x, y, z, c0);
+      r[32] = make_float4(c1, c2, c3, c4);
+      r[64] = make_float4(c5, nx, ny, nz);
+      if (!b) {
+        cm = fmaxf(cm, fmaxf(fmaxf(fmaxf(fabsf(c0), fabsf(c1)), fmaxf(fabsf(c2), fabsf(c3))),
+                             fmaxf(fabsf(c4), fabsf(c5))));
+        const int32_t ox = float_to_ordered(x), oy = float_to_ordered(y), oz = float_to_ordered(z);
+        lox = min(lox, ox); hix = max(hix, ox);
+        loy = min(loy, oy); hiy = max(hiy, oy);
+        loz = min(loz, oz); hiz = max(hiz, oz);
+      }
     }
-    bad = !(finite3(x, y, z) && finite3(c0, c1, c2) && finite3(c3, c4, c5) && finite3(nx, ny, nz));
-    float4* r = P + pt_off(i);
-    r[0] = make_float4(x, y, z, c0);
-    r[32] = make_float4(c1, c2, c3, c4);
-    r[64] = make_float4(c5, nx, ny, nz);
-    cm = fmaxf(fmaxf(fmaxf(fabsf(c0), fabsf(c1)), fmaxf(fabsf(c2), fabsf(c3))),
-               fmaxf(fabsf(c4), fabsf(c5)));
-    if (!bad) {
-      const float p[3] = {x, y, z};
-      for (int a = 0; a < 3; ++a) lo[a] = hi[a] = float_to_ordered(p[a]);
-    } else {
-      cm = 0.f;
+    // the chunk's box of means (points of the chunk only)
+    float bl0 = in ? x : INFINITY, bl1 = in ? y : INFINITY, bl2 = in ? z : INFINITY;
+    float bh0 = in ? x : -INFINITY, bh1 = in ? y : -INFINITY, bh2 = in ? z : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bl0 = fminf(bl0, __shfl_xor_sync(0xffffffffu, bl0, o));
+      bl1 = fminf(bl1, __shfl_xor_sync(0xffffffffu, bl1, o));
+      bl2 = fminf(bl2, __shfl_xor_sync(0xffffffffu, bl2, o));
+      bh0 = fmaxf(bh0, __shfl_xor_sync(0xffffffffu, bh0, o));
+      bh1 = fmaxf(bh1, __shfl_xor_sync(0xffffffffu, bh1, o));
+      bh2 = fmaxf(bh2, __shfl_xor_sync(0xffffffffu, bh2, o));
     }
+    if (lane < 6)
+      chunk_box[6 * ch + lane] = lane == 0 ? bl0 : lane == 1 ? bl1 : lane == 2 ? bl2
+                               : lane == 3 ? bh0 : lane == 4 ? bh1 : bh2;
   }
-  // warp reductions, then one atomic per warp and statistic
+  // warp reductions of the statistics, then one atomic per warp and statistic
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
-      hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
-    }
+    lox = min(lox, __shfl_xor_sync(0xffffffffu, lox, o));
+    loy = min(loy, __shfl_xor_sync(0xffffffffu, loy, o));
+    loz = min(loz, __shfl_xor_sync(0xffffffffu, loz, o));
+    hix = max(hix, __shfl_xor_sync(0xffffffffu, hix, o));
+    hiy = max(hiy, __shfl_xor_sync(0xffffffffu, hiy, o));
+    hiz = max(hiz, __shfl_xor_sync(0xffffffffu, hiz, o));
   }
-  // per-32-point chunk boxes (blocks are 256 threads from the cloud start, so
-  // every warp is exactly one chunk)
-  {
-    float lo3[3], hi3[3];
-    const bool in = i < n;
-    for (int a = 0; a < 3; ++a) {
-      const float v = in ? (a == 0 ? mu[3 * i] : a == 1 ? mu[3 * i + 1] : mu[3 * i + 2]) : 0.f;
-      lo3[a] = in ? v : INFINITY;
-      hi3[a] = in ? v : -INFINITY;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        lo3[a] = fminf(lo3[a], __shfl_xor_sync(0xffffffffu, lo3[a], o));
-        hi3[a] = fmaxf(hi3[a], __shfl_xor_sync(0xffffffffu, hi3[a], o));
-      }
-    const int64_t chunk = i / kChunk;
-    if ((threadIdx.x & 31) < 6 && chunk * kChunk < n)
-      chunk_box[6 * chunk + (threadIdx.x & 31)] =
-          (threadIdx.x & 31) < 3 ? lo3[threadIdx.x & 31] : hi3[(threadIdx.x & 31) - 3];
-  }
-  unsigned anybad = __ballot_sync(0xffffffffu, bad);
-  if ((threadIdx.x & 31) == 0) {
+  const unsigned anybad = __ballot_sync(0xffffffffu, bad);
+  if (lane == 0) {
     if (anybad) atomicOr(stats, 1);
     if (cm > 0.f) atomicMax(reinterpret_cast<uint32_t*>(stats + 1), __float_as_uint(cm));
-    for (int a = 0; a < 3; ++a) {
-      if (lo[a] != INT_MAX) atomicMin(stats + 2 + a, lo[a]);
-      if (hi[a] != INT_MIN) atomicMax(stats + 5 + a, hi[a]);
+    if (lox != INT_MAX) {
+      atomicMin(stats + 2, lox);
+      atomicMin(stats + 3, loy);
+      atomicMin(stats + 4, loz);
+      atomicMax(stats + 5, hix);
+      atomicMax(stats + 6, hiy);
+      atomicMax(stats + 7, hiz);
     }
   }
 }
+
+constexpr int kPackBlocksPerCloud = 16;  // 128 warps per cloud, grid-strided over its chunks
 
 __global__ void k_cloud_pack(const float* __restrict__ mu, const float* __restrict__ cov,
                              const float* __restrict__ nrm, int64_t n, float4* __restrict__ P,
                              float* __restrict__ chunk_box, int32_t* __restrict__ stats) {
-  cloud_pack_body(mu, cov, nrm, n, P, chunk_box, stats);
+  cloud_pack_body(mu, cov, nrm, n, P, chunk_box, stats,
+                  ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+                  ((int64_t)gridDim.x * blockDim.x) >> 5);
 }
 
-// All clouds of a batch in one launch: blockIdx.y = cloud (blocks past a
-// cloud's end exit; the body has no block barrier).
+// All clouds of a batch in one launch: blockIdx.y = cloud.
 __global__ void k_cloud_pack_batch(const PackSeg* __restrict__ segs) {
   const PackSeg sg = segs[blockIdx.y];
-  if ((int64_t)blockIdx.x * blockDim.x >= sg.n) return;
-  cloud_pack_body(sg.mu, sg.cov, sg.nrm, sg.n, sg.P, sg.chunk_box, sg.stats);
+  cloud_pack_body(sg.mu, sg.cov, sg.nrm, sg.n, sg.P, sg.chunk_box, sg.stats,
+                  ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+                  ((int64_t)gridDim.x * blockDim.x) >> 5);
 }
 
 // Both passes aggregate within a warp: lanes holding the same (map, key) --
@@ -608,14 +628,19 @@ inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 
 void launch_cloud_pack(const float* mu, const float* cov, const float* nrm, int64_t n, float4* P,
                        float* chunk_box, int32_t* stats, cudaStream_t stream) {
   if (n <= 0) return;
-  k_cloud_pack<<<grid_for(n, 256), 256, 0, stream>>>(mu, cov, nrm, n, P, chunk_box, stats);
+  const unsigned blocks = std::min<unsigned>(grid_for(n, 256), 148 * 8);  // grid-strided chunks
+  k_cloud_pack<<<blocks, 256, 0, stream>>>(mu, cov, nrm, n, P, chunk_box, stats);
   note_launch();
 }
 
 void launch_cloud_pack_batch(const PackSeg* segs_dev, int64_t count, int64_t max_n,
                              cudaStream_t stream) {
   if (count <= 0 || max_n <= 0) return;
-  dim3 grid(grid_for(max_n, 256), (unsigned)count);
+  // (a batch of many clouds fills the GPU with a few blocks per cloud; one or a
+  // few clouds get up to ~1200 blocks in all)
+  const unsigned per_cloud = std::max<unsigned>(
+      kPackBlocksPerCloud, (unsigned)std::min<int64_t>(148 * 8 / count, grid_for(max_n, 256)));
+  dim3 grid(std::min<unsigned>(grid_for(max_n, 256), per_cloud), (unsigned)count);
   k_cloud_pack_batch<<<grid, 256, 0, stream>>>(segs_dev);
   note_launch();
 }
