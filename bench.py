@@ -78,7 +78,7 @@ def parse():
                     help="e2e: step k+1's upload overlapping step k's compute (default; r02p: "
                          "237 ms vs 367 ms serial per C5 step at 5 steps), or each step's "
                          "upload inside it")
-    ap.add_argument("--e2e-steps", type=int, default=10,
+    ap.add_argument("--e2e-steps", type=int, default=20,
                     help="e2e steps timed (the first step's upload is never overlapped)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
