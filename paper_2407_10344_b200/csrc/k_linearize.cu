@@ -80,15 +80,10 @@ namespace {
 #ifndef GVOX_LIN_FUSEOM
 #define GVOX_LIN_FUSEOM 1
 #endif
-// FAST pipeline: a level no lane of the warp hits is skipped as a whole (one
-// vote per level; warp-uniform branch) (1), or evaluated masked (0)
-#ifndef GVOX_LIN_WSKIP
-#define GVOX_LIN_WSKIP 0
-#endif
-// FAST pipeline: the current point's record gathers are issued before the next
-// point's transform and probes (1; they land during prep) or after (0)
-#ifndef GVOX_LIN_EARLYGATHER
-#define GVOX_LIN_EARLYGATHER 0
+// FAST pipeline: loop unrolled twice with the current / next point's data in
+// alternating register sets (1), or one set copied into the other (0)
+#ifndef GVOX_LIN_UNROLL2
+#define GVOX_LIN_UNROLL2 1
 #endif
 
 
@@ -100,6 +95,10 @@ struct FactorShared {
   double t[3];
   double v[3];
   float Rf[9];
+  // the rotation's columns 0-2, rows 0 and 1, as packed pairs (R0, R3), (R1, R4),
+  // (R2, R5): one 8-byte shared load lands a pair in an aligned register pair,
+  // ready for the packed FMAs of R C R^T (no register moves to form them)
+  f2_t Rp[3];
   const float4* A;  // the tile's chunked point records (B = A + 32, N = A + 64 per chunk)
   const float* cbox;  // the tile's first chunk box (6 floats per chunk)
   int64_t begin, end;
@@ -276,6 +275,8 @@ __device__ __forceinline__ void stage_factor(FactorShared& sh, double* pose_s,
     relative_pose_dev(pose_s, pose_s + 12, sh.R, sh.t, sh.v);
 #pragma unroll
     for (int j = 0; j < 9; ++j) sh.Rf[j] = (float)sh.R[j];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) sh.Rp[j] = pk(sh.Rf[j], sh.Rf[3 + j]);
   }
   __syncthreads();
 }
@@ -310,10 +311,10 @@ __device__ __forceinline__ void transform_point(const FactorShared& sh, const fl
 }
 
 // R C R^T (symmetric) in packed pairs over rows 0/1: M = R C by columns, S = M R^T.
-__device__ __forceinline__ void rcr(const float* R, const float4 a, const float4 b, const float4 c,
-                                    PointData& pd) {
+__device__ __forceinline__ void rcr(const float* R, const f2_t* Rp, const float4 a, const float4 b,
+                                    const float4 c, PointData& pd) {
   const float c00 = a.w, c01 = b.x, c02 = b.y, c11 = b.z, c12 = b.w, c22 = c.x;
-  const f2_t Rc0 = pk(R[0], R[3]), Rc1 = pk(R[1], R[4]), Rc2 = pk(R[2], R[5]);
+  const f2_t Rc0 = Rp[0], Rc1 = Rp[1], Rc2 = Rp[2];  // (R0, R3), (R1, R4), (R2, R5)
   const f2_t Mp0 = fma2(Rc2, bc(c02), fma2(Rc1, bc(c01), mul2(Rc0, bc(c00))));
   const f2_t Mp1 = fma2(Rc2, bc(c12), fma2(Rc1, bc(c11), mul2(Rc0, bc(c01))));
   const f2_t Mp2 = fma2(Rc2, bc(c22), fma2(Rc1, bc(c12), mul2(Rc0, bc(c02))));
@@ -668,10 +669,14 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     issue_l(i_cur, s_lane);
     issue_l(i_nxt, s_lane + kStageBytes);
     cp_async_wait<S - 2>();  // the first live iteration landed
-    PointData pn;
-    int32_t vn[MAXL];
-    bool inv_n = false;  // VALID: the next point is discarded by the P:197 test
-    auto prep = [&](int32_t i, int stg) {
+    // the current and the next point's transform, probe results and P:197
+    // flag: two named sets whose roles alternate (GVOX_LIN_UNROLL2: the loop
+    // is unrolled twice, so no register copy moves the next point's data into
+    // the current one's)
+    PointData pA, pB;
+    int32_t vA[MAXL], vB[MAXL];
+    bool invA = false, invB = false;
+    auto prep = [&](int32_t i, int stg, PointData& pn, int32_t (&vn)[MAXL], bool& inv_n) {
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) vn[l] = -1;
       inv_n = false;
@@ -695,71 +700,72 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
         }
       }
     };
-    prep(i_cur, 0);
     int st = 0;  // stage of the current live iteration
-#pragma unroll 1
-    for (int32_t j = 0; j < nlive; ++j) {
+    // live iteration j: issue slot j + 2's copy, prepare point j + 1 (into the
+    // other set), then this point's level terms and fold
+    auto step = [&](int32_t j, const PointData& pd, const int32_t (&vid)[MAXL], const bool inv,
+                    PointData& pn, int32_t (&vn)[MAXL], bool& inv_n) {
       issue_l(i_nx2, s_lane + (unsigned)(st == 0 ? S - 1 : st - 1) * kStageBytes);  // slot j + 2
       cp_async_wait<S - 2>();                                                        // slot j + 1 landed
       const int cur = st;
       if (++st == S) st = 0;
-      PointData pd = pn;
-      int32_t vid[MAXL];
-#pragma unroll
-      for (int l = 0; l < MAXL; ++l) vid[l] = vn[l];
-      // levels some lane of the warp hits (all lanes converged here)
-      uint32_t lany = (1u << MAXL) - 1u;
-      if (GVOX_LIN_WSKIP) {
-        lany = 0u;
-#pragma unroll
-        for (int l = 0; l < MAXL; ++l) lany |= (__any_sync(0xffffffffu, vid[l] >= 0) ? 1u : 0u) << l;
+      prep(i_nxt, st, pn, vn, inv_n);
+      i_cur = i_nxt;
+      i_nxt = i_nx2;
+      i_nx2 = live_at(j + 3);
+      if (VALID && inv) {  // (only real points are marked)
+        ++ac.n_invisible;
+        return;
       }
-      const bool inv = VALID && inv_n;
+      bool any = false;
+#pragma unroll
+      for (int l = 0; l < MAXL; ++l) any |= vid[l] >= 0;
+      if (!any) return;  // (also every lane without a point: prep left its indices -1)
       // every level's record is loaded unconditionally: a level without a
       // correspondence (index -1) reads the level's all-zero sentinel record
       // at index -1 (masked out in level_term, exactly as zeros)
       float4 v0[MAXL], v1[MAXL];
       float v2[MAXL];
-      auto gather = [&]() {
 #pragma unroll
-        for (int l = 0; l < MAXL; ++l) {
-          if (lany >> l & 1u) {
-            const float4* vp = sh.lv[l].vox + 3 * vid[l];
-            v0[l] = __ldg(vp);
-            v1[l] = __ldg(vp + 1);
-            v2[l] = __ldg(&vp[2].x);
-          }
-        }
-      };
-      if (GVOX_LIN_EARLYGATHER) gather();
-      prep(i_nxt, st);
-      i_cur = i_nxt;
-      i_nxt = i_nx2;
-      i_nx2 = live_at(j + 3);
-      if (VALID && inv) {  // (k < npts: only real points are marked)
-        ++ac.n_invisible;
-        continue;
+      for (int l = 0; l < MAXL; ++l) {
+        const float4* vp = sh.lv[l].vox + 3 * vid[l];
+        v0[l] = __ldg(vp);
+        v1[l] = __ldg(vp + 1);
+        v2[l] = __ldg(&vp[2].x);
       }
-      bool any = false;
-#pragma unroll
-      for (int l = 0; l < MAXL; ++l) any |= vid[l] >= 0;
-      if (!any) continue;  // (also every lane without a point: prep left its indices -1)
-      if (!GVOX_LIN_EARLYGATHER) gather();
       const float4 a = sbuf[warp][cur][0][lane], b = sbuf[warp][cur][1][lane],
                    c = sbuf[warp][cur][2][lane];
-      rcr(sh.Rf, a, b, c, pd);
+      PointData q = pd;  // (R C R^T lands in the point's record)
+      rcr(sh.Rf, sh.Rp, a, b, c, q);
       LevelSum ls;
       ls.Oa = ls.Oc = ls.G = 0;
       ls.o11 = ls.o22 = ls.gz = 0.f;
-      float bx = pd.ex, by = pd.ey, bz = pd.ez;
+      float bx = q.ex, by = q.ey, bz = q.ez;
 #pragma unroll
       for (int l = 0; l < MAXL; ++l) {
-        level_base(pd, l, r0f, bx, by, bz);
-        if (lany >> l & 1u)
-          level_term<MAXL>(ac, ls, pd, v0[l], v1[l], v2[l], l, bx, by, bz, vid[l] >= 0);
+        level_base(q, l, r0f, bx, by, bz);
+        level_term<MAXL>(ac, ls, q, v0[l], v1[l], v2[l], l, bx, by, bz, vid[l] >= 0);
       }
-      if (!error_only) fold_point<MAXL>(ac, ls, pd);
+      if (!error_only) fold_point<MAXL>(ac, ls, q);
+    };
+    prep(i_cur, 0, pA, vA, invA);
+#if GVOX_LIN_UNROLL2
+#pragma unroll 1
+    for (int32_t j = 0; j < nlive; j += 2) {
+      step(j, pA, vA, invA, pB, vB, invB);
+      if (j + 1 >= nlive) break;
+      step(j + 1, pB, vB, invB, pA, vA, invA);
     }
+#else
+#pragma unroll 1
+    for (int32_t j = 0; j < nlive; ++j) {
+      step(j, pA, vA, invA, pB, vB, invB);
+      pA = pB;
+#pragma unroll
+      for (int l = 0; l < MAXL; ++l) vA[l] = vB[l];
+      invA = invB;
+    }
+#endif
     tile_reduce<MAXL>(ac, red, partials, tile);
     return;
   }
@@ -840,7 +846,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       }
       if (!have_rcr) {
         have_rcr = true;
-        rcr(sh.Rf, a, b, c, pd);
+        rcr(sh.Rf, sh.Rp, a, b, c, pd);
       }
 #pragma unroll
       for (int j = 0; j < G; ++j) {

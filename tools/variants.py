@@ -17,9 +17,7 @@ VARIANTS = {
     "lin_incbase": ["GVOX_LIN_INCBASE=1"],
     "lin_b5": ["GVOX_LIN_MINB=5"],
     "lin_nofuse": ["GVOX_LIN_FUSEOM=0"],
-    "lin_wskip": ["GVOX_LIN_WSKIP=1"],
-    "lin_early": ["GVOX_LIN_EARLYGATHER=1"],
-    "lin_early_wskip": ["GVOX_LIN_EARLYGATHER=1", "GVOX_LIN_WSKIP=1"],
+    "lin_nounroll": ["GVOX_LIN_UNROLL2=0"],
     "lin_b6": ["GVOX_LIN_MINB=6"],
     "s3": ["GVOX_LIN_STAGES=3"],
     "nopipe": ["GVOX_LIN_PIPE=0"],
