@@ -867,7 +867,9 @@ def main():
                          "and cross-thread accumulation",
             "stages": stages,
             "rates": rates,
-            "roofline": ({"kernel": "k_linearize", "bound": "alu", "limiter": "instruction issue",
+            "roofline": ({"kernel": "k_linearize", "bound": "alu",
+                          "limiter": "instruction issue and memory latency at 25 % occupancy "
+                                     "(128 registers); HBM and the FP32 pipe are below their peaks",
                           "achieved": issue["achieved"], "peak": issue["peak"], "unit": issue["unit"],
                           "frac": issue["frac"], "traffic": traffic,
                           "peak_derivation": issue["peak_derivation"],
