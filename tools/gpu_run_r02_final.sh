@@ -2,9 +2,9 @@
 # parity-margin records, the C5 bench line, the ncu launch list of the bench
 # command, ncu --set full of the dominant kernel and of the build / screening
 # kernels, the per-config table, 2-rank gloo plumbing runs of bench.py, the
-# NEXT-row benches and the reference arm.  Everything lands in gpurun_out/r02f_*.
+# NEXT-row benches and the reference arm.  Everything lands in gpurun_out/${TAG}_*.
 set -x
-T=${TAG:-r02z}
+T=${TAG:-r02final}
 python __graft_entry__.py > gpurun_out/${T}_build.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo smoke=$? >> gpurun_out/${T}_smoke.log
 rm -f gpurun_out/${T}_margins.jsonl
