@@ -191,7 +191,7 @@ struct BuildSeg {
   ulonglong2* tmp_slots[GVOX_MAX_LEVELS];  // hash levels: temp tables (capacity tmp_mask+1)
   uint64_t tmp_mask;
   int32_t tmp_shift;
-  int32_t pad;
+  int32_t lift;  // 1: only level 0 accumulated from the points, coarser levels lifted (k_build_lift)
   uint64_t* keys_by_idx[GVOX_MAX_LEVELS];  // [n] workspace: key of voxel idx
   int32_t* counter;         // [levels] voxel counts (atomic)
   // sync-free builds (acc sized by upper bounds before the insert): the
@@ -226,7 +226,6 @@ void launch_build_accum(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int
 void launch_build_lift(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int64_t num_segs,
                        int levels, const int64_t* max_level_voxels, double r0,
                        unsigned long long* acc, cudaStream_t stream);
-bool build_lift_enabled();
 
 // phase 3: per voxel, finalize the record and insert into the final table.
 struct FinalSeg {

@@ -861,6 +861,12 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   // exactly).  A large chunk reads the counts back once and sizes exactly.
   bool nosync = total <= kNoSyncBuildPoints;
   if (const char* e = std::getenv("GVOX_BUILD_NOSYNC")) nosync = std::atoi(e) != 0;
+  // Lifted accumulation (level 0 from the points, every coarser level from the
+  // voxels below it, k_build_lift) pays on large chunks (C5: 17.96 -> 14.95 ms);
+  // small ones (odometry frames) are launch-bound and accumulate every level
+  // from the points in one kernel.  GVOX_BUILD_LIFT=0/1 overrides.
+  bool lift = L > 1 && total > kNoSyncBuildPoints;
+  if (const char* e = std::getenv("GVOX_BUILD_LIFT")) lift = L > 1 && std::atoi(e) != 0;
   for (int64_t s = 0; s < count; ++s) {
     const gvox_cloud* c = clouds[s];
     if (c->n <= 0) continue;
@@ -905,6 +911,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     g.pl_offset = seg_start[s] * L;
     g.tmp_mask = tcap[s] - 1;
     g.tmp_shift = shift_for_capacity(tcap[s]);
+    g.lift = lift ? 1 : 0;
     int hslot = 0;
     for (int l = 0; l < L; ++l) {
       const LevelPlan& p = plan[s * L + l];
@@ -1049,7 +1056,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       a.acc_offset[l] = vacc;
       // lifted builds: one offset scale for every level (the coarsest level's),
       // so k_build_lift moves a voxel's sums into its parent exactly
-      a.mu_scale[l] = std::ldexp(1.0, F) / (build_lift_enabled() ? std::ldexp(r0, L - 1) : r);
+      a.mu_scale[l] = std::ldexp(1.0, F) / (lift ? std::ldexp(r0, L - 1) : r);
       if (nosync) {
         bseg[s].acc = (unsigned long long*)(b1 + o_acc);
         bseg[s].acc_offset[l] = vacc;
@@ -1137,8 +1144,9 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     for (int64_t s2 = 0; s2 < count; ++s2)
       for (int l = 0; l < L; ++l) maxv[l] = std::max<int64_t>(maxv[l], vcap[s2 * L + l]);
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
-    launch_build_lift((const BuildSeg*)(b0 + o_bseg), (const AccumSeg*)(ab + o_aseg), count, L,
-                      maxv.data(), r0, (unsigned long long*)(b1 + o_acc), ctx->stream);
+    if (lift)
+      launch_build_lift((const BuildSeg*)(b0 + o_bseg), (const AccumSeg*)(ab + o_aseg), count, L,
+                        maxv.data(), r0, (unsigned long long*)(b1 + o_acc), ctx->stream);
   }
   CK_LAUNCH("voxelmap lift");
   {

@@ -166,11 +166,6 @@ __global__ void k_cloud_pack_batch(const PackSeg* __restrict__ segs) {
 #ifndef GVOX_ACC_MAXRUN
 #define GVOX_ACC_MAXRUN 1
 #endif
-// accumulate only level 0 from the points and derive every coarser level from
-// the one below it (k_build_lift), or every level from the points (0)
-#ifndef GVOX_ACC_LIFT
-#define GVOX_ACC_LIFT 1
-#endif
 
 template <int kMaxL>
 __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const BuildSeg* __restrict__ segs, int levels, double r0,
@@ -287,7 +282,7 @@ __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const Build
     const int32_t hl = __shfl_sync(0xffffffffu, h_out[l], leader[l]);
     const bool inr = key[l] < (1ull << 63);
     // (lifted builds accumulate only level 0 from the points)
-    if (valid && (!GVOX_ACC_LIFT || l == 0)) pslot[sg.pl_offset + k * levels + l] = inr ? hl : -1;
+    if (valid && (!sg.lift || l == 0)) pslot[sg.pl_offset + k * levels + l] = inr ? hl : -1;
   }
 }
 
@@ -330,7 +325,7 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
     cov_hi[j] = (int)((long long)f >> 24);
   }
 #endif
-  for (int l = 0; l < (GVOX_ACC_LIFT ? 1 : levels); ++l) {
+  for (int l = 0; l < (bs.lift ? 1 : levels); ++l) {
     int32_t sl = valid ? pslot[sg.pl_offset + k * levels + l] : -1;
     int32_t idx;
     if (bs.box[l].dense) {
@@ -671,7 +666,7 @@ void launch_build_accum(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int
 void launch_build_lift(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int64_t num_segs,
                        int levels, const int64_t* max_level_voxels, double r0,
                        unsigned long long* acc, cudaStream_t stream) {
-  if (!GVOX_ACC_LIFT || num_segs <= 0) return;
+  if (num_segs <= 0) return;
   for (int l = 0; l + 1 < levels; ++l) {
     if (max_level_voxels[l] <= 0) continue;
     dim3 grid(grid_for(max_level_voxels[l], 256), (unsigned)num_segs);
@@ -679,7 +674,6 @@ void launch_build_lift(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int6
     note_launch();
   }
 }
-bool build_lift_enabled() { return GVOX_ACC_LIFT != 0; }
 
 void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs, int64_t max_seg_voxels,
                            const unsigned long long* acc, cudaStream_t stream) {

@@ -727,3 +727,34 @@ def test_sync_free_build_equals_counted(gv, ctx, monkeypatch, hash_levels):
         monkeypatch.setenv("GVOX_BUILD_NOSYNC", flag)
         with pytest.raises(gv.GvoxError, match="GVOX_ERR_RANGE"):
             gv.create_voxelmap(ctx, far, 1.0, 1)
+
+
+@pytest.mark.parametrize("nosync", ["0", "1"])
+def test_lifted_accumulation_equals_direct(gv, ctx, monkeypatch, nosync):
+    """Lifted builds (level 0 accumulated from the points, every coarser level
+    from the voxels below it -- large chunks by default) and direct builds
+    (every level from the points) give the same voxels and counts bit for bit
+    and the same statistics up to the fixed-point scale (one scale for every
+    level vs one per level: ~2^-40 r), for counted and sync-free builds."""
+    sc = synth.global_scene(n_submaps=6, n_points=20000, half_blocks=2, factor_dist=40.0,
+                            cand_dist=60.0)
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    monkeypatch.setenv("GVOX_BUILD_NOSYNC", nosync)
+    out = {}
+    for lift in ("1", "0"):
+        monkeypatch.setenv("GVOX_BUILD_LIFT", lift)
+        out[lift] = gv.create_voxelmaps(ctx, [clouds[int(c)] for c in sc.map_clouds], sc.r0, sc.levels)
+    for a, b in zip(out["1"], out["0"]):
+        for l in range(sc.levels):
+            ka, ma, ca, na = a.export(ctx, l)
+            kb, mb, cb, nb = b.export(ctx, l)
+            assert np.array_equal(ka, kb) and np.array_equal(na, nb)
+            r = sc.r0 * 2 ** l
+            np.testing.assert_allclose(ma, mb, rtol=0, atol=1e-6 * r)
+            np.testing.assert_allclose(ca, cb, rtol=0, atol=1e-6 * np.abs(cb).max())
+    f = sc.factors.copy()
+    f[:, 4] = 0
+    r1 = gv.linearize_batch(ctx, clouds, out["1"], f, sc.poses)
+    r0 = gv.linearize_batch(ctx, clouds, out["0"], f, sc.poses)
+    assert np.array_equal(r1["inliers"], r0["inliers"])
+    np.testing.assert_allclose(r1["error"], r0["error"], rtol=1e-5)

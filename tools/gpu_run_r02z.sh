@@ -1,0 +1,7 @@
+# r02z: lifted accumulation only for large chunks; tests + small configs
+set -x
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/r02z_smoke.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/r02z_pytest_gpu.log 2>&1
+for c in C1 C2 C3; do
+  timeout 300 python bench.py --config $c --steps 50 --no-cpu-baseline --per-call-runs 20 2>/dev/null | python -c "import sys,json; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); s=d['stages']; print('$c', 'step', round(d['ms_per_step'],4), 'lin', round(s['linearize']['ms_per_step'],4), 'build', round(s['build']['ms_per_step'],4), 'ovl', round(s['overlap']['ms_per_step'],4), 'e2e', round(d['e2e']['ms_per_step'],4), 'per_call', round(d['per_call']['ms_median'],4))" >> gpurun_out/r02z_configs.log
+done

@@ -56,7 +56,6 @@ VARIANTS = {
     "acc_seg6": ["GVOX_ACC_SEG_MIN=6"],
     "acc_noseg": ["GVOX_ACC_SEG_MIN=99"],
     "acc_base": [],
-    "acc_nolift": ["GVOX_ACC_LIFT=0"],
     "acc_seg2": ["GVOX_ACC_SEG_MIN=2"],
     "acc_seg3": ["GVOX_ACC_SEG_MIN=3"],
     "acc_nohoist": ["GVOX_ACC_HOIST=0"],
