@@ -372,14 +372,16 @@ gvox_status gvox_linearize_batch_accum(gvox_ctx* ctx, const gvox_cloud* const* c
    capacity num_candidates) is the k-th selected candidate's record,
    k < *num_selected (host out).  selected_host (optional, HOST,
    num_candidates bytes) receives a copy of the decisions.  One H2D (the
-   candidate table), one 8-byte D2H of the selected and tile counts (plus the
-   optional decision copy) before the launch; returns with the linearization
-   enqueued on ctx's stream.  The kernel variant (FAST all-dense / generic) is
-   chosen on the host from ALL candidates, before the decisions exist: one
-   unselected candidate with a hash level or non-dyadic map sends the batch to
-   the generic kernel.  The records are the same either way (the two variants
-   are bitwise equal, tested), only the speed differs; tile partials are sized
-   for every candidate.  Errors as gvox_linearize_batch_accum. */
+   candidate table), one 16-byte D2H before the launch (the selected and tile
+   counts, and the kernel class of the SELECTED candidates -- OR of their
+   hash-level / non-FAST / validation bits and their maximum level count,
+   reduced on the device during the compaction -- plus the optional decision
+   copy); returns with the linearization enqueued on ctx's stream.  The kernel
+   variant (FAST all-dense / generic) is therefore the one
+   gvox_linearize_batch_accum picks for the selected list: an unselected
+   candidate with a hash level or a non-dyadic map does not change it.  Tile
+   partials are sized for every candidate.  Errors as
+   gvox_linearize_batch_accum. */
 gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* const* clouds,
                                               int64_t num_clouds, const gvox_map* const* maps,
                                               int64_t num_maps, const gvox_factor* candidates,
@@ -543,6 +545,16 @@ const char* gvox_last_error(void);
 /* Kernel launches issued by this thread since the last reset (evidence for
    bench.py's gpu_launches). */
 int64_t gvox_launch_count(int reset);
+/* The k_linearize instantiation this thread launched last (introspection for
+   tests and tools; 0 before any linearization): GVOX_LINVAR_FAST (the
+   specialised 3-level dyadic kernel), GVOX_LINVAR_DENSE (all levels dense
+   grids), GVOX_LINVAR_VALID (P:197 visibility test compiled in) | the kernel's
+   level capacity << 8.  The records do not depend on it (the variants are
+   bitwise equal, tested); only the speed does. */
+#define GVOX_LINVAR_FAST 1
+#define GVOX_LINVAR_DENSE 2
+#define GVOX_LINVAR_VALID 4
+int32_t gvox_last_linearize_variant(void);
 const char* gvox_version(void);
 
 #ifdef __cplusplus

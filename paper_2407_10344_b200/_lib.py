@@ -67,7 +67,8 @@ SYMBOLS = [
     "gvox_register_batch", "gvox_overlap_union", "gvox_keyframe_update",
     "gvox_keyframe_insert_test", "gvox_keyframe_update_counts", "gvox_knn",
     "gvox_estimate_covariances", "gvox_solve_global", "gvox_optimize_global",
-    "gvox_status_string", "gvox_last_error", "gvox_launch_count", "gvox_version",
+    "gvox_status_string", "gvox_last_error", "gvox_launch_count", "gvox_last_linearize_variant",
+    "gvox_version",
 ]
 
 
@@ -125,6 +126,7 @@ def lib():
         "gvox_status_string": (ctypes.c_char_p, [I32]),
         "gvox_last_error": (ctypes.c_char_p, []),
         "gvox_launch_count": (I64, [I32]),
+        "gvox_last_linearize_variant": (I32, []),
         "gvox_version": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -143,6 +145,11 @@ def check(status: int):
 
 def launch_count(reset: bool = False) -> int:
     return int(lib().gvox_launch_count(int(reset)))
+
+
+def last_linearize_variant() -> int:
+    """GVOX_LINVAR_* bits | level capacity << 8 of the last k_linearize launch."""
+    return int(lib().gvox_last_linearize_variant())
 
 
 def version() -> str:

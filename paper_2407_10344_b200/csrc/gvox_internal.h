@@ -187,7 +187,8 @@ struct LevelBox {
 struct BuildSeg {
   const float4* A;          // cloud means (+C.xx)
   int64_t n;                // points
-  int64_t pl_offset;        // offset of this cloud's (point, level) records
+  int64_t pl_offset;        // this cloud's first point in the level-major (level, point) slots
+  int64_t pl_stride;        // slots per level (the chunk's points): coalesced per level
   ulonglong2* tmp_slots[GVOX_MAX_LEVELS];  // hash levels: temp tables (capacity tmp_mask+1)
   uint64_t tmp_mask;
   int32_t tmp_shift;
@@ -214,6 +215,7 @@ struct AccumSeg {
   const float4* N;
   int64_t n;
   int64_t pl_offset;
+  int64_t pl_stride;
   int64_t acc_offset[GVOX_MAX_LEVELS];  // first voxel of (seg, level) in acc[]
   double mu_scale[GVOX_MAX_LEVELS];     // offset scale: 2^F / r_l, or (lifted builds) 2^F / r_(L-1) for every l
   double cov_scale;                     // 2^(F - e_c), 2^e_c >= max |C_ij| of the cloud
@@ -231,6 +233,7 @@ void launch_build_lift(const BuildSeg* bsegs_dev, const AccumSeg* segs_dev, int6
 struct FinalSeg {
   int64_t acc_offset;       // first voxel in acc[] / keys
   const int32_t* nvox;      // device: the level's voxel count (the insert's counter)
+  int32_t* nvox_out;        // device: the map's copy of it (written by the finalize)
   const uint64_t* keys_by_idx;
   double r;
   double mu_scale;
@@ -404,11 +407,15 @@ void launch_sum_error(const gvox_factor_accum* acc, int64_t n, double* out, cuda
 void launch_tile_map(const int32_t* tile_start, int64_t num_items, int32_t* tile_owner,
                      cudaStream_t stream);
 // compact the selected candidates (device plan of gvox_linearize_batch_accum_select)
-void launch_select_plan(const uint8_t* selected, const int32_t* ntiles, const FactorDev* factors,
-                        int64_t num_cand, FactorDev* factors_c, int32_t* tile_start_c,
-                        int32_t* counts, int2* block_tot /* ceil(num_cand / 1024) */,
-                        cudaStream_t stream);
+// counts (4 int32): {selected, their tiles, OR of their class bits, max of their levels};
+// cls: per-candidate kernel-class byte (gvox_runtime.cu kCls*, levels << 4)
+void launch_select_plan(const uint8_t* selected, const int32_t* ntiles, const uint8_t* cls,
+                        const FactorDev* factors, int64_t num_cand, FactorDev* factors_c,
+                        int32_t* tile_start_c, int32_t* counts,
+                        int2* block_tot /* ceil(num_cand / 1024) */, cudaStream_t stream);
 
 void note_launch();
+// the k_linearize instantiation just launched: GVOX_LINVAR_* bits | MAXL << 8
+void note_linearize_variant(int32_t v);
 
 }  // namespace gvox

@@ -42,6 +42,7 @@ struct DebugClock {
 namespace {
 thread_local std::string g_last_error;
 thread_local int64_t g_launches = 0;
+thread_local int32_t g_lin_variant = 0;  // the last k_linearize instantiation (gvox_last_linearize_variant)
 
 gvox_status fail(gvox_status s, const char* fmt, ...) {
   char buf[512];
@@ -250,6 +251,7 @@ gvox_status grid_arena_take(const std::shared_ptr<GridPool>& pool, size_t bytes,
 
 namespace gvox {
 void note_launch() { ++g_launches; }
+void note_linearize_variant(int32_t v) { g_lin_variant = v; }
 }  // namespace gvox
 
 // ------------------------------------------------------------------ handles
@@ -380,6 +382,14 @@ gvox_status h2d_small(gvox_ctx* ctx, void* dst, const void* pinned_src, size_t b
     CK(cudaMemcpyAsync(dst, pinned_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
   }
   return GVOX_OK;
+}
+
+// Small batches carry their tile -> owner map in the input block (filled on the
+// host; no k_tile_map launch on the critical path of an odometry-sized call).
+constexpr int64_t kHostTileMapMax = 4096;
+void fill_tile_map(const int32_t* tstart, int64_t n, int32_t* tm) {
+  for (int64_t f = 0; f < n; ++f)
+    for (int32_t t = tstart[f]; t < tstart[f + 1]; ++t) tm[t] = (int32_t)f;
 }
 
 // H2D out of the slot pin_reserve handed out last
@@ -892,8 +902,10 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   const size_t tmp_bytes = lay.size;  // temp tables first: one 0xFF memset
   for (int64_t s = 0; s < count; ++s) o_keys[s] = lay.add((size_t)clouds[s]->n * 8 * L);
   size_t o_pslot = lay.add((size_t)total * L * 4);
+  // the counters and the insert descriptors: ONE upload (zeros, then BuildSeg[])
   size_t o_cnt = lay.add((size_t)count * L * 4 + 4);
   size_t o_bseg = lay.add(sizeof(BuildSeg) * count);
+  const size_t ins_bytes = o_bseg + sizeof(BuildSeg) * count - o_cnt;
   void* ws0 = nullptr;
   st = ws_reserve(ctx, 0, lay.size, &ws0);
   if (st) return st;
@@ -908,7 +920,8 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     std::memset(&g, 0, sizeof(g));
     g.A = clouds[s]->desc.A;
     g.n = clouds[s]->n;
-    g.pl_offset = seg_start[s] * L;
+    g.pl_offset = seg_start[s];
+    g.pl_stride = total;
     g.tmp_mask = tcap[s] - 1;
     g.tmp_shift = shift_for_capacity(tcap[s]);
     g.lift = lift ? 1 : 0;
@@ -930,7 +943,6 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     g.counter = d_cnt + s * L;
   }
   if (tmp_bytes) CK(cudaMemsetAsync(b0, 0xFF, tmp_bytes, ctx->stream));
-  CK(cudaMemsetAsync(d_cnt, 0, (size_t)count * L * 4 + 4, ctx->stream));
 
   // voxel capacity of every (map, level): the point count (sync-free) or the
   // exact count (counted, after the readback)
@@ -938,10 +950,11 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   std::vector<int32_t> hcnt((size_t)count * L + 1, 0);
   auto launch_insert = [&]() -> gvox_status {
     void* hp = nullptr;
-    gvox_status st2 = pin_b_reserve(ctx, 0, sizeof(BuildSeg) * count, &hp);
+    gvox_status st2 = pin_b_reserve(ctx, 0, ins_bytes, &hp);
     if (st2) return st2;
-    std::memcpy(hp, bseg.data(), sizeof(BuildSeg) * count);
-    st2 = pin_b_upload(ctx, 0, b0 + o_bseg, sizeof(BuildSeg) * count);
+    std::memset(hp, 0, o_bseg - o_cnt);  // the voxel counters and the range flag start at 0
+    std::memcpy((char*)hp + (o_bseg - o_cnt), bseg.data(), sizeof(BuildSeg) * count);
+    st2 = pin_b_upload(ctx, 0, b0 + o_cnt, ins_bytes);
     if (st2) return st2;
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
     launch_build_insert((const BuildSeg*)(b0 + o_bseg), count, max_pts, L, r0, dyadic,
@@ -1033,7 +1046,8 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     a.B = c->desc.B;
     a.N = c->desc.N;
     a.n = c->n;
-    a.pl_offset = seg_start[s] * L;
+    a.pl_offset = seg_start[s];
+    a.pl_stride = total;
     a.cov_scale = std::ldexp(1.0, F - ec);
     MapDev& md = mdesc[s];
     std::memset(&md, 0, sizeof(md));
@@ -1064,7 +1078,8 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       FinalSeg& f = fseg[s * L + l];
       std::memset(&f, 0, sizeof(f));
       f.acc_offset = vacc;
-      f.nvox = d_counts + s * L + l;
+      f.nvox = d_cnt + s * L + l;  // the insert's counter (this build's workspace)
+      f.nvox_out = const_cast<int32_t*>(d_counts) + s * L + l;  // the map's copy
       f.keys_by_idx = bseg[s].keys_by_idx[l];
       f.r = r;
       f.mu_scale = a.mu_scale[l];
@@ -1127,9 +1142,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   if (nosync) {
     st = launch_insert();  // (its zeroing of the accumulators needs bseg's acc fields)
     if (st) return st;
-    // the maps' counts: the insert's counters, copied into the record arena
-    CK(cudaMemcpyAsync(ab + o_counts, d_cnt, (size_t)count * L * 4, cudaMemcpyDeviceToDevice,
-                       ctx->stream));
+    // (the maps' counts: copied from the insert's counters by the finalize)
     dbg.lap("insert enqueued (sync-free)");
   }
   {
@@ -1388,6 +1401,8 @@ gvox_status overlap_impl(const char* fn, gvox_ctx* ctx, const gvox_cloud* const*
   size_t o_pose = lay.add(96 * num_poses);
   size_t o_pair = lay.add(sizeof(PairDev) * num_pairs);
   size_t o_ts = lay.add(4 * tstart.size());
+  const bool host_tm = counts && T <= kHostTileMapMax;  // (selection: no tiles)
+  size_t o_tm = lay.add(host_tm ? 4 * (size_t)T : 0);
   size_t o_cl = lay.add(8 * num_clouds);
   size_t o_mp = lay.add(8 * num_maps);
   size_t in_bytes = lay.size;
@@ -1398,11 +1413,12 @@ gvox_status overlap_impl(const char* fn, gvox_ctx* ctx, const gvox_cloud* const*
   std::memcpy(hp + o_pose, poses, 96 * num_poses);
   std::memcpy(hp + o_pair, pairs, sizeof(PairDev) * num_pairs);
   std::memcpy(hp + o_ts, tstart.data(), 4 * tstart.size());
+  if (host_tm) fill_tile_map(tstart.data(), num_pairs, (int32_t*)(hp + o_tm));
   for (int64_t i = 0; i < num_clouds; ++i) ((const CloudDev**)(hp + o_cl))[i] = clouds[i] ? clouds[i]->dev : nullptr;
   for (int64_t i = 0; i < num_maps; ++i) ((const MapDev**)(hp + o_mp))[i] = maps[i] ? maps[i]->dev : nullptr;
   Layout wl;
   size_t o_in = wl.add(in_bytes);
-  size_t o_tp = wl.add(4 * (size_t)std::max<int64_t>(T, 1));
+  size_t o_tp = wl.add(host_tm ? 0 : 4 * (size_t)std::max<int64_t>(T, 1));
   size_t o_out = wl.add(4 * num_pairs);
   void* ws = nullptr;
   st = ws_reserve(ctx, 0, wl.size, &ws);
@@ -1420,10 +1436,11 @@ gvox_status overlap_impl(const char* fn, gvox_ctx* ctx, const gvox_cloud* const*
   if (counts) {
     int32_t* dcounts = mem == GVOX_DEVICE ? counts : (int32_t*)(wb + o_out);
     CK(cudaMemsetAsync(dcounts, 0, 4 * num_pairs, ctx->stream));
-    launch_tile_map((const int32_t*)(din + o_ts), num_pairs, (int32_t*)(wb + o_tp), ctx->stream);
+    int32_t* dtm = host_tm ? (int32_t*)(din + o_tm) : (int32_t*)(wb + o_tp);
+    if (!host_tm) launch_tile_map((const int32_t*)(din + o_ts), num_pairs, dtm, ctx->stream);
     TimerScope ts(ctx, GVOX_TIMER_OVERLAP);
     launch_overlap(dcl, dmp, dpairs, (const int32_t*)(din + o_ts), num_pairs, T, tile_pts, dposes,
-                   level, (int32_t*)(wb + o_tp), dcounts, all_dense, ctx->stream);
+                   level, dtm, dcounts, all_dense, ctx->stream);
     dout = dcounts;
     out_bytes = 4 * num_pairs;
   } else {
@@ -1502,6 +1519,10 @@ gvox_status validate_factors(const char* fn, const gvox_cloud* const* clouds, in
 // Tile plan of a linearization batch: tiles of tile_pts consecutive points of
 // one factor; tile_pts = 256 * ppt, ppt = pow2 <= n / 2048 in [1, 128] (a
 // function of the factor alone: bitwise batch/shard independence).
+// per-factor kernel-class bits (gvox_linearize_batch_accum_select: reduced over
+// the SELECTED candidates on the device); levels in the high nibble
+constexpr uint8_t kClsHash = 1, kClsNotFast = 2, kClsValidate = 4;
+
 struct LinPlan {
   std::vector<int32_t> tstart;
   std::vector<FactorDev> fdev;
@@ -1514,7 +1535,7 @@ struct LinPlan {
 gvox_status plan_linearize(const char* fn, const gvox_cloud* const* clouds,
                            const gvox_map* const* maps, const gvox_factor* factors,
                            int64_t num_factors, bool fast_allowed, LinPlan* p,
-                           int min_tiles = GVOX_TILE_MIN_TILES) {
+                           int min_tiles = GVOX_TILE_MIN_TILES, uint8_t* cls = nullptr) {
   p->fast = fast_allowed;
   p->tstart.assign(num_factors + 1, 0);
   p->fdev.resize(num_factors);
@@ -1522,6 +1543,12 @@ gvox_status plan_linearize(const char* fn, const gvox_cloud* const* clouds,
   for (int64_t f = 0; f < num_factors; ++f) {
     const gvox_factor& q = factors[f];
     const gvox_map* m = maps[q.target_map];
+    if (cls) {  // this factor's kernel class alone (the screened batch decides on the device)
+      bool dense = true;
+      for (int l = 0; l < m->levels; ++l) dense = dense && m->desc.lv[l].dense;
+      cls[f] = (uint8_t)((dense ? 0 : kClsHash) | (m->levels == 3 && m->desc.dyadic ? 0 : kClsNotFast) |
+                         ((q.flags & GVOX_F_VALIDATE_SURFACE) ? kClsValidate : 0) | (m->levels << 4));
+    }
     p->max_levels = std::max(p->max_levels, m->levels);
     for (int l = 0; l < m->levels; ++l) p->all_dense = p->all_dense && m->desc.lv[l].dense;
     p->fast = p->fast && m->levels == 3 && m->desc.dyadic;
@@ -1579,6 +1606,8 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
   size_t o_pose = lay.add(96 * num_poses);
   size_t o_fac = lay.add(sizeof(FactorDev) * num_factors);
   size_t o_ts = lay.add(4 * (num_factors + 1));
+  const bool host_tm = T <= kHostTileMapMax;
+  size_t o_tm = lay.add(host_tm ? 4 * (size_t)T : 0);
   size_t o_cl = lay.add(8 * num_clouds);
   size_t o_mp = lay.add(8 * num_maps);
   const size_t in_bytes = lay.size;
@@ -1589,13 +1618,14 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
   std::memcpy(hp + o_pose, poses, 96 * num_poses);
   std::memcpy(hp + o_fac, fdev.data(), sizeof(FactorDev) * num_factors);
   std::memcpy(hp + o_ts, tstart.data(), 4 * (num_factors + 1));
+  if (host_tm) fill_tile_map(tstart.data(), num_factors, (int32_t*)(hp + o_tm));
   for (int64_t i = 0; i < num_clouds; ++i) ((const CloudDev**)(hp + o_cl))[i] = clouds[i] ? clouds[i]->dev : nullptr;
   for (int64_t i = 0; i < num_maps; ++i) ((const MapDev**)(hp + o_mp))[i] = maps[i] ? maps[i]->dev : nullptr;
   // ---- device workspace
   Layout wl;
   size_t o_in = wl.add(in_bytes);
   size_t o_part = wl.add(8 * kPartialStride * (size_t)std::max<int64_t>(T, 1));
-  size_t o_tf = wl.add(4 * (size_t)std::max<int64_t>(T, 1));
+  size_t o_tf = wl.add(host_tm ? 0 : 4 * (size_t)std::max<int64_t>(T, 1));
   size_t out_rec = out_full ? sizeof(gvox_linear_factor) : sizeof(gvox_factor_accum);
   size_t o_out = wl.add(mem == GVOX_HOST ? out_rec * num_factors : 0);
   void* ws = nullptr;
@@ -1606,13 +1636,14 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
   if (st) return st;
   char* din = wb + o_in;
   void* dout = mem == GVOX_DEVICE ? (out_full ? (void*)out_full : (void*)out_accum) : (void*)(wb + o_out);
-  launch_tile_map((const int32_t*)(din + o_ts), num_factors, (int32_t*)(wb + o_tf), ctx->stream);
+  int32_t* dtf = host_tm ? (int32_t*)(din + o_tm) : (int32_t*)(wb + o_tf);
+  if (!host_tm) launch_tile_map((const int32_t*)(din + o_ts), num_factors, dtf, ctx->stream);
   {
     TimerScope ts(ctx, GVOX_TIMER_LINEARIZE);
     launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp),
                      (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
                      0, max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
-                     (int32_t*)(wb + o_tf), corr_dump, all_dense, fast, plan.validate,
+                     dtf, corr_dump, all_dense, fast, plan.validate,
                      ctx->stream);
   }
   CK_LAUNCH("linearize");
@@ -1677,8 +1708,10 @@ gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* c
   // host plan of every candidate (tiles are a function of the factor alone, so
   // the selected subset's tiles are exactly gvox_linearize_batch_accum's)
   LinPlan plan;
+  std::vector<uint8_t> cls(num_candidates);
   st = plan_linearize(fn, clouds, maps, candidates, num_candidates,
-                      std::getenv("GVOX_LIN_GENERIC") == nullptr, &plan);
+                      std::getenv("GVOX_LIN_GENERIC") == nullptr, &plan, GVOX_TILE_MIN_TILES,
+                      cls.data());
   if (st) return st;
   const int64_t T_all = plan.tstart[num_candidates];
   std::vector<int32_t> ntiles(num_candidates);
@@ -1688,6 +1721,7 @@ gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* c
   size_t o_pose = lay.add(96 * num_poses);
   size_t o_fac = lay.add(sizeof(FactorDev) * num_candidates);
   size_t o_nt = lay.add(4 * num_candidates);
+  size_t o_cls = lay.add(num_candidates);
   size_t o_cl = lay.add(8 * num_clouds);
   size_t o_mp = lay.add(8 * num_maps);
   const size_t in_bytes = lay.size;
@@ -1698,6 +1732,7 @@ gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* c
   std::memcpy(hp + o_pose, poses, 96 * num_poses);
   std::memcpy(hp + o_fac, plan.fdev.data(), sizeof(FactorDev) * num_candidates);
   std::memcpy(hp + o_nt, ntiles.data(), 4 * num_candidates);
+  std::memcpy(hp + o_cls, cls.data(), num_candidates);
   for (int64_t i = 0; i < num_clouds; ++i) ((const CloudDev**)(hp + o_cl))[i] = clouds[i] ? clouds[i]->dev : nullptr;
   for (int64_t i = 0; i < num_maps; ++i) ((const MapDev**)(hp + o_mp))[i] = maps[i] ? maps[i]->dev : nullptr;
   // ---- device workspace (partials and tile map sized for every candidate)
@@ -1707,7 +1742,7 @@ gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* c
   size_t o_tf = wl.add(4 * (size_t)std::max<int64_t>(T_all, 1));
   size_t o_fc = wl.add(sizeof(FactorDev) * num_candidates);
   size_t o_tsc = wl.add(4 * (num_candidates + 1));
-  size_t o_cnt = wl.add(8);
+  size_t o_cnt = wl.add(16);
   size_t o_bt = wl.add(8 * ((num_candidates + 1023) / 1024));
   void* ws = nullptr;
   st = ws_reserve(ctx, 0, wl.size, &ws);
@@ -1719,21 +1754,30 @@ gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* c
   FactorDev* fc = (FactorDev*)(wb + o_fc);
   int32_t* tsc = (int32_t*)(wb + o_tsc);
   int32_t* dcnt = (int32_t*)(wb + o_cnt);
-  launch_select_plan(selected, (const int32_t*)(din + o_nt), (const FactorDev*)(din + o_fac),
-                     num_candidates, fc, tsc, dcnt, (int2*)(wb + o_bt), ctx->stream);
+  launch_select_plan(selected, (const int32_t*)(din + o_nt), (const uint8_t*)(din + o_cls),
+                     (const FactorDev*)(din + o_fac), num_candidates, fc, tsc, dcnt,
+                     (int2*)(wb + o_bt), ctx->stream);
   CK_LAUNCH("select plan");
-  // the one readback before the launch: {S, T} (the grid size)
+  // the one readback before the launch: {S, T} (the grid size) and the kernel
+  // class of the selected candidates {OR of their class bits, max levels}
   if (!ctx->pin_counts) {
     cudaError_t e = cudaHostAlloc((void**)&ctx->pin_counts, 64, cudaHostAllocDefault);
     if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
   }
-  CK(cudaMemcpyAsync(ctx->pin_counts, dcnt, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->pin_counts, dcnt, 16, cudaMemcpyDeviceToHost, ctx->stream));
   if (selected_host)
     CK(cudaMemcpyAsync(selected_host, selected, num_candidates, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   const int64_t S = ctx->pin_counts[0], T = ctx->pin_counts[1];
+  const int32_t cls_or = ctx->pin_counts[2], sel_levels = ctx->pin_counts[3];
   *num_selected = S;
   if (S == 0) return GVOX_OK;
+  // the kernel variant of the SELECTED batch (as gvox_linearize_batch_accum would
+  // choose it on that list), not of every candidate
+  plan.fast = std::getenv("GVOX_LIN_GENERIC") == nullptr && !(cls_or & kClsNotFast);
+  plan.all_dense = !(cls_or & kClsHash);
+  plan.validate = (cls_or & kClsValidate) != 0;
+  plan.max_levels = std::max(1, sel_levels);
   launch_tile_map(tsc, S, (int32_t*)(wb + o_tf), ctx->stream);
   {
     TimerScope ts(ctx, GVOX_TIMER_LINEARIZE);
@@ -2812,6 +2856,8 @@ int64_t gvox_launch_count(int reset) {
   if (reset) g_launches = 0;
   return v;
 }
+
+int32_t gvox_last_linearize_variant(void) { return g_lin_variant; }
 
 const char* gvox_version(void) { return "gvox 0.1 (sm_100a)"; }
 

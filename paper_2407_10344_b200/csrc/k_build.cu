@@ -18,6 +18,9 @@
 #include <climits>
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
 
 #include "k_common.cuh"
 
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const Build
     const int32_t hl = __shfl_sync(0xffffffffu, h_out[l], leader[l]);
     const bool inr = key[l] < (1ull << 63);
     // (lifted builds accumulate only level 0 from the points)
-    if (valid && (!sg.lift || l == 0)) pslot[sg.pl_offset + k * levels + l] = inr ? hl : -1;
+    if (valid && (!sg.lift || l == 0)) pslot[sg.pl_offset + l * sg.pl_stride + k] = inr ? hl : -1;
   }
 }
 
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
   }
 #endif
   for (int l = 0; l < (bs.lift ? 1 : levels); ++l) {
-    int32_t sl = valid ? pslot[sg.pl_offset + k * levels + l] : -1;
+    int32_t sl = valid ? pslot[sg.pl_offset + l * sg.pl_stride + k] : -1;
     int32_t idx;
     if (bs.box[l].dense) {
       // dense level: the final grid holds the voxel index (phase 1 is complete)
@@ -532,7 +535,9 @@ __global__ void __launch_bounds__(256, GVOX_FIN_MINB) k_build_finalize(const Fin
   // record -1 of every level: all zeros, the record a lookup miss (index -1)
   // gathers in the linearize kernel's unconditional loads
   if (v < 3) sg.vox[v - 3] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (v >= *sg.nvox) return;
+  const int32_t nv = *sg.nvox;
+  if (v == 0 && sg.nvox_out) *sg.nvox_out = nv;  // the map keeps its count (no separate copy)
+  if (v >= nv) return;
   const unsigned long long* src = acc + (sg.acc_offset + v) * 10;
   double cnt = (double)(long long)src[9];
   double inv = 1.0 / cnt;
@@ -593,6 +598,28 @@ __global__ void k_h2d_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict_
     for (int64_t i = (n16 << 4) + t0; i < bytes; i += stride) dst[i] = *(const volatile uint8_t*)(src + i);
   } else {
     for (int64_t i = t0; i < bytes; i += stride) dst[i] = *(const volatile uint8_t*)(src + i);
+  }
+}
+
+// Small blocks ride in the launch itself: the bytes are copied into the
+// kernel's parameter buffer when the launch is enqueued (up to 32,000 bytes;
+// the launch limit is 32,764) and the kernel stores them from the constant bank -- no PCIe
+// round trip at execution time (k_h2d_copy's uncached loads of the pinned slot
+// cost ~1-2 us each on the critical path of an odometry-sized call).
+template <int N>
+struct ParamBlock {
+  int4 w[N / 16];
+};
+template <int N>
+__global__ void k_param_copy(const __grid_constant__ ParamBlock<N> p, uint8_t* __restrict__ dst,
+                             int bytes) {
+  const int n16 = bytes >> 4;
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(p.w);
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) reinterpret_cast<int4*>(dst)[i] = p.w[i];
+    for (int i = (n16 << 4) + threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+  } else {
+    for (int i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
   }
 }
 
@@ -693,6 +720,34 @@ void launch_grid_reset(const ResetSeg* segs_dev, int64_t num_segs, int64_t max_s
 
 void launch_h2d_copy(void* dst, const void* pinned_src, int64_t bytes, cudaStream_t stream) {
   if (bytes <= 0) return;
+  // blocks up to GVOX_H2D_PARAM bytes (at most 32000; default 0: never).
+  // Measured (r02ad, one B200, C1/C2/C3 steps in ms at 0 / 1024 / 4096 / 32000):
+  // C2 0.132 / 0.133 / 0.136 / 0.155 -- the small-config steps are bound by the
+  // host's enqueue time, and a larger parameter buffer costs the host more than
+  // the PCIe round trip costs the device; per-call latency improves slightly
+  // (C2 0.056 -> 0.051 ms at 32000).  Off by default, kept as the knob.
+  static const int64_t param_max = [] {
+    const char* e = std::getenv("GVOX_H2D_PARAM");
+    return e ? std::min<int64_t>(std::max<int64_t>(std::atoll(e), 0), 32000) : (int64_t)0;
+  }();
+  if (bytes <= param_max) {
+    auto go = [&](auto tag) {
+      constexpr int N = decltype(tag)::value;
+      ParamBlock<N> pb;
+      std::memcpy(&pb, pinned_src, (size_t)bytes);
+      k_param_copy<N><<<1, 256, 0, stream>>>(pb, (uint8_t*)dst, (int)bytes);
+    };
+    if (bytes <= 1024)
+      go(std::integral_constant<int, 1024>{});
+    else if (bytes <= 4096)
+      go(std::integral_constant<int, 4096>{});
+    else if (bytes <= 16384)
+      go(std::integral_constant<int, 16384>{});
+    else
+      go(std::integral_constant<int, 32000>{});
+    note_launch();
+    return;
+  }
   int64_t blocks = ((bytes >> 4) + 255) / 256;
   blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 4));
   k_h2d_copy<<<(unsigned)blocks, 256, 0, stream>>>((uint8_t*)dst, (const uint8_t*)pinned_src, bytes);

@@ -387,6 +387,139 @@ __global__ void __launch_bounds__(kPcgThreads)
   }
 }
 
+// Persistent PCG with TWO grid barriers per iteration (default; the kernel
+// above has four).  The direction p = z + beta p is not a phase of its own:
+// the SpMV forms p of every column block on the fly, fma(beta, p_old, z) (the
+// same expression, so bitwise the value the row's owner stores), and the
+// owner writes its rows' p in the update phase after the barrier, when no warp
+// reads p_old any more.  Per iteration:
+//   phase 1: q partials = A (z + beta p) over row chunks, p . q partials  | grid.sync
+//   phase 2: alpha (every CTA sums the chunk partials in the same order);
+//            own rows: p, q = sum of the chunks, x += alpha p, r -= alpha q,
+//            z = M^-1 r, (r.z, r.r) partials                              | grid.sync
+//   phase 3: beta, residual, stopping test (every CTA, same order)
+// The chunk partials are rewritten in the next phase 1 only after the second
+// barrier, and the row partials in the next phase 2 only after the next first
+// barrier, so no buffer needs doubling.  Same PCG recurrence as the 4-barrier
+// kernel and the WHILE-node version (rounding may differ in the last bits).
+__global__ void __launch_bounds__(kPcgThreads)
+    k_pcg_persistent2(const double* __restrict__ blocks, const int32_t* __restrict__ row_start,
+                      const int32_t* __restrict__ col, int64_t num_vars, const double* __restrict__ minv,
+                      const double* __restrict__ rhs, double* __restrict__ x, double* __restrict__ r,
+                      double* __restrict__ z, double* __restrict__ p, double* __restrict__ q,
+                      double* __restrict__ part_a, double* __restrict__ part_b, PcgState* __restrict__ st,
+                      int32_t max_iter, double tol, const int32_t* __restrict__ chunk_row,
+                      const int32_t* __restrict__ chunk_b0, const int32_t* __restrict__ row_chunk,
+                      int64_t num_chunks, double* __restrict__ qpart, double* __restrict__ part_c) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[33];
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // z = M^-1 r and the (r.z, r.r) partials of this warp's rows
+  auto precond_rows = [&](int64_t v) {
+    double zi = 0.0, rv = 0.0;
+    if (lane < 6) {
+      rv = r[6 * v + lane];
+      for (int k = 0; k < 6; ++k) zi += minv[36 * v + lane * 6 + k] * r[6 * v + k];
+      z[6 * v + lane] = zi;
+    }
+    double rz = lane < 6 ? rv * zi : 0.0, rr = lane < 6 ? rv * rv : 0.0;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      rz += __shfl_xor_sync(0xffffffffu, rz, o);
+      rr += __shfl_xor_sync(0xffffffffu, rr, o);
+    }
+    if (lane == 0) {
+      part_a[v] = rz;
+      part_b[v] = rr;
+    }
+  };
+  // ---- start: x = 0, r = rhs, z = M^-1 r, p = 0 (the first direction is
+  // z + 0 * p = z)
+  for (int64_t v = gwarp; v < num_vars; v += nwarps) {
+    if (lane < 6) {
+      x[6 * v + lane] = 0.0;
+      r[6 * v + lane] = rhs[6 * v + lane];
+      p[6 * v + lane] = 0.0;
+    }
+    __syncwarp();
+    precond_rows(v);
+  }
+  grid.sync();
+  double rz = sum_parts(part_a, num_vars, red);
+  const double r0 = sqrt(sum_parts(part_b, num_vars, red));
+  double res = r0, beta = 0.0;
+  int32_t it = 0;
+  bool go = r0 > 0.0 && !(r0 <= tol * r0);
+  while (go) {
+    // phase 1: chunk partials of A (z + beta p) and their dot with the row's p
+    for (int64_t c = gwarp; c < num_chunks; c += nwarps) {
+      const int32_t v = chunk_row[c];
+      const int32_t bend = (c + 1 < num_chunks && chunk_row[c + 1] == v) ? chunk_b0[c + 1]
+                                                                          : row_start[v + 1];
+      double acc[6] = {0, 0, 0, 0, 0, 0};
+      for (int32_t b = chunk_b0[c] + lane; b < bend; b += 32) {
+        const double* B = blocks + 36 * (int64_t)b;
+        const int64_t c6 = 6 * (int64_t)col[b];
+        double pv[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) pv[k] = fma(beta, p[c6 + k], z[c6 + k]);
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+          for (int k = 0; k < 6; ++k) acc[i] += B[i * 6 + k] * pv[k];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < 6; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+      if (lane == 0) {
+        double d = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          qpart[6 * c + i] = acc[i];
+          d += fma(beta, p[6 * (int64_t)v + i], z[6 * (int64_t)v + i]) * acc[i];
+        }
+        part_c[c] = d;
+      }
+    }
+    grid.sync();
+    // phase 2: alpha, then the row updates
+    const double pq = sum_parts(part_c, num_chunks, red);
+    const double alpha = pq > 0.0 ? rz / pq : 0.0;
+    for (int64_t v = gwarp; v < num_vars; v += nwarps) {
+      if (lane < 6) {
+        const int64_t e = 6 * v + lane;
+        const double pv = fma(beta, p[e], z[e]);
+        double qv = 0.0;  // the row's chunks in order
+        for (int32_t c = row_chunk[v]; c < row_chunk[v + 1]; ++c) qv += qpart[6 * (int64_t)c + lane];
+        p[e] = pv;
+        q[e] = qv;
+        x[e] += alpha * pv;
+        r[e] -= alpha * qv;
+      }
+      __syncwarp();
+      precond_rows(v);
+    }
+    grid.sync();
+    // phase 3: beta and the stopping test (identical in every CTA)
+    const double rzn = sum_parts(part_a, num_vars, red);
+    res = sqrt(sum_parts(part_b, num_vars, red));
+    beta = rz > 0.0 ? rzn / rz : 0.0;
+    rz = rzn;
+    ++it;
+    go = res > tol * r0 && it < max_iter && pq > 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->rz = rz;
+    st->r0 = r0;
+    st->res = res;
+    st->iter = it;
+    st->done = 1;
+  }
+}
+
 // Cluster PCG (small and medium graphs): the same iteration on ONE thread-block
 // cluster of up to 16 CTAs (one per SM) instead of the whole grid.  The three
 // barriers per iteration are hardware cluster barriers (barrier.cluster
@@ -568,7 +701,10 @@ void launch_pcg_persistent(const double* blocks, const int32_t* row_start, const
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_persistent, kPcgThreads, 0);
+  // two grid barriers per iteration (default) or four (GVOX_PCG_BARRIERS=4)
+  const char* eb = std::getenv("GVOX_PCG_BARRIERS");
+  void* kern = (eb && std::atoi(eb) == 4) ? (void*)k_pcg_persistent : (void*)k_pcg_persistent2;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPcgThreads, 0);
   const int64_t want = (std::max(num_vars, num_chunks) * 32 + kPcgThreads - 1) / kPcgThreads;  // a warp per chunk
   int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)sms * std::max(per_sm, 1));
   void* args[] = {(void*)&blocks, (void*)&row_start, (void*)&col, (void*)&num_vars, (void*)&minv,
@@ -576,7 +712,7 @@ void launch_pcg_persistent(const double* blocks, const int32_t* row_start, const
                   (void*)&part_a, (void*)&part_b, (void*)&st, (void*)&max_iter, (void*)&tol,
                   (void*)&chunk_row, (void*)&chunk_b0, (void*)&row_chunk, (void*)&num_chunks,
                   (void*)&qpart, (void*)&part_c};
-  cudaLaunchCooperativeKernel((void*)k_pcg_persistent, grid, kPcgThreads, args, 0, stream);
+  cudaLaunchCooperativeKernel(kern, grid, kPcgThreads, args, 0, stream);
   note_launch();
 }
 

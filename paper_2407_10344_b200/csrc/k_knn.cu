@@ -30,6 +30,39 @@ __device__ __forceinline__ double sq_dist_pinned(float px, float py, float pz, f
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
+// fp32 pre-filter of the insertion test (exact): the fp32 squared distance
+// (three rounded differences, squares and sums: relative error below 6 * 2^-24
+// for finite inputs without underflow) exceeds the fp64 gate by more than that
+// error only if the pinned fp64 distance (relative error ~2^-51) does too, so
+// a candidate rejected here would have been rejected by `d2 < gate` -- the
+// fp64 distance is computed only for the candidates that might enter the list.
+// gate32(g) = an upper bound of g * (1 + 2^-20) in fp32 (+inf stays +inf; the
+// absolute 1e-30 covers underflowing squares).
+__device__ __forceinline__ float gate32(double g) {
+  return __double2float_ru(fma(g, 9.5367431640625e-07, g)) + 1e-30f;
+}
+__device__ __forceinline__ float sq_dist_f32(float px, float py, float pz, float qx, float qy,
+                                             float qz) {
+  const float dx = qx - px, dy = qy - py, dz = qz - pz;
+  return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+}
+
+// (j == km1) ? a : b through PTX selp: opaque to the compiler, so an unrolled
+// `for j: if (j == k - 1) x = list[j]` is not folded back into the dynamic
+// index list[k - 1], which would move the whole top-k list into local memory
+__device__ __forceinline__ double sel_eq(int j, int km1, double a, double b) {
+  double r;
+  asm("{ .reg .pred p; setp.eq.s32 p, %1, %2; selp.f64 %0, %3, %4, p; }"
+      : "=d"(r) : "r"(j), "r"(km1), "d"(a), "d"(b));
+  return r;
+}
+__device__ __forceinline__ int32_t sel_eq(int j, int km1, int32_t a, int32_t b) {
+  int32_t r;
+  asm("{ .reg .pred p; setp.eq.s32 p, %1, %2; selp.b32 %0, %3, %4, p; }"
+      : "=r"(r) : "r"(j), "r"(km1), "r"(a), "r"(b));
+  return r;
+}
+
 __device__ __forceinline__ int32_t cell_coord(float x, double lo, double inv_s, int32_t dim) {
   int32_t c = __double2int_rd(((double)x - lo) * inv_s);
   return min(max(c, 0), dim - 1);
@@ -134,6 +167,7 @@ __global__ void __launch_bounds__(kKnnThreads)
     int found = 0;
     double kth = __longlong_as_double(0x7ff0000000000000ll);  // (bd, bi)[k - 1]: the insertion gate
     int32_t kidx = INT32_MAX;
+    float kth32 = __int_as_float(0x7f800000);  // gate32(kth)
     // slack for the cell assignment's rounding (floor((x - lo) / s) in fp64)
     const double slack = 1e-9 * (fabs(cd.lo[0]) + fabs(cd.lo[1]) + fabs(cd.lo[2]) +
                                  cd.s * (cd.dim[0] + cd.dim[1] + cd.dim[2]) + 1.0);
@@ -148,9 +182,10 @@ __global__ void __launch_bounds__(kKnnThreads)
         const int32_t s0 = __ldg(cell_start + c0), s1 = __ldg(cell_start + c1 + 1);
         for (int32_t si = s0; si < s1; ++si) {
           const float4 p = __ldg(sorted + si);
+          ++found;
+          if (sq_dist_f32(p.x, p.y, p.z, q.x, q.y, q.z) > kth32) continue;
           const double d2 = sq_dist_pinned(q.x, q.y, q.z, p.x, p.y, p.z);
           const int32_t pi = __float_as_int(p.w);
-          ++found;
           if (d2 < kth || (d2 == kth && pi < kidx)) {
             // insertion into the (d2, index)-sorted list (registers: unrolled)
             double cd2 = d2;
@@ -166,11 +201,11 @@ __global__ void __launch_bounds__(kKnnThreads)
               ci = lt ? ti : ci;
             }
 #pragma unroll
-            for (int j = 0; j < MAXK; ++j)
-              if (j == k - 1) {
-                kth = bd[j];
-                kidx = bi[j];
-              }
+            for (int j = 0; j < MAXK; ++j) {
+              kth = sel_eq(j, k - 1, bd[j], kth);
+              kidx = sel_eq(j, k - 1, bi[j], kidx);
+            }
+            kth32 = gate32(kth);
           }
         }
       };
@@ -278,13 +313,15 @@ __global__ void __launch_bounds__(kKnnThreads)
       // the gate: the smaller of this lane's own k-th and the merged bound
       double gth = kth;
       int32_t gidx = kidx;
+      float gth32 = gate32(gth);
       auto scan_run = [&](int32_t c0, int32_t c1) {
         const int32_t s0 = __ldg(cell_start + c0), s1 = __ldg(cell_start + c1 + 1);
         for (int32_t si = s0 + sub; si < s1; si += G) {
           const float4 p = __ldg(sorted + si);
+          ++found;
+          if (sq_dist_f32(p.x, p.y, p.z, q.x, q.y, q.z) > gth32) continue;
           const double d2 = sq_dist_pinned(q.x, q.y, q.z, p.x, p.y, p.z);
           const int32_t pi = __float_as_int(p.w);
-          ++found;
           if (d2 < gth || (d2 == gth && pi < gidx)) {
             double cd2 = d2;
             int32_t ci = pi;
@@ -298,12 +335,19 @@ __global__ void __launch_bounds__(kKnnThreads)
               cd2 = lt ? td : cd2;
               ci = lt ? ti : ci;
             }
+            // the own list's k-th, if it is below the merged bound
+            double ok = kInf;
+            int32_t oi = INT32_MAX;
 #pragma unroll
-            for (int j = 0; j < MAXK; ++j)
-              if (j == k - 1 && (bd[j] < gth || (bd[j] == gth && bi[j] < gidx))) {
-                gth = bd[j];
-                gidx = bi[j];
-              }
+            for (int j = 0; j < MAXK; ++j) {
+              ok = sel_eq(j, k - 1, bd[j], ok);
+              oi = sel_eq(j, k - 1, bi[j], oi);
+            }
+            if (ok < gth || (ok == gth && oi < gidx)) {
+              gth = ok;
+              gidx = oi;
+            }
+            gth32 = gate32(gth);
           }
         }
       };
@@ -327,45 +371,43 @@ __global__ void __launch_bounds__(kKnnThreads)
           }
         }
       }
-      // ---- merge: round j takes the group minimum of the lanes' heads
+      // ---- merge: round j takes the group minimum of the lanes' heads (all
+      // MAXK rounds, every index static: the lists stay in registers; rounds
+      // past k merge entries nobody reads)
       __syncwarp(gmask);
       double md[MAXK];
       int32_t mi[MAXK];
 #pragma unroll
       for (int j = 0; j < MAXK; ++j) {
-        md[j] = kInf;
-        mi[j] = INT32_MAX;
-        if (j < k) {
-          double hd = bd[0];
-          int32_t hi = bi[0];
-          int who = sub;
+        double hd = bd[0];
+        int32_t hi = bi[0];
+        int who = sub;
 #pragma unroll
-          for (int o = G / 2; o > 0; o >>= 1) {
-            const double od = __shfl_xor_sync(gmask, hd, o, G);
-            const int32_t oi = __shfl_xor_sync(gmask, hi, o, G);
-            const int ow = __shfl_xor_sync(gmask, who, o, G);
-            if (od < hd || (od == hd && oi < hi)) {
-              hd = od;
-              hi = oi;
-              who = ow;
-            }
-          }
-          if (who == sub) {  // the winner pops its head
-#pragma unroll
-            for (int m = 0; m < MAXK - 1; ++m) {
-              bd[m] = bd[m + 1];
-              bi[m] = bi[m + 1];
-            }
-            bd[MAXK - 1] = kInf;
-            bi[MAXK - 1] = INT32_MAX;
-          }
-          md[j] = hd;
-          mi[j] = hi;
-          if (j == k - 1) {
-            kth = hd;
-            kidx = hi;
+        for (int o = G / 2; o > 0; o >>= 1) {
+          const double od = __shfl_xor_sync(gmask, hd, o, G);
+          const int32_t oi = __shfl_xor_sync(gmask, hi, o, G);
+          const int ow = __shfl_xor_sync(gmask, who, o, G);
+          if (od < hd || (od == hd && oi < hi)) {
+            hd = od;
+            hi = oi;
+            who = ow;
           }
         }
+        const bool pop = who == sub;  // the winner pops its head
+#pragma unroll
+        for (int m = 0; m < MAXK - 1; ++m) {
+          bd[m] = pop ? bd[m + 1] : bd[m];
+          bi[m] = pop ? bi[m + 1] : bi[m];
+        }
+        bd[MAXK - 1] = pop ? kInf : bd[MAXK - 1];
+        bi[MAXK - 1] = pop ? INT32_MAX : bi[MAXK - 1];
+        md[j] = hd;
+        mi[j] = hi;
+      }
+#pragma unroll
+      for (int j = 0; j < MAXK; ++j) {
+        kth = sel_eq(j, k - 1, md[j], kth);
+        kidx = sel_eq(j, k - 1, mi[j], kidx);
       }
       // lane 0 holds the merged list, the others start the next ring empty
 #pragma unroll
@@ -641,7 +683,16 @@ void launch_knn_query(const KnnCloudDev* clouds, const int32_t* tile_start, cons
   // at G = 1, 4.21 at G = 4).  GVOX_KNN_GROUP overrides (1, 4, 8).
   int kGroup = (int64_t)num_tiles * tile_pts <= (64 << 10) ? 4 : 1;
   if (const char* e = std::getenv("GVOX_KNN_GROUP")) kGroup = std::atoi(e);
-  if (k <= 16 && kGroup == 8 && tile_pts % 8 == 0)
+  if (k <= 10 && kGroup == 8 && tile_pts % 8 == 0)
+    k_knn_query_g<10, 8><<<(unsigned)(num_tiles * 8), kKnnThreads, 0, stream>>>(
+        clouds, tile_start, tile_cloud, tile_pts, sorted, cell_start, k, out);
+  else if (k <= 10 && kGroup == 4 && tile_pts % 4 == 0)
+    k_knn_query_g<10, 4><<<(unsigned)(num_tiles * 4), kKnnThreads, 0, stream>>>(
+        clouds, tile_start, tile_cloud, tile_pts, sorted, cell_start, k, out);
+  else if (k <= 10)
+    k_knn_query<10><<<(unsigned)num_tiles, kKnnThreads, 0, stream>>>(clouds, tile_start, tile_cloud,
+                                                                     tile_pts, sorted, cell_start, k, out);
+  else if (k <= 16 && kGroup == 8 && tile_pts % 8 == 0)
     k_knn_query_g<16, 8><<<(unsigned)(num_tiles * 8), kKnnThreads, 0, stream>>>(
         clouds, tile_start, tile_cloud, tile_pts, sorted, cell_start, k, out);
   else if (k <= 16 && kGroup == 4 && tile_pts % 4 == 0)

@@ -85,6 +85,26 @@ namespace {
 #ifndef GVOX_LIN_UNROLL2
 #define GVOX_LIN_UNROLL2 1
 #endif
+// FAST all-dense pipeline three points deep with the voxel records gathered
+// into shared memory by cp.async one point ahead (1), or the two-point register
+// pipeline (0); GVOX_LIN_DEEP_CG: the 16-byte record gathers bypass L1 (1).
+// Measured (r02aa, full C5, ncu): DEEP 248.6 ms vs 121.9 -- 17 % more
+// instructions (LDGSTS + LDS per record word), short_scoreboard 4.1 and
+// mio_throttle 1.1 cycles/issue, and the grid probes now wait (44 KB of shared
+// memory per CTA leaves L1 a third of its size): rejected, kept for the record.
+#ifndef GVOX_LIN_DEEP
+#define GVOX_LIN_DEEP 0
+#endif
+#ifndef GVOX_LIN_DEEP_CG
+#define GVOX_LIN_DEEP_CG 0
+#endif
+// FAST all-dense pipeline three points deep in REGISTERS (1): the grid probes
+// two points ahead, the voxel records gathered one point ahead into registers
+// (a 4-stage source ring); needs more registers per thread (build with
+// GVOX_LIN_MINB=3)
+#ifndef GVOX_LIN_RPIPE
+#define GVOX_LIN_RPIPE 0
+#endif
 
 
 constexpr int kThreads = GVOX_LIN_THREADS;
@@ -114,6 +134,17 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async16_s(unsigned s, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+// L1-allocating copies (the record gathers: neighbouring points share voxels)
+__device__ __forceinline__ void cp_async16_ca(unsigned s, const void* gmem) {
+#if GVOX_LIN_DEEP_CG
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+#else
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+#endif
+}
+__device__ __forceinline__ void cp_async4_ca(unsigned s, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 // all but the newest N groups have landed
@@ -552,7 +583,15 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
   __shared__ double red[kWarps][kPartialStride];
   __shared__ double pose_s[24];
   constexpr int S = GVOX_LIN_STAGES;
-  __shared__ __align__(128) float4 sbuf[kWarps][S][3][32];
+  // the deep FAST pipeline (GVOX_LIN_DEEP) keeps, per warp, 2 stages of the
+  // source A plane (64 float4), 2 of the B and N planes (128), 2 of the gathered
+  // records' first two float4 per level (128 MAXL) and of their C_zz (16 MAXL)
+  constexpr bool DEEP = GVOX_LIN_DEEP && GVOX_LIN_PIPE && !GVOX_LIN_BULK && FAST && ALL_DENSE && !VALID;
+  constexpr int kDeepF4 = 64 + 128 + 128 * MAXL + 16 * MAXL;
+  constexpr bool RPIPE = GVOX_LIN_RPIPE && !DEEP && GVOX_LIN_PIPE && !GVOX_LIN_BULK && FAST && ALL_DENSE && !VALID;
+  constexpr int kWarpF4 = DEEP ? kDeepF4 : RPIPE ? 4 * 3 * 32 : S * 3 * 32;
+  __shared__ __align__(128) float4 sbuf_raw[kWarps * kWarpF4];
+  auto& sbuf = *reinterpret_cast<float4 (*)[kWarps][S][3][32]>(sbuf_raw);
   __shared__ __align__(8) uint64_t mbar[kWarps][S];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -652,6 +691,277 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     const float4* const g_lane = sh.A + (warp * 96 + lane);
     constexpr int kChunkStride = kWarps * 96;  // float4 per iteration
     constexpr unsigned kStageBytes = (unsigned)sizeof(sbuf[0][0]);
+#if GVOX_LIN_DEEP
+    if constexpr (DEEP) {
+      // Three points deep, per thread (no warp barrier: each thread copies and
+      // reads only its own slots).  Live iteration j, with X = point j,
+      // Y = point j + 1, Z = point j + 2:
+      //   wait for group j - 1 = {A plane of j + 2, B/N planes of j, records of j}
+      //   prep Z: transform from its A plane, level-0 key, the three grid probes
+      //   group j = {A plane of j + 3, B/N planes of Y, Y's voxel records (its
+      //             probes landed during the previous point)} -> shared memory
+      //   X's level terms and fold from shared memory
+      // so a record gather has a whole point's work to land (the two-point
+      // register pipeline consumed it right after issuing it).  Same arithmetic
+      // in the same order as the other pipelines (bitwise equal, tested).
+      struct DP {
+        float qx, qy, qz, ex, ey, ez, cxx;
+        uint32_t kb;  // low 24 bits: PointData::kb; bits 24 + l: level l has a voxel
+        int32_t v[MAXL];
+      };
+      float4* const wbuf = sbuf_raw + warp * kDeepF4;
+      const unsigned sw = smem_addr(wbuf) + 16u * (unsigned)lane;
+      const unsigned sA = sw, sBN = sw + 64u * 16u, sG = sw + 192u * 16u;
+      const unsigned sG2 = smem_addr(wbuf + 192 + 128 * MAXL) + 4u * (unsigned)lane;
+      const float4* const rA = wbuf + lane;
+      const float4* const rBN = wbuf + 64 + lane;
+      const float4* const rG = wbuf + 192 + lane;
+      const float* const rG2 = reinterpret_cast<const float*>(wbuf + 192 + 128 * MAXL) + lane;
+      auto copy_a = [&](int32_t i, int s) {
+        if (i < my_iters) cp_async16_s(sA + 512u * (unsigned)s, g_lane + i * kChunkStride);
+      };
+      auto copy_bn = [&](int32_t i, int s) {
+        if (i < my_iters) {
+          const float4* g = g_lane + i * kChunkStride;
+          cp_async16_s(sBN + 1024u * (unsigned)s, g + 32);
+          cp_async16_s(sBN + 1024u * (unsigned)s + 512u, g + 64);
+        }
+      };
+      // Y's records: every level's, a miss (index -1) from the level's all-zero
+      // sentinel record; nothing when Y hits no level (or has no point)
+      auto gather = [&](DP& y, int s) {
+        uint32_t hits = 0;
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) hits |= (y.v[l] >= 0 ? 1u : 0u) << l;
+        y.kb |= hits << 24;
+        if (hits) {
+#pragma unroll
+          for (int l = 0; l < MAXL; ++l) {
+            const float4* vp = sh.lv[l].vox + 3 * y.v[l];
+            const unsigned g = sG + (unsigned)(s * MAXL + l) * 1024u;
+            cp_async16_ca(g, vp);
+            cp_async16_ca(g + 512u, vp + 1);
+            cp_async4_ca(sG2 + (unsigned)(s * MAXL + l) * 128u, &vp[2].x);
+          }
+        }
+      };
+      auto prep = [&](int32_t i, int s, DP& z) {
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) z.v[l] = -1;
+        z.kb = 0;
+        if (i < my_iters) {
+          const float4 a = rA[32 * s];
+          PointData pd;
+          transform_point(sh, a, 1, r0, inv_r0, r0f, pd);
+          lookup_nested<MAXL>(sh.lv, pd.k0x, pd.k0y, pd.k0z, z.v);
+          z.qx = pd.qx;
+          z.qy = pd.qy;
+          z.qz = pd.qz;
+          z.ex = pd.ex;
+          z.ey = pd.ey;
+          z.ez = pd.ez;
+          z.kb = pd.kb;
+          z.cxx = a.w;
+        }
+      };
+      auto compute = [&](const DP& x, int s) {
+        const uint32_t hits = x.kb >> 24;
+        if (!hits) return;
+        PointData q;
+        q.qx = x.qx;
+        q.qy = x.qy;
+        q.qz = x.qz;
+        q.ex = x.ex;
+        q.ey = x.ey;
+        q.ez = x.ez;
+        q.kb = x.kb;
+        const float4 b = rBN[64 * s], c = rBN[64 * s + 32];
+        rcr(sh.Rf, sh.Rp, make_float4(0.f, 0.f, 0.f, x.cxx), b, c, q);
+        LevelSum ls;
+        ls.Oa = ls.Oc = ls.G = 0;
+        ls.o11 = ls.o22 = ls.gz = 0.f;
+        float bx = q.ex, by = q.ey, bz = q.ez;
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) {
+          const float4 v0 = rG[(s * MAXL + l) * 64], v1 = rG[(s * MAXL + l) * 64 + 32];
+          const float v2 = rG2[(s * MAXL + l) * 32];
+          level_base(q, l, r0f, bx, by, bz);
+          level_term<MAXL>(ac, ls, q, v0, v1, v2, l, bx, by, bz, (hits >> l) & 1u);
+        }
+        if (!error_only) fold_point<MAXL>(ac, ls, q);
+      };
+      // live iteration j (X, Y, Z as above; stage of point k = k & 1)
+      int32_t i_n1 = live_at(1), i_n2 = live_at(2);
+      auto step = [&](int32_t j, const DP& X, DP& Y, DP& Z) {
+        cp_async_wait<0>();
+        const int sj = j & 1;
+        const int32_t i1 = i_n1, i2 = i_n2, i3 = live_at(j + 3);
+        prep(i2, sj, Z);
+        copy_a(i3, sj ^ 1);
+        copy_bn(i1, sj ^ 1);
+        gather(Y, sj ^ 1);
+        cp_async_commit();
+        compute(X, sj);
+        i_n1 = i2;
+        i_n2 = i3;
+      };
+      DP P0, P1, P2;
+      {
+        const int32_t i0 = live_at(0);
+        copy_a(i0, 0);
+        copy_a(i_n1, 1);
+        cp_async_commit();
+        cp_async_wait<0>();
+        prep(i0, 0, P0);
+        prep(i_n1, 1, P1);
+        // group -1 = {A plane of point 2, B/N planes and records of point 0}
+        copy_a(i_n2, 0);
+        copy_bn(i0, 0);
+        gather(P0, 0);
+        cp_async_commit();
+      }
+#pragma unroll 1
+      for (int32_t j = 0; j < nlive; j += 3) {
+        step(j, P0, P1, P2);
+        if (j + 1 >= nlive) break;
+        step(j + 1, P1, P2, P0);
+        if (j + 2 >= nlive) break;
+        step(j + 2, P2, P0, P1);
+      }
+      cp_async_wait<0>();
+      tile_reduce<MAXL>(ac, red, partials, tile);
+      return;
+    } else
+#endif
+#if GVOX_LIN_RPIPE
+    if constexpr (RPIPE) {
+      // Register pipeline, per thread.  Live iteration j (X = point j, Y = j + 1,
+      // Z = j + 2; source stage of point k = k & 3):
+      //   copy point j + 3's source planes (group j); wait for point j + 2's
+      //   prep Z (transform, key, the three grid probes)
+      //   gather Y's three voxel records into registers (its probes were issued
+      //   one point ago)
+      //   X's level terms and fold (its records were gathered one point ago)
+      struct RP {
+        float qx, qy, qz, ex, ey, ez;
+        uint32_t kb;
+        int32_t v[MAXL];
+      };
+      struct RR {
+        float4 v0[MAXL], v1[MAXL];
+        float v2[MAXL];
+      };
+      float4(*const rb)[3][32] = reinterpret_cast<float4(*)[3][32]>(sbuf_raw + warp * (4 * 3 * 32));
+      const unsigned s_w = smem_addr(&rb[0][0][lane]);
+      auto copy_src = [&](int32_t i, int s) {
+        if (i < my_iters) {
+          const float4* g = g_lane + i * kChunkStride;
+          const unsigned sa = s_w + (unsigned)s * 1536u;
+          cp_async16_s(sa, g);
+          cp_async16_s(sa + 512u, g + 32);
+          cp_async16_s(sa + 1024u, g + 64);
+        }
+        cp_async_commit();
+      };
+      auto prep = [&](int32_t i, int s, RP& z) {
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) z.v[l] = -1;
+        if (i < my_iters) {
+          const float4 a = rb[s][0][lane];
+          PointData pd;
+          transform_point(sh, a, 1, r0, inv_r0, r0f, pd);
+          lookup_nested<MAXL>(sh.lv, pd.k0x, pd.k0y, pd.k0z, z.v);
+          z.qx = pd.qx;
+          z.qy = pd.qy;
+          z.qz = pd.qz;
+          z.ex = pd.ex;
+          z.ey = pd.ey;
+          z.ez = pd.ez;
+          z.kb = pd.kb;
+        }
+      };
+      // every level's record, a miss from the level's all-zero sentinel at -1
+      auto gather = [&](const RP& y, RR& r) {
+        bool any = false;
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) any |= y.v[l] >= 0;
+        if (!any) return;  // (compute skips the point)
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) {
+          const float4* vp = sh.lv[l].vox + 3 * y.v[l];
+          r.v0[l] = __ldg(vp);
+          r.v1[l] = __ldg(vp + 1);
+          r.v2[l] = __ldg(&vp[2].x);
+        }
+      };
+      auto compute = [&](const RP& x, const RR& r, int s) {
+        bool any = false;
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) any |= x.v[l] >= 0;
+        if (!any) return;
+        PointData q;
+        q.qx = x.qx;
+        q.qy = x.qy;
+        q.qz = x.qz;
+        q.ex = x.ex;
+        q.ey = x.ey;
+        q.ez = x.ez;
+        q.kb = x.kb;
+        const float4 a = rb[s][0][lane], b = rb[s][1][lane], c = rb[s][2][lane];
+        rcr(sh.Rf, sh.Rp, a, b, c, q);
+        LevelSum ls;
+        ls.Oa = ls.Oc = ls.G = 0;
+        ls.o11 = ls.o22 = ls.gz = 0.f;
+        float bx = q.ex, by = q.ey, bz = q.ez;
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) {
+          level_base(q, l, r0f, bx, by, bz);
+          level_term<MAXL>(ac, ls, q, r.v0[l], r.v1[l], r.v2[l], l, bx, by, bz, x.v[l] >= 0);
+        }
+        if (!error_only) fold_point<MAXL>(ac, ls, q);
+      };
+      int32_t i_n2 = live_at(2);  // before step j: live iteration j + 2
+      auto step = [&](int32_t j, const RP& X, const RP& Y, RP& Z, const RR& RX, RR& RY) {
+        const int32_t i3 = live_at(j + 3);
+        copy_src(i3, (j + 3) & 3);
+        cp_async_wait<1>();  // point j + 2's planes landed
+        prep(i_n2, (j + 2) & 3, Z);
+        gather(Y, RY);
+        compute(X, RX, j & 3);
+        i_n2 = i3;
+      };
+      RP P0, P1, P2;
+      RR R0, R1;
+      {
+        const int32_t i0 = live_at(0), i1 = live_at(1);
+        copy_src(i0, 0);
+        copy_src(i1, 1);
+        copy_src(i_n2, 2);
+        cp_async_wait<1>();  // points 0 and 1 landed
+        prep(i0, 0, P0);
+        prep(i1, 1, P1);
+        gather(P0, R0);
+      }
+#pragma unroll 1
+      for (int32_t j = 0; j < nlive; j += 6) {
+        step(j, P0, P1, P2, R0, R1);
+        if (j + 1 >= nlive) break;
+        step(j + 1, P1, P2, P0, R1, R0);
+        if (j + 2 >= nlive) break;
+        step(j + 2, P2, P0, P1, R0, R1);
+        if (j + 3 >= nlive) break;
+        step(j + 3, P0, P1, P2, R1, R0);
+        if (j + 4 >= nlive) break;
+        step(j + 4, P1, P2, P0, R0, R1);
+        if (j + 5 >= nlive) break;
+        step(j + 5, P2, P0, P1, R1, R0);
+      }
+      cp_async_wait<0>();
+      tile_reduce<MAXL>(ac, red, partials, tile);
+      return;
+    } else
+#endif
+    {
     // the j-th live iteration's copy into stage j % S (one group per slot,
     // empty when the iteration does not exist or this lane has no point)
     auto issue_l = [&](int32_t i, unsigned sa) {
@@ -768,6 +1078,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
 #endif
     tile_reduce<MAXL>(ac, red, partials, tile);
     return;
+    }
   }
 #endif
 #pragma unroll
@@ -1046,11 +1357,14 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
   // FAST (3 dyadic levels, no dump): dense grids or hash levels, with or
   // without the P:197 visibility test
   if (fast && max_levels == 3) {
+    note_linearize_variant(GVOX_LINVAR_FAST | (all_dense ? GVOX_LINVAR_DENSE : 0) |
+                           (validate ? GVOX_LINVAR_VALID : 0) | (3 << 8));
     auto* k = all_dense ? (validate ? k_linearize<3, true, true, true> : k_linearize<3, true, true, false>)
                         : (validate ? k_linearize<3, false, true, true> : k_linearize<3, false, true, false>);
     k<<<grid, kThreads, 0, stream>>>(clouds, maps, factors, tile_start, tile_factor, tile_pts, poses,
                                      partials, nullptr);
   } else if (max_levels <= 3) {
+    note_linearize_variant((all_dense ? GVOX_LINVAR_DENSE : 0) | (3 << 8));
     if (all_dense)
       k_linearize<3, true, false><<<grid, kThreads, 0, stream>>>(
           clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
@@ -1058,6 +1372,7 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
       k_linearize<3, false, false><<<grid, kThreads, 0, stream>>>(
           clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
   } else {
+    note_linearize_variant(GVOX_MAX_LEVELS << 8);
     k_linearize<GVOX_MAX_LEVELS, false, false><<<grid, kThreads, 0, stream>>>(
         clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
   }
@@ -1116,8 +1431,9 @@ __device__ __forceinline__ int2 block_scan2(int32_t& a, int32_t& b, int2* s_w) {
 
 __global__ void __launch_bounds__(kPlanThreads)
     k_select_count(const uint8_t* __restrict__ selected, const int32_t* __restrict__ ntiles,
-                   int64_t num_cand, int2* __restrict__ block_tot) {
+                   int64_t num_cand, int2* __restrict__ block_tot, int32_t* __restrict__ counts) {
   __shared__ int2 s_w[32];
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[2] = counts[3] = 0;  // (k_select_scatter reduces into them)
   const int64_t p = (int64_t)blockIdx.x * kPlanThreads + threadIdx.x;
   int32_t f = p < num_cand && selected[p] ? 1 : 0;
   int32_t t = f ? ntiles[p] : 0;
@@ -1127,7 +1443,8 @@ __global__ void __launch_bounds__(kPlanThreads)
 
 __global__ void __launch_bounds__(kPlanThreads)
     k_select_scatter(const uint8_t* __restrict__ selected, const int32_t* __restrict__ ntiles,
-                     const FactorDev* __restrict__ factors, int64_t num_cand,
+                     const uint8_t* __restrict__ cls, const FactorDev* __restrict__ factors,
+                     int64_t num_cand,
                      const int2* __restrict__ block_tot, FactorDev* __restrict__ factors_c,
                      int32_t* __restrict__ tile_start_c, int32_t* __restrict__ counts) {
   __shared__ int2 s_w[32];
@@ -1156,6 +1473,15 @@ __global__ void __launch_bounds__(kPlanThreads)
     factors_c[k] = factors[p];
     tile_start_c[k] = off.y + t - nt;
   }
+  // kernel class of the selected candidates: OR of the class bits, max levels
+  // (warp-aggregated, one atomic pair per warp with a selected candidate)
+  const uint32_t c = sel ? (uint32_t)cls[p] : 0u;
+  const uint32_t c_or = __reduce_or_sync(0xffffffffu, c & 15u);
+  const uint32_t c_lv = __reduce_max_sync(0xffffffffu, c >> 4);
+  if ((threadIdx.x & 31) == 0 && (c_or | c_lv)) {
+    atomicOr(counts + 2, (int32_t)c_or);
+    atomicMax(counts + 3, (int32_t)c_lv);
+  }
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
     tile_start_c[off.x + tot.x] = off.y + tot.y;
     counts[0] = off.x + tot.x;
@@ -1163,14 +1489,15 @@ __global__ void __launch_bounds__(kPlanThreads)
   }
 }
 
-void launch_select_plan(const uint8_t* selected, const int32_t* ntiles, const FactorDev* factors,
-                        int64_t num_cand, FactorDev* factors_c, int32_t* tile_start_c,
-                        int32_t* counts, int2* block_tot, cudaStream_t stream) {
+void launch_select_plan(const uint8_t* selected, const int32_t* ntiles, const uint8_t* cls,
+                        const FactorDev* factors, int64_t num_cand, FactorDev* factors_c,
+                        int32_t* tile_start_c, int32_t* counts, int2* block_tot,
+                        cudaStream_t stream) {
   const unsigned nb = (unsigned)((num_cand + kPlanThreads - 1) / kPlanThreads);
-  k_select_count<<<nb, kPlanThreads, 0, stream>>>(selected, ntiles, num_cand, block_tot);
+  k_select_count<<<nb, kPlanThreads, 0, stream>>>(selected, ntiles, num_cand, block_tot, counts);
   note_launch();
-  k_select_scatter<<<nb, kPlanThreads, 0, stream>>>(selected, ntiles, factors, num_cand, block_tot,
-                                                    factors_c, tile_start_c, counts);
+  k_select_scatter<<<nb, kPlanThreads, 0, stream>>>(selected, ntiles, cls, factors, num_cand,
+                                                    block_tot, factors_c, tile_start_c, counts);
   note_launch();
 }
 

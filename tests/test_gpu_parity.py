@@ -636,6 +636,50 @@ def test_linearize_select_equals_two_calls(gv, ctx, num, den):
     assert gv.linearize_batch_accum_select(ctx, clouds, maps, cand[:0], dsel, sc.poses, out) == 0
 
 
+def test_linearize_select_variant_from_selected(gv, ctx, monkeypatch):
+    """The screened batch picks its kernel variant from the SELECTED candidates
+    (class bits reduced on the device during the compaction), as
+    gvox_linearize_batch_accum would for the selected list: unselected
+    candidates on a 2-level map and on a hash-level map leave the batch on the
+    FAST all-dense kernel; selecting the 2-level one switches it to the generic
+    kernel, selecting the hash-level one to the FAST hash-level kernel.  Records
+    bitwise the two-call path's either way."""
+    import torch
+    sc = synth.make("C5", n_submaps=24, half_blocks=3)
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    maps = gv.create_voxelmaps(ctx, clouds, sc.r0, sc.levels)
+    t0 = int(sc.pairs[0, 1])
+    two = gv.create_voxelmap(ctx, clouds[t0], sc.r0, 2)
+    monkeypatch.setenv("GVOX_DENSE_BUDGET_MB", "0")
+    hashed = gv.create_voxelmap(ctx, clouds[t0], sc.r0, sc.levels)
+    monkeypatch.delenv("GVOX_DENSE_BUDGET_MB")
+    allm = list(maps) + [two, hashed]
+    cand = np.zeros(len(sc.pairs) + 2, gv.FACTOR_DTYPE)
+    for i, name in enumerate(("source_cloud", "target_map", "pose_i", "pose_j")):
+        cand[name][:-2] = sc.pairs[:, i]
+        cand[name][-2:] = sc.pairs[0, i]
+    cand["target_map"][-2:] = [len(maps), len(maps) + 1]
+    sel = np.zeros(len(cand), np.uint8)
+    sel[:-2] = gv.overlap_select(ctx, clouds, maps, sc.pairs, sc.poses, sc.overlap_level, 1, 20)
+    assert sel.sum() > 0
+    FAST, DENSE = 1, 2
+    for extra, want_fast in ((None, True), (-2, False), (-1, True)):
+        s = sel.copy()
+        if extra is not None:
+            s[extra] = 1
+        out = gv.device_records(ctx, len(cand), gv.FACTOR_ACCUM_DTYPE)
+        ns = gv.linearize_batch_accum_select(ctx, clouds, allm, cand, torch.from_numpy(s).cuda(),
+                                             sc.poses, out)
+        v = gv.last_linearize_variant()
+        assert ns == int(s.sum())
+        assert bool(v & FAST) == want_fast, (extra, v)
+        assert bool(v & DENSE) == (extra != -1), (extra, v)
+        ref = gv.device_records(ctx, ns, gv.FACTOR_ACCUM_DTYPE)
+        gv.linearize_batch_accum(ctx, clouds, allm, cand[s.view(bool)], sc.poses, out=ref)
+        assert gv.last_linearize_variant() == v
+        assert torch.equal(out[:ns], ref)
+
+
 def test_dense_and_hash_levels_agree(gv, ctx, monkeypatch):
     """The two voxel index structures (dense grids, hash tables) give identical
     maps and bitwise identical linearizations and overlap counts: the build is

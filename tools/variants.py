@@ -84,6 +84,12 @@ VARIANTS = {
     "acc_acc5": ["GVOX_ACC_MINB=5"],
     "acc_acc4_ins8": ["GVOX_ACC_MINB=4", "GVOX_INS_MINB=8"],
     "acc_acc4_ins6_fin": ["GVOX_ACC_MINB=4", "GVOX_INS_MINB=6", "GVOX_FIN_MINB=8"],
+    # r02 session 3: the three-point pipeline with records gathered into shared memory
+    "deep0": ["GVOX_LIN_DEEP=0"],
+    "deep1": ["GVOX_LIN_DEEP=1"],
+    "deep_cg": ["GVOX_LIN_DEEP=1", "GVOX_LIN_DEEP_CG=1"],
+    "rpipe_b3": ["GVOX_LIN_RPIPE=1", "GVOX_LIN_MINB=3"],
+    "rpipe_b2": ["GVOX_LIN_RPIPE=1", "GVOX_LIN_MINB=2"],
 }
 
 
