@@ -267,6 +267,38 @@ __device__ double sum_parts(const double* __restrict__ part, int64_t n, double* 
   return block_sum(s, red);
 }
 
+// two block sums in one pass (same per-thread order and tree as block_sum)
+__device__ void block_sum2(double& a, double& b, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    red[w] = a;
+    red[32 + w] = b;
+  }
+  __syncthreads();
+  if (w == 0) {
+    double x = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+    double y = lane < (int)(blockDim.x >> 5) ? red[32 + lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      x += __shfl_xor_sync(0xffffffffu, x, o);
+      y += __shfl_xor_sync(0xffffffffu, y, o);
+    }
+    if (lane == 0) {
+      red[64] = x;
+      red[65] = y;
+    }
+  }
+  __syncthreads();
+  a = red[64];
+  b = red[65];
+}
+
 __global__ void __launch_bounds__(kPcgThreads)
     k_pcg_persistent(const double* __restrict__ blocks, const int32_t* __restrict__ row_start,
                      const int32_t* __restrict__ col, int64_t num_vars, const double* __restrict__ minv,
@@ -412,7 +444,7 @@ __global__ void __launch_bounds__(kPcgThreads)
                       const int32_t* __restrict__ chunk_b0, const int32_t* __restrict__ row_chunk,
                       int64_t num_chunks, double* __restrict__ qpart, double* __restrict__ part_c) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double red[33];
+  __shared__ double red[66];
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -447,8 +479,13 @@ __global__ void __launch_bounds__(kPcgThreads)
     precond_rows(v);
   }
   grid.sync();
-  double rz = sum_parts(part_a, num_vars, red);
-  const double r0 = sqrt(sum_parts(part_b, num_vars, red));
+  double rz = 0.0, r0 = 0.0;
+  for (int64_t v = threadIdx.x; v < num_vars; v += blockDim.x) {
+    rz += part_a[v];
+    r0 += part_b[v];
+  }
+  block_sum2(rz, r0, red);
+  r0 = sqrt(r0);
   double res = r0, beta = 0.0;
   int32_t it = 0;
   bool go = r0 > 0.0 && !(r0 <= tol * r0);
@@ -504,8 +541,13 @@ __global__ void __launch_bounds__(kPcgThreads)
     }
     grid.sync();
     // phase 3: beta and the stopping test (identical in every CTA)
-    const double rzn = sum_parts(part_a, num_vars, red);
-    res = sqrt(sum_parts(part_b, num_vars, red));
+    double rzn = 0.0, rr = 0.0;  // (r.z, r.r) in one pass
+    for (int64_t v = threadIdx.x; v < num_vars; v += blockDim.x) {
+      rzn += part_a[v];
+      rr += part_b[v];
+    }
+    block_sum2(rzn, rr, red);
+    res = sqrt(rr);
     beta = rz > 0.0 ? rzn / rz : 0.0;
     rz = rzn;
     ++it;
@@ -707,6 +749,8 @@ void launch_pcg_persistent(const double* blocks, const int32_t* row_start, const
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPcgThreads, 0);
   const int64_t want = (std::max(num_vars, num_chunks) * 32 + kPcgThreads - 1) / kPcgThreads;  // a warp per chunk
   int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)sms * std::max(per_sm, 1));
+  if (const char* e = std::getenv("GVOX_PCG_CTAS"))  // experiments: fewer, busier CTAs
+    grid = std::max(1, std::min(grid, std::atoi(e)));
   void* args[] = {(void*)&blocks, (void*)&row_start, (void*)&col, (void*)&num_vars, (void*)&minv,
                   (void*)&rhs, (void*)&x, (void*)&r, (void*)&z, (void*)&p, (void*)&q,
                   (void*)&part_a, (void*)&part_b, (void*)&st, (void*)&max_iter, (void*)&tol,

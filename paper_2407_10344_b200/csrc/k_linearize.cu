@@ -105,6 +105,13 @@ namespace {
 #ifndef GVOX_LIN_RPIPE
 #define GVOX_LIN_RPIPE 0
 #endif
+// FAST two-point pipeline, order inside a live iteration: 0 = prep of the next
+// point, gathers, R C R^T, level terms; 1 = prep, R C R^T, gathers, level terms
+// (ncu: the first R C R^T instruction after the gathers waited on their
+// scoreboard); 2 = gathers, then prep of the next point, R C R^T, level terms
+#ifndef GVOX_LIN_ORDER
+#define GVOX_LIN_ORDER 0
+#endif
 
 
 constexpr int kThreads = GVOX_LIN_THREADS;
@@ -1015,6 +1022,24 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     // other set), then this point's level terms and fold
     auto step = [&](int32_t j, const PointData& pd, const int32_t (&vid)[MAXL], const bool inv,
                     PointData& pn, int32_t (&vn)[MAXL], bool& inv_n) {
+      bool any = false;
+#pragma unroll
+      for (int l = 0; l < MAXL; ++l) any |= vid[l] >= 0;
+      // every level's record is loaded unconditionally: a level without a
+      // correspondence (index -1) reads the level's all-zero sentinel record
+      // at index -1 (masked out in level_term, exactly as zeros)
+      float4 v0[MAXL], v1[MAXL];
+      float v2[MAXL];
+      auto gather = [&]() {
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) {
+          const float4* vp = sh.lv[l].vox + 3 * vid[l];
+          v0[l] = __ldg(vp);
+          v1[l] = __ldg(vp + 1);
+          v2[l] = __ldg(&vp[2].x);
+        }
+      };
+      if (GVOX_LIN_ORDER == 2 && any && !(VALID && inv)) gather();
       issue_l(i_nx2, s_lane + (unsigned)(st == 0 ? S - 1 : st - 1) * kStageBytes);  // slot j + 2
       cp_async_wait<S - 2>();                                                        // slot j + 1 landed
       const int cur = st;
@@ -1027,26 +1052,15 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
         ++ac.n_invisible;
         return;
       }
-      bool any = false;
-#pragma unroll
-      for (int l = 0; l < MAXL; ++l) any |= vid[l] >= 0;
       if (!any) return;  // (also every lane without a point: prep left its indices -1)
-      // every level's record is loaded unconditionally: a level without a
-      // correspondence (index -1) reads the level's all-zero sentinel record
-      // at index -1 (masked out in level_term, exactly as zeros)
-      float4 v0[MAXL], v1[MAXL];
-      float v2[MAXL];
-#pragma unroll
-      for (int l = 0; l < MAXL; ++l) {
-        const float4* vp = sh.lv[l].vox + 3 * vid[l];
-        v0[l] = __ldg(vp);
-        v1[l] = __ldg(vp + 1);
-        v2[l] = __ldg(&vp[2].x);
-      }
-      const float4 a = sbuf[warp][cur][0][lane], b = sbuf[warp][cur][1][lane],
-                   c = sbuf[warp][cur][2][lane];
       PointData q = pd;  // (R C R^T lands in the point's record)
-      rcr(sh.Rf, sh.Rp, a, b, c, q);
+      if (GVOX_LIN_ORDER == 0) gather();
+      {
+        const float4 a = sbuf[warp][cur][0][lane], b = sbuf[warp][cur][1][lane],
+                     c = sbuf[warp][cur][2][lane];
+        rcr(sh.Rf, sh.Rp, a, b, c, q);
+      }
+      if (GVOX_LIN_ORDER == 1) gather();
       LevelSum ls;
       ls.Oa = ls.Oc = ls.G = 0;
       ls.o11 = ls.o22 = ls.gz = 0.f;

@@ -90,6 +90,8 @@ VARIANTS = {
     "deep_cg": ["GVOX_LIN_DEEP=1", "GVOX_LIN_DEEP_CG=1"],
     "rpipe_b3": ["GVOX_LIN_RPIPE=1", "GVOX_LIN_MINB=3"],
     "rpipe_b2": ["GVOX_LIN_RPIPE=1", "GVOX_LIN_MINB=2"],
+    "order1": ["GVOX_LIN_ORDER=1"],
+    "order2": ["GVOX_LIN_ORDER=2"],
 }
 
 
