@@ -203,6 +203,10 @@ gvox_status gvox_voxelmap_lookup(gvox_ctx* ctx, const gvox_map* map, int level, 
                                  int64_t n, int64_t* keys_out, int mem);
 
 void gvox_map_destroy(gvox_map* map);
+/* Destroy count maps (NULL entries skipped) in one call: what a caller that
+   built a batch with gvox_create_voxelmaps does once the batch is done (the
+   per-call overhead of one destroy per map shows in odometry-sized steps). */
+void gvox_maps_destroy(gvox_map* const* maps, int64_t count);
 
 /* ---------------------------------------------------------------- overlap */
 

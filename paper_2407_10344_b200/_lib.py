@@ -61,7 +61,7 @@ SYMBOLS = [
     "gvox_ctx_timing", "gvox_cloud_create", "gvox_clouds_create", "gvox_cloud_size",
     "gvox_cloud_destroy",
     "gvox_create_voxelmap", "gvox_create_voxelmaps", "gvox_voxelmap_info", "gvox_voxelmap_levels",
-    "gvox_voxelmap_export", "gvox_voxelmap_lookup", "gvox_map_destroy",
+    "gvox_voxelmap_export", "gvox_voxelmap_lookup", "gvox_map_destroy", "gvox_maps_destroy",
     "gvox_overlap", "gvox_overlap_select", "gvox_linearize_batch", "gvox_linearize_batch_accum",
     "gvox_linearize_batch_accum_select", "gvox_expand",
     "gvox_register_batch", "gvox_overlap_union", "gvox_keyframe_update",
@@ -108,6 +108,7 @@ def lib():
         "gvox_voxelmap_export": (I32, [P, P, I32, P, P, P, P]),
         "gvox_voxelmap_lookup": (I32, [P, P, I32, P, I64, P, I32]),
         "gvox_map_destroy": (None, [P]),
+        "gvox_maps_destroy": (None, [P, I64]),
         "gvox_overlap": (I32, [P, P, I64, P, I64, P, I64, P, I64, I32, P, I32]),
         "gvox_overlap_select": (I32, [P, P, I64, P, I64, P, I64, P, I64, I32, I32, I32, P, I32]),
         "gvox_linearize_batch": (I32, [P, P, I64, P, I64, P, I64, P, I64, P, I32, P]),

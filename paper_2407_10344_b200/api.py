@@ -174,9 +174,10 @@ def create_clouds(ctx: Context, mu, cov, normals, offsets):
 class VoxelMap:
     """gvox_map: multi-resolution Gaussian voxelmap."""
 
-    def __init__(self, handle: ctypes.c_void_p):
+    def __init__(self, handle: ctypes.c_void_p, levels: int = None, batch=None):
         self.handle = handle
-        self.levels = int(lib().gvox_voxelmap_levels(handle))
+        self.levels = int(lib().gvox_voxelmap_levels(handle)) if levels is None else int(levels)
+        self._batch = batch  # _MapBatch of create_voxelmaps: destroys the maps left in one call
 
     def info(self, level: int):
         n = ctypes.c_int64()
@@ -214,12 +215,38 @@ class VoxelMap:
 
     def close(self):
         if getattr(self, "handle", None):
+            if self._batch is not None:
+                self._batch.release(self.handle)
             lib().gvox_map_destroy(self.handle)
             self.handle = None
 
     def __del__(self):
+        # a batch member is destroyed with its batch (one call for all of them)
+        if getattr(self, "_batch", None) is not None:
+            return
         try:
             self.close()
+        except Exception:  # pragma: no cover
+            pass
+
+
+class _MapBatch:
+    """The maps of one create_voxelmaps call: whatever its VoxelMaps have not
+    closed explicitly is destroyed with ONE gvox_maps_destroy call when the
+    last of them goes (each VoxelMap holds a reference)."""
+
+    def __init__(self, handles):
+        self.arr = handles  # ctypes array of gvox_map*
+        self.n = len(handles)
+
+    def release(self, handle):
+        for i in range(self.n):
+            if self.arr[i] == handle.value:
+                self.arr[i] = None
+
+    def __del__(self):
+        try:
+            lib().gvox_maps_destroy(self.arr, self.n)
         except Exception:  # pragma: no cover
             pass
 
@@ -236,7 +263,8 @@ def create_voxelmaps(ctx: Context, clouds: Sequence[Cloud], r0: float, levels: i
     arr = (ctypes.c_void_p * max(n, 1))(*[c.handle.value for c in clouds])
     out = (ctypes.c_void_p * max(n, 1))()
     check(lib().gvox_create_voxelmaps(ctx.handle, arr, n, float(r0), int(levels), out))
-    return [VoxelMap(ctypes.c_void_p(out[i])) for i in range(n)]
+    batch = _MapBatch(out)
+    return [VoxelMap(ctypes.c_void_p(out[i]), levels, batch) for i in range(n)]
 
 
 class HandleArray:

@@ -1336,6 +1336,11 @@ gvox_status gvox_voxelmap_lookup(gvox_ctx* ctx, const gvox_map* map, int level, 
 
 void gvox_map_destroy(gvox_map* map) { delete map; }
 
+void gvox_maps_destroy(gvox_map* const* maps, int64_t count) {
+  if (!maps) return;
+  for (int64_t i = 0; i < count; ++i) delete maps[i];
+}
+
 // ------------------------------------------------------------------ overlap
 namespace {
 

@@ -151,6 +151,9 @@ __global__ void k_cloud_pack_batch(const PackSeg* __restrict__ segs) {
 
 // Grids are 2D: blockIdx.y = segment (cloud), blockIdx.x * blockDim.x +
 // threadIdx.x = point within it, so a block never straddles two maps.
+#ifndef GVOX_INS_SEG_MAJOR
+#define GVOX_INS_SEG_MAJOR 1
+#endif
 #ifndef GVOX_INS_MINB
 #define GVOX_INS_MINB 8
 #endif
@@ -170,16 +173,21 @@ __global__ void k_cloud_pack_batch(const PackSeg* __restrict__ segs) {
 #define GVOX_ACC_MAXRUN 1
 #endif
 
-template <int kMaxL>
+// SEG_MAJOR: blockIdx.x = segment, blockIdx.y = block of the segment, so the
+// CTAs resident at one time belong to many maps and their per-map voxel
+// counters (one global atomicAdd per block and level) are not all contended
+// by the same few maps' blocks
+template <int kMaxL, bool SEG_MAJOR = false>
 __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const BuildSeg* __restrict__ segs, int levels, double r0,
                                double inv_r0, int dyadic, int32_t* __restrict__ pslot,
                                int32_t* __restrict__ err) {
   const int lane = threadIdx.x & 31;
-  const BuildSeg& sg = segs[blockIdx.y];
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned bseg = SEG_MAJOR ? blockIdx.x : blockIdx.y, bblk = SEG_MAJOR ? blockIdx.y : blockIdx.x;
+  const BuildSeg& sg = segs[bseg];
+  const int64_t k = (int64_t)bblk * blockDim.x + threadIdx.x;
   const bool valid = k < sg.n;
   // (block-uniform exit only: the index allocation below uses block barriers)
-  if ((int64_t)blockIdx.x * blockDim.x >= sg.n) return;
+  if ((int64_t)bblk * blockDim.x >= sg.n) return;
   int32_t k0x = 0, k0y = 0, k0z = 0;
   if (valid) {
     const float4 a = __ldg(sg.A + pt_off(k));
@@ -672,7 +680,11 @@ void launch_build_insert(const BuildSeg* segs_dev, int64_t num_segs, int64_t max
                          cudaStream_t stream) {
   if (num_segs <= 0 || max_seg_points <= 0) return;
   dim3 grid(grid_for(max_seg_points, 256), (unsigned)num_segs);
-  if (levels <= 3)
+  const bool seg_major = GVOX_INS_SEG_MAJOR && num_segs > 1 && grid.x <= 65535;
+  if (levels <= 3 && seg_major)
+    k_build_insert<3, true><<<dim3(grid.y, grid.x), 256, 0, stream>>>(segs_dev, levels, r0, 1.0 / r0,
+                                                                      dyadic, pslot, err);
+  else if (levels <= 3)
     k_build_insert<3><<<grid, 256, 0, stream>>>(segs_dev, levels, r0, 1.0 / r0, dyadic, pslot, err);
   else
     k_build_insert<GVOX_MAX_LEVELS><<<grid, 256, 0, stream>>>(segs_dev, levels, r0, 1.0 / r0,

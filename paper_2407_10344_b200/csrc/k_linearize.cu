@@ -112,6 +112,10 @@ namespace {
 #ifndef GVOX_LIN_ORDER
 #define GVOX_LIN_ORDER 0
 #endif
+// culling pass: the next pass's chunk boxes prefetched (1)
+#ifndef GVOX_CULL_PREFETCH
+#define GVOX_CULL_PREFETCH 1
+#endif
 
 
 constexpr int kThreads = GVOX_LIN_THREADS;
@@ -671,6 +675,30 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
     const bool cull_on = GVOX_LIN_CULL && sh.cbox != nullptr && cv.grid != nullptr && !validate;
     // the warp's LIVE iterations, compacted in order into live_s[warp][0 .. nlive)
     int32_t nlive = 0;
+#if GVOX_CULL_PREFETCH
+    // the next pass's chunk box is loaded (3 x 8 B: boxes are 24 B apart) while
+    // this pass's cells are tested
+    auto load_box = [&](int32_t i, float2 (&b)[3]) {
+      if (cull_on && i < iters) {
+        const float2* bx = reinterpret_cast<const float2*>(sh.cbox + 6 * (i * kWarps + warp));
+#pragma unroll
+        for (int j = 0; j < 3; ++j) b[j] = __ldg(bx + j);
+      }
+    };
+    float2 bnext[3];
+    load_box(lane, bnext);
+#pragma unroll 1
+    for (int i0 = 0; i0 < iters; i0 += 32) {
+      const int32_t i = i0 + lane;
+      bool live = i < iters;
+      const float box[6] = {bnext[0].x, bnext[0].y, bnext[1].x, bnext[1].y, bnext[2].x, bnext[2].y};
+      load_box(i + 32, bnext);
+      if (cull_on && live) live = !chunk_culled_grid(box, sh.Rf, sh.t, cv);
+      const uint32_t m = __ballot_sync(0xffffffffu, live);
+      if (live) live_s[warp][nlive + __popc(m & ((1u << lane) - 1u))] = (uint16_t)i;
+      nlive += __popc(m);
+    }
+#else
 #pragma unroll 1
     for (int i0 = 0; i0 < iters; i0 += 32) {
       const int32_t i = i0 + lane;
@@ -686,6 +714,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
       if (live) live_s[warp][nlive + __popc(m & ((1u << lane) - 1u))] = (uint16_t)i;
       nlive += __popc(m);
     }
+#endif
     if (lane < 3) live_s[warp][nlive + lane] = (uint16_t)kNone;  // the pipeline reads up to j + 3
     __syncwarp();
     const uint16_t* live_w = live_s[warp];

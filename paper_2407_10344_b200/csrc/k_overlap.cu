@@ -34,6 +34,15 @@ constexpr int kThreads = 256;
 #ifndef GVOX_OVL_LV_SMEM
 #define GVOX_OVL_LV_SMEM 0
 #endif
+// exact chunk culling against the occupancy of the overlap's OWN level (1)
+// instead of the coarsest level (0): also exact (a chunk whose transformed box
+// meets no occupied cell of that level has no point in an occupied voxel of
+// it), but measured slower at C5 (r02aj: screening 13.60 vs 12.54 ms -- at 1 m
+// more chunk ranges exceed 3 cells per axis and go unculled, and the finer
+// grid's cells are colder in L2), so the coarsest level stays
+#ifndef GVOX_OVL_CULL_AT_LEVEL
+#define GVOX_OVL_CULL_AT_LEVEL 0
+#endif
 #ifndef GVOX_OVL_CULL
 #define GVOX_OVL_CULL 1
 #endif
@@ -59,7 +68,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   __shared__ int warp_cnt[kThreads / 32];
   __shared__ float Rf[9], map_lo[4], map_hi[4];
   __shared__ const float* cbox_s;
-  __shared__ MapLevelDev cv_s;  // coarsest level (culling), valid if cv_dense
+  __shared__ MapLevelDev cv_s;  // culling level (GVOX_OVL_CULL_AT_LEVEL), used if dense
   const int tid = threadIdx.x;
   const int64_t tile = blockIdx.x;
   const int32_t p = __ldg(tile_pair + tile);
@@ -82,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
       map_lo[j] = md->box_lo[j];
       map_hi[j] = md->box_hi[j];
     }
-    cv_s = md->lv[md->levels - 1];
+    cv_s = md->lv[GVOX_OVL_CULL_AT_LEVEL ? level : md->levels - 1];
   }
   __syncthreads();
   if (tid == 0) {
@@ -164,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
   __shared__ int warp_cnt[2][kThreads / 32];
   __shared__ float Rf[9], map_lo[4], map_hi[4];
   __shared__ const float* cbox_s;
-  __shared__ MapLevelDev cv_s;  // coarsest level (culling), valid if cv_dense
+  __shared__ MapLevelDev cv_s;  // culling level (GVOX_OVL_CULL_AT_LEVEL), used if dense
   const int tid = threadIdx.x;
   const int32_t p = blockIdx.x;
   const PairDev pd = pairs[p];
@@ -183,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
       map_lo[j] = md->box_lo[j];
       map_hi[j] = md->box_hi[j];
     }
-    cv_s = md->lv[md->levels - 1];
+    cv_s = md->lv[GVOX_OVL_CULL_AT_LEVEL ? level : md->levels - 1];
   }
   __syncthreads();
   if (tid == 0) {
@@ -333,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_OVL_MINB)
       map_lo[j] = md->box_lo[j];
       map_hi[j] = md->box_hi[j];
     }
-    cv_s = md->lv[md->levels - 1];
+    cv_s = md->lv[GVOX_OVL_CULL_AT_LEVEL ? level : md->levels - 1];
   }
   __syncthreads();
   if (tid == 0) {

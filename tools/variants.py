@@ -92,6 +92,13 @@ VARIANTS = {
     "rpipe_b2": ["GVOX_LIN_RPIPE=1", "GVOX_LIN_MINB=2"],
     "order1": ["GVOX_LIN_ORDER=1"],
     "order2": ["GVOX_LIN_ORDER=2"],
+    "cullrows": ["GVOX_CULL_ROWS=1"],
+    "ovl_cullrows": ["GVOX_CULL_ROWS=1"],
+    "cullpf0": ["GVOX_CULL_PREFETCH=0"],
+    "cullold": ["GVOX_CULL_ROWS=1", "GVOX_CULL_PREFETCH=0"],
+    "cull27pf": ["GVOX_CULL_ROWS=0", "GVOX_CULL_PREFETCH=1"],
+    "ovl_cullcoarse": ["GVOX_OVL_CULL_AT_LEVEL=0"],
+    "acc_segmajor0": ["GVOX_INS_SEG_MAJOR=0"],
 }
 
 
