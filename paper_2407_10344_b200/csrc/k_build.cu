@@ -151,8 +151,11 @@ __global__ void k_cloud_pack_batch(const PackSeg* __restrict__ segs) {
 
 // Grids are 2D: blockIdx.y = segment (cloud), blockIdx.x * blockDim.x +
 // threadIdx.x = point within it, so a block never straddles two maps.
+#ifndef GVOX_INS_KNOWN_IDX
+#define GVOX_INS_KNOWN_IDX 1
+#endif
 #ifndef GVOX_INS_SEG_MAJOR
-#define GVOX_INS_SEG_MAJOR 1
+#define GVOX_INS_SEG_MAJOR 0  // r02ak: build 15.30 vs 15.21 ms (off)
 #endif
 #ifndef GVOX_INS_MINB
 #define GVOX_INS_MINB 8
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const Build
   uint64_t key[kMaxL];
   uint64_t h[kMaxL];
   unsigned long long prev[kMaxL];
+  int32_t dold[kMaxL];  // dense levels: the cell's value before the claim (an index >= 0: known)
   bool lead[kMaxL];
   int leader[kMaxL];
 #pragma unroll
@@ -221,6 +225,7 @@ __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const Build
   }
 #pragma unroll
   for (int l = 0; l < kMaxL; ++l) {
+    dold[l] = -1;
     if (lead[l]) {
       if (sg.box[l].dense) {
         // dense level: claim the final grid cell (-1 -> -2); h = cell
@@ -229,6 +234,7 @@ __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const Build
                           (uint32_t)((k0y >> l) - bx.y0) * bx.dz + (uint32_t)((k0z >> l) - bx.z0));
         const int old = atomicCAS(bx.grid + h[l], -1, -2);
         prev[l] = old == -1 ? kEmptyKey : key[l];  // "empty" = new voxel, else found
+        dold[l] = old;
       } else {
         h[l] = hash_slot(key[l], sg.tmp_shift);
         prev[l] = atomicCAS(reinterpret_cast<unsigned long long*>(&sg.tmp_slots[l][h[l]].x),
@@ -273,11 +279,15 @@ __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const Build
 #pragma unroll
   for (int l = 0; l < kMaxL; ++l) {
     if (l >= levels) break;
+    // the voxel index where this build already knows it: a new voxel's, or a
+    // found dense cell that held an index (not a -2 claim still being filled)
+    int32_t known = lead[l] && dold[l] >= 0 ? dold[l] : -1;
     if (new_mask[l]) {
       const int32_t b =
           blk_base[l] + __shfl_sync(0xffffffffu, woff[l], __ffs(new_mask[l]) - 1);
       if (is_new[l]) {
         const int32_t idx = b + __popc(new_mask[l] & ((1u << lane) - 1u));
+        known = idx;
         if (sg.box[l].dense)
           sg.box[l].grid[h_out[l]] = idx;
         else
@@ -291,9 +301,15 @@ __global__ void __launch_bounds__(256, GVOX_INS_MINB) k_build_insert(const Build
       }
     }
     const int32_t hl = __shfl_sync(0xffffffffu, h_out[l], leader[l]);
+    const int32_t kidx = __shfl_sync(0xffffffffu, known, leader[l]);
     const bool inr = key[l] < (1ull << 63);
-    // (lifted builds accumulate only level 0 from the points)
-    if (valid && (!sg.lift || l == 0)) pslot[sg.pl_offset + l * sg.pl_stride + k] = inr ? hl : -1;
+    // (lifted builds accumulate only level 0 from the points).  Slot: the cell
+    // / hash slot (>= 0, resolved by the accumulation), -1 no voxel, or -(index
+    // + 2) for a dense level whose index is already known here -- the
+    // accumulation then skips the grid read (one 32 B sector per point)
+    if (valid && (!sg.lift || l == 0))
+      pslot[sg.pl_offset + l * sg.pl_stride + k] =
+          !inr ? -1 : (GVOX_INS_KNOWN_IDX && sg.box[l].dense && kidx >= 0) ? -(kidx + 2) : hl;
   }
 }
 
@@ -338,10 +354,12 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
 #endif
   for (int l = 0; l < (bs.lift ? 1 : levels); ++l) {
     int32_t sl = valid ? pslot[sg.pl_offset + l * sg.pl_stride + k] : -1;
+    const bool has = sl != -1;  // the point has a voxel at this level
     int32_t idx;
     if (bs.box[l].dense) {
-      // dense level: the final grid holds the voxel index (phase 1 is complete)
-      idx = sl >= 0 ? __ldg(bs.box[l].grid + sl) : -1 - lane;
+      // dense level: the index the insert already knew (sl = -(idx + 2)), else
+      // the final grid's (phase 1 is complete)
+      idx = sl >= 0 ? __ldg(bs.box[l].grid + sl) : sl < -1 ? -sl - 2 : -1 - lane;
     } else {
       idx = sl >= 0 ? (int32_t)(uint32_t)bs.tmp_slots[l][sl].y : -1 - lane;
     }
@@ -368,7 +386,7 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
     }
 #else
     unsigned long long v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    if (sl >= 0) {
+    if (has) {
       const double r = ldexp(r0, l);
       // offset of the point within its voxel (voxel corner = k_l * r_l), fixed point
       const double S = sg.mu_scale[l];
@@ -390,19 +408,19 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
       hi_c[j] = (int)((long long)v[j] >> 24);
     }
 #endif
-    unsigned todo = __ballot_sync(0xffffffffu, sl >= 0);
+    unsigned todo = __ballot_sync(0xffffffffu, has);
     // many groups (fine levels): segmented suffix sums over RUNS of equal index
     // in lane order (shuffles; cost independent of the group count), one set
     // of atomics per run head.  A voxel split over several runs gets several
     // atomic contributions -- integer sums, so the result is the same.
-    const int ngroups = __popc(__ballot_sync(0xffffffffu, sl >= 0 && lane == __ffs(grp) - 1));
+    const int ngroups = __popc(__ballot_sync(0xffffffffu, has && lane == __ffs(grp) - 1));
     if (ngroups > GVOX_ACC_SEG_MIN) {
       const int32_t idx_prev = __shfl_up_sync(0xffffffffu, idx, 1);
       const bool head = lane == 0 || idx != idx_prev;
       const unsigned H = __ballot_sync(0xffffffffu, head);
       const unsigned after = lane == 31 ? 0u : (H & (0xffffffffu << (lane + 1)));
       const int run_end = after ? __ffs(after) - 2 : 31;
-      int cnt = sl >= 0 ? 1 : 0;
+      int cnt = has ? 1 : 0;
       // only as many doubling rounds as the warp's longest run needs
       const int max_run = GVOX_ACC_MAXRUN ? __reduce_max_sync(0xffffffffu, head ? (unsigned)(run_end - lane + 1) : 0u) : 32;
 #pragma unroll 1
@@ -420,7 +438,7 @@ __global__ void __launch_bounds__(256, GVOX_ACC_MINB) k_build_accum(const BuildS
         const int oc = __shfl_down_sync(0xffffffffu, cnt, off);
         if (take) cnt += oc;
       }
-      if (head && sl >= 0) {
+      if (head && has) {
         unsigned long long* dst = acc + (sg.acc_offset[l] + idx) * 10;
 #pragma unroll
         for (int j = 0; j < 9; ++j)

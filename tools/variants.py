@@ -99,6 +99,7 @@ VARIANTS = {
     "cull27pf": ["GVOX_CULL_ROWS=0", "GVOX_CULL_PREFETCH=1"],
     "ovl_cullcoarse": ["GVOX_OVL_CULL_AT_LEVEL=0"],
     "acc_segmajor0": ["GVOX_INS_SEG_MAJOR=0"],
+    "acc_known0": ["GVOX_INS_KNOWN_IDX=0"],
 }
 
 
