@@ -670,6 +670,10 @@ def main():
         # Default (serial): the copy inside each step, nothing overlapped.
         pipelined = args.e2e_mode == "pipelined"
         e2e_device_select = os.environ.get("GVOX_E2E_HOST_SELECT") is None
+        # GVOX_E2E_ASYNC_READBACK=1: the result readback on a D2H stream,
+        # double-buffered, overlapping the next step (r02ao, C5, 20 steps x 2:
+        # 173.9 / 189.8 ms vs 177.7 / 177.4 synchronous -- no steadier gain)
+        sync_readback = os.environ.get("GVOX_E2E_ASYNC_READBACK") is None
         if pipelined:
             stage = [tuple(torch.empty(t_.shape, dtype=t_.dtype, device=dev) for t_ in (mu_h, cov_h, nrm_h))
                      for _ in range(2)]
@@ -679,9 +683,10 @@ def main():
             # buffers and read back into pinned memory on a D2H stream, so the
             # readback of step k overlaps step k + 1 (the host does not wait
             # for it; the timed region ends after every copy has landed)
-            rec_dev = [gv.device_records(ctx, n_out, gv.LINEAR_FACTOR_DTYPE) for _ in range(2)]
-            rec_pin = [torch.empty((n_out, gv.LINEAR_FACTOR_DTYPE.itemsize), dtype=torch.uint8).pin_memory()
-                       for _ in range(2)]
+            if not sync_readback:
+                rec_dev = [gv.device_records(ctx, n_out, gv.LINEAR_FACTOR_DTYPE) for _ in range(2)]
+                rec_pin = [torch.empty((n_out, gv.LINEAR_FACTOR_DTYPE.itemsize), dtype=torch.uint8)
+                           .pin_memory() for _ in range(2)]
             d2h_stream = torch.cuda.Stream(dev)
             d2h_ev = [None, None]
 
@@ -785,7 +790,7 @@ def main():
                 _dbg("select + linearize")
                 fe = all_fac[sel_h.view(bool)]
                 cnt = sel_h
-                if pipelined:
+                if pipelined and not sync_readback:
                     b_ = k % 2
                     if d2h_ev[b_] is not None:  # this buffer's previous readback has landed
                         stream.wait_event(d2h_ev[b_])
@@ -852,9 +857,10 @@ def main():
             ms_e2e, p_e2e = float(tm_[0]), float(ts_[1])
         e2e = {"value": p_e2e / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": k_e2e, "ms_per_step": ms_e2e / k_e2e,
-               "mode": "pipelined: step k+1's H2D (copy stream, double-buffered device staging) "
-                       "overlaps step k's compute, step k's result read back on a D2H stream while "
-                       "step k+1 runs; every copy inside the timed region"
+               "mode": ("pipelined: step k+1's H2D (copy stream, double-buffered device staging) "
+                        "overlaps step k's compute" +
+                        ("" if sync_readback else ", step k's result read back on a D2H stream while "
+                         "step k+1 runs") + "; every copy inside the timed region")
                if pipelined else "serial: each step's H2D inside the step"}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
