@@ -254,6 +254,14 @@ void launch_build_finalize(const FinalSeg* segs_dev, int64_t num_segs, int64_t m
 void launch_fill_u64(uint64_t* p, uint64_t value, int64_t count, cudaStream_t stream);
 // H2D of a small pinned block by an SM kernel (no copy engine)
 void launch_h2d_copy(void* dst, const void* pinned_src, int64_t bytes, cudaStream_t stream);
+// up to 4 segments in ONE launch: copy pinned src -> dst, or zero-fill dst
+// when src is NULL (a call's input blocks and the zeroing of its counters)
+struct H2DSeg {
+  void* dst;
+  const void* src;
+  int64_t bytes;
+};
+void launch_h2d_segments(const H2DSeg* segs, int n, cudaStream_t stream);
 
 // Recycling of dense index grids (gvox_runtime.cu GridArena): a dense level's
 // only non-empty cells are its voxels' cells, so writing -1 back into exactly

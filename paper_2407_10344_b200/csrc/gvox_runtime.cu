@@ -384,6 +384,26 @@ gvox_status h2d_small(gvox_ctx* ctx, void* dst, const void* pinned_src, size_t b
   return GVOX_OK;
 }
 
+// h2d_block plus a zero-fill of `zbytes` at `zdst` (a call's counters), both in
+// ONE launch when the block goes by kernel
+gvox_status h2d_block_zero(gvox_ctx* ctx, void* dst, const void* pinned_src, size_t bytes, void* zdst,
+                           size_t zbytes) {
+  gvox_ctx::PinSlot& sl = ctx->pin_ring[ctx->pin_slot];
+  if (bytes && h2d_by_kernel(bytes)) {
+    const H2DSeg segs[2] = {{dst, pinned_src, (int64_t)bytes}, {zdst, nullptr, (int64_t)zbytes}};
+    launch_h2d_segments(segs, zbytes ? 2 : 1, ctx->stream);
+    CK_LAUNCH("h2d copy");
+  } else {
+    if (bytes) CK(cudaMemcpyAsync(dst, pinned_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    if (zbytes) CK(cudaMemsetAsync(zdst, 0, zbytes, ctx->stream));
+  }
+  if (bytes) {
+    CK(cudaEventRecord(sl.done, ctx->stream));
+    sl.pending = true;
+  }
+  return GVOX_OK;
+}
+
 // Small batches carry their tile -> owner map in the input block (filled on the
 // host; no k_tile_map launch on the critical path of an odometry-sized call).
 constexpr int64_t kHostTileMapMax = 4096;
@@ -426,6 +446,22 @@ gvox_status pin_b_upload(gvox_ctx* ctx, int slot, void* dst, size_t bytes) {
   if (bytes) {
     gvox_status st = h2d_small(ctx, dst, ctx->pin_b[slot], bytes);
     if (st) return st;
+  }
+  CK(cudaEventRecord(ctx->pin_b_done[slot], ctx->stream));
+  return GVOX_OK;
+}
+
+// two blocks out of pinned slot `slot` (at offsets 0 and off2) in one launch
+gvox_status pin_b_upload2(gvox_ctx* ctx, int slot, void* dst1, size_t n1, size_t off2, void* dst2,
+                          size_t n2) {
+  const char* src = (const char*)ctx->pin_b[slot];
+  if (h2d_by_kernel(std::max(n1, n2))) {
+    const H2DSeg segs[2] = {{dst1, src, (int64_t)n1}, {dst2, src + off2, (int64_t)n2}};
+    launch_h2d_segments(segs, 2, ctx->stream);
+    CK_LAUNCH("h2d copy");
+  } else {
+    CK(cudaMemcpyAsync(dst1, src, n1, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(dst2, src + off2, n2, cudaMemcpyHostToDevice, ctx->stream));
   }
   CK(cudaEventRecord(ctx->pin_b_done[slot], ctx->stream));
   return GVOX_OK;
@@ -948,14 +984,16 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   // exact count (counted, after the readback)
   std::vector<int64_t> vcap((size_t)count * L);
   std::vector<int32_t> hcnt((size_t)count * L + 1, 0);
-  auto launch_insert = [&]() -> gvox_status {
-    void* hp = nullptr;
-    gvox_status st2 = pin_b_reserve(ctx, 0, ins_bytes, &hp);
-    if (st2) return st2;
-    std::memset(hp, 0, o_bseg - o_cnt);  // the voxel counters and the range flag start at 0
-    std::memcpy((char*)hp + (o_bseg - o_cnt), bseg.data(), sizeof(BuildSeg) * count);
-    st2 = pin_b_upload(ctx, 0, b0 + o_cnt, ins_bytes);
-    if (st2) return st2;
+  auto launch_insert = [&](bool upload) -> gvox_status {
+    if (upload) {
+      void* hp = nullptr;
+      gvox_status st2 = pin_b_reserve(ctx, 0, ins_bytes, &hp);
+      if (st2) return st2;
+      std::memset(hp, 0, o_bseg - o_cnt);  // the voxel counters and the range flag start at 0
+      std::memcpy((char*)hp + (o_bseg - o_cnt), bseg.data(), sizeof(BuildSeg) * count);
+      st2 = pin_b_upload(ctx, 0, b0 + o_cnt, ins_bytes);
+      if (st2) return st2;
+    }
     TimerScope ts(ctx, GVOX_TIMER_BUILD);
     launch_build_insert((const BuildSeg*)(b0 + o_bseg), count, max_pts, L, r0, dyadic,
                         (int32_t*)(b0 + o_pslot), d_err, ctx->stream);
@@ -966,7 +1004,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     for (int64_t s = 0; s < count; ++s)
       for (int l = 0; l < L; ++l) vcap[s * L + l] = clouds[s]->n;
   } else {
-    st = launch_insert();
+    st = launch_insert(true);
     if (st) return st;
     CK(cudaMemcpyAsync(hcnt.data(), d_cnt, ((size_t)count * L + 1) * 4, cudaMemcpyDeviceToHost,
                        ctx->stream));
@@ -1123,8 +1161,12 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       r.x0 = p.x0; r.y0 = p.y0; r.z0 = p.z0;
       r.dy = p.dy; r.dz = p.dz;
     }
+    // sync-free builds: the metadata and the insert descriptors (+ zeroed
+    // counters) go up in ONE launch out of one pinned slot
+    const size_t meta_bytes = meta_end - o_descs;
+    const size_t ins_off = align_up(meta_bytes, 256);
     void* hp = nullptr;
-    st = pin_b_reserve(ctx, 1, meta_end - o_descs, &hp);
+    st = pin_b_reserve(ctx, 1, nosync ? ins_off + ins_bytes : meta_bytes, &hp);
     if (st) return st;
     char* h = (char*)hp - o_descs;  // the pinned block mirrors [o_descs, meta_end)
     std::memcpy(h + o_descs, mdesc.data(), sizeof(MapDev) * count);
@@ -1132,7 +1174,14 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     std::memcpy(h + o_aseg, aseg.data(), sizeof(AccumSeg) * count);
     std::memcpy(h + o_fseg, fseg.data(), sizeof(FinalSeg) * count * L);
     std::memcpy(h + o_counts, hcnt.data(), (size_t)count * L * 4);  // counted: the exact counts
-    st = pin_b_upload(ctx, 1, ab + o_descs, meta_end - o_descs);
+    if (nosync) {
+      char* hi = (char*)hp + ins_off;
+      std::memset(hi, 0, o_bseg - o_cnt);  // the voxel counters and the range flag start at 0
+      std::memcpy(hi + (o_bseg - o_cnt), bseg.data(), sizeof(BuildSeg) * count);
+      st = pin_b_upload2(ctx, 1, ab + o_descs, meta_bytes, ins_off, b0 + o_cnt, ins_bytes);
+    } else {
+      st = pin_b_upload(ctx, 1, ab + o_descs, meta_bytes);
+    }
     if (st) return st;
     grid_arena->rec = arena;
     grid_arena->reset = (const ResetSeg*)(ab + o_reset);
@@ -1140,7 +1189,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     grid_arena->max_vox = max_vox;
   }
   if (nosync) {
-    st = launch_insert();  // (its zeroing of the accumulators needs bseg's acc fields)
+    st = launch_insert(false);  // (uploaded above; its accumulator zeroing needs bseg's acc fields)
     if (st) return st;
     // (the maps' counts: copied from the insert's counters by the finalize)
     dbg.lap("insert enqueued (sync-free)");
@@ -1429,7 +1478,9 @@ gvox_status overlap_impl(const char* fn, gvox_ctx* ctx, const gvox_cloud* const*
   st = ws_reserve(ctx, 0, wl.size, &ws);
   if (st) return st;
   char* wb = (char*)ws;
-  st = h2d_block(ctx, wb + o_in, hp, in_bytes);
+  // the counts start at zero: zeroed by the same launch that uploads the block
+  int32_t* const dcounts0 = counts ? (mem == GVOX_DEVICE ? counts : (int32_t*)(wb + o_out)) : nullptr;
+  st = h2d_block_zero(ctx, wb + o_in, hp, in_bytes, dcounts0, counts ? 4 * (size_t)num_pairs : 0);
   if (st) return st;
   char* din = wb + o_in;
   const CloudDev* const* dcl = (const CloudDev* const*)(din + o_cl);
@@ -1439,8 +1490,7 @@ gvox_status overlap_impl(const char* fn, gvox_ctx* ctx, const gvox_cloud* const*
   size_t out_bytes;
   void* dout;
   if (counts) {
-    int32_t* dcounts = mem == GVOX_DEVICE ? counts : (int32_t*)(wb + o_out);
-    CK(cudaMemsetAsync(dcounts, 0, 4 * num_pairs, ctx->stream));
+    int32_t* dcounts = dcounts0;
     int32_t* dtm = host_tm ? (int32_t*)(din + o_tm) : (int32_t*)(wb + o_tp);
     if (!host_tm) launch_tile_map((const int32_t*)(din + o_ts), num_pairs, dtm, ctx->stream);
     TimerScope ts(ctx, GVOX_TIMER_OVERLAP);

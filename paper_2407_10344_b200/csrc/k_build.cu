@@ -649,6 +649,34 @@ __global__ void k_param_copy(const __grid_constant__ ParamBlock<N> p, uint8_t* _
   }
 }
 
+// H2D segments (launch_h2d_segments): blockIdx.y = segment
+struct H2DSegs {
+  H2DSeg s[4];
+};
+__global__ void k_h2d_segments(const __grid_constant__ H2DSegs segs) {
+  const H2DSeg sg = segs.s[blockIdx.y];
+  uint8_t* dst = static_cast<uint8_t*>(sg.dst);
+  const uint8_t* src = static_cast<const uint8_t*>(sg.src);
+  const int64_t n16 = sg.bytes >> 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  if (src == nullptr) {
+    if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      for (int64_t i = t0; i < n16; i += stride) reinterpret_cast<int4*>(dst)[i] = make_int4(0, 0, 0, 0);
+      for (int64_t i = (n16 << 4) + t0; i < sg.bytes; i += stride) dst[i] = 0;
+    } else {
+      for (int64_t i = t0; i < sg.bytes; i += stride) dst[i] = 0;
+    }
+  } else if (aligned) {
+    for (int64_t i = t0; i < n16; i += stride)
+      reinterpret_cast<int4*>(dst)[i] = __ldcv(reinterpret_cast<const int4*>(src) + i);
+    for (int64_t i = (n16 << 4) + t0; i < sg.bytes; i += stride) dst[i] = *(const volatile uint8_t*)(src + i);
+  } else {
+    for (int64_t i = t0; i < sg.bytes; i += stride) dst[i] = *(const volatile uint8_t*)(src + i);
+  }
+}
+
 __global__ void k_fill_u64(uint64_t* p, uint64_t value, int64_t count) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -781,6 +809,21 @@ void launch_h2d_copy(void* dst, const void* pinned_src, int64_t bytes, cudaStrea
   int64_t blocks = ((bytes >> 4) + 255) / 256;
   blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 4));
   k_h2d_copy<<<(unsigned)blocks, 256, 0, stream>>>((uint8_t*)dst, (const uint8_t*)pinned_src, bytes);
+  note_launch();
+}
+
+void launch_h2d_segments(const H2DSeg* segs, int n, cudaStream_t stream) {
+  if (n <= 0) return;
+  H2DSegs p{};
+  int64_t mx = 0;
+  for (int i = 0; i < n && i < 4; ++i) {
+    p.s[i] = segs[i];
+    mx = std::max<int64_t>(mx, segs[i].bytes);
+  }
+  if (mx <= 0) return;
+  int64_t blocks = ((mx >> 4) + 255) / 256;
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 4));
+  k_h2d_segments<<<dim3((unsigned)blocks, (unsigned)std::min(n, 4)), 256, 0, stream>>>(p);
   note_launch();
 }
 
