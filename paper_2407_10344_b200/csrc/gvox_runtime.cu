@@ -109,28 +109,83 @@ bool is_dyadic(double r) {
 // allocated from the device's default memory pool on the creating context's
 // stream and returned to the pool on that stream when the last handle goes
 // (handles must therefore be destroyed before that stream is).
+// Recycled record arenas (small builds rebuild maps of about the same size
+// every frame): a released arena is parked here instead of freed, and the next
+// build on the SAME stream that needs at most that many bytes (and at least
+// half) takes it -- stream order already puts the new build after everything
+// that used it.  At most kRecPoolKeep are kept.
+constexpr size_t kRecPoolKeep = 2;
+struct RecPool {
+  struct Entry {
+    void* ptr;
+    size_t bytes;
+    cudaStream_t stream;
+  };
+  std::mutex mu;
+  std::vector<Entry> free;
+  int device = 0;
+  static void release(const Entry& e, int device) {
+    DeviceGuard g(device);
+    if (cudaFreeAsync(e.ptr, e.stream) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(e.ptr);
+    }
+  }
+  ~RecPool() {
+    for (const Entry& e : free) release(e, device);
+  }
+};
+
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
+  std::shared_ptr<RecPool> pool;  // null: freed, not recycled
   ~DevBuf() {
-    if (ptr) {
-      DeviceGuard g(device);
-      if (cudaFreeAsync(ptr, stream) != cudaSuccess) {
-        cudaGetLastError();
-        cudaFree(ptr);
+    if (!ptr) return;
+    if (pool) {
+      std::lock_guard<std::mutex> lk(pool->mu);
+      pool->free.push_back({ptr, bytes, stream});
+      while (pool->free.size() > kRecPoolKeep) {
+        RecPool::release(pool->free.front(), device);
+        pool->free.erase(pool->free.begin());
       }
+      return;
+    }
+    DeviceGuard g(device);
+    if (cudaFreeAsync(ptr, stream) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(ptr);
     }
   }
 };
 
 gvox_status devbuf_alloc(size_t bytes, int device, cudaStream_t stream,
-                         std::shared_ptr<DevBuf>* out) {
+                         std::shared_ptr<DevBuf>* out,
+                         const std::shared_ptr<RecPool>& pool = nullptr) {
   auto b = std::make_shared<DevBuf>();
   b->device = device;
   b->bytes = bytes;
   b->stream = stream;
+  b->pool = pool;
+  if (bytes && pool) {
+    std::lock_guard<std::mutex> lk(pool->mu);
+    size_t best = pool->free.size();
+    for (size_t i = 0; i < pool->free.size(); ++i) {
+      const RecPool::Entry& e = pool->free[i];
+      if (e.stream == stream && e.bytes >= bytes && e.bytes <= 2 * bytes &&
+          (best == pool->free.size() || e.bytes < pool->free[best].bytes))
+        best = i;
+    }
+    if (best < pool->free.size()) {
+      b->ptr = pool->free[best].ptr;
+      b->bytes = pool->free[best].bytes;
+      pool->free.erase(pool->free.begin() + best);
+      *out = b;
+      return GVOX_OK;
+    }
+  }
   if (bytes) {
     cudaError_t e = cudaMallocAsync(&b->ptr, bytes, stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
@@ -157,6 +212,7 @@ struct GridPool {
   };
   std::mutex mu;
   std::vector<Entry> free;
+  std::vector<cudaEvent_t> spare;  // events of taken entries, reused (no create / destroy per build)
   int device = 0;
   static void release(const Entry& e, int device) {
     DeviceGuard g(device);
@@ -168,6 +224,7 @@ struct GridPool {
   }
   ~GridPool() {
     for (const Entry& e : free) release(e, device);
+    for (cudaEvent_t e : spare) cudaEventDestroy(e);
   }
 };
 
@@ -184,7 +241,14 @@ struct GridArena {
     if (!ptr) return;
     DeviceGuard g(device);
     cudaEvent_t ev = nullptr;
-    if (pool && reset && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+    if (pool) {
+      std::lock_guard<std::mutex> lk(pool->mu);
+      if (!pool->spare.empty()) {
+        ev = pool->spare.back();
+        pool->spare.pop_back();
+      }
+    }
+    if (pool && reset && (ev || cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess)) {
       launch_grid_reset(reset, nreset, max_vox, stream);
       if (cudaGetLastError() == cudaSuccess && cudaEventRecord(ev, stream) == cudaSuccess) {
         std::lock_guard<std::mutex> lk(pool->mu);
@@ -231,8 +295,8 @@ gvox_status grid_arena_take(const std::shared_ptr<GridPool>& pool, size_t bytes,
     if (best < pool->free.size()) {
       const GridPool::Entry e = pool->free[best];
       pool->free.erase(pool->free.begin() + best);
-      CK(cudaStreamWaitEvent(stream, e.ready, 0));
-      cudaEventDestroy(e.ready);
+      if (e.stream != stream) CK(cudaStreamWaitEvent(stream, e.ready, 0));  // (same stream: ordered)
+      pool->spare.push_back(e.ready);
       a->ptr = e.ptr;
       a->bytes = e.bytes;
       *fresh = false;
@@ -287,6 +351,7 @@ struct gvox_ctx {
   int32_t* pin_counts = nullptr;  // pinned {S, T} of gvox_linearize_batch_accum_select
   uint64_t dense_budget = 16ull << 30;  // bytes of dense index grids per build chunk
   std::shared_ptr<GridPool> grid_pool = std::make_shared<GridPool>();
+  std::shared_ptr<RecPool> rec_pool = std::make_shared<RecPool>();  // record arenas of small builds
   // pinned staging of the build's two descriptor uploads (pageable copies
   // would wait for the stream to drain before they start)
   void* pin_b[2] = {nullptr, nullptr};
@@ -529,6 +594,7 @@ gvox_status gvox_ctx_create(int device, void* cuda_stream, gvox_ctx** out) {
   }
   c->stream = (cudaStream_t)cuda_stream;
   c->grid_pool->device = device;
+  c->rec_pool->device = device;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     uint64_t keep = UINT64_MAX;  // freed blocks stay in the pool for reuse
@@ -1047,7 +1113,8 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
       total_vox += V;
     }
   std::shared_ptr<DevBuf> arena;
-  st = devbuf_alloc(al.size, ctx->device, ctx->stream, &arena);
+  // (small, sync-free builds recycle their record arenas; large ones free them)
+  st = devbuf_alloc(al.size, ctx->device, ctx->stream, &arena, nosync ? ctx->rec_pool : nullptr);
   if (st) return st;
   dbg.lap("record alloc");
   char* ab = (char*)arena->ptr;

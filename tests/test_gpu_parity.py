@@ -90,6 +90,34 @@ def test_voxelmap_batched_equals_single(gv, ctx):
                 assert np.array_equal(x, y)
 
 
+def test_voxelmap_batch_lifetime_and_recycling(gv, ctx):
+    """A batch's maps go with ONE gvox_maps_destroy when the last of them does;
+    a map closed explicitly before that is not destroyed twice; the record
+    arenas and grids the batches release are recycled by the next builds of
+    the same size, which still give identical maps."""
+    import gc
+    rs = np.random.default_rng(9)
+    data = [rand_scene(rs, n) for n in (4000, 2500, 3000)]
+    clouds = [gv.Cloud(ctx, *d) for d in data]
+    ref = [[m.export(ctx, l) for l in range(3)] for m in gv.create_voxelmaps(ctx, clouds, 0.5, 3)]
+    gc.collect()
+    for rep in range(4):
+        ms = gv.create_voxelmaps(ctx, clouds, 0.5, 3)
+        assert [m.levels for m in ms] == [3, 3, 3]
+        if rep % 2:
+            ms[1].close()  # explicit close of one member, the rest with the batch
+            ms[1].close()  # (idempotent)
+        for i, m in enumerate(ms):
+            if m.handle is None:
+                continue
+            got = [m.export(ctx, l) for l in range(3)]
+            for a, b in zip(got, ref[i]):
+                for x, y in zip(a, b):
+                    assert np.array_equal(x, y)
+        del ms
+        gc.collect()
+
+
 def test_voxelmap_golden_and_errors(gv, ctx, oracle):
     g = GOLDEN["two_points_voxel"]
     cl = gv.Cloud(ctx, np.array(g["mu"], np.float32), np.array(g["cov"], np.float32))
