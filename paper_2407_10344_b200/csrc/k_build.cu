@@ -636,6 +636,35 @@ template <int N>
 struct ParamBlock {
   int4 w[N / 16];
 };
+// up to 4 segments whose bytes ride in the parameter buffer (src = offset into
+// the block) or are zero-filled (bytes < 0: -bytes zeros); blockIdx.y = segment
+struct ParamSeg {
+  void* dst;
+  int32_t off, bytes;
+};
+template <int N>
+struct ParamSegs {
+  ParamSeg s[4];
+  int4 w[N / 16];
+};
+template <int N>
+__global__ void k_param_segments(const __grid_constant__ ParamSegs<N> p) {
+  const ParamSeg sg = p.s[blockIdx.y];
+  uint8_t* dst = static_cast<uint8_t*>(sg.dst);
+  const bool zero = sg.bytes < 0;
+  const int bytes = zero ? -sg.bytes : sg.bytes;
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(p.w) + sg.off;
+  const int n16 = bytes >> 4;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  if (((reinterpret_cast<uintptr_t>(dst) | (uintptr_t)sg.off) & 15) == 0) {
+    for (int i = t0; i < n16; i += stride)
+      reinterpret_cast<int4*>(dst)[i] = zero ? make_int4(0, 0, 0, 0) : reinterpret_cast<const int4*>(src)[i];
+    for (int i = (n16 << 4) + t0; i < bytes; i += stride) dst[i] = zero ? 0 : src[i];
+  } else {
+    for (int i = t0; i < bytes; i += stride) dst[i] = zero ? 0 : src[i];
+  }
+}
+
 template <int N>
 __global__ void k_param_copy(const __grid_constant__ ParamBlock<N> p, uint8_t* __restrict__ dst,
                              int bytes) {
@@ -776,18 +805,26 @@ void launch_grid_reset(const ResetSeg* segs_dev, int64_t num_segs, int64_t max_s
   note_launch();
 }
 
+// Calls' input blocks of up to GVOX_H2D_PARAM bytes (default 4096, at most
+// 31,744) ride in the launch's parameter buffer.  With a bulk upload sharing
+// PCIe (the pipelined e2e) the SM-driven copies' PCIe reads queue behind it
+// while parameter bytes do not (r02av, the linearize block as parameters: C2
+// e2e 0.423 -> 0.362-0.375 ms, C3 0.893 -> 0.801-0.807 ms, steps unchanged);
+// but a large parameter buffer costs the host more than it saves the device
+// on the host-bound small steps (r02aw, every block up to 31,744 B, i.e. also
+// the ~22 KB build block: C2 step 0.1255 -> 0.133-0.137 ms, C1 0.097 ->
+// 0.109 ms), so only blocks up to 4 KB go this way.  0: always SM-driven.
+int64_t h2d_param_max() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("GVOX_H2D_PARAM");
+    return e ? std::min<int64_t>(std::max<int64_t>(std::atoll(e), 0), 31744) : (int64_t)4096;
+  }();
+  return v;
+}
+
 void launch_h2d_copy(void* dst, const void* pinned_src, int64_t bytes, cudaStream_t stream) {
   if (bytes <= 0) return;
-  // blocks up to GVOX_H2D_PARAM bytes (at most 32000; default 0: never).
-  // Measured (r02ad, one B200, C1/C2/C3 steps in ms at 0 / 1024 / 4096 / 32000):
-  // C2 0.132 / 0.133 / 0.136 / 0.155 -- the small-config steps are bound by the
-  // host's enqueue time, and a larger parameter buffer costs the host more than
-  // the PCIe round trip costs the device; per-call latency improves slightly
-  // (C2 0.056 -> 0.051 ms at 32000).  Off by default, kept as the knob.
-  static const int64_t param_max = [] {
-    const char* e = std::getenv("GVOX_H2D_PARAM");
-    return e ? std::min<int64_t>(std::max<int64_t>(std::atoll(e), 0), 32000) : (int64_t)0;
-  }();
+  const int64_t param_max = h2d_param_max();
   if (bytes <= param_max) {
     auto go = [&](auto tag) {
       constexpr int N = decltype(tag)::value;
@@ -802,7 +839,7 @@ void launch_h2d_copy(void* dst, const void* pinned_src, int64_t bytes, cudaStrea
     else if (bytes <= 16384)
       go(std::integral_constant<int, 16384>{});
     else
-      go(std::integral_constant<int, 32000>{});
+      go(std::integral_constant<int, 31744>{});
     note_launch();
     return;
   }
@@ -814,6 +851,49 @@ void launch_h2d_copy(void* dst, const void* pinned_src, int64_t bytes, cudaStrea
 
 void launch_h2d_segments(const H2DSeg* segs, int n, cudaStream_t stream) {
   if (n <= 0) return;
+  n = std::min(n, 4);
+  {
+    // every copied segment's bytes in the parameter buffer (16-byte aligned
+    // offsets), zero-fills as negative sizes
+    int64_t tot = 0;
+    bool ok = true;
+    for (int i = 0; i < n; ++i) {
+      if (segs[i].bytes > INT32_MAX / 2) ok = false;
+      if (segs[i].src) tot += (segs[i].bytes + 15) & ~int64_t(15);
+    }
+    if (ok && tot <= h2d_param_max()) {
+      auto go = [&](auto tag) {
+        constexpr int N = decltype(tag)::value;
+        ParamSegs<N> pb;
+        int32_t off = 0;
+        for (int i = 0; i < n; ++i) {
+          pb.s[i].dst = segs[i].dst;
+          pb.s[i].off = off;
+          if (segs[i].src) {
+            std::memcpy(reinterpret_cast<char*>(pb.w) + off, segs[i].src, (size_t)segs[i].bytes);
+            pb.s[i].bytes = (int32_t)segs[i].bytes;
+            off += (int32_t)((segs[i].bytes + 15) & ~int64_t(15));
+          } else {
+            pb.s[i].bytes = -(int32_t)segs[i].bytes;
+          }
+        }
+        int64_t mx = 0;
+        for (int i = 0; i < n; ++i) mx = std::max<int64_t>(mx, segs[i].bytes);
+        const unsigned bx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(((mx >> 4) + 255) / 256, 148 * 4));
+        k_param_segments<N><<<dim3(bx, (unsigned)n), 256, 0, stream>>>(pb);
+      };
+      if (tot <= 1024)
+        go(std::integral_constant<int, 1024>{});
+      else if (tot <= 4096)
+        go(std::integral_constant<int, 4096>{});
+      else if (tot <= 16384)
+        go(std::integral_constant<int, 16384>{});
+      else
+        go(std::integral_constant<int, 31744>{});
+      note_launch();
+      return;
+    }
+  }
   H2DSegs p{};
   int64_t mx = 0;
   for (int i = 0; i < n && i < 4; ++i) {
