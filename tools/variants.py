@@ -100,6 +100,7 @@ VARIANTS = {
     "ovl_cullcoarse": ["GVOX_OVL_CULL_AT_LEVEL=0"],
     "acc_segmajor0": ["GVOX_INS_SEG_MAJOR=0"],
     "acc_known0": ["GVOX_INS_KNOWN_IDX=0"],
+    "tmin1": ["GVOX_TILE_MIN_TILES=1"],
 }
 
 
