@@ -262,6 +262,9 @@ struct H2DSeg {
   int64_t bytes;
 };
 void launch_h2d_segments(const H2DSeg* segs, int n, cudaStream_t stream);
+// blocks of at most this many bytes go up inside the launch's parameters (the
+// pinned source is free again as soon as the launch is enqueued)
+int64_t h2d_param_max();
 
 // Recycling of dense index grids (gvox_runtime.cu GridArena): a dense level's
 // only non-empty cells are its voxels' cells, so writing -1 back into exactly

@@ -462,7 +462,10 @@ gvox_status h2d_block_zero(gvox_ctx* ctx, void* dst, const void* pinned_src, siz
     if (bytes) CK(cudaMemcpyAsync(dst, pinned_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
     if (zbytes) CK(cudaMemsetAsync(zdst, 0, zbytes, ctx->stream));
   }
-  if (bytes) {
+  // (a block that went up in the launch's parameters left the slot free)
+  const bool by_param = bytes && h2d_by_kernel(bytes) && zbytes <= (size_t)(INT32_MAX / 2) &&
+                        (int64_t)((bytes + 15) & ~size_t(15)) <= h2d_param_max();
+  if (bytes && !by_param) {
     CK(cudaEventRecord(sl.done, ctx->stream));
     sl.pending = true;
   }
@@ -483,6 +486,7 @@ gvox_status h2d_block(gvox_ctx* ctx, void* dst, const void* pinned_src, size_t b
   gvox_ctx::PinSlot& sl = ctx->pin_ring[ctx->pin_slot];
   gvox_status st = h2d_small(ctx, dst, pinned_src, bytes);
   if (st) return st;
+  if (h2d_by_kernel(bytes) && (int64_t)bytes <= h2d_param_max()) return GVOX_OK;  // (slot free)
   CK(cudaEventRecord(sl.done, ctx->stream));
   sl.pending = true;
   return GVOX_OK;
