@@ -301,6 +301,18 @@ def main():
     t_gen = time.perf_counter()
     sc = make_scene(args, rank, world, dist)
     t_gen = time.perf_counter() - t_gen
+    # experiments: the candidate list's order (generated sorted by source) --
+    # "target" (by target, then source) or "blockN" (N x N blocks of the
+    # (source, target) pair matrix, then source, target)
+    po = os.environ.get("GVOX_BENCH_PAIR_ORDER")
+    if po and po != "source":
+        i_, j_ = sc.pairs[:, 0], sc.pairs[:, 1]
+        if po == "target":
+            perm = np.lexsort((i_, j_))
+        else:
+            B_ = int(po[5:])
+            perm = np.lexsort((j_, i_, j_ // B_, i_ // B_))
+        sc.pairs = np.ascontiguousarray(sc.pairs[perm])
     n_pts = np.diff(sc.offsets)
     log(f"[bench r{rank}] scene {sc.name}: {sc.num_clouds} clouds, {len(sc.mu)} points, "
         f"{len(sc.pairs)} candidate pairs, generated in {t_gen:.1f}s")

@@ -354,7 +354,13 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
                       const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
                       int64_t num_tiles, int tile_pts, int max_levels, const double* poses,
                       double* partials, int32_t* tile_factor, int64_t* corr_dump,
-                      bool all_dense, bool fast, bool validate, cudaStream_t stream);
+                      bool all_dense, bool fast, bool validate, cudaStream_t stream,
+                      const int32_t* exec_order = nullptr /* [num_tiles] block -> tile */);
+// execution order of a screened batch's tiles grouped by target map (device
+// counting sort; hist: num_maps int32 workspace)
+void launch_exec_order_by_target(const FactorDev* fc, const int32_t* tsc, int64_t S,
+                                 int64_t num_maps, int32_t* hist, int32_t* exec,
+                                 cudaStream_t stream);
 // reduce tile partials per factor in fixed order; write full or compact records.
 void launch_reduce(const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
                    const double* poses, const double* partials, gvox_linear_factor* out_full,

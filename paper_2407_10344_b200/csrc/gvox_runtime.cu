@@ -472,6 +472,23 @@ gvox_status h2d_block_zero(gvox_ctx* ctx, void* dst, const void* pinned_src, siz
   return GVOX_OK;
 }
 
+// GVOX_LIN_EXEC_ORDER=1: linearization tiles executed grouped by target map
+// (the CTAs resident together share the target's grid and records in L2); the
+// results do not depend on the order.  Measured at C5: the kernel drops from
+// 120.8 to 116.2 ms at full clocks (ncu launch list, r02bd), but the whole step
+// then runs into the B200's power limit -- sw_power_cap, SM clocks 1886-1897
+// instead of 1965 MHz -- and is no faster (r02be, 20 steps x 3 interleaved:
+// 152.0 / 152.1 / 152.1 ms against 152.0 / 151.8 / 152.5), the build and the
+// screening paying for the lower clock.  Same time at the cap costs more
+// energy, so the batch order stays the default.
+bool exec_by_target() {
+  static const bool v = [] {
+    const char* e = std::getenv("GVOX_LIN_EXEC_ORDER");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 // Small batches carry their tile -> owner map in the input block (filled on the
 // host; no k_tile_map launch on the critical path of an odometry-sized call).
 constexpr int64_t kHostTileMapMax = 4096;
@@ -1734,6 +1751,9 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
   size_t o_ts = lay.add(4 * (num_factors + 1));
   const bool host_tm = T <= kHostTileMapMax;
   size_t o_tm = lay.add(host_tm ? 4 * (size_t)T : 0);
+  // large batches: tiles executed grouped by target map (host counting sort)
+  const bool by_target = exec_by_target() && T > kHostTileMapMax && num_factors > 1;
+  size_t o_ex = lay.add(by_target ? 4 * (size_t)T : 0);
   size_t o_cl = lay.add(8 * num_clouds);
   size_t o_mp = lay.add(8 * num_maps);
   const size_t in_bytes = lay.size;
@@ -1745,6 +1765,14 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
   std::memcpy(hp + o_fac, fdev.data(), sizeof(FactorDev) * num_factors);
   std::memcpy(hp + o_ts, tstart.data(), 4 * (num_factors + 1));
   if (host_tm) fill_tile_map(tstart.data(), num_factors, (int32_t*)(hp + o_tm));
+  if (by_target) {
+    std::vector<int32_t> cur((size_t)num_maps + 1, 0);
+    for (int64_t f = 0; f < num_factors; ++f) cur[fdev[f].tgt + 1] += tstart[f + 1] - tstart[f];
+    for (int64_t m = 0; m < num_maps; ++m) cur[m + 1] += cur[m];
+    int32_t* ex = (int32_t*)(hp + o_ex);
+    for (int64_t f = 0; f < num_factors; ++f)
+      for (int32_t t = tstart[f]; t < tstart[f + 1]; ++t) ex[cur[fdev[f].tgt]++] = t;
+  }
   for (int64_t i = 0; i < num_clouds; ++i) ((const CloudDev**)(hp + o_cl))[i] = clouds[i] ? clouds[i]->dev : nullptr;
   for (int64_t i = 0; i < num_maps; ++i) ((const MapDev**)(hp + o_mp))[i] = maps[i] ? maps[i]->dev : nullptr;
   // ---- device workspace
@@ -1770,7 +1798,7 @@ gvox_status linearize_impl(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64
                      (const FactorDev*)(din + o_fac), (const int32_t*)(din + o_ts), num_factors, T,
                      0, max_levels, (const double*)(din + o_pose), (double*)(wb + o_part),
                      dtf, corr_dump, all_dense, fast, plan.validate,
-                     ctx->stream);
+                     ctx->stream, by_target ? (const int32_t*)(din + o_ex) : nullptr);
   }
   CK_LAUNCH("linearize");
   {
@@ -1869,6 +1897,10 @@ gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* c
   size_t o_fc = wl.add(sizeof(FactorDev) * num_candidates);
   size_t o_tsc = wl.add(4 * (num_candidates + 1));
   size_t o_cnt = wl.add(16);
+  // tiles grouped by target map for execution (GVOX_LIN_EXEC_ORDER=0: batch order)
+  const bool by_target = exec_by_target();
+  size_t o_hist = wl.add(by_target ? 4 * (size_t)std::max<int64_t>(num_maps, 1) : 0);
+  size_t o_exec = wl.add(by_target ? 4 * (size_t)std::max<int64_t>(T_all, 1) : 0);
   size_t o_bt = wl.add(8 * ((num_candidates + 1023) / 1024));
   void* ws = nullptr;
   st = ws_reserve(ctx, 0, wl.size, &ws);
@@ -1905,12 +1937,16 @@ gvox_status gvox_linearize_batch_accum_select(gvox_ctx* ctx, const gvox_cloud* c
   plan.validate = (cls_or & kClsValidate) != 0;
   plan.max_levels = std::max(1, sel_levels);
   launch_tile_map(tsc, S, (int32_t*)(wb + o_tf), ctx->stream);
+  if (by_target)
+    launch_exec_order_by_target(fc, tsc, S, num_maps, (int32_t*)(wb + o_hist), (int32_t*)(wb + o_exec),
+                                ctx->stream);
   {
     TimerScope ts(ctx, GVOX_TIMER_LINEARIZE);
     launch_linearize((const CloudDev* const*)(din + o_cl), (const MapDev* const*)(din + o_mp), fc,
                      tsc, S, T, 0, plan.max_levels, (const double*)(din + o_pose),
                      (double*)(wb + o_part), (int32_t*)(wb + o_tf), nullptr, plan.all_dense,
-                     plan.fast, plan.validate, ctx->stream);
+                     plan.fast, plan.validate, ctx->stream,
+                     by_target ? (const int32_t*)(wb + o_exec) : nullptr);
   }
   CK_LAUNCH("linearize");
   {

@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
                 const FactorDev* __restrict__ factors, const int32_t* __restrict__ tile_start,
                 const int32_t* __restrict__ tile_factor, int tile_pts,
                 const double* __restrict__ poses, double* __restrict__ partials,
-                int64_t* __restrict__ corr) {
+                int64_t* __restrict__ corr, const int32_t* __restrict__ exec_order) {
   __shared__ FactorShared sh;
   __shared__ double red[kWarps][kPartialStride];
   __shared__ double pose_s[24];
@@ -606,7 +606,10 @@ __global__ void __launch_bounds__(kThreads, GVOX_LIN_MINB)
   __shared__ __align__(8) uint64_t mbar[kWarps][S];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int64_t tile = blockIdx.x;
+  // execution order -> tile (exec_order: the tiles grouped by target map, so
+  // the CTAs resident together read the same target's grid and records; the
+  // results do not depend on the order)
+  const int64_t tile = exec_order ? (int64_t)__ldg(exec_order + blockIdx.x) : (int64_t)blockIdx.x;
   if (GVOX_LIN_BULK && lane == 0) {
 #pragma unroll
     for (int j = 0; j < S; ++j) mbar_init(&mbar[warp][j], 1);
@@ -1394,7 +1397,8 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
                       const FactorDev* factors, const int32_t* tile_start, int64_t num_factors,
                       int64_t num_tiles, int tile_pts, int max_levels, const double* poses,
                       double* partials, int32_t* tile_factor, int64_t* corr_dump,
-                      bool all_dense, bool fast, bool validate, cudaStream_t stream) {
+                      bool all_dense, bool fast, bool validate, cudaStream_t stream,
+                      const int32_t* exec_order) {
   if (num_tiles <= 0) return;
   const unsigned grid = (unsigned)num_tiles;
   // FAST (3 dyadic levels, no dump): dense grids or hash levels, with or
@@ -1405,19 +1409,19 @@ void launch_linearize(const CloudDev* const* clouds, const MapDev* const* maps,
     auto* k = all_dense ? (validate ? k_linearize<3, true, true, true> : k_linearize<3, true, true, false>)
                         : (validate ? k_linearize<3, false, true, true> : k_linearize<3, false, true, false>);
     k<<<grid, kThreads, 0, stream>>>(clouds, maps, factors, tile_start, tile_factor, tile_pts, poses,
-                                     partials, nullptr);
+                                     partials, nullptr, exec_order);
   } else if (max_levels <= 3) {
     note_linearize_variant((all_dense ? GVOX_LINVAR_DENSE : 0) | (3 << 8));
     if (all_dense)
       k_linearize<3, true, false><<<grid, kThreads, 0, stream>>>(
-          clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
+          clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump, exec_order);
     else
       k_linearize<3, false, false><<<grid, kThreads, 0, stream>>>(
-          clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
+          clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump, exec_order);
   } else {
     note_linearize_variant(GVOX_MAX_LEVELS << 8);
     k_linearize<GVOX_MAX_LEVELS, false, false><<<grid, kThreads, 0, stream>>>(
-        clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump);
+        clouds, maps, factors, tile_start, tile_factor, tile_pts, poses, partials, corr_dump, exec_order);
   }
   note_launch();
 }
@@ -1530,6 +1534,73 @@ __global__ void __launch_bounds__(kPlanThreads)
     counts[0] = off.x + tot.x;
     counts[1] = off.y + tot.y;
   }
+}
+
+// ---- execution order of a screened batch's tiles, grouped by target map
+// (counting sort on the device: tiles per target, an exclusive scan, then each
+// factor's tiles scattered to its target's range; the order inside a target is
+// whatever the atomics give -- execution order only, results unaffected)
+__global__ void k_exec_count(const FactorDev* __restrict__ fc, const int32_t* __restrict__ tsc,
+                             int64_t S, int32_t* __restrict__ hist) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < S) atomicAdd(hist + fc[f].tgt, tsc[f + 1] - tsc[f]);
+}
+__global__ void __launch_bounds__(1024) k_exec_scan(int32_t* __restrict__ hist, int64_t n) {
+  // one block: exclusive scan of n counts in chunks of 1024
+  __shared__ int32_t s_w[32];
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t b = 0; b < n; b += 1024) {
+    const int64_t i = b + threadIdx.x;
+    const int32_t v = i < n ? hist[i] : 0;
+    int32_t x = v;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) s_w[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int32_t w = s_w[threadIdx.x];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (threadIdx.x >= o) w += y;
+      }
+      s_w[threadIdx.x] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int32_t warp_off = (threadIdx.x >> 5) ? s_w[(threadIdx.x >> 5) - 1] : 0;
+    const int32_t c = carry;
+    if (i < n) hist[i] = c + warp_off + x - v;  // exclusive
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = c + warp_off + x;
+    __syncthreads();
+  }
+}
+__global__ void k_exec_scatter(const FactorDev* __restrict__ fc, const int32_t* __restrict__ tsc,
+                               int64_t S, int32_t* __restrict__ cursor, int32_t* __restrict__ exec) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= S) return;
+  const int32_t t0 = tsc[f], nt = tsc[f + 1] - t0;
+  const int32_t b = atomicAdd(cursor + fc[f].tgt, nt);
+  for (int32_t k = 0; k < nt; ++k) exec[b + k] = t0 + k;
+}
+
+void launch_exec_order_by_target(const FactorDev* fc, const int32_t* tsc, int64_t S,
+                                 int64_t num_maps, int32_t* hist, int32_t* exec,
+                                 cudaStream_t stream) {
+  if (S <= 0) return;
+  cudaMemsetAsync(hist, 0, 4 * (size_t)num_maps, stream);
+  const unsigned nb = (unsigned)((S + 255) / 256);
+  k_exec_count<<<nb, 256, 0, stream>>>(fc, tsc, S, hist);
+  note_launch();
+  k_exec_scan<<<1, 1024, 0, stream>>>(hist, num_maps);
+  note_launch();
+  k_exec_scatter<<<nb, 256, 0, stream>>>(fc, tsc, S, hist, exec);
+  note_launch();
 }
 
 void launch_select_plan(const uint8_t* selected, const int32_t* ntiles, const uint8_t* cls,
