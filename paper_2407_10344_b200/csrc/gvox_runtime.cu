@@ -482,11 +482,8 @@ gvox_status h2d_block_zero(gvox_ctx* ctx, void* dst, const void* pinned_src, siz
 // screening paying for the lower clock.  Same time at the cap costs more
 // energy, so the batch order stays the default.
 bool exec_by_target() {
-  static const bool v = [] {
-    const char* e = std::getenv("GVOX_LIN_EXEC_ORDER");
-    return e != nullptr && std::atoi(e) != 0;
-  }();
-  return v;
+  const char* e = std::getenv("GVOX_LIN_EXEC_ORDER");  // (read per call: tests switch it)
+  return e != nullptr && std::atoi(e) != 0;
 }
 
 // Small batches carry their tile -> owner map in the input block (filled on the

@@ -708,6 +708,34 @@ def test_linearize_select_variant_from_selected(gv, ctx, monkeypatch):
         assert torch.equal(out[:ns], ref)
 
 
+def test_exec_order_by_target_is_bitwise_neutral(gv, ctx, monkeypatch):
+    """GVOX_LIN_EXEC_ORDER=1 executes the tiles grouped by target map (device
+    counting sort in the screened batch, host sort in gvox_linearize_batch for
+    batches of more than 4096 tiles): the records are bitwise those of the
+    batch order."""
+    import torch
+    sc = synth.make("C5", n_submaps=96, half_blocks=5)
+    clouds = [gv.Cloud(ctx, *sc.cloud(c)) for c in range(sc.num_clouds)]
+    maps = gv.create_voxelmaps(ctx, clouds, sc.r0, sc.levels)
+    cand = np.zeros(len(sc.pairs), gv.FACTOR_DTYPE)
+    for i, name in enumerate(("source_cloud", "target_map", "pose_i", "pose_j")):
+        cand[name] = sc.pairs[:, i]
+    sel = gv.overlap_select(ctx, clouds, maps, sc.pairs, sc.poses, sc.overlap_level, 1, 20)
+    dsel = torch.from_numpy(sel).cuda()
+    fac = cand[sel.view(bool)]
+    res = {}
+    for eo in ("0", "1"):
+        monkeypatch.setenv("GVOX_LIN_EXEC_ORDER", eo)
+        out = gv.device_records(ctx, len(cand), gv.FACTOR_ACCUM_DTYPE)
+        ns = gv.linearize_batch_accum_select(ctx, clouds, maps, cand, dsel, sc.poses, out)
+        full = gv.linearize_batch(ctx, clouds, maps, cand, sc.poses)  # every candidate: > 4096 tiles
+        res[eo] = (ns, out[:ns].clone(), full)
+    monkeypatch.delenv("GVOX_LIN_EXEC_ORDER")
+    assert res["0"][0] == res["1"][0] == len(fac)
+    assert torch.equal(res["0"][1], res["1"][1])
+    assert res["0"][2].tobytes() == res["1"][2].tobytes()
+
+
 def test_dense_and_hash_levels_agree(gv, ctx, monkeypatch):
     """The two voxel index structures (dense grids, hash tables) give identical
     maps and bitwise identical linearizations and overlap counts: the build is
