@@ -690,6 +690,7 @@ def main():
         # double-buffered, overlapping the next step (r02ao, C5, 20 steps x 2:
         # 173.9 / 189.8 ms vs 177.7 / 177.4 synchronous -- no steadier gain)
         sync_readback = os.environ.get("GVOX_E2E_ASYNC_READBACK") is None
+        early_upload = os.environ.get("GVOX_E2E_EARLY_UPLOAD") is not None
         if pipelined:
             stage_flat = [torch.empty(host_flat.shape, dtype=host_flat.dtype, device=dev) for _ in range(2)]
             stage = [(f_[:3 * tot_n].view(tot_n, 3), f_[3 * tot_n:9 * tot_n].view(tot_n, 6),
@@ -756,7 +757,17 @@ def main():
 
         dbg_t = [time.perf_counter()]
 
+        # GVOX_E2E_EVENTS=1: CUDA events at the phase boundaries (no syncs):
+        # the GPU-side time from each boundary to the next, averaged over the
+        # timed steps (idle gaps included), printed to stderr at the end
+        ev_on = os.environ.get("GVOX_E2E_EVENTS") is not None
+        ev_log = []
+
         def _dbg(what):
+            if ev_on:
+                e_ = torch.cuda.Event(enable_timing=True)
+                e_.record(stream)
+                ev_log.append((what, e_))
             if os.environ.get("GVOX_E2E_DEBUG"):
                 t_ = time.perf_counter()
                 log(f"[e2e] {what}: {1e3 * (t_ - dbg_t[0]):.1f} ms")
@@ -773,7 +784,13 @@ def main():
                 if os.environ.get("GVOX_E2E_DEBUG") and len(ev_in[1]) > 1:
                     ev_in[1][0].synchronize()
                     log(f"[e2e] upload of step {k}: {ev_in[1][1].elapsed_time(ev_in[1][0]):.1f} ms")
-                if not last:
+                # (C4/C5: step k + 1's upload is issued once this step's own
+                # input blocks are on the device -- after the screened batch's
+                # launch -- unless GVOX_E2E_EARLY_UPLOAD: the library's MB-sized
+                # blocks are copied by SMs over PCIe and crawl behind a bulk
+                # upload.  C1-C3: issued here, their blocks ride in launch
+                # parameters)
+                if not last and (early_upload or not (select and e2e_device_select)):
                     ev_next = issue_h2d(k + 1)
                 b_ = k % 2
                 cl_loc = gv.create_clouds(ctx, stage[b_][0], stage[b_][1],
@@ -803,6 +820,8 @@ def main():
                                   out=sel_d)
                 ns = gv.linearize_batch_accum_select(ctx, carr, marr, all_fac, sel_d, poses,
                                                      acc_out, selected_host=sel_h)
+                if pipelined and not last and not early_upload:
+                    ev_next = issue_h2d(k + 1)
                 _dbg("select + linearize")
                 fe = all_fac[sel_h.view(bool)]
                 cnt = sel_h
@@ -868,6 +887,13 @@ def main():
         if world > 1:
             dist.barrier()
         ms_e2e = a0.elapsed_time(a1)
+        if ev_on and ev_log:
+            acc_ = {}
+            for (w0, e0_), (w1, e1_) in zip(ev_log, ev_log[1:]):
+                k_ = f"{w0.split(' ')[0]} -> {w1.split(' ')[0]}"
+                acc_.setdefault(k_, []).append(e0_.elapsed_time(e1_))
+            for k_, v_ in acc_.items():
+                log(f"[e2e events] {k_}: {np.mean(v_):.3f} ms (n = {len(v_)})")
         if world > 1:
             t = torch.tensor([ms_e2e, p_e2e], dtype=torch.float64, device=dev)
             tm_ = t.clone()
