@@ -437,7 +437,14 @@ gvox_status pin_reserve(gvox_ctx* ctx, size_t bytes, void** out) {
 // GVOX_H2D_DMA=1 restores cudaMemcpyAsync for every block.
 bool h2d_by_kernel(size_t bytes) {
   static const bool dma = std::getenv("GVOX_H2D_DMA") != nullptr;
-  return !dma && bytes <= (64u << 20);
+  // blocks above GVOX_H2D_SM_MAX bytes (default 64 MiB) go by DMA: with a bulk
+  // upload issued in pieces, a DMA waits for at most one piece, while SM reads
+  // of a MB-sized block crawl over the busy link
+  static const size_t sm_max = [] {
+    const char* e = std::getenv("GVOX_H2D_SM_MAX");
+    return e ? (size_t)std::max(0ll, std::atoll(e)) : (size_t)(64u << 20);
+  }();
+  return !dma && bytes <= sm_max;
 }
 gvox_status h2d_small(gvox_ctx* ctx, void* dst, const void* pinned_src, size_t bytes) {
   if (h2d_by_kernel(bytes)) {
