@@ -681,11 +681,15 @@ void launch_knn_query(const KnnCloudDev* clouds, const int32_t* tile_start, cons
   // (r02m, one 15.6k-point frame: 193 -> 142 us, issue-active 20 -> 34 %);
   // larger batches fill the GPU already and keep 1 (C3's 0.8 M points: 2.31 ms
   // at G = 1, 4.21 at G = 4).  GVOX_KNN_GROUP overrides (1, 4, 8).
-  // (r02aq, one 15.6k-point frame: G = 8 0.112 ms vs G = 4 0.117 ms)
+  // (r02aq, one 15.6k-point frame: G = 8 0.112 ms vs G = 4 0.117 ms; r02bj:
+  // G = 16 0.120 ms -- the merges cost more than the extra lanes give)
   const int64_t nq = (int64_t)num_tiles * tile_pts;
   int kGroup = nq <= (32 << 10) ? 8 : nq <= (64 << 10) ? 4 : 1;
   if (const char* e = std::getenv("GVOX_KNN_GROUP")) kGroup = std::atoi(e);
-  if (k <= 10 && kGroup == 8 && tile_pts % 8 == 0)
+  if (k <= 10 && kGroup == 16 && tile_pts % 16 == 0)
+    k_knn_query_g<10, 16><<<(unsigned)(num_tiles * 16), kKnnThreads, 0, stream>>>(
+        clouds, tile_start, tile_cloud, tile_pts, sorted, cell_start, k, out);
+  else if (k <= 10 && kGroup == 8 && tile_pts % 8 == 0)
     k_knn_query_g<10, 8><<<(unsigned)(num_tiles * 8), kKnnThreads, 0, stream>>>(
         clouds, tile_start, tile_cloud, tile_pts, sorted, cell_start, k, out);
   else if (k <= 10 && kGroup == 4 && tile_pts % 4 == 0)

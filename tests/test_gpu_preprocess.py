@@ -123,13 +123,13 @@ def test_full_c3_batch_sampled(gv, ctx):
 
 @pytest.mark.parametrize("k", [1, 10, 16])
 def test_knn_lanes_per_query_agree(gv, ctx, monkeypatch, k):
-    """The k-NN query with 1, 4 or 8 lanes per query (GVOX_KNN_GROUP; the
+    """The k-NN query with 1, 4, 8 or 16 lanes per query (GVOX_KNN_GROUP; the
     library picks 4 for small batches, 1 for large ones) returns bitwise the
     same tables -- each is checked against the brute-force oracle too."""
     pts = lidar_cloud(6000, seed=5)
     want = pp.knn(pts, k)
     got = {}
-    for g in ("1", "4", "8"):
+    for g in ("1", "4", "8", "16"):
         monkeypatch.setenv("GVOX_KNN_GROUP", g)
         got[g] = gv.knn(ctx, pts, k, cell_size=0.5)
         assert np.array_equal(got[g], want), f"G = {g}"
