@@ -1155,9 +1155,18 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   if (!nosync) CK(cudaMemsetAsync(b1 + o_acc, 0, (size_t)total_vox * 80, ctx->stream));
   if (idx_end > idx_begin) CK(cudaMemsetAsync(ab + idx_begin, 0xFF, idx_end - idx_begin, ctx->stream));
 
-  std::vector<AccumSeg> aseg(count);
-  std::vector<FinalSeg> fseg((size_t)count * L);
-  std::vector<MapDev> mdesc(count);
+  // the metadata is written straight into the pinned block that uploads it
+  // (no staging vectors and copies: this host work sits between the count
+  // readback and the accumulation, with the GPU idle, in counted builds)
+  const size_t meta_bytes = meta_end - o_descs;
+  const size_t ins_off = align_up(meta_bytes, 256);
+  void* hp = nullptr;
+  st = pin_b_reserve(ctx, 1, nosync ? ins_off + ins_bytes : meta_bytes, &hp);
+  if (st) return st;
+  char* const h = (char*)hp - o_descs;  // the pinned block mirrors [o_descs, meta_end)
+  AccumSeg* const aseg = (AccumSeg*)(h + o_aseg);
+  FinalSeg* const fseg = (FinalSeg*)(h + o_fseg);
+  MapDev* const mdesc = (MapDev*)(h + o_descs);
   int64_t vacc = 0;
   for (int64_t s = 0; s < count; ++s) {
     const gvox_cloud* c = clouds[s];
@@ -1241,7 +1250,7 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
   for (int64_t q = 0; q < count * L; ++q) max_vox = std::max<int64_t>(max_vox, vcap[q]);
   {
     // reset table of the dense levels (GridArena: recycling the grids)
-    std::vector<ResetSeg> rseg((size_t)count * L);
+    ResetSeg* const rseg = (ResetSeg*)(h + o_reset);
     for (int64_t q = 0; q < count * L; ++q) {
       const LevelPlan& p = plan[q];
       ResetSeg& r = rseg[q];
@@ -1255,16 +1264,6 @@ gvox_status build_chunk(gvox_ctx* ctx, const gvox_cloud* const* clouds, int64_t 
     }
     // sync-free builds: the metadata and the insert descriptors (+ zeroed
     // counters) go up in ONE launch out of one pinned slot
-    const size_t meta_bytes = meta_end - o_descs;
-    const size_t ins_off = align_up(meta_bytes, 256);
-    void* hp = nullptr;
-    st = pin_b_reserve(ctx, 1, nosync ? ins_off + ins_bytes : meta_bytes, &hp);
-    if (st) return st;
-    char* h = (char*)hp - o_descs;  // the pinned block mirrors [o_descs, meta_end)
-    std::memcpy(h + o_descs, mdesc.data(), sizeof(MapDev) * count);
-    std::memcpy(h + o_reset, rseg.data(), sizeof(ResetSeg) * count * L);
-    std::memcpy(h + o_aseg, aseg.data(), sizeof(AccumSeg) * count);
-    std::memcpy(h + o_fseg, fseg.data(), sizeof(FinalSeg) * count * L);
     std::memcpy(h + o_counts, hcnt.data(), (size_t)count * L * 4);  // counted: the exact counts
     if (nosync) {
       char* hi = (char*)hp + ins_off;
